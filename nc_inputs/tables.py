@@ -1,0 +1,114 @@
+"""Patch-operator table container, file IO and *synthetic* tables.
+
+The tables are the Step-1 outputs the paper stores per patch radius (§8
+"Step 1": "only the p x K matrix T and the 1 x K vector I") plus the Zernike sampling nodes and
+the discrete Zernike transform P (§6) and the skeleton nodes x^f_{pi(m)}
+(eq:outgoingcompressed).  They are an *input* of ``nc_setup`` (SURVEY.md
+§8(b)); both the oracle and the CUDA path read the same arrays.
+
+Synthetic tables (``synthetic_tables``) keep the real node geometry (a tensor polar grid on the
+patch: Gauss-Legendre radii x equispaced angles) but draw T, P and I at random:
+matvec parity only needs *identical* tables on both sides.  Physical tables
+come from ``nc_tables`` (the CPU Step-1 builder) and are stored with the same keys.
+
+Layout conventions (all float64, C order):
+  zhat  (Kstar, 3)  Zernike sampling nodes, canonical frame (patch centre = +z, theta=0 along +x)
+  P     (K, Kstar)  discrete Zernike transform
+  shat  (p, 3)      skeleton (outgoing) nodes, canonical frame
+  T     (p, K)      outgoing map rho = T fhat (eq:Tmap)
+  I     (K,)        integration row, I_sigma = I . sum_i fhat_i (eq:getI)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+TABLE_VERSION = 1
+
+
+@dataclass
+class PatchTables:
+    kind: int            # 0 = interior / narrow escape (G_I), 1 = exterior / narrow capture (G_E)
+    eps: float           # patch radius in arc length
+    M: int               # Zernike truncation, K = (M+1)(M+2)/2
+    zhat: np.ndarray
+    P: np.ndarray
+    shat: np.ndarray
+    T: np.ndarray
+    I: np.ndarray
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def K(self) -> int:
+        return self.T.shape[1]
+
+    @property
+    def Kstar(self) -> int:
+        return self.zhat.shape[0]
+
+    @property
+    def p(self) -> int:
+        return self.shat.shape[0]
+
+    def validate(self):
+        K = (self.M + 1) * (self.M + 2) // 2
+        assert self.T.shape == (self.p, K), (self.T.shape, self.p, K)
+        assert self.P.shape == (K, self.Kstar)
+        assert self.I.shape == (K,)
+        assert self.zhat.shape == (self.Kstar, 3) and self.shat.shape == (self.p, 3)
+        for a in (self.zhat, self.shat):
+            assert np.allclose(np.linalg.norm(a, axis=1), 1.0, atol=1e-13)
+        return self
+
+
+def save_tables(path, t: PatchTables):
+    np.savez(path, version=TABLE_VERSION, kind=t.kind, eps=t.eps, M=t.M, zhat=t.zhat, P=t.P,
+             shat=t.shat, T=t.T, I=t.I, meta=np.array(repr(t.meta)))
+
+
+def load_tables(path) -> PatchTables:
+    z = np.load(path, allow_pickle=False)
+    assert int(z["version"]) == TABLE_VERSION, "table file version mismatch"
+    return PatchTables(kind=int(z["kind"]), eps=float(z["eps"]), M=int(z["M"]),
+                       zhat=np.ascontiguousarray(z["zhat"]), P=np.ascontiguousarray(z["P"]),
+                       shat=np.ascontiguousarray(z["shat"]), T=np.ascontiguousarray(z["T"]),
+                       I=np.ascontiguousarray(z["I"]), meta={"repr": str(z["meta"])}).validate()
+
+
+def patch_point(t, theta):
+    """Canonical-frame point at arc distance t from the pole in azimuth theta."""
+    t = np.asarray(t, dtype=np.float64)
+    theta = np.asarray(theta, dtype=np.float64)
+    return np.stack([np.sin(t) * np.cos(theta), np.sin(t) * np.sin(theta), np.cos(t)], axis=-1)
+
+
+def polar_node_grid(eps: float, n_r: int, n_theta: int):
+    """Tensor Gauss-Legendre (radius r in [0,1], t = eps*r) x trapezoid (theta) node set.
+
+    Returns (r, theta, xyz) with node index k = i_r * n_theta + i_theta.
+    """
+    x, _ = np.polynomial.legendre.leggauss(n_r)
+    r = 0.5 * (x + 1.0)
+    th = 2.0 * np.pi * np.arange(n_theta) / n_theta
+    R, TH = np.meshgrid(r, th, indexing="ij")
+    xyz = patch_point(eps * R.ravel(), TH.ravel())
+    return R.ravel(), TH.ravel(), xyz
+
+
+def synthetic_tables(kind: int, eps: float, seed: int, M: int = 15, p: int = 120, n_r: int = 16,
+                     n_theta: int = 32, coupling: float = 1.0) -> PatchTables:
+    """Real node geometry, random operators (parity-only tables)."""
+    rng = np.random.default_rng(seed)
+    K = (M + 1) * (M + 2) // 2
+    _, _, zhat = polar_node_grid(eps, n_r, n_theta)
+    # skeleton nodes: random points strictly inside the patch
+    t = eps * np.sqrt(rng.random(p)) * 0.999
+    th = 2.0 * np.pi * rng.random(p)
+    shat = patch_point(t, th)
+    Kstar = zhat.shape[0]
+    T = rng.standard_normal((p, K)) * (coupling * eps / np.sqrt(K * p))
+    P = rng.standard_normal((K, Kstar)) / Kstar
+    I = rng.standard_normal(K) * eps
+    return PatchTables(kind=kind, eps=eps, M=M, zhat=zhat, P=P, shat=shat, T=T, I=I,
+                       meta={"synthetic": True, "seed": seed, "coupling": coupling}).validate()

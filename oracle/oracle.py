@@ -1,0 +1,236 @@
+"""CPU oracle for the multiple-scattering matvec, GMRES and read-out -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and
+``--impl reference``) may import this module.  The product path (``paper_1906_04209_b200``) never
+does, and this module never imports the product.  It is deliberately plain and slow: numpy for the
+library primitives (matmul, dense solve), ``oracle_field.c`` (plain C + OpenMP) for the O(N^2)
+Green's-function sum.  Floating point is fp64 throughout.
+
+Steps, in the paper's order and notation (SURVEY.md §8(c) "What it computes"):
+
+1. frames R_i = [e1 e2 c_i] -- "a coordinate system fixed about the centre" (§3);
+   the rule is DESIGN.md reading R8 (part of the ABI).
+2. global nodes z_{ik} = R_i zhat_k (Zernike sampling nodes, §4) and
+   s_{jm} = R_j shat_m (skeleton nodes x^f_{j,pi(m)}, §7).
+3. outgoing charges rho_j = T fhat_j  (eq:Tmap; matvec step 1).
+4. field u_{ik} = sum_{j != i} sum_m G(z_{ik}, s_{jm}) rho_{jm}  (eq:mssums with eq:outgoingcompressed;
+   oracle_field.c).
+5. y_i = fhat_i + P u_i  (eq:opinteqnsdisc / eq:sysmatapply; step 5,
+   PAPER.md:1404-1408).
+6. GMRES on (I + A_off) fhat = P 1, x0 = 0, modified Gram-Schmidt with one
+   re-orthogonalisation pass, Givens rotations, no restart (R9).
+7. read-out I_sigma = I . sum_i fhat_i (eq:getI); interior
+   mu = 1/(3 I_sigma) - 3/5 (eq:mufromsigma2); exterior J = -4 pi I_sigma (R2,
+   correcting the 4 pi dropped at PAPER.md:475).
+
+Pins (tests/test_oracle.py): the Green's-function sphere means, the N = 1 identity
+(PAPER.md:883), rotation/permutation invariance, the dense-LU solve (a textbook routine), and the
+physical single-patch limit once real tables exist.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build_oracle(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle_field.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c99", "-o", _LIB_PATH,
+                               src, "-lm"])
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build_oracle()
+        L = ctypes.CDLL(_LIB_PATH)
+        dp = ctypes.POINTER(ctypes.c_double)
+        ip = ctypes.POINTER(ctypes.c_int64)
+        L.oracle_field.argtypes = [ctypes.c_int, ctypes.c_int64, dp, ip, ctypes.c_int64, dp, ip, dp, dp]
+        L.oracle_field.restype = None
+        L.oracle_green_batch.argtypes = [ctypes.c_int, ctypes.c_int64, dp, dp, dp]
+        L.oracle_green_batch.restype = None
+        L.oracle_num_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _dp(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ip(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())
+
+
+# ---------------------------------------------------------------------------------------------
+# Green's function (on-surface), for pins
+# ---------------------------------------------------------------------------------------------
+def green(kind: int, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(np.broadcast_to(x, np.broadcast(x, y).shape), dtype=np.float64).reshape(-1, 3)
+    y = np.ascontiguousarray(np.broadcast_to(y, np.broadcast(x, y).shape), dtype=np.float64).reshape(-1, 3)
+    g = np.empty(len(x))
+    lib().oracle_green_batch(int(kind), len(x), _dp(x), _dp(y), _dp(g))
+    return g
+
+
+# ---------------------------------------------------------------------------------------------
+# Step 1-2: frames and global nodes
+# ---------------------------------------------------------------------------------------------
+def frames(centers: np.ndarray) -> np.ndarray:
+    """R_i = [e1 e2 c_i] (3x3 per patch; columns).  e1 = normalize(xhat - (xhat.c) c), with yhat used
+    instead of xhat when |c . xhat| > 0.9; e2 = c x e1 (R8)."""
+    c = np.asarray(centers, dtype=np.float64)
+    R = np.empty((len(c), 3, 3))
+    for i, ci in enumerate(c):
+        a = np.array([1.0, 0.0, 0.0]) if abs(ci[0]) <= 0.9 else np.array([0.0, 1.0, 0.0])
+        e1 = a - a.dot(ci) * ci
+        e1 /= np.linalg.norm(e1)
+        e2 = np.cross(ci, e1)
+        R[i, :, 0], R[i, :, 1], R[i, :, 2] = e1, e2, ci
+    return R
+
+
+def global_nodes(R: np.ndarray, local: np.ndarray) -> np.ndarray:
+    """x_{i,k} = R_i xhat_k  -> array (N, n, 3)."""
+    return np.einsum("iab,kb->ika", R, local)
+
+
+# ---------------------------------------------------------------------------------------------
+# Step 3-5: the matvec
+# ---------------------------------------------------------------------------------------------
+def outgoing(T: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """rho_j = T fhat_j for every patch (eq:Tmap)."""
+    return x @ T.T
+
+
+def field(kind, tgt, tpatch, src, spatch, rho):
+    tgt = np.ascontiguousarray(tgt, dtype=np.float64).reshape(-1, 3)
+    src = np.ascontiguousarray(src, dtype=np.float64).reshape(-1, 3)
+    tpatch = np.ascontiguousarray(tpatch, dtype=np.int64)
+    spatch = np.ascontiguousarray(spatch, dtype=np.int64)
+    rho = np.ascontiguousarray(rho, dtype=np.float64).reshape(-1)
+    u = np.empty(len(tgt))
+    lib().oracle_field(int(kind), len(tgt), _dp(tgt), _ip(tpatch), len(src), _dp(src), _ip(spatch), _dp(rho),
+                       _dp(u))
+    return u
+
+
+def matvec(kind, centers, tab, x, rows=None, R=None):
+    """y = (I + A_off) x  (eq:sysmatapply).  ``rows``: optional subset of target patches (sampled rows);
+    returns y for those rows only.  ``R``: optional explicit frames (default: the ABI rule)."""
+    N = len(centers)
+    x = np.asarray(x, dtype=np.float64).reshape(N, -1)
+    R = frames(centers) if R is None else R
+    rows = np.arange(N) if rows is None else np.asarray(rows, dtype=np.int64)
+    z = global_nodes(R[rows], tab.zhat)                      # (nr, K*, 3)
+    s = global_nodes(R, tab.shat)                            # (N, p, 3)
+    rho = outgoing(tab.T, x)                                 # (N, p)
+    tpatch = np.repeat(rows, tab.Kstar)
+    spatch = np.repeat(np.arange(N), tab.p)
+    u = field(kind, z, tpatch, s, spatch, rho).reshape(len(rows), tab.Kstar)
+    return x[rows] + u @ tab.P.T
+
+
+def rhs(tab, N):
+    """b_i = P 1 (eq:opinteqnsdisc right-hand side)."""
+    return np.tile(tab.P @ np.ones(tab.Kstar), (N, 1))
+
+
+# ---------------------------------------------------------------------------------------------
+# Step 6: GMRES
+# ---------------------------------------------------------------------------------------------
+def gmres(apply, b, tol=1e-10, max_iter=300):
+    """Unrestarted GMRES, x0 = 0, MGS + one re-orthogonalisation pass, Givens rotations.
+
+    Returns (x, iterations, history) where history[j] = implicit relative residual after j steps."""
+    b = np.asarray(b, dtype=np.float64).ravel()
+    n = b.size
+    beta = np.linalg.norm(b)
+    hist = [1.0]
+    if beta == 0.0:
+        return np.zeros(n), 0, hist
+    V = np.zeros((max_iter + 1, n))
+    H = np.zeros((max_iter + 1, max_iter))
+    cs = np.zeros(max_iter)
+    sn = np.zeros(max_iter)
+    g = np.zeros(max_iter + 1)
+    g[0] = beta
+    V[0] = b / beta
+    k = 0
+    for j in range(max_iter):
+        w = np.asarray(apply(V[j]), dtype=np.float64).ravel()
+        for _ in range(2):                                   # MGS + one re-orthogonalisation pass
+            for i in range(j + 1):
+                h = V[i] @ w
+                H[i, j] += h
+                w = w - h * V[i]
+        H[j + 1, j] = np.linalg.norm(w)
+        if H[j + 1, j] > 0:
+            V[j + 1] = w / H[j + 1, j]
+        for i in range(j):                                   # apply previous rotations
+            t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+            H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+            H[i, j] = t
+        r = np.hypot(H[j, j], H[j + 1, j])
+        cs[j], sn[j] = H[j, j] / r, H[j + 1, j] / r
+        H[j, j] = r
+        H[j + 1, j] = 0.0
+        g[j + 1] = -sn[j] * g[j]
+        g[j] = cs[j] * g[j]
+        k = j + 1
+        hist.append(abs(g[j + 1]) / beta)
+        if hist[-1] <= tol:
+            break
+    y = np.zeros(k)
+    for i in range(k - 1, -1, -1):                            # back substitution
+        y[i] = (g[i] - H[i, i + 1:k] @ y[i + 1:k]) / H[i, i]
+    x = V[:k].T @ y
+    return x, k, hist
+
+
+# ---------------------------------------------------------------------------------------------
+# Step 7: read-out
+# ---------------------------------------------------------------------------------------------
+def readout(kind, I_row, x):
+    """Returns (I_sigma, value): value = mu (interior) or J (exterior)."""
+    xs = np.asarray(x, dtype=np.float64).reshape(-1, len(I_row))
+    I_sigma = float(I_row @ xs.sum(axis=0))
+    if kind == 0:
+        return I_sigma, 1.0 / (3.0 * I_sigma) - 3.0 / 5.0
+    return I_sigma, -4.0 * np.pi * I_sigma
+
+
+def solve(kind, centers, tab, tol=1e-10, max_iter=300):
+    N = len(centers)
+    b = rhs(tab, N)
+    x, it, hist = gmres(lambda v: matvec(kind, centers, tab, v.reshape(N, -1)).ravel(), b.ravel(), tol, max_iter)
+    I_sigma, value = readout(kind, tab.I, x)
+    xr = x.reshape(N, -1)
+    res = np.linalg.norm(b - matvec(kind, centers, tab, xr)) / np.linalg.norm(b)
+    return dict(x=xr, iters=it, hist=hist, I_sigma=I_sigma, value=value, explicit_residual=res)
+
+
+def dense_operator(kind, centers, tab):
+    """Assemble (I + A_off) column by column (tiny N only)."""
+    N = len(centers)
+    n = N * tab.K
+    A = np.empty((n, n))
+    for c in range(n):
+        e = np.zeros(n)
+        e[c] = 1.0
+        A[:, c] = matvec(kind, centers, tab, e.reshape(N, -1)).ravel()
+    return A
