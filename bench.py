@@ -1,0 +1,314 @@
+"""bench.py -- GMRES matvecs/s (and time-to-solution) of the multiple-scattering matvec on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--mode direct|hier] [--impl nc|reference]
+
+A "step" is one full matvec (I + A_off) x over all N patches (all of SURVEY.md §8(a)'s matvec rows), with
+inputs resident in HBM.  N > 1 runs under torchrun, one rank per GPU, target patches sharded, one NCCL
+all-gather per matvec (strong scaling: the layout is fixed).  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, the deliberately slow reference of this tier) on the box's
+host cores on a bounded sample of the same workload (sampled target patches), on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.txt")
+# FP64-pipe flops executed per pair by k_pairs_direct's inner loop (2 per DFMA, 1 per DMUL/DADD),
+# counted from its SASS (profiles/r01_direct_sass_count.txt).
+FP64_FLOPS_PER_PAIR = {0: None, 1: None}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--mode", default="direct", choices=["direct", "hier"])
+    ap.add_argument("--impl", default="nc", choices=["nc", "reference"])
+    ap.add_argument("--tables", default="synthetic", choices=["synthetic", "physical"])
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="target patches in the oracle sample (0 = auto)")
+    return ap.parse_args()
+
+
+def load_fp64_peak():
+    best = {}
+    try:
+        for line in open(FP64_PEAK_FILE):
+            line = line.strip()
+            if line.startswith("{") and '"kind"' in line:
+                d = json.loads(line)
+                best[d["kind"]] = max(best.get(d["kind"], 0.0), d["tflops"])
+    except OSError:
+        pass
+    return best
+
+
+def make_tables(cfg, which):
+    from nc_inputs import synthetic_tables
+    if which == "physical":
+        from nc_inputs.tables import load_tables
+        path = os.path.join(ROOT, "tables", "data", f"{cfg.name}.npz")
+        return load_tables(path)
+    return synthetic_tables(cfg.kind, cfg.eps, seed=4242)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_sample(cfg, tab, x, n_rows, seed=0):
+    """Time the oracle on n_rows sampled target patches; returns (seconds, rows, threads)."""
+    from oracle import oracle as O
+    c = cfg.centers()
+    rows = np.sort(np.random.default_rng(seed).choice(cfg.N, n_rows, replace=False))
+    O.lib()
+    t0 = time.perf_counter()
+    O.matvec(cfg.kind, c, tab, x, rows=rows)
+    return time.perf_counter() - t0, rows, O.num_threads()
+
+
+def auto_sample_rows(cfg, tab, target_s=12.0):
+    # calibrate with a 1-patch run, then size the sample to ~target_s of CPU work
+    from nc_inputs import random_coeffs
+    x = random_coeffs(cfg.N, tab.K, 2000 + int(cfg.name[1:]))
+    t1, _, _ = cpu_oracle_sample(cfg, tab, x, 1)
+    return int(max(1, min(cfg.N, round(target_s / max(t1, 1e-4)))))
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, on the host cores, bounded samples."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from nc_inputs import CONFIGS, random_coeffs
+    cfg = CONFIGS[args.config]
+    tab = make_tables(cfg, args.tables)
+    x = random_coeffs(cfg.N, tab.K, 2000 + int(cfg.name[1:]))
+    n_rows = args.cpu_sample or auto_sample_rows(cfg, tab, target_s=8.0)
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_oracle_sample(cfg, tab, x, max(1, n_rows // 8))
+    times = []
+    for k in range(args.steps):
+        t, rows, thr = cpu_oracle_sample(cfg, tab, x, n_rows, seed=k)
+        times.append(t * cfg.N / n_rows)      # extrapolated full-matvec seconds
+    sec = float(np.mean(times))
+    val = 1.0 / sec
+    line = {"metric": "gmres_matvecs_per_s", "value": val, "unit": "matvec/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{cfg.name} {args.mode}", "N": cfg.N, "eps": cfg.eps, "kind": cfg.kind,
+                       "layout": cfg.layout, "tables": args.tables, "K": tab.K, "Kstar": tab.Kstar, "p": tab.p},
+            "cpu_baseline": {"value": val, "unit": "matvec/s", "cores": thr, "kind": "oracle",
+                             "sample": f"{n_rows} of {cfg.N} target patches per step, extrapolated x{cfg.N / n_rows:.1f}"},
+            "e2e": {"value": val, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1906_04209_b200 as nc
+    from nc_inputs import CONFIGS, random_coeffs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    tab = make_tables(cfg, args.tables)
+    centers = cfg.centers()
+    mode = nc.NC_HIER if args.mode == "hier" else nc.NC_DIRECT
+    nid = None
+    if world > 1:
+        obj = [nc.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    t_setup0 = time.perf_counter()
+    h = nc.Handle(cfg.kind, centers, cfg.eps, tab, mode=mode, precision=cfg.precision, device=local, world=world,
+                  rank=rank, nccl_id=nid)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup0
+    x_all = random_coeffs(cfg.N, tab.K, 2000 + int(cfg.name[1:]))
+    x = torch.from_numpy(h.to_internal(x_all)).cuda()
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(int(256 * 2**20 // 4), dtype=torch.float32, device="cuda")   # 256 MB > 126 MB L2
+
+    for _ in range(max(args.warmup, 0)):
+        h.matvec(x, y)
+    torch.cuda.synchronize()
+    # per-stage times (one extra, untimed matvec with stage events)
+    h.time_stages(True)
+    h.matvec(x, y)
+    torch.cuda.synchronize()
+    st = h.stats()
+    h.time_stages(False)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()                                   # L2 flush between timed steps (not timed)
+            starts[k].record(stream)
+            h.matvec(x, y)
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_total = float(np.sum(ms_steps))
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    value = args.steps / (ms_total / 1e3)
+
+    # end to end through the host-buffer C-ABI entry point (pinned host buffers, H2D + matvec + D2H)
+    xh = torch.from_numpy(h.to_internal(x_all)).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    import ctypes
+    from paper_1906_04209_b200.nc import _dp, _check
+    h._L.nc_matvec_host(h._h, ctypes.cast(xh.data_ptr(), _dp), ctypes.cast(yh.data_ptr(), _dp))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _check(h._L.nc_matvec_host(h._h, ctypes.cast(xh.data_ptr(), _dp), ctypes.cast(yh.data_ptr(), _dp)))
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": args.steps / e2e_s, "unit": "matvec/s", "h2d_bytes_per_step": int(xh.numel() * 8),
+           "d2h_bytes_per_step": int(yh.numel() * 8)}
+
+    # time to solution (GMRES from x0 = 0 on the physical right-hand side P.1, then the read-out)
+    solve = None
+    if not args.no_solve:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        xs, its, hist = h.gmres(rtol=cfg.gmres_tol, max_iter=300, allow_noconv=True)
+        Is, val = h.flux_or_mfpt(xs) if (cfg.kind == 1 or args.tables == "physical") else (float("nan"), float("nan"))
+        tts = time.perf_counter() - t0
+        solve = {"time_to_solution_s": tts, "gmres_iters": its, "final_rel_residual": float(hist[-1]),
+                 "I_sigma": Is, ("mu" if cfg.kind == 0 else "J"): val, "setup_s": setup_s,
+                 "tables": args.tables}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    # roofline of the dominant kernel (direct pair sums): FP64 pipe
+    peaks = load_fp64_peak()
+    pair_ms = st["ms_last"][2] if args.mode == "direct" else st["ms_last"][4]
+    pairs = st["pairs_per_matvec"]
+    fpp = FP64_FLOPS_PER_PAIR.get(cfg.kind)
+    roof = None
+    if pair_ms > 0 and fpp:
+        ach = pairs * fpp / (pair_ms * 1e-3) / 1e12
+        peak = peaks.get("dfma")
+        roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": (ach / peak) if peak else None, "traffic": None,
+                "kernel": "k_pairs_direct", "note": "FP64-pipe flops executed per pair (SASS count) x pairs / "
+                "kernel ms; peak = measured DFMA throughput (profiles/r01_fp64_peak.txt)",
+                "pairs_per_s": pairs / (pair_ms * 1e-3)}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            n_rows = args.cpu_sample or auto_sample_rows(cfg, tab)
+            t, rows, thr = cpu_oracle_sample(cfg, tab, x_all, n_rows)
+            cpu = {"value": 1.0 / (t * cfg.N / n_rows), "unit": "matvec/s", "cores": thr, "kind": "oracle",
+                   "sample": f"{n_rows} of {cfg.N} target patches (direct sum), extrapolated x{cfg.N / n_rows:.1f}"}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "error": str(e)}
+    line = {"metric": "gmres_matvecs_per_s", "value": value, "unit": "matvec/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{cfg.name} {args.mode}", "N": cfg.N, "eps": cfg.eps, "kind": cfg.kind,
+                       "layout": cfg.layout, "tables": args.tables, "K": tab.K, "Kstar": tab.Kstar, "p": tab.p,
+                       "l2": "flushed between timed steps (256 MB write, untimed)"},
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": 3 * args.steps if args.mode == "direct" else None,
+            "roofline": roof, "cpu_baseline": cpu, "stages_ms": st["ms_last"][:7], "pairs_per_matvec": pairs,
+            "solve": solve}
+    print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,161 @@
+/*
+ * nc.h -- C ABI of libnc: the preconditioned multiple-scattering matvec of Kaye & Greengard,
+ * "A fast solver for the narrow capture and narrow escape problems in the sphere"
+ * (arXiv:1906.04209; PAPER.md = the paper's LaTeX source), its GMRES solve and its scalar read-out,
+ * on NVIDIA B200 (sm_100a), fp64.
+ *
+ * The operator (eq:opinteqnsdisc; step 3 of §8):
+ *
+ *     y_i = fhat_i + P sum_{j != i} S_ij B fhat_j,    i = 1..N,
+ *
+ * with the source patches in their skeletonised outgoing representation (eq:outgoingcompressed,
+ * PAPER.md:1078-1096; eq:Tmap):
+ *
+ *     (S_ij B fhat_j)(z_{ik}) = sum_m G(z_{ik}, s_{jm}) rho_{jm},   rho_j = T fhat_j,
+ *
+ * G = G_I (interior / narrow escape, eq:Gintonsurface) or G_E (exterior / narrow
+ * capture, eq:Gextonsurface), z_{ik} = R_i zhat_k the Zernike sampling nodes and
+ * s_{jm} = R_j shat_m the skeleton nodes of patch j in its frame R_j.
+ *
+ * Conventions for every entry point:
+ *   - return 0 (NC_OK) on success, a negative NC_E* code on failure; nc_last_error() returns a
+ *     thread-local human-readable message for the last failure of the calling thread.
+ *   - "host" pointers are ordinary CPU memory, "device" pointers are CUDA global memory on the
+ *     handle's device.  All arrays are fp64, C order (row-major), densely packed.
+ *   - Coefficient vectors use the library's INTERNAL patch order (see nc_partition) and are sharded
+ *     by rank: rank r owns rows [row_begin, row_begin + row_count), each row = K contiguous doubles.
+ *   - One handle per host thread.  Multi-rank calls (world > 1) are collective: every rank must
+ *     make the same sequence of calls.
+ *   - There is no CPU fallback: every arithmetic step runs in this library's CUDA kernels.
+ */
+#ifndef NC_H_
+#define NC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NC_OK 0
+#define NC_EINVAL (-1)   /* invalid argument (sizes, null pointers, non-unit centres, K mismatch) */
+#define NC_ESEP (-2)     /* two patch centres closer than 3 eps in arc length */
+#define NC_ENOMEM (-3)   /* device allocation failed */
+#define NC_ECUDA (-4)    /* CUDA runtime error (message has the CUDA error string) */
+#define NC_ENCCL (-5)    /* NCCL error (world > 1) */
+#define NC_ESTATE (-6)   /* call not valid in the handle's state (e.g. I_sigma <= 0 for the interior) */
+#define NC_ENOCONV (-7)  /* GMRES reached max_iter above rtol; x holds the last iterate */
+#define NC_EUNSUP (-8)   /* option not supported by this build */
+
+#define NC_INTERIOR 0    /* narrow escape, G_I, read-out mu (eq:mufromsigma2) */
+#define NC_EXTERIOR 1    /* narrow capture, G_E, read-out J = -4 pi I_sigma (reading R2) */
+
+#define NC_DIRECT 0      /* tiled direct sum over all source patches j != i (eq:mssums) */
+#define NC_HIER 1        /* hierarchical O(N log N) scheme of §8 steps 1-5 */
+
+/* Patch-operator tables: Step-1 outputs for one patch radius, host memory,
+ * copied by nc_setup (the caller may free them afterwards).  Canonical frame: patch centre at +z,
+ * azimuth theta = 0 along +x. */
+typedef struct nc_tables {
+  int32_t M;           /* Zernike truncation; K must equal (M+1)(M+2)/2      */
+  int32_t K;           /* compressed dofs per patch                                             */
+  int32_t Kstar;       /* Zernike sampling nodes per patch, >= K             */
+  int32_t p;           /* skeleton size (rank of the ID), 1 <= p <= 1024    */
+  const double* zhat;  /* Kstar x 3  Zernike sampling nodes (unit vectors)                      */
+  const double* P;     /* K x Kstar  discrete Zernike transform               */
+  const double* shat;  /* p x 3      skeleton nodes x^f_{pi(m)} (unit vectors, inside the patch) */
+  const double* T;     /* p x K      outgoing map rho = T fhat (eq:Tmap)                         */
+  const double* I;     /* K          integration row, I_sigma = I . sum_i fhat_i (eq:getI)       */
+} nc_tables;
+
+typedef struct nc_opts {
+  int32_t mode;          /* NC_DIRECT or NC_HIER                                                 */
+  double precision;      /* NC_HIER: requested matvec precision (default 1e-9 when <= 0)         */
+  int32_t device;        /* CUDA device ordinal (-1: current device)                             */
+  int32_t world;         /* number of ranks (1 = single GPU)                                     */
+  int32_t rank;          /* this rank, 0 <= rank < world                                         */
+  const void* nccl_id;   /* world > 1: pointer to the 128-byte ncclUniqueId made by rank 0       */
+  int32_t check_separation; /* 1: verify the 3 eps separation (NC_ESEP on failure); 0: trust input */
+} nc_opts;
+
+typedef struct nc_stats_t {
+  int64_t N, row_begin, row_count;
+  int32_t K, Kstar, p, mode, world, rank;
+  int64_t matvecs;              /* matvecs applied since setup                                     */
+  double pairs_per_matvec;      /* kernel evaluations G(x,y) rho per matvec on this rank           */
+  double gemm_flops_per_matvec; /* 2 p K n + 2 K Kstar n on this rank (n = row_count)              */
+  double ms_last[8];            /* per-stage device ms of the last timed matvec:                   */
+                                /*   [0] T-apply  [1] all-gather  [2] pair sums  [3] P-apply       */
+                                /*   [4] hier step 2+3  [5] hier step 4  [6] total  [7] reserved   */
+  int32_t tree_levels;          /* NC_HIER: depth L of the sphere quadtree                         */
+  int64_t tree_groups;          /* NC_HIER: number of non-empty boxes over all levels              */
+  double device_bytes;          /* device memory held by the handle                                */
+} nc_stats_t;
+
+typedef struct nc_handle nc_handle;
+
+/* Build the per-layout state (Step 2): frames R_i, global Zernike and skeleton
+ * nodes, and (NC_HIER) the sphere quadtree, interaction lists and incoming grids.
+ *   kind    NC_INTERIOR | NC_EXTERIOR
+ *   N       number of patches (>= 1)
+ *   centers host, N x 3, unit vectors, caller order
+ *   eps     patch radius (arc length, > 0)
+ * Frames follow the ABI rule (R8): e1 = normalize(xhat - (xhat.c)c) (yhat instead of xhat
+ * when |c.xhat| > 0.9), e2 = c x e1, R_i = [e1 e2 c_i].
+ * Errors: NC_EINVAL, NC_ESEP, NC_ENOMEM, NC_ECUDA, NC_ENCCL.  On error *h is set to NULL. */
+int nc_setup(nc_handle** h, int kind, int64_t N, const double* centers, double eps, const nc_tables* tab,
+             const nc_opts* opt);
+
+/* This rank's shard and the internal order.  perm (host, N entries, nullable): perm[internal] =
+ * caller index.  Errors: NC_EINVAL (null handle). */
+int nc_partition(const nc_handle* h, int64_t* row_begin, int64_t* row_count, int64_t* perm);
+
+/* y = (I + A_off) x on this rank's rows (eq:sysmatapply).  x, y: device, row_count x K, must not
+ * alias.  stream: cudaStream_t (NULL = legacy default stream).  Asynchronous with respect to the
+ * host for world == 1; collective (one all-gather) for world > 1.  Errors: NC_EINVAL, NC_ECUDA,
+ * NC_ENCCL. */
+int nc_matvec(nc_handle* h, const double* x, double* y, void* stream);
+
+/* Same map with HOST buffers (row_count x K each): copies x in, applies, copies y out, synchronizes.
+ * This is the end-to-end entry point timed as "e2e" by bench.py. */
+int nc_matvec_host(nc_handle* h, const double* x_host, double* y_host);
+
+/* Unrestarted GMRES for (I + A_off) x = b, x0 = 0, classical Gram-Schmidt with
+ * one full re-orthogonalisation (CGS2), stop when the implicit residual ||b - A x|| / ||b|| <= rtol.
+ *   b     device, row_count x K, or NULL for the physical right-hand side b_i = P 1 (eq:opinteqnsdisc)
+ *   x     device, row_count x K (output)
+ *   iters host (output), number of iterations (= matvecs) performed
+ *   hist  host, max_iter + 1 doubles or NULL: relative residual after 0..iters iterations
+ * Synchronizes the stream.  Errors: NC_ENOCONV (x = last iterate), NC_EINVAL, NC_ECUDA, NC_ENCCL. */
+int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x, int* iters, double* hist,
+             void* stream);
+
+/* Read-out (eq:getI): I_sigma = I . sum_i x_i over all ranks (collective), then
+ * value = mu = 1/(3 I_sigma) - 3/5 (interior, eq:mufromsigma2) or J = -4 pi I_sigma (exterior,
+ * DESIGN.md R2).  x: device, row_count x K.  I_sigma, value: host.  Synchronizes.
+ * Errors: NC_ESTATE when the interior I_sigma <= 0 (the Lemma of PAPER.md:579-590 needs I_sigma != 0). */
+int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* value);
+
+/* Counters and the last matvec's per-stage device times.  nc_time_stages(h, 1) makes the next
+ * matvecs record per-stage CUDA events (adds event overhead; off by default). */
+int nc_stats(const nc_handle* h, nc_stats_t* out);
+int nc_time_stages(nc_handle* h, int enable);
+
+/* Debug/introspection (NC_HIER): number of (level, target group, source group) interaction-list
+ * entries and leaf-neighbour entries, copied to host arrays of 3 int64 per entry when non-NULL.
+ * Used by the exactly-once pair-coverage audit (tests/test_hier.py). */
+int nc_tree_lists(const nc_handle* h, int64_t* n_ilist, int64_t* ilist, int64_t* n_nbr, int64_t* nbr,
+                  int64_t* box_of_patch /* L+1 x N, nullable */);
+
+/* world > 1 bootstrap: rank 0 creates the 128-byte NCCL unique id (host buffer), the caller broadcasts it
+ * (e.g. torch.distributed) and passes it as nc_opts.nccl_id on every rank.  NC_EUNSUP without NCCL. */
+int nc_nccl_unique_id(void* id_out);
+
+void nc_destroy(nc_handle* h);
+const char* nc_last_error(void);
+const char* nc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NC_H_ */

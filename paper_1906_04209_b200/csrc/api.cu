@@ -1,0 +1,553 @@
+// api.cu -- the C ABI of libnc (include/nc.h): setup, matvec, GMRES, read-out.
+//
+// Matvec pipeline per call (direct mode), all in this library's kernels:
+//   K1  rho = X T^T          fp64 DMMA GEMM, epilogue writes rho into the packed source records
+//   AG  ncclAllGather of the source records (world > 1 only)
+//   K2  pair sums            u_{ik} = sum_{j != i} sum_m G(z_ik, s_jm) rho_jm  (direct.cu)
+//   K3  Y = X + U P^T        fp64 DMMA GEMM with the segment reduction fused into its operand load
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "hier.cuh"
+#include "nc_common.cuh"
+
+namespace nc {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what;
+  return NC_ECUDA;
+}
+
+template <class T>
+static int dalloc(nc_handle* h, T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(NC_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed: " +
+                               cudaGetErrorString(e));
+  }
+  h->device_bytes += (double)count * sizeof(T);
+  return NC_OK;
+}
+
+// -------------------------------------------------------------------------------------------------
+// host-side validation helpers
+// -------------------------------------------------------------------------------------------------
+// Minimum arc separation >= 3 eps (§3) via a uniform 3-D hash grid on chords.
+static int check_separation(const double* c, int64_t N, double eps) {
+  const double min_arc = 3.0 * eps * (1.0 - 1e-12);
+  const double chord = 2.0 * sin(0.5 * std::min(min_arc, M_PI));
+  const double cell = std::max(chord, 1e-6);
+  const int64_t nc = (int64_t)ceil(2.0 / cell) + 2;
+  auto key = [&](int64_t a, int64_t b, int64_t d) { return (a * nc + b) * nc + d; };
+  std::unordered_map<int64_t, std::vector<int64_t>> grid;
+  grid.reserve((size_t)N * 2);
+  auto cidx = [&](double v) { return (int64_t)floor((v + 1.0) / cell); };
+  for (int64_t i = 0; i < N; ++i) grid[key(cidx(c[3 * i]), cidx(c[3 * i + 1]), cidx(c[3 * i + 2]))].push_back(i);
+  for (int64_t i = 0; i < N; ++i) {
+    int64_t a = cidx(c[3 * i]), b = cidx(c[3 * i + 1]), d = cidx(c[3 * i + 2]);
+    for (int da = -1; da <= 1; ++da)
+      for (int db = -1; db <= 1; ++db)
+        for (int dd = -1; dd <= 1; ++dd) {
+          auto it = grid.find(key(a + da, b + db, d + dd));
+          if (it == grid.end()) continue;
+          for (int64_t j : it->second) {
+            if (j <= i) continue;
+            double dx = c[3 * i] - c[3 * j], dy = c[3 * i + 1] - c[3 * j + 1], dz = c[3 * i + 2] - c[3 * j + 2];
+            double ch = sqrt(dx * dx + dy * dy + dz * dz);
+            double arc = 2.0 * asin(std::min(1.0, 0.5 * ch));
+            if (arc < min_arc) {
+              char buf[256];
+              snprintf(buf, sizeof buf, "patches %lld and %lld are %.6g apart in arc length (< 3 eps = %.6g)",
+                       (long long)i, (long long)j, arc, 3.0 * eps);
+              return fail(NC_ESEP, buf);
+            }
+          }
+        }
+  }
+  return NC_OK;
+}
+
+static void compute_nseg(nc_handle* h) {
+  int64_t tiles = (h->row_count * h->Kstar + kPairThreads - 1) / kPairThreads;
+  if (tiles < 1) tiles = 1;
+  int64_t want = (8 * 148 * 4 + tiles - 1) / tiles;   // >= ~8 waves of 4 CTAs/SM
+  int64_t cap = std::min<int64_t>(h->N, 64);
+  h->nseg = (int)std::max<int64_t>(1, std::min(want, cap));
+}
+
+static int ensure_red(nc_handle* h, int64_t count) {
+  if (count <= h->red_cap) return NC_OK;
+  if (h->d_red) cudaFree(h->d_red);
+  if (h->h_red) cudaFreeHost(h->h_red);
+  h->d_red = nullptr;
+  h->h_red = nullptr;
+  NC_TRY(dalloc(h, &h->d_red, (size_t)count));
+  NC_CUDA_TRY(cudaMallocHost((void**)&h->h_red, count * sizeof(double)));
+  h->red_cap = count;
+  return NC_OK;
+}
+
+static int allreduce_sum(nc_handle* h, double* dev, int64_t count, cudaStream_t s) {
+  if (h->world <= 1) return NC_OK;
+#if NC_WITH_NCCL
+  ncclResult_t r = ncclAllReduce(dev, dev, (size_t)count, ncclDouble, ncclSum, h->comm, s);
+  if (r != ncclSuccess) return fail(NC_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+  return NC_OK;
+#else
+  (void)dev; (void)count; (void)s;
+  return fail(NC_EUNSUP, "built without NCCL");
+#endif
+}
+
+}  // namespace nc
+
+using namespace nc;
+
+extern "C" {
+
+const char* nc_last_error(void) { return g_err.c_str(); }
+const char* nc_version(void) { return "libnc 0.1 (sm_100a, fp64)"; }
+
+int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double eps, const nc_tables* tab,
+             const nc_opts* opt) {
+  if (!out) return fail(NC_EINVAL, "nc_setup: null output handle pointer");
+  *out = nullptr;
+  if (!centers || !tab || !opt) return fail(NC_EINVAL, "nc_setup: null centers/tables/opts");
+  if (kind != NC_INTERIOR && kind != NC_EXTERIOR) return fail(NC_EINVAL, "nc_setup: kind must be 0 or 1");
+  if (N < 1) return fail(NC_EINVAL, "nc_setup: N must be >= 1");
+  if (!(eps > 0.0) || !(eps < 1.0)) return fail(NC_EINVAL, "nc_setup: eps must be in (0, 1)");
+  if (tab->M < 0 || tab->K != (tab->M + 1) * (tab->M + 2) / 2)
+    return fail(NC_EINVAL, "nc_setup: K != (M+1)(M+2)/2");
+  if (tab->K > 1024) return fail(NC_EINVAL, "nc_setup: K > 1024 not supported");
+  if (tab->Kstar < 1 || tab->p < 1 || tab->p > kMaxP) return fail(NC_EINVAL, "nc_setup: bad Kstar or p");
+  if (!tab->zhat || !tab->P || !tab->shat || !tab->T || !tab->I) return fail(NC_EINVAL, "nc_setup: null table");
+  if (opt->mode != NC_DIRECT && opt->mode != NC_HIER) return fail(NC_EINVAL, "nc_setup: bad mode");
+  if (opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world) return fail(NC_EINVAL, "nc_setup: bad rank/world");
+  for (int64_t i = 0; i < N; ++i) {
+    double r = sqrt(centers[3 * i] * centers[3 * i] + centers[3 * i + 1] * centers[3 * i + 1] +
+                    centers[3 * i + 2] * centers[3 * i + 2]);
+    if (!(fabs(r - 1.0) < 1e-10)) return fail(NC_EINVAL, "nc_setup: centre " + std::to_string(i) + " is not unit");
+  }
+  if (opt->check_separation) NC_TRY(check_separation(centers, N, eps));
+#if !NC_WITH_NCCL
+  if (opt->world > 1) return fail(NC_EUNSUP, "nc_setup: world > 1 needs a build with NCCL");
+#endif
+
+  nc_handle* h = new nc_handle();
+  auto bail = [&](int rc) {
+    std::string keep = g_err;
+    nc_destroy(h);
+    g_err = keep;
+    return rc;
+  };
+  h->kind = kind;
+  h->mode = opt->mode;
+  h->world = opt->world;
+  h->rank = opt->rank;
+  h->N = N;
+  h->M = tab->M;
+  h->K = tab->K;
+  h->Kstar = tab->Kstar;
+  h->p = tab->p;
+  h->eps = eps;
+  h->precision = opt->precision > 0 ? opt->precision : 1e-9;
+  if (opt->device >= 0) {
+    cudaError_t e = cudaSetDevice(opt->device);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaSetDevice"));
+  }
+  {
+    cudaError_t e = cudaGetDevice(&h->device);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaGetDevice"));
+    e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaStreamCreate"));
+    for (auto& ev : h->ev) {
+      e = cudaEventCreate(&ev);
+      if (e != cudaSuccess) return bail(cuda_fail(e, "cudaEventCreate"));
+    }
+  }
+  cudaStream_t s = h->stream;
+  const int K = h->K, Ks = h->Kstar, p = h->p;
+
+  // tables
+  int rc;
+  if ((rc = dalloc(h, &h->d_T, (size_t)p * K)) || (rc = dalloc(h, &h->d_P, (size_t)K * Ks)) ||
+      (rc = dalloc(h, &h->d_I, (size_t)K)) || (rc = dalloc(h, &h->d_zhat, (size_t)Ks * 3)) ||
+      (rc = dalloc(h, &h->d_shat, (size_t)p * 3)))
+    return bail(rc);
+  h->h_I.assign(tab->I, tab->I + K);
+  h->h_P1.assign(K, 0.0);
+  for (int a = 0; a < K; ++a) {
+    double v = 0.0;
+    for (int k = 0; k < Ks; ++k) v += tab->P[(size_t)a * Ks + k];
+    h->h_P1[a] = v;
+  }
+#define UP(dst, src, cnt)                                                                   \
+  do {                                                                                      \
+    cudaError_t _e = cudaMemcpyAsync(dst, src, (cnt) * sizeof(double), cudaMemcpyHostToDevice, s); \
+    if (_e != cudaSuccess) return bail(cuda_fail(_e, "upload " #src));                      \
+  } while (0)
+  UP(h->d_T, tab->T, (size_t)p * K);
+  UP(h->d_P, tab->P, (size_t)K * Ks);
+  UP(h->d_I, tab->I, (size_t)K);
+  UP(h->d_zhat, tab->zhat, (size_t)Ks * 3);
+  UP(h->d_shat, tab->shat, (size_t)p * 3);
+
+  // internal order: identity (direct); the tree order (hierarchical) is applied by hier_setup
+  h->perm.resize(N);
+  for (int64_t i = 0; i < N; ++i) h->perm[i] = i;
+  std::vector<double> cs(centers, centers + 3 * N);
+  if (h->mode == NC_HIER) {
+    rc = hier_order(h, cs);          // Morton order of the cube-face quadtree; fills h->perm, permutes cs
+    if (rc) return bail(rc);
+  }
+
+  // partition: equal contiguous row ranges (all rows carry the same work in direct mode)
+  h->rows_per_rank = (N + h->world - 1) / h->world;
+  h->row_begin = std::min<int64_t>(N, (int64_t)h->rank * h->rows_per_rank);
+  h->row_count = std::min<int64_t>(h->rows_per_rank, N - h->row_begin);
+  if (h->mode == NC_HIER) {
+    rc = hier_partition(h);
+    if (rc) return bail(rc);
+  }
+
+  if ((rc = dalloc(h, &h->d_centers, (size_t)N * 3)) || (rc = dalloc(h, &h->d_frames, (size_t)N * 9))) return bail(rc);
+  UP(h->d_centers, cs.data(), (size_t)N * 3);
+  launch_frames(h->d_centers, N, h->d_frames, s);
+
+  // source records (x, y, z, rho) for all patches, padded to world * rows_per_rank
+  const int64_t n_src_rows = (int64_t)h->world * h->rows_per_rank;
+  if ((rc = dalloc(h, &h->d_src4, (size_t)n_src_rows * p * 4))) return bail(rc);
+  {
+    cudaError_t e = cudaMemsetAsync(h->d_src4, 0, (size_t)n_src_rows * p * 4 * sizeof(double), s);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "memset src4"));
+  }
+  launch_sources(h->d_frames, N, h->d_shat, p, h->d_src4, s);
+
+  if (h->mode == NC_DIRECT) {
+    const int64_t nt = h->row_count * Ks;
+    if ((rc = dalloc(h, &h->d_tx, (size_t)nt)) || (rc = dalloc(h, &h->d_ty, (size_t)nt)) ||
+        (rc = dalloc(h, &h->d_tz, (size_t)nt)))
+      return bail(rc);
+    launch_targets(h->d_frames, h->row_begin, h->row_count, h->d_zhat, Ks, h->d_tx, h->d_ty, h->d_tz, s);
+    compute_nseg(h);
+    if ((rc = dalloc(h, &h->d_upart, (size_t)h->nseg * nt))) return bail(rc);
+    h->pairs_per_matvec = (double)h->row_count * Ks * (double)(N - 1) * p;
+  } else {
+    rc = hier_setup(h, s);
+    if (rc) return bail(rc);
+  }
+  if ((rc = ensure_red(h, 4096))) return bail(rc);
+
+#if NC_WITH_NCCL
+  if (h->world > 1) {
+    if (!opt->nccl_id) return bail(fail(NC_EINVAL, "nc_setup: world > 1 needs nccl_id"));
+    ncclUniqueId id;
+    memcpy(&id, opt->nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&h->comm, h->world, id, h->rank);
+    if (r != ncclSuccess) return bail(fail(NC_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
+  }
+#endif
+  {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "nc_setup sync"));
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return bail(cuda_fail(e, "nc_setup kernels"));
+  }
+#undef UP
+  *out = h;
+  return NC_OK;
+}
+
+int nc_partition(const nc_handle* h, int64_t* row_begin, int64_t* row_count, int64_t* perm) {
+  if (!h) return fail(NC_EINVAL, "nc_partition: null handle");
+  if (row_begin) *row_begin = h->row_begin;
+  if (row_count) *row_count = h->row_count;
+  if (perm) memcpy(perm, h->perm.data(), h->N * sizeof(int64_t));
+  return NC_OK;
+}
+
+int nc_time_stages(nc_handle* h, int enable) {
+  if (!h) return fail(NC_EINVAL, "nc_time_stages: null handle");
+  h->time_stages = enable != 0;
+  return NC_OK;
+}
+
+static inline void mark(nc_handle* h, int i, cudaStream_t s) {
+  if (h->time_stages) cudaEventRecord(h->ev[i], s);
+}
+
+int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
+  if (!h || !x || !y) return fail(NC_EINVAL, "nc_matvec: null argument");
+  if (x == y) return fail(NC_EINVAL, "nc_matvec: x and y must not alias");
+  NC_CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int K = h->K, p = h->p, Ks = h->Kstar;
+  mark(h, 0, s);
+  // K1: rho_i = T fhat_i for this rank's rows, written into the source records' 4th slot
+  launch_gemm_dmma(x, K, 1, 0, h->d_T, h->row_count, p, K, h->d_src4 + (size_t)h->row_begin * p * 4 + 3,
+                   (int64_t)p * 4, 4, nullptr, 0, s);
+  mark(h, 1, s);
+  if (h->world > 1) {
+#if NC_WITH_NCCL
+    const size_t cnt = (size_t)h->rows_per_rank * p * 4;
+    ncclResult_t r = ncclAllGather(h->d_src4 + (size_t)h->rank * cnt, h->d_src4, cnt, ncclDouble, h->comm, s);
+    if (r != ncclSuccess) return fail(NC_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+#endif
+  }
+  mark(h, 2, s);
+  if (h->mode == NC_DIRECT) {
+    launch_pairs_direct(h->kind, h->d_tx, h->d_ty, h->d_tz, h->row_count * Ks, Ks, h->row_begin, h->d_src4, p, h->N,
+                        h->nseg, h->d_upart, s);
+    mark(h, 3, s);
+    // K3: Y = X + (sum_seg U_seg) P^T
+    launch_gemm_dmma(h->d_upart, Ks, h->nseg, h->row_count * Ks, h->d_P, h->row_count, K, Ks, y, K, 1, x, K, s);
+    mark(h, 4, s);
+  } else {
+    NC_TRY(hier_matvec(h, x, y, s));
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "nc_matvec launch");
+  if (h->time_stages) {
+    NC_CUDA_TRY(cudaEventSynchronize(h->ev[4]));
+    float ms;
+    cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]); h->ms_last[0] = ms;
+    cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]); h->ms_last[1] = ms;
+    if (h->mode == NC_DIRECT) {
+      cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); h->ms_last[2] = ms;
+      cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]); h->ms_last[3] = ms;
+    }
+    cudaEventElapsedTime(&ms, h->ev[0], h->ev[4]); h->ms_last[6] = ms;
+  }
+  h->matvecs++;
+  return NC_OK;
+}
+
+int nc_matvec_host(nc_handle* h, const double* x_host, double* y_host) {
+  if (!h || !x_host || !y_host) return fail(NC_EINVAL, "nc_matvec_host: null argument");
+  NC_CUDA_TRY(cudaSetDevice(h->device));
+  const size_t n = (size_t)h->row_count * h->K;
+  if (!h->d_hx) {
+    NC_TRY(dalloc(h, &h->d_hx, n));
+    NC_TRY(dalloc(h, &h->d_hy, n));
+  }
+  cudaStream_t s = h->stream;
+  NC_CUDA_TRY(cudaMemcpyAsync(h->d_hx, x_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  NC_TRY(nc_matvec(h, h->d_hx, h->d_hy, s));
+  NC_CUDA_TRY(cudaMemcpyAsync(y_host, h->d_hy, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NC_CUDA_TRY(cudaStreamSynchronize(s));
+  return NC_OK;
+}
+
+// helper: device dot products of V[0..nv) with w into d_out (nv doubles), all-reduced across ranks
+static int dots(nc_handle* h, const double* V, int64_t ldv, int nv, const double* w, int64_t n, double* d_out,
+                cudaStream_t s) {
+  double* part = h->d_red + 2048;   // partial buffer region (needs nv * 592 doubles)
+  launch_multidot(V, ldv, nv, w, n, part, d_out, s);
+  return allreduce_sum(h, d_out, nv, s);
+}
+
+int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x, int* iters, double* hist,
+             void* stream) {
+  if (!h || !x || max_iter < 1 || !(rtol > 0)) return fail(NC_EINVAL, "nc_gmres: bad arguments");
+  NC_CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = h->row_count * h->K;
+  const int64_t ldv = std::max<int64_t>(n, 1);
+  if (h->V_cap < max_iter + 1) {
+    if (h->d_V) {
+      cudaFree(h->d_V);
+      h->device_bytes -= (double)h->V_cap * ldv * sizeof(double);
+      h->d_V = nullptr;
+    }
+    NC_TRY(dalloc(h, &h->d_V, (size_t)(max_iter + 1) * ldv));
+    h->V_cap = max_iter + 1;
+  }
+  // reduction scratch: [0, 2048) small vectors, [2048, ...) multidot partials
+  NC_TRY(ensure_red(h, 2048 + (int64_t)(max_iter + 2) * multidot_partials(n) + 16));
+  double* V = h->d_V;
+  double* d_h1 = h->d_red;            // first-pass projections  (<= max_iter+1)
+  double* d_h2 = h->d_red + 640;      // second-pass projections
+  double* d_nrm = h->d_red + 1280;    // ||w||^2
+  if (max_iter + 1 > 640) return fail(NC_EINVAL, "nc_gmres: max_iter must be <= 639");
+
+  // v0 = b / ||b||
+  if (b) {
+    NC_CUDA_TRY(cudaMemcpyAsync(V, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  } else {
+    if (!h->d_b) NC_TRY(dalloc(h, &h->d_b, (size_t)h->K));
+    NC_CUDA_TRY(cudaMemcpyAsync(h->d_b, h->h_P1.data(), h->K * sizeof(double), cudaMemcpyHostToDevice, s));
+    launch_fill_rows(V, h->d_b, h->K, h->row_count, s);
+  }
+  NC_TRY(dots(h, V, ldv, 1, V, n, d_nrm, s));
+  NC_CUDA_TRY(cudaMemcpyAsync(h->h_red, d_nrm, sizeof(double), cudaMemcpyDeviceToHost, s));
+  NC_CUDA_TRY(cudaStreamSynchronize(s));
+  const double beta = sqrt(h->h_red[0]);
+  if (hist) hist[0] = 1.0;
+  if (beta == 0.0) {
+    NC_CUDA_TRY(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+    if (iters) *iters = 0;
+    NC_CUDA_TRY(cudaStreamSynchronize(s));
+    return NC_OK;
+  }
+  {
+    double inv = beta;
+    NC_CUDA_TRY(cudaMemcpyAsync(d_nrm, &inv, sizeof(double), cudaMemcpyHostToDevice, s));
+    launch_scale(V, V, d_nrm, 1, n, s);
+  }
+  const int m = max_iter;
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1, 0.0);
+  auto Hc = [&](int i, int j) -> double& { return H[(size_t)i * m + j]; };
+  g[0] = beta;
+  int k = 0;
+  bool converged = false;
+  for (int j = 0; j < m; ++j) {
+    double* w = V + (size_t)(j + 1) * ldv;
+    NC_TRY(nc_matvec(h, V + (size_t)j * ldv, w, s));
+    // CGS2: two classical Gram-Schmidt passes
+    NC_TRY(dots(h, V, ldv, j + 1, w, n, d_h1, s));
+    launch_gemv_sub(V, ldv, j + 1, d_h1, w, n, s);
+    NC_TRY(dots(h, V, ldv, j + 1, w, n, d_h2, s));
+    launch_gemv_sub(V, ldv, j + 1, d_h2, w, n, s);
+    NC_TRY(dots(h, w, ldv, 1, w, n, d_nrm, s));
+    NC_CUDA_TRY(cudaMemcpyAsync(h->h_red, h->d_red, 1281 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    NC_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int i = 0; i <= j; ++i) Hc(i, j) = h->h_red[i] + h->h_red[640 + i];
+    double hn = sqrt(std::max(0.0, h->h_red[1280]));
+    Hc(j + 1, j) = hn;
+    if (hn > 0) {
+      NC_CUDA_TRY(cudaMemcpyAsync(d_nrm, &Hc(j + 1, j), sizeof(double), cudaMemcpyHostToDevice, s));
+      launch_scale(w, w, d_nrm, 1, n, s);
+    }
+    for (int i = 0; i < j; ++i) {
+      double t = cs[i] * Hc(i, j) + sn[i] * Hc(i + 1, j);
+      Hc(i + 1, j) = -sn[i] * Hc(i, j) + cs[i] * Hc(i + 1, j);
+      Hc(i, j) = t;
+    }
+    double r = hypot(Hc(j, j), Hc(j + 1, j));
+    cs[j] = Hc(j, j) / r;
+    sn[j] = Hc(j + 1, j) / r;
+    Hc(j, j) = r;
+    Hc(j + 1, j) = 0.0;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    k = j + 1;
+    double rel = fabs(g[j + 1]) / beta;
+    if (hist) hist[k] = rel;
+    if (rel <= rtol) {
+      converged = true;
+      break;
+    }
+    if (hn == 0.0) break;   // lucky breakdown
+  }
+  std::vector<double> yv(k, 0.0);
+  for (int i = k - 1; i >= 0; --i) {
+    double v = g[i];
+    for (int l = i + 1; l < k; ++l) v -= Hc(i, l) * yv[l];
+    yv[i] = v / Hc(i, i);
+  }
+  NC_CUDA_TRY(cudaMemcpyAsync(h->d_red, yv.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+  launch_lincomb(V, ldv, k, h->d_red, x, n, s);
+  NC_CUDA_TRY(cudaStreamSynchronize(s));
+  NC_CUDA_TRY(cudaGetLastError());
+  if (iters) *iters = k;
+  if (!converged && fabs(g[k]) / beta > rtol)
+    return fail(NC_ENOCONV, "nc_gmres: no convergence in " + std::to_string(k) + " iterations");
+  return NC_OK;
+}
+
+int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* value) {
+  if (!h || !x) return fail(NC_EINVAL, "nc_flux_or_mfpt: null argument");
+  NC_CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t s = h->stream;
+  NC_TRY(ensure_red(h, std::max<int64_t>(4096, 1024 + (int64_t)592 * h->K + 16)));
+  double* d_sum = h->d_red;             // K <= 1024 (checked in nc_setup)
+  double* part = h->d_red + 1024;
+  launch_colsum(x, h->row_count, h->K, part, d_sum, s);
+  NC_TRY(allreduce_sum(h, d_sum, h->K, s));
+  std::vector<double> col(h->K);
+  NC_CUDA_TRY(cudaMemcpyAsync(col.data(), d_sum, h->K * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NC_CUDA_TRY(cudaStreamSynchronize(s));
+  double Is = 0.0;
+  for (int a = 0; a < h->K; ++a) Is += h->h_I[a] * col[a];
+  if (I_sigma) *I_sigma = Is;
+  double v;
+  if (h->kind == NC_INTERIOR) {
+    if (!(Is > 0.0)) return fail(NC_ESTATE, "nc_flux_or_mfpt: interior I_sigma <= 0");
+    v = 1.0 / (3.0 * Is) - 3.0 / 5.0;   // eq:mufromsigma2
+  } else {
+    v = -4.0 * M_PI * Is;                // J = -4 pi I_sigma (R2)
+  }
+  if (value) *value = v;
+  return NC_OK;
+}
+
+int nc_stats(const nc_handle* h, nc_stats_t* o) {
+  if (!h || !o) return fail(NC_EINVAL, "nc_stats: null argument");
+  memset(o, 0, sizeof(*o));
+  o->N = h->N;
+  o->row_begin = h->row_begin;
+  o->row_count = h->row_count;
+  o->K = h->K;
+  o->Kstar = h->Kstar;
+  o->p = h->p;
+  o->mode = h->mode;
+  o->world = h->world;
+  o->rank = h->rank;
+  o->matvecs = h->matvecs;
+  o->pairs_per_matvec = h->pairs_per_matvec;
+  o->gemm_flops_per_matvec = 2.0 * h->row_count * ((double)h->p * h->K + (double)h->K * h->Kstar);
+  for (int i = 0; i < 8; ++i) o->ms_last[i] = h->ms_last[i];
+  o->device_bytes = h->device_bytes;
+  hier_fill_stats(h, o);
+  return NC_OK;
+}
+
+int nc_nccl_unique_id(void* id_out) {
+  if (!id_out) return fail(NC_EINVAL, "nc_nccl_unique_id: null buffer");
+#if NC_WITH_NCCL
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(NC_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  memcpy(id_out, &id, sizeof(id));
+  return NC_OK;
+#else
+  return fail(NC_EUNSUP, "built without NCCL");
+#endif
+}
+
+void nc_destroy(nc_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  hier_destroy(h);
+  double* bufs[] = {h->d_T, h->d_P, h->d_I, h->d_zhat, h->d_shat, h->d_centers, h->d_frames, h->d_tx, h->d_ty,
+                    h->d_tz, h->d_src4, h->d_upart, h->d_V, h->d_red, h->d_b, h->d_hx, h->d_hy};
+  for (double* b : bufs)
+    if (b) cudaFree(b);
+  if (h->h_red) cudaFreeHost(h->h_red);
+  for (auto& ev : h->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (h->stream) cudaStreamDestroy(h->stream);
+#if NC_WITH_NCCL
+  if (h->comm) ncclCommDestroy(h->comm);
+#endif
+  delete h;
+}
+
+}  // extern "C"

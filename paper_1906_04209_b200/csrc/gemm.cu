@@ -1,0 +1,102 @@
+// gemm.cu -- the two per-patch operator applications of the matvec as fp64 tensor-core GEMMs.
+//
+//   step 1: rho_i = T fhat_i for all i      -> C = X T^T        (N x p)
+//   step 5: y_i = fhat_i + P u_i for all i  -> Y = X + U P^T    (N x K)
+//
+// B200 has no fp64 kind in tcgen05; the fp64 tensor path is the legacy warp-level
+// mma.sync.aligned.m8n8k4.f64 (SASS DMMA.8x8x4), measured at 37.1 TF/s on this pool
+// (profiles/r01_fp64_peak.txt).  CTA tile 64 x 64 x 16, 8 warps (4 x 2), each warp 16 x 32 = 2 x 4 DMMA tiles;
+// operands staged in padded shared memory (row stride BK+4 doubles: conflict-free fragment loads).
+// For step 5 the A operand is the sum of the direct kernel's per-segment partial fields (fused
+// deterministic reduction), and the epilogue adds the identity term.
+#include "nc_common.cuh"
+
+namespace nc {
+
+namespace {
+constexpr int BM = 64, BN = 64, BK = 16, LDS = BK + 4;
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A, int64_t lda, int nparts,
+                                                   int64_t part_stride, const double* __restrict__ Bt, int64_t rows,
+                                                   int ncols, int kd, double* __restrict__ C, int64_t ldc,
+                                                   int cstride, const double* __restrict__ X, int64_t ldx) {
+  __shared__ double As[BM][LDS];
+  __shared__ double Bs[BN][LDS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int64_t row0 = (int64_t)blockIdx.x * BM;
+  const int col0 = blockIdx.y * BN;
+
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  for (int k0 = 0; k0 < kd; k0 += BK) {
+    // stage A (sum of parts) and Bt tiles; consecutive threads read consecutive k (coalesced)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int r = (tid >> 4) + 16 * q, c = tid & 15;
+      int64_t gr = row0 + r;
+      int gk = k0 + c;
+      double v = 0.0;
+      if (gr < rows && gk < kd) {
+        const double* pa = A + gr * lda + gk;
+        v = pa[0];
+        for (int s = 1; s < nparts; ++s) v += pa[s * part_stride];
+      }
+      As[r][c] = v;
+      int n = col0 + r;
+      Bs[r][c] = (n < ncols && gk < kd) ? Bt[(int64_t)n * kd + gk] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) af[mi] = As[wm * 16 + mi * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) bf[ni] = Bs[wn * 32 + ni * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
+    }
+    __syncthreads();
+  }
+  // epilogue: C(i, n) = [X(i, n) +] acc
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi) {
+    int64_t gr = row0 + wm * 16 + mi * 8 + (lane >> 2);
+    if (gr >= rows) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int n = col0 + wn * 32 + ni * 8 + (lane & 3) * 2 + e;
+        if (n >= ncols) continue;
+        double v = acc[mi][ni][e];
+        if (X) v += X[gr * ldx + n];
+        C[gr * ldc + (int64_t)n * cstride] = v;
+      }
+    }
+  }
+}
+
+void launch_gemm_dmma(const double* A, int64_t lda, int nparts, int64_t part_stride, const double* Bt, int64_t rows,
+                      int ncols, int kd, double* C, int64_t ldc, int cstride, const double* X, int64_t ldx,
+                      cudaStream_t s) {
+  if (rows <= 0) return;
+  dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((ncols + BN - 1) / BN));
+  k_gemm_dmma<<<grid, 256, 0, s>>>(A, lda, nparts, part_stride, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx);
+}
+
+}  // namespace nc

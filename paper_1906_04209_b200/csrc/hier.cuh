@@ -1,0 +1,14 @@
+// hier.cuh -- hierarchical (NC_HIER) mode entry points used by api.cu (implemented in hier.cu).
+#pragma once
+#include <vector>
+
+#include "nc_common.cuh"
+
+namespace nc {
+int hier_order(nc_handle* h, std::vector<double>& centers);   // tree order; fills h->perm, permutes centers
+int hier_partition(nc_handle* h);                              // work-weighted contiguous row ranges
+int hier_setup(nc_handle* h, cudaStream_t s);                  // tree, lists, grids (device)
+int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s);
+void hier_fill_stats(const nc_handle* h, nc_stats_t* o);
+void hier_destroy(nc_handle* h);
+}  // namespace nc

@@ -1,0 +1,142 @@
+// nc_common.cuh -- internal declarations shared by the libnc translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/nc.h"
+
+#if NC_WITH_NCCL
+#include <nccl.h>
+#endif
+
+namespace nc {
+
+// ------------------------------------------------------------------------------------------------
+// error plumbing
+// ------------------------------------------------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define NC_CUDA_TRY(expr)                                   \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return ::nc::cuda_fail(_e, #expr); \
+  } while (0)
+
+#define NC_TRY(expr)             \
+  do {                           \
+    int _rc = (expr);            \
+    if (_rc != NC_OK) return _rc; \
+  } while (0)
+
+constexpr int kMaxP = 1024;
+constexpr int kPairThreads = 256;   // targets per CTA in the direct pair-sum kernel
+
+// ------------------------------------------------------------------------------------------------
+// hierarchical-mode state (kernels in hier.cu)
+// ------------------------------------------------------------------------------------------------
+struct HierState;
+
+// ------------------------------------------------------------------------------------------------
+// the handle
+// ------------------------------------------------------------------------------------------------
+}  // namespace nc
+
+struct nc_handle {
+  int kind = 0, mode = 0, device = 0, world = 1, rank = 0;
+  int64_t N = 0, row_begin = 0, row_count = 0, rows_per_rank = 0;
+  int M = 0, K = 0, Kstar = 0, p = 0;
+  double eps = 0.0, precision = 1e-9;
+  cudaStream_t stream = nullptr;  // library's own stream (used when caller passes NULL to setup ops)
+
+  // tables on device
+  double* d_T = nullptr;   // p x K
+  double* d_P = nullptr;   // K x Kstar
+  double* d_I = nullptr;   // K
+  double* d_zhat = nullptr;  // Kstar x 3
+  double* d_shat = nullptr;  // p x 3
+  std::vector<double> h_P1;  // P . 1 (K), the physical right-hand side of every patch
+  std::vector<double> h_I;
+
+  // layout (internal order)
+  std::vector<int64_t> perm;      // perm[internal] = caller index
+  double* d_centers = nullptr;    // N x 3 (internal order)
+  double* d_frames = nullptr;     // N x 9, R_i column-major: [e1 | e2 | c]
+
+  // direct-mode geometry and work buffers
+  double* d_tx = nullptr;         // row_count*Kstar targets (SoA)
+  double* d_ty = nullptr;
+  double* d_tz = nullptr;
+  double* d_src4 = nullptr;       // (world*rows_per_rank) * p records (x, y, z, rho)
+  double* d_upart = nullptr;      // nseg x (row_count*Kstar) partial fields
+  int nseg = 1;
+
+  // GMRES workspace
+  double* d_V = nullptr;
+  int V_cap = 0;
+  double* d_red = nullptr;        // reduction scratch
+  int64_t red_cap = 0;
+  double* h_red = nullptr;        // pinned host mirror
+  double* d_b = nullptr;          // scratch rhs
+  double* d_hx = nullptr;         // host-API staging (x and y)
+  double* d_hy = nullptr;
+
+  // per-stage timing
+  bool time_stages = false;
+  cudaEvent_t ev[8] = {};
+  double ms_last[8] = {};
+  int64_t matvecs = 0;
+  double pairs_per_matvec = 0.0;
+  double device_bytes = 0.0;
+
+  nc::HierState* hier = nullptr;
+
+#if NC_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+};
+
+namespace nc {
+
+// ------------------------------------------------------------------------------------------------
+// kernels / launchers (geometry.cu, gemm.cu, direct.cu, blas.cu)
+// ------------------------------------------------------------------------------------------------
+// frames R_i (ABI rule) and global node sets
+void launch_frames(const double* centers, int64_t N, double* frames, cudaStream_t s);
+void launch_targets(const double* frames, int64_t row_begin, int64_t row_count, const double* zhat, int Kstar,
+                    double* tx, double* ty, double* tz, cudaStream_t s);
+void launch_sources(const double* frames, int64_t N, const double* shat, int p, double* src4, cudaStream_t s);
+
+// C[i, n] (+)= sum_k A[i, k] * Bt[n, k]   (fp64 DMMA m8n8k4)
+//   A: rows x kd, leading dim lda; if nparts > 1, A is the sum of nparts matrices spaced part_stride apart
+//   Bt: ncols x kd row-major
+//   C element (i, n) is stored at C[i * ldc + n * cstride]; if X != nullptr, C = X + A Bt^T with X (ldx)
+void launch_gemm_dmma(const double* A, int64_t lda, int nparts, int64_t part_stride, const double* Bt, int64_t rows,
+                      int ncols, int kd, double* C, int64_t ldc, int cstride, const double* X, int64_t ldx,
+                      cudaStream_t s);
+
+// direct pair sums: upart[seg][t] = sum over source patches j in segment seg, j != patch(t), of
+// sum_m G(target t, s_jm) rho_jm
+void launch_pairs_direct(int kind, const double* tx, const double* ty, const double* tz, int64_t n_tgt, int Kstar,
+                         int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
+                         cudaStream_t s);
+
+// BLAS-1 style helpers for GMRES (deterministic two-stage reductions)
+int64_t multidot_partials(int64_t n);
+void launch_multidot(const double* V, int64_t ldv, int nv, const double* w, int64_t n, double* part, double* out,
+                     cudaStream_t s);  // out[i] = V_i . w, i < nv
+void launch_gemv_sub(const double* V, int64_t ldv, int nv, const double* h, double* w, int64_t n,
+                     cudaStream_t s);  // w -= sum_i h_i V_i, h on device
+void launch_lincomb(const double* V, int64_t ldv, int nv, const double* y, double* x, int64_t n,
+                    cudaStream_t s);  // x = sum_i y_i V_i
+void launch_scale(double* dst, const double* src, const double* alpha_dev, int invert, int64_t n,
+                  cudaStream_t s);  // dst = src * (*alpha or 1/ *alpha)
+void launch_fill_rows(double* dst, const double* row_dev, int K, int64_t rows, cudaStream_t s);
+void launch_colsum(const double* X, int64_t rows, int K, double* part, double* out, cudaStream_t s);
+
+}  // namespace nc

@@ -1,0 +1,219 @@
+"""Thin ctypes binding of libnc (include/nc.h).  Argument marshalling only: every arithmetic step of
+the matvec, GMRES and read-out runs in libnc's CUDA kernels.  PyTorch supplies device memory and
+streams.  There is no CPU fallback: if libnc.so is missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnc.so")
+
+NC_OK, NC_EINVAL, NC_ESEP, NC_ENOMEM, NC_ECUDA, NC_ENCCL, NC_ESTATE, NC_ENOCONV, NC_EUNSUP = 0, -1, -2, -3, -4, -5, -6, -7, -8
+NC_INTERIOR, NC_EXTERIOR = 0, 1
+NC_DIRECT, NC_HIER = 0, 1
+_ERRNAMES = {-1: "NC_EINVAL", -2: "NC_ESEP", -3: "NC_ENOMEM", -4: "NC_ECUDA", -5: "NC_ENCCL", -6: "NC_ESTATE",
+             -7: "NC_ENOCONV", -8: "NC_EUNSUP"}
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+class NcError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class NcTables(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int32), ("K", ctypes.c_int32), ("Kstar", ctypes.c_int32), ("p", ctypes.c_int32),
+                ("zhat", _dp), ("P", _dp), ("shat", _dp), ("T", _dp), ("I", _dp)]
+
+
+class NcOpts(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("precision", ctypes.c_double), ("device", ctypes.c_int32),
+                ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+                ("check_separation", ctypes.c_int32)]
+
+
+class NcStats(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("row_begin", ctypes.c_int64), ("row_count", ctypes.c_int64),
+                ("K", ctypes.c_int32), ("Kstar", ctypes.c_int32), ("p", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("matvecs", ctypes.c_int64),
+                ("pairs_per_matvec", ctypes.c_double), ("gemm_flops_per_matvec", ctypes.c_double),
+                ("ms_last", ctypes.c_double * 8), ("tree_levels", ctypes.c_int32), ("tree_groups", ctypes.c_int64),
+                ("device_bytes", ctypes.c_double)]
+
+
+EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt", "nc_stats",
+           "nc_time_stages", "nc_tree_lists", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libnc.so (raises if it is missing: the product has no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libnc.so not built at {path}; run `python -m paper_1906_04209_b200.build`")
+    L = ctypes.CDLL(path)
+    vp = ctypes.c_void_p
+    L.nc_setup.argtypes = [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int64, _dp, ctypes.c_double,
+                           ctypes.POINTER(NcTables), ctypes.POINTER(NcOpts)]
+    L.nc_partition.argtypes = [vp, _i64p, _i64p, _i64p]
+    L.nc_matvec.argtypes = [vp, vp, vp, vp]
+    L.nc_matvec_host.argtypes = [vp, _dp, _dp]
+    L.nc_gmres.argtypes = [vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int), _dp, vp]
+    L.nc_flux_or_mfpt.argtypes = [vp, vp, _dp, _dp]
+    L.nc_stats.argtypes = [vp, ctypes.POINTER(NcStats)]
+    L.nc_time_stages.argtypes = [vp, ctypes.c_int]
+    L.nc_tree_lists.argtypes = [vp, _i64p, _i64p, _i64p, _i64p, _i64p]
+    L.nc_nccl_unique_id.argtypes = [vp]
+    L.nc_destroy.argtypes = [vp]
+    L.nc_destroy.restype = None
+    L.nc_last_error.restype = ctypes.c_char_p
+    L.nc_version.restype = ctypes.c_char_p
+    for name in EXPORTS:
+        if name not in ("nc_destroy", "nc_last_error", "nc_version"):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc != NC_OK:
+        raise NcError(rc, load_library().nc_last_error().decode())
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().nc_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+def _ptr(t):
+    """Device pointer of a contiguous float64 CUDA tensor."""
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise TypeError("expected a contiguous float64 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Handle:
+    """One nc_setup'd layout.  ``tables`` is any object with M, zhat, P, shat, T, I numpy attributes."""
+
+    def __init__(self, kind, centers, eps, tables, mode=NC_DIRECT, precision=1e-9, device=0, world=1, rank=0,
+                 nccl_id: bytes | None = None, check_separation=True):
+        L = load_library()
+        self._L = L
+        c = np.ascontiguousarray(centers, dtype=np.float64)
+        self._keep = [np.ascontiguousarray(getattr(tables, k), dtype=np.float64) for k in ("zhat", "P", "shat", "T", "I")]
+        zhat, P, shat, T, I = self._keep
+        tab = NcTables(int(tables.M), T.shape[1], zhat.shape[0], shat.shape[0],
+                       zhat.ctypes.data_as(_dp), P.ctypes.data_as(_dp), shat.ctypes.data_as(_dp),
+                       T.ctypes.data_as(_dp), I.ctypes.data_as(_dp))
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        opts = NcOpts(int(mode), float(precision), int(device), int(world), int(rank),
+                      ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None, int(bool(check_separation)))
+        h = ctypes.c_void_p()
+        _check(L.nc_setup(ctypes.byref(h), int(kind), len(c), c.ctypes.data_as(_dp), float(eps), ctypes.byref(tab),
+                          ctypes.byref(opts)))
+        self._h = h
+        self.kind, self.N, self.eps, self.mode = int(kind), len(c), float(eps), int(mode)
+        self.K, self.Kstar, self.p = T.shape[1], zhat.shape[0], shat.shape[0]
+        rb, rc = ctypes.c_int64(), ctypes.c_int64()
+        perm = np.empty(self.N, dtype=np.int64)
+        _check(L.nc_partition(h, ctypes.byref(rb), ctypes.byref(rc), perm.ctypes.data_as(_i64p)))
+        self.row_begin, self.row_count, self.perm = rb.value, rc.value, perm
+
+    # ----------------------------------------------------------------------------------------------
+    def to_internal(self, x_caller: np.ndarray) -> np.ndarray:
+        """Caller-order (N, K) -> this rank's internal rows."""
+        x = np.asarray(x_caller).reshape(self.N, -1)[self.perm]
+        return np.ascontiguousarray(x[self.row_begin:self.row_begin + self.row_count])
+
+    def to_caller(self, y_rows_all: np.ndarray) -> np.ndarray:
+        """All ranks' internal rows (N, K) -> caller order."""
+        out = np.empty_like(y_rows_all)
+        out[self.perm] = y_rows_all
+        return out
+
+    def matvec(self, x, y=None, stream=None):
+        import torch
+        if y is None:
+            y = torch.empty_like(x)
+        _check(self._L.nc_matvec(self._h, _ptr(x), _ptr(y), _stream_ptr(stream)))
+        return y
+
+    def matvec_host(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        _check(self._L.nc_matvec_host(self._h, x.ctypes.data_as(_dp), y.ctypes.data_as(_dp)))
+        return y
+
+    def gmres(self, b=None, rtol=1e-10, max_iter=300, x=None, stream=None, allow_noconv=False):
+        import torch
+        if x is None:
+            x = torch.empty((self.row_count, self.K), dtype=torch.float64, device="cuda")
+        it = ctypes.c_int()
+        hist = np.zeros(max_iter + 1)
+        rc = self._L.nc_gmres(self._h, _ptr(b) if b is not None else None, float(rtol), int(max_iter), _ptr(x),
+                              ctypes.byref(it), hist.ctypes.data_as(_dp), _stream_ptr(stream))
+        if rc != NC_OK and not (allow_noconv and rc == NC_ENOCONV):
+            _check(rc)
+        return x, it.value, hist[: it.value + 1]
+
+    def flux_or_mfpt(self, x):
+        Is, v = ctypes.c_double(), ctypes.c_double()
+        _check(self._L.nc_flux_or_mfpt(self._h, _ptr(x), ctypes.byref(Is), ctypes.byref(v)))
+        return Is.value, v.value
+
+    def time_stages(self, enable=True):
+        _check(self._L.nc_time_stages(self._h, int(enable)))
+
+    def stats(self) -> dict:
+        s = NcStats()
+        _check(self._L.nc_stats(self._h, ctypes.byref(s)))
+        d = {k: getattr(s, k) for k, _ in NcStats._fields_}
+        d["ms_last"] = list(s.ms_last)
+        return d
+
+    def tree_lists(self):
+        L = self._L
+        ni, nn = ctypes.c_int64(), ctypes.c_int64()
+        _check(L.nc_tree_lists(self._h, ctypes.byref(ni), None, ctypes.byref(nn), None, None))
+        il = np.empty((ni.value, 3), dtype=np.int64)
+        nb = np.empty((nn.value, 3), dtype=np.int64)
+        st = self.stats()
+        bop = np.empty((st["tree_levels"] + 1, self.N), dtype=np.int64)
+        _check(L.nc_tree_lists(self._h, ctypes.byref(ni), il.ctypes.data_as(_i64p), ctypes.byref(nn),
+                               nb.ctypes.data_as(_i64p), bop.ctypes.data_as(_i64p)))
+        return il, nb, bop
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.nc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
