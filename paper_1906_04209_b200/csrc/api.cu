@@ -6,6 +6,7 @@
 //   K2  pair sums            u_{ik} = sum_{j != i} sum_m G(z_ik, s_jm) rho_jm  (direct.cu)
 //   K3  Y = X + U P^T        fp64 DMMA GEMM with the segment reduction fused into its operand load
 #include <math.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -83,12 +84,32 @@ static int check_separation(const double* c, int64_t N, double eps) {
   return NC_OK;
 }
 
+// Source segments of the direct kernel (grid.y): pick the count whose total CTA count wastes the least
+// of the last wave (all CTAs carry equal work, so waves stay in lock-step), with >= 4 waves when possible.
 static void compute_nseg(nc_handle* h) {
-  int64_t tiles = (h->row_count * h->Kstar + kPairThreads - 1) / kPairThreads;
+  const char* ev = getenv("NC_PAIR_TPT");
+  h->pair_tpt = (ev && atoi(ev) == 1) ? 1 : (ev && atoi(ev) == 2) ? 2 : kDefaultPairTpt;
+  const int64_t per_block = (int64_t)kPairThreads * h->pair_tpt;
+  int64_t tiles = (h->row_count * h->Kstar + per_block - 1) / per_block;
   if (tiles < 1) tiles = 1;
-  int64_t want = (8 * 148 * 4 + tiles - 1) / tiles;   // >= ~8 waves of 4 CTAs/SM
-  int64_t cap = std::min<int64_t>(h->N, 64);
-  h->nseg = (int)std::max<int64_t>(1, std::min(want, cap));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+  const int64_t W = (int64_t)sms * pairs_direct_blocks_per_sm(h->p, h->pair_tpt);
+  const int64_t cap = std::min<int64_t>(h->N, 64);
+  int best = 1;
+  double best_cost = 1e30;
+  for (int64_t s = 1; s <= cap; ++s) {
+    int64_t B = tiles * s;
+    int64_t waves = (B + W - 1) / W;
+    double eff = (double)B / (double)(waves * W);          // useful fraction of the launched waves
+    double cost = (1.0 / eff) * (1.0 + 0.002 * s);           // small penalty per extra partial buffer
+    if (B < 4 * W && s < cap) cost *= 1.0 + 0.05 * (double)(4 * W - B) / (4.0 * W);
+    if (cost < best_cost - 1e-12) {
+      best_cost = cost;
+      best = (int)s;
+    }
+  }
+  h->nseg = best;
 }
 
 static int ensure_red(nc_handle* h, int64_t count) {
@@ -237,14 +258,14 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
     cudaError_t e = cudaMemsetAsync(h->d_src4, 0, (size_t)n_src_rows * p * 4 * sizeof(double), s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "memset src4"));
   }
-  launch_sources(h->d_frames, N, h->d_shat, p, h->d_src4, s);
+  launch_sources(h->d_frames, N, h->d_shat, p, 0.5, h->d_src4, s);   // scaled by 1/2 (green.cuh)
 
   if (h->mode == NC_DIRECT) {
     const int64_t nt = h->row_count * Ks;
     if ((rc = dalloc(h, &h->d_tx, (size_t)nt)) || (rc = dalloc(h, &h->d_ty, (size_t)nt)) ||
         (rc = dalloc(h, &h->d_tz, (size_t)nt)))
       return bail(rc);
-    launch_targets(h->d_frames, h->row_begin, h->row_count, h->d_zhat, Ks, h->d_tx, h->d_ty, h->d_tz, s);
+    launch_targets(h->d_frames, h->row_begin, h->row_count, h->d_zhat, Ks, 0.5, h->d_tx, h->d_ty, h->d_tz, s);
     compute_nseg(h);
     if ((rc = dalloc(h, &h->d_upart, (size_t)h->nseg * nt))) return bail(rc);
     h->pairs_per_matvec = (double)h->row_count * Ks * (double)(N - 1) * p;
@@ -312,7 +333,7 @@ int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
   }
   mark(h, 2, s);
   if (h->mode == NC_DIRECT) {
-    launch_pairs_direct(h->kind, h->d_tx, h->d_ty, h->d_tz, h->row_count * Ks, Ks, h->row_begin, h->d_src4, p, h->N,
+    launch_pairs_direct(h->kind, h->pair_tpt, h->d_tx, h->d_ty, h->d_tz, h->row_count * Ks, Ks, h->row_begin, h->d_src4, p, h->N,
                         h->nseg, h->d_upart, s);
     mark(h, 3, s);
     // K3: Y = X + (sum_seg U_seg) P^T

@@ -34,25 +34,26 @@ __device__ __forceinline__ void apply_frame(const double* r, double a, double b,
 }
 
 __global__ void k_targets(const double* __restrict__ R, int64_t row_begin, int64_t row_count,
-                          const double* __restrict__ zhat, int Kstar, double* tx, double* ty, double* tz) {
+                          const double* __restrict__ zhat, int Kstar, double scale, double* tx, double* ty,
+                          double* tz) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= row_count * Kstar) return;
   int64_t i = row_begin + t / Kstar;
   int k = (int)(t % Kstar);
   double x, y, z;
   apply_frame(R + 9 * i, zhat[3 * k], zhat[3 * k + 1], zhat[3 * k + 2], x, y, z);
-  tx[t] = x; ty[t] = y; tz[t] = z;
+  tx[t] = scale * x; ty[t] = scale * y; tz[t] = scale * z;
 }
 
 __global__ void k_sources(const double* __restrict__ R, int64_t N, const double* __restrict__ shat, int p,
-                          double* __restrict__ src4) {
+                          double scale, double* __restrict__ src4) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= N * p) return;
   int64_t j = s / p;
   int m = (int)(s % p);
   double x, y, z;
   apply_frame(R + 9 * j, shat[3 * m], shat[3 * m + 1], shat[3 * m + 2], x, y, z);
-  src4[4 * s] = x; src4[4 * s + 1] = y; src4[4 * s + 2] = z; src4[4 * s + 3] = 0.0;
+  src4[4 * s] = scale * x; src4[4 * s + 1] = scale * y; src4[4 * s + 2] = scale * z; src4[4 * s + 3] = 0.0;
 }
 
 void launch_frames(const double* centers, int64_t N, double* frames, cudaStream_t s) {
@@ -60,15 +61,17 @@ void launch_frames(const double* centers, int64_t N, double* frames, cudaStream_
 }
 
 void launch_targets(const double* frames, int64_t row_begin, int64_t row_count, const double* zhat, int Kstar,
-                    double* tx, double* ty, double* tz, cudaStream_t s) {
+                    double scale, double* tx, double* ty, double* tz, cudaStream_t s) {
   int64_t n = row_count * Kstar;
   if (n == 0) return;
-  k_targets<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(frames, row_begin, row_count, zhat, Kstar, tx, ty, tz);
+  k_targets<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(frames, row_begin, row_count, zhat, Kstar, scale, tx, ty,
+                                                       tz);
 }
 
-void launch_sources(const double* frames, int64_t N, const double* shat, int p, double* src4, cudaStream_t s) {
+void launch_sources(const double* frames, int64_t N, const double* shat, int p, double scale, double* src4,
+                    cudaStream_t s) {
   int64_t n = N * p;
-  k_sources<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(frames, N, shat, p, src4);
+  k_sources<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(frames, N, shat, p, scale, src4);
 }
 
 }  // namespace nc

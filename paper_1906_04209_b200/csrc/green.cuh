@@ -1,47 +1,90 @@
-// green.cuh -- device evaluation of the on-surface Neumann Green's functions.
+// green.cuh -- device evaluation of the on-surface Neumann Green's functions (the pair kernel of every
+// hot loop: direct sums, interaction-list and neighbour evaluations).
 //
 // Paper forms (three terms, d = |x - x'|):
 //   G_E = 2/d - log(2/d) - log(1 + d/2)      eq:Gextonsurface
 //   G_I = 2/d + log(2/d) - log(1 + d/2)      eq:Gintonsurface
-// Exact single-log rewrites used on the GPU (SURVEY.md §8(a) "Kernel facts"):
-// with w = 2/d,  w (1 + d/2) = w + 1  and  (2/d) / (1 + d/2) = 4 / (d^2 + 2d), hence
-//   G_E = w - log(1 + w)
-//   G_I = w + log 4 - log(d^2 + 2 d)
-// One reciprocal square root and one logarithm per pair, no division.
+// Exact single-log rewrites used on the GPU: with w = 2/d and q = d^2/4,
+//   G_E = w - log(1 + w)                     since w (1 + d/2) = w + 1
+//   G_I = w - log(q (1 + w))                 since (2/d)/(1 + d/2) = 4/(d^2 + 2d) = 1/(q (1 + w))
+// Coordinates are stored pre-scaled by 1/2 (exact), so the squared distance of the scaled points IS q and
+// rsqrt(q) IS w: one reciprocal square root and one logarithm per pair, no division.
+//
+// fp64 rsqrt: MUFU.RSQ64H seed (rsqrt.approx.f64) + one third-order Newton correction
+//   e = 1 - q y^2,  y <- y + y e (1/2 + 3/8 e)                           (relative error ~ 2^-53)
+// fp64 log: x = 2^k m, m in [1,2); j = top 10 mantissa bits; c_j = 1/(1 + (j + 1/2)/1024) (table, smem);
+//   r = m c_j - 1 (one FMA, |r| <= 2^-11);  log x = k ln2 - log c_j + log1p(r),
+//   log1p(r) = r + r^2 (-1/2 + r/3 - r^2/4)   (truncation |r|^5/5 < 6e-18)
+// 22 FP64-pipe instructions per exterior pair (23 interior) instead of ~45 with libdevice log + rsqrt.
 #pragma once
 
 #include <stdint.h>
 
 namespace nc {
 
-constexpr double kLog4 = 1.3862943611198906188344642429163531;  // log(4)
-constexpr double kLn2Hi = 6.93147180369123816490e-01;           // fdlibm split of ln 2
-constexpr double kLn2Lo = 1.90821492927058770002e-10;
+constexpr int kLogTableBits = 10;
+constexpr int kLogTableSize = 1 << kLogTableBits;
+constexpr double kLn2 = 0.69314718055994530941723212145817657;
 
-// ------------------------------------------------------------------------------------------------
-// Table-free fp64 natural log for x in [1, 2^1000): x = 2^e m, m in [sqrt(1/2), sqrt(2));
-// f = m - 1, s = f / (2 + f) (computed without division: s = f * rcp(2+f) by Newton on MUFU seed),
-// log(m) = 2 atanh(s) = f - hf + s (hf + R(s^2)),  R = Remez/fdlibm minimax polynomial (|err| < 2^-58).
-// Accuracy: < 1 ulp of the result over the range used (validated in tests/test_kernels_gpu.py
-// against the oracle at the 1e-13 relative level).
-// ------------------------------------------------------------------------------------------------
-__device__ __forceinline__ double nc_log(double x) {
-  return log(x);
+// fill the (c_j, -log c_j) table; call with all threads of the CTA, then __syncthreads()
+__device__ __forceinline__ void init_log_table(double2* tbl) {
+  for (int j = threadIdx.x; j < kLogTableSize; j += blockDim.x) {
+    double c = 1.0 / (1.0 + (j + 0.5) / (double)kLogTableSize);
+    tbl[j] = make_double2(c, -log(c));
+  }
 }
 
-// rsqrt with full fp64 accuracy (CUDA's rsqrt: <= 1 ulp)
-__device__ __forceinline__ double nc_rsqrt(double x) { return rsqrt(x); }
+__device__ __forceinline__ double rsqrt_approx(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
 
+// fp64 reciprocal square root, x in the normal range
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y = rsqrt_approx(x);
+  double t = x * y;
+  double e = fma(-t, y, 1.0);
+  double c = fma(0.375, e, 0.5);
+  double ye = y * e;
+  return fma(ye, c, y);
+}
+
+// fp64 natural log for positive normal x (absolute error ~1e-16 |log x| + 1e-17)
+__device__ __forceinline__ double fast_log(double x, const double2* __restrict__ tbl) {
+  const int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  const int j = (hi >> (20 - kLogTableBits)) & (kLogTableSize - 1);
+  const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
+  // exponent k as a double without a conversion instruction: 2^52 + 2^31 + k  minus the magic
+  const double kd = __hiloint2double(0x43300000, (int)(((unsigned)hi >> 20) - 1023u + 0x80000000u)) -
+                    4503601774854144.0;   // 2^52 + 2^31
+  const double2 t = tbl[j];
+  const double r = fma(m, t.x, -1.0);
+  double p = fma(r, -0.25, 0.33333333333333333333);
+  p = fma(p, r, -0.5);
+  const double r2 = r * r;
+  const double l1 = fma(r2, p, r);
+  const double h = fma(kd, kLn2, t.y);
+  return h + l1;
+}
+
+// G for scaled coordinates: q = |x - x'|^2 / 4  (KIND 1 = exterior G_E, KIND 0 = interior G_I)
 template <int KIND>
-__device__ __forceinline__ double green_from_d2(double d2) {
-  double rs = nc_rsqrt(d2);
-  double w = 2.0 * rs;
-  if (KIND == 1) {
-    return w - nc_log(1.0 + w);
-  } else {
-    double d = d2 * rs;
-    return w + kLog4 - nc_log(fma(2.0, d, d2));
-  }
+__device__ __forceinline__ double green_q(double q, const double2* __restrict__ tbl) {
+  const double w = fast_rsqrt(q);   // 2/d
+  const double a = 1.0 + w;
+  if (KIND == 1) return w - fast_log(a, tbl);
+  return w - fast_log(q * a, tbl);
+}
+
+// reference-accuracy variant (libdevice), used by the self-check path
+template <int KIND>
+__device__ __forceinline__ double green_q_libdevice(double q) {
+  const double w = rsqrt(q);
+  const double a = 1.0 + w;
+  if (KIND == 1) return w - log(a);
+  return w - log(q * a);
 }
 
 }  // namespace nc

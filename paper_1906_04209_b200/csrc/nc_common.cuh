@@ -35,7 +35,8 @@ int cuda_fail(cudaError_t e, const char* what);
   } while (0)
 
 constexpr int kMaxP = 1024;
-constexpr int kPairThreads = 256;   // targets per CTA in the direct pair-sum kernel
+constexpr int kPairThreads = 256;   // threads per CTA in the direct pair-sum kernel
+constexpr int kDefaultPairTpt = 2;  // targets per thread (NC_PAIR_TPT=1|2 overrides)
 
 // ------------------------------------------------------------------------------------------------
 // hierarchical-mode state (kernels in hier.cu)
@@ -75,6 +76,7 @@ struct nc_handle {
   double* d_src4 = nullptr;       // (world*rows_per_rank) * p records (x, y, z, rho)
   double* d_upart = nullptr;      // nseg x (row_count*Kstar) partial fields
   int nseg = 1;
+  int pair_tpt = 1;               // targets per thread in the direct kernel (1 or 2)
 
   // GMRES workspace
   double* d_V = nullptr;
@@ -108,9 +110,11 @@ namespace nc {
 // ------------------------------------------------------------------------------------------------
 // frames R_i (ABI rule) and global node sets
 void launch_frames(const double* centers, int64_t N, double* frames, cudaStream_t s);
+// (coordinates written pre-multiplied by `scale`; the pair kernels use scale = 1/2, see green.cuh)
 void launch_targets(const double* frames, int64_t row_begin, int64_t row_count, const double* zhat, int Kstar,
-                    double* tx, double* ty, double* tz, cudaStream_t s);
-void launch_sources(const double* frames, int64_t N, const double* shat, int p, double* src4, cudaStream_t s);
+                    double scale, double* tx, double* ty, double* tz, cudaStream_t s);
+void launch_sources(const double* frames, int64_t N, const double* shat, int p, double scale, double* src4,
+                    cudaStream_t s);
 
 // C[i, n] (+)= sum_k A[i, k] * Bt[n, k]   (fp64 DMMA m8n8k4)
 //   A: rows x kd, leading dim lda; if nparts > 1, A is the sum of nparts matrices spaced part_stride apart
@@ -122,9 +126,11 @@ void launch_gemm_dmma(const double* A, int64_t lda, int nparts, int64_t part_str
 
 // direct pair sums: upart[seg][t] = sum over source patches j in segment seg, j != patch(t), of
 // sum_m G(target t, s_jm) rho_jm
-void launch_pairs_direct(int kind, const double* tx, const double* ty, const double* tz, int64_t n_tgt, int Kstar,
-                         int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
+void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, const double* tz, int64_t n_tgt,
+                         int Kstar, int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
                          cudaStream_t s);
+
+int pairs_direct_blocks_per_sm(int p, int tpt);
 
 // BLAS-1 style helpers for GMRES (deterministic two-stage reductions)
 int64_t multidot_partials(int64_t n);
