@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--mode", default="direct", choices=["direct", "hier"])
     ap.add_argument("--impl", default="nc", choices=["nc", "reference"])
-    ap.add_argument("--tables", default="synthetic", choices=["synthetic", "physical"])
+    ap.add_argument("--tables", default="physical", choices=["synthetic", "physical"])
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="target patches in the oracle sample (0 = auto)")

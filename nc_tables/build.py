@@ -1,0 +1,74 @@
+"""Step-1 precomputation: build the patch-operator tables for one (kind, eps).
+
+    python -m nc_tables.build --kind 0 --eps 0.003 --out tables/data/C5.npz
+    python -m nc_tables.build --configs          # the five BASELINE.json configs
+
+CPU, untimed, N-independent; its output file is the `nc_tables` input of nc_setup (include/nc.h) and of the
+oracle.  Neither the oracle nor the CUDA path imports this package.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+from . import zernike
+from .onepatch import fine_grid, solve_onepatch
+from .skeleton import interp_decomp, outgoing_error, training_grid
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20, n_theta: int = 64,
+                 id_tol: float = 1e-11, zn_r: int | None = None, zn_theta: int | None = None, verbose=False):
+    t0 = time.time()
+    op = solve_onepatch(kind, eps, M, npan, k, n_theta)
+    t1 = time.time()
+    fine, wf, B = fine_grid(op)
+    train = training_grid(eps)
+    J, Pi = interp_decomp(kind, train, fine, id_tol)
+    T = Pi @ (wf[:, None] * B)
+    shat = fine[J]
+    t2 = time.time()
+    r, th, P = zernike.transform(M, zn_r, zn_theta)
+    zhat = zernike.patch_xyz(eps, r, th)
+    I = wf @ B
+    err = outgoing_error(kind, fine, wf, B, shat, T, eps)
+    meta = dict(kind=kind, eps=eps, M=M, npan=npan, k=k, n_theta=n_theta, id_tol=id_tol, p=len(J), n_f=len(wf),
+                n_train=len(train), outgoing_rel_err=err, t_onepatch_s=t1 - t0, t_id_s=t2 - t1)
+    if verbose:
+        print(meta, file=sys.stderr)
+    return dict(kind=kind, eps=eps, M=M, zhat=zhat, P=P, shat=shat, T=T, I=I, meta=meta)
+
+
+def save(d, path):
+    np.savez(path, version=1, kind=d["kind"], eps=d["eps"], M=d["M"], zhat=d["zhat"], P=d["P"], shat=d["shat"],
+             T=d["T"], I=d["I"], meta=np.array(repr(d["meta"])))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kind", type=int, default=0)
+    ap.add_argument("--eps", type=float, default=0.1)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--configs", action="store_true")
+    ap.add_argument("--id-tol", type=float, default=1e-11)
+    a = ap.parse_args()
+    outdir = os.path.join(ROOT, "tables", "data")
+    os.makedirs(outdir, exist_ok=True)
+    if a.configs:
+        sys.path.insert(0, ROOT)
+        from nc_inputs import CONFIGS
+        for name, cfg in CONFIGS.items():
+            d = build_tables(cfg.kind, cfg.eps, id_tol=a.id_tol, verbose=True)
+            save(d, os.path.join(outdir, f"{name}.npz"))
+        return
+    d = build_tables(a.kind, a.eps, id_tol=a.id_tol, verbose=True)
+    save(d, a.out or os.path.join(outdir, f"k{a.kind}_eps{a.eps:g}.npz"))
+
+
+if __name__ == "__main__":
+    main()

@@ -127,3 +127,45 @@ def test_errors():
     bad.M = 4
     with pytest.raises(nc.NcError, match="NC_EINVAL"):
         nc.Handle(0, np.array([[0, 0, 1.0]]), 0.1, bad)
+
+
+def _phys(name):
+    import os
+    from nc_inputs.tables import load_tables
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tables", "data", f"{name}.npz")
+    return load_tables(path)
+
+
+def test_solve_physical_tables_C1_mu_matches_oracle():
+    # BASELINE north_star: solved mu within 1e-7 relative of the oracle on the same seeded inputs
+    cfg = CONFIGS["C1"]
+    c = cfg.centers()
+    tab = _phys("C1")
+    ref = O.solve(cfg.kind, c, tab, tol=1e-10)
+    h = _nc().Handle(cfg.kind, c, cfg.eps, tab)
+    x, it, hist = h.gmres(rtol=1e-10, max_iter=100)
+    Is, mu = h.flux_or_mfpt(x)
+    assert abs(it - ref["iters"]) <= 1
+    assert abs(mu - ref["value"]) <= 1e-7 * abs(ref["value"])
+    assert abs(Is - ref["I_sigma"]) <= 1e-7 * abs(ref["I_sigma"])
+    assert rel(h.to_caller(x.cpu().numpy()), ref["x"]) < 1e-8
+
+
+def test_solve_physical_tables_C2_residual_via_oracle_rows():
+    # C2 (N = 1000, exterior): the GPU solution's residual measured by the oracle on sampled rows
+    cfg = CONFIGS["C2"]
+    c = cfg.centers()
+    tab = _phys("C2")
+    h = _nc().Handle(cfg.kind, c, cfg.eps, tab)
+    x, it, hist = h.gmres(rtol=1e-10, max_iter=200)
+    Is, J = h.flux_or_mfpt(x)
+    assert hist[-1] <= 1e-10 and -4 * np.pi < J < 0
+    xg = h.to_caller(x.cpu().numpy())
+    rows = np.random.default_rng(1).choice(cfg.N, 6, replace=False)
+    b = O.rhs(tab, cfg.N)
+    r = O.matvec(cfg.kind, c, tab, xg, rows=rows) - b[rows]
+    assert np.linalg.norm(r) / np.linalg.norm(b[rows]) < 1e-9
+    # matvec parity with physical tables at full size (sampled rows)
+    xr = random_coeffs(cfg.N, tab.K, 77)
+    y = gpu_matvec(h, xr)
+    assert rel(y[rows], O.matvec(cfg.kind, c, tab, xr, rows=rows)) <= MATVEC_TOL
