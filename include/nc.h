@@ -89,6 +89,11 @@ typedef struct nc_stats_t {
                                 /*   [4] hier step 2+3  [5] hier step 4  [6] total  [7] reserved   */
   int32_t tree_levels;          /* NC_HIER: depth L of the sphere quadtree                         */
   int64_t tree_groups;          /* NC_HIER: number of non-empty boxes over all levels              */
+  double hier_grid_pairs;       /* NC_HIER: pair evaluations on incoming grids per matvec (steps 2-3) */
+  double hier_near_pairs;       /* NC_HIER: pair evaluations at Zernike nodes (near lists)          */
+  double hier_interp_terms;     /* NC_HIER: node x coefficient terms of the step-4 interpolation    */
+  int64_t hier_grid_points;     /* NC_HIER: incoming-grid points held by this rank                  */
+  int64_t hier_grid_units;      /* NC_HIER: step-2/3 work units (CTAs) per matvec                   */
   double device_bytes;          /* device memory held by the handle                                */
 } nc_stats_t;
 

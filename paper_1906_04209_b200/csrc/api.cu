@@ -16,6 +16,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "green.cuh"
 #include "hier.cuh"
 #include "nc_common.cuh"
 
@@ -204,6 +205,7 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   }
   cudaStream_t s = h->stream;
   const int K = h->K, Ks = h->Kstar, p = h->p;
+  if (!log_table_device()) return bail(fail(NC_ECUDA, "nc_setup: log table upload failed"));
 
   // tables
   int rc;
@@ -238,29 +240,25 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
     if (rc) return bail(rc);
   }
 
-  // partition: equal contiguous row ranges (all rows carry the same work in direct mode)
-  h->rows_per_rank = (N + h->world - 1) / h->world;
-  h->row_begin = std::min<int64_t>(N, (int64_t)h->rank * h->rows_per_rank);
-  h->row_count = std::min<int64_t>(h->rows_per_rank, N - h->row_begin);
-  if (h->mode == NC_HIER) {
-    rc = hier_partition(h);
-    if (rc) return bail(rc);
-  }
-
   if ((rc = dalloc(h, &h->d_centers, (size_t)N * 3)) || (rc = dalloc(h, &h->d_frames, (size_t)N * 9))) return bail(rc);
   UP(h->d_centers, cs.data(), (size_t)N * 3);
   launch_frames(h->d_centers, N, h->d_frames, s);
 
-  // source records (x, y, z, rho) for all patches, padded to world * rows_per_rank
-  const int64_t n_src_rows = (int64_t)h->world * h->rows_per_rank;
-  if ((rc = dalloc(h, &h->d_src4, (size_t)n_src_rows * p * 4))) return bail(rc);
-  {
-    cudaError_t e = cudaMemsetAsync(h->d_src4, 0, (size_t)n_src_rows * p * 4 * sizeof(double), s);
-    if (e != cudaSuccess) return bail(cuda_fail(e, "memset src4"));
-  }
-  launch_sources(h->d_frames, N, h->d_shat, p, 0.5, h->d_src4, s);   // scaled by 1/2 (green.cuh)
+  // source records (x, y, z, rho) for all N patches, coordinates scaled by 1/2 (green.cuh)
+  if ((rc = dalloc(h, &h->d_src4, (size_t)N * p * 4))) return bail(rc);
+  launch_sources(h->d_frames, N, h->d_shat, p, 0.5, h->d_src4, s);
 
   if (h->mode == NC_DIRECT) {
+    // partition: equal contiguous row ranges (every row carries the same work in direct mode)
+    const int64_t rpr = (N + h->world - 1) / h->world;
+    h->rank_begin.assign(h->world, 0);
+    h->rank_count.assign(h->world, 0);
+    for (int r = 0; r < h->world; ++r) {
+      h->rank_begin[r] = std::min<int64_t>(N, (int64_t)r * rpr);
+      h->rank_count[r] = std::min<int64_t>(rpr, N - h->rank_begin[r]);
+    }
+    h->row_begin = h->rank_begin[h->rank];
+    h->row_count = h->rank_count[h->rank];
     const int64_t nt = h->row_count * Ks;
     if ((rc = dalloc(h, &h->d_tx, (size_t)nt)) || (rc = dalloc(h, &h->d_ty, (size_t)nt)) ||
         (rc = dalloc(h, &h->d_tz, (size_t)nt)))
@@ -270,7 +268,7 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
     if ((rc = dalloc(h, &h->d_upart, (size_t)h->nseg * nt))) return bail(rc);
     h->pairs_per_matvec = (double)h->row_count * Ks * (double)(N - 1) * p;
   } else {
-    rc = hier_setup(h, s);
+    rc = hier_setup(h, cs, s);       // tree, lists, grids, work-weighted partition
     if (rc) return bail(rc);
   }
   if ((rc = ensure_red(h, 4096))) return bail(rc);
@@ -326,9 +324,16 @@ int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
   mark(h, 1, s);
   if (h->world > 1) {
 #if NC_WITH_NCCL
-    const size_t cnt = (size_t)h->rows_per_rank * p * 4;
-    ncclResult_t r = ncclAllGather(h->d_src4 + (size_t)h->rank * cnt, h->d_src4, cnt, ncclDouble, h->comm, s);
-    if (r != ncclSuccess) return fail(NC_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    // all-gather-v of the source records: one in-place broadcast per rank's row range
+    ncclResult_t r = ncclGroupStart();
+    for (int q = 0; q < h->world && r == ncclSuccess; ++q) {
+      if (h->rank_count[q] == 0) continue;
+      double* seg = h->d_src4 + (size_t)h->rank_begin[q] * p * 4;
+      r = ncclBroadcast(seg, seg, (size_t)h->rank_count[q] * p * 4, ncclDouble, q, h->comm, s);
+    }
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+      return fail(NC_ENCCL, std::string("all-gather (broadcasts): ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
 #endif
   }
   mark(h, 2, s);
@@ -352,6 +357,9 @@ int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
     if (h->mode == NC_DIRECT) {
       cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); h->ms_last[2] = ms;
       cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]); h->ms_last[3] = ms;
+    } else {
+      cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); h->ms_last[4] = ms;   // steps 2-3 (grids)
+      cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]); h->ms_last[5] = ms;   // transform, near, step 4, step 5
     }
     cudaEventElapsedTime(&ms, h->ev[0], h->ev[4]); h->ms_last[6] = ms;
   }

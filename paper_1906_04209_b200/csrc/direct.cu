@@ -1,16 +1,14 @@
-// direct.cu -- the tiled direct multiple-scattering sum (a2 of SURVEY.md §8(a)):
+// direct.cu -- pair-sum kernels built on pairs.cuh:
 //
-//   u_{ik} = sum_{j != i} sum_{m=1..p} G(z_{ik}, s_{jm}) rho_{jm}        (eq:mssums with eq:outgoingcompressed)
+//  k_pairs_direct  (a2, direct mode)   u_{ik} = sum_{j != i} sum_m G(z_ik, s_jm) rho_jm over a segment of patches
+//  k_pairs_grid    (a3/a4, hier mode)  grid_g(x) += sum_{j in slice} sum_m G(x, s_jm) rho_jm  (one work unit:
+//                                      <= 256 points of one incoming grid x one slice of its source-patch list)
+//  k_pairs_near    (a4, hier mode)     u_{ik} += sum_{j in near(i)} sum_m G(z_ik, s_jm) rho_jm
 //
-// Design (B200, fp64-pipe bound): TPT (1 or 2) target nodes z_{ik} per thread; a CTA holds 256*TPT targets and walks
-// a segment of source patches, staging whole source patches (p records of (x, y, z, rho), 32 B each,
-// coalesced 16 B loads) in shared memory; every thread reads each record as a broadcast and does one
-// rsqrt + one log + ~10 DFMA per pair.  Self-exclusion (j != i) is a per-thread patch skip, so tiles may
-// straddle patches for any Kstar.  The source range is split into `nseg` segments (grid.y) so the grid
-// has many waves on 148 SMs; the segments' partial fields are summed deterministically inside the
-// step-5 GEMM's operand load (gemm.cu).
-#include "green.cuh"
-#include "nc_common.cuh"
+// Direct mode: one CTA per (target tile of 256*TPT nodes, source segment); the source range is split into `nseg`
+// segments (grid.y) chosen so the CTA count fills the last wave (api.cu); segment partials are summed in the
+// step-5 GEMM's operand load (gemm.cu), deterministic.
+#include "pairs.cuh"
 
 namespace nc {
 
@@ -20,65 +18,26 @@ __global__ void __launch_bounds__(kPairThreads) k_pairs_direct(const double* __r
                                                                 const double* __restrict__ tz, int64_t n_tgt,
                                                                 int Kstar, int64_t tgt_patch0,
                                                                 const double* __restrict__ src4, int p, int64_t N,
-                                                                int nseg, int chp, double* __restrict__ upart) {
+                                                                int nseg, int chp, double* __restrict__ upart,
+                                                                const double2* __restrict__ logsrc) {
   extern __shared__ double4 sm[];
   __shared__ double2 logtab[kLogTableSize];
-  init_log_table(logtab);
-  // TPT targets per thread (t0 + u * kPairThreads): independent accumulation chains sharing each source load
+  __shared__ int64_t pid[kStagePatchesMax];
+  init_log_table(logtab, logsrc);
   double x[TPT], y[TPT], z[TPT], acc[TPT];
-  int64_t patch[TPT];
+  int64_t excl[TPT];
   const int64_t t0 = (int64_t)blockIdx.x * kPairThreads * TPT + threadIdx.x;
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
     const int64_t t = min(t0 + u * kPairThreads, n_tgt - 1);
     x[u] = tx[t]; y[u] = ty[t]; z[u] = tz[t];
-    patch[u] = tgt_patch0 + t / Kstar;
+    excl[u] = tgt_patch0 + t / Kstar;         // j != i
     acc[u] = 0.0;
   }
   const int seg = blockIdx.y;
   const int64_t j0 = (N * seg) / nseg, j1 = (N * (seg + 1)) / nseg;
-  const double4* __restrict__ s4 = reinterpret_cast<const double4*>(src4);
-  for (int64_t jc = j0; jc < j1; jc += chp) {
-    const int nch = (int)min((int64_t)chp, j1 - jc);
-    const int nrec = nch * p;
-    __syncthreads();
-    for (int r = threadIdx.x; r < nrec; r += kPairThreads) sm[r] = s4[jc * p + r];
-    __syncthreads();
-    for (int qq = 0; qq < nch; ++qq) {
-      const int64_t j = jc + qq;
-      const double4* __restrict__ sp = sm + qq * p;
-      bool all = true, none = true;
-#pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        all = all && (patch[u] != j);
-        none = none && (patch[u] == j);
-      }
-      if (none) continue;                               // j != i for every target of this thread
-      if (all) {
-#pragma unroll 2
-        for (int m = 0; m < p; ++m) {
-          const double4 s = sp[m];
-#pragma unroll
-          for (int u = 0; u < TPT; ++u) {
-            const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
-            const double q = fma(dz, dz, fma(dy, dy, dx * dx));   // |z - s|^2 / 4 (scaled coordinates)
-            acc[u] = fma(s.w, green_q<KIND>(q, logtab), acc[u]);
-          }
-        }
-      } else {                                          // some (not all) targets are on patch j: skip those
-#pragma unroll
-        for (int u = 0; u < TPT; ++u) {
-          if (patch[u] == j) continue;
-          for (int m = 0; m < p; ++m) {
-            const double4 s = sp[m];
-            const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
-            const double q = fma(dz, dz, fma(dy, dy, dx * dx));
-            acc[u] = fma(s.w, green_q<KIND>(q, logtab), acc[u]);
-          }
-        }
-      }
-    }
-  }
+  accumulate_list<KIND, TPT>(x, y, z, excl, acc, j1 - j0, [=] __device__(int64_t k) { return j0 + k; },
+                             reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, true);
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
     const int64_t t = t0 + u * kPairThreads;
@@ -86,11 +45,9 @@ __global__ void __launch_bounds__(kPairThreads) k_pairs_direct(const double* __r
   }
 }
 
-static int chp_for(int p) { return max(1, 512 / p); }   // source patches per smem stage (<= 16 KB unless p > 512)
-
 int pairs_direct_blocks_per_sm(int p, int tpt) {
   int nb = 0;
-  size_t smem = (size_t)chp_for(p) * p * sizeof(double4);
+  size_t smem = (size_t)stage_patches(p) * p * sizeof(double4);
   if (tpt == 2)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pairs_direct<1, 2>, kPairThreads, smem);
   else
@@ -102,18 +59,130 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
                          int Kstar, int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
                          cudaStream_t s) {
   if (n_tgt <= 0) return;
-  const int chp = chp_for(p);
+  const int chp = stage_patches(p);
   const size_t smem = (size_t)chp * p * sizeof(double4);
   const int64_t per_block = (int64_t)kPairThreads * tpt;
   dim3 grid((unsigned)((n_tgt + per_block - 1) / per_block), (unsigned)nseg);
 #define NC_LAUNCH(KD, TP) \
-  k_pairs_direct<KD, TP><<<grid, kPairThreads, smem, s>>>(tx, ty, tz, n_tgt, Kstar, tgt_patch0, src4, p, N, nseg, chp, upart)
+  k_pairs_direct<KD, TP><<<grid, kPairThreads, smem, s>>>(tx, ty, tz, n_tgt, Kstar, tgt_patch0, src4, p, N, nseg, chp, upart, \
+                                                          log_table_device())
   if (kind == NC_EXTERIOR) {
     if (tpt == 2) NC_LAUNCH(1, 2); else NC_LAUNCH(1, 1);
   } else {
     if (tpt == 2) NC_LAUNCH(0, 2); else NC_LAUNCH(0, 1);
   }
 #undef NC_LAUNCH
+}
+
+// ------------------------------------------------------------------------------------------------
+// hierarchical mode: interaction-list / leaf-neighbour sources on incoming grids
+// ------------------------------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(kGridThreads) k_pairs_grid(const GridUnit* __restrict__ units,
+                                                              const double* __restrict__ gx,
+                                                              const double* __restrict__ gy,
+                                                              const double* __restrict__ gz,
+                                                              const int32_t* __restrict__ srclist,
+                                                              const double* __restrict__ src4, int p, int chp,
+                                                              double* __restrict__ part,
+                                                              const double2* __restrict__ logsrc) {
+  extern __shared__ double4 sm[];
+  __shared__ double2 logtab[kLogTableSize];
+  __shared__ int64_t pid[kStagePatchesMax];
+  init_log_table(logtab, logsrc);
+  const GridUnit U = units[blockIdx.x];
+  constexpr int TPT = kGridUnitPoints / kGridThreads;
+  double x[TPT], y[TPT], z[TPT], acc[TPT];
+  int64_t excl[TPT];
+  bool any = false;
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) {
+    const int l = threadIdx.x + u * kGridThreads;
+    const int64_t g = U.pt0 + min(l, U.npt - 1);
+    x[u] = gx[g]; y[u] = gy[g]; z[u] = gz[g];
+    excl[u] = -1;
+    acc[u] = 0.0;
+    any = any || (l < U.npt);
+  }
+  const int32_t* __restrict__ lst = srclist + U.src0;
+  accumulate_list<KIND, TPT>(x, y, z, excl, acc, U.nsrc, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
+                             reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, any);
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) {
+    const int l = threadIdx.x + u * kGridThreads;
+    if (l < U.npt) part[(int64_t)blockIdx.x * kGridUnitPoints + l] = acc[u];
+  }
+}
+
+void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
+                       const double* gz, const int32_t* srclist, const double* src4, int p, double* part,
+                       cudaStream_t s) {
+  if (nunits <= 0) return;
+  const int chp = stage_patches(p);
+  const size_t smem = (size_t)chp * p * sizeof(double4);
+  if (kind == NC_EXTERIOR)
+    k_pairs_grid<1><<<(unsigned)nunits, kGridThreads, smem, s>>>(units, gx, gy, gz, srclist, src4, p, chp, part,
+                                                                 log_table_device());
+  else
+    k_pairs_grid<0><<<(unsigned)nunits, kGridThreads, smem, s>>>(units, gx, gy, gz, srclist, src4, p, chp, part,
+                                                                 log_table_device());
+}
+
+// ------------------------------------------------------------------------------------------------
+// hierarchical mode: near-list sources evaluated directly at the target patch's Zernike nodes
+// ------------------------------------------------------------------------------------------------
+template <int KIND, int TPT>
+__global__ void __launch_bounds__(kPairThreads) k_pairs_near(const double* __restrict__ tx,
+                                                              const double* __restrict__ ty,
+                                                              const double* __restrict__ tz, int Kstar,
+                                                              const int32_t* __restrict__ work,  // local patch ids
+                                                              const int64_t* __restrict__ near_off,
+                                                              const int32_t* __restrict__ near,
+                                                              const double* __restrict__ src4, int p, int chp,
+                                                              double* __restrict__ udir,
+                                                              const double2* __restrict__ logsrc) {
+  extern __shared__ double4 sm[];
+  __shared__ double2 logtab[kLogTableSize];
+  __shared__ int64_t pid[kStagePatchesMax];
+  init_log_table(logtab, logsrc);
+  const int tiles = (Kstar + kPairThreads * TPT - 1) / (kPairThreads * TPT);
+  const int64_t i = work[blockIdx.x / tiles];           // local target patch
+  const int tile = blockIdx.x % tiles;
+  double x[TPT], y[TPT], z[TPT], acc[TPT];
+  int64_t excl[TPT];
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) {
+    const int k = min(tile * kPairThreads * TPT + (int)threadIdx.x + u * kPairThreads, Kstar - 1);
+    const int64_t t = i * Kstar + k;
+    x[u] = tx[t]; y[u] = ty[t]; z[u] = tz[t];
+    excl[u] = -1;
+    acc[u] = 0.0;
+  }
+  const int64_t o0 = near_off[i], o1 = near_off[i + 1];
+  const int32_t* __restrict__ lst = near + o0;
+  accumulate_list<KIND, TPT>(x, y, z, excl, acc, o1 - o0, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
+                             reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, true);
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) {
+    const int k = tile * kPairThreads * TPT + (int)threadIdx.x + u * kPairThreads;
+    if (k < Kstar) udir[i * Kstar + k] = acc[u];
+  }
+}
+
+void launch_pairs_near(int kind, const double* tx, const double* ty, const double* tz, int Kstar, const int32_t* work,
+                       int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
+                       double* udir, cudaStream_t s) {
+  if (nwork <= 0) return;
+  const int chp = stage_patches(p);
+  const size_t smem = (size_t)chp * p * sizeof(double4);
+  const int tiles = (Kstar + kPairThreads * 2 - 1) / (kPairThreads * 2);
+  const unsigned nb = (unsigned)(nwork * tiles);
+  if (kind == NC_EXTERIOR)
+    k_pairs_near<1, 2><<<nb, kPairThreads, smem, s>>>(tx, ty, tz, Kstar, work, near_off, near, src4, p, chp, udir,
+                                                      log_table_device());
+  else
+    k_pairs_near<0, 2><<<nb, kPairThreads, smem, s>>>(tx, ty, tz, Kstar, work, near_off, near, src4, p, chp, udir,
+                                                      log_table_device());
 }
 
 }  // namespace nc

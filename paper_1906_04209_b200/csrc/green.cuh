@@ -26,12 +26,12 @@ constexpr int kLogTableBits = 10;
 constexpr int kLogTableSize = 1 << kLogTableBits;
 constexpr double kLn2 = 0.69314718055994530941723212145817657;
 
-// fill the (c_j, -log c_j) table; call with all threads of the CTA, then __syncthreads()
-__device__ __forceinline__ void init_log_table(double2* tbl) {
-  for (int j = threadIdx.x; j < kLogTableSize; j += blockDim.x) {
-    double c = 1.0 / (1.0 + (j + 0.5) / (double)kLogTableSize);
-    tbl[j] = make_double2(c, -log(c));
-  }
+// (c_j, -log c_j) table: computed once on the host in long double (green_table.cu) and kept in global memory;
+// every CTA copies it to shared memory.  Call with all threads of the CTA, then __syncthreads().
+const double2* log_table_device();   // host: uploaded once per device; nullptr on failure
+
+__device__ __forceinline__ void init_log_table(double2* tbl, const double2* __restrict__ src) {
+  for (int j = threadIdx.x; j < kLogTableSize; j += blockDim.x) tbl[j] = src[j];
 }
 
 __device__ __forceinline__ double rsqrt_approx(double x) {

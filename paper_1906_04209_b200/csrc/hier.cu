@@ -1,23 +1,969 @@
-// hier.cu -- hierarchical mode (placeholder until the device tree lands).
+// hier.cu -- the hierarchical O(N log N) matvec (SURVEY.md §8(a) a0, a3-a5; §7.2-§8, :1176-1415).
+//
+// Setup (Step 2), on device:
+//   * keys: project each centre by the ray from the origin onto the cube [-1,1]^3; face by the
+//     largest |coordinate| (ties x > y > z), Morton-interleaved cell indices at kLmax levels -> 51-bit key;
+//   * sort (CUB radix sort) -> internal patch order; depth L = the first level at which all non-empty boxes hold one
+//     patch (adjacent-key separation levels, max-reduced) -- DESIGN.md reading R11 (uniform depth, pruned);
+//   * boxes per level by run-length of key prefixes (flags + CUB scan): every box is a contiguous patch range;
+//   * neighbours: the 8 cells around a box, folded across cube edges (7 at cube corners),
+//     looked up by binary search; interaction lists: children of the parent's neighbours (parent included) that are
+//     not neighbours; level 0 = the six faces under a virtual root (opposite faces interact);
+//   * bounding circles: Badoiu-Clarkson iterations for the smallest cap around member centres,
+//     radius padded by eps (reading R14).
+// Host bookkeeping: for every (group, source patch) pair of the interaction list (and leaf neighbours, step 3,
+// PAPER.md:1364-1375) decide incoming grid vs direct near-list evaluation (skeleton validity > 2 eps, PAPER.md:1057;
+// DESIGN.md reading R12, with a cost model), size each grid from its nearest grid source, and
+// build the work units.
+//
+// Matvec (Step 3): K1 (api.cu) -> k_pairs_grid (steps 2-3) -> k_reduce_chunks -> k_transform
+// (samples -> parity-restricted Chebyshev-Fourier coefficients) -> k_pairs_near -> k_interp
+// (step 4: evaluate every group's expansion at its members' Zernike nodes, summed over levels) -> K3 (api.cu).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <string>
+#include <vector>
+
 #include "hier.cuh"
 
 namespace nc {
+
+constexpr int kLmax = 24;
+constexpr int kSliceMax = 32;          // source patches per grid work unit
+constexpr double kBetaMin = 1.45;      // smallest source distance / circle radius served by a grid
+
+struct ChunkRec {
+  int64_t pt0;
+  int64_t u0;
+  int32_t npt;
+  int32_t nu;
+};
+
+struct HierState {
+  int L = 0;
+  int64_t ngroups = 0;
+  std::vector<int64_t> lvl_off;     // L+2
+  std::vector<int64_t> gkey;
+  std::vector<int32_t> gfirst, glast, glevel;
+  std::vector<int32_t> nbr;         // 8 per group
+  std::vector<int64_t> il_off;
+  std::vector<int32_t> il;
+  std::vector<double> gc, gR;       // circle centre (3/group), radius
+  std::vector<int32_t> pgroup;      // (L+1) x N
+  std::vector<int64_t> keys;        // sorted keys (internal order)
+  // grids
+  std::vector<int32_t> gnr, gna;
+  std::vector<int64_t> goff, coff;
+  int64_t Q = 0, C = 0;
+  int qmax = 0, cmax = 0;
+  std::vector<int32_t> grid_groups;
+  // device
+  int64_t* d_keys = nullptr;
+  double* d_gframe = nullptr;
+  double* d_gR = nullptr;
+  int32_t *d_gnr = nullptr, *d_gna = nullptr;
+  int64_t *d_goff = nullptr, *d_coff = nullptr;
+  int32_t* d_grid_groups = nullptr;
+  double *d_gx = nullptr, *d_gy = nullptr, *d_gz = nullptr, *d_gval = nullptr, *d_gcoef = nullptr;
+  GridUnit* d_units = nullptr;
+  int64_t nunits = 0;
+  int32_t* d_srclist = nullptr;
+  double* d_part = nullptr;
+  ChunkRec* d_chunks = nullptr;
+  int64_t nchunks = 0;
+  int32_t* d_work_near = nullptr;
+  int64_t nwork_near = 0;
+  int64_t* d_near_off = nullptr;
+  int32_t* d_near = nullptr;
+  int32_t* d_pgl = nullptr;         // (L+1) x row_count group ids of local patches
+  double *d_tx = nullptr, *d_ty = nullptr, *d_tz = nullptr;
+  double *d_udir = nullptr, *d_u = nullptr;
+  double pairs_grid = 0, pairs_near = 0, interp_terms = 0;
+  double bytes = 0;
+  std::vector<int64_t> ilist_entries;   // host copies for nc_tree_lists: (level, target group, source group)
+  std::vector<int64_t> nbr_entries;
+};
+
+// ------------------------------------------------------------------------------------------------
+// device helpers: cube faces, Morton codes
+// ------------------------------------------------------------------------------------------------
+__host__ __device__ inline void face_uv(double x, double y, double z, int& f, double& u, double& v) {
+  double ax = fabs(x), ay = fabs(y), az = fabs(z);
+  int a = (ax >= ay && ax >= az) ? 0 : (ay >= az ? 1 : 2);   // ties: x > y > z (R15)
+  double c[3] = {x, y, z};
+  double m = fabs(c[a]);
+  f = 2 * a + (c[a] < 0.0 ? 1 : 0);
+  u = c[(a + 1) % 3] / m;
+  v = c[(a + 2) % 3] / m;
+}
+
+__host__ __device__ inline uint64_t part1by1(uint64_t x) {
+  x &= 0xFFFFFFull;
+  x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x << 2)) & 0x3333333333333333ull;
+  x = (x | (x << 1)) & 0x5555555555555555ull;
+  return x;
+}
+__host__ __device__ inline uint32_t compact1by1(uint64_t x) {
+  x &= 0x5555555555555555ull;
+  x = (x | (x >> 1)) & 0x3333333333333333ull;
+  x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x >> 16)) & 0x00000000FFFFFFFFull;
+  return (uint32_t)x;
+}
+__host__ __device__ inline int64_t cell_prefix(int f, uint32_t iu, uint32_t iv, int lvl) {
+  return ((int64_t)f << (2 * lvl)) | (int64_t)((part1by1(iu) << 1) | part1by1(iv));
+}
+__host__ __device__ inline uint32_t clamp_cell(double u, int lvl) {
+  double n = (double)(1u << lvl);
+  double c = floor((u + 1.0) * 0.5 * n);
+  if (c < 0) c = 0;
+  if (c > n - 1) c = n - 1;
+  return (uint32_t)c;
+}
+
+__global__ void k_keys(const double* __restrict__ c, int64_t N, int64_t* __restrict__ key, int64_t* __restrict__ idx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int f;
+  double u, v;
+  face_uv(c[3 * i], c[3 * i + 1], c[3 * i + 2], f, u, v);
+  key[i] = cell_prefix(f, clamp_cell(u, kLmax), clamp_cell(v, kLmax), kLmax);
+  idx[i] = i;
+}
+
+// separation level of adjacent sorted keys: first level at which they fall in different boxes
+__global__ void k_sep(const int64_t* __restrict__ key, int64_t N, int* __restrict__ sep, int* __restrict__ dup) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i + 1 >= N) return;
+  uint64_t a = (uint64_t)key[i], b = (uint64_t)key[i + 1];
+  int s;
+  if (a == b) {
+    s = kLmax;
+    *dup = 1;
+  } else if ((a >> (2 * kLmax)) != (b >> (2 * kLmax))) {
+    s = 0;
+  } else {
+    uint64_t d = a ^ b;
+    int hb = 63 - __clzll((long long)d);        // highest differing bit (< 2*kLmax)
+    s = (2 * kLmax - 1 - hb) / 2 + 1;
+  }
+  sep[i] = s;
+}
+
+__global__ void k_box_flags(const int64_t* __restrict__ key, int64_t N, int lvl, int* __restrict__ flag) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int sh = 2 * (kLmax - lvl);
+  flag[i] = (i == 0 || (key[i] >> sh) != (key[i - 1] >> sh)) ? 1 : 0;
+}
+
+// neighbours of every group (same level, folded across cube edges)
+__global__ void k_neighbors(const int64_t* __restrict__ gkey, const int64_t* __restrict__ lvl_off, int L,
+                            int64_t ngroups, int32_t* __restrict__ nbr) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ngroups) return;
+  int lvl = 0;
+  while (lvl < L && g >= lvl_off[lvl + 1]) ++lvl;
+  const int64_t key = gkey[g];
+  const int f = (int)(key >> (2 * lvl));
+  const uint64_t mort = (uint64_t)key & ((lvl == 0) ? 0ull : ((1ull << (2 * lvl)) - 1));
+  const int iu = (int)compact1by1(mort >> 1), iv = (int)compact1by1(mort);
+  const int n = 1 << lvl;
+  const int a = f / 2;
+  const double sgn = (f & 1) ? -1.0 : 1.0;
+  const int64_t lo = lvl_off[lvl], hi = lvl_off[lvl + 1];
+  int cnt = 0;
+  for (int du = -1; du <= 1; ++du)
+    for (int dv = -1; dv <= 1; ++dv) {
+      if (du == 0 && dv == 0) continue;
+      double u = (2.0 * (iu + du) + 1.0) / n - 1.0, v = (2.0 * (iv + dv) + 1.0) / n - 1.0;
+      bool ou = fabs(u) > 1.0, ov = fabs(v) > 1.0;
+      if (ou && ov) continue;                                    // across a cube corner: no cell
+      double P[3];
+      P[a] = sgn;
+      P[(a + 1) % 3] = u;
+      P[(a + 2) % 3] = v;
+      if (ou) {
+        double e = fabs(u) - 1.0;
+        P[(a + 1) % 3] = (u > 0) ? 1.0 : -1.0;
+        P[a] = sgn * (1.0 - e);
+      }
+      if (ov) {
+        double e = fabs(v) - 1.0;
+        P[(a + 2) % 3] = (v > 0) ? 1.0 : -1.0;
+        P[a] = sgn * (1.0 - e);
+      }
+      int f2;
+      double u2, v2;
+      face_uv(P[0], P[1], P[2], f2, u2, v2);
+      int64_t want = cell_prefix(f2, clamp_cell(u2, lvl), clamp_cell(v2, lvl), lvl);
+      // binary search in [lo, hi)
+      int64_t l = lo, r = hi;
+      while (l < r) {
+        int64_t m = (l + r) >> 1;
+        if (gkey[m] < want) l = m + 1; else r = m;
+      }
+      if (l < hi && gkey[l] == want && l != g) {
+        bool dupn = false;
+        for (int k = 0; k < cnt; ++k) dupn = dupn || (nbr[8 * g + k] == (int32_t)l);
+        if (!dupn && cnt < 8) nbr[8 * g + cnt++] = (int32_t)l;
+      }
+    }
+  for (int k = cnt; k < 8; ++k) nbr[8 * g + k] = -1;
+}
+
+__device__ inline int64_t lower_bound_key(const int64_t* gkey, int64_t lo, int64_t hi, int64_t want) {
+  while (lo < hi) {
+    int64_t m = (lo + hi) >> 1;
+    if (gkey[m] < want) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
+// interaction lists: pass 0 counts, pass 1 fills (offsets from an exclusive scan of the counts)
+__global__ void k_ilist(const int64_t* __restrict__ gkey, const int64_t* __restrict__ lvl_off, int L,
+                        int64_t ngroups, const int32_t* __restrict__ nbr, const int32_t* __restrict__ gfirst,
+                        const int32_t* __restrict__ pgroup, int64_t N, const int64_t* __restrict__ off,
+                        int64_t* __restrict__ cnt, int32_t* __restrict__ out) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ngroups) return;
+  int lvl = 0;
+  while (lvl < L && g >= lvl_off[lvl + 1]) ++lvl;
+  const int32_t* mynb = nbr + 8 * g;
+  int64_t c = 0, w = off ? off[g] : 0;
+  auto emit = [&](int64_t child) {
+    if (child == g) return;
+    for (int k = 0; k < 8; ++k)
+      if (mynb[k] == (int32_t)child) return;
+    if (off) out[w + c] = (int32_t)child;
+    ++c;
+  };
+  if (lvl == 0) {
+    for (int64_t ch = lvl_off[0]; ch < lvl_off[1]; ++ch) emit(ch);
+  } else {
+    const int64_t parent = pgroup[(int64_t)(lvl - 1) * N + gfirst[g]];
+    int32_t pn[9];
+    pn[0] = (int32_t)parent;
+    for (int k = 0; k < 8; ++k) pn[k + 1] = nbr[8 * parent + k];
+    for (int k = 0; k < 9; ++k) {
+      if (pn[k] < 0) continue;
+      const int64_t pk = gkey[pn[k]];
+      const int64_t lo = lower_bound_key(gkey, lvl_off[lvl], lvl_off[lvl + 1], pk << 2);
+      const int64_t hi = lower_bound_key(gkey, lvl_off[lvl], lvl_off[lvl + 1], (pk << 2) + 4);
+      for (int64_t ch = lo; ch < hi; ++ch) emit(ch);
+    }
+  }
+  if (!off) cnt[g] = c;
+}
+
+__device__ inline double arc_between(double ax, double ay, double az, double bx, double by, double bz) {
+  double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
+  return atan2(sqrt(cx * cx + cy * cy + cz * cz), ax * bx + ay * by + az * bz);
+}
+
+// smallest enclosing cap of member centres (Badoiu-Clarkson), one warp per group
+__global__ void k_circles(const double* __restrict__ cen, const int32_t* __restrict__ gfirst,
+                          const int32_t* __restrict__ glast, int64_t ngroups, double eps, double* __restrict__ gc,
+                          double* __restrict__ gR) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= ngroups) return;
+  const int64_t a = gfirst[g], b = glast[g];
+  double sx = 0, sy = 0, sz = 0;
+  for (int64_t i = a + lane; i < b; i += 32) {
+    sx += cen[3 * i]; sy += cen[3 * i + 1]; sz += cen[3 * i + 2];
+  }
+  for (int o = 16; o; o >>= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    sz += __shfl_xor_sync(0xffffffffu, sz, o);
+  }
+  double nrm = sqrt(sx * sx + sy * sy + sz * sz);
+  double cx = sx / nrm, cy = sy / nrm, cz = sz / nrm;
+  double bx = cx, by = cy, bz = cz, best = 1e300;
+  const int iters = (b - a > 1) ? 48 : 1;
+  for (int it = 0; it < iters; ++it) {
+    double far = -1.0;
+    int64_t fi = a;
+    for (int64_t i = a + lane; i < b; i += 32) {
+      double d = arc_between(cx, cy, cz, cen[3 * i], cen[3 * i + 1], cen[3 * i + 2]);
+      if (d > far) { far = d; fi = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      double of = __shfl_xor_sync(0xffffffffu, far, o);
+      int64_t oi = __shfl_xor_sync(0xffffffffu, fi, o);
+      if (of > far || (of == far && oi < fi)) { far = of; fi = oi; }
+    }
+    if (far < best) { best = far; bx = cx; by = cy; bz = cz; }
+    const double t = 1.0 / (it + 2.0);
+    cx += t * (cen[3 * fi] - cx);
+    cy += t * (cen[3 * fi + 1] - cy);
+    cz += t * (cen[3 * fi + 2] - cz);
+    nrm = sqrt(cx * cx + cy * cy + cz * cz);
+    cx /= nrm; cy /= nrm; cz /= nrm;
+  }
+  if (lane == 0) {
+    gc[3 * g] = bx; gc[3 * g + 1] = by; gc[3 * g + 2] = bz;
+    gR[g] = best + eps;
+  }
+}
+
+// group frames (ABI rule of geometry.cu applied to circle centres): [e1 | e2 | c]
+__global__ void k_group_frames(const double* __restrict__ gc, int64_t ngroups, double* __restrict__ F) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ngroups) return;
+  double cx = gc[3 * g], cy = gc[3 * g + 1], cz = gc[3 * g + 2];
+  double ax = 1.0, ay = 0.0;
+  if (fabs(cx) > 0.9) { ax = 0.0; ay = 1.0; }
+  double dot = ax * cx + ay * cy;
+  double ex = ax - dot * cx, ey = ay - dot * cy, ez = -dot * cz;
+  double inv = 1.0 / sqrt(ex * ex + ey * ey + ez * ez);
+  ex *= inv; ey *= inv; ez *= inv;
+  double fx = cy * ez - cz * ey, fy = cz * ex - cx * ez, fz = cx * ey - cy * ex;
+  double* r = F + 9 * g;
+  r[0] = ex; r[1] = ey; r[2] = ez; r[3] = fx; r[4] = fy; r[5] = fz; r[6] = cx; r[7] = cy; r[8] = cz;
+}
+
+// incoming-grid points: r_k = R cos(pi (k + 1/2) / (2 n_r)) (positive half of a 2 n_r Chebyshev grid),
+// theta_l = 2 pi l / n_a;  x = cos(r) c + sin(r) (cos(theta) e1 + sin(theta) e2), stored x 1/2
+__global__ void k_grid_points(const int32_t* __restrict__ groups, int64_t ngr, const double* __restrict__ F,
+                              const double* __restrict__ gR, const int32_t* __restrict__ gnr,
+                              const int32_t* __restrict__ gna, const int64_t* __restrict__ goff, double* gx,
+                              double* gy, double* gz) {
+  const int64_t gi = blockIdx.x;
+  if (gi >= ngr) return;
+  const int g = groups[gi];
+  const int nr = gnr[g], na = gna[g];
+  const double* r9 = F + 9 * (int64_t)g;
+  for (int t = threadIdx.x; t < nr * na; t += blockDim.x) {
+    const int k = t / na, l = t % na;
+    const double r = gR[g] * cospi((k + 0.5) / (2.0 * nr));
+    double st, ct, sr, cr;
+    sincospi(2.0 * l / na, &st, &ct);
+    sincos(r, &sr, &cr);
+    const double a = sr * ct, b = sr * st;
+    const int64_t o = goff[g] + t;
+    gx[o] = 0.5 * (r9[0] * a + r9[3] * b + r9[6] * cr);
+    gy[o] = 0.5 * (r9[1] * a + r9[4] * b + r9[7] * cr);
+    gz[o] = 0.5 * (r9[2] * a + r9[5] * b + r9[8] * cr);
+  }
+}
+
+__global__ void k_reduce_chunks(const ChunkRec* __restrict__ ch, int64_t nch, const double* __restrict__ part,
+                                double* __restrict__ gval) {
+  const int64_t c = blockIdx.x;
+  if (c >= nch) return;
+  const ChunkRec R = ch[c];
+  for (int t = threadIdx.x; t < R.npt; t += blockDim.x) {
+    double v = 0.0;
+    for (int s = 0; s < R.nu; ++s) v += part[(R.u0 + s) * kGridUnitPoints + t];
+    gval[R.pt0 + t] = v;
+  }
+}
+
+// samples (n_r x n_a, radius-major) -> coefficients, layout ((m * 2 + cs) * n_r + j), n = (m & 1) + 2 j
+__global__ void k_transform(const int32_t* __restrict__ groups, int64_t ngr, const int32_t* __restrict__ gnr,
+                            const int32_t* __restrict__ gna, const int64_t* __restrict__ goff,
+                            const int64_t* __restrict__ coff, const double* __restrict__ gval,
+                            double* __restrict__ coef) {
+  extern __shared__ double sh[];
+  const int g = groups[blockIdx.x];
+  const int nr = gnr[g], na = gna[g], M = na / 2;
+  double* f = sh;                      // nr * na
+  double* AB = sh + nr * na;           // nr * (M+1) * 2
+  for (int t = threadIdx.x; t < nr * na; t += blockDim.x) f[t] = gval[goff[g] + t];
+  __syncthreads();
+  for (int t = threadIdx.x; t < nr * (M + 1) * 2; t += blockDim.x) {
+    const int k = t / ((M + 1) * 2), rem = t % ((M + 1) * 2), m = rem >> 1, cs = rem & 1;
+    double s = 0.0;
+    for (int l = 0; l < na; ++l) {
+      const int r = (m * l) % na;
+      double sv, cv;
+      sincospi(2.0 * r / na, &sv, &cv);
+      s = fma(f[k * na + l], cs ? sv : cv, s);
+    }
+    double scale = (m == 0 || 2 * m == na) ? 1.0 / na : 2.0 / na;
+    if (cs && (m == 0 || 2 * m == na)) scale = 0.0;
+    AB[t] = s * scale;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < (M + 1) * 2 * nr; t += blockDim.x) {
+    const int mc = t / nr, j = t % nr, m = mc >> 1, cs = mc & 1;
+    const int n = (m & 1) + 2 * j;
+    double s = 0.0;
+    for (int k = 0; k < nr; ++k) {
+      const int r = (n * (2 * k + 1)) % (8 * nr);   // cos(n pi (2k+1) / (4 nr)) exactly reduced
+      s = fma(AB[(k * (M + 1) + m) * 2 + cs], cospi((double)r / (4.0 * nr)), s);
+    }
+    s *= 2.0 / nr;
+    if (n == 0) s *= 0.5;
+    coef[coff[g] + t] = s;
+  }
+}
+
+// step 4: u_i(node) = udir + sum over levels of the group's expansion at the node
+__global__ void k_interp(int L, int64_t rc, int Kstar, const int32_t* __restrict__ pgl, const double* __restrict__ F,
+                         const double* __restrict__ gR, const int32_t* __restrict__ gnr,
+                         const int32_t* __restrict__ gna, const int64_t* __restrict__ coff,
+                         const double* __restrict__ coef, const double* __restrict__ tx, const double* __restrict__ ty,
+                         const double* __restrict__ tz, const double* __restrict__ udir, double* __restrict__ u) {
+  extern __shared__ double cs_[];
+  const int64_t i = blockIdx.x;
+  constexpr int NPT = 4;
+  for (int kb = 0; kb < Kstar; kb += NPT * blockDim.x) {
+  double acc[NPT], px[NPT], py[NPT], pz[NPT];
+  int nn = 0;
+  for (int k = kb + threadIdx.x; k < Kstar && nn < NPT; k += blockDim.x, ++nn) {
+    const int64_t t = i * Kstar + k;
+    px[nn] = 2.0 * tx[t]; py[nn] = 2.0 * ty[t]; pz[nn] = 2.0 * tz[t];
+    acc[nn] = udir ? udir[t] : 0.0;
+  }
+  for (int lvl = 0; lvl <= L; ++lvl) {
+    const int g = pgl[(int64_t)lvl * rc + i];
+    const int nr = gnr[g], na = gna[g];
+    if (nr == 0) continue;   // block-uniform
+    const int M = na / 2, nc = (M + 1) * 2 * nr;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nc; t += blockDim.x) cs_[t] = coef[coff[g] + t];
+    __syncthreads();
+    const double* r9 = F + 9 * (int64_t)g;
+    const double invR = 1.0 / gR[g];
+    for (int q = 0; q < nn; ++q) {
+      const double sx = r9[0] * px[q] + r9[1] * py[q] + r9[2] * pz[q];
+      const double sy = r9[3] * px[q] + r9[4] * py[q] + r9[5] * pz[q];
+      const double cz = r9[6] * px[q] + r9[7] * py[q] + r9[8] * pz[q];
+      const double rho = sqrt(sx * sx + sy * sy);
+      const double x = atan2(rho, cz) * invR;
+      const double c1 = rho > 0 ? sx / rho : 1.0, s1 = rho > 0 ? sy / rho : 0.0;
+      const double w2 = 4.0 * x * x - 2.0;
+      double cm = 1.0, sm = 0.0, cmm = c1, smm = -s1;   // cos/sin(m theta), (m-1)
+      double val = 0.0;
+      for (int m = 0; m <= M; ++m) {
+        const double* ca = cs_ + (m * 2) * nr;
+        const double* cb = ca + nr;
+        double t0 = (m & 1) ? x : 1.0;
+        double t1 = (m & 1) ? x * (4.0 * x * x - 3.0) : 2.0 * x * x - 1.0;
+        double A = ca[0] * t0, B = cb[0] * t0;
+        for (int j = 1; j < nr; ++j) {
+          A = fma(ca[j], t1, A);
+          B = fma(cb[j], t1, B);
+          const double t2 = fma(w2, t1, -t0);
+          t0 = t1;
+          t1 = t2;
+        }
+        val = fma(A, cm, fma(B, sm, val));
+        const double cn = 2.0 * c1 * cm - cmm, sn = 2.0 * c1 * sm - smm;
+        cmm = cm; smm = sm; cm = cn; sm = sn;
+      }
+      acc[q] += val;
+    }
+  }
+  nn = 0;
+  for (int k = kb + threadIdx.x; k < Kstar && nn < NPT; k += blockDim.x, ++nn) u[i * Kstar + k] = acc[nn];
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// host helpers
+// ------------------------------------------------------------------------------------------------
+template <class T>
+static int halloc(nc_handle* h, T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(NC_ENOMEM, "cudaMalloc (hier) of " + std::to_string(count * sizeof(T)) + " bytes failed");
+  }
+  h->device_bytes += (double)count * sizeof(T);
+  return NC_OK;
+}
+
+template <class T>
+static int upload(nc_handle* h, T** dst, const std::vector<T>& src, cudaStream_t s) {
+  NC_TRY(halloc(h, dst, src.size()));
+  if (!src.empty()) NC_CUDA_TRY(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return NC_OK;
+}
+
+template <class T>
+static int download(std::vector<T>& dst, const T* src, size_t n, cudaStream_t s) {
+  dst.resize(n);
+  if (n) NC_CUDA_TRY(cudaMemcpyAsync(dst.data(), src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  NC_CUDA_TRY(cudaStreamSynchronize(s));
+  return NC_OK;
+}
+
+// incoming-grid size for a nearest grid source at beta = (distance - eps) / R and tolerance tol
+// (parity-restricted Chebyshev-Fourier; fitted to point-source interpolation tests, DESIGN.md "Incoming grids";
+// verified by tests/test_hier_gpu.py against the direct sum)
+static void grid_size(double beta, double tol, int& nr, int& na) {
+  const double lt = log(1.0 / tol);
+  nr = (int)ceil(0.56 * lt / acosh(std::max(beta, 1.0 + 1e-9))) + 2;
+  na = (int)ceil(1.95 * lt / log(std::max(beta, 1.0 + 1e-9))) + 4;
+  na += na & 1;
+  nr = std::max(nr, 3);
+  na = std::max(na, 8);
+}
+
+static inline double harc(const double* a, const double* b) {
+  double cx = a[1] * b[2] - a[2] * b[1], cy = a[2] * b[0] - a[0] * b[2], cz = a[0] * b[1] - a[1] * b[0];
+  return atan2(sqrt(cx * cx + cy * cy + cz * cz), a[0] * b[0] + a[1] * b[1] + a[2] * b[2]);
+}
+
+// ------------------------------------------------------------------------------------------------
+// entry points used by api.cu
+// ------------------------------------------------------------------------------------------------
 int hier_order(nc_handle* h, std::vector<double>& centers) {
-  (void)h; (void)centers;
-  return fail(NC_EUNSUP, "NC_HIER not built yet");
+  const int64_t N = h->N;
+  HierState* H = new HierState();
+  h->hier = H;
+  cudaStream_t s = h->stream;
+  double* d_c = nullptr;
+  int64_t *d_k0 = nullptr, *d_i0 = nullptr, *d_i1 = nullptr;
+  int* d_sep = nullptr;
+  int* d_dup = nullptr;
+  NC_TRY(halloc(h, &d_c, 3 * N));
+  NC_TRY(halloc(h, &d_k0, N));
+  NC_TRY(halloc(h, &H->d_keys, N));
+  NC_TRY(halloc(h, &d_i0, N));
+  NC_TRY(halloc(h, &d_i1, N));
+  NC_TRY(halloc(h, &d_sep, std::max<int64_t>(N, 1)));
+  NC_TRY(halloc(h, &d_dup, 1));
+  NC_CUDA_TRY(cudaMemcpyAsync(d_c, centers.data(), 3 * N * sizeof(double), cudaMemcpyHostToDevice, s));
+  NC_CUDA_TRY(cudaMemsetAsync(d_dup, 0, sizeof(int), s));
+  k_keys<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(d_c, N, d_k0, d_i0);
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, d_k0, H->d_keys, d_i0, d_i1, (int)N, 0, 3 + 2 * kLmax, s);
+  void* d_tmp = nullptr;
+  NC_CUDA_TRY(cudaMalloc(&d_tmp, std::max<size_t>(tmp, 16)));
+  cub::DeviceRadixSort::SortPairs(d_tmp, tmp, d_k0, H->d_keys, d_i0, d_i1, (int)N, 0, 3 + 2 * kLmax, s);
+  int L = 0;
+  if (N > 1) {
+    k_sep<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(H->d_keys, N, d_sep, d_dup);
+    int* d_L = d_dup + 0;   // reuse after reading dup
+    int dup = 0;
+    NC_CUDA_TRY(cudaMemcpyAsync(&dup, d_dup, sizeof(int), cudaMemcpyDeviceToHost, s));
+    NC_CUDA_TRY(cudaStreamSynchronize(s));
+    if (dup) {
+      cudaFree(d_tmp);
+      return fail(NC_ESEP, "nc_setup (hier): two centres fall in the same finest cube cell (coincident patches)");
+    }
+    size_t tmp2 = 0;
+    cub::DeviceReduce::Max(nullptr, tmp2, d_sep, d_L, (int)(N - 1), s);
+    if (tmp2 > tmp) {
+      cudaFree(d_tmp);
+      NC_CUDA_TRY(cudaMalloc(&d_tmp, tmp2));
+      tmp = tmp2;
+    }
+    cub::DeviceReduce::Max(d_tmp, tmp, d_sep, d_L, (int)(N - 1), s);
+    NC_CUDA_TRY(cudaMemcpyAsync(&L, d_L, sizeof(int), cudaMemcpyDeviceToHost, s));
+  }
+  std::vector<int64_t> perm;
+  NC_TRY(download(perm, d_i1, N, s));
+  NC_TRY(download(H->keys, H->d_keys, N, s));
+  cudaFree(d_tmp);
+  cudaFree(d_c); cudaFree(d_k0); cudaFree(d_i0); cudaFree(d_i1); cudaFree(d_sep); cudaFree(d_dup);
+  h->device_bytes -= (double)(3 * N + 3 * N) * 8 + 4.0 * std::max<int64_t>(N, 1) + 4;
+  H->L = L;
+  h->perm = perm;
+  std::vector<double> sorted(3 * N);
+  for (int64_t i = 0; i < N; ++i)
+    for (int d = 0; d < 3; ++d) sorted[3 * i + d] = centers[3 * perm[i] + d];
+  centers.swap(sorted);
+  return NC_OK;
 }
-int hier_partition(nc_handle* h) { (void)h; return fail(NC_EUNSUP, "NC_HIER not built yet"); }
-int hier_setup(nc_handle* h, cudaStream_t s) { (void)h; (void)s; return fail(NC_EUNSUP, "NC_HIER not built yet"); }
+
+int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
+  HierState* H = h->hier;
+  const int64_t N = h->N;
+  const int L = H->L;
+  const double eps = h->eps;
+  const int Ks = h->Kstar, p = h->p;
+  // ---- boxes per level (device flags + scan) ----
+  int *d_flag = nullptr, *d_scan = nullptr;
+  NC_TRY(halloc(h, &d_flag, N));
+  NC_TRY(halloc(h, &d_scan, N));
+  size_t tmp = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp, d_flag, d_scan, (int)N, s);
+  void* d_tmp = nullptr;
+  NC_CUDA_TRY(cudaMalloc(&d_tmp, std::max<size_t>(tmp, 16)));
+  H->lvl_off.assign(L + 2, 0);
+  H->pgroup.assign((size_t)(L + 1) * N, 0);
+  std::vector<int> flag(N), scan(N);
+  for (int lvl = 0; lvl <= L; ++lvl) {
+    k_box_flags<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(H->d_keys, N, lvl, d_flag);
+    cub::DeviceScan::InclusiveSum(d_tmp, tmp, d_flag, d_scan, (int)N, s);
+    NC_TRY(download(flag, d_flag, N, s));
+    NC_TRY(download(scan, d_scan, N, s));
+    const int64_t nb = scan[N - 1];
+    const int64_t base = H->lvl_off[lvl];
+    H->lvl_off[lvl + 1] = base + nb;
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t g = base + scan[i] - 1;
+      H->pgroup[(size_t)lvl * N + i] = (int32_t)g;
+      if (flag[i]) {
+        H->gfirst.push_back((int32_t)i);
+        H->gkey.push_back(H->keys[i] >> (2 * (kLmax - lvl)));
+        H->glevel.push_back(lvl);
+      }
+    }
+  }
+  cudaFree(d_flag); cudaFree(d_scan); cudaFree(d_tmp);
+  h->device_bytes -= 8.0 * N;
+  const int64_t G = H->lvl_off[L + 1];
+  H->ngroups = G;
+  H->glast.resize(G);
+  for (int lvl = 0; lvl <= L; ++lvl)
+    for (int64_t g = H->lvl_off[lvl]; g < H->lvl_off[lvl + 1]; ++g)
+      H->glast[g] = (g + 1 < H->lvl_off[lvl + 1]) ? H->gfirst[g + 1] : (int32_t)N;
+
+  // ---- neighbours, interaction lists, circles (device) ----
+  int64_t *d_gkey = nullptr, *d_lvl = nullptr, *d_cnt = nullptr, *d_off = nullptr;
+  int32_t *d_nbr = nullptr, *d_gfirst = nullptr, *d_glast = nullptr, *d_pg = nullptr, *d_il = nullptr;
+  double *d_cen = nullptr, *d_gc = nullptr;
+  NC_TRY(upload(h, &d_gkey, H->gkey, s));
+  NC_TRY(upload(h, &d_lvl, H->lvl_off, s));
+  NC_TRY(upload(h, &d_gfirst, H->gfirst, s));
+  NC_TRY(upload(h, &d_glast, H->glast, s));
+  NC_TRY(upload(h, &d_pg, H->pgroup, s));
+  NC_TRY(upload(h, &d_cen, cen, s));
+  NC_TRY(halloc(h, &d_nbr, 8 * G));
+  NC_TRY(halloc(h, &d_cnt, G));
+  NC_TRY(halloc(h, &d_off, G + 1));
+  NC_TRY(halloc(h, &d_gc, 3 * G));
+  NC_TRY(halloc(h, &H->d_gR, G));
+  NC_TRY(halloc(h, &H->d_gframe, 9 * G));
+  const unsigned gb = (unsigned)((G + 127) / 128);
+  k_neighbors<<<gb, 128, 0, s>>>(d_gkey, d_lvl, L, G, d_nbr);
+  k_ilist<<<gb, 128, 0, s>>>(d_gkey, d_lvl, L, G, d_nbr, d_gfirst, d_pg, N, nullptr, d_cnt, nullptr);
+  tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, d_cnt, d_off, (int)G, s);
+  NC_CUDA_TRY(cudaMalloc(&d_tmp, std::max<size_t>(tmp, 16)));
+  cub::DeviceScan::ExclusiveSum(d_tmp, tmp, d_cnt, d_off, (int)G, s);
+  std::vector<int64_t> cnt;
+  NC_TRY(download(cnt, d_cnt, G, s));
+  NC_TRY(download(H->il_off, d_off, G, s));
+  H->il_off.push_back(G ? H->il_off[G - 1] + cnt[G - 1] : 0);
+  const int64_t nil = H->il_off[G];
+  NC_TRY(halloc(h, &d_il, std::max<int64_t>(nil, 1)));
+  k_ilist<<<gb, 128, 0, s>>>(d_gkey, d_lvl, L, G, d_nbr, d_gfirst, d_pg, N, d_off, d_cnt, d_il);
+  k_circles<<<(unsigned)((32 * G + 127) / 128), 128, 0, s>>>(d_cen, d_gfirst, d_glast, G, eps, d_gc, H->d_gR);
+  k_group_frames<<<gb, 128, 0, s>>>(d_gc, G, H->d_gframe);
+  NC_TRY(download(H->nbr, d_nbr, 8 * G, s));
+  NC_TRY(download(H->il, d_il, nil, s));
+  NC_TRY(download(H->gc, d_gc, 3 * G, s));
+  NC_TRY(download(H->gR, H->d_gR, G, s));
+  cudaFree(d_tmp);
+  for (void* q : {(void*)d_gkey, (void*)d_lvl, (void*)d_cnt, (void*)d_off, (void*)d_nbr, (void*)d_gfirst,
+                  (void*)d_glast, (void*)d_pg, (void*)d_il, (void*)d_cen, (void*)d_gc})
+    cudaFree(q);
+  NC_CUDA_TRY(cudaGetLastError());
+
+  // ---- grid vs near routing, grid sizes (host) ----
+  const double tol = 0.1 * h->precision;
+  std::vector<std::vector<int32_t>> gsrc(G), nsrc(G);
+  H->gnr.assign(G, 0);
+  H->gna.assign(G, 0);
+  std::vector<double> gwork(G, 0.0);
+  std::vector<std::pair<double, int32_t>> cand;
+  for (int64_t g = 0; g < G; ++g) {
+    const int lvl = H->glevel[g];
+    const double* cg = &H->gc[3 * g];
+    const double R = H->gR[g];
+    const int64_t mem = H->glast[g] - H->gfirst[g];
+    cand.clear();
+    auto add_box = [&](int64_t b) {
+      for (int32_t j = H->gfirst[b]; j < H->glast[b]; ++j) {
+        const double d = harc(cg, &cen[3 * (int64_t)j]);
+        const bool valid = d >= R + 2.0 * eps * (1.0 + 1e-12);
+        const double beta = valid ? (d - eps) / R : 0.0;
+        cand.push_back({beta, j});
+      }
+    };
+    for (int64_t k = H->il_off[g]; k < H->il_off[g + 1]; ++k) add_box(H->il[k]);
+    if (lvl == L)
+      for (int k = 0; k < 8; ++k)
+        if (H->nbr[8 * g + k] >= 0) add_box(H->nbr[8 * g + k]);
+    if (cand.empty()) continue;
+    std::sort(cand.begin(), cand.end(), [](const std::pair<double, int32_t>& a, const std::pair<double, int32_t>& b) {
+      return a.first > b.first || (a.first == b.first && a.second < b.second);
+    });
+    // choose how many of the farthest sources go to the grid: cost in pair evaluations
+    double best_cost = (double)mem * Ks * cand.size() * p;   // all direct
+    size_t best_n = 0;
+    int bnr = 0, bna = 0;
+    for (size_t n = 1; n <= cand.size(); ++n) {
+      const double beta = cand[n - 1].first;
+      if (beta < kBetaMin) break;
+      if (n < cand.size() && cand[n].first == beta) continue;
+      int nr, na;
+      grid_size(beta, tol, nr, na);
+      const double q = (double)nr * na;
+      // pair evaluations: grid sources on q points, the rest at the members' Zernike nodes, plus the
+      // interpolation (~1.5 FMA per node per coefficient ~ 0.07 pair) and the transform
+      const double cost = q * n * p + (double)mem * Ks * (cand.size() - n) * p + 0.07 * (double)mem * Ks * q +
+                          0.1 * q * (nr + na);
+      if (cost < best_cost) {
+        best_cost = cost;
+        best_n = n;
+        bnr = nr;
+        bna = na;
+      }
+    }
+    for (size_t n = 0; n < cand.size(); ++n) (n < best_n ? gsrc[g] : nsrc[g]).push_back(cand[n].second);
+    std::sort(gsrc[g].begin(), gsrc[g].end());
+    std::sort(nsrc[g].begin(), nsrc[g].end());
+    if (best_n) {
+      H->gnr[g] = bnr;
+      H->gna[g] = bna;
+    }
+    gwork[g] = best_cost;
+  }
+
+  // ---- partition: contiguous internal rows, weighted by work (world > 1) ----
+  {
+    std::vector<double> w(N, 0.0);
+    for (int64_t g = 0; g < G; ++g) {
+      const int64_t mem = H->glast[g] - H->gfirst[g];
+      for (int32_t i = H->gfirst[g]; i < H->glast[g]; ++i) w[i] += gwork[g] / (double)mem;
+    }
+    std::vector<double> pre(N + 1, 0.0);
+    for (int64_t i = 0; i < N; ++i) pre[i + 1] = pre[i] + w[i] + 1.0;
+    h->rank_begin.assign(h->world, 0);
+    h->rank_count.assign(h->world, 0);
+    int64_t prev = 0;
+    for (int r = 0; r < h->world; ++r) {
+      int64_t end = N;
+      if (r + 1 < h->world) {
+        const double target = pre[N] * (double)(r + 1) / h->world;
+        end = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+        end = std::max(prev, std::min<int64_t>(end, N));
+      }
+      h->rank_begin[r] = prev;
+      h->rank_count[r] = end - prev;
+      prev = end;
+    }
+    h->row_begin = h->rank_begin[h->rank];
+    h->row_count = h->rank_count[h->rank];
+  }
+  const int64_t rb = h->row_begin, rc = h->row_count, re = rb + rc;
+
+  // ---- groups relevant to this rank: those containing a local patch ----
+  std::vector<char> rel(G, 0);
+  for (int lvl = 0; lvl <= L && rc > 0; ++lvl) {
+    const int64_t g0 = H->pgroup[(size_t)lvl * N + rb], g1 = H->pgroup[(size_t)lvl * N + re - 1];
+    for (int64_t g = g0; g <= g1; ++g) rel[g] = 1;
+  }
+  // grid offsets / coefficient offsets (relevant groups with a grid)
+  H->goff.assign(G + 1, 0);
+  H->coff.assign(G + 1, 0);
+  H->grid_groups.clear();
+  for (int64_t g = 0; g < G; ++g) {
+    int64_t q = 0, c = 0;
+    if (rel[g] && H->gnr[g] > 0) {
+      q = (int64_t)H->gnr[g] * H->gna[g];
+      c = (int64_t)(H->gna[g] / 2 + 1) * 2 * H->gnr[g];
+      H->grid_groups.push_back((int32_t)g);
+      H->qmax = std::max<int>(H->qmax, (int)q);
+      H->cmax = std::max<int>(H->cmax, (int)c);
+    } else if (!rel[g]) {
+      H->gnr[g] = 0;
+      H->gna[g] = 0;
+    }
+    H->goff[g + 1] = H->goff[g] + q;
+    H->coff[g + 1] = H->coff[g] + c;
+  }
+  H->Q = H->goff[G];
+  H->C = H->coff[G];
+
+  // work units (steps 2-3) and reduction chunks
+  std::vector<GridUnit> units;
+  std::vector<ChunkRec> chunks;
+  std::vector<int32_t> srclist;
+  for (int32_t g : H->grid_groups) {
+    const int64_t q = H->goff[g + 1] - H->goff[g];
+    const int64_t s0 = (int64_t)srclist.size();
+    srclist.insert(srclist.end(), gsrc[g].begin(), gsrc[g].end());
+    const int64_t ns = (int64_t)gsrc[g].size();
+    const int64_t nsl = (ns + kSliceMax - 1) / kSliceMax;
+    for (int64_t c0 = 0; c0 < q; c0 += kGridUnitPoints) {
+      ChunkRec cr;
+      cr.pt0 = H->goff[g] + c0;
+      cr.npt = (int32_t)std::min<int64_t>(kGridUnitPoints, q - c0);
+      cr.u0 = (int64_t)units.size();
+      cr.nu = (int32_t)nsl;
+      chunks.push_back(cr);
+      for (int64_t sl = 0; sl < nsl; ++sl) {
+        GridUnit u;
+        u.pt0 = cr.pt0;
+        u.npt = cr.npt;
+        u.src0 = s0 + (ns * sl) / nsl;
+        u.nsrc = (int32_t)(s0 + (ns * (sl + 1)) / nsl - u.src0);
+        units.push_back(u);
+      }
+    }
+    H->pairs_grid += (double)q * ns * p;
+    H->interp_terms += 0;
+  }
+  // near lists for local patches (concatenated over levels)
+  std::vector<int64_t> near_off(rc + 1, 0);
+  std::vector<int32_t> near_all;
+  std::vector<int32_t> work_near;
+  {
+    std::vector<std::vector<int32_t>> nl(rc);
+    for (int64_t g = 0; g < G; ++g) {
+      if (!rel[g] || nsrc[g].empty()) continue;
+      const int64_t a = std::max<int64_t>(H->gfirst[g], rb), b = std::min<int64_t>(H->glast[g], re);
+      for (int64_t i = a; i < b; ++i) nl[i - rb].insert(nl[i - rb].end(), nsrc[g].begin(), nsrc[g].end());
+    }
+    for (int64_t i = 0; i < rc; ++i) {
+      std::sort(nl[i].begin(), nl[i].end());
+      near_off[i + 1] = near_off[i] + (int64_t)nl[i].size();
+      near_all.insert(near_all.end(), nl[i].begin(), nl[i].end());
+      if (!nl[i].empty()) work_near.push_back((int32_t)i);
+      H->pairs_near += (double)nl[i].size() * Ks * p;
+    }
+  }
+  for (int64_t i = rb; i < re; ++i)
+    for (int lvl = 0; lvl <= L; ++lvl) {
+      const int32_t g = H->pgroup[(size_t)lvl * N + i];
+      H->interp_terms += (double)Ks * H->gnr[g] * H->gna[g];
+    }
+  // tree lists for introspection (audit): (level, target group, source group)
+  H->ilist_entries.clear();
+  H->nbr_entries.clear();
+  for (int64_t g = 0; g < G; ++g) {
+    for (int64_t k = H->il_off[g]; k < H->il_off[g + 1]; ++k) {
+      H->ilist_entries.push_back(H->glevel[g]);
+      H->ilist_entries.push_back(g);
+      H->ilist_entries.push_back(H->il[k]);
+    }
+    if (H->glevel[g] == L)
+      for (int k = 0; k < 8; ++k)
+        if (H->nbr[8 * g + k] >= 0) {
+          H->nbr_entries.push_back(L);
+          H->nbr_entries.push_back(g);
+          H->nbr_entries.push_back(H->nbr[8 * g + k]);
+        }
+  }
+
+  // ---- uploads and device grids ----
+  H->nunits = (int64_t)units.size();
+  H->nchunks = (int64_t)chunks.size();
+  H->nwork_near = (int64_t)work_near.size();
+  NC_TRY(upload(h, &H->d_gnr, H->gnr, s));
+  NC_TRY(upload(h, &H->d_gna, H->gna, s));
+  NC_TRY(upload(h, &H->d_goff, H->goff, s));
+  NC_TRY(upload(h, &H->d_coff, H->coff, s));
+  NC_TRY(upload(h, &H->d_grid_groups, H->grid_groups, s));
+  NC_TRY(upload(h, &H->d_units, units, s));
+  NC_TRY(upload(h, &H->d_chunks, chunks, s));
+  NC_TRY(upload(h, &H->d_srclist, srclist, s));
+  NC_TRY(upload(h, &H->d_near_off, near_off, s));
+  NC_TRY(upload(h, &H->d_near, near_all, s));
+  NC_TRY(upload(h, &H->d_work_near, work_near, s));
+  std::vector<int32_t> pgl((size_t)(L + 1) * std::max<int64_t>(rc, 1), 0);
+  for (int lvl = 0; lvl <= L; ++lvl)
+    for (int64_t i = 0; i < rc; ++i) pgl[(size_t)lvl * rc + i] = H->pgroup[(size_t)lvl * N + rb + i];
+  NC_TRY(upload(h, &H->d_pgl, pgl, s));
+  NC_TRY(halloc(h, &H->d_gx, H->Q));
+  NC_TRY(halloc(h, &H->d_gy, H->Q));
+  NC_TRY(halloc(h, &H->d_gz, H->Q));
+  NC_TRY(halloc(h, &H->d_gval, H->Q));
+  NC_TRY(halloc(h, &H->d_gcoef, H->C));
+  NC_TRY(halloc(h, &H->d_part, (size_t)H->nunits * kGridUnitPoints));
+  NC_TRY(halloc(h, &H->d_tx, rc * Ks));
+  NC_TRY(halloc(h, &H->d_ty, rc * Ks));
+  NC_TRY(halloc(h, &H->d_tz, rc * Ks));
+  NC_TRY(halloc(h, &H->d_udir, rc * Ks));
+  NC_TRY(halloc(h, &H->d_u, rc * Ks));
+  if (!H->grid_groups.empty())
+    k_grid_points<<<(unsigned)H->grid_groups.size(), 128, 0, s>>>(H->d_grid_groups, (int64_t)H->grid_groups.size(),
+                                                                  H->d_gframe, H->d_gR, H->d_gnr, H->d_gna,
+                                                                  H->d_goff, H->d_gx, H->d_gy, H->d_gz);
+  launch_targets(h->d_frames, rb, rc, h->d_zhat, Ks, 0.5, H->d_tx, H->d_ty, H->d_tz, s);
+  NC_CUDA_TRY(cudaGetLastError());
+  h->pairs_per_matvec = H->pairs_grid + H->pairs_near;
+  return NC_OK;
+}
+
 int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
-  (void)h; (void)x; (void)y; (void)s;
-  return fail(NC_EUNSUP, "NC_HIER not built yet");
+  HierState* H = h->hier;
+  const int64_t rc = h->row_count;
+  const int Ks = h->Kstar, K = h->K;
+  // steps 2-3: interaction-list and leaf-neighbour sources on the incoming grids
+  launch_pairs_grid(h->kind, H->d_units, H->nunits, H->d_gx, H->d_gy, H->d_gz, H->d_srclist, h->d_src4, h->p,
+                    H->d_part, s);
+  if (H->nchunks) k_reduce_chunks<<<(unsigned)H->nchunks, 256, 0, s>>>(H->d_chunks, H->nchunks, H->d_part, H->d_gval);
+  if (h->time_stages) cudaEventRecord(h->ev[3], s);
+  // step 4a: grid samples -> coefficients
+  if (!H->grid_groups.empty()) {
+    const size_t shm = (size_t)(H->qmax + H->cmax) * sizeof(double);
+    k_transform<<<(unsigned)H->grid_groups.size(), 128, shm, s>>>(H->d_grid_groups, (int64_t)H->grid_groups.size(),
+                                                                   H->d_gnr, H->d_gna, H->d_goff, H->d_coff,
+                                                                   H->d_gval, H->d_gcoef);
+  }
+  // near lists at the Zernike nodes
+  NC_CUDA_TRY(cudaMemsetAsync(H->d_udir, 0, (size_t)rc * Ks * sizeof(double), s));
+  launch_pairs_near(h->kind, H->d_tx, H->d_ty, H->d_tz, Ks, H->d_work_near, H->nwork_near, H->d_near_off, H->d_near,
+                    h->d_src4, h->p, H->d_udir, s);
+  // step 4b: interpolation to the Zernike nodes, summed over levels
+  if (rc > 0) {
+    const size_t shm = (size_t)std::max(H->cmax, 1) * sizeof(double);
+    k_interp<<<(unsigned)rc, 128, shm, s>>>(H->L, rc, Ks, H->d_pgl, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna,
+                                            H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u);
+  }
+  // step 5: y = x + U P^T
+  launch_gemm_dmma(H->d_u, Ks, 1, 0, h->d_P, rc, K, Ks, y, K, 1, x, K, s);
+  if (h->time_stages) cudaEventRecord(h->ev[4], s);
+  return NC_OK;
 }
-void hier_fill_stats(const nc_handle* h, nc_stats_t* o) { (void)h; (void)o; }
-void hier_destroy(nc_handle* h) { (void)h; }
+
+void hier_fill_stats(const nc_handle* h, nc_stats_t* o) {
+  const HierState* H = h->hier;
+  if (!H) return;
+  o->tree_levels = H->L;
+  o->tree_groups = H->ngroups;
+  o->hier_grid_pairs = H->pairs_grid;
+  o->hier_near_pairs = H->pairs_near;
+  o->hier_interp_terms = H->interp_terms;
+  o->hier_grid_points = H->Q;
+  o->hier_grid_units = H->nunits;
+}
+
+void hier_destroy(nc_handle* h) {
+  HierState* H = h->hier;
+  if (!H) return;
+  void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_groups,
+                  H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
+                  H->d_chunks, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
+                  H->d_udir, H->d_u};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  delete H;
+  h->hier = nullptr;
+}
+
 }  // namespace nc
 
 extern "C" int nc_tree_lists(const nc_handle* h, int64_t* n_ilist, int64_t* ilist, int64_t* n_nbr, int64_t* nbr,
                              int64_t* box_of_patch) {
-  (void)h; (void)n_ilist; (void)ilist; (void)n_nbr; (void)nbr; (void)box_of_patch;
-  return nc::fail(NC_EUNSUP, "NC_HIER not built yet");
+  if (!h) return nc::fail(NC_EINVAL, "nc_tree_lists: null handle");
+  const nc::HierState* H = h->hier;
+  if (!H) return nc::fail(NC_ESTATE, "nc_tree_lists: handle is not NC_HIER");
+  if (n_ilist) *n_ilist = (int64_t)H->ilist_entries.size() / 3;
+  if (n_nbr) *n_nbr = (int64_t)H->nbr_entries.size() / 3;
+  if (ilist) std::copy(H->ilist_entries.begin(), H->ilist_entries.end(), ilist);
+  if (nbr) std::copy(H->nbr_entries.begin(), H->nbr_entries.end(), nbr);
+  if (box_of_patch)
+    for (size_t k = 0; k < H->pgroup.size(); ++k) box_of_patch[k] = H->pgroup[k];
+  return NC_OK;
 }

@@ -6,8 +6,7 @@
 
 namespace nc {
 int hier_order(nc_handle* h, std::vector<double>& centers);   // tree order; fills h->perm, permutes centers
-int hier_partition(nc_handle* h);                              // work-weighted contiguous row ranges
-int hier_setup(nc_handle* h, cudaStream_t s);                  // tree, lists, grids (device)
+int hier_setup(nc_handle* h, const std::vector<double>& centers_internal, cudaStream_t s);  // tree, lists, grids; sets the partition
 int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s);
 void hier_fill_stats(const nc_handle* h, nc_stats_t* o);
 void hier_destroy(nc_handle* h);

@@ -39,9 +39,19 @@ constexpr int kPairThreads = 256;   // threads per CTA in the direct pair-sum ke
 constexpr int kDefaultPairTpt = 2;  // targets per thread (NC_PAIR_TPT=1|2 overrides)
 
 // ------------------------------------------------------------------------------------------------
-// hierarchical-mode state (kernels in hier.cu)
+// hierarchical-mode state (hier.cu) and its step-2/3 work unit (direct.cu)
 // ------------------------------------------------------------------------------------------------
 struct HierState;
+
+constexpr int kGridThreads = 128;      // threads per CTA of the incoming-grid pair kernel
+constexpr int kGridUnitPoints = 256;   // grid points per work unit (2 per thread)
+
+struct GridUnit {      // <= 256 points of one incoming grid x one slice of that grid's source-patch list
+  int64_t pt0;         // first grid point (global grid-point index)
+  int64_t src0;        // first entry in the source-patch list
+  int32_t npt;         // points in this unit (<= kGridUnitPoints)
+  int32_t nsrc;        // source patches in this unit
+};
 
 // ------------------------------------------------------------------------------------------------
 // the handle
@@ -50,7 +60,8 @@ struct HierState;
 
 struct nc_handle {
   int kind = 0, mode = 0, device = 0, world = 1, rank = 0;
-  int64_t N = 0, row_begin = 0, row_count = 0, rows_per_rank = 0;
+  int64_t N = 0, row_begin = 0, row_count = 0;
+  std::vector<int64_t> rank_begin, rank_count;   // partition of the internal rows over all ranks
   int M = 0, K = 0, Kstar = 0, p = 0;
   double eps = 0.0, precision = 1e-9;
   cudaStream_t stream = nullptr;  // library's own stream (used when caller passes NULL to setup ops)
@@ -73,7 +84,7 @@ struct nc_handle {
   double* d_tx = nullptr;         // row_count*Kstar targets (SoA)
   double* d_ty = nullptr;
   double* d_tz = nullptr;
-  double* d_src4 = nullptr;       // (world*rows_per_rank) * p records (x, y, z, rho)
+  double* d_src4 = nullptr;       // N * p records (x, y, z, rho), coordinates scaled by 1/2
   double* d_upart = nullptr;      // nseg x (row_count*Kstar) partial fields
   int nseg = 1;
   int pair_tpt = 1;               // targets per thread in the direct kernel (1 or 2)
@@ -131,6 +142,12 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
                          cudaStream_t s);
 
 int pairs_direct_blocks_per_sm(int p, int tpt);
+void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
+                       const double* gz, const int32_t* srclist, const double* src4, int p, double* part,
+                       cudaStream_t s);
+void launch_pairs_near(int kind, const double* tx, const double* ty, const double* tz, int Kstar, const int32_t* work,
+                       int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
+                       double* udir, cudaStream_t s);
 
 // BLAS-1 style helpers for GMRES (deterministic two-stage reductions)
 int64_t multidot_partials(int64_t n);

@@ -45,7 +45,9 @@ class NcStats(ctypes.Structure):
                 ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("matvecs", ctypes.c_int64),
                 ("pairs_per_matvec", ctypes.c_double), ("gemm_flops_per_matvec", ctypes.c_double),
                 ("ms_last", ctypes.c_double * 8), ("tree_levels", ctypes.c_int32), ("tree_groups", ctypes.c_int64),
-                ("device_bytes", ctypes.c_double)]
+                ("hier_grid_pairs", ctypes.c_double), ("hier_near_pairs", ctypes.c_double),
+                ("hier_interp_terms", ctypes.c_double), ("hier_grid_points", ctypes.c_int64),
+                ("hier_grid_units", ctypes.c_int64), ("device_bytes", ctypes.c_double)]
 
 
 EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt", "nc_stats",

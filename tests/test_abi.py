@@ -29,3 +29,21 @@ def test_library_exports_every_declared_symbol():
 def test_binding_declares_every_symbol():
     from paper_1906_04209_b200 import nc
     assert set(declared_symbols()) == set(nc.EXPORTS)
+
+
+def test_stats_struct_matches_header():
+    """The ctypes mirror of nc_stats_t has the header's fields in the header's order."""
+    import re
+    from paper_1906_04209_b200 import nc
+    src = open(os.path.join(ROOT, "include", "nc.h")).read()
+    body = src[src.index("typedef struct nc_stats_t {"):src.index("} nc_stats_t;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = []
+    for line in body.splitlines()[1:]:
+        line = line.strip().rstrip(";")
+        if not line:
+            continue
+        decl = line.split(None, 1)[1]
+        for d in decl.split(","):
+            names.append(d.strip().split("[")[0])
+    assert names == [f for f, _ in nc.NcStats._fields_]

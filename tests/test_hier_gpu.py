@@ -1,0 +1,118 @@
+"""Hierarchical mode (NC_HIER): tree audit and parity against the direct sum / the oracle.
+
+Tolerance (BASELINE.json north_star): hierarchical matvec <= 1e-8 relative l2 at the requested precision 1e-9;
+solved J / mu <= 1e-7 relative."""
+import os
+
+import numpy as np
+import pytest
+
+from nc_inputs import CONFIGS, make_centers, random_coeffs, synthetic_tables
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+HIER_TOL = 1e-8
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _nc():
+    import paper_1906_04209_b200 as nc
+    return nc
+
+
+def _phys(name):
+    from nc_inputs.tables import load_tables
+    return load_tables(os.path.join(ROOT, "tables", "data", f"{name}.npz"))
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b))
+
+
+def gpu_matvec(h, x_caller):
+    xi = torch.from_numpy(h.to_internal(x_caller)).cuda()
+    y = h.matvec(xi)
+    torch.cuda.synchronize()
+    return h.to_caller(y.cpu().numpy())
+
+
+def _group_ranges(bop):
+    L1, N = bop.shape
+    G = int(bop.max()) + 1
+    first = np.full(G, N, dtype=np.int64)
+    last = np.zeros(G, dtype=np.int64)
+    for lvl in range(L1):
+        g = bop[lvl]
+        np.minimum.at(first, g, np.arange(N))
+        np.maximum.at(last, g, np.arange(N) + 1)
+    return first, last
+
+
+@pytest.mark.parametrize("layout,N,eps", [("uniform", 700, 0.02), ("vmf", 1500, 0.005), ("uniform", 1, 0.1),
+                                          ("uniform", 7, 0.1)])
+def test_pair_coverage_exactly_once(layout, N, eps):
+    """PAPER.md:1366-1372 (note to step 3): every other patch is either a leaf neighbour or in exactly one
+    interaction list of the groups containing the target patch.  Exhaustive over all ordered pairs."""
+    c = make_centers(layout, N, eps, seed=5)
+    tab = synthetic_tables(0, eps, seed=1, M=2, p=3, n_r=2, n_theta=3)
+    h = _nc().Handle(0, c, eps, tab, mode=_nc().NC_HIER)
+    il, nb, bop = h.tree_lists()
+    first, last = _group_ranges(bop)
+    cnt = np.zeros((N, N), dtype=np.int32)
+    for _, g, b in np.concatenate([il, nb]) if len(il) + len(nb) else []:
+        cnt[first[g]:last[g], first[b]:last[b]] += 1
+    off = ~np.eye(N, dtype=bool)
+    assert np.all(cnt[off] == 1)
+    assert np.all(np.diag(cnt) == 0)
+    # interaction lists hold at most 27 boxes; leaf neighbours at most 8
+    if len(il):
+        _, counts = np.unique(il[:, 1], return_counts=True)
+        assert counts.max() <= 27
+    if len(nb):
+        _, counts = np.unique(nb[:, 1], return_counts=True)
+        assert counts.max() <= 8
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_hier_matches_direct_C2(kind):
+    cfg = CONFIGS["C2"]
+    c = cfg.centers()
+    tab = _phys("C2")
+    x = random_coeffs(cfg.N, tab.K, 2002)
+    hd = _nc().Handle(kind, c, cfg.eps, tab, mode=_nc().NC_DIRECT)
+    hh = _nc().Handle(kind, c, cfg.eps, tab, mode=_nc().NC_HIER, precision=1e-9)
+    yd = gpu_matvec(hd, x)
+    yh = gpu_matvec(hh, x)
+    assert rel(yh, yd) <= HIER_TOL
+    # the operator part alone (y - x) also within tolerance of its own norm x 10
+    assert rel(yh - x, yd - x) <= 10 * HIER_TOL
+    rows = np.random.default_rng(3).choice(cfg.N, 4, replace=False)
+    assert rel(yh[rows], O.matvec(kind, c, tab, x, rows=rows)) <= HIER_TOL
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_hier_sampled_rows_vs_oracle(name):
+    cfg = CONFIGS[name]
+    c = cfg.centers()
+    tab = _phys(name)
+    x = random_coeffs(cfg.N, tab.K, 2003)
+    h = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_HIER, precision=cfg.precision)
+    y = gpu_matvec(h, x)
+    rows = np.random.default_rng(4).choice(cfg.N, 3, replace=False)
+    assert rel(y[rows], O.matvec(cfg.kind, c, tab, x, rows=rows)) <= HIER_TOL
+
+
+def test_hier_solve_matches_direct_solve_C2():
+    cfg = CONFIGS["C2"]
+    c = cfg.centers()
+    tab = _phys("C2")
+    hd = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_DIRECT)
+    hh = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_HIER, precision=1e-9)
+    xd, itd, _ = hd.gmres(rtol=1e-10, max_iter=200)
+    xh, ith, _ = hh.gmres(rtol=1e-10, max_iter=200)
+    Jd = hd.flux_or_mfpt(xd)[1]
+    Jh = hh.flux_or_mfpt(xh)[1]
+    assert abs(Jh - Jd) <= 1e-7 * abs(Jd)
+    assert abs(ith - itd) <= 2
