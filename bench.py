@@ -25,18 +25,20 @@ sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.txt")
-# FP64-pipe flops executed per pair by k_pairs_direct's inner loop (2 per DFMA, 1 per DMUL/DADD),
-# counted from its SASS (profiles/r01_direct_sass_count.txt).
-FP64_FLOPS_PER_PAIR = {0: None, 1: None}
+# FP64-pipe flops executed per pair by the pair kernels' inner loop (pairs.cuh / green.cuh): 2 per DFMA, 1 per
+# DMUL/DADD.  Exterior: 11 DFMA + 4 DMUL + 7 DADD = 33; interior adds one DMUL (q (1 + w)) = 34.
+# Cross-checked against ncu's sass_thread_inst_executed_op_{dfma,dmul,dadd} counts (profiles/).
+FP64_FLOPS_PER_PAIR = {0: 34, 1: 33}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--mode", default="direct", choices=["direct", "hier"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--mode", default=None, choices=["direct", "hier"],
+                    help="default: hier for C3-C5, direct for C1-C2")
     ap.add_argument("--impl", default="nc", choices=["nc", "reference"])
     ap.add_argument("--tables", default="physical", choices=["synthetic", "physical"])
     ap.add_argument("--no-solve", action="store_true")
@@ -165,6 +167,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.mode is None:
+        args.mode = "direct" if args.config in ("C1", "C2") else "hier"
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -241,15 +245,16 @@ def main():
     h._L.nc_matvec_host(h._h, ctypes.cast(xh.data_ptr(), _dp), ctypes.cast(yh.data_ptr(), _dp))
     if world > 1:
         dist.barrier()
+    n_e2e = max(1, min(args.steps, 3))
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(n_e2e):
         _check(h._L.nc_matvec_host(h._h, ctypes.cast(xh.data_ptr(), _dp), ctypes.cast(yh.data_ptr(), _dp)))
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": args.steps / e2e_s, "unit": "matvec/s", "h2d_bytes_per_step": int(xh.numel() * 8),
+    e2e = {"value": n_e2e / e2e_s, "unit": "matvec/s", "steps": n_e2e, "h2d_bytes_per_step": int(xh.numel() * 8),
            "d2h_bytes_per_step": int(yh.numel() * 8)}
 
     # time to solution (GMRES from x0 = 0 on the physical right-hand side P.1, then the read-out)
@@ -273,7 +278,7 @@ def main():
     # roofline of the dominant kernel (direct pair sums): FP64 pipe
     peaks = load_fp64_peak()
     pair_ms = st["ms_last"][2] if args.mode == "direct" else st["ms_last"][4]
-    pairs = st["pairs_per_matvec"]
+    pairs = st["pairs_per_matvec"] if args.mode == "direct" else st["hier_grid_pairs"]
     fpp = FP64_FLOPS_PER_PAIR.get(cfg.kind)
     roof = None
     if pair_ms > 0 and fpp:
@@ -281,7 +286,8 @@ def main():
         peak = peaks.get("dfma")
         roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                 "frac": (ach / peak) if peak else None, "traffic": None,
-                "kernel": "k_pairs_direct", "note": "FP64-pipe flops executed per pair (SASS count) x pairs / "
+                "kernel": "k_pairs_direct" if args.mode == "direct" else "k_pairs_grid",
+                "kernel_ms": pair_ms, "note": "FP64-pipe flops executed per pair (SASS count) x pairs / "
                 "kernel ms; peak = measured DFMA throughput (profiles/r01_fp64_peak.txt)",
                 "pairs_per_s": pairs / (pair_ms * 1e-3)}
     cpu = None
@@ -300,8 +306,12 @@ def main():
             "config": {"workload": f"{cfg.name} {args.mode}", "N": cfg.N, "eps": cfg.eps, "kind": cfg.kind,
                        "layout": cfg.layout, "tables": args.tables, "K": tab.K, "Kstar": tab.Kstar, "p": tab.p,
                        "l2": "flushed between timed steps (256 MB write, untimed)"},
-            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": 3 * args.steps if args.mode == "direct" else None,
-            "roofline": roof, "cpu_baseline": cpu, "stages_ms": st["ms_last"][:7], "pairs_per_matvec": pairs,
+            "clocks": clk.summary(), "e2e": e2e,
+            "gpu_launches": (3 if args.mode == "direct" else 7) * args.steps,
+            "roofline": roof, "cpu_baseline": cpu, "stages_ms": st["ms_last"][:7], "pairs_per_matvec": st["pairs_per_matvec"],
+            "hier": ({k: st[k] for k in ("tree_levels", "tree_groups", "hier_grid_pairs", "hier_near_pairs",
+                                         "hier_interp_terms", "hier_grid_points", "hier_grid_units")}
+                     if args.mode == "hier" else None),
             "solve": solve}
     print(json.dumps(line), flush=True)
     h.close()

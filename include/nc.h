@@ -152,6 +152,12 @@ int nc_time_stages(nc_handle* h, int enable);
 int nc_tree_lists(const nc_handle* h, int64_t* n_ilist, int64_t* ilist, int64_t* n_nbr, int64_t* nbr,
                   int64_t* box_of_patch /* L+1 x N, nullable */);
 
+/* Host-only helper (no GPU needed): the contiguous row partition used by nc_setup.  Rank r of `world` gets
+ * rows [begin[r], begin[r] + count[r]) of the internal order, cut so that the prefix sums of (weights[i] + 1)
+ * are split evenly (weights NULL = equal split, as in NC_DIRECT; NC_HIER passes its per-patch work).
+ * begin, count: host arrays of `world` entries.  Errors: NC_EINVAL. */
+int nc_split_rows(const double* weights, int64_t N, int world, int64_t* begin, int64_t* count);
+
 /* world > 1 bootstrap: rank 0 creates the 128-byte NCCL unique id (host buffer), the caller broadcasts it
  * (e.g. torch.distributed) and passes it as nc_opts.nccl_id on every rank.  NC_EUNSUP without NCCL. */
 int nc_nccl_unique_id(void* id_out);

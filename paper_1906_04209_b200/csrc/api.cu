@@ -87,6 +87,26 @@ static int check_separation(const double* c, int64_t N, double eps) {
 
 // Source segments of the direct kernel (grid.y): pick the count whose total CTA count wastes the least
 // of the last wave (all CTAs carry equal work, so waves stay in lock-step), with >= 4 waves when possible.
+// contiguous partition of N rows over `world` ranks with (approximately) equal total weight: rank r gets
+// [begin[r], begin[r] + count[r]); cut where the prefix sum of (w_i + 1) crosses r/world of the total
+// (the +1 keeps every rank non-empty when N >= world).  Host-only; exported as nc_split_rows.
+void split_rows(const double* w, int64_t N, int world, int64_t* begin, int64_t* count) {
+  std::vector<double> pre(N + 1, 0.0);
+  for (int64_t i = 0; i < N; ++i) pre[i + 1] = pre[i] + (w ? w[i] : 0.0) + 1.0;
+  int64_t prev = 0;
+  for (int r = 0; r < world; ++r) {
+    int64_t end = N;
+    if (r + 1 < world) {
+      const double target = pre[N] * (double)(r + 1) / world;
+      end = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+      end = std::max(prev, std::min<int64_t>(end, N));
+    }
+    begin[r] = prev;
+    count[r] = end - prev;
+    prev = end;
+  }
+}
+
 static void compute_nseg(nc_handle* h) {
   const char* ev = getenv("NC_PAIR_TPT");
   h->pair_tpt = (ev && atoi(ev) == 1) ? 1 : (ev && atoi(ev) == 2) ? 2 : kDefaultPairTpt;
@@ -249,14 +269,10 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   launch_sources(h->d_frames, N, h->d_shat, p, 0.5, h->d_src4, s);
 
   if (h->mode == NC_DIRECT) {
-    // partition: equal contiguous row ranges (every row carries the same work in direct mode)
-    const int64_t rpr = (N + h->world - 1) / h->world;
+    // partition: contiguous row ranges of equal size (every row carries the same work in direct mode)
     h->rank_begin.assign(h->world, 0);
     h->rank_count.assign(h->world, 0);
-    for (int r = 0; r < h->world; ++r) {
-      h->rank_begin[r] = std::min<int64_t>(N, (int64_t)r * rpr);
-      h->rank_count[r] = std::min<int64_t>(rpr, N - h->rank_begin[r]);
-    }
+    split_rows(nullptr, N, h->world, h->rank_begin.data(), h->rank_count.data());
     h->row_begin = h->rank_begin[h->rank];
     h->row_count = h->rank_count[h->rank];
     const int64_t nt = h->row_count * Ks;
@@ -544,6 +560,12 @@ int nc_stats(const nc_handle* h, nc_stats_t* o) {
   for (int i = 0; i < 8; ++i) o->ms_last[i] = h->ms_last[i];
   o->device_bytes = h->device_bytes;
   hier_fill_stats(h, o);
+  return NC_OK;
+}
+
+int nc_split_rows(const double* weights, int64_t N, int world, int64_t* begin, int64_t* count) {
+  if (N < 0 || world < 1 || !begin || !count) return fail(NC_EINVAL, "nc_split_rows: bad arguments");
+  split_rows(weights, N, world, begin, count);
   return NC_OK;
 }
 

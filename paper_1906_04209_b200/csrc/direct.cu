@@ -8,12 +8,14 @@
 // Direct mode: one CTA per (target tile of 256*TPT nodes, source segment); the source range is split into `nseg`
 // segments (grid.y) chosen so the CTA count fills the last wave (api.cu); segment partials are summed in the
 // step-5 GEMM's operand load (gemm.cu), deterministic.
+#include <stdlib.h>
+
 #include "pairs.cuh"
 
 namespace nc {
 
 template <int KIND, int TPT>
-__global__ void __launch_bounds__(kPairThreads) k_pairs_direct(const double* __restrict__ tx,
+__global__ void __launch_bounds__(kPairThreads, 2) k_pairs_direct(const double* __restrict__ tx,
                                                                 const double* __restrict__ ty,
                                                                 const double* __restrict__ tz, int64_t n_tgt,
                                                                 int Kstar, int64_t tgt_patch0,
@@ -36,8 +38,14 @@ __global__ void __launch_bounds__(kPairThreads) k_pairs_direct(const double* __r
   }
   const int seg = blockIdx.y;
   const int64_t j0 = (N * seg) / nseg, j1 = (N * (seg + 1)) / nseg;
-  accumulate_list<KIND, TPT>(x, y, z, excl, acc, j1 - j0, [=] __device__(int64_t k) { return j0 + k; },
-                             reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, true);
+  if (chp == 0) {
+    __syncthreads();
+    accumulate_list_ldg<KIND, TPT>(x, y, z, excl, acc, j1 - j0, [=] __device__(int64_t k) { return j0 + k; },
+                                   reinterpret_cast<const double4*>(src4), p, logtab);
+  } else {
+    accumulate_list<KIND, TPT>(x, y, z, excl, acc, j1 - j0, [=] __device__(int64_t k) { return j0 + k; },
+                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, true);
+  }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
     const int64_t t = t0 + u * kPairThreads;
@@ -45,9 +53,11 @@ __global__ void __launch_bounds__(kPairThreads) k_pairs_direct(const double* __r
   }
 }
 
+static bool stage_ldg();
+
 int pairs_direct_blocks_per_sm(int p, int tpt) {
   int nb = 0;
-  size_t smem = (size_t)stage_patches(p) * p * sizeof(double4);
+  size_t smem = stage_ldg() ? 0 : (size_t)stage_patches(p) * p * sizeof(double4);
   if (tpt == 2)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pairs_direct<1, 2>, kPairThreads, smem);
   else
@@ -59,7 +69,7 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
                          int Kstar, int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
                          cudaStream_t s) {
   if (n_tgt <= 0) return;
-  const int chp = stage_patches(p);
+  const int chp = stage_ldg() ? 0 : stage_patches(p);
   const size_t smem = (size_t)chp * p * sizeof(double4);
   const int64_t per_block = (int64_t)kPairThreads * tpt;
   dim3 grid((unsigned)((n_tgt + per_block - 1) / per_block), (unsigned)nseg);
@@ -77,7 +87,7 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
 // ------------------------------------------------------------------------------------------------
 // hierarchical mode: interaction-list / leaf-neighbour sources on incoming grids
 // ------------------------------------------------------------------------------------------------
-template <int KIND>
+template <int KIND, bool LDG>
 __global__ void __launch_bounds__(kGridThreads) k_pairs_grid(const GridUnit* __restrict__ units,
                                                               const double* __restrict__ gx,
                                                               const double* __restrict__ gy,
@@ -94,24 +104,40 @@ __global__ void __launch_bounds__(kGridThreads) k_pairs_grid(const GridUnit* __r
   constexpr int TPT = kGridUnitPoints / kGridThreads;
   double x[TPT], y[TPT], z[TPT], acc[TPT];
   int64_t excl[TPT];
-  bool any = false;
+  // adjacent points per thread (l = TPT t + u): a partial chunk leaves at most one partially idle warp
+  const bool any = (int)(TPT * threadIdx.x) < U.npt;
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
-    const int l = threadIdx.x + u * kGridThreads;
+    const int l = TPT * threadIdx.x + u;
     const int64_t g = U.pt0 + min(l, U.npt - 1);
     x[u] = gx[g]; y[u] = gy[g]; z[u] = gz[g];
     excl[u] = -1;
     acc[u] = 0.0;
-    any = any || (l < U.npt);
   }
   const int32_t* __restrict__ lst = srclist + U.src0;
-  accumulate_list<KIND, TPT>(x, y, z, excl, acc, U.nsrc, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
-                             reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, any);
+  if (LDG) {
+    __syncthreads();
+    if (any)
+      accumulate_list_ldg<KIND, TPT>(x, y, z, excl, acc, U.nsrc, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
+                                     reinterpret_cast<const double4*>(src4), p, logtab);
+  } else {
+    accumulate_list<KIND, TPT>(x, y, z, excl, acc, U.nsrc, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
+                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, any);
+  }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
-    const int l = threadIdx.x + u * kGridThreads;
+    const int l = TPT * threadIdx.x + u;
     if (l < U.npt) part[(int64_t)blockIdx.x * kGridUnitPoints + l] = acc[u];
   }
+}
+
+static bool stage_ldg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NC_PAIR_STAGE");
+    v = (e && e[0] == 's') ? 0 : (e && e[0] == 'l') ? 1 : kDefaultStageLdg;
+  }
+  return v == 1;
 }
 
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
@@ -119,13 +145,17 @@ void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const do
                        cudaStream_t s) {
   if (nunits <= 0) return;
   const int chp = stage_patches(p);
-  const size_t smem = (size_t)chp * p * sizeof(double4);
-  if (kind == NC_EXTERIOR)
-    k_pairs_grid<1><<<(unsigned)nunits, kGridThreads, smem, s>>>(units, gx, gy, gz, srclist, src4, p, chp, part,
-                                                                 log_table_device());
-  else
-    k_pairs_grid<0><<<(unsigned)nunits, kGridThreads, smem, s>>>(units, gx, gy, gz, srclist, src4, p, chp, part,
-                                                                 log_table_device());
+  const bool ldg = stage_ldg();
+  const size_t smem = ldg ? 0 : (size_t)chp * p * sizeof(double4);
+#define NC_LAUNCH_G(KD, LD)                                                                                     \
+  k_pairs_grid<KD, LD><<<(unsigned)nunits, kGridThreads, smem, s>>>(units, gx, gy, gz, srclist, src4, p, chp, part, \
+                                                                    log_table_device())
+  if (kind == NC_EXTERIOR) {
+    if (ldg) NC_LAUNCH_G(1, true); else NC_LAUNCH_G(1, false);
+  } else {
+    if (ldg) NC_LAUNCH_G(0, true); else NC_LAUNCH_G(0, false);
+  }
+#undef NC_LAUNCH_G
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -160,8 +190,14 @@ __global__ void __launch_bounds__(kPairThreads) k_pairs_near(const double* __res
   }
   const int64_t o0 = near_off[i], o1 = near_off[i + 1];
   const int32_t* __restrict__ lst = near + o0;
-  accumulate_list<KIND, TPT>(x, y, z, excl, acc, o1 - o0, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
-                             reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, true);
+  if (chp == 0) {
+    __syncthreads();
+    accumulate_list_ldg<KIND, TPT>(x, y, z, excl, acc, o1 - o0, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
+                                   reinterpret_cast<const double4*>(src4), p, logtab);
+  } else {
+    accumulate_list<KIND, TPT>(x, y, z, excl, acc, o1 - o0, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
+                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, true);
+  }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
     const int k = tile * kPairThreads * TPT + (int)threadIdx.x + u * kPairThreads;
@@ -173,7 +209,7 @@ void launch_pairs_near(int kind, const double* tx, const double* ty, const doubl
                        int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
                        double* udir, cudaStream_t s) {
   if (nwork <= 0) return;
-  const int chp = stage_patches(p);
+  const int chp = stage_ldg() ? 0 : stage_patches(p);
   const size_t smem = (size_t)chp * p * sizeof(double4);
   const int tiles = (Kstar + kPairThreads * 2 - 1) / (kPairThreads * 2);
   const unsigned nb = (unsigned)(nwork * tiles);

@@ -20,6 +20,7 @@
 // (samples -> parity-restricted Chebyshev-Fourier coefficients) -> k_pairs_near -> k_interp
 // (step 4: evaluate every group's expansion at its members' Zernike nodes, summed over levels) -> K3 (api.cu).
 #include <cub/cub.cuh>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <cmath>
@@ -34,6 +35,7 @@ namespace nc {
 constexpr int kLmax = 24;
 constexpr int kSliceMax = 32;          // source patches per grid work unit
 constexpr double kBetaMin = 1.45;      // smallest source distance / circle radius served by a grid
+constexpr double kGridTolFactor = 300.0;  // per-grid tolerance / requested precision (calibrated: DESIGN.md R21)
 
 struct ChunkRec {
   int64_t pt0;
@@ -668,7 +670,11 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_CUDA_TRY(cudaGetLastError());
 
   // ---- grid vs near routing, grid sizes (host) ----
-  const double tol = 0.1 * h->precision;
+  // per-grid interpolation tolerance = kGridTolFactor x requested precision (calibrated, R21;
+  // NC_GRID_TOL_FACTOR overrides for calibration runs)
+  double tol_factor = kGridTolFactor;
+  if (const char* e = getenv("NC_GRID_TOL_FACTOR")) tol_factor = atof(e);
+  const double tol = tol_factor * h->precision;
   std::vector<std::vector<int32_t>> gsrc(G), nsrc(G);
   H->gnr.assign(G, 0);
   H->gna.assign(G, 0);
@@ -735,22 +741,9 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       const int64_t mem = H->glast[g] - H->gfirst[g];
       for (int32_t i = H->gfirst[g]; i < H->glast[g]; ++i) w[i] += gwork[g] / (double)mem;
     }
-    std::vector<double> pre(N + 1, 0.0);
-    for (int64_t i = 0; i < N; ++i) pre[i + 1] = pre[i] + w[i] + 1.0;
     h->rank_begin.assign(h->world, 0);
     h->rank_count.assign(h->world, 0);
-    int64_t prev = 0;
-    for (int r = 0; r < h->world; ++r) {
-      int64_t end = N;
-      if (r + 1 < h->world) {
-        const double target = pre[N] * (double)(r + 1) / h->world;
-        end = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
-        end = std::max(prev, std::min<int64_t>(end, N));
-      }
-      h->rank_begin[r] = prev;
-      h->rank_count[r] = end - prev;
-      prev = end;
-    }
+    split_rows(w.data(), N, h->world, h->rank_begin.data(), h->rank_count.data());
     h->row_begin = h->rank_begin[h->rank];
     h->row_count = h->rank_count[h->rank];
   }

@@ -37,6 +37,7 @@ int cuda_fail(cudaError_t e, const char* what);
 constexpr int kMaxP = 1024;
 constexpr int kPairThreads = 256;   // threads per CTA in the direct pair-sum kernel
 constexpr int kDefaultPairTpt = 2;  // targets per thread (NC_PAIR_TPT=1|2 overrides)
+constexpr int kDefaultStageLdg = 0; // 1: pair kernels read sources via L1 broadcasts (NC_PAIR_STAGE=ldg|smem)
 
 // ------------------------------------------------------------------------------------------------
 // hierarchical-mode state (hier.cu) and its step-2/3 work unit (direct.cu)
@@ -142,6 +143,7 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
                          cudaStream_t s);
 
 int pairs_direct_blocks_per_sm(int p, int tpt);
+void split_rows(const double* w, int64_t N, int world, int64_t* begin, int64_t* count);
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
                        const double* gz, const int32_t* srclist, const double* src4, int p, double* part,
                        cudaStream_t s);

@@ -77,4 +77,49 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
   }
 }
 
+// Variant without shared-memory staging: every warp reads the source records straight from global memory with
+// warp-uniform addresses (one L1 broadcast per record), so warps never wait on CTA barriers.
+template <int KIND, int TPT, class PatchAt>
+__device__ __forceinline__ void accumulate_list_ldg(const double (&x)[TPT], const double (&y)[TPT],
+                                                    const double (&z)[TPT], const int64_t (&excl)[TPT],
+                                                    double (&acc)[TPT], int64_t nlist, PatchAt patch_at,
+                                                    const double4* __restrict__ s4, int p,
+                                                    const double2* __restrict__ logtab) {
+  const double2* __restrict__ s2 = reinterpret_cast<const double2*>(s4);
+  for (int64_t k = 0; k < nlist; ++k) {
+    const int64_t j = patch_at(k);
+    bool all = true, none = true;
+#pragma unroll
+    for (int u = 0; u < TPT; ++u) {
+      all = all && (excl[u] != j);
+      none = none && (excl[u] == j);
+    }
+    if (none) continue;
+    const double2* __restrict__ sp = s2 + 2 * j * p;
+    if (all) {
+#pragma unroll 2
+      for (int m = 0; m < p; ++m) {
+        const double2 a = __ldg(sp + 2 * m), b = __ldg(sp + 2 * m + 1);
+#pragma unroll
+        for (int u = 0; u < TPT; ++u) {
+          const double dx = x[u] - a.x, dy = y[u] - a.y, dz = z[u] - b.x;
+          const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
+          acc[u] = fma(b.y, green_q<KIND>(qd, logtab), acc[u]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        if (excl[u] == j) continue;
+        for (int m = 0; m < p; ++m) {
+          const double2 a = __ldg(sp + 2 * m), b = __ldg(sp + 2 * m + 1);
+          const double dx = x[u] - a.x, dy = y[u] - a.y, dz = z[u] - b.x;
+          const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
+          acc[u] = fma(b.y, green_q<KIND>(qd, logtab), acc[u]);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace nc

@@ -51,7 +51,7 @@ class NcStats(ctypes.Structure):
 
 
 EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt", "nc_stats",
-           "nc_time_stages", "nc_tree_lists", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
+           "nc_time_stages", "nc_tree_lists", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
 
 _lib = None
 
@@ -75,6 +75,7 @@ def load_library(path: str = LIB_PATH):
     L.nc_stats.argtypes = [vp, ctypes.POINTER(NcStats)]
     L.nc_time_stages.argtypes = [vp, ctypes.c_int]
     L.nc_tree_lists.argtypes = [vp, _i64p, _i64p, _i64p, _i64p, _i64p]
+    L.nc_split_rows.argtypes = [_dp, ctypes.c_int64, ctypes.c_int, _i64p, _i64p]
     L.nc_nccl_unique_id.argtypes = [vp]
     L.nc_destroy.argtypes = [vp]
     L.nc_destroy.restype = None
@@ -96,6 +97,17 @@ def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(load_library().nc_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
     return buf.raw
+
+
+def split_rows(N: int, world: int, weights=None):
+    """Host-only: the contiguous row partition nc_setup uses -> (begin, count) arrays of length world."""
+    L = load_library()
+    b = np.zeros(world, dtype=np.int64)
+    c = np.zeros(world, dtype=np.int64)
+    w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    _check(L.nc_split_rows(w.ctypes.data_as(_dp) if w is not None else None, int(N), int(world),
+                           b.ctypes.data_as(_i64p), c.ctypes.data_as(_i64p)))
+    return b, c
 
 
 def _ptr(t):
