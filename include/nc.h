@@ -66,6 +66,14 @@ typedef struct nc_tables {
   const double* shat;  /* p x 3      skeleton nodes x^f_{pi(m)} (unit vectors, inside the patch) */
   const double* T;     /* p x K      outgoing map rho = T fhat (eq:Tmap)                         */
   const double* I;     /* K          integration row, I_sigma = I . sum_i fhat_i (eq:getI)       */
+  /* Optional per-level outgoing operators ("one matrix T per level"), used by NC_HIER on
+   * incoming grids whose nearest point is at arc distance >= ladder_r[k] from the source centre.  The base
+   * (shat, T, p) above is valid beyond 2 eps.  n_ladder = 0 (and NULL pointers) disables. */
+  int32_t n_ladder;           /* number of rungs                                                   */
+  const double* ladder_r;     /* n_ladder inner radii (arc length), increasing, > 2 eps            */
+  const int32_t* ladder_p;    /* n_ladder skeleton sizes, 1..1024                                  */
+  const double* ladder_shat;  /* sum(ladder_p) x 3 skeleton nodes, rung-major                      */
+  const double* ladder_T;     /* sum(ladder_p) x K outgoing maps, rung-major                       */
 } nc_tables;
 
 typedef struct nc_opts {

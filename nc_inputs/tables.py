@@ -17,6 +17,8 @@ Layout conventions (all float64, C order):
   shat  (p, 3)      skeleton (outgoing) nodes, canonical frame
   T     (p, K)      outgoing map rho = T fhat (eq:Tmap)
   I     (K,)        integration row, I_sigma = I . sum_i fhat_i (eq:getI)
+Optional per-level outgoing operators, rung k valid for targets at arc > ladder_r[k]:
+  ladder_r (nk,), ladder_p (nk,) int32, ladder_shat (sum p_k, 3), ladder_T (sum p_k, K)
 """
 from __future__ import annotations
 
@@ -38,6 +40,10 @@ class PatchTables:
     T: np.ndarray
     I: np.ndarray
     meta: dict = field(default_factory=dict)
+    ladder_r: np.ndarray | None = None
+    ladder_p: np.ndarray | None = None
+    ladder_shat: np.ndarray | None = None
+    ladder_T: np.ndarray | None = None
 
     @property
     def K(self) -> int:
@@ -59,21 +65,30 @@ class PatchTables:
         assert self.zhat.shape == (self.Kstar, 3) and self.shat.shape == (self.p, 3)
         for a in (self.zhat, self.shat):
             assert np.allclose(np.linalg.norm(a, axis=1), 1.0, atol=1e-13)
+        if self.ladder_r is not None:
+            n = int(np.sum(self.ladder_p))
+            assert self.ladder_shat.shape == (n, 3) and self.ladder_T.shape == (n, K)
+            assert np.all(np.diff(self.ladder_r) > 0) and self.ladder_r[0] > 2 * self.eps
         return self
+
+    def without_ladder(self):
+        return PatchTables(self.kind, self.eps, self.M, self.zhat, self.P, self.shat, self.T, self.I, self.meta)
 
 
 def save_tables(path, t: PatchTables):
+    extra = {k: getattr(t, k) for k in ("ladder_r", "ladder_p", "ladder_shat", "ladder_T") if getattr(t, k) is not None}
     np.savez(path, version=TABLE_VERSION, kind=t.kind, eps=t.eps, M=t.M, zhat=t.zhat, P=t.P,
-             shat=t.shat, T=t.T, I=t.I, meta=np.array(repr(t.meta)))
+             shat=t.shat, T=t.T, I=t.I, meta=np.array(repr(t.meta)), **extra)
 
 
 def load_tables(path) -> PatchTables:
     z = np.load(path, allow_pickle=False)
     assert int(z["version"]) == TABLE_VERSION, "table file version mismatch"
+    lad = {k: np.ascontiguousarray(z[k]) for k in ("ladder_r", "ladder_p", "ladder_shat", "ladder_T") if k in z.files}
     return PatchTables(kind=int(z["kind"]), eps=float(z["eps"]), M=int(z["M"]),
                        zhat=np.ascontiguousarray(z["zhat"]), P=np.ascontiguousarray(z["P"]),
                        shat=np.ascontiguousarray(z["shat"]), T=np.ascontiguousarray(z["T"]),
-                       I=np.ascontiguousarray(z["I"]), meta={"repr": str(z["meta"])}).validate()
+                       I=np.ascontiguousarray(z["I"]), meta={"repr": str(z["meta"])}, **lad).validate()
 
 
 def patch_point(t, theta):

@@ -23,7 +23,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20, n_theta: int = 64,
-                 id_tol: float = 1e-11, zn_r: int | None = None, zn_theta: int | None = None, verbose=False):
+                 id_tol: float = 1e-11, zn_r: int | None = None, zn_theta: int | None = None, verbose=False,
+                 ladder: bool = True, ladder_max: float = 1.2):
     t0 = time.time()
     op = solve_onepatch(kind, eps, M, npan, k, n_theta)
     t1 = time.time()
@@ -37,16 +38,38 @@ def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20
     zhat = zernike.patch_xyz(eps, r, th)
     I = wf @ B
     err = outgoing_error(kind, fine, wf, B, shat, T, eps)
+    # per-level recompression ("one matrix T per level"): a ladder of far-field regions
+    # {arc > r_k}, r_k = 2 eps 2^k, each with its own ID against a training grid on that region
+    lad_r, lad_p, lad_s, lad_T, lad_err = [], [], [], [], []
+    if ladder:
+        rung = 1
+        while 2.0 * eps * 2.0 ** rung < ladder_max:
+            inner = 2.0 * 2.0 ** rung
+            Jk, Pik = interp_decomp(kind, training_grid(eps, inner=inner), fine, id_tol)
+            Tk = Pik @ (wf[:, None] * B)
+            lad_r.append(inner * eps)
+            lad_p.append(len(Jk))
+            lad_s.append(fine[Jk])
+            lad_T.append(Tk)
+            lad_err.append(outgoing_error(kind, fine, wf, B, fine[Jk], Tk, eps, inner=inner))
+            rung += 1
+    t3 = time.time()
     meta = dict(kind=kind, eps=eps, M=M, npan=npan, k=k, n_theta=n_theta, id_tol=id_tol, p=len(J), n_f=len(wf),
-                n_train=len(train), outgoing_rel_err=err, t_onepatch_s=t1 - t0, t_id_s=t2 - t1)
+                n_train=len(train), outgoing_rel_err=err, t_onepatch_s=t1 - t0, t_id_s=t2 - t1,
+                ladder_r=lad_r, ladder_p=lad_p, ladder_err=lad_err, t_ladder_s=t3 - t2)
     if verbose:
         print(meta, file=sys.stderr)
-    return dict(kind=kind, eps=eps, M=M, zhat=zhat, P=P, shat=shat, T=T, I=I, meta=meta)
+    out = dict(kind=kind, eps=eps, M=M, zhat=zhat, P=P, shat=shat, T=T, I=I, meta=meta)
+    if lad_r:
+        out.update(ladder_r=np.array(lad_r), ladder_p=np.array(lad_p, dtype=np.int32),
+                   ladder_shat=np.concatenate(lad_s), ladder_T=np.concatenate(lad_T))
+    return out
 
 
 def save(d, path):
+    extra = {k: d[k] for k in ("ladder_r", "ladder_p", "ladder_shat", "ladder_T") if k in d}
     np.savez(path, version=1, kind=d["kind"], eps=d["eps"], M=d["M"], zhat=d["zhat"], P=d["P"], shat=d["shat"],
-             T=d["T"], I=d["I"], meta=np.array(repr(d["meta"])))
+             T=d["T"], I=d["I"], meta=np.array(repr(d["meta"])), **extra)
 
 
 def main():

@@ -50,11 +50,12 @@ def interp_decomp(kind: int, train: np.ndarray, fine: np.ndarray, tol: float, ov
     return piv[:p], Pi
 
 
-def outgoing_error(kind: int, fine, wf, B, shat, T, eps: float, n_test: int = 400, seed: int = 1):
+def outgoing_error(kind: int, fine, wf, B, shat, T, eps: float, n_test: int = 400, seed: int = 1, inner: float = 2.0):
     """max relative error of the compressed field (eq:outgoingcompressed) over random far-field points and
     random coefficient vectors, relative to the field's max norm."""
     rng = np.random.default_rng(seed)
-    rad = 2.0 * eps * (1.0 + 1e-9) * (np.pi / (2.0 * eps)) ** rng.random(n_test) ** 3
+    r0 = inner * eps * (1.0 + 1e-9)
+    rad = r0 * (np.pi / r0) ** rng.random(n_test) ** 3
     az = 2.0 * np.pi * rng.random(n_test)
     X = np.stack([np.sin(rad) * np.cos(az), np.sin(rad) * np.sin(az), np.cos(rad)], axis=-1)
     F = rng.standard_normal((B.shape[1], 8))

@@ -179,6 +179,14 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   if (tab->K > 1024) return fail(NC_EINVAL, "nc_setup: K > 1024 not supported");
   if (tab->Kstar < 1 || tab->p < 1 || tab->p > kMaxP) return fail(NC_EINVAL, "nc_setup: bad Kstar or p");
   if (!tab->zhat || !tab->P || !tab->shat || !tab->T || !tab->I) return fail(NC_EINVAL, "nc_setup: null table");
+  if (tab->n_ladder < 0 || (tab->n_ladder > 0 && (!tab->ladder_r || !tab->ladder_p || !tab->ladder_shat ||
+                                                   !tab->ladder_T)))
+    return fail(NC_EINVAL, "nc_setup: inconsistent ladder tables");
+  for (int k = 0; k < tab->n_ladder; ++k) {
+    if (tab->ladder_p[k] < 1 || tab->ladder_p[k] > kMaxP) return fail(NC_EINVAL, "nc_setup: bad ladder_p");
+    if (!(tab->ladder_r[k] > 2.0 * eps) || (k > 0 && !(tab->ladder_r[k] > tab->ladder_r[k - 1])))
+      return fail(NC_EINVAL, "nc_setup: ladder_r must increase and exceed 2 eps");
+  }
   if (opt->mode != NC_DIRECT && opt->mode != NC_HIER) return fail(NC_EINVAL, "nc_setup: bad mode");
   if (opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world) return fail(NC_EINVAL, "nc_setup: bad rank/world");
   for (int64_t i = 0; i < N; ++i) {
@@ -227,11 +235,28 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   const int K = h->K, Ks = h->Kstar, p = h->p;
   if (!log_table_device()) return bail(fail(NC_ECUDA, "nc_setup: log table upload failed"));
 
-  // tables
+  // tables; outgoing-operator rungs (0 = base, 1.. = ladder, NC_HIER only)
   int rc;
-  if ((rc = dalloc(h, &h->d_T, (size_t)p * K)) || (rc = dalloc(h, &h->d_P, (size_t)K * Ks)) ||
+  h->nrung = 1 + ((opt->mode == NC_HIER) ? tab->n_ladder : 0);
+  h->rung_r.assign(1, 2.0 * eps);
+  h->rung_p.assign(1, p);
+  for (int k = 1; k < h->nrung; ++k) {
+    h->rung_r.push_back(tab->ladder_r[k - 1]);
+    h->rung_p.push_back(tab->ladder_p[k - 1]);
+  }
+  h->rung_trow.assign(h->nrung, 0);
+  h->rung_soff.assign(h->nrung, 0);
+  h->rung_used.assign(h->nrung, 0);
+  h->rung_used[0] = 1;
+  int64_t ptot = 0;
+  for (int k = 0; k < h->nrung; ++k) {
+    h->rung_trow[k] = ptot;
+    h->rung_soff[k] = 4 * N * ptot;
+    ptot += h->rung_p[k];
+  }
+  if ((rc = dalloc(h, &h->d_T, (size_t)ptot * K)) || (rc = dalloc(h, &h->d_P, (size_t)K * Ks)) ||
       (rc = dalloc(h, &h->d_I, (size_t)K)) || (rc = dalloc(h, &h->d_zhat, (size_t)Ks * 3)) ||
-      (rc = dalloc(h, &h->d_shat, (size_t)p * 3)))
+      (rc = dalloc(h, &h->d_shat, (size_t)ptot * 3)))
     return bail(rc);
   h->h_I.assign(tab->I, tab->I + K);
   h->h_P1.assign(K, 0.0);
@@ -250,6 +275,10 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   UP(h->d_I, tab->I, (size_t)K);
   UP(h->d_zhat, tab->zhat, (size_t)Ks * 3);
   UP(h->d_shat, tab->shat, (size_t)p * 3);
+  if (h->nrung > 1) {
+    UP(h->d_T + (size_t)p * K, tab->ladder_T, (size_t)(ptot - p) * K);
+    UP(h->d_shat + (size_t)p * 3, tab->ladder_shat, (size_t)(ptot - p) * 3);
+  }
 
   // internal order: identity (direct); the tree order (hierarchical) is applied by hier_setup
   h->perm.resize(N);
@@ -264,9 +293,11 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   UP(h->d_centers, cs.data(), (size_t)N * 3);
   launch_frames(h->d_centers, N, h->d_frames, s);
 
-  // source records (x, y, z, rho) for all N patches, coordinates scaled by 1/2 (green.cuh)
-  if ((rc = dalloc(h, &h->d_src4, (size_t)N * p * 4))) return bail(rc);
-  launch_sources(h->d_frames, N, h->d_shat, p, 0.5, h->d_src4, s);
+  // source records (x, y, z, rho) for all N patches and every rung, coordinates scaled by 1/2 (green.cuh)
+  if ((rc = dalloc(h, &h->d_src4, (size_t)N * ptot * 4))) return bail(rc);
+  for (int k = 0; k < h->nrung; ++k)
+    launch_sources(h->d_frames, N, h->d_shat + 3 * h->rung_trow[k], h->rung_p[k], 0.5, h->d_src4 + h->rung_soff[k],
+                   s);
 
   if (h->mode == NC_DIRECT) {
     // partition: contiguous row ranges of equal size (every row carries the same work in direct mode)
@@ -334,18 +365,27 @@ int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int K = h->K, p = h->p, Ks = h->Kstar;
   mark(h, 0, s);
-  // K1: rho_i = T fhat_i for this rank's rows, written into the source records' 4th slot
-  launch_gemm_dmma(x, K, 1, 0, h->d_T, h->row_count, p, K, h->d_src4 + (size_t)h->row_begin * p * 4 + 3,
-                   (int64_t)p * 4, 4, nullptr, 0, s);
+  // K1: rho_i = T_k fhat_i for this rank's rows and every rung in use, written into the records' 4th slot
+  for (int k = 0; k < h->nrung; ++k) {
+    if (!h->rung_used[k]) continue;
+    const int pk = h->rung_p[k];
+    launch_gemm_dmma(x, K, 1, 0, h->d_T + (size_t)h->rung_trow[k] * K, h->row_count, pk, K,
+                     h->d_src4 + h->rung_soff[k] + (size_t)h->row_begin * pk * 4 + 3, (int64_t)pk * 4, 4, nullptr, 0,
+                     s);
+  }
   mark(h, 1, s);
   if (h->world > 1) {
 #if NC_WITH_NCCL
-    // all-gather-v of the source records: one in-place broadcast per rank's row range
+    // all-gather-v of the source records: one in-place broadcast per (rung, rank row range)
     ncclResult_t r = ncclGroupStart();
-    for (int q = 0; q < h->world && r == ncclSuccess; ++q) {
-      if (h->rank_count[q] == 0) continue;
-      double* seg = h->d_src4 + (size_t)h->rank_begin[q] * p * 4;
-      r = ncclBroadcast(seg, seg, (size_t)h->rank_count[q] * p * 4, ncclDouble, q, h->comm, s);
+    for (int k = 0; k < h->nrung; ++k) {
+      if (!h->rung_used[k]) continue;
+      const int pk = h->rung_p[k];
+      for (int q = 0; q < h->world && r == ncclSuccess; ++q) {
+        if (h->rank_count[q] == 0) continue;
+        double* seg = h->d_src4 + h->rung_soff[k] + (size_t)h->rank_begin[q] * pk * 4;
+        r = ncclBroadcast(seg, seg, (size_t)h->rank_count[q] * pk * 4, ncclDouble, q, h->comm, s);
+      }
     }
     ncclResult_t r2 = ncclGroupEnd();
     if (r != ncclSuccess || r2 != ncclSuccess)
@@ -556,7 +596,10 @@ int nc_stats(const nc_handle* h, nc_stats_t* o) {
   o->rank = h->rank;
   o->matvecs = h->matvecs;
   o->pairs_per_matvec = h->pairs_per_matvec;
-  o->gemm_flops_per_matvec = 2.0 * h->row_count * ((double)h->p * h->K + (double)h->K * h->Kstar);
+  double psum = 0.0;
+  for (int k = 0; k < h->nrung; ++k)
+    if (h->rung_used[k]) psum += h->rung_p[k];
+  o->gemm_flops_per_matvec = 2.0 * h->row_count * (psum * h->K + (double)h->K * h->Kstar);
   for (int i = 0; i < 8; ++i) o->ms_last[i] = h->ms_last[i];
   o->device_bytes = h->device_bytes;
   hier_fill_stats(h, o);

@@ -10,6 +10,8 @@
 // step-5 GEMM's operand load (gemm.cu), deterministic.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "pairs.cuh"
 
 namespace nc {
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(kGridThreads) k_pairs_grid(const GridUnit* __r
                                                               const double* __restrict__ gy,
                                                               const double* __restrict__ gz,
                                                               const int32_t* __restrict__ srclist,
-                                                              const double* __restrict__ src4, int p, int chp,
+                                                              const double* __restrict__ src4,
                                                               double* __restrict__ part,
                                                               const double2* __restrict__ logsrc) {
   extern __shared__ double4 sm[];
@@ -115,14 +117,15 @@ __global__ void __launch_bounds__(kGridThreads) k_pairs_grid(const GridUnit* __r
     acc[u] = 0.0;
   }
   const int32_t* __restrict__ lst = srclist + U.src0;
+  const double4* __restrict__ s4 = reinterpret_cast<const double4*>(src4 + U.soff);   // the unit's rung
   if (LDG) {
     __syncthreads();
     if (any)
       accumulate_list_ldg<KIND, TPT>(x, y, z, excl, acc, U.nsrc, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
-                                     reinterpret_cast<const double4*>(src4), p, logtab);
+                                     s4, U.p, logtab);
   } else {
     accumulate_list<KIND, TPT>(x, y, z, excl, acc, U.nsrc, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
-                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, any);
+                               s4, U.p, sm, pid, stage_patches(U.p), logtab, any);
   }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
@@ -141,14 +144,13 @@ static bool stage_ldg() {
 }
 
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
-                       const double* gz, const int32_t* srclist, const double* src4, int p, double* part,
+                       const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
                        cudaStream_t s) {
   if (nunits <= 0) return;
-  const int chp = stage_patches(p);
   const bool ldg = stage_ldg();
-  const size_t smem = ldg ? 0 : (size_t)chp * p * sizeof(double4);
+  const size_t smem = ldg ? 0 : (size_t)std::max(512, pmax) * sizeof(double4);   // >= stage_patches(p) * p
 #define NC_LAUNCH_G(KD, LD)                                                                                     \
-  k_pairs_grid<KD, LD><<<(unsigned)nunits, kGridThreads, smem, s>>>(units, gx, gy, gz, srclist, src4, p, chp, part, \
+  k_pairs_grid<KD, LD><<<(unsigned)nunits, kGridThreads, smem, s>>>(units, gx, gy, gz, srclist, src4, part,       \
                                                                     log_table_device())
   if (kind == NC_EXTERIOR) {
     if (ldg) NC_LAUNCH_G(1, true); else NC_LAUNCH_G(1, false);

@@ -60,7 +60,7 @@ struct HierState {
   std::vector<int32_t> gnr, gna;
   std::vector<int64_t> goff, coff;
   int64_t Q = 0, C = 0;
-  int qmax = 0, cmax = 0;
+  int qmax = 0, cmax = 0, pmax = 0;
   std::vector<int32_t> grid_groups;
   // device
   int64_t* d_keys = nullptr;
@@ -679,6 +679,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   H->gnr.assign(G, 0);
   H->gna.assign(G, 0);
   std::vector<double> gwork(G, 0.0);
+  std::vector<std::vector<int>> grung_src(G);   // rung of each grid source
   std::vector<std::pair<double, int32_t>> cand;
   for (int64_t g = 0; g < G; ++g) {
     const int lvl = H->glevel[g];
@@ -702,8 +703,19 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     std::sort(cand.begin(), cand.end(), [](const std::pair<double, int32_t>& a, const std::pair<double, int32_t>& b) {
       return a.first > b.first || (a.first == b.first && a.second < b.second);
     });
-    // choose how many of the farthest sources go to the grid: cost in pair evaluations
-    double best_cost = (double)mem * Ks * cand.size() * p;   // all direct
+    // choose how many of the farthest sources go to the grid: cost in pair evaluations.  Grid sources use the
+    // outgoing-operator rung valid at their distance to the nearest grid point, gap = d - R = R (beta - 1) + eps
+    // (per-level recompression); the others are evaluated at the members' Zernike nodes.
+    const int p0 = h->rung_p[0];
+    std::vector<double> psum(cand.size() + 1, 0.0);   // sum of the rung sizes of the n farthest candidates
+    for (size_t n = 0; n < cand.size(); ++n) {
+      const double gap = R * (cand[n].first - 1.0) + eps;
+      int rung = 0;
+      for (int k = 1; k < h->nrung; ++k)
+        if (h->rung_r[k] <= gap * (1.0 - 1e-12)) rung = k;
+      psum[n + 1] = psum[n] + h->rung_p[rung];
+    }
+    double best_cost = (double)mem * Ks * cand.size() * p0;   // all direct
     size_t best_n = 0;
     int bnr = 0, bna = 0;
     for (size_t n = 1; n <= cand.size(); ++n) {
@@ -713,9 +725,9 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       int nr, na;
       grid_size(beta, tol, nr, na);
       const double q = (double)nr * na;
-      // pair evaluations: grid sources on q points, the rest at the members' Zernike nodes, plus the
-      // interpolation (~1.5 FMA per node per coefficient ~ 0.07 pair) and the transform
-      const double cost = q * n * p + (double)mem * Ks * (cand.size() - n) * p + 0.07 * (double)mem * Ks * q +
+      // pair evaluations: grid sources on q points (each with its own rung), the rest at the members' Zernike
+      // nodes, plus the interpolation (~1.5 FMA per node per coefficient ~ 0.07 pair) and the transform
+      const double cost = q * psum[n] + (double)mem * Ks * (cand.size() - n) * p0 + 0.07 * (double)mem * Ks * q +
                           0.1 * q * (nr + na);
       if (cost < best_cost) {
         best_cost = cost;
@@ -724,8 +736,18 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         bna = na;
       }
     }
-    for (size_t n = 0; n < cand.size(); ++n) (n < best_n ? gsrc[g] : nsrc[g]).push_back(cand[n].second);
-    std::sort(gsrc[g].begin(), gsrc[g].end());
+    for (size_t n = 0; n < cand.size(); ++n) {
+      if (n < best_n) {
+        const double gap = R * (cand[n].first - 1.0) + eps;
+        int rung = 0;
+        for (int k = 1; k < h->nrung; ++k)
+          if (h->rung_r[k] <= gap * (1.0 - 1e-12)) rung = k;
+        gsrc[g].push_back(cand[n].second);
+        grung_src[g].push_back(rung);
+      } else {
+        nsrc[g].push_back(cand[n].second);
+      }
+    }
     std::sort(nsrc[g].begin(), nsrc[g].end());
     if (best_n) {
       H->gnr[g] = bnr;
@@ -733,6 +755,10 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     }
     gwork[g] = best_cost;
   }
+
+  // rungs in use: a global decision (identical on every rank, so the per-rung all-gathers match)
+  for (int64_t g = 0; g < G; ++g)
+    for (int r : grung_src[g]) h->rung_used[r] = 1;
 
   // ---- partition: contiguous internal rows, weighted by work (world > 1) ----
   {
@@ -783,28 +809,48 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   std::vector<int32_t> srclist;
   for (int32_t g : H->grid_groups) {
     const int64_t q = H->goff[g + 1] - H->goff[g];
-    const int64_t s0 = (int64_t)srclist.size();
-    srclist.insert(srclist.end(), gsrc[g].begin(), gsrc[g].end());
-    const int64_t ns = (int64_t)gsrc[g].size();
-    const int64_t nsl = (ns + kSliceMax - 1) / kSliceMax;
+    // grid sources bucketed by rung (sorted by patch within a bucket); slices never mix rungs
+    std::vector<std::pair<int, int32_t>> rs;
+    for (size_t n = 0; n < gsrc[g].size(); ++n) rs.push_back({grung_src[g][n], gsrc[g][n]});
+    std::sort(rs.begin(), rs.end());
+    struct Slice { int64_t src0; int32_t nsrc; int rung; };
+    std::vector<Slice> slices;
+    size_t a = 0;
+    while (a < rs.size()) {
+      size_t b = a;
+      while (b < rs.size() && rs[b].first == rs[a].first) ++b;
+      const int rung = rs[a].first;
+      h->rung_used[rung] = 1;
+      const int64_t s0 = (int64_t)srclist.size();
+      for (size_t k = a; k < b; ++k) srclist.push_back(rs[k].second);
+      const int64_t ns = (int64_t)(b - a);
+      const int64_t nsl = (ns + kSliceMax - 1) / kSliceMax;
+      for (int64_t sl = 0; sl < nsl; ++sl) {
+        const int64_t x0 = s0 + (ns * sl) / nsl, x1 = s0 + (ns * (sl + 1)) / nsl;
+        slices.push_back({x0, (int32_t)(x1 - x0), rung});
+      }
+      H->pairs_grid += (double)q * ns * h->rung_p[rung];
+      a = b;
+    }
     for (int64_t c0 = 0; c0 < q; c0 += kGridUnitPoints) {
       ChunkRec cr;
       cr.pt0 = H->goff[g] + c0;
       cr.npt = (int32_t)std::min<int64_t>(kGridUnitPoints, q - c0);
       cr.u0 = (int64_t)units.size();
-      cr.nu = (int32_t)nsl;
+      cr.nu = (int32_t)slices.size();
       chunks.push_back(cr);
-      for (int64_t sl = 0; sl < nsl; ++sl) {
+      for (const Slice& sl : slices) {
         GridUnit u;
         u.pt0 = cr.pt0;
         u.npt = cr.npt;
-        u.src0 = s0 + (ns * sl) / nsl;
-        u.nsrc = (int32_t)(s0 + (ns * (sl + 1)) / nsl - u.src0);
+        u.src0 = sl.src0;
+        u.nsrc = sl.nsrc;
+        u.soff = h->rung_soff[sl.rung];
+        u.p = h->rung_p[sl.rung];
+        u.pad_ = 0;
         units.push_back(u);
       }
     }
-    H->pairs_grid += (double)q * ns * p;
-    H->interp_terms += 0;
   }
   // near lists for local patches (concatenated over levels)
   std::vector<int64_t> near_off(rc + 1, 0);
@@ -848,6 +894,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         }
   }
 
+  for (int k = 0; k < h->nrung; ++k) H->pmax = std::max(H->pmax, h->rung_p[k]);
   // ---- uploads and device grids ----
   H->nunits = (int64_t)units.size();
   H->nchunks = (int64_t)chunks.size();
@@ -893,7 +940,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   const int64_t rc = h->row_count;
   const int Ks = h->Kstar, K = h->K;
   // steps 2-3: interaction-list and leaf-neighbour sources on the incoming grids
-  launch_pairs_grid(h->kind, H->d_units, H->nunits, H->d_gx, H->d_gy, H->d_gz, H->d_srclist, h->d_src4, h->p,
+  launch_pairs_grid(h->kind, H->d_units, H->nunits, H->d_gx, H->d_gy, H->d_gz, H->d_srclist, h->d_src4, H->pmax,
                     H->d_part, s);
   if (H->nchunks) k_reduce_chunks<<<(unsigned)H->nchunks, 256, 0, s>>>(H->d_chunks, H->nchunks, H->d_part, H->d_gval);
   if (h->time_stages) cudaEventRecord(h->ev[3], s);

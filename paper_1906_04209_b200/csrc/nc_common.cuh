@@ -50,8 +50,11 @@ constexpr int kGridUnitPoints = 256;   // grid points per work unit (2 per threa
 struct GridUnit {      // <= 256 points of one incoming grid x one slice of that grid's source-patch list
   int64_t pt0;         // first grid point (global grid-point index)
   int64_t src0;        // first entry in the source-patch list
+  int64_t soff;        // offset (doubles) of the outgoing-operator rung's source records in d_src4
   int32_t npt;         // points in this unit (<= kGridUnitPoints)
   int32_t nsrc;        // source patches in this unit
+  int32_t p;           // skeleton size of the rung
+  int32_t pad_;
 };
 
 // ------------------------------------------------------------------------------------------------
@@ -85,7 +88,15 @@ struct nc_handle {
   double* d_tx = nullptr;         // row_count*Kstar targets (SoA)
   double* d_ty = nullptr;
   double* d_tz = nullptr;
-  double* d_src4 = nullptr;       // N * p records (x, y, z, rho), coordinates scaled by 1/2
+  double* d_src4 = nullptr;       // per rung k: N * p_k records (x, y, z, rho), coordinates scaled by 1/2
+  // outgoing-operator rungs: 0 = base (T, shat, p); 1.. = per-level ladder
+  int nrung = 1;
+  std::vector<double> rung_r;     // inner radius (arc length) of validity
+  std::vector<int> rung_p;
+  std::vector<int64_t> rung_trow; // first row of the rung in d_T (rows of K)
+  std::vector<int64_t> rung_soff; // offset (doubles) of the rung's records in d_src4
+  std::vector<char> rung_used;    // rungs whose rho K1 must produce
+  double* d_shat_all = nullptr;   // sum p_k x 3
   double* d_upart = nullptr;      // nseg x (row_count*Kstar) partial fields
   int nseg = 1;
   int pair_tpt = 1;               // targets per thread in the direct kernel (1 or 2)
@@ -145,7 +156,7 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
 int pairs_direct_blocks_per_sm(int p, int tpt);
 void split_rows(const double* w, int64_t N, int world, int64_t* begin, int64_t* count);
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
-                       const double* gz, const int32_t* srclist, const double* src4, int p, double* part,
+                       const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
                        cudaStream_t s);
 void launch_pairs_near(int kind, const double* tx, const double* ty, const double* tz, int Kstar, const int32_t* work,
                        int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,

@@ -30,7 +30,9 @@ class NcError(RuntimeError):
 
 class NcTables(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int32), ("K", ctypes.c_int32), ("Kstar", ctypes.c_int32), ("p", ctypes.c_int32),
-                ("zhat", _dp), ("P", _dp), ("shat", _dp), ("T", _dp), ("I", _dp)]
+                ("zhat", _dp), ("P", _dp), ("shat", _dp), ("T", _dp), ("I", _dp),
+                ("n_ladder", ctypes.c_int32), ("ladder_r", _dp), ("ladder_p", ctypes.POINTER(ctypes.c_int32)),
+                ("ladder_shat", _dp), ("ladder_T", _dp)]
 
 
 class NcOpts(ctypes.Structure):
@@ -128,7 +130,7 @@ class Handle:
     """One nc_setup'd layout.  ``tables`` is any object with M, zhat, P, shat, T, I numpy attributes."""
 
     def __init__(self, kind, centers, eps, tables, mode=NC_DIRECT, precision=1e-9, device=0, world=1, rank=0,
-                 nccl_id: bytes | None = None, check_separation=True):
+                 nccl_id: bytes | None = None, check_separation=True, use_ladder=True):
         L = load_library()
         self._L = L
         c = np.ascontiguousarray(centers, dtype=np.float64)
@@ -136,7 +138,18 @@ class Handle:
         zhat, P, shat, T, I = self._keep
         tab = NcTables(int(tables.M), T.shape[1], zhat.shape[0], shat.shape[0],
                        zhat.ctypes.data_as(_dp), P.ctypes.data_as(_dp), shat.ctypes.data_as(_dp),
-                       T.ctypes.data_as(_dp), I.ctypes.data_as(_dp))
+                       T.ctypes.data_as(_dp), I.ctypes.data_as(_dp), 0, None, None, None, None)
+        if use_ladder and getattr(tables, "ladder_r", None) is not None and len(tables.ladder_r) > 0:
+            lr = np.ascontiguousarray(tables.ladder_r, dtype=np.float64)
+            lp = np.ascontiguousarray(tables.ladder_p, dtype=np.int32)
+            ls = np.ascontiguousarray(tables.ladder_shat, dtype=np.float64)
+            lt = np.ascontiguousarray(tables.ladder_T, dtype=np.float64)
+            self._keep += [lr, lp, ls, lt]
+            tab.n_ladder = len(lr)
+            tab.ladder_r = lr.ctypes.data_as(_dp)
+            tab.ladder_p = lp.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            tab.ladder_shat = ls.ctypes.data_as(_dp)
+            tab.ladder_T = lt.ctypes.data_as(_dp)
         idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         opts = NcOpts(int(mode), float(precision), int(device), int(world), int(rank),
                       ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None, int(bool(check_separation)))

@@ -116,3 +116,20 @@ def test_hier_solve_matches_direct_solve_C2():
     Jh = hh.flux_or_mfpt(xh)[1]
     assert abs(Jh - Jd) <= 1e-7 * abs(Jd)
     assert abs(ith - itd) <= 2
+
+
+def test_per_level_outgoing_ladder_matches_direct_C2():
+    """Per-level recompressed outgoing operators: hier with the ladder == hier without it ==
+    direct, within the hierarchical tolerance; the ladder lowers the grid pair count."""
+    cfg = CONFIGS["C2"]
+    c = cfg.centers()
+    tab = _phys("C2")
+    assert tab.ladder_r is not None and len(tab.ladder_r) >= 2
+    x = random_coeffs(cfg.N, tab.K, 2004)
+    hd = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_DIRECT)
+    h1 = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_HIER, use_ladder=True)
+    h0 = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_HIER, use_ladder=False)
+    yd = gpu_matvec(hd, x)
+    assert rel(gpu_matvec(h1, x), yd) <= HIER_TOL
+    assert rel(gpu_matvec(h0, x), yd) <= HIER_TOL
+    assert h1.stats()["hier_grid_pairs"] < 0.8 * h0.stats()["hier_grid_pairs"]

@@ -131,3 +131,15 @@ def test_oracle_physics_bounds_C1():
     cE = CONFIGS["C2"].centers()[:20]
     rE = O.solve(1, cE, tabE)
     assert -4 * np.pi < rE["value"] < 0
+
+
+@pytest.mark.parametrize("name", ["C2", "C5"])
+def test_per_level_ladder_tables(name):
+    """Per-level recompression: rung k compresses the outgoing field on {arc > r_k} with fewer
+    skeleton points than the base (valid beyond 2 eps); every rung meets the ID tolerance on its region."""
+    tab = _load(name)
+    meta = eval(tab.meta["repr"], {"__builtins__": {}})
+    assert tab.ladder_r is not None
+    assert np.all(np.diff(tab.ladder_p) <= 0) and tab.ladder_p[0] < tab.p
+    assert max(meta["ladder_err"]) < 1e-9
+    np.testing.assert_allclose(tab.ladder_r / tab.eps, 2.0 * 2.0 ** np.arange(1, len(tab.ladder_r) + 1))
