@@ -60,6 +60,24 @@ def load_fp64_peak():
     return best
 
 
+# ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
+TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01b_ncu_full_pairs_grid.json"}
+
+
+def profiled_traffic(kernel, config, mode):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu capture, or (None, None)."""
+    rel = TRAFFIC_PROFILES.get((kernel, config, mode))
+    if not rel:
+        return None, None
+    try:
+        for rec in json.load(open(os.path.join(ROOT, rel))):
+            if kernel in rec.get("kernel", "") and rec.get("dram_bytes_total"):
+                return float(rec["dram_bytes_total"]), rel
+    except (OSError, ValueError):
+        pass
+    return None, None
+
+
 def make_tables(cfg, which):
     from nc_inputs import synthetic_tables
     if which == "physical":
@@ -208,15 +226,13 @@ def main():
     for _ in range(max(args.warmup, 0)):
         h.matvec(x, y)
     torch.cuda.synchronize()
-    # per-stage times (one extra, untimed matvec with stage events)
-    h.time_stages(True)
-    h.matvec(x, y)
-    torch.cuda.synchronize()
-    st = h.stats()
-    h.time_stages(False)
 
+    # timed region: per-step CUDA events around each matvec on the launching stream, plus the library's own
+    # events around the dominant kernel inside every timed matvec (nc_time_stages; no host sync inside nc_matvec)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stage_ms, launches = [], 0
+    h.time_stages(True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -226,11 +242,16 @@ def main():
             starts[k].record(stream)
             h.matvec(x, y)
             ends[k].record(stream)
+            st = h.stats()                                  # waits for this step's stage events
+            stage_ms.append(st["ms_last"][:7])
+            launches += st["launches_per_matvec"]
         torch.cuda.synchronize()
+    h.time_stages(False)
     if world > 1:
         dist.barrier()
     ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_total = float(np.sum(ms_steps))
+    stages_avg = [float(v) for v in np.mean(np.asarray(stage_ms), axis=0)]
     if world > 1:
         t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -263,33 +284,54 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        h.time_stages(True)                 # events only (no host sync inside nc_matvec); GMRES CGS2 timing
         t0 = time.perf_counter()
         xs, its, hist = h.gmres(rtol=cfg.gmres_tol, max_iter=300, allow_noconv=True)
         Is, val = h.flux_or_mfpt(xs) if (cfg.kind == 1 or args.tables == "physical") else (float("nan"), float("nan"))
         tts = time.perf_counter() - t0
+        h.time_stages(False)
+        gst = h.stats()
         solve = {"time_to_solution_s": tts, "gmres_iters": its, "final_rel_residual": float(hist[-1]),
                  "I_sigma": Is, ("mu" if cfg.kind == 0 else "J"): val, "setup_s": setup_s,
                  "tables": args.tables}
+        if gst["gmres_ortho_iters"] > 0 and gst["gmres_ortho_ms"] > 0:
+            hbm = json.load(open(PEAKS_FILE)).get("hbm_gbs") if os.path.exists(PEAKS_FILE) else None
+            gbs = gst["gmres_ortho_bytes"] / (gst["gmres_ortho_ms"] * 1e-3) / 1e9
+            solve["gmres_cgs2"] = {"bound": "hbm", "ms_total": gst["gmres_ortho_ms"], "iters": gst["gmres_ortho_iters"],
+                                   "achieved": gbs, "unit": "GB/s", "peak": hbm, "frac": gbs / hbm if hbm else None,
+                                   "note": "CGS2 (2 x multidot + gemv_sub, norm): algorithmic bytes / device time; "
+                                           "peak = MEASURED_PEAKS.json hbm_gbs (of measured)"}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
-    # roofline of the dominant kernel (direct pair sums): FP64 pipe
+    # roofline of the dominant kernel (direct: k_pairs_direct; hier: k_pairs_grid): FP64 pipe
     peaks = load_fp64_peak()
-    pair_ms = st["ms_last"][2] if args.mode == "direct" else st["ms_last"][4]
+    pair_ms = stages_avg[2] if args.mode == "direct" else stages_avg[4]
     pairs = st["pairs_per_matvec"] if args.mode == "direct" else st["hier_grid_pairs"]
+    kname = "k_pairs_direct" if args.mode == "direct" else "k_pairs_grid"
     fpp = FP64_FLOPS_PER_PAIR.get(cfg.kind)
     roof = None
     if pair_ms > 0 and fpp:
         ach = pairs * fpp / (pair_ms * 1e-3) / 1e12
         peak = peaks.get("dfma")
+        traffic, tsrc = profiled_traffic(kname, cfg.name, args.mode)
         roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": (ach / peak) if peak else None, "traffic": None,
-                "kernel": "k_pairs_direct" if args.mode == "direct" else "k_pairs_grid",
-                "kernel_ms": pair_ms, "note": "FP64-pipe flops executed per pair (SASS count) x pairs / "
-                "kernel ms; peak = measured DFMA throughput (profiles/r01_fp64_peak.txt)",
+                "frac": (ach / peak) if peak else None, "traffic": traffic,
+                "kernel": kname, "kernel_ms": pair_ms, "kernel_share_of_step": pair_ms / (ms_total / args.steps),
+                "note": "FP64-pipe flops executed per pair (SASS count, 2 per DFMA) x pairs / kernel ms (CUDA events "
+                        "around the kernel in every timed step); peak = measured DFMA throughput "
+                        "(profiles/r01_fp64_peak.txt); traffic = DRAM bytes per launch from " + (tsrc or "no capture"),
                 "pairs_per_s": pairs / (pair_ms * 1e-3)}
+    # the fp64 tensor-core GEMMs (K1 T-apply over the used rungs, K3 P-apply + identity): DMMA roofline
+    kd = st["K"] * st["Kstar"] * 2.0 * st["row_count"]
+    gemms = {}
+    for name, ms, fl in (("T_apply", stages_avg[0], st["gemm_flops_per_matvec"] - kd), ("P_apply", stages_avg[3], kd)):
+        if ms > 0:
+            tf = fl / (ms * 1e-3) / 1e12
+            gemms[name] = {"bound": "tensor", "kernel": "k_gemm_dmma", "ms": ms, "achieved": tf, "unit": "TFLOP/s",
+                           "peak": peaks.get("dmma"), "frac": tf / peaks["dmma"] if peaks.get("dmma") else None}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -307,8 +349,10 @@ def main():
                        "layout": cfg.layout, "tables": args.tables, "K": tab.K, "Kstar": tab.Kstar, "p": tab.p,
                        "l2": "flushed between timed steps (256 MB write, untimed)"},
             "clocks": clk.summary(), "e2e": e2e,
-            "gpu_launches": (3 if args.mode == "direct" else 7) * args.steps,
-            "roofline": roof, "cpu_baseline": cpu, "stages_ms": st["ms_last"][:7], "pairs_per_matvec": st["pairs_per_matvec"],
+            "gpu_launches": launches,
+            "roofline": roof, "gemm_roofline": gemms, "cpu_baseline": cpu,
+            "stages_ms": dict(zip(["T_apply", "all_gather", "direct_pairs", "P_apply", "grid_pairs", "hier_rest",
+                                   "total"], stages_avg)), "pairs_per_matvec": st["pairs_per_matvec"],
             "hier": ({k: st[k] for k in ("tree_levels", "tree_groups", "hier_grid_pairs", "hier_near_pairs",
                                          "hier_interp_terms", "hier_grid_points", "hier_grid_units")}
                      if args.mode == "hier" else None),

@@ -82,7 +82,9 @@ typedef struct nc_opts {
   int32_t device;        /* CUDA device ordinal (-1: current device)                             */
   int32_t world;         /* number of ranks (1 = single GPU)                                     */
   int32_t rank;          /* this rank, 0 <= rank < world                                         */
-  const void* nccl_id;   /* world > 1: pointer to the 128-byte ncclUniqueId made by rank 0       */
+  const void* nccl_id;   /* world > 1: pointer to the 128-byte ncclUniqueId made by rank 0;      */
+                         /* NULL with world > 1 = rank EMULATION: no communicator, this handle  */
+                         /* serves nc_matvec_emulated only (single-GPU tests of the partition)  */
   int32_t check_separation; /* 1: verify the 3 eps separation (NC_ESEP on failure); 0: trust input */
 } nc_opts;
 
@@ -92,9 +94,11 @@ typedef struct nc_stats_t {
   int64_t matvecs;              /* matvecs applied since setup                                     */
   double pairs_per_matvec;      /* kernel evaluations G(x,y) rho per matvec on this rank           */
   double gemm_flops_per_matvec; /* 2 p K n + 2 K Kstar n on this rank (n = row_count)              */
-  double ms_last[8];            /* per-stage device ms of the last timed matvec:                   */
-                                /*   [0] T-apply  [1] all-gather  [2] pair sums  [3] P-apply       */
-                                /*   [4] hier step 2+3  [5] hier step 4  [6] total  [7] reserved   */
+  double ms_last[8];            /* per-stage device ms of the last matvec run with nc_time_stages:  */
+                                /*   [0] T-apply  [1] all-gather  [2] direct pair sums  [3] P-apply */
+                                /*   [4] hier k_pairs_grid alone (steps 2-3 on incoming grids)      */
+                                /*   [5] hier grid reduce + transform + near list + step 4          */
+                                /*   [6] total  [7] reserved                                        */
   int32_t tree_levels;          /* NC_HIER: depth L of the sphere quadtree                         */
   int64_t tree_groups;          /* NC_HIER: number of non-empty boxes over all levels              */
   double hier_grid_pairs;       /* NC_HIER: pair evaluations on incoming grids per matvec (steps 2-3) */
@@ -103,6 +107,10 @@ typedef struct nc_stats_t {
   int64_t hier_grid_points;     /* NC_HIER: incoming-grid points held by this rank                  */
   int64_t hier_grid_units;      /* NC_HIER: step-2/3 work units (CTAs) per matvec                   */
   double device_bytes;          /* device memory held by the handle                                */
+  int32_t launches_per_matvec;  /* kernels this library launched in the last nc_matvec              */
+  double gmres_ortho_ms;        /* GMRES CGS2 orthogonalisation device ms summed over the iterations */
+  double gmres_ortho_bytes;     /*   run with nc_time_stages on, and its algorithmic HBM bytes       */
+  int64_t gmres_ortho_iters;    /*   (iterations counted)                                          */
 } nc_stats_t;
 
 typedef struct nc_handle nc_handle;
@@ -129,6 +137,13 @@ int nc_partition(const nc_handle* h, int64_t* row_begin, int64_t* row_count, int
  * NC_ENCCL. */
 int nc_matvec(nc_handle* h, const double* x, double* y, void* stream);
 
+/* Rank emulation (handle set up with world > 1 and nccl_id == NULL): the same map for this rank's rows, with
+ * the all-gather replaced by computing every rank's outgoing records from the FULL input.
+ *   x_all  device, N x K (all rows, internal order);  y  device, row_count x K (this rank's rows)
+ * Exercises the rank's partition (row range, work-weighted cut, redundant straddling groups, near lists) on one
+ * GPU.  Errors: NC_EINVAL, NC_ECUDA. */
+int nc_matvec_emulated(nc_handle* h, const double* x_all, double* y, void* stream);
+
 /* Same map with HOST buffers (row_count x K each): copies x in, applies, copies y out, synchronizes.
  * This is the end-to-end entry point timed as "e2e" by bench.py. */
 int nc_matvec_host(nc_handle* h, const double* x_host, double* y_host);
@@ -150,7 +165,8 @@ int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x
 int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* value);
 
 /* Counters and the last matvec's per-stage device times.  nc_time_stages(h, 1) makes the next
- * matvecs record per-stage CUDA events (adds event overhead; off by default). */
+ * matvecs record per-stage CUDA events on the matvec's stream (no host synchronisation inside nc_matvec);
+ * nc_stats waits for the last recorded matvec's events and converts them to ms_last. */
 int nc_stats(const nc_handle* h, nc_stats_t* out);
 int nc_time_stages(nc_handle* h, int enable);
 

@@ -196,7 +196,7 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   }
   if (opt->check_separation) NC_TRY(check_separation(centers, N, eps));
 #if !NC_WITH_NCCL
-  if (opt->world > 1) return fail(NC_EUNSUP, "nc_setup: world > 1 needs a build with NCCL");
+  if (opt->world > 1 && opt->nccl_id) return fail(NC_EUNSUP, "nc_setup: world > 1 needs a build with NCCL");
 #endif
 
   nc_handle* h = new nc_handle();
@@ -320,9 +320,9 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   }
   if ((rc = ensure_red(h, 4096))) return bail(rc);
 
+  h->emulated = h->world > 1 && !opt->nccl_id;   // rank emulation: no communicator, nc_matvec_emulated only
 #if NC_WITH_NCCL
-  if (h->world > 1) {
-    if (!opt->nccl_id) return bail(fail(NC_EINVAL, "nc_setup: world > 1 needs nccl_id"));
+  if (h->world > 1 && !h->emulated) {
     ncclUniqueId id;
     memcpy(&id, opt->nccl_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&h->comm, h->world, id, h->rank);
@@ -358,21 +358,51 @@ static inline void mark(nc_handle* h, int i, cudaStream_t s) {
   if (h->time_stages) cudaEventRecord(h->ev[i], s);
 }
 
-int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
-  if (!h || !x || !y) return fail(NC_EINVAL, "nc_matvec: null argument");
-  if (x == y) return fail(NC_EINVAL, "nc_matvec: x and y must not alias");
-  NC_CUDA_TRY(cudaSetDevice(h->device));
-  cudaStream_t s = (cudaStream_t)stream;
-  const int K = h->K, p = h->p, Ks = h->Kstar;
-  mark(h, 0, s);
-  // K1: rho_i = T_k fhat_i for this rank's rows and every rung in use, written into the records' 4th slot
+// K1 for rows [r0, r0 + nr) of the internal order (x points at row r0): rho_i = T_k fhat_i for every rung in use,
+// written into the records' 4th slot
+static void outgoing(nc_handle* h, const double* x, int64_t r0, int64_t nr, cudaStream_t s) {
+  const int K = h->K;
   for (int k = 0; k < h->nrung; ++k) {
     if (!h->rung_used[k]) continue;
     const int pk = h->rung_p[k];
-    launch_gemm_dmma(x, K, 1, 0, h->d_T + (size_t)h->rung_trow[k] * K, h->row_count, pk, K,
-                     h->d_src4 + h->rung_soff[k] + (size_t)h->row_begin * pk * 4 + 3, (int64_t)pk * 4, 4, nullptr, 0,
-                     s);
+    launch_gemm_dmma(x, K, 1, 0, h->d_T + (size_t)h->rung_trow[k] * K, nr, pk, K,
+                     h->d_src4 + h->rung_soff[k] + (size_t)r0 * pk * 4 + 3, (int64_t)pk * 4, 4, nullptr, 0, s);
+    h->launches_last++;
   }
+}
+
+// everything after the source records are complete: pair sums (direct) or steps 2-4 (hier), then step 5
+static int matvec_tail(nc_handle* h, const double* x, double* y, cudaStream_t s) {
+  const int K = h->K, p = h->p, Ks = h->Kstar;
+  mark(h, 2, s);
+  if (h->mode == NC_DIRECT) {
+    launch_pairs_direct(h->kind, h->pair_tpt, h->d_tx, h->d_ty, h->d_tz, h->row_count * Ks, Ks, h->row_begin, h->d_src4, p, h->N,
+                        h->nseg, h->d_upart, s);
+    mark(h, 3, s);
+    // K3: Y = X + (sum_seg U_seg) P^T
+    launch_gemm_dmma(h->d_upart, Ks, h->nseg, h->row_count * Ks, h->d_P, h->row_count, K, Ks, y, K, 1, x, K, s);
+    h->launches_last += 2;
+    mark(h, 4, s);
+  } else {
+    NC_TRY(hier_matvec(h, x, y, s));   // records ev[3] right after its pair kernel, ev[7] before step 5, ev[4] at the end
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "nc_matvec launch");
+  h->stages_pending = h->time_stages;
+  h->matvecs++;
+  return NC_OK;
+}
+
+int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
+  if (!h || !x || !y) return fail(NC_EINVAL, "nc_matvec: null argument");
+  if (x == y) return fail(NC_EINVAL, "nc_matvec: x and y must not alias");
+  if (h->world > 1 && h->emulated)
+    return fail(NC_ESTATE, "nc_matvec: emulated rank (no communicator): use nc_matvec_emulated");
+  NC_CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  h->launches_last = 0;
+  mark(h, 0, s);
+  outgoing(h, x, h->row_begin, h->row_count, s);
   mark(h, 1, s);
   if (h->world > 1) {
 #if NC_WITH_NCCL
@@ -392,34 +422,40 @@ int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
       return fail(NC_ENCCL, std::string("all-gather (broadcasts): ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
 #endif
   }
-  mark(h, 2, s);
+  return matvec_tail(h, x, y, s);
+}
+
+int nc_matvec_emulated(nc_handle* h, const double* x_all, double* y, void* stream) {
+  if (!h || !x_all || !y) return fail(NC_EINVAL, "nc_matvec_emulated: null argument");
+  NC_CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  h->launches_last = 0;
+  mark(h, 0, s);
+  outgoing(h, x_all, 0, h->N, s);   // every rank's rows: stands in for the all-gather of the records
+  mark(h, 1, s);
+  const double* xl = x_all + (size_t)h->row_begin * h->K;
+  if (xl == y) return fail(NC_EINVAL, "nc_matvec_emulated: y aliases x");
+  return matvec_tail(h, xl, y, s);
+}
+
+// per-stage device times of the last timed matvec (waits for its events)
+static int read_stages(nc_handle* h) {
+  if (!h->stages_pending) return NC_OK;
+  h->stages_pending = false;
+  NC_CUDA_TRY(cudaEventSynchronize(h->ev[4]));
+  float ms;
+  for (double& v : h->ms_last) v = 0.0;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]); h->ms_last[0] = ms;
+  cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]); h->ms_last[1] = ms;
   if (h->mode == NC_DIRECT) {
-    launch_pairs_direct(h->kind, h->pair_tpt, h->d_tx, h->d_ty, h->d_tz, h->row_count * Ks, Ks, h->row_begin, h->d_src4, p, h->N,
-                        h->nseg, h->d_upart, s);
-    mark(h, 3, s);
-    // K3: Y = X + (sum_seg U_seg) P^T
-    launch_gemm_dmma(h->d_upart, Ks, h->nseg, h->row_count * Ks, h->d_P, h->row_count, K, Ks, y, K, 1, x, K, s);
-    mark(h, 4, s);
+    cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); h->ms_last[2] = ms;
+    cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]); h->ms_last[3] = ms;
   } else {
-    NC_TRY(hier_matvec(h, x, y, s));
+    cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); h->ms_last[4] = ms;   // k_pairs_grid (steps 2-3)
+    cudaEventElapsedTime(&ms, h->ev[3], h->ev[7]); h->ms_last[5] = ms;   // reduce, transform, near list, step 4
+    cudaEventElapsedTime(&ms, h->ev[7], h->ev[4]); h->ms_last[3] = ms;   // step 5 (P-apply GEMM)
   }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "nc_matvec launch");
-  if (h->time_stages) {
-    NC_CUDA_TRY(cudaEventSynchronize(h->ev[4]));
-    float ms;
-    cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]); h->ms_last[0] = ms;
-    cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]); h->ms_last[1] = ms;
-    if (h->mode == NC_DIRECT) {
-      cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); h->ms_last[2] = ms;
-      cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]); h->ms_last[3] = ms;
-    } else {
-      cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); h->ms_last[4] = ms;   // steps 2-3 (grids)
-      cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]); h->ms_last[5] = ms;   // transform, near, step 4, step 5
-    }
-    cudaEventElapsedTime(&ms, h->ev[0], h->ev[4]); h->ms_last[6] = ms;
-  }
-  h->matvecs++;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[4]); h->ms_last[6] = ms;
   return NC_OK;
 }
 
@@ -450,6 +486,7 @@ static int dots(nc_handle* h, const double* V, int64_t ldv, int nv, const double
 int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x, int* iters, double* hist,
              void* stream) {
   if (!h || !x || max_iter < 1 || !(rtol > 0)) return fail(NC_EINVAL, "nc_gmres: bad arguments");
+  if (h->world > 1 && h->emulated) return fail(NC_ESTATE, "nc_gmres: emulated rank has no communicator");
   NC_CUDA_TRY(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = h->row_count * h->K;
@@ -505,13 +542,25 @@ int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x
     double* w = V + (size_t)(j + 1) * ldv;
     NC_TRY(nc_matvec(h, V + (size_t)j * ldv, w, s));
     // CGS2: two classical Gram-Schmidt passes
+    if (h->time_stages) NC_CUDA_TRY(cudaEventRecord(h->ev[5], s));
     NC_TRY(dots(h, V, ldv, j + 1, w, n, d_h1, s));
     launch_gemv_sub(V, ldv, j + 1, d_h1, w, n, s);
     NC_TRY(dots(h, V, ldv, j + 1, w, n, d_h2, s));
     launch_gemv_sub(V, ldv, j + 1, d_h2, w, n, s);
     NC_TRY(dots(h, w, ldv, 1, w, n, d_nrm, s));
+    if (h->time_stages) NC_CUDA_TRY(cudaEventRecord(h->ev[6], s));
     NC_CUDA_TRY(cudaMemcpyAsync(h->h_red, h->d_red, 1281 * sizeof(double), cudaMemcpyDeviceToHost, s));
     NC_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h->time_stages) {
+      // HBM-bound orthogonalisation (K9): algorithmic bytes = two (multidot + gemv_sub) passes + the norm, with
+      // multidot re-reading w once per group of 8 basis vectors
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, h->ev[5], h->ev[6]);
+      const double nv = j + 1;
+      h->gmres_ortho_ms += ms;
+      h->gmres_ortho_bytes += 8.0 * (double)n * (2.0 * (nv + std::ceil(nv / 8.0)) + 2.0 * (nv + 2.0) + 1.0);
+      h->gmres_ortho_iters++;
+    }
     for (int i = 0; i <= j; ++i) Hc(i, j) = h->h_red[i] + h->h_red[640 + i];
     double hn = sqrt(std::max(0.0, h->h_red[1280]));
     Hc(j + 1, j) = hn;
@@ -558,6 +607,7 @@ int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x
 
 int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* value) {
   if (!h || !x) return fail(NC_EINVAL, "nc_flux_or_mfpt: null argument");
+  if (h->world > 1 && h->emulated) return fail(NC_ESTATE, "nc_flux_or_mfpt: emulated rank has no communicator");
   NC_CUDA_TRY(cudaSetDevice(h->device));
   cudaStream_t s = h->stream;
   NC_TRY(ensure_red(h, std::max<int64_t>(4096, 1024 + (int64_t)592 * h->K + 16)));
@@ -584,6 +634,7 @@ int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* valu
 
 int nc_stats(const nc_handle* h, nc_stats_t* o) {
   if (!h || !o) return fail(NC_EINVAL, "nc_stats: null argument");
+  NC_TRY(read_stages(const_cast<nc_handle*>(h)));
   memset(o, 0, sizeof(*o));
   o->N = h->N;
   o->row_begin = h->row_begin;
@@ -602,6 +653,10 @@ int nc_stats(const nc_handle* h, nc_stats_t* o) {
   o->gemm_flops_per_matvec = 2.0 * h->row_count * (psum * h->K + (double)h->K * h->Kstar);
   for (int i = 0; i < 8; ++i) o->ms_last[i] = h->ms_last[i];
   o->device_bytes = h->device_bytes;
+  o->launches_per_matvec = h->launches_last;
+  o->gmres_ortho_ms = h->gmres_ortho_ms;
+  o->gmres_ortho_bytes = h->gmres_ortho_bytes;
+  o->gmres_ortho_iters = h->gmres_ortho_iters;
   hier_fill_stats(h, o);
   return NC_OK;
 }

@@ -10,7 +10,10 @@
 // step-5 GEMM's operand load (gemm.cu), deterministic.
 #include <stdlib.h>
 
+#include <stdio.h>
+
 #include <algorithm>
+#include <type_traits>
 
 #include "pairs.cuh"
 
@@ -89,23 +92,25 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
 // ------------------------------------------------------------------------------------------------
 // hierarchical mode: interaction-list / leaf-neighbour sources on incoming grids
 // ------------------------------------------------------------------------------------------------
-template <int KIND, bool LDG>
+// One CTA of kGridThreads threads per work unit: <= kGridThreads * TPT adjacent points of one incoming grid x one
+// slice (<= kSliceMax patches, one outgoing-operator rung) of its source list.  Sources are staged in shared memory
+// `chp` patches at a time; the log table is double2 (LOG8 = false) or the 8-byte table of green.cuh (LOG8 = true).
+template <int KIND, int TPT, int UNROLL, bool LOG8, bool FAR>
 __global__ void __launch_bounds__(kGridThreads) k_pairs_grid(const GridUnit* __restrict__ units,
                                                               const double* __restrict__ gx,
                                                               const double* __restrict__ gy,
                                                               const double* __restrict__ gz,
                                                               const int32_t* __restrict__ srclist,
-                                                              const double* __restrict__ src4,
+                                                              const double* __restrict__ src4, int stage_records,
                                                               double* __restrict__ part,
-                                                              const double2* __restrict__ logsrc) {
+                                                              const void* __restrict__ logsrc) {
+  using Tab = typename std::conditional<LOG8, double, double2>::type;
   extern __shared__ double4 sm[];
-  __shared__ double2 logtab[kLogTableSize];
+  __shared__ Tab logtab[kLogTableSize];
   __shared__ int64_t pid[kStagePatchesMax];
-  init_log_table(logtab, logsrc);
+  init_table(logtab, reinterpret_cast<const Tab*>(logsrc));
   const GridUnit U = units[blockIdx.x];
-  constexpr int TPT = kGridUnitPoints / kGridThreads;
-  double x[TPT], y[TPT], z[TPT], acc[TPT];
-  int64_t excl[TPT];
+  double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
   // adjacent points per thread (l = TPT t + u): a partial chunk leaves at most one partially idle warp
   const bool any = (int)(TPT * threadIdx.x) < U.npt;
 #pragma unroll
@@ -113,24 +118,22 @@ __global__ void __launch_bounds__(kGridThreads) k_pairs_grid(const GridUnit* __r
     const int l = TPT * threadIdx.x + u;
     const int64_t g = U.pt0 + min(l, U.npt - 1);
     x[u] = gx[g]; y[u] = gy[g]; z[u] = gz[g];
-    excl[u] = -1;
+    cq[u] = fma(x[u], x[u], fma(y[u], y[u], fma(z[u], z[u], 0.25)));
+    if (FAR) { x[u] *= -2.0; y[u] *= -2.0; z[u] *= -2.0; }
     acc[u] = 0.0;
   }
   const int32_t* __restrict__ lst = srclist + U.src0;
   const double4* __restrict__ s4 = reinterpret_cast<const double4*>(src4 + U.soff);   // the unit's rung
-  if (LDG) {
-    __syncthreads();
-    if (any)
-      accumulate_list_ldg<KIND, TPT>(x, y, z, excl, acc, U.nsrc, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
-                                     s4, U.p, logtab);
-  } else {
-    accumulate_list<KIND, TPT>(x, y, z, excl, acc, U.nsrc, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
-                               s4, U.p, sm, pid, stage_patches(U.p), logtab, any);
-  }
+  int chp = stage_records / U.p;
+  chp = chp < 1 ? 1 : (chp > kStagePatchesMax ? kStagePatchesMax : chp);
+  accumulate_grid<KIND, TPT, UNROLL, FAR, Tab>(x, y, z, cq, acc, U.nsrc,
+                                               [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p, sm, pid,
+                                               chp, logtab, any);
+  const int upts = kGridThreads * TPT;
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
     const int l = TPT * threadIdx.x + u;
-    if (l < U.npt) part[(int64_t)blockIdx.x * kGridUnitPoints + l] = acc[u];
+    if (l < U.npt) part[(int64_t)blockIdx.x * upts + l] = acc[u];
   }
 }
 
@@ -143,21 +146,52 @@ static bool stage_ldg() {
   return v == 1;
 }
 
+// grid-kernel variant: NC_GRID_VARIANT="TPT,UNROLL,LOG8,STAGE" (default kGridVariantDefault)
+static GridVariant grid_variant() {
+  static GridVariant v = {0, 0, 0, 0, 0};
+  if (v.tpt == 0) {
+    v = kGridVariantDefault;
+    if (const char* e = getenv("NC_GRID_VARIANT")) {
+      GridVariant w = v;
+      const int n = sscanf(e, "%d,%d,%d,%d,%d", &w.tpt, &w.unroll, &w.log8, &w.stage, &w.far);
+      if (n >= 4 && (w.tpt == 2 || w.tpt == 4) && (w.unroll == 1 || w.unroll == 2 || w.unroll == 4) &&
+          (w.log8 == 0 || w.log8 == 1) && w.stage >= 32 && (w.far == 0 || w.far == 1))
+        v = w;
+    }
+  }
+  return v;
+}
+
+int grid_far_variant() { return grid_variant().far; }
+
+int grid_unit_points() { return kGridThreads * grid_variant().tpt; }
+
+template <int KIND, int TPT, int UNROLL, bool LOG8, bool FAR>
+static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* gx, const double* gy, const double* gz,
+                          const int32_t* srclist, const double* src4, int stage, size_t smem, double* part,
+                          cudaStream_t s) {
+  const void* tab = LOG8 ? (const void*)log8_table_device() : (const void*)log_table_device();
+  auto kern = k_pairs_grid<KIND, TPT, UNROLL, LOG8, FAR>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<(unsigned)nunits, kGridThreads, smem, s>>>(units, gx, gy, gz, srclist, src4, stage, part, tab);
+}
+
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
                        const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
                        cudaStream_t s) {
   if (nunits <= 0) return;
-  const bool ldg = stage_ldg();
-  const size_t smem = ldg ? 0 : (size_t)std::max(512, pmax) * sizeof(double4);   // >= stage_patches(p) * p
-#define NC_LAUNCH_G(KD, LD)                                                                                     \
-  k_pairs_grid<KD, LD><<<(unsigned)nunits, kGridThreads, smem, s>>>(units, gx, gy, gz, srclist, src4, part,       \
-                                                                    log_table_device())
-  if (kind == NC_EXTERIOR) {
-    if (ldg) NC_LAUNCH_G(1, true); else NC_LAUNCH_G(1, false);
-  } else {
-    if (ldg) NC_LAUNCH_G(0, true); else NC_LAUNCH_G(0, false);
-  }
-#undef NC_LAUNCH_G
+  const GridVariant v = grid_variant();
+  const size_t smem = (size_t)std::max(v.stage, pmax) * sizeof(double4);   // >= chp * p and >= one whole patch
+#define NC_G(KD, TP, UR, L8, FR) \
+  if (kind == KD && v.tpt == TP && v.unroll == UR && v.log8 == L8 && v.far == FR) \
+    return launch_grid_t<KD, TP, UR, L8, FR>(units, nunits, gx, gy, gz, srclist, src4, std::max(v.stage, pmax), smem, part, s);
+#define NC_GK(KD) \
+  NC_G(KD, 2, 2, 0, 0) NC_G(KD, 2, 4, 0, 0) NC_G(KD, 2, 2, 0, 1) NC_G(KD, 2, 4, 0, 1) NC_G(KD, 2, 1, 0, 1) \
+  NC_G(KD, 4, 2, 0, 0) NC_G(KD, 4, 2, 0, 1) NC_G(KD, 2, 4, 1, 0)
+  NC_GK(0)
+  NC_GK(1)
+#undef NC_GK
+#undef NC_G
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -50,6 +50,17 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
   return fma(ye, c, y);
 }
 
+// far-field rsqrt: the MUFU.RSQ64H seed and ONE Newton step (y + (y/2)(1 - x y^2); y/2 by an exponent decrement on
+// the integer pipe): 3 FP64-pipe instructions instead of 5; relative error ~ (3/2) e0^2 for a seed error e0
+// (measured in tests/test_hier_gpu.py through the whole matvec; used only by k_pairs_grid's FAR variant)
+__device__ __forceinline__ double fast_rsqrt_far(double x) {
+  const double y = rsqrt_approx(x);
+  const double t = x * y;
+  const double e = fma(-t, y, 1.0);
+  const double h = __hiloint2double(__double2hiint(y) - 0x00100000, __double2loint(y));
+  return fma(h, e, y);
+}
+
 // fp64 natural log for positive normal x (absolute error ~1e-16 |log x| + 1e-17)
 __device__ __forceinline__ double fast_log(double x, const double2* __restrict__ tbl) {
   const int hi = __double2hiint(x);
@@ -69,10 +80,54 @@ __device__ __forceinline__ double fast_log(double x, const double2* __restrict__
   return h + l1;
 }
 
+// 8-byte-table variant: c_j is not stored but recomputed from j in two integer ops around one fp32 MUFU.RCP,
+//   c_j = fp32 rcp.approx(1 + (j + 1/2)/1024) truncated to 15 mantissa bits (exact as a double, low word 0),
+// and the table holds only -log c_j (fp64, built on the device by the same instruction sequence and converted
+// on the host in long double: log8_table_device).  |r| = |m c_j - 1| <= 2^-11 + 2^-15 (truncation r^5/5 < 1e-17).
+// Halves the shared-memory bytes per lookup (one LDS.64 instead of one LDS.128: fewer bank-conflict wavefronts).
+__device__ __forceinline__ double log8_c(int j) {
+  const unsigned fb = 0x3F800000u | ((unsigned)j << (23 - kLogTableBits)) | (1u << (22 - kLogTableBits));
+  float c;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(__uint_as_float(fb)));
+  const unsigned cb = __float_as_uint(c) & 0xFFFFFF00u;
+  return __hiloint2double((int)((cb >> 3) + 0x38000000u), 0);
+}
+
+__device__ __forceinline__ double fast_log(double x, const double* __restrict__ tbl) {
+  const int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  const int j = (hi >> (20 - kLogTableBits)) & (kLogTableSize - 1);
+  const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
+  const double kd = __hiloint2double(0x43300000, (int)(((unsigned)hi >> 20) - 1023u + 0x80000000u)) -
+                    4503601774854144.0;   // 2^52 + 2^31
+  const double r = fma(m, log8_c(j), -1.0);
+  double p = fma(r, -0.25, 0.33333333333333333333);
+  p = fma(p, r, -0.5);
+  const double r2 = r * r;
+  const double l1 = fma(r2, p, r);
+  const double h = fma(kd, kLn2, tbl[j]);
+  return h + l1;
+}
+const double* log8_table_device();   // host: -log c_j of log8_c, uploaded once per device; nullptr on failure
+
+template <class Tab>
+__device__ __forceinline__ void init_table(Tab* tbl, const Tab* __restrict__ src) {
+  for (int j = threadIdx.x; j < kLogTableSize; j += blockDim.x) tbl[j] = src[j];
+}
+
 // G for scaled coordinates: q = |x - x'|^2 / 4  (KIND 1 = exterior G_E, KIND 0 = interior G_I)
-template <int KIND>
-__device__ __forceinline__ double green_q(double q, const double2* __restrict__ tbl) {
+template <int KIND, class Tab>
+__device__ __forceinline__ double green_q(double q, const Tab* __restrict__ tbl) {
   const double w = fast_rsqrt(q);   // 2/d
+  const double a = 1.0 + w;
+  if (KIND == 1) return w - fast_log(a, tbl);
+  return w - fast_log(q * a, tbl);
+}
+
+// far-field G (k_pairs_grid FAR variant): one-Newton rsqrt, same table log
+template <int KIND, class Tab>
+__device__ __forceinline__ double green_q_far(double q, const Tab* __restrict__ tbl) {
+  const double w = fast_rsqrt_far(q);
   const double a = 1.0 + w;
   if (KIND == 1) return w - fast_log(a, tbl);
   return w - fast_log(q * a, tbl);

@@ -35,7 +35,7 @@ namespace nc {
 constexpr int kLmax = 24;
 constexpr int kSliceMax = 32;          // source patches per grid work unit
 constexpr double kBetaMin = 1.45;      // smallest source distance / circle radius served by a grid
-constexpr double kGridTolFactor = 300.0;  // per-grid tolerance / requested precision (calibrated: DESIGN.md R21)
+constexpr double kGridTolFactor = 1000.0;  // per-grid tolerance / requested precision (calibrated: DESIGN.md R21)
 
 struct ChunkRec {
   int64_t pt0;
@@ -60,7 +60,7 @@ struct HierState {
   std::vector<int32_t> gnr, gna;
   std::vector<int64_t> goff, coff;
   int64_t Q = 0, C = 0;
-  int qmax = 0, cmax = 0, pmax = 0;
+  int qmax = 0, cmax = 0, pmax = 0, namax = 0, nrmax = 0;
   std::vector<int32_t> grid_groups;
   // device
   int64_t* d_keys = nullptr;
@@ -72,6 +72,7 @@ struct HierState {
   double *d_gx = nullptr, *d_gy = nullptr, *d_gz = nullptr, *d_gval = nullptr, *d_gcoef = nullptr;
   GridUnit* d_units = nullptr;
   int64_t nunits = 0;
+  int upts = 256;                   // grid points per work unit (grid_unit_points())
   int32_t* d_srclist = nullptr;
   double* d_part = nullptr;
   ChunkRec* d_chunks = nullptr;
@@ -360,18 +361,22 @@ __global__ void k_grid_points(const int32_t* __restrict__ groups, int64_t ngr, c
 }
 
 __global__ void k_reduce_chunks(const ChunkRec* __restrict__ ch, int64_t nch, const double* __restrict__ part,
-                                double* __restrict__ gval) {
+                                int upts, double* __restrict__ gval) {
   const int64_t c = blockIdx.x;
   if (c >= nch) return;
   const ChunkRec R = ch[c];
   for (int t = threadIdx.x; t < R.npt; t += blockDim.x) {
     double v = 0.0;
-    for (int s = 0; s < R.nu; ++s) v += part[(R.u0 + s) * kGridUnitPoints + t];
+    for (int s = 0; s < R.nu; ++s) v += part[(R.u0 + s) * upts + t];
     gval[R.pt0 + t] = v;
   }
 }
 
-// samples (n_r x n_a, radius-major) -> coefficients, layout ((m * 2 + cs) * n_r + j), n = (m & 1) + 2 j
+// step 4a: samples f(r_k, theta_l) (n_r x n_a, radius-major) -> parity-restricted
+// Chebyshev-Fourier coefficients c[m][j][cs], layout ((m * n_r + j) * 2 + cs), n = (m & 1) + 2 j:
+//   Fourier:   AB[k][m][cs] = (2 - delta) / n_a  sum_l f(r_k, theta_l) {cos, sin}(2 pi m l / n_a)
+//   Chebyshev: c[m][j][cs]  = (2 - delta_n0) / n_r sum_k AB[k][m][cs] cos(n pi (2k + 1) / (4 n_r))
+// Twiddles are tabulated once per group in shared memory (exact index reduction, no per-term sincos).
 __global__ void k_transform(const int32_t* __restrict__ groups, int64_t ngr, const int32_t* __restrict__ gnr,
                             const int32_t* __restrict__ gna, const int64_t* __restrict__ goff,
                             const int64_t* __restrict__ coff, const double* __restrict__ gval,
@@ -380,17 +385,22 @@ __global__ void k_transform(const int32_t* __restrict__ groups, int64_t ngr, con
   const int g = groups[blockIdx.x];
   const int nr = gnr[g], na = gna[g], M = na / 2;
   double* f = sh;                      // nr * na
-  double* AB = sh + nr * na;           // nr * (M+1) * 2
+  double* AB = f + nr * na;            // nr * (M+1) * 2
+  double* tw = AB + nr * (M + 1) * 2;  // 2 * na: (cos, sin)(2 pi r / na)
+  double* ch = tw + 2 * na;            // 8 * nr: cos(pi r / (4 nr))
   for (int t = threadIdx.x; t < nr * na; t += blockDim.x) f[t] = gval[goff[g] + t];
+  for (int t = threadIdx.x; t < na; t += blockDim.x) sincospi(2.0 * t / na, &tw[2 * t + 1], &tw[2 * t]);
+  for (int t = threadIdx.x; t < 8 * nr; t += blockDim.x) ch[t] = cospi((double)t / (4.0 * nr));
   __syncthreads();
   for (int t = threadIdx.x; t < nr * (M + 1) * 2; t += blockDim.x) {
     const int k = t / ((M + 1) * 2), rem = t % ((M + 1) * 2), m = rem >> 1, cs = rem & 1;
+    const double* fk = f + k * na;
     double s = 0.0;
+    int r = 0;
     for (int l = 0; l < na; ++l) {
-      const int r = (m * l) % na;
-      double sv, cv;
-      sincospi(2.0 * r / na, &sv, &cv);
-      s = fma(f[k * na + l], cs ? sv : cv, s);
+      s = fma(fk[l], tw[2 * r + cs], s);
+      r += m;
+      if (r >= na) r -= na;
     }
     double scale = (m == 0 || 2 * m == na) ? 1.0 / na : 2.0 / na;
     if (cs && (m == 0 || 2 * m == na)) scale = 0.0;
@@ -398,12 +408,15 @@ __global__ void k_transform(const int32_t* __restrict__ groups, int64_t ngr, con
   }
   __syncthreads();
   for (int t = threadIdx.x; t < (M + 1) * 2 * nr; t += blockDim.x) {
-    const int mc = t / nr, j = t % nr, m = mc >> 1, cs = mc & 1;
+    const int m = t / (2 * nr), rem = t % (2 * nr), j = rem >> 1, cs = rem & 1;
     const int n = (m & 1) + 2 * j;
+    const int P = 8 * nr, step = (2 * n) % P;
+    int idx = n % P;                                   // n (2k + 1) mod 8 n_r, exactly reduced
     double s = 0.0;
     for (int k = 0; k < nr; ++k) {
-      const int r = (n * (2 * k + 1)) % (8 * nr);   // cos(n pi (2k+1) / (4 nr)) exactly reduced
-      s = fma(AB[(k * (M + 1) + m) * 2 + cs], cospi((double)r / (4.0 * nr)), s);
+      s = fma(AB[(k * (M + 1) + m) * 2 + cs], ch[idx], s);
+      idx += step;
+      if (idx >= P) idx -= P;
     }
     s *= 2.0 / nr;
     if (n == 0) s *= 0.5;
@@ -411,65 +424,89 @@ __global__ void k_transform(const int32_t* __restrict__ groups, int64_t ngr, con
   }
 }
 
-// step 4: u_i(node) = udir + sum over levels of the group's expansion at the node
-__global__ void k_interp(int L, int64_t rc, int Kstar, const int32_t* __restrict__ pgl, const double* __restrict__ F,
-                         const double* __restrict__ gR, const int32_t* __restrict__ gnr,
-                         const int32_t* __restrict__ gna, const int64_t* __restrict__ coff,
-                         const double* __restrict__ coef, const double* __restrict__ tx, const double* __restrict__ ty,
-                         const double* __restrict__ tz, const double* __restrict__ udir, double* __restrict__ u) {
-  extern __shared__ double cs_[];
+// step 4b: u_i(node) = udir + sum over levels of the level's group expansion at the node,
+//   u(x, theta) = sum_m sum_j c[m][j] . (cos m theta, sin m theta) T_{(m & 1) + 2 j}(rho / R)
+// (rho = geodesic distance from the cap centre).  One CTA per target patch, kInterpNpt nodes per thread; every
+// coefficient pair is one broadcast shared-memory load reused by the thread's nodes (independent FP64 chains).
+constexpr int kInterpNpt = 4;
+__global__ void __launch_bounds__(128) k_interp(int L, int64_t rc, int Kstar, const int32_t* __restrict__ pgl,
+                                                 const double* __restrict__ F, const double* __restrict__ gR,
+                                                 const int32_t* __restrict__ gnr, const int32_t* __restrict__ gna,
+                                                 const int64_t* __restrict__ coff, const double* __restrict__ coef,
+                                                 const double* __restrict__ tx, const double* __restrict__ ty,
+                                                 const double* __restrict__ tz, const double* __restrict__ udir,
+                                                 double* __restrict__ u) {
+  extern __shared__ double2 c2[];
+  constexpr int NPT = kInterpNpt;
   const int64_t i = blockIdx.x;
-  constexpr int NPT = 4;
   for (int kb = 0; kb < Kstar; kb += NPT * blockDim.x) {
-  double acc[NPT], px[NPT], py[NPT], pz[NPT];
-  int nn = 0;
-  for (int k = kb + threadIdx.x; k < Kstar && nn < NPT; k += blockDim.x, ++nn) {
-    const int64_t t = i * Kstar + k;
-    px[nn] = 2.0 * tx[t]; py[nn] = 2.0 * ty[t]; pz[nn] = 2.0 * tz[t];
-    acc[nn] = udir ? udir[t] : 0.0;
-  }
-  for (int lvl = 0; lvl <= L; ++lvl) {
-    const int g = pgl[(int64_t)lvl * rc + i];
-    const int nr = gnr[g], na = gna[g];
-    if (nr == 0) continue;   // block-uniform
-    const int M = na / 2, nc = (M + 1) * 2 * nr;
-    __syncthreads();
-    for (int t = threadIdx.x; t < nc; t += blockDim.x) cs_[t] = coef[coff[g] + t];
-    __syncthreads();
-    const double* r9 = F + 9 * (int64_t)g;
-    const double invR = 1.0 / gR[g];
-    for (int q = 0; q < nn; ++q) {
-      const double sx = r9[0] * px[q] + r9[1] * py[q] + r9[2] * pz[q];
-      const double sy = r9[3] * px[q] + r9[4] * py[q] + r9[5] * pz[q];
-      const double cz = r9[6] * px[q] + r9[7] * py[q] + r9[8] * pz[q];
-      const double rho = sqrt(sx * sx + sy * sy);
-      const double x = atan2(rho, cz) * invR;
-      const double c1 = rho > 0 ? sx / rho : 1.0, s1 = rho > 0 ? sy / rho : 0.0;
-      const double w2 = 4.0 * x * x - 2.0;
-      double cm = 1.0, sm = 0.0, cmm = c1, smm = -s1;   // cos/sin(m theta), (m-1)
-      double val = 0.0;
-      for (int m = 0; m <= M; ++m) {
-        const double* ca = cs_ + (m * 2) * nr;
-        const double* cb = ca + nr;
-        double t0 = (m & 1) ? x : 1.0;
-        double t1 = (m & 1) ? x * (4.0 * x * x - 3.0) : 2.0 * x * x - 1.0;
-        double A = ca[0] * t0, B = cb[0] * t0;
-        for (int j = 1; j < nr; ++j) {
-          A = fma(ca[j], t1, A);
-          B = fma(cb[j], t1, B);
-          const double t2 = fma(w2, t1, -t0);
-          t0 = t1;
-          t1 = t2;
-        }
-        val = fma(A, cm, fma(B, sm, val));
-        const double cn = 2.0 * c1 * cm - cmm, sn = 2.0 * c1 * sm - smm;
-        cmm = cm; smm = sm; cm = cn; sm = sn;
-      }
-      acc[q] += val;
+    double acc[NPT], px[NPT], py[NPT], pz[NPT];
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      const int k = min(kb + (int)threadIdx.x + q * (int)blockDim.x, Kstar - 1);
+      const int64_t t = i * Kstar + k;
+      px[q] = 2.0 * tx[t]; py[q] = 2.0 * ty[t]; pz[q] = 2.0 * tz[t];
+      acc[q] = udir ? udir[t] : 0.0;
     }
-  }
-  nn = 0;
-  for (int k = kb + threadIdx.x; k < Kstar && nn < NPT; k += blockDim.x, ++nn) u[i * Kstar + k] = acc[nn];
+    for (int lvl = 0; lvl <= L; ++lvl) {
+      const int g = pgl[(int64_t)lvl * rc + i];
+      const int nr = gnr[g], na = gna[g];
+      if (nr == 0) continue;   // block-uniform
+      const int M = na / 2, ncp = (M + 1) * nr;
+      __syncthreads();
+      const double2* __restrict__ src = reinterpret_cast<const double2*>(coef + coff[g]);
+      for (int t = threadIdx.x; t < ncp; t += blockDim.x) c2[t] = src[t];
+      __syncthreads();
+      const double* r9 = F + 9 * (int64_t)g;
+      const double invR = 1.0 / gR[g];
+      double x[NPT], w2[NPT], c1[NPT], s1[NPT], cm[NPT], sm[NPT], cmm[NPT], smm[NPT];
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) {
+        const double sx = r9[0] * px[q] + r9[1] * py[q] + r9[2] * pz[q];
+        const double sy = r9[3] * px[q] + r9[4] * py[q] + r9[5] * pz[q];
+        const double cz = r9[6] * px[q] + r9[7] * py[q] + r9[8] * pz[q];
+        const double rho = sqrt(sx * sx + sy * sy);
+        x[q] = atan2(rho, cz) * invR;
+        c1[q] = rho > 0 ? sx / rho : 1.0;
+        s1[q] = rho > 0 ? sy / rho : 0.0;
+        w2[q] = 4.0 * x[q] * x[q] - 2.0;
+        cm[q] = 1.0; sm[q] = 0.0; cmm[q] = c1[q]; smm[q] = -s1[q];   // cos/sin(m theta), (m - 1) theta
+      }
+      for (int m = 0; m <= M; ++m) {
+        const double2* __restrict__ cmj = c2 + m * nr;
+        double A[NPT], B[NPT], t0[NPT], t1[NPT];
+        const double2 c0 = cmj[0];
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) {
+          t0[q] = (m & 1) ? x[q] : 1.0;
+          t1[q] = (m & 1) ? x[q] * (4.0 * x[q] * x[q] - 3.0) : 2.0 * x[q] * x[q] - 1.0;
+          A[q] = c0.x * t0[q];
+          B[q] = c0.y * t0[q];
+        }
+        for (int j = 1; j < nr; ++j) {
+          const double2 c = cmj[j];
+#pragma unroll
+          for (int q = 0; q < NPT; ++q) {
+            A[q] = fma(c.x, t1[q], A[q]);
+            B[q] = fma(c.y, t1[q], B[q]);
+            const double t2 = fma(w2[q], t1[q], -t0[q]);
+            t0[q] = t1[q];
+            t1[q] = t2;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) {
+          acc[q] = fma(A[q], cm[q], fma(B[q], sm[q], acc[q]));
+          const double cn = 2.0 * c1[q] * cm[q] - cmm[q], sn = 2.0 * c1[q] * sm[q] - smm[q];
+          cmm[q] = cm[q]; smm[q] = sm[q]; cm[q] = cn; sm[q] = sn;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      const int k = kb + (int)threadIdx.x + q * (int)blockDim.x;
+      if (k < Kstar) u[i * Kstar + k] = acc[q];
+    }
   }
 }
 
@@ -793,6 +830,8 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       H->grid_groups.push_back((int32_t)g);
       H->qmax = std::max<int>(H->qmax, (int)q);
       H->cmax = std::max<int>(H->cmax, (int)c);
+      H->namax = std::max<int>(H->namax, H->gna[g]);
+      H->nrmax = std::max<int>(H->nrmax, H->gnr[g]);
     } else if (!rel[g]) {
       H->gnr[g] = 0;
       H->gna[g] = 0;
@@ -804,6 +843,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   H->C = H->coff[G];
 
   // work units (steps 2-3) and reduction chunks
+  H->upts = grid_unit_points();
   std::vector<GridUnit> units;
   std::vector<ChunkRec> chunks;
   std::vector<int32_t> srclist;
@@ -832,10 +872,10 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       H->pairs_grid += (double)q * ns * h->rung_p[rung];
       a = b;
     }
-    for (int64_t c0 = 0; c0 < q; c0 += kGridUnitPoints) {
+    for (int64_t c0 = 0; c0 < q; c0 += H->upts) {
       ChunkRec cr;
       cr.pt0 = H->goff[g] + c0;
-      cr.npt = (int32_t)std::min<int64_t>(kGridUnitPoints, q - c0);
+      cr.npt = (int32_t)std::min<int64_t>(H->upts, q - c0);
       cr.u0 = (int64_t)units.size();
       cr.nu = (int32_t)slices.size();
       chunks.push_back(cr);
@@ -919,7 +959,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_TRY(halloc(h, &H->d_gz, H->Q));
   NC_TRY(halloc(h, &H->d_gval, H->Q));
   NC_TRY(halloc(h, &H->d_gcoef, H->C));
-  NC_TRY(halloc(h, &H->d_part, (size_t)H->nunits * kGridUnitPoints));
+  NC_TRY(halloc(h, &H->d_part, (size_t)H->nunits * H->upts));
   NC_TRY(halloc(h, &H->d_tx, rc * Ks));
   NC_TRY(halloc(h, &H->d_ty, rc * Ks));
   NC_TRY(halloc(h, &H->d_tz, rc * Ks));
@@ -942,27 +982,38 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   // steps 2-3: interaction-list and leaf-neighbour sources on the incoming grids
   launch_pairs_grid(h->kind, H->d_units, H->nunits, H->d_gx, H->d_gy, H->d_gz, H->d_srclist, h->d_src4, H->pmax,
                     H->d_part, s);
-  if (H->nchunks) k_reduce_chunks<<<(unsigned)H->nchunks, 256, 0, s>>>(H->d_chunks, H->nchunks, H->d_part, H->d_gval);
+  h->launches_last += H->nunits > 0;
   if (h->time_stages) cudaEventRecord(h->ev[3], s);
+  if (H->nchunks) {
+    k_reduce_chunks<<<(unsigned)H->nchunks, 256, 0, s>>>(H->d_chunks, H->nchunks, H->d_part, H->upts, H->d_gval);
+    h->launches_last++;
+  }
   // step 4a: grid samples -> coefficients
   if (!H->grid_groups.empty()) {
-    const size_t shm = (size_t)(H->qmax + H->cmax) * sizeof(double);
+    const size_t shm = (size_t)(H->qmax + H->cmax + 2 * H->namax + 8 * H->nrmax) * sizeof(double);
+    if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(k_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     k_transform<<<(unsigned)H->grid_groups.size(), 128, shm, s>>>(H->d_grid_groups, (int64_t)H->grid_groups.size(),
                                                                    H->d_gnr, H->d_gna, H->d_goff, H->d_coff,
                                                                    H->d_gval, H->d_gcoef);
+    h->launches_last++;
   }
   // near lists at the Zernike nodes
   NC_CUDA_TRY(cudaMemsetAsync(H->d_udir, 0, (size_t)rc * Ks * sizeof(double), s));
   launch_pairs_near(h->kind, H->d_tx, H->d_ty, H->d_tz, Ks, H->d_work_near, H->nwork_near, H->d_near_off, H->d_near,
                     h->d_src4, h->p, H->d_udir, s);
+  h->launches_last += H->nwork_near > 0;
   // step 4b: interpolation to the Zernike nodes, summed over levels
   if (rc > 0) {
     const size_t shm = (size_t)std::max(H->cmax, 1) * sizeof(double);
+    if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     k_interp<<<(unsigned)rc, 128, shm, s>>>(H->L, rc, Ks, H->d_pgl, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna,
                                             H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u);
+    h->launches_last++;
   }
   // step 5: y = x + U P^T
+  if (h->time_stages) cudaEventRecord(h->ev[7], s);
   launch_gemm_dmma(H->d_u, Ks, 1, 0, h->d_P, rc, K, Ks, y, K, 1, x, K, s);
+  h->launches_last++;
   if (h->time_stages) cudaEventRecord(h->ev[4], s);
   return NC_OK;
 }

@@ -45,13 +45,19 @@ constexpr int kDefaultStageLdg = 0; // 1: pair kernels read sources via L1 broad
 struct HierState;
 
 constexpr int kGridThreads = 128;      // threads per CTA of the incoming-grid pair kernel
-constexpr int kGridUnitPoints = 256;   // grid points per work unit (2 per thread)
+// k_pairs_grid variant {targets per thread, source unroll, 8-byte log table, staged source records, far-field G}
+struct GridVariant {
+  int tpt, unroll, log8, stage, far;
+};
+#define kGridVariantDefault (GridVariant{2, 4, 0, 256, 1})
+int grid_far_variant();
+int grid_unit_points();                // grid points per work unit = kGridThreads x targets per thread
 
-struct GridUnit {      // <= 256 points of one incoming grid x one slice of that grid's source-patch list
+struct GridUnit {      // <= grid_unit_points() points of one incoming grid x one slice of its source-patch list
   int64_t pt0;         // first grid point (global grid-point index)
   int64_t src0;        // first entry in the source-patch list
   int64_t soff;        // offset (doubles) of the outgoing-operator rung's source records in d_src4
-  int32_t npt;         // points in this unit (<= kGridUnitPoints)
+  int32_t npt;         // points in this unit (<= grid_unit_points())
   int32_t nsrc;        // source patches in this unit
   int32_t p;           // skeleton size of the rung
   int32_t pad_;
@@ -64,6 +70,7 @@ struct GridUnit {      // <= 256 points of one incoming grid x one slice of that
 
 struct nc_handle {
   int kind = 0, mode = 0, device = 0, world = 1, rank = 0;
+  bool emulated = false;          // world > 1 without a communicator (nc_matvec_emulated; partition tests)
   int64_t N = 0, row_begin = 0, row_count = 0;
   std::vector<int64_t> rank_begin, rank_count;   // partition of the internal rows over all ranks
   int M = 0, K = 0, Kstar = 0, p = 0;
@@ -113,8 +120,13 @@ struct nc_handle {
 
   // per-stage timing
   bool time_stages = false;
+  bool stages_pending = false;    // events of the last matvec recorded, not yet read (nc_stats reads them)
   cudaEvent_t ev[8] = {};
   double ms_last[8] = {};
+  int launches_last = 0;          // kernels launched by the last nc_matvec
+  double gmres_ortho_ms = 0.0;    // GMRES CGS2 orthogonalisation device time / algorithmic bytes (time_stages on)
+  double gmres_ortho_bytes = 0.0;
+  int64_t gmres_ortho_iters = 0;
   int64_t matvecs = 0;
   double pairs_per_matvec = 0.0;
   double device_bytes = 0.0;

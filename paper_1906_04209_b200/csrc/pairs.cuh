@@ -23,12 +23,14 @@ __host__ __device__ inline int stage_patches(int p) {
 }
 
 // patch_at(k) -> patch index of the k-th list entry.  All threads of the CTA must call (barriers inside).
-template <int KIND, int TPT, class PatchAt>
+// UNROLL: source records in flight per target (independent FP64 chains = TPT x UNROLL); Tab: double2 (c_j, -log c_j)
+// or double (-log c_j, c_j recomputed: green.cuh log8_c).
+template <int KIND, int TPT, int UNROLL = 2, class Tab = double2, class PatchAt>
 __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
                                                 const int64_t (&excl)[TPT], double (&acc)[TPT], int64_t nlist,
                                                 PatchAt patch_at, const double4* __restrict__ s4, int p,
                                                 double4* __restrict__ sm, int64_t* __restrict__ sm_pid, int chp,
-                                                const double2* __restrict__ logtab, bool active) {
+                                                const Tab* __restrict__ logtab, bool active) {
   for (int64_t c0 = 0; c0 < nlist; c0 += chp) {
     const int nch = (int)min((int64_t)chp, nlist - c0);
     __syncthreads();
@@ -51,7 +53,7 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
       }
       if (none) continue;
       if (all) {
-#pragma unroll 2
+#pragma unroll UNROLL
         for (int m = 0; m < p; ++m) {
           const double4 s = sp[m];
 #pragma unroll
@@ -71,6 +73,47 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
             const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
             acc[u] = fma(s.w, green_q<KIND>(qd, logtab), acc[u]);
           }
+        }
+      }
+    }
+  }
+}
+
+// Incoming-grid variant (no self exclusion: grid sources never include the target's own patch).  FAR = false: the
+// exact kernel of accumulate_list.  FAR = true (far-field evaluation, hierarchical mode only): the squared distance
+// from the dot product, q = |X|^2 + 1/4 - 2 X.S with the target pre-scaled T = -2X (3 DFMA instead of 6 FP64 ops;
+// absolute error ~3e-16, i.e. relative ~1e-10 at the closest grid pairs q ~ eps^2/4, far below the hierarchical
+// tolerance) and the one-Newton rsqrt.  x/y/z hold T when FAR, and cq[u] = |X_u|^2 + 1/4.
+template <int KIND, int TPT, int UNROLL, bool FAR, class Tab, class PatchAt>
+__device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
+                                                const double (&cq)[TPT], double (&acc)[TPT], int64_t nlist,
+                                                PatchAt patch_at, const double4* __restrict__ s4, int p,
+                                                double4* __restrict__ sm, int64_t* __restrict__ sm_pid, int chp,
+                                                const Tab* __restrict__ logtab, bool active) {
+  for (int64_t c0 = 0; c0 < nlist; c0 += chp) {
+    const int nch = (int)min((int64_t)chp, nlist - c0);
+    __syncthreads();
+    if (threadIdx.x < nch) sm_pid[threadIdx.x] = patch_at(c0 + threadIdx.x);
+    __syncthreads();
+    for (int r = threadIdx.x; r < nch * p; r += blockDim.x) {
+      const int q = r / p;
+      sm[r] = s4[sm_pid[q] * p + (r - q * p)];
+    }
+    __syncthreads();
+    if (!active) continue;
+    const int nrec = nch * p;
+#pragma unroll UNROLL
+    for (int m = 0; m < nrec; ++m) {
+      const double4 s = sm[m];
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        if (FAR) {
+          const double qd = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
+          acc[u] = fma(s.w, green_q_far<KIND>(qd, logtab), acc[u]);
+        } else {
+          const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
+          const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
+          acc[u] = fma(s.w, green_q<KIND>(qd, logtab), acc[u]);
         }
       }
     }

@@ -49,10 +49,12 @@ class NcStats(ctypes.Structure):
                 ("ms_last", ctypes.c_double * 8), ("tree_levels", ctypes.c_int32), ("tree_groups", ctypes.c_int64),
                 ("hier_grid_pairs", ctypes.c_double), ("hier_near_pairs", ctypes.c_double),
                 ("hier_interp_terms", ctypes.c_double), ("hier_grid_points", ctypes.c_int64),
-                ("hier_grid_units", ctypes.c_int64), ("device_bytes", ctypes.c_double)]
+                ("hier_grid_units", ctypes.c_int64), ("device_bytes", ctypes.c_double),
+                ("launches_per_matvec", ctypes.c_int32), ("gmres_ortho_ms", ctypes.c_double),
+                ("gmres_ortho_bytes", ctypes.c_double), ("gmres_ortho_iters", ctypes.c_int64)]
 
 
-EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt", "nc_stats",
+EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt", "nc_stats",
            "nc_time_stages", "nc_tree_lists", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
 
 _lib = None
@@ -71,6 +73,7 @@ def load_library(path: str = LIB_PATH):
                            ctypes.POINTER(NcTables), ctypes.POINTER(NcOpts)]
     L.nc_partition.argtypes = [vp, _i64p, _i64p, _i64p]
     L.nc_matvec.argtypes = [vp, vp, vp, vp]
+    L.nc_matvec_emulated.argtypes = [vp, vp, vp, vp]
     L.nc_matvec_host.argtypes = [vp, _dp, _dp]
     L.nc_gmres.argtypes = [vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int), _dp, vp]
     L.nc_flux_or_mfpt.argtypes = [vp, vp, _dp, _dp]
@@ -181,6 +184,14 @@ class Handle:
         if y is None:
             y = torch.empty_like(x)
         _check(self._L.nc_matvec(self._h, _ptr(x), _ptr(y), _stream_ptr(stream)))
+        return y
+
+    def matvec_emulated(self, x_all, y=None, stream=None):
+        """Rank emulation (world > 1, no nccl_id): this rank's rows from the full internal-order input."""
+        import torch
+        if y is None:
+            y = torch.empty((self.row_count, x_all.shape[1]), dtype=x_all.dtype, device=x_all.device)
+        _check(self._L.nc_matvec_emulated(self._h, _ptr(x_all), _ptr(y), _stream_ptr(stream)))
         return y
 
     def matvec_host(self, x: np.ndarray) -> np.ndarray:

@@ -133,3 +133,46 @@ def test_per_level_outgoing_ladder_matches_direct_C2():
     assert rel(gpu_matvec(h1, x), yd) <= HIER_TOL
     assert rel(gpu_matvec(h0, x), yd) <= HIER_TOL
     assert h1.stats()["hier_grid_pairs"] < 0.8 * h0.stats()["hier_grid_pairs"]
+
+
+def test_hier_C5_full_size_sampled_rows_bench_config():
+    """C5 (N = 100,000, the bench.py workload) in exactly the configuration bench.py times (physical tables with
+    the per-level ladder, precision 1e-9, seeded x of bench.py): sampled output blocks against the oracle, which
+    computes those rows one by one by the brute-force direct sum."""
+    cfg = CONFIGS["C5"]
+    c = cfg.centers()
+    tab = _phys("C5")
+    x = random_coeffs(cfg.N, tab.K, 2000 + 5)
+    h = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_HIER, precision=cfg.precision)
+    y = gpu_matvec(h, x)
+    assert np.all(np.isfinite(y))
+    rows = np.random.default_rng(55).choice(cfg.N, 2, replace=False)
+    assert rel(y[rows], O.matvec(cfg.kind, c, tab, x, rows=rows)) <= HIER_TOL
+
+
+_FAR_CHILD = r"""
+import os, sys, numpy as np, torch
+sys.path.insert(0, os.environ["ROOT"])
+import paper_1906_04209_b200 as nc
+from nc_inputs import CONFIGS, random_coeffs
+from nc_inputs.tables import load_tables
+cfg = CONFIGS["C3"]
+tab = load_tables(os.path.join(os.environ["ROOT"], "tables", "data", "C3.npz"))
+h = nc.Handle(cfg.kind, cfg.centers(), cfg.eps, tab, mode=nc.NC_HIER, precision=cfg.precision)
+x = torch.from_numpy(h.to_internal(random_coeffs(cfg.N, tab.K, 2006))).cuda()
+np.save(os.environ["OUT"], h.matvec(x).cpu().numpy())
+"""
+
+
+def test_far_field_pair_variant_error(tmp_path):
+    """k_pairs_grid's far-field evaluation (dot-product distance + one-Newton rsqrt, R23) against the
+    exact pair kernel on the same grids (C3): the difference must stay far below the hierarchical precision."""
+    import subprocess
+    import sys
+    outs = []
+    for v in ("2,4,0,256,0", "2,4,0,256,1"):
+        out = str(tmp_path / f"y{v[-1]}.npy")
+        env = dict(os.environ, NC_GRID_VARIANT=v, ROOT=ROOT, OUT=out)
+        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=env, check=True, timeout=600)
+        outs.append(np.load(out))
+    assert rel(outs[1], outs[0]) <= 1e-11
