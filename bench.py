@@ -25,10 +25,6 @@ sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.txt")
-# FP64-pipe flops executed per pair by the pair kernels' inner loop (pairs.cuh / green.cuh): 2 per DFMA, 1 per
-# DMUL/DADD.  Exterior: 11 DFMA + 4 DMUL + 7 DADD = 33; interior adds one DMUL (q (1 + w)) = 34.
-# Cross-checked against ncu's sass_thread_inst_executed_op_{dfma,dmul,dadd} counts (profiles/).
-FP64_FLOPS_PER_PAIR = {0: 34, 1: 33}
 
 
 def parse():
@@ -61,7 +57,7 @@ def load_fp64_peak():
 
 
 # ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
-TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01b_ncu_full_pairs_grid.json"}
+TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01c_ncu_full_pairs_grid.json"}
 
 
 def profiled_traffic(kernel, config, mode):
@@ -311,7 +307,8 @@ def main():
     pair_ms = stages_avg[2] if args.mode == "direct" else stages_avg[4]
     pairs = st["pairs_per_matvec"] if args.mode == "direct" else st["hier_grid_pairs"]
     kname = "k_pairs_direct" if args.mode == "direct" else "k_pairs_grid"
-    fpp = FP64_FLOPS_PER_PAIR.get(cfg.kind)
+    fpp = st["pair_fp64_flops_direct"] if args.mode == "direct" else st["pair_fp64_flops_grid"]
+    ipp = st["pair_fp64_inst_direct"] if args.mode == "direct" else st["pair_fp64_inst_grid"]
     roof = None
     if pair_ms > 0 and fpp:
         ach = pairs * fpp / (pair_ms * 1e-3) / 1e12
@@ -319,10 +316,13 @@ def main():
         traffic, tsrc = profiled_traffic(kname, cfg.name, args.mode)
         roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                 "frac": (ach / peak) if peak else None, "traffic": traffic,
+                "fp64_flops_per_pair": fpp, "fp64_inst_per_pair": ipp,
+                "fp64_pipe_util": (pairs * ipp / (pair_ms * 1e-3)) / (peak * 1e12 / 2) if peak else None,
                 "kernel": kname, "kernel_ms": pair_ms, "kernel_share_of_step": pair_ms / (ms_total / args.steps),
-                "note": "FP64-pipe flops executed per pair (SASS count, 2 per DFMA) x pairs / kernel ms (CUDA events "
-                        "around the kernel in every timed step); peak = measured DFMA throughput "
-                        "(profiles/r01_fp64_peak.txt); traffic = DRAM bytes per launch from " + (tsrc or "no capture"),
+                "note": "FP64 flops executed per pair by the running variant (SASS count, 2 per DFMA; nc_stats) x pairs "
+                        "/ kernel ms (CUDA events around the kernel in every timed step); peak = measured DFMA "
+                        "throughput (profiles/r01_fp64_peak.txt, of measured); fp64_pipe_util = FP64 instructions / "
+                        "(peak / 2); traffic = DRAM bytes per launch from " + (tsrc or "no capture"),
                 "pairs_per_s": pairs / (pair_ms * 1e-3)}
     # the fp64 tensor-core GEMMs (K1 T-apply over the used rungs, K3 P-apply + identity): DMMA roofline
     kd = st["K"] * st["Kstar"] * 2.0 * st["row_count"]

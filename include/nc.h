@@ -111,6 +111,10 @@ typedef struct nc_stats_t {
   double gmres_ortho_ms;        /* GMRES CGS2 orthogonalisation device ms summed over the iterations */
   double gmres_ortho_bytes;     /*   run with nc_time_stages on, and its algorithmic HBM bytes       */
   int64_t gmres_ortho_iters;    /*   (iterations counted)                                          */
+  double pair_fp64_flops_direct; /* FP64 flops executed per pair (2 per DFMA, 1 per DMUL/DADD; SASS  */
+  double pair_fp64_inst_direct;  /*   count, verified with ncu) and FP64-pipe instructions per pair,  */
+  double pair_fp64_flops_grid;   /*   for the direct / near-list kernels and for k_pairs_grid's       */
+  double pair_fp64_inst_grid;    /*   variant in use (kind-dependent)                                */
 } nc_stats_t;
 
 typedef struct nc_handle nc_handle;
