@@ -354,7 +354,7 @@ def main():
             "stages_ms": dict(zip(["T_apply", "all_gather", "direct_pairs", "P_apply", "grid_pairs", "hier_rest",
                                    "total"], stages_avg)), "pairs_per_matvec": st["pairs_per_matvec"],
             "hier": ({k: st[k] for k in ("tree_levels", "tree_groups", "hier_grid_pairs", "hier_near_pairs",
-                                         "hier_interp_terms", "hier_grid_points", "hier_grid_units")}
+                                         "hier_interp_terms", "hier_grid_points", "hier_grid_units", "hier_grid_fill")}
                      if args.mode == "hier" else None),
             "solve": solve}
     print(json.dumps(line), flush=True)

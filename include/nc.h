@@ -115,6 +115,7 @@ typedef struct nc_stats_t {
   double pair_fp64_inst_direct;  /*   count, verified with ncu) and FP64-pipe instructions per pair,  */
   double pair_fp64_flops_grid;   /*   for the direct / near-list kernels and for k_pairs_grid's       */
   double pair_fp64_inst_grid;    /*   variant in use (kind-dependent)                                */
+  double hier_grid_fill;         /* NC_HIER: grid pairs / (work-unit thread slots x sources x p)     */
 } nc_stats_t;
 
 typedef struct nc_handle nc_handle;

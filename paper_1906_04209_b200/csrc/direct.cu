@@ -92,23 +92,19 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
 // ------------------------------------------------------------------------------------------------
 // hierarchical mode: interaction-list / leaf-neighbour sources on incoming grids
 // ------------------------------------------------------------------------------------------------
-// One CTA of kGridThreads threads per work unit: <= kGridThreads * TPT adjacent points of one incoming grid x one
-// slice (<= kSliceMax patches, one outgoing-operator rung) of its source list.  Sources are staged in shared memory
-// `chp` patches at a time; the log table is double2 (LOG8 = false) or the 8-byte table of green.cuh (LOG8 = true).
-template <int KIND, int TPT, int UNROLL, bool LOG8, bool FAR>
-__global__ void __launch_bounds__(kGridThreads) k_pairs_grid(const GridUnit* __restrict__ units,
-                                                              const double* __restrict__ gx,
-                                                              const double* __restrict__ gy,
-                                                              const double* __restrict__ gz,
-                                                              const int32_t* __restrict__ srclist,
-                                                              const double* __restrict__ src4, int stage_records,
-                                                              double* __restrict__ part,
-                                                              const void* __restrict__ logsrc) {
-  using Tab = typename std::conditional<LOG8, double, double2>::type;
+// One CTA of NT threads per work unit: <= NT * TPT adjacent points of one incoming grid x one slice (<= kSliceMax
+// patches, one outgoing-operator rung) of its source list.  Sources are staged in shared memory `chp` patches at a
+// time (a CTA barrier per stage); FAR selects the far-field arithmetic (pairs.cuh accumulate_grid, R23).
+template <int KIND, int NT, int TPT, int UNROLL, bool FAR, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restrict__ units, const double* __restrict__ gx,
+                                                   const double* __restrict__ gy, const double* __restrict__ gz,
+                                                   const int32_t* __restrict__ srclist,
+                                                   const double* __restrict__ src4, int stage_records,
+                                                   double* __restrict__ part, const double2* __restrict__ logsrc) {
   extern __shared__ double4 sm[];
-  __shared__ Tab logtab[kLogTableSize];
+  __shared__ double2 logtab[kLogTableSize];
   __shared__ int64_t pid[kStagePatchesMax];
-  init_table(logtab, reinterpret_cast<const Tab*>(logsrc));
+  init_table(logtab, logsrc);
   const GridUnit U = units[blockIdx.x];
   double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
   // adjacent points per thread (l = TPT t + u): a partial chunk leaves at most one partially idle warp
@@ -118,18 +114,65 @@ __global__ void __launch_bounds__(kGridThreads) k_pairs_grid(const GridUnit* __r
     const int l = TPT * threadIdx.x + u;
     const int64_t g = U.pt0 + min(l, U.npt - 1);
     x[u] = gx[g]; y[u] = gy[g]; z[u] = gz[g];
-    cq[u] = fma(x[u], x[u], fma(y[u], y[u], fma(z[u], z[u], 0.25)));
-    if (FAR) { x[u] *= -2.0; y[u] *= -2.0; z[u] *= -2.0; }
+    cq[u] = 0.5 * fma(x[u], x[u], fma(y[u], y[u], fma(z[u], z[u], 0.25)));
+    if (FAR) { x[u] = -x[u]; y[u] = -y[u]; z[u] = -z[u]; }
     acc[u] = 0.0;
   }
   const int32_t* __restrict__ lst = srclist + U.src0;
   const double4* __restrict__ s4 = reinterpret_cast<const double4*>(src4 + U.soff);   // the unit's rung
   int chp = stage_records / U.p;
   chp = chp < 1 ? 1 : (chp > kStagePatchesMax ? kStagePatchesMax : chp);
-  accumulate_grid<KIND, TPT, UNROLL, FAR, Tab>(x, y, z, cq, acc, U.nsrc,
-                                               [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p, sm, pid,
-                                               chp, logtab, any);
-  const int upts = kGridThreads * TPT;
+  accumulate_grid<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc,
+                                                   [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p, sm,
+                                                   pid, chp, logtab, any);
+  const int upts = NT * TPT;
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) {
+    const int l = TPT * threadIdx.x + u;
+    if (l < U.npt) part[(int64_t)blockIdx.x * upts + l] = acc[u];
+  }
+}
+
+// Same unit, sources streamed by cp.async.bulk into a two-buffer mbarrier pipeline (pairs.cuh accumulate_grid_tma):
+// no CTA barrier after the prologue; warps without an active point leave at once.  Measured slower than the staged
+// kernel at C5 (profiles/r01b_grid_variant_sweep*.jsonl): selectable (NC_GRID_VARIANT), not the default.
+template <int KIND, int NT, int TPT, int UNROLL, bool FAR, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_pairs_grid_tma(const GridUnit* __restrict__ units,
+                                                       const double* __restrict__ gx, const double* __restrict__ gy,
+                                                       const double* __restrict__ gz,
+                                                       const int32_t* __restrict__ srclist,
+                                                       const double* __restrict__ src4, int brec,
+                                                       double* __restrict__ part,
+                                                       const double2* __restrict__ logsrc) {
+  extern __shared__ __align__(128) double4 bufs[];
+  __shared__ double2 logtab[kLogTableSize];
+  __shared__ __align__(8) uint64_t bars[4];
+  const GridUnit U = units[blockIdx.x];
+  const int nwarps_act = min(NT / 32, (U.npt + 32 * TPT - 1) / (32 * TPT));
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], (unsigned)nwarps_act);
+    mbar_init(&bars[3], (unsigned)nwarps_act);
+    mbar_fence_init();
+  }
+  init_table(logtab, logsrc);
+  __syncthreads();
+  if ((int)(threadIdx.x >> 5) >= nwarps_act) return;
+  double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) {
+    const int l = TPT * threadIdx.x + u;
+    const int64_t g = U.pt0 + min(l, U.npt - 1);
+    x[u] = gx[g]; y[u] = gy[g]; z[u] = gz[g];
+    cq[u] = 0.5 * fma(x[u], x[u], fma(y[u], y[u], fma(z[u], z[u], 0.25)));
+    if (FAR) { x[u] = -x[u]; y[u] = -y[u]; z[u] = -z[u]; }
+    acc[u] = 0.0;
+  }
+  accumulate_grid_tma<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc, srclist + U.src0,
+                                                       reinterpret_cast<const double4*>(src4 + U.soff), U.p, bufs, brec,
+                                                       bars, logtab);
+  const int upts = NT * TPT;
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
     const int l = TPT * threadIdx.x + u;
@@ -146,16 +189,19 @@ static bool stage_ldg() {
   return v == 1;
 }
 
-// grid-kernel variant: NC_GRID_VARIANT="TPT,UNROLL,LOG8,STAGE" (default kGridVariantDefault)
+// grid-kernel variant: NC_GRID_VARIANT="NT,TPT,UNROLL,STAGE,FAR,TMA,MINB" (default kGridVariantDefault); only the
+// combinations instantiated in launch_pairs_grid launch (others fall back to the default)
 static GridVariant grid_variant() {
-  static GridVariant v = {0, 0, 0, 0, 0};
-  if (v.tpt == 0) {
+  static GridVariant v = {0, 0, 0, 0, 0, 0, 0};
+  if (v.nt == 0) {
     v = kGridVariantDefault;
     if (const char* e = getenv("NC_GRID_VARIANT")) {
       GridVariant w = v;
-      const int n = sscanf(e, "%d,%d,%d,%d,%d", &w.tpt, &w.unroll, &w.log8, &w.stage, &w.far);
-      if (n >= 4 && (w.tpt == 2 || w.tpt == 4) && (w.unroll == 1 || w.unroll == 2 || w.unroll == 4) &&
-          (w.log8 == 0 || w.log8 == 1) && w.stage >= 32 && (w.far == 0 || w.far == 1))
+      w.tma = 0;
+      w.minb = 8;
+      if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d", &w.nt, &w.tpt, &w.unroll, &w.stage, &w.far, &w.tma, &w.minb) >= 5 &&
+          (w.nt == 128 || w.nt == 256) && (w.tpt == 1 || w.tpt == 2) && (w.unroll == 1 || w.unroll == 2 || w.unroll == 4) &&
+          w.stage >= 32 && (w.far == 0 || w.far == 1) && (w.tma == 0 || w.tma == 1))
         v = w;
     }
   }
@@ -164,16 +210,17 @@ static GridVariant grid_variant() {
 
 int grid_far_variant() { return grid_variant().far; }
 
-int grid_unit_points() { return kGridThreads * grid_variant().tpt; }
+int grid_unit_points() { return grid_variant().nt * grid_variant().tpt; }
 
-template <int KIND, int TPT, int UNROLL, bool LOG8, bool FAR>
+template <int KIND, int NT, int TPT, int UNROLL, bool FAR, bool TMA, int MINB>
 static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* gx, const double* gy, const double* gz,
-                          const int32_t* srclist, const double* src4, int stage, size_t smem, double* part,
+                          const int32_t* srclist, const double* src4, int stage, int pmax, double* part,
                           cudaStream_t s) {
-  const void* tab = LOG8 ? (const void*)log8_table_device() : (const void*)log_table_device();
-  auto kern = k_pairs_grid<KIND, TPT, UNROLL, LOG8, FAR>;
+  const int rec = std::max(stage, pmax);   // records per stage buffer: >= one whole patch of any rung
+  const size_t smem = (TMA ? 2 : 1) * (size_t)rec * sizeof(double4);
+  auto kern = TMA ? k_pairs_grid_tma<KIND, NT, TPT, UNROLL, FAR, MINB> : k_pairs_grid<KIND, NT, TPT, UNROLL, FAR, MINB>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<(unsigned)nunits, kGridThreads, smem, s>>>(units, gx, gy, gz, srclist, src4, stage, part, tab);
+  kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device());
 }
 
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
@@ -181,17 +228,21 @@ void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const do
                        cudaStream_t s) {
   if (nunits <= 0) return;
   const GridVariant v = grid_variant();
-  const size_t smem = (size_t)std::max(v.stage, pmax) * sizeof(double4);   // >= chp * p and >= one whole patch
-#define NC_G(KD, TP, UR, L8, FR) \
-  if (kind == KD && v.tpt == TP && v.unroll == UR && v.log8 == L8 && v.far == FR) \
-    return launch_grid_t<KD, TP, UR, L8, FR>(units, nunits, gx, gy, gz, srclist, src4, std::max(v.stage, pmax), smem, part, s);
-#define NC_GK(KD) \
-  NC_G(KD, 2, 2, 0, 0) NC_G(KD, 2, 4, 0, 0) NC_G(KD, 2, 2, 0, 1) NC_G(KD, 2, 4, 0, 1) NC_G(KD, 2, 1, 0, 1) \
-  NC_G(KD, 4, 2, 0, 0) NC_G(KD, 4, 2, 0, 1) NC_G(KD, 2, 4, 1, 0)
+#define NC_G(KD, NT, TP, UR, FR, TM, MB)                                                                   \
+  if (kind == KD && v.nt == NT && v.tpt == TP && v.unroll == UR && v.far == FR && v.tma == TM && v.minb == MB) \
+    return launch_grid_t<KD, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, pmax, part, s);
+#define NC_GK(KD)                                                                                                 \
+  NC_G(KD, 128, 2, 4, 1, 0, 8) NC_G(KD, 128, 2, 4, 0, 0, 8) NC_G(KD, 128, 2, 4, 1, 1, 8) NC_G(KD, 128, 2, 4, 1, 0, 4) \
+  NC_G(KD, 128, 2, 4, 1, 0, 6) NC_G(KD, 256, 1, 4, 1, 0, 1) \
+  NC_G(KD, 256, 1, 4, 1, 0, 5) NC_G(KD, 256, 1, 4, 1, 0, 6) NC_G(KD, 256, 1, 2, 1, 0, 6) NC_G(KD, 256, 2, 2, 1, 0, 5) \
+  NC_G(KD, 256, 1, 4, 1, 1, 6)
   NC_GK(0)
   NC_GK(1)
 #undef NC_GK
 #undef NC_G
+  const GridVariant d = kGridVariantDefault;   // combination not instantiated: the default
+  if (kind == 0) return launch_grid_t<0, 128, 2, 4, true, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part, s);
+  return launch_grid_t<1, 128, 2, 4, true, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part, s);
 }
 
 // ------------------------------------------------------------------------------------------------

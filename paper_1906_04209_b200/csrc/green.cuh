@@ -50,17 +50,6 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
   return fma(ye, c, y);
 }
 
-// far-field rsqrt: the MUFU.RSQ64H seed and ONE Newton step (y + (y/2)(1 - x y^2); y/2 by an exponent decrement on
-// the integer pipe): 3 FP64-pipe instructions instead of 5; relative error ~ (3/2) e0^2 for a seed error e0
-// (measured in tests/test_hier_gpu.py through the whole matvec; used only by k_pairs_grid's FAR variant)
-__device__ __forceinline__ double fast_rsqrt_far(double x) {
-  const double y = rsqrt_approx(x);
-  const double t = x * y;
-  const double e = fma(-t, y, 1.0);
-  const double h = __hiloint2double(__double2hiint(y) - 0x00100000, __double2loint(y));
-  return fma(h, e, y);
-}
-
 // fp64 natural log for positive normal x (absolute error ~1e-16 |log x| + 1e-17)
 __device__ __forceinline__ double fast_log(double x, const double2* __restrict__ tbl) {
   const int hi = __double2hiint(x);
@@ -80,36 +69,6 @@ __device__ __forceinline__ double fast_log(double x, const double2* __restrict__
   return h + l1;
 }
 
-// 8-byte-table variant: c_j is not stored but recomputed from j in two integer ops around one fp32 MUFU.RCP,
-//   c_j = fp32 rcp.approx(1 + (j + 1/2)/1024) truncated to 15 mantissa bits (exact as a double, low word 0),
-// and the table holds only -log c_j (fp64, built on the device by the same instruction sequence and converted
-// on the host in long double: log8_table_device).  |r| = |m c_j - 1| <= 2^-11 + 2^-15 (truncation r^5/5 < 1e-17).
-// Halves the shared-memory bytes per lookup (one LDS.64 instead of one LDS.128: fewer bank-conflict wavefronts).
-__device__ __forceinline__ double log8_c(int j) {
-  const unsigned fb = 0x3F800000u | ((unsigned)j << (23 - kLogTableBits)) | (1u << (22 - kLogTableBits));
-  float c;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(__uint_as_float(fb)));
-  const unsigned cb = __float_as_uint(c) & 0xFFFFFF00u;
-  return __hiloint2double((int)((cb >> 3) + 0x38000000u), 0);
-}
-
-__device__ __forceinline__ double fast_log(double x, const double* __restrict__ tbl) {
-  const int hi = __double2hiint(x);
-  const int lo = __double2loint(x);
-  const int j = (hi >> (20 - kLogTableBits)) & (kLogTableSize - 1);
-  const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
-  const double kd = __hiloint2double(0x43300000, (int)(((unsigned)hi >> 20) - 1023u + 0x80000000u)) -
-                    4503601774854144.0;   // 2^52 + 2^31
-  const double r = fma(m, log8_c(j), -1.0);
-  double p = fma(r, -0.25, 0.33333333333333333333);
-  p = fma(p, r, -0.5);
-  const double r2 = r * r;
-  const double l1 = fma(r2, p, r);
-  const double h = fma(kd, kLn2, tbl[j]);
-  return h + l1;
-}
-const double* log8_table_device();   // host: -log c_j of log8_c, uploaded once per device; nullptr on failure
-
 template <class Tab>
 __device__ __forceinline__ void init_table(Tab* tbl, const Tab* __restrict__ src) {
   for (int j = threadIdx.x; j < kLogTableSize; j += blockDim.x) tbl[j] = src[j];
@@ -124,13 +83,37 @@ __device__ __forceinline__ double green_q(double q, const Tab* __restrict__ tbl)
   return w - fast_log(q * a, tbl);
 }
 
-// far-field G (k_pairs_grid FAR variant): one-Newton rsqrt, same table log
-template <int KIND, class Tab>
-__device__ __forceinline__ double green_q_far(double q, const Tab* __restrict__ tbl) {
-  const double w = fast_rsqrt_far(q);
+// Far-field G (k_pairs_grid FAR variant, hierarchical mode only; R23), from qh = |x - x'|^2 / 8 (half the
+// scaled squared distance, formed by the caller as a dot product).  Trimmed for the issue rate (an FP64 instruction
+// holds the warp scheduler two cycles, any other one cycle):
+//   w  = 2/d = rsqrt(2 qh): MUFU.RSQ64H seed of 2 qh (exponent + 1 on the integer pipe), one Newton step
+//        w = y + y (1/2 - qh y^2)                                      [3 FP64; relative error ~(3/2) e0^2]
+//   log: r = x c_j 2^-k - 1 with the table's c_j rescaled by an integer exponent subtract (no mantissa extraction),
+//        log1p(r) = r + r^2 (-1/2 + r/3)  (|r| <= 2^-11: truncation r^4/4 < 1.5e-14 absolute)
+//   interior: log(q (1 + w)) = log(qh (1 + w)) + ln 2, the ln 2 folded into the exponent's magic constant.
+// 16 FP64 instructions exterior / 17 interior, ~12 others.
+template <int KIND>
+__device__ __forceinline__ double green_far_h(double qh, const double2* __restrict__ tbl) {
+  const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
+  const double t = qh * y;
+  const double e = fma(-t, y, 0.5);
+  const double w = fma(y, e, y);
   const double a = 1.0 + w;
-  if (KIND == 1) return w - fast_log(a, tbl);
-  return w - fast_log(q * a, tbl);
+  const double x = (KIND == 1) ? a : qh * a;
+  const int hi = __double2hiint(x);
+  const int j = (hi >> (20 - kLogTableBits)) & (kLogTableSize - 1);
+  const double2 tj = tbl[j];
+  // c_j 2^-k: subtract the unbiased exponent of x from c_j's exponent field (exact; no range issue for 2^-30..2^30)
+  const double c = __hiloint2double(__double2hiint(tj.x) - (hi & 0x7FF00000) + 0x3FF00000, __double2loint(tj.x));
+  const double r = fma(x, c, -1.0);
+  const double p = fma(r, 0.33333333333333333333, -0.5);
+  const double r2 = r * r;
+  const double l1 = fma(r2, p, r);
+  // k (+1 interior) as a double: 2^52 + 2^31 + e - 1023 minus the magic (minus one more for the interior ln 2)
+  const double kd = __hiloint2double(0x43300000, (int)(((unsigned)hi >> 20) - 1023u + 0x80000000u)) -
+                    (KIND == 1 ? 4503601774854144.0 : 4503601774854143.0);
+  const double h = fma(kd, kLn2, tj.y);
+  return w - (h + l1);
 }
 
 // reference-accuracy variant (libdevice), used by the self-check path

@@ -20,6 +20,7 @@
 // (samples -> parity-restricted Chebyshev-Fourier coefficients) -> k_pairs_near -> k_interp
 // (step 4: evaluate every group's expansion at its members' Zernike nodes, summed over levels) -> K3 (api.cu).
 #include <cub/cub.cuh>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -35,6 +36,7 @@ namespace nc {
 constexpr int kLmax = 24;
 constexpr int kSliceMax = 32;          // source patches per grid work unit
 constexpr double kBetaMin = 1.45;      // smallest source distance / circle radius served by a grid
+constexpr double kCostNear = 1.0, kCostInterp = 0.07, kCostTransform = 0.1;   // grid-vs-near cost model
 constexpr double kGridTolFactor = 1000.0;  // per-grid tolerance / requested precision (calibrated: DESIGN.md R21)
 
 struct ChunkRec {
@@ -84,7 +86,7 @@ struct HierState {
   int32_t* d_pgl = nullptr;         // (L+1) x row_count group ids of local patches
   double *d_tx = nullptr, *d_ty = nullptr, *d_tz = nullptr;
   double *d_udir = nullptr, *d_u = nullptr;
-  double pairs_grid = 0, pairs_near = 0, interp_terms = 0;
+  double pairs_grid = 0, pairs_near = 0, interp_terms = 0, slot_pairs = 0;
   double bytes = 0;
   std::vector<int64_t> ilist_entries;   // host copies for nc_tree_lists: (level, target group, source group)
   std::vector<int64_t> nbr_entries;
@@ -426,24 +428,26 @@ __global__ void k_transform(const int32_t* __restrict__ groups, int64_t ngr, con
 
 // step 4b: u_i(node) = udir + sum over levels of the level's group expansion at the node,
 //   u(x, theta) = sum_m sum_j c[m][j] . (cos m theta, sin m theta) T_{(m & 1) + 2 j}(rho / R)
-// (rho = geodesic distance from the cap centre).  One CTA per target patch, kInterpNpt nodes per thread; every
-// coefficient pair is one broadcast shared-memory load reused by the thread's nodes (independent FP64 chains).
-constexpr int kInterpNpt = 4;
-__global__ void __launch_bounds__(128) k_interp(int L, int64_t rc, int Kstar, const int32_t* __restrict__ pgl,
-                                                 const double* __restrict__ F, const double* __restrict__ gR,
-                                                 const int32_t* __restrict__ gnr, const int32_t* __restrict__ gna,
-                                                 const int64_t* __restrict__ coff, const double* __restrict__ coef,
-                                                 const double* __restrict__ tx, const double* __restrict__ ty,
-                                                 const double* __restrict__ tz, const double* __restrict__ udir,
-                                                 double* __restrict__ u) {
+// (rho = geodesic distance from the cap centre).  One CTA of NT threads per target patch, NPT nodes per thread.  The
+// m loop runs in blocks of MB orders: inside a block the j loop advances BOTH parity sequences T_{2j}, T_{2j+1}
+// once (2 FMA) and feeds MB (A_m, B_m) accumulator pairs, so the Chebyshev recurrence is shared by the block's
+// orders (2 + 2/MB FMA per coefficient pair instead of 3); every coefficient pair is one broadcast shared-memory load
+// reused by the thread's NPT nodes.
+template <int NT, int NPT, int MB>
+__global__ void __launch_bounds__(NT) k_interp(int L, int64_t rc, int Kstar, const int32_t* __restrict__ pgl,
+                                               const double* __restrict__ F, const double* __restrict__ gR,
+                                               const int32_t* __restrict__ gnr, const int32_t* __restrict__ gna,
+                                               const int64_t* __restrict__ coff, const double* __restrict__ coef,
+                                               const double* __restrict__ tx, const double* __restrict__ ty,
+                                               const double* __restrict__ tz, const double* __restrict__ udir,
+                                               double* __restrict__ u) {
   extern __shared__ double2 c2[];
-  constexpr int NPT = kInterpNpt;
   const int64_t i = blockIdx.x;
-  for (int kb = 0; kb < Kstar; kb += NPT * blockDim.x) {
+  for (int kb = 0; kb < Kstar; kb += NPT * NT) {
     double acc[NPT], px[NPT], py[NPT], pz[NPT];
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
-      const int k = min(kb + (int)threadIdx.x + q * (int)blockDim.x, Kstar - 1);
+      const int k = min(kb + (int)threadIdx.x + q * NT, Kstar - 1);
       const int64_t t = i * Kstar + k;
       px[q] = 2.0 * tx[t]; py[q] = 2.0 * ty[t]; pz[q] = 2.0 * tz[t];
       acc[q] = udir ? udir[t] : 0.0;
@@ -455,11 +459,11 @@ __global__ void __launch_bounds__(128) k_interp(int L, int64_t rc, int Kstar, co
       const int M = na / 2, ncp = (M + 1) * nr;
       __syncthreads();
       const double2* __restrict__ src = reinterpret_cast<const double2*>(coef + coff[g]);
-      for (int t = threadIdx.x; t < ncp; t += blockDim.x) c2[t] = src[t];
+      for (int t = threadIdx.x; t < ncp; t += NT) c2[t] = src[t];
       __syncthreads();
       const double* r9 = F + 9 * (int64_t)g;
       const double invR = 1.0 / gR[g];
-      double x[NPT], w2[NPT], c1[NPT], s1[NPT], cm[NPT], sm[NPT], cmm[NPT], smm[NPT];
+      double x[NPT], w2[NPT], c1[NPT], cm[NPT], sm[NPT], cmm[NPT], smm[NPT];
 #pragma unroll
       for (int q = 0; q < NPT; ++q) {
         const double sx = r9[0] * px[q] + r9[1] * py[q] + r9[2] * pz[q];
@@ -467,47 +471,109 @@ __global__ void __launch_bounds__(128) k_interp(int L, int64_t rc, int Kstar, co
         const double cz = r9[6] * px[q] + r9[7] * py[q] + r9[8] * pz[q];
         const double rho = sqrt(sx * sx + sy * sy);
         x[q] = atan2(rho, cz) * invR;
-        c1[q] = rho > 0 ? sx / rho : 1.0;
-        s1[q] = rho > 0 ? sy / rho : 0.0;
+        const double irho = rho > 0 ? 1.0 / rho : 0.0;
+        c1[q] = rho > 0 ? sx * irho : 1.0;
+        const double s1 = rho > 0 ? sy * irho : 0.0;
         w2[q] = 4.0 * x[q] * x[q] - 2.0;
-        cm[q] = 1.0; sm[q] = 0.0; cmm[q] = c1[q]; smm[q] = -s1[q];   // cos/sin(m theta), (m - 1) theta
+        cm[q] = 1.0; sm[q] = 0.0; cmm[q] = c1[q]; smm[q] = -s1;   // cos/sin(m theta), ((m - 1) theta)
       }
-      for (int m = 0; m <= M; ++m) {
-        const double2* __restrict__ cmj = c2 + m * nr;
-        double A[NPT], B[NPT], t0[NPT], t1[NPT];
-        const double2 c0 = cmj[0];
+      for (int m0 = 0; m0 <= M; m0 += MB) {
+        double A[MB][NPT], B[MB][NPT], te[NPT], tep[NPT], to[NPT], top[NPT];
+        // j = 0: T_0 = 1, T_1 = x; the step-2 recurrence T_{n+2} = w2 T_n - T_{n-2} (w2 = 2 T_2) starts from
+        // T_{-2} = T_2 and T_{-1} = T_1 (T_{-n} = T_n)
 #pragma unroll
         for (int q = 0; q < NPT; ++q) {
-          t0[q] = (m & 1) ? x[q] : 1.0;
-          t1[q] = (m & 1) ? x[q] * (4.0 * x[q] * x[q] - 3.0) : 2.0 * x[q] * x[q] - 1.0;
-          A[q] = c0.x * t0[q];
-          B[q] = c0.y * t0[q];
+          te[q] = 1.0; tep[q] = 2.0 * x[q] * x[q] - 1.0;
+          to[q] = x[q]; top[q] = x[q];
         }
-        for (int j = 1; j < nr; ++j) {
-          const double2 c = cmj[j];
+#pragma unroll
+        for (int b = 0; b < MB; ++b) {
+          const int m = m0 + b;
+          const double2 c = (m <= M) ? c2[m * nr] : make_double2(0.0, 0.0);
 #pragma unroll
           for (int q = 0; q < NPT; ++q) {
-            A[q] = fma(c.x, t1[q], A[q]);
-            B[q] = fma(c.y, t1[q], B[q]);
-            const double t2 = fma(w2[q], t1[q], -t0[q]);
-            t0[q] = t1[q];
-            t1[q] = t2;
+            const double tv = (m & 1) ? to[q] : te[q];
+            A[b][q] = c.x * tv;
+            B[b][q] = c.y * tv;
+          }
+        }
+        for (int j = 1; j < nr; ++j) {
+#pragma unroll
+          for (int q = 0; q < NPT; ++q) {   // advance: te = T_{2j}, to = T_{2j+1}
+            const double ne = fma(w2[q], te[q], -tep[q]);
+            const double no = fma(w2[q], to[q], -top[q]);
+            tep[q] = te[q]; te[q] = ne;
+            top[q] = to[q]; to[q] = no;
+          }
+#pragma unroll
+          for (int b = 0; b < MB; ++b) {
+            const int m = m0 + b;
+            const double2 c = (m <= M) ? c2[m * nr + j] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < NPT; ++q) {
+              const double tv = (m & 1) ? to[q] : te[q];
+              A[b][q] = fma(c.x, tv, A[b][q]);
+              B[b][q] = fma(c.y, tv, B[b][q]);
+            }
           }
         }
 #pragma unroll
-        for (int q = 0; q < NPT; ++q) {
-          acc[q] = fma(A[q], cm[q], fma(B[q], sm[q], acc[q]));
-          const double cn = 2.0 * c1[q] * cm[q] - cmm[q], sn = 2.0 * c1[q] * sm[q] - smm[q];
-          cmm[q] = cm[q]; smm[q] = sm[q]; cm[q] = cn; sm[q] = sn;
+        for (int b = 0; b < MB; ++b) {
+#pragma unroll
+          for (int q = 0; q < NPT; ++q) {
+            acc[q] = fma(A[b][q], cm[q], fma(B[b][q], sm[q], acc[q]));
+            const double cn = 2.0 * c1[q] * cm[q] - cmm[q], sn = 2.0 * c1[q] * sm[q] - smm[q];
+            cmm[q] = cm[q]; smm[q] = sm[q]; cm[q] = cn; sm[q] = sn;
+          }
         }
       }
     }
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
-      const int k = kb + (int)threadIdx.x + q * (int)blockDim.x;
+      const int k = kb + (int)threadIdx.x + q * NT;
       if (k < Kstar) u[i * Kstar + k] = acc[q];
     }
   }
+}
+
+// interpolation variant: NC_INTERP_VARIANT="NT,NPT,MB"
+struct InterpVariant {
+  int nt, npt, mb;
+};
+static InterpVariant interp_variant() {
+  static InterpVariant v = {0, 0, 0};
+  if (v.nt == 0) {
+    v = {256, 2, 4};
+    if (const char* e = getenv("NC_INTERP_VARIANT")) {
+      InterpVariant w = v;
+      if (sscanf(e, "%d,%d,%d", &w.nt, &w.npt, &w.mb) == 3) v = w;
+    }
+  }
+  return v;
+}
+
+template <int NT, int NPT, int MB>
+static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const double* F, const double* gR,
+                           const int32_t* gnr, const int32_t* gna, const int64_t* coff, const double* coef,
+                           const double* tx, const double* ty, const double* tz, const double* udir, double* u,
+                           cudaStream_t s) {
+  auto kern = k_interp<NT, NPT, MB>;
+  if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u);
+  return NC_OK;
+}
+
+static int launch_interp(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const double* F, const double* gR,
+                         const int32_t* gnr, const int32_t* gna, const int64_t* coff, const double* coef,
+                         const double* tx, const double* ty, const double* tz, const double* udir, double* u,
+                         cudaStream_t s) {
+  const InterpVariant v = interp_variant();
+#define NC_I(NT, NPT, MB)                                                                                  \
+  if (v.nt == NT && v.npt == NPT && v.mb == MB)                                                            \
+    return launch_interp_t<NT, NPT, MB>(shm, L, rc, Ks, pgl, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
+  NC_I(128, 4, 1) NC_I(128, 4, 2) NC_I(256, 2, 4) NC_I(256, 2, 2) NC_I(256, 1, 4) NC_I(256, 1, 8) NC_I(128, 2, 4)
+#undef NC_I
+  return launch_interp_t<256, 2, 4>(shm, L, rc, Ks, pgl, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -712,6 +778,12 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   double tol_factor = kGridTolFactor;
   if (const char* e = getenv("NC_GRID_TOL_FACTOR")) tol_factor = atof(e);
   const double tol = tol_factor * h->precision;
+  // relative costs in grid-pair units (measured at C5): a near-list pair (exact form), one
+  // interpolation term (node x coefficient), one transform term; NC_COST_NEAR / _INTERP / _TRANSFORM override
+  double c_near = kCostNear, c_interp = kCostInterp, c_trans = kCostTransform;
+  if (const char* e = getenv("NC_COST_NEAR")) c_near = atof(e);
+  if (const char* e = getenv("NC_COST_INTERP")) c_interp = atof(e);
+  if (const char* e = getenv("NC_COST_TRANSFORM")) c_trans = atof(e);
   std::vector<std::vector<int32_t>> gsrc(G), nsrc(G);
   H->gnr.assign(G, 0);
   H->gna.assign(G, 0);
@@ -752,7 +824,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         if (h->rung_r[k] <= gap * (1.0 - 1e-12)) rung = k;
       psum[n + 1] = psum[n] + h->rung_p[rung];
     }
-    double best_cost = (double)mem * Ks * cand.size() * p0;   // all direct
+    double best_cost = c_near * (double)mem * Ks * cand.size() * p0;   // all direct
     size_t best_n = 0;
     int bnr = 0, bna = 0;
     for (size_t n = 1; n <= cand.size(); ++n) {
@@ -764,8 +836,8 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       const double q = (double)nr * na;
       // pair evaluations: grid sources on q points (each with its own rung), the rest at the members' Zernike
       // nodes, plus the interpolation (~1.5 FMA per node per coefficient ~ 0.07 pair) and the transform
-      const double cost = q * psum[n] + (double)mem * Ks * (cand.size() - n) * p0 + 0.07 * (double)mem * Ks * q +
-                          0.1 * q * (nr + na);
+      const double cost = q * psum[n] + c_near * (double)mem * Ks * (cand.size() - n) * p0 +
+                          c_interp * (double)mem * Ks * q + c_trans * q * (nr + na);
       if (cost < best_cost) {
         best_cost = cost;
         best_n = n;
@@ -889,6 +961,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         u.p = h->rung_p[sl.rung];
         u.pad_ = 0;
         units.push_back(u);
+        H->slot_pairs += (double)H->upts * u.nsrc * u.p;
       }
     }
   }
@@ -1005,9 +1078,8 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   // step 4b: interpolation to the Zernike nodes, summed over levels
   if (rc > 0) {
     const size_t shm = (size_t)std::max(H->cmax, 1) * sizeof(double);
-    if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(k_interp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    k_interp<<<(unsigned)rc, 128, shm, s>>>(H->L, rc, Ks, H->d_pgl, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna,
-                                            H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u);
+    NC_TRY(launch_interp(shm, H->L, rc, Ks, H->d_pgl, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef,
+                         H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u, s));
     h->launches_last++;
   }
   // step 5: y = x + U P^T
@@ -1028,6 +1100,7 @@ void hier_fill_stats(const nc_handle* h, nc_stats_t* o) {
   o->hier_interp_terms = H->interp_terms;
   o->hier_grid_points = H->Q;
   o->hier_grid_units = H->nunits;
+  o->hier_grid_fill = H->slot_pairs > 0 ? H->pairs_grid / H->slot_pairs : 0.0;
 }
 
 void hier_destroy(nc_handle* h) {

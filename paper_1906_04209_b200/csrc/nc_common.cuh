@@ -44,14 +44,14 @@ constexpr int kDefaultStageLdg = 0; // 1: pair kernels read sources via L1 broad
 // ------------------------------------------------------------------------------------------------
 struct HierState;
 
-constexpr int kGridThreads = 128;      // threads per CTA of the incoming-grid pair kernel
-// k_pairs_grid variant {targets per thread, source unroll, 8-byte log table, staged source records, far-field G}
+// k_pairs_grid variant {threads per CTA, targets per thread, source unroll, staged source records (per buffer when
+// tma), far-field arithmetic, bulk-copy mbarrier pipeline}; NC_GRID_VARIANT overrides (tools/sweep_grid.py)
 struct GridVariant {
-  int tpt, unroll, log8, stage, far;
+  int nt, tpt, unroll, stage, far, tma, minb;   // minb: __launch_bounds__ min blocks per SM (register cap)
 };
-#define kGridVariantDefault (GridVariant{2, 4, 0, 256, 1})
+#define kGridVariantDefault (GridVariant{128, 2, 4, 256, 1, 0, 8})
 int grid_far_variant();
-int grid_unit_points();                // grid points per work unit = kGridThreads x targets per thread
+int grid_unit_points();                // grid points per work unit = threads per CTA x targets per thread
 
 struct GridUnit {      // <= grid_unit_points() points of one incoming grid x one slice of its source-patch list
   int64_t pt0;         // first grid point (global grid-point index)

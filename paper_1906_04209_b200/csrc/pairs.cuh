@@ -24,7 +24,7 @@ __host__ __device__ inline int stage_patches(int p) {
 
 // patch_at(k) -> patch index of the k-th list entry.  All threads of the CTA must call (barriers inside).
 // UNROLL: source records in flight per target (independent FP64 chains = TPT x UNROLL); Tab: double2 (c_j, -log c_j)
-// or double (-log c_j, c_j recomputed: green.cuh log8_c).
+// (c_j, -log c_j).
 template <int KIND, int TPT, int UNROLL = 2, class Tab = double2, class PatchAt>
 __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
                                                 const int64_t (&excl)[TPT], double (&acc)[TPT], int64_t nlist,
@@ -80,10 +80,10 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
 }
 
 // Incoming-grid variant (no self exclusion: grid sources never include the target's own patch).  FAR = false: the
-// exact kernel of accumulate_list.  FAR = true (far-field evaluation, hierarchical mode only): the squared distance
-// from the dot product, q = |X|^2 + 1/4 - 2 X.S with the target pre-scaled T = -2X (3 DFMA instead of 6 FP64 ops;
-// absolute error ~3e-16, i.e. relative ~1e-10 at the closest grid pairs q ~ eps^2/4, far below the hierarchical
-// tolerance) and the one-Newton rsqrt.  x/y/z hold T when FAR, and cq[u] = |X_u|^2 + 1/4.
+// exact kernel of accumulate_list.  FAR = true (far-field evaluation, hierarchical mode only): half the squared
+// distance from the dot product, qh = (|X|^2 + 1/4)/2 - X.S with the target pre-negated (3 DFMA instead of 6 FP64
+// ops; absolute error ~2e-16, i.e. relative ~1e-10 at the closest grid pairs qh ~ eps^2/8, far below the
+// hierarchical tolerance) and green_far_h.  x/y/z hold -X when FAR, and cq[u] = (|X_u|^2 + 1/4)/2.
 template <int KIND, int TPT, int UNROLL, bool FAR, class Tab, class PatchAt>
 __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
                                                 const double (&cq)[TPT], double (&acc)[TPT], int64_t nlist,
@@ -108,8 +108,8 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
         if (FAR) {
-          const double qd = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
-          acc[u] = fma(s.w, green_q_far<KIND>(qd, logtab), acc[u]);
+          const double qh = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
+          acc[u] = fma(s.w, green_far_h<KIND>(qh, logtab), acc[u]);
         } else {
           const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
           const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
@@ -117,6 +117,89 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
         }
       }
     }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Bulk-copy (TMA) pipeline for the incoming-grid sums: one elected thread streams whole source patches (p contiguous
+// 32-byte records each) into two shared-memory buffers with cp.async.bulk, completion tracked by a `full` mbarrier per
+// buffer (transaction bytes); each consumer warp releases a buffer by arriving on its `empty` mbarrier.  No CTA-wide
+// barrier in the loop: the copy of chunk c+1 overlaps the evaluation of chunk c, and warps drift freely.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n NC_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra NC_WAIT_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// bufs: 2 x brec records; bars: full[2], empty[2] (initialised here; the caller __syncthreads() before the first
+// wait is done inside).  Threads of warps with no active target must not call (they return before).  nwarps_act:
+// warps that call.  lst: the unit's source-patch list (nsrc entries), s4: the rung's records.
+template <int KIND, int TPT, int UNROLL, bool FAR, class Tab>
+__device__ __forceinline__ void accumulate_grid_tma(const double (&x)[TPT], const double (&y)[TPT],
+                                                    const double (&z)[TPT], const double (&cq)[TPT],
+                                                    double (&acc)[TPT], int nsrc, const int32_t* __restrict__ lst,
+                                                    const double4* __restrict__ s4, int p, double4* __restrict__ bufs,
+                                                    int brec, uint64_t* __restrict__ bars,
+                                                    const Tab* __restrict__ logtab) {
+  uint64_t* full = bars;
+  uint64_t* empty = bars + 2;
+  const int chp = brec / p;                              // patches per chunk (>= 1: brec >= p)
+  const int nch = (nsrc + chp - 1) / chp;
+  const bool producer = threadIdx.x == 0;
+  auto issue = [&](int c) {
+    const int b = c & 1, k0 = c * chp, k1 = min(nsrc, k0 + chp);
+    mbar_expect_tx(&full[b], (unsigned)((k1 - k0) * p * sizeof(double4)));
+    for (int k = k0; k < k1; ++k)
+      bulk_g2s(bufs + (size_t)b * brec + (size_t)(k - k0) * p, s4 + (size_t)lst[k] * p, (unsigned)(p * sizeof(double4)),
+               &full[b]);
+  };
+  if (producer) issue(0);
+  for (int c = 0; c < nch; ++c) {
+    const int b = c & 1;
+    if (producer && c + 1 < nch) {
+      if (c >= 1) mbar_wait(&empty[(c + 1) & 1], (unsigned)(((c - 1) >> 1) & 1));   // chunk c-1 released its buffer
+      issue(c + 1);
+    }
+    mbar_wait(&full[b], (unsigned)((c >> 1) & 1));
+    const double4* __restrict__ sp = bufs + (size_t)b * brec;
+    const int nrec = (min(nsrc, (c + 1) * chp) - c * chp) * p;
+#pragma unroll UNROLL
+    for (int m = 0; m < nrec; ++m) {
+      const double4 s = sp[m];
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        if (FAR) {
+          const double qh = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
+          acc[u] = fma(s.w, green_far_h<KIND>(qh, logtab), acc[u]);
+        } else {
+          const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
+          const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
+          acc[u] = fma(s.w, green_q<KIND>(qd, logtab), acc[u]);
+        }
+      }
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[b]);
   }
 }
 

@@ -1,6 +1,6 @@
 """Sweep the k_pairs_grid variants (NC_GRID_VARIANT="TPT,UNROLL,LOG8,STAGE") on one config (GPU box).
 
-    python tools/sweep_grid.py C5 "2,2,0,512" "2,2,0,256" ...
+    python tools/sweep_grid.py C5 "128,2,4,256,1" "NC_INTERP_VARIANT=256,2,4" "NC_COST_NEAR=1.3;NC_COST_INTERP=0.15" ...
 
 Each variant runs in its own process (the variant is read once per process); prints one JSON line per variant with
 the per-matvec k_pairs_grid time (library CUDA events), the whole matvec time, and the relative difference of the
@@ -30,15 +30,15 @@ for _ in range(2):
     h.matvec(x, y)
 torch.cuda.synchronize()
 h.time_stages(True)
-g, t = [], []
+g, t, r = [], [], []
 for _ in range(3):
     h.matvec(x, y)
     st = h.stats()
-    g.append(st["ms_last"][4]); t.append(st["ms_last"][6])
+    g.append(st["ms_last"][4]); t.append(st["ms_last"][6]); r.append(st["ms_last"][5])
 np.save(os.environ["OUT"], y.cpu().numpy())
-print(json.dumps({"variant": os.environ.get("NC_GRID_VARIANT"), "grid_ms": float(np.median(g)),
+print(json.dumps({"variant": os.environ.get("VARIANT"), "grid_ms": float(np.median(g)), "rest_ms": float(np.median(r)),
                   "matvec_ms": float(np.median(t)), "pairs": st["hier_grid_pairs"],
-                  "units": st["hier_grid_units"]}))
+                  "units": st["hier_grid_units"], "fill": st["hier_grid_fill"]}))
 """
 
 
@@ -47,8 +47,14 @@ def main():
     ref = None
     for k, v in enumerate(sys.argv[2:]):
         out = f"/tmp/sweep_{k}.npy"
-        env = dict(os.environ, NC_GRID_VARIANT=v, ROOT=ROOT, CFG=cfg, OUT=out)
-        r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
+        env = dict(os.environ, ROOT=ROOT, CFG=cfg, OUT=out, VARIANT=v)
+        for spec in v.split(";"):                 # "NAME=value;..." sets env vars, a bare value NC_GRID_VARIANT
+            if "=" in spec:
+                k_, v_ = spec.split("=", 1)
+                env[k_] = v_
+            elif spec:
+                env["NC_GRID_VARIANT"] = spec
+        r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=240)
         if r.returncode != 0:
             print(json.dumps({"variant": v, "error": r.stderr[-400:]}), flush=True)
             continue
