@@ -44,6 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     inc, lib = nccl_paths()
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--extended-lambda", "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+           "-Xcompiler", "-fopenmp", "-lgomp",
            "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"]
     if inc:
         cmd += ["-DNC_WITH_NCCL=1", "-I", inc, "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]

@@ -91,15 +91,14 @@ __device__ __forceinline__ double green_q(double q, const Tab* __restrict__ tbl)
 //   log: r = x c_j 2^-k - 1 with the table's c_j rescaled by an integer exponent subtract (no mantissa extraction),
 //        log1p(r) = r + r^2 (-1/2 + r/3)  (|r| <= 2^-11: truncation r^4/4 < 1.5e-14 absolute)
 //   interior: log(q (1 + w)) = log(qh (1 + w)) + ln 2, the ln 2 folded into the exponent's magic constant.
-// 16 FP64 instructions exterior / 17 interior, ~12 others.
+// 16 FP64 instructions (both kinds: the interior argument qh (1 + w) is one FMA), ~13 others.
 template <int KIND>
 __device__ __forceinline__ double green_far_h(double qh, const double2* __restrict__ tbl) {
   const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
   const double t = qh * y;
   const double e = fma(-t, y, 0.5);
   const double w = fma(y, e, y);
-  const double a = 1.0 + w;
-  const double x = (KIND == 1) ? a : qh * a;
+  const double x = (KIND == 1) ? 1.0 + w : fma(qh, w, qh);   // 1 + w  |  qh (1 + w)
   const int hi = __double2hiint(x);
   const int j = (hi >> (20 - kLogTableBits)) & (kLogTableSize - 1);
   const double2 tj = tbl[j];

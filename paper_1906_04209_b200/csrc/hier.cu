@@ -35,6 +35,8 @@ namespace nc {
 
 constexpr int kLmax = 24;
 constexpr int kSliceMax = 32;          // source patches per grid work unit
+constexpr int kMaxGrids = 2;           // incoming grids per group (source bands by distance; R24)
+constexpr int kGridCutQuantiles = 48;  // candidate cut points of the two-grid search
 constexpr double kBetaMin = 1.45;      // smallest source distance / circle radius served by a grid
 constexpr double kCostNear = 1.0, kCostInterp = 0.07, kCostTransform = 0.1;   // grid-vs-near cost model
 constexpr double kGridTolFactor = 1000.0;  // per-grid tolerance / requested precision (calibrated: DESIGN.md R21)
@@ -58,19 +60,23 @@ struct HierState {
   std::vector<double> gc, gR;       // circle centre (3/group), radius
   std::vector<int32_t> pgroup;      // (L+1) x N
   std::vector<int64_t> keys;        // sorted keys (internal order)
-  // grids
-  std::vector<int32_t> gnr, gna;
-  std::vector<int64_t> goff, coff;
+  // incoming grids (up to kMaxGrids per group; arrays indexed by grid id)
+  int64_t ngrids = 0;
+  std::vector<int64_t> ggrid0;      // G+1: grids of group g are [ggrid0[g], ggrid0[g+1])
+  std::vector<int32_t> gnr, gna, grid_group;
+  std::vector<int64_t> goff, coff;  // ngrids+1 point / coefficient offsets (0-sized for other ranks' groups)
   int64_t Q = 0, C = 0;
   int qmax = 0, cmax = 0, pmax = 0, namax = 0, nrmax = 0;
-  std::vector<int32_t> grid_groups;
+  std::vector<int32_t> grid_ids;    // grids with points on this rank
   // device
   int64_t* d_keys = nullptr;
   double* d_gframe = nullptr;
   double* d_gR = nullptr;
   int32_t *d_gnr = nullptr, *d_gna = nullptr;
   int64_t *d_goff = nullptr, *d_coff = nullptr;
-  int32_t* d_grid_groups = nullptr;
+  int32_t* d_grid_ids = nullptr;
+  int32_t* d_grid_group = nullptr;
+  int64_t* d_ggrid0 = nullptr;
   double *d_gx = nullptr, *d_gy = nullptr, *d_gz = nullptr, *d_gval = nullptr, *d_gcoef = nullptr;
   GridUnit* d_units = nullptr;
   int64_t nunits = 0;
@@ -339,23 +345,24 @@ __global__ void k_group_frames(const double* __restrict__ gc, int64_t ngroups, d
 
 // incoming-grid points: r_k = R cos(pi (k + 1/2) / (2 n_r)) (positive half of a 2 n_r Chebyshev grid),
 // theta_l = 2 pi l / n_a;  x = cos(r) c + sin(r) (cos(theta) e1 + sin(theta) e2), stored x 1/2
-__global__ void k_grid_points(const int32_t* __restrict__ groups, int64_t ngr, const double* __restrict__ F,
-                              const double* __restrict__ gR, const int32_t* __restrict__ gnr,
-                              const int32_t* __restrict__ gna, const int64_t* __restrict__ goff, double* gx,
-                              double* gy, double* gz) {
+__global__ void k_grid_points(const int32_t* __restrict__ grids, int64_t ngr, const int32_t* __restrict__ grid_group,
+                              const double* __restrict__ F, const double* __restrict__ gR,
+                              const int32_t* __restrict__ gnr, const int32_t* __restrict__ gna,
+                              const int64_t* __restrict__ goff, double* gx, double* gy, double* gz) {
   const int64_t gi = blockIdx.x;
   if (gi >= ngr) return;
-  const int g = groups[gi];
-  const int nr = gnr[g], na = gna[g];
+  const int k = grids[gi];
+  const int g = grid_group[k];
+  const int nr = gnr[k], na = gna[k];
   const double* r9 = F + 9 * (int64_t)g;
   for (int t = threadIdx.x; t < nr * na; t += blockDim.x) {
-    const int k = t / na, l = t % na;
-    const double r = gR[g] * cospi((k + 0.5) / (2.0 * nr));
+    const int kr = t / na, l = t % na;
+    const double r = gR[g] * cospi((kr + 0.5) / (2.0 * nr));
     double st, ct, sr, cr;
     sincospi(2.0 * l / na, &st, &ct);
     sincos(r, &sr, &cr);
     const double a = sr * ct, b = sr * st;
-    const int64_t o = goff[g] + t;
+    const int64_t o = goff[k] + t;
     gx[o] = 0.5 * (r9[0] * a + r9[3] * b + r9[6] * cr);
     gy[o] = 0.5 * (r9[1] * a + r9[4] * b + r9[7] * cr);
     gz[o] = 0.5 * (r9[2] * a + r9[5] * b + r9[8] * cr);
@@ -379,12 +386,12 @@ __global__ void k_reduce_chunks(const ChunkRec* __restrict__ ch, int64_t nch, co
 //   Fourier:   AB[k][m][cs] = (2 - delta) / n_a  sum_l f(r_k, theta_l) {cos, sin}(2 pi m l / n_a)
 //   Chebyshev: c[m][j][cs]  = (2 - delta_n0) / n_r sum_k AB[k][m][cs] cos(n pi (2k + 1) / (4 n_r))
 // Twiddles are tabulated once per group in shared memory (exact index reduction, no per-term sincos).
-__global__ void k_transform(const int32_t* __restrict__ groups, int64_t ngr, const int32_t* __restrict__ gnr,
+__global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, const int32_t* __restrict__ gnr,
                             const int32_t* __restrict__ gna, const int64_t* __restrict__ goff,
                             const int64_t* __restrict__ coff, const double* __restrict__ gval,
                             double* __restrict__ coef) {
   extern __shared__ double sh[];
-  const int g = groups[blockIdx.x];
+  const int g = grids[blockIdx.x];   // grid id
   const int nr = gnr[g], na = gna[g], M = na / 2;
   double* f = sh;                      // nr * na
   double* AB = f + nr * na;            // nr * (M+1) * 2
@@ -435,6 +442,7 @@ __global__ void k_transform(const int32_t* __restrict__ groups, int64_t ngr, con
 // reused by the thread's NPT nodes.
 template <int NT, int NPT, int MB>
 __global__ void __launch_bounds__(NT) k_interp(int L, int64_t rc, int Kstar, const int32_t* __restrict__ pgl,
+                                               const int64_t* __restrict__ ggrid0,
                                                const double* __restrict__ F, const double* __restrict__ gR,
                                                const int32_t* __restrict__ gnr, const int32_t* __restrict__ gna,
                                                const int64_t* __restrict__ coff, const double* __restrict__ coef,
@@ -452,13 +460,14 @@ __global__ void __launch_bounds__(NT) k_interp(int L, int64_t rc, int Kstar, con
       px[q] = 2.0 * tx[t]; py[q] = 2.0 * ty[t]; pz[q] = 2.0 * tz[t];
       acc[q] = udir ? udir[t] : 0.0;
     }
-    for (int lvl = 0; lvl <= L; ++lvl) {
-      const int g = pgl[(int64_t)lvl * rc + i];
-      const int nr = gnr[g], na = gna[g];
+    for (int lvl = 0; lvl <= L; ++lvl)
+    for (int64_t kg = ggrid0[pgl[(int64_t)lvl * rc + i]]; kg < ggrid0[pgl[(int64_t)lvl * rc + i] + 1]; ++kg) {
+      const int g = pgl[(int64_t)lvl * rc + i];   // group (frame, radius); kg: one of its grids
+      const int nr = gnr[kg], na = gna[kg];
       if (nr == 0) continue;   // block-uniform
       const int M = na / 2, ncp = (M + 1) * nr;
       __syncthreads();
-      const double2* __restrict__ src = reinterpret_cast<const double2*>(coef + coff[g]);
+      const double2* __restrict__ src = reinterpret_cast<const double2*>(coef + coff[kg]);
       for (int t = threadIdx.x; t < ncp; t += NT) c2[t] = src[t];
       __syncthreads();
       const double* r9 = F + 9 * (int64_t)g;
@@ -543,7 +552,7 @@ struct InterpVariant {
 static InterpVariant interp_variant() {
   static InterpVariant v = {0, 0, 0};
   if (v.nt == 0) {
-    v = {256, 2, 4};
+    v = {128, 4, 1};
     if (const char* e = getenv("NC_INTERP_VARIANT")) {
       InterpVariant w = v;
       if (sscanf(e, "%d,%d,%d", &w.nt, &w.npt, &w.mb) == 3) v = w;
@@ -553,27 +562,27 @@ static InterpVariant interp_variant() {
 }
 
 template <int NT, int NPT, int MB>
-static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const double* F, const double* gR,
-                           const int32_t* gnr, const int32_t* gna, const int64_t* coff, const double* coef,
-                           const double* tx, const double* ty, const double* tz, const double* udir, double* u,
-                           cudaStream_t s) {
+static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const int64_t* ggrid0,
+                           const double* F, const double* gR, const int32_t* gnr, const int32_t* gna,
+                           const int64_t* coff, const double* coef, const double* tx, const double* ty,
+                           const double* tz, const double* udir, double* u, cudaStream_t s) {
   auto kern = k_interp<NT, NPT, MB>;
   if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u);
+  kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u);
   return NC_OK;
 }
 
-static int launch_interp(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const double* F, const double* gR,
-                         const int32_t* gnr, const int32_t* gna, const int64_t* coff, const double* coef,
-                         const double* tx, const double* ty, const double* tz, const double* udir, double* u,
-                         cudaStream_t s) {
+static int launch_interp(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const int64_t* ggrid0,
+                         const double* F, const double* gR, const int32_t* gnr, const int32_t* gna,
+                         const int64_t* coff, const double* coef, const double* tx, const double* ty,
+                         const double* tz, const double* udir, double* u, cudaStream_t s) {
   const InterpVariant v = interp_variant();
 #define NC_I(NT, NPT, MB)                                                                                  \
   if (v.nt == NT && v.npt == NPT && v.mb == MB)                                                            \
-    return launch_interp_t<NT, NPT, MB>(shm, L, rc, Ks, pgl, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
-  NC_I(128, 4, 1) NC_I(128, 4, 2) NC_I(256, 2, 4) NC_I(256, 2, 2) NC_I(256, 1, 4) NC_I(256, 1, 8) NC_I(128, 2, 4)
+    return launch_interp_t<NT, NPT, MB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
+  NC_I(128, 4, 1) NC_I(256, 1, 4)
 #undef NC_I
-  return launch_interp_t<256, 2, 4>(shm, L, rc, Ks, pgl, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
+  return launch_interp_t<128, 4, 1>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -784,13 +793,27 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   if (const char* e = getenv("NC_COST_NEAR")) c_near = atof(e);
   if (const char* e = getenv("NC_COST_INTERP")) c_interp = atof(e);
   if (const char* e = getenv("NC_COST_TRANSFORM")) c_trans = atof(e);
-  std::vector<std::vector<int32_t>> gsrc(G), nsrc(G);
-  H->gnr.assign(G, 0);
-  H->gna.assign(G, 0);
+  // Incoming grids per group (§8.1 :1424-1434): the group's interaction-list / leaf-neighbour
+  // sources, sorted by beta = (distance - eps) / R descending, are cut into up to kMaxGrids consecutive bands, each
+  // on its own grid sized by the band's nearest source, and a near tail evaluated directly at the members' Zernike
+  // nodes (R12, R24).  The cut minimises the cost model (grid-pair units).
+  int max_grids = kMaxGrids;
+  if (const char* e = getenv("NC_MAX_GRIDS")) max_grids = std::max(1, std::min(kMaxGrids, atoi(e)));
+  std::vector<std::vector<int32_t>> nsrc(G);
+  struct GridPlan {
+    int32_t group, nr, na;
+    std::vector<int32_t> src;
+    std::vector<int> rung;
+  };
+  std::vector<std::vector<GridPlan>> gplans(G);
   std::vector<double> gwork(G, 0.0);
-  std::vector<std::vector<int>> grung_src(G);   // rung of each grid source
-  std::vector<std::pair<double, int32_t>> cand;
+  const bool diag = getenv("NC_HIER_DIAG") != nullptr;
+  double diag_cost = 0.0;
+  int64_t diag_groups2 = 0;
+  // groups are independent: host threads (OpenMP), results stored per group and concatenated in group order
+#pragma omp parallel for schedule(dynamic, 64) reduction(+ : diag_cost, diag_groups2)
   for (int64_t g = 0; g < G; ++g) {
+    std::vector<std::pair<double, int32_t>> cand;
     const int lvl = H->glevel[g];
     const double* cg = &H->gc[3 * g];
     const double R = H->gR[g];
@@ -812,62 +835,86 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     std::sort(cand.begin(), cand.end(), [](const std::pair<double, int32_t>& a, const std::pair<double, int32_t>& b) {
       return a.first > b.first || (a.first == b.first && a.second < b.second);
     });
-    // choose how many of the farthest sources go to the grid: cost in pair evaluations.  Grid sources use the
-    // outgoing-operator rung valid at their distance to the nearest grid point, gap = d - R = R (beta - 1) + eps
-    // (per-level recompression); the others are evaluated at the members' Zernike nodes.
+    // grid sources use the outgoing-operator rung valid at their distance to the nearest grid point,
+    // gap = d - R = R (beta - 1) + eps (per-level recompression)
+    const size_t nc = cand.size();
     const int p0 = h->rung_p[0];
-    std::vector<double> psum(cand.size() + 1, 0.0);   // sum of the rung sizes of the n farthest candidates
-    for (size_t n = 0; n < cand.size(); ++n) {
+    std::vector<int> rung_of(nc, 0);
+    std::vector<double> psum(nc + 1, 0.0);   // sum of the rung sizes of the n farthest candidates
+    for (size_t n = 0; n < nc; ++n) {
       const double gap = R * (cand[n].first - 1.0) + eps;
       int rung = 0;
       for (int k = 1; k < h->nrung; ++k)
         if (h->rung_r[k] <= gap * (1.0 - 1e-12)) rung = k;
+      rung_of[n] = rung;
       psum[n + 1] = psum[n] + h->rung_p[rung];
     }
-    double best_cost = c_near * (double)mem * Ks * cand.size() * p0;   // all direct
-    size_t best_n = 0;
-    int bnr = 0, bna = 0;
-    for (size_t n = 1; n <= cand.size(); ++n) {
-      const double beta = cand[n - 1].first;
-      if (beta < kBetaMin) break;
-      if (n < cand.size() && cand[n].first == beta) continue;
-      int nr, na;
-      grid_size(beta, tol, nr, na);
+    // a band [a, b) of the sorted candidates on one grid sized by cand[b - 1]: pair evaluations on its q points
+    // (each source with its own rung) + interpolation to the members' nodes + transform
+    auto band = [&](size_t a, size_t b, int& nr, int& na) {
+      grid_size(cand[b - 1].first, tol, nr, na);
       const double q = (double)nr * na;
-      // pair evaluations: grid sources on q points (each with its own rung), the rest at the members' Zernike
-      // nodes, plus the interpolation (~1.5 FMA per node per coefficient ~ 0.07 pair) and the transform
-      const double cost = q * psum[n] + c_near * (double)mem * Ks * (cand.size() - n) * p0 +
-                          c_interp * (double)mem * Ks * q + c_trans * q * (nr + na);
-      if (cost < best_cost) {
-        best_cost = cost;
-        best_n = n;
-        bnr = nr;
-        bna = na;
+      return q * (psum[b] - psum[a]) + c_interp * (double)mem * Ks * q + c_trans * q * (nr + na);
+    };
+    auto near_cost = [&](size_t b) { return c_near * (double)mem * Ks * (double)(nc - b) * p0; };
+    size_t n_ok = 0;   // candidates a grid may serve (beta >= kBetaMin)
+    while (n_ok < nc && cand[n_ok].first >= kBetaMin) ++n_ok;
+    double best_cost = near_cost(0);   // all direct
+    size_t cut1 = 0, cut2 = 0;         // bands [0, cut1) and [cut1, cut2); cut1 == 0: at most one grid [0, cut2)
+    for (size_t n = 1; n <= n_ok; ++n) {   // one grid: exhaustive over distinct betas
+      if (n < nc && cand[n].first == cand[n - 1].first) continue;
+      int nr, na;
+      const double c = band(0, n, nr, na) + near_cost(n);
+      if (c < best_cost) { best_cost = c; cut1 = 0; cut2 = n; }
+    }
+    if (max_grids >= 2 && n_ok >= 2) {     // two grids: cut points on quantiles of the servable candidates
+      std::vector<size_t> qs;
+      for (int k = 1; k <= kGridCutQuantiles; ++k) qs.push_back(std::max<size_t>(1, (n_ok * k) / kGridCutQuantiles));
+      qs.erase(std::unique(qs.begin(), qs.end()), qs.end());
+      for (size_t a1 : qs) {
+        int nr1, na1;
+        const double c1 = band(0, a1, nr1, na1);
+        if (c1 >= best_cost) continue;
+        for (size_t a2 : qs) {
+          if (a2 <= a1) continue;
+          int nr2, na2;
+          const double c = c1 + band(a1, a2, nr2, na2) + near_cost(a2);
+          if (c < best_cost) { best_cost = c; cut1 = a1; cut2 = a2; }
+        }
       }
     }
-    for (size_t n = 0; n < cand.size(); ++n) {
-      if (n < best_n) {
-        const double gap = R * (cand[n].first - 1.0) + eps;
-        int rung = 0;
-        for (int k = 1; k < h->nrung; ++k)
-          if (h->rung_r[k] <= gap * (1.0 - 1e-12)) rung = k;
-        gsrc[g].push_back(cand[n].second);
-        grung_src[g].push_back(rung);
-      } else {
-        nsrc[g].push_back(cand[n].second);
+    auto emit = [&](size_t a, size_t b) {
+      GridPlan gp;
+      gp.group = (int32_t)g;
+      grid_size(cand[b - 1].first, tol, gp.nr, gp.na);
+      for (size_t n = a; n < b; ++n) {
+        gp.src.push_back(cand[n].second);
+        gp.rung.push_back(rung_of[n]);
       }
-    }
+      gplans[g].push_back(std::move(gp));
+    };
+    if (cut1 > 0) emit(0, cut1);
+    if (cut2 > cut1) emit(cut1, cut2);
+    for (size_t n = cut2; n < nc; ++n) nsrc[g].push_back(cand[n].second);
     std::sort(nsrc[g].begin(), nsrc[g].end());
-    if (best_n) {
-      H->gnr[g] = bnr;
-      H->gna[g] = bna;
-    }
     gwork[g] = best_cost;
+    diag_cost += best_cost;
+    diag_groups2 += cut1 > 0;
   }
+  std::vector<GridPlan> plans;
+  H->ggrid0.assign(G + 1, 0);
+  for (int64_t g = 0; g < G; ++g) {
+    H->ggrid0[g] = (int64_t)plans.size();
+    for (GridPlan& gp : gplans[g]) plans.push_back(std::move(gp));
+  }
+  H->ggrid0[G] = (int64_t)plans.size();
+  if (diag)
+    fprintf(stderr, "[nc hier diag] cost %.4g, grids %zu, groups with two grids %lld, max grids %d\n", diag_cost,
+            plans.size(), (long long)diag_groups2, max_grids);
 
   // rungs in use: a global decision (identical on every rank, so the per-rung all-gathers match)
-  for (int64_t g = 0; g < G; ++g)
-    for (int r : grung_src[g]) h->rung_used[r] = 1;
+  for (const GridPlan& gp : plans)
+    for (int r : gp.rung) h->rung_used[r] = 1;
 
   // ---- partition: contiguous internal rows, weighted by work (world > 1) ----
   {
@@ -890,40 +937,47 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     const int64_t g0 = H->pgroup[(size_t)lvl * N + rb], g1 = H->pgroup[(size_t)lvl * N + re - 1];
     for (int64_t g = g0; g <= g1; ++g) rel[g] = 1;
   }
-  // grid offsets / coefficient offsets (relevant groups with a grid)
-  H->goff.assign(G + 1, 0);
-  H->coff.assign(G + 1, 0);
-  H->grid_groups.clear();
-  for (int64_t g = 0; g < G; ++g) {
+  // per-grid sizes and point / coefficient offsets (grids of irrelevant groups get no points)
+  const int64_t NG = (int64_t)plans.size();
+  H->ngrids = NG;
+  H->gnr.assign(NG, 0);
+  H->gna.assign(NG, 0);
+  H->grid_group.assign(NG, 0);
+  H->goff.assign(NG + 1, 0);
+  H->coff.assign(NG + 1, 0);
+  H->grid_ids.clear();
+  for (int64_t k = 0; k < NG; ++k) {
+    const GridPlan& gp = plans[k];
+    H->grid_group[k] = gp.group;
     int64_t q = 0, c = 0;
-    if (rel[g] && H->gnr[g] > 0) {
-      q = (int64_t)H->gnr[g] * H->gna[g];
-      c = (int64_t)(H->gna[g] / 2 + 1) * 2 * H->gnr[g];
-      H->grid_groups.push_back((int32_t)g);
+    if (rel[gp.group]) {
+      H->gnr[k] = gp.nr;
+      H->gna[k] = gp.na;
+      q = (int64_t)gp.nr * gp.na;
+      c = (int64_t)(gp.na / 2 + 1) * 2 * gp.nr;
+      H->grid_ids.push_back((int32_t)k);
       H->qmax = std::max<int>(H->qmax, (int)q);
       H->cmax = std::max<int>(H->cmax, (int)c);
-      H->namax = std::max<int>(H->namax, H->gna[g]);
-      H->nrmax = std::max<int>(H->nrmax, H->gnr[g]);
-    } else if (!rel[g]) {
-      H->gnr[g] = 0;
-      H->gna[g] = 0;
+      H->namax = std::max<int>(H->namax, gp.na);
+      H->nrmax = std::max<int>(H->nrmax, gp.nr);
     }
-    H->goff[g + 1] = H->goff[g] + q;
-    H->coff[g + 1] = H->coff[g] + c;
+    H->goff[k + 1] = H->goff[k] + q;
+    H->coff[k + 1] = H->coff[k] + c;
   }
-  H->Q = H->goff[G];
-  H->C = H->coff[G];
+  H->Q = H->goff[NG];
+  H->C = H->coff[NG];
 
   // work units (steps 2-3) and reduction chunks
   H->upts = grid_unit_points();
   std::vector<GridUnit> units;
   std::vector<ChunkRec> chunks;
   std::vector<int32_t> srclist;
-  for (int32_t g : H->grid_groups) {
-    const int64_t q = H->goff[g + 1] - H->goff[g];
+  for (int32_t k : H->grid_ids) {
+    const GridPlan& gp = plans[k];
+    const int64_t q = H->goff[k + 1] - H->goff[k];
     // grid sources bucketed by rung (sorted by patch within a bucket); slices never mix rungs
     std::vector<std::pair<int, int32_t>> rs;
-    for (size_t n = 0; n < gsrc[g].size(); ++n) rs.push_back({grung_src[g][n], gsrc[g][n]});
+    for (size_t n = 0; n < gp.src.size(); ++n) rs.push_back({gp.rung[n], gp.src[n]});
     std::sort(rs.begin(), rs.end());
     struct Slice { int64_t src0; int32_t nsrc; int rung; };
     std::vector<Slice> slices;
@@ -932,9 +986,8 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       size_t b = a;
       while (b < rs.size() && rs[b].first == rs[a].first) ++b;
       const int rung = rs[a].first;
-      h->rung_used[rung] = 1;
       const int64_t s0 = (int64_t)srclist.size();
-      for (size_t k = a; k < b; ++k) srclist.push_back(rs[k].second);
+      for (size_t k2 = a; k2 < b; ++k2) srclist.push_back(rs[k2].second);
       const int64_t ns = (int64_t)(b - a);
       const int64_t nsl = (ns + kSliceMax - 1) / kSliceMax;
       for (int64_t sl = 0; sl < nsl; ++sl) {
@@ -946,7 +999,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     }
     for (int64_t c0 = 0; c0 < q; c0 += H->upts) {
       ChunkRec cr;
-      cr.pt0 = H->goff[g] + c0;
+      cr.pt0 = H->goff[k] + c0;
       cr.npt = (int32_t)std::min<int64_t>(H->upts, q - c0);
       cr.u0 = (int64_t)units.size();
       cr.nu = (int32_t)slices.size();
@@ -987,7 +1040,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   for (int64_t i = rb; i < re; ++i)
     for (int lvl = 0; lvl <= L; ++lvl) {
       const int32_t g = H->pgroup[(size_t)lvl * N + i];
-      H->interp_terms += (double)Ks * H->gnr[g] * H->gna[g];
+      for (int64_t kg = H->ggrid0[g]; kg < H->ggrid0[g + 1]; ++kg) H->interp_terms += (double)Ks * H->gnr[kg] * H->gna[kg];
     }
   // tree lists for introspection (audit): (level, target group, source group)
   H->ilist_entries.clear();
@@ -1016,7 +1069,9 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_TRY(upload(h, &H->d_gna, H->gna, s));
   NC_TRY(upload(h, &H->d_goff, H->goff, s));
   NC_TRY(upload(h, &H->d_coff, H->coff, s));
-  NC_TRY(upload(h, &H->d_grid_groups, H->grid_groups, s));
+  NC_TRY(upload(h, &H->d_grid_ids, H->grid_ids, s));
+  NC_TRY(upload(h, &H->d_grid_group, H->grid_group, s));
+  NC_TRY(upload(h, &H->d_ggrid0, H->ggrid0, s));
   NC_TRY(upload(h, &H->d_units, units, s));
   NC_TRY(upload(h, &H->d_chunks, chunks, s));
   NC_TRY(upload(h, &H->d_srclist, srclist, s));
@@ -1038,10 +1093,10 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_TRY(halloc(h, &H->d_tz, rc * Ks));
   NC_TRY(halloc(h, &H->d_udir, rc * Ks));
   NC_TRY(halloc(h, &H->d_u, rc * Ks));
-  if (!H->grid_groups.empty())
-    k_grid_points<<<(unsigned)H->grid_groups.size(), 128, 0, s>>>(H->d_grid_groups, (int64_t)H->grid_groups.size(),
-                                                                  H->d_gframe, H->d_gR, H->d_gnr, H->d_gna,
-                                                                  H->d_goff, H->d_gx, H->d_gy, H->d_gz);
+  if (!H->grid_ids.empty())
+    k_grid_points<<<(unsigned)H->grid_ids.size(), 128, 0, s>>>(H->d_grid_ids, (int64_t)H->grid_ids.size(),
+                                                               H->d_grid_group, H->d_gframe, H->d_gR, H->d_gnr,
+                                                               H->d_gna, H->d_goff, H->d_gx, H->d_gy, H->d_gz);
   launch_targets(h->d_frames, rb, rc, h->d_zhat, Ks, 0.5, H->d_tx, H->d_ty, H->d_tz, s);
   NC_CUDA_TRY(cudaGetLastError());
   h->pairs_per_matvec = H->pairs_grid + H->pairs_near;
@@ -1062,10 +1117,10 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
     h->launches_last++;
   }
   // step 4a: grid samples -> coefficients
-  if (!H->grid_groups.empty()) {
+  if (!H->grid_ids.empty()) {
     const size_t shm = (size_t)(H->qmax + H->cmax + 2 * H->namax + 8 * H->nrmax) * sizeof(double);
     if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(k_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    k_transform<<<(unsigned)H->grid_groups.size(), 128, shm, s>>>(H->d_grid_groups, (int64_t)H->grid_groups.size(),
+    k_transform<<<(unsigned)H->grid_ids.size(), 128, shm, s>>>(H->d_grid_ids, (int64_t)H->grid_ids.size(),
                                                                    H->d_gnr, H->d_gna, H->d_goff, H->d_coff,
                                                                    H->d_gval, H->d_gcoef);
     h->launches_last++;
@@ -1078,8 +1133,8 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   // step 4b: interpolation to the Zernike nodes, summed over levels
   if (rc > 0) {
     const size_t shm = (size_t)std::max(H->cmax, 1) * sizeof(double);
-    NC_TRY(launch_interp(shm, H->L, rc, Ks, H->d_pgl, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef,
-                         H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u, s));
+    NC_TRY(launch_interp(shm, H->L, rc, Ks, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna,
+                         H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u, s));
     h->launches_last++;
   }
   // step 5: y = x + U P^T
@@ -1106,7 +1161,8 @@ void hier_fill_stats(const nc_handle* h, nc_stats_t* o) {
 void hier_destroy(nc_handle* h) {
   HierState* H = h->hier;
   if (!H) return;
-  void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_groups,
+  void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_ids,
+                  H->d_grid_group, H->d_ggrid0,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
                   H->d_chunks, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
                   H->d_udir, H->d_u};
