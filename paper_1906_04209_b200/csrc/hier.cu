@@ -35,7 +35,7 @@ namespace nc {
 
 constexpr int kLmax = 24;
 constexpr int kSliceMax = 32;          // source patches per grid work unit
-constexpr int kMaxGrids = 2;           // incoming grids per group (source bands by distance; R24)
+constexpr int kMaxGrids = 3;           // incoming grids per group (source bands by distance; R24)
 constexpr int kGridCutQuantiles = 48;  // candidate cut points of the two-grid search
 constexpr double kBetaMin = 1.45;      // smallest source distance / circle radius served by a grid
 constexpr double kCostNear = 1.0, kCostInterp = 0.07, kCostTransform = 0.1;   // grid-vs-near cost model
@@ -860,29 +860,48 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     size_t n_ok = 0;   // candidates a grid may serve (beta >= kBetaMin)
     while (n_ok < nc && cand[n_ok].first >= kBetaMin) ++n_ok;
     double best_cost = near_cost(0);   // all direct
-    size_t cut1 = 0, cut2 = 0;         // bands [0, cut1) and [cut1, cut2); cut1 == 0: at most one grid [0, cut2)
+    size_t cut2 = 0;                   // best single grid: [0, cut2)
     for (size_t n = 1; n <= n_ok; ++n) {   // one grid: exhaustive over distinct betas
       if (n < nc && cand[n].first == cand[n - 1].first) continue;
       int nr, na;
       const double c = band(0, n, nr, na) + near_cost(n);
-      if (c < best_cost) { best_cost = c; cut1 = 0; cut2 = n; }
+      if (c < best_cost) { best_cost = c; cut2 = n; }
     }
-    if (max_grids >= 2 && n_ok >= 2) {     // two grids: cut points on quantiles of the servable candidates
+    // K >= 2 bands: dynamic programme over cut points on kGridCutQuantiles quantiles of the servable candidates;
+    // a band ending at cut i lives on a grid sized by cand[cut_i - 1] (its q and overhead precomputed per cut)
+    std::vector<size_t> cuts;   // band boundaries chosen (ascending, last = end of the grid-served prefix)
+    if (max_grids >= 2 && n_ok >= 2) {
       std::vector<size_t> qs;
       for (int k = 1; k <= kGridCutQuantiles; ++k) qs.push_back(std::max<size_t>(1, (n_ok * k) / kGridCutQuantiles));
       qs.erase(std::unique(qs.begin(), qs.end()), qs.end());
-      for (size_t a1 : qs) {
-        int nr1, na1;
-        const double c1 = band(0, a1, nr1, na1);
-        if (c1 >= best_cost) continue;
-        for (size_t a2 : qs) {
-          if (a2 <= a1) continue;
-          int nr2, na2;
-          const double c = c1 + band(a1, a2, nr2, na2) + near_cost(a2);
-          if (c < best_cost) { best_cost = c; cut1 = a1; cut2 = a2; }
-        }
+      const int Q = (int)qs.size();
+      std::vector<double> qi(Q), ovh(Q);
+      for (int i = 0; i < Q; ++i) {
+        int nr, na;
+        grid_size(cand[qs[i] - 1].first, tol, nr, na);
+        qi[i] = (double)nr * na;
+        ovh[i] = c_interp * (double)mem * Ks * qi[i] + c_trans * qi[i] * (nr + na);
       }
+      // dp[k][i]: cheapest cover of [0, qs[i]) by k bands; from[k][i]: previous cut index (-1: band starts at 0)
+      std::vector<std::vector<double>> dp(max_grids + 1, std::vector<double>(Q, 1e300));
+      std::vector<std::vector<int>> from(max_grids + 1, std::vector<int>(Q, -1));
+      for (int i = 0; i < Q; ++i) dp[1][i] = qi[i] * psum[qs[i]] + ovh[i];
+      for (int k = 2; k <= max_grids; ++k)
+        for (int i = 1; i < Q; ++i)
+          for (int j = 0; j < i; ++j) {
+            const double c = dp[k - 1][j] + qi[i] * (psum[qs[i]] - psum[qs[j]]) + ovh[i];
+            if (c < dp[k][i]) { dp[k][i] = c; from[k][i] = j; }
+          }
+      int bk = 0, bi = -1;
+      for (int k = 2; k <= max_grids; ++k)
+        for (int i = 0; i < Q; ++i) {
+          const double c = dp[k][i] + near_cost(qs[i]);
+          if (c < best_cost) { best_cost = c; bk = k; bi = i; }
+        }
+      for (int k = bk, i = bi; k >= 1 && i >= 0; i = from[k][i], --k) cuts.push_back(qs[i]);
+      std::reverse(cuts.begin(), cuts.end());
     }
+    if (cuts.empty() && cut2 > 0) cuts.push_back(cut2);   // the best single grid
     auto emit = [&](size_t a, size_t b) {
       GridPlan gp;
       gp.group = (int32_t)g;
@@ -893,13 +912,16 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       }
       gplans[g].push_back(std::move(gp));
     };
-    if (cut1 > 0) emit(0, cut1);
-    if (cut2 > cut1) emit(cut1, cut2);
-    for (size_t n = cut2; n < nc; ++n) nsrc[g].push_back(cand[n].second);
+    size_t prev = 0;
+    for (size_t c : cuts) {
+      emit(prev, c);
+      prev = c;
+    }
+    for (size_t n = prev; n < nc; ++n) nsrc[g].push_back(cand[n].second);
     std::sort(nsrc[g].begin(), nsrc[g].end());
     gwork[g] = best_cost;
     diag_cost += best_cost;
-    diag_groups2 += cut1 > 0;
+    diag_groups2 += cuts.size() > 1;
   }
   std::vector<GridPlan> plans;
   H->ggrid0.assign(G + 1, 0);
@@ -909,7 +931,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   }
   H->ggrid0[G] = (int64_t)plans.size();
   if (diag)
-    fprintf(stderr, "[nc hier diag] cost %.4g, grids %zu, groups with two grids %lld, max grids %d\n", diag_cost,
+    fprintf(stderr, "[nc hier diag] cost %.4g, grids %zu, groups with several grids %lld, max grids %d\n", diag_cost,
             plans.size(), (long long)diag_groups2, max_grids);
 
   // rungs in use: a global decision (identical on every rank, so the per-rung all-gathers match)
