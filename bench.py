@@ -57,7 +57,7 @@ def load_fp64_peak():
 
 
 # ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
-TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01e_ncu_full_pairs_grid.json"}
+TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01f_ncu_full_pairs_grid.json"}
 
 
 def profiled_traffic(kernel, config, mode):
@@ -354,7 +354,8 @@ def main():
             "stages_ms": dict(zip(["T_apply", "all_gather", "direct_pairs", "P_apply", "grid_pairs", "hier_rest",
                                    "total"], stages_avg)), "pairs_per_matvec": st["pairs_per_matvec"],
             "hier": ({k: st[k] for k in ("tree_levels", "tree_groups", "hier_grid_pairs", "hier_near_pairs",
-                                         "hier_interp_terms", "hier_grid_points", "hier_grid_units", "hier_grid_fill")}
+                                         "hier_interp_terms", "hier_grid_points", "hier_grid_units", "hier_grid_fill",
+                                         "hier_grid_warp_fill")}
                      if args.mode == "hier" else None),
             "solve": solve}
     print(json.dumps(line), flush=True)

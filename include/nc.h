@@ -116,6 +116,7 @@ typedef struct nc_stats_t {
   double pair_fp64_flops_grid;   /*   for the direct / near-list kernels and for k_pairs_grid's       */
   double pair_fp64_inst_grid;    /*   variant in use (kind-dependent)                                */
   double hier_grid_fill;         /* NC_HIER: grid pairs / (work-unit thread slots x sources x p)     */
+  double hier_grid_warp_fill;    /* NC_HIER: grid pairs / (active-warp thread slots x sources x p)   */
 } nc_stats_t;
 
 typedef struct nc_handle nc_handle;

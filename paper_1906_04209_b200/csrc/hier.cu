@@ -36,9 +36,10 @@ namespace nc {
 constexpr int kLmax = 24;
 constexpr int kSliceMax = 32;          // source patches per grid work unit
 constexpr int kMaxGrids = 3;           // incoming grids per group (source bands by distance; R24)
-constexpr int kGridCutQuantiles = 48;  // candidate cut points of the two-grid search
+constexpr int kGridCutQuantiles = 48;  // candidate cut points of the multi-grid search
+constexpr int kGridThreadsForFill = 128;   // threads per grid-kernel CTA assumed by the warp-fill statistic
 constexpr double kBetaMin = 1.45;      // smallest source distance / circle radius served by a grid
-constexpr double kCostNear = 1.0, kCostInterp = 0.07, kCostTransform = 0.1;   // grid-vs-near cost model
+constexpr double kCostNear = 1.0, kCostInterp = 0.15, kCostTransform = 0.1;   // grid-vs-near cost model (grid-pair units)
 constexpr double kGridTolFactor = 1000.0;  // per-grid tolerance / requested precision (calibrated: DESIGN.md R21)
 
 struct ChunkRec {
@@ -92,7 +93,7 @@ struct HierState {
   int32_t* d_pgl = nullptr;         // (L+1) x row_count group ids of local patches
   double *d_tx = nullptr, *d_ty = nullptr, *d_tz = nullptr;
   double *d_udir = nullptr, *d_u = nullptr;
-  double pairs_grid = 0, pairs_near = 0, interp_terms = 0, slot_pairs = 0;
+  double pairs_grid = 0, pairs_near = 0, interp_terms = 0, slot_pairs = 0, warp_slot_pairs = 0;
   double bytes = 0;
   std::vector<int64_t> ilist_entries;   // host copies for nc_tree_lists: (level, target group, source group)
   std::vector<int64_t> nbr_entries;
@@ -545,13 +546,13 @@ __global__ void __launch_bounds__(NT) k_interp(int L, int64_t rc, int Kstar, con
   }
 }
 
-// interpolation variant: NC_INTERP_VARIANT="NT,NPT,MB"
+// interpolation variant: NC_INTERP_VARIANT="NT,NPT,MB" (k_interp<NT,NPT,MB>; default 128,4,1)
 struct InterpVariant {
   int nt, npt, mb;
 };
 static InterpVariant interp_variant() {
-  static InterpVariant v = {0, 0, 0};
-  if (v.nt == 0) {
+  static InterpVariant v = {-1, 0, 0};
+  if (v.nt < 0) {
     v = {128, 4, 1};
     if (const char* e = getenv("NC_INTERP_VARIANT")) {
       InterpVariant w = v;
@@ -572,11 +573,13 @@ static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t*
   return NC_OK;
 }
 
-static int launch_interp(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const int64_t* ggrid0,
-                         const double* F, const double* gR, const int32_t* gnr, const int32_t* gna,
-                         const int64_t* coff, const double* coef, const double* tx, const double* ty,
-                         const double* tz, const double* udir, double* u, cudaStream_t s) {
+static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int namax, const int32_t* pgl,
+                         const int64_t* ggrid0, const double* F, const double* gR, const int32_t* gnr,
+                         const int32_t* gna, const int64_t* coff, const double* coef, const double* tx,
+                         const double* ty, const double* tz, const double* udir, double* u, cudaStream_t s) {
   const InterpVariant v = interp_variant();
+  (void)nrmax;
+  (void)namax;
 #define NC_I(NT, NPT, MB)                                                                                  \
   if (v.nt == NT && v.npt == NPT && v.mb == MB)                                                            \
     return launch_interp_t<NT, NPT, MB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
@@ -1037,6 +1040,8 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         u.pad_ = 0;
         units.push_back(u);
         H->slot_pairs += (double)H->upts * u.nsrc * u.p;
+        const int wpts = 32 * (H->upts / kGridThreadsForFill);   // points per warp
+        H->warp_slot_pairs += (double)((u.npt + wpts - 1) / wpts) * wpts * u.nsrc * u.p;
       }
     }
   }
@@ -1155,8 +1160,8 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   // step 4b: interpolation to the Zernike nodes, summed over levels
   if (rc > 0) {
     const size_t shm = (size_t)std::max(H->cmax, 1) * sizeof(double);
-    NC_TRY(launch_interp(shm, H->L, rc, Ks, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna,
-                         H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u, s));
+    NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gR,
+                         H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u, s));
     h->launches_last++;
   }
   // step 5: y = x + U P^T
@@ -1178,6 +1183,7 @@ void hier_fill_stats(const nc_handle* h, nc_stats_t* o) {
   o->hier_grid_points = H->Q;
   o->hier_grid_units = H->nunits;
   o->hier_grid_fill = H->slot_pairs > 0 ? H->pairs_grid / H->slot_pairs : 0.0;
+  o->hier_grid_warp_fill = H->warp_slot_pairs > 0 ? H->pairs_grid / H->warp_slot_pairs : 0.0;
 }
 
 void hier_destroy(nc_handle* h) {

@@ -54,7 +54,7 @@ class NcStats(ctypes.Structure):
                 ("gmres_ortho_bytes", ctypes.c_double), ("gmres_ortho_iters", ctypes.c_int64),
                 ("pair_fp64_flops_direct", ctypes.c_double), ("pair_fp64_inst_direct", ctypes.c_double),
                 ("pair_fp64_flops_grid", ctypes.c_double), ("pair_fp64_inst_grid", ctypes.c_double),
-                ("hier_grid_fill", ctypes.c_double)]
+                ("hier_grid_fill", ctypes.c_double), ("hier_grid_warp_fill", ctypes.c_double)]
 
 
 EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt", "nc_stats",

@@ -38,7 +38,7 @@ for _ in range(3):
 np.save(os.environ["OUT"], y.cpu().numpy())
 print(json.dumps({"variant": os.environ.get("VARIANT"), "grid_ms": float(np.median(g)), "rest_ms": float(np.median(r)),
                   "matvec_ms": float(np.median(t)), "pairs": st["hier_grid_pairs"],
-                  "units": st["hier_grid_units"], "fill": st["hier_grid_fill"]}))
+                  "units": st["hier_grid_units"], "fill": st["hier_grid_fill"], "warp_fill": st["hier_grid_warp_fill"]}))
 """
 
 
