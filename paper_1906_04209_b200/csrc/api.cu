@@ -658,13 +658,14 @@ int nc_stats(const nc_handle* h, nc_stats_t* o) {
   o->gmres_ortho_bytes = h->gmres_ortho_bytes;
   o->gmres_ortho_iters = h->gmres_ortho_iters;
   // per-pair FP64 work of the pair kernels (green.cuh / pairs.cuh; SASS counts, checked against ncu's
-  // sass_thread_inst_executed_op_{dfma,dmul,dadd}): exact form 11 DFMA + 4 DMUL + 7 DADD (+1 DMUL interior);
+  // sass_thread_inst_executed_op_{dfma,dmul,dadd}): exact form 11 DFMA + 4 DMUL + 7 DADD exterior, 12 DFMA + 4 DMUL +
+  // 6 DADD interior;
   // far-field form (R23, green_far_h) 10 DFMA + 2 DMUL + 4 DADD exterior, 11 DFMA + 2 DMUL + 3 DADD interior
   const int interior = h->kind == NC_INTERIOR;
-  o->pair_fp64_inst_direct = 22 + interior;
+  o->pair_fp64_inst_direct = 22;
   o->pair_fp64_flops_direct = 33 + interior;
   const bool far = grid_far_variant() != 0;
-  o->pair_fp64_inst_grid = far ? 16 : 22 + interior;
+  o->pair_fp64_inst_grid = 22 - 6 * far;
   o->pair_fp64_flops_grid = far ? 26 + interior : 33 + interior;
   hier_fill_stats(h, o);
   return NC_OK;

@@ -6,16 +6,16 @@
 //   G_I = 2/d + log(2/d) - log(1 + d/2)      eq:Gintonsurface
 // Exact single-log rewrites used on the GPU: with w = 2/d and q = d^2/4,
 //   G_E = w - log(1 + w)                     since w (1 + d/2) = w + 1
-//   G_I = w - log(q (1 + w))                 since (2/d)/(1 + d/2) = 4/(d^2 + 2d) = 1/(q (1 + w))
+//   G_I = w - log(q (1 + w))                 since (2/d)/(1 + d/2) = 4/(d^2 + 2d) = 1/(q (1 + w)); q (1 + w) = fma(q, w, q)
 // Coordinates are stored pre-scaled by 1/2 (exact), so the squared distance of the scaled points IS q and
 // rsqrt(q) IS w: one reciprocal square root and one logarithm per pair, no division.
 //
 // fp64 rsqrt: MUFU.RSQ64H seed (rsqrt.approx.f64) + one third-order Newton correction
 //   e = 1 - q y^2,  y <- y + y e (1/2 + 3/8 e)                           (relative error ~ 2^-53)
 // fp64 log: x = 2^k m, m in [1,2); j = top 10 mantissa bits; c_j = 1/(1 + (j + 1/2)/1024) (table, smem);
-//   r = m c_j - 1 (one FMA, |r| <= 2^-11);  log x = k ln2 - log c_j + log1p(r),
+//   r = m c_j - 1 = x (c_j 2^-k) - 1 (one FMA, |r| <= 2^-11);  log x = k ln2 - log c_j + log1p(r),
 //   log1p(r) = r + r^2 (-1/2 + r/3 - r^2/4)   (truncation |r|^5/5 < 6e-18)
-// 22 FP64-pipe instructions per exterior pair (23 interior) instead of ~45 with libdevice log + rsqrt.
+// 22 FP64-pipe instructions per pair (both kinds) instead of ~45 with libdevice log + rsqrt.
 #pragma once
 
 #include <stdint.h>
@@ -50,17 +50,18 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
   return fma(ye, c, y);
 }
 
-// fp64 natural log for positive normal x (absolute error ~1e-16 |log x| + 1e-17)
+// fp64 natural log for positive normal x (absolute error ~1e-16 |log x| + 1e-17).  The table's c_j is rescaled by
+// 2^-k with an integer subtract on its exponent field (x c_j 2^-k = m c_j exactly), so the mantissa m is never
+// formed: r = fma(x, c_j 2^-k, -1) equals fma(m, c_j, -1) bit for bit.
 __device__ __forceinline__ double fast_log(double x, const double2* __restrict__ tbl) {
   const int hi = __double2hiint(x);
-  const int lo = __double2loint(x);
   const int j = (hi >> (20 - kLogTableBits)) & (kLogTableSize - 1);
-  const double m = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
   // exponent k as a double without a conversion instruction: 2^52 + 2^31 + k  minus the magic
   const double kd = __hiloint2double(0x43300000, (int)(((unsigned)hi >> 20) - 1023u + 0x80000000u)) -
                     4503601774854144.0;   // 2^52 + 2^31
   const double2 t = tbl[j];
-  const double r = fma(m, t.x, -1.0);
+  const double c = __hiloint2double(__double2hiint(t.x) - (hi & 0x7FF00000) + 0x3FF00000, __double2loint(t.x));
+  const double r = fma(x, c, -1.0);
   double p = fma(r, -0.25, 0.33333333333333333333);
   p = fma(p, r, -0.5);
   const double r2 = r * r;
@@ -78,9 +79,8 @@ __device__ __forceinline__ void init_table(Tab* tbl, const Tab* __restrict__ src
 template <int KIND, class Tab>
 __device__ __forceinline__ double green_q(double q, const Tab* __restrict__ tbl) {
   const double w = fast_rsqrt(q);   // 2/d
-  const double a = 1.0 + w;
-  if (KIND == 1) return w - fast_log(a, tbl);
-  return w - fast_log(q * a, tbl);
+  if (KIND == 1) return w - fast_log(1.0 + w, tbl);
+  return w - fast_log(fma(q, w, q), tbl);   // q (1 + w), one rounding
 }
 
 // Far-field G (k_pairs_grid FAR variant, hierarchical mode only; R23), from qh = |x - x'|^2 / 8 (half the

@@ -67,7 +67,7 @@ struct HierState {
   std::vector<int32_t> gnr, gna, grid_group;
   std::vector<int64_t> goff, coff;  // ngrids+1 point / coefficient offsets (0-sized for other ranks' groups)
   int64_t Q = 0, C = 0;
-  int qmax = 0, cmax = 0, pmax = 0, namax = 0, nrmax = 0;
+  int qmax = 0, cmax = 0, pmax = 0, namax = 0, nrmax = 0, cgroupmax = 0;
   std::vector<int32_t> grid_ids;    // grids with points on this rank
   // device
   int64_t* d_keys = nullptr;
@@ -434,13 +434,14 @@ __global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, cons
   }
 }
 
-// step 4b: u_i(node) = udir + sum over levels of the level's group expansion at the node,
+// step 4b: u_i(node) = udir + sum over levels of the level's group expansions at the node,
 //   u(x, theta) = sum_m sum_j c[m][j] . (cos m theta, sin m theta) T_{(m & 1) + 2 j}(rho / R)
-// (rho = geodesic distance from the cap centre).  One CTA of NT threads per target patch, NPT nodes per thread.  The
-// m loop runs in blocks of MB orders: inside a block the j loop advances BOTH parity sequences T_{2j}, T_{2j+1}
-// once (2 FMA) and feeds MB (A_m, B_m) accumulator pairs, so the Chebyshev recurrence is shared by the block's
-// orders (2 + 2/MB FMA per coefficient pair instead of 3); every coefficient pair is one broadcast shared-memory load
-// reused by the thread's NPT nodes.
+// (rho = geodesic distance from the cap centre).  One CTA of NT threads per target patch, NPT nodes per thread.
+// Per level, the coefficients of all the group's grids (<= kMaxGrids) are staged in shared memory in one pass and
+// the node geometry (rho / R, theta) is computed once; then, per grid and order m, the j loop advances the
+// parity's Chebyshev recurrence T_{n+2} = w2 T_n - T_{n-2} and accumulates both trig components from one broadcast
+// shared-memory load of the coefficient pair (3 FMA per (m, j, node)).  MB > 1: MB orders per j loop (both parity
+// recurrences advanced once, 2 + 2/MB FMA per pair; measured slower at C5, kept selectable).
 template <int NT, int NPT, int MB>
 __global__ void __launch_bounds__(NT) k_interp(int L, int64_t rc, int Kstar, const int32_t* __restrict__ pgl,
                                                const int64_t* __restrict__ ggrid0,
@@ -461,19 +462,24 @@ __global__ void __launch_bounds__(NT) k_interp(int L, int64_t rc, int Kstar, con
       px[q] = 2.0 * tx[t]; py[q] = 2.0 * ty[t]; pz[q] = 2.0 * tz[t];
       acc[q] = udir ? udir[t] : 0.0;
     }
-    for (int lvl = 0; lvl <= L; ++lvl)
-    for (int64_t kg = ggrid0[pgl[(int64_t)lvl * rc + i]]; kg < ggrid0[pgl[(int64_t)lvl * rc + i] + 1]; ++kg) {
-      const int g = pgl[(int64_t)lvl * rc + i];   // group (frame, radius); kg: one of its grids
-      const int nr = gnr[kg], na = gna[kg];
-      if (nr == 0) continue;   // block-uniform
-      const int M = na / 2, ncp = (M + 1) * nr;
-      __syncthreads();
-      const double2* __restrict__ src = reinterpret_cast<const double2*>(coef + coff[kg]);
-      for (int t = threadIdx.x; t < ncp; t += NT) c2[t] = src[t];
+    for (int lvl = 0; lvl <= L; ++lvl) {
+      const int g = pgl[(int64_t)lvl * rc + i];
+      const int64_t kg0 = ggrid0[g], kg1 = ggrid0[g + 1];
+      if (kg0 == kg1 || gnr[kg0] == 0) continue;   // block-uniform (a group's grids are all local or none)
+      __syncthreads();                              // previous level's readers of c2 are done
+      {
+        int base = 0;
+        for (int64_t kg = kg0; kg < kg1; ++kg) {
+          const int ncp = (gna[kg] / 2 + 1) * gnr[kg];
+          const double2* __restrict__ src = reinterpret_cast<const double2*>(coef + coff[kg]);
+          for (int t = threadIdx.x; t < ncp; t += NT) c2[base + t] = src[t];
+          base += ncp;
+        }
+      }
       __syncthreads();
       const double* r9 = F + 9 * (int64_t)g;
       const double invR = 1.0 / gR[g];
-      double x[NPT], w2[NPT], c1[NPT], cm[NPT], sm[NPT], cmm[NPT], smm[NPT];
+      double x[NPT], w2[NPT], c1[NPT], s1[NPT];
 #pragma unroll
       for (int q = 0; q < NPT; ++q) {
         const double sx = r9[0] * px[q] + r9[1] * py[q] + r9[2] * pz[q];
@@ -483,57 +489,97 @@ __global__ void __launch_bounds__(NT) k_interp(int L, int64_t rc, int Kstar, con
         x[q] = atan2(rho, cz) * invR;
         const double irho = rho > 0 ? 1.0 / rho : 0.0;
         c1[q] = rho > 0 ? sx * irho : 1.0;
-        const double s1 = rho > 0 ? sy * irho : 0.0;
+        s1[q] = rho > 0 ? sy * irho : 0.0;
         w2[q] = 4.0 * x[q] * x[q] - 2.0;
-        cm[q] = 1.0; sm[q] = 0.0; cmm[q] = c1[q]; smm[q] = -s1;   // cos/sin(m theta), ((m - 1) theta)
       }
-      for (int m0 = 0; m0 <= M; m0 += MB) {
-        double A[MB][NPT], B[MB][NPT], te[NPT], tep[NPT], to[NPT], top[NPT];
-        // j = 0: T_0 = 1, T_1 = x; the step-2 recurrence T_{n+2} = w2 T_n - T_{n-2} (w2 = 2 T_2) starts from
-        // T_{-2} = T_2 and T_{-1} = T_1 (T_{-n} = T_n)
+      int base = 0;
+      for (int64_t kg = kg0; kg < kg1; ++kg) {
+        const int nr = gnr[kg], M = gna[kg] / 2;
+        const double2* __restrict__ cg = c2 + base;
+        base += (M + 1) * nr;
+        double cm[NPT], sm[NPT], cmm[NPT], smm[NPT];   // cos/sin(m theta), ((m - 1) theta)
 #pragma unroll
-        for (int q = 0; q < NPT; ++q) {
-          te[q] = 1.0; tep[q] = 2.0 * x[q] * x[q] - 1.0;
-          to[q] = x[q]; top[q] = x[q];
-        }
-#pragma unroll
-        for (int b = 0; b < MB; ++b) {
-          const int m = m0 + b;
-          const double2 c = (m <= M) ? c2[m * nr] : make_double2(0.0, 0.0);
-#pragma unroll
-          for (int q = 0; q < NPT; ++q) {
-            const double tv = (m & 1) ? to[q] : te[q];
-            A[b][q] = c.x * tv;
-            B[b][q] = c.y * tv;
-          }
-        }
-        for (int j = 1; j < nr; ++j) {
-#pragma unroll
-          for (int q = 0; q < NPT; ++q) {   // advance: te = T_{2j}, to = T_{2j+1}
-            const double ne = fma(w2[q], te[q], -tep[q]);
-            const double no = fma(w2[q], to[q], -top[q]);
-            tep[q] = te[q]; te[q] = ne;
-            top[q] = to[q]; to[q] = no;
-          }
-#pragma unroll
-          for (int b = 0; b < MB; ++b) {
-            const int m = m0 + b;
-            const double2 c = (m <= M) ? c2[m * nr + j] : make_double2(0.0, 0.0);
+        for (int q = 0; q < NPT; ++q) { cm[q] = 1.0; sm[q] = 0.0; cmm[q] = c1[q]; smm[q] = -s1[q]; }
+        if (MB == 1) {
+          for (int m = 0; m <= M; ++m) {
+            const double2* __restrict__ cmj = cg + m * nr;
+            double A[NPT], B[NPT], t0[NPT], t1[NPT];
+            const double2 c0 = cmj[0];
 #pragma unroll
             for (int q = 0; q < NPT; ++q) {
-              const double tv = (m & 1) ? to[q] : te[q];
-              A[b][q] = fma(c.x, tv, A[b][q]);
-              B[b][q] = fma(c.y, tv, B[b][q]);
+              t0[q] = (m & 1) ? x[q] : 1.0;
+              t1[q] = (m & 1) ? x[q] * (4.0 * x[q] * x[q] - 3.0) : 2.0 * x[q] * x[q] - 1.0;
+              A[q] = c0.x * t0[q];
+              B[q] = c0.y * t0[q];
+            }
+#pragma unroll 2
+            for (int j = 1; j < nr; ++j) {
+              const double2 c = cmj[j];
+#pragma unroll
+              for (int q = 0; q < NPT; ++q) {
+                A[q] = fma(c.x, t1[q], A[q]);
+                B[q] = fma(c.y, t1[q], B[q]);
+                const double t2 = fma(w2[q], t1[q], -t0[q]);
+                t0[q] = t1[q];
+                t1[q] = t2;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < NPT; ++q) {
+              acc[q] = fma(A[q], cm[q], fma(B[q], sm[q], acc[q]));
+              const double cn = 2.0 * c1[q] * cm[q] - cmm[q], sn = 2.0 * c1[q] * sm[q] - smm[q];
+              cmm[q] = cm[q]; smm[q] = sm[q]; cm[q] = cn; sm[q] = sn;
             }
           }
-        }
+        } else {
+          for (int m0 = 0; m0 <= M; m0 += MB) {
+            double A[MB][NPT], B[MB][NPT], te[NPT], tep[NPT], to[NPT], top[NPT];
+            // T_0 = 1, T_1 = x; the step-2 recurrence starts from T_{-2} = T_2 and T_{-1} = T_1 (T_{-n} = T_n)
 #pragma unroll
-        for (int b = 0; b < MB; ++b) {
+            for (int q = 0; q < NPT; ++q) {
+              te[q] = 1.0; tep[q] = 2.0 * x[q] * x[q] - 1.0;
+              to[q] = x[q]; top[q] = x[q];
+            }
 #pragma unroll
-          for (int q = 0; q < NPT; ++q) {
-            acc[q] = fma(A[b][q], cm[q], fma(B[b][q], sm[q], acc[q]));
-            const double cn = 2.0 * c1[q] * cm[q] - cmm[q], sn = 2.0 * c1[q] * sm[q] - smm[q];
-            cmm[q] = cm[q]; smm[q] = sm[q]; cm[q] = cn; sm[q] = sn;
+            for (int b = 0; b < MB; ++b) {
+              const int m = m0 + b;
+              const double2 c = (m <= M) ? cg[m * nr] : make_double2(0.0, 0.0);
+#pragma unroll
+              for (int q = 0; q < NPT; ++q) {
+                const double tv = (m & 1) ? to[q] : te[q];
+                A[b][q] = c.x * tv;
+                B[b][q] = c.y * tv;
+              }
+            }
+            for (int j = 1; j < nr; ++j) {
+#pragma unroll
+              for (int q = 0; q < NPT; ++q) {   // advance: te = T_{2j}, to = T_{2j+1}
+                const double ne = fma(w2[q], te[q], -tep[q]);
+                const double no = fma(w2[q], to[q], -top[q]);
+                tep[q] = te[q]; te[q] = ne;
+                top[q] = to[q]; to[q] = no;
+              }
+#pragma unroll
+              for (int b = 0; b < MB; ++b) {
+                const int m = m0 + b;
+                const double2 c = (m <= M) ? cg[m * nr + j] : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int q = 0; q < NPT; ++q) {
+                  const double tv = (m & 1) ? to[q] : te[q];
+                  A[b][q] = fma(c.x, tv, A[b][q]);
+                  B[b][q] = fma(c.y, tv, B[b][q]);
+                }
+              }
+            }
+#pragma unroll
+            for (int b = 0; b < MB; ++b) {
+#pragma unroll
+              for (int q = 0; q < NPT; ++q) {
+                acc[q] = fma(A[b][q], cm[q], fma(B[b][q], sm[q], acc[q]));
+                const double cn = 2.0 * c1[q] * cm[q] - cmm[q], sn = 2.0 * c1[q] * sm[q] - smm[q];
+                cmm[q] = cm[q]; smm[q] = sm[q]; cm[q] = cn; sm[q] = sn;
+              }
+            }
           }
         }
       }
@@ -583,7 +629,7 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
 #define NC_I(NT, NPT, MB)                                                                                  \
   if (v.nt == NT && v.npt == NPT && v.mb == MB)                                                            \
     return launch_interp_t<NT, NPT, MB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
-  NC_I(128, 4, 1) NC_I(256, 1, 4)
+  NC_I(128, 4, 1) NC_I(256, 2, 1) NC_I(512, 1, 1) NC_I(256, 1, 4) NC_I(256, 2, 4)
 #undef NC_I
   return launch_interp_t<128, 4, 1>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
 }
@@ -846,9 +892,9 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     std::vector<double> psum(nc + 1, 0.0);   // sum of the rung sizes of the n farthest candidates
     for (size_t n = 0; n < nc; ++n) {
       const double gap = R * (cand[n].first - 1.0) + eps;
-      int rung = 0;
+      int rung = 0;   // the smallest skeleton among the rungs valid on the whole grid (r_k <= gap)
       for (int k = 1; k < h->nrung; ++k)
-        if (h->rung_r[k] <= gap * (1.0 - 1e-12)) rung = k;
+        if (h->rung_r[k] <= gap * (1.0 - 1e-12) && h->rung_p[k] <= h->rung_p[rung]) rung = k;
       rung_of[n] = rung;
       psum[n + 1] = psum[n] + h->rung_p[rung];
     }
@@ -991,9 +1037,12 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   }
   H->Q = H->goff[NG];
   H->C = H->coff[NG];
+  for (int64_t g = 0; g < G; ++g)
+    H->cgroupmax = std::max<int>(H->cgroupmax, (int)(H->coff[H->ggrid0[g + 1]] - H->coff[H->ggrid0[g]]));
 
   // work units (steps 2-3) and reduction chunks
   H->upts = grid_unit_points();
+  std::vector<double> rung_pairs(h->nrung, 0.0);
   std::vector<GridUnit> units;
   std::vector<ChunkRec> chunks;
   std::vector<int32_t> srclist;
@@ -1020,6 +1069,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         slices.push_back({x0, (int32_t)(x1 - x0), rung});
       }
       H->pairs_grid += (double)q * ns * h->rung_p[rung];
+      rung_pairs[rung] += (double)q * ns * h->rung_p[rung];
       a = b;
     }
     for (int64_t c0 = 0; c0 < q; c0 += H->upts) {
@@ -1044,6 +1094,11 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         H->warp_slot_pairs += (double)((u.npt + wpts - 1) / wpts) * wpts * u.nsrc * u.p;
       }
     }
+  }
+  if (diag) {
+    fprintf(stderr, "[nc hier diag] grid pairs by rung (r/eps: pairs):");
+    for (int k = 0; k < h->nrung; ++k) fprintf(stderr, " %.3g:%.3g", h->rung_r[k] / eps, rung_pairs[k]);
+    fprintf(stderr, "\n");
   }
   // near lists for local patches (concatenated over levels)
   std::vector<int64_t> near_off(rc + 1, 0);
@@ -1159,7 +1214,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   h->launches_last += H->nwork_near > 0;
   // step 4b: interpolation to the Zernike nodes, summed over levels
   if (rc > 0) {
-    const size_t shm = (size_t)std::max(H->cmax, 1) * sizeof(double);
+    const size_t shm = (size_t)std::max(H->cgroupmax, 1) * sizeof(double);   // all grids of one group
     NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gR,
                          H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u, s));
     h->launches_last++;

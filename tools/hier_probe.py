@@ -7,7 +7,7 @@ from nc_inputs import CONFIGS, random_coeffs
 from nc_inputs.tables import load_tables
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 cfg = CONFIGS[name]
-tab = load_tables(f"tables/data/{name}.npz")
+tab = load_tables(os.environ.get("NC_TABLES_FILE") or f"tables/data/{name}.npz")
 c = cfg.centers()
 t0 = time.time()
 h = nc.Handle(cfg.kind, c, cfg.eps, tab, mode=nc.NC_HIER, precision=cfg.precision)

@@ -22,7 +22,7 @@ import paper_1906_04209_b200 as nc
 from nc_inputs import CONFIGS, random_coeffs
 from nc_inputs.tables import load_tables
 cfg = CONFIGS[os.environ["CFG"]]
-tab = load_tables(os.path.join(os.environ["ROOT"], "tables", "data", cfg.name + ".npz"))
+tab = load_tables(os.environ.get("NC_TABLES_FILE") or os.path.join(os.environ["ROOT"], "tables", "data", cfg.name + ".npz"))
 h = nc.Handle(cfg.kind, cfg.centers(), cfg.eps, tab, mode=nc.NC_HIER, precision=cfg.precision)
 x = torch.from_numpy(h.to_internal(random_coeffs(cfg.N, tab.K, 2000 + int(cfg.name[1:])))).cuda()
 y = torch.empty_like(x)

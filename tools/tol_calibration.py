@@ -39,7 +39,8 @@ def main():
     name = sys.argv[1]
     facs = [float(v) for v in sys.argv[2:]] or [300.0]
     cfg = CONFIGS[name]
-    tab = load_tables(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tables", "data",
+    tab = load_tables(os.environ.get("NC_TABLES_FILE") or
+                      os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tables", "data",
                                    f"{name}.npz"))
     c = cfg.centers()
     xs = [random_coeffs(cfg.N, tab.K, 7), np.tile(tab.P @ np.ones(tab.Kstar), (cfg.N, 1))]
