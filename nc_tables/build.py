@@ -24,7 +24,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20, n_theta: int = 64,
                  id_tol: float = 1e-11, zn_r: int | None = None, zn_theta: int | None = None, verbose=False,
-                 ladder: bool = True, ladder_max: float = 1.2, ladder_ratio: float = 2.0):
+                 ladder: bool = True, ladder_max: float = 1.2, ladder_ratio: float = 2.0 ** (1.0 / 3.0),
+                 ladder_id_tol: float | None = 1e-10):
     t0 = time.time()
     op = solve_onepatch(kind, eps, M, npan, k, n_theta)
     t1 = time.time()
@@ -39,13 +40,14 @@ def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20
     I = wf @ B
     err = outgoing_error(kind, fine, wf, B, shat, T, eps)
     # per-level recompression ("one matrix T per level"): a ladder of far-field regions
-    # {arc > r_k}, r_k = 2 eps ladder_ratio^k, each with its own ID against a training grid on that region
+    # {arc > r_k}, r_k = 2 eps ladder_ratio^k (default 2^(1/3)), each with its own ID against a training grid on that
+    # region at the ladder tolerance (default 1e-10: SURVEY.md A10 "per-level T_l at 1e-10"; the base T keeps id_tol)
     lad_r, lad_p, lad_s, lad_T, lad_err = [], [], [], [], []
     if ladder:
         rung = 1
         while 2.0 * eps * ladder_ratio ** rung < ladder_max:
             inner = 2.0 * ladder_ratio ** rung
-            Jk, Pik = interp_decomp(kind, training_grid(eps, inner=inner), fine, id_tol)
+            Jk, Pik = interp_decomp(kind, training_grid(eps, inner=inner), fine, ladder_id_tol or id_tol)
             Tk = Pik @ (wf[:, None] * B)
             lad_r.append(inner * eps)
             lad_p.append(len(Jk))
@@ -55,7 +57,7 @@ def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20
             rung += 1
     t3 = time.time()
     meta = dict(kind=kind, eps=eps, M=M, npan=npan, k=k, n_theta=n_theta, id_tol=id_tol, p=len(J), n_f=len(wf),
-                ladder_ratio=ladder_ratio,
+                ladder_ratio=ladder_ratio, ladder_id_tol=ladder_id_tol or id_tol,
                 n_train=len(train), outgoing_rel_err=err, t_onepatch_s=t1 - t0, t_id_s=t2 - t1,
                 ladder_r=lad_r, ladder_p=lad_p, ladder_err=lad_err, t_ladder_s=t3 - t2)
     if verbose:
@@ -80,7 +82,8 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--configs", action="store_true")
     ap.add_argument("--id-tol", type=float, default=1e-11)
-    ap.add_argument("--ladder-ratio", type=float, default=2.0)
+    ap.add_argument("--ladder-ratio", type=float, default=2.0 ** (1.0 / 3.0))
+    ap.add_argument("--ladder-id-tol", type=float, default=1e-10)
     a = ap.parse_args()
     outdir = os.path.join(ROOT, "tables", "data")
     os.makedirs(outdir, exist_ok=True)
@@ -88,10 +91,12 @@ def main():
         sys.path.insert(0, ROOT)
         from nc_inputs import CONFIGS
         for name, cfg in CONFIGS.items():
-            d = build_tables(cfg.kind, cfg.eps, id_tol=a.id_tol, verbose=True, ladder_ratio=a.ladder_ratio)
+            d = build_tables(cfg.kind, cfg.eps, id_tol=a.id_tol, verbose=True, ladder_ratio=a.ladder_ratio,
+                             ladder_id_tol=a.ladder_id_tol)
             save(d, os.path.join(outdir, f"{name}.npz"))
         return
-    d = build_tables(a.kind, a.eps, id_tol=a.id_tol, verbose=True, ladder_ratio=a.ladder_ratio)
+    d = build_tables(a.kind, a.eps, id_tol=a.id_tol, verbose=True, ladder_ratio=a.ladder_ratio,
+                     ladder_id_tol=a.ladder_id_tol)
     save(d, a.out or os.path.join(outdir, f"k{a.kind}_eps{a.eps:g}.npz"))
 
 

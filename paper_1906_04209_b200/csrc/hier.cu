@@ -442,8 +442,8 @@ __global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, cons
 // parity's Chebyshev recurrence T_{n+2} = w2 T_n - T_{n-2} and accumulates both trig components from one broadcast
 // shared-memory load of the coefficient pair (3 FMA per (m, j, node)).  MB > 1: MB orders per j loop (both parity
 // recurrences advanced once, 2 + 2/MB FMA per pair; measured slower at C5, kept selectable).
-template <int NT, int NPT, int MB>
-__global__ void __launch_bounds__(NT) k_interp(int L, int64_t rc, int Kstar, const int32_t* __restrict__ pgl,
+template <int NT, int NPT, int MB, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Kstar, const int32_t* __restrict__ pgl,
                                                const int64_t* __restrict__ ggrid0,
                                                const double* __restrict__ F, const double* __restrict__ gR,
                                                const int32_t* __restrict__ gnr, const int32_t* __restrict__ gna,
@@ -594,26 +594,27 @@ __global__ void __launch_bounds__(NT) k_interp(int L, int64_t rc, int Kstar, con
 
 // interpolation variant: NC_INTERP_VARIANT="NT,NPT,MB" (k_interp<NT,NPT,MB>; default 128,4,1)
 struct InterpVariant {
-  int nt, npt, mb;
+  int nt, npt, mb, minb;
 };
 static InterpVariant interp_variant() {
-  static InterpVariant v = {-1, 0, 0};
+  static InterpVariant v = {-1, 0, 0, 0};
   if (v.nt < 0) {
-    v = {128, 4, 1};
+    v = {128, 4, 1, 5};
     if (const char* e = getenv("NC_INTERP_VARIANT")) {
       InterpVariant w = v;
-      if (sscanf(e, "%d,%d,%d", &w.nt, &w.npt, &w.mb) == 3) v = w;
+      w.minb = 1;
+      if (sscanf(e, "%d,%d,%d,%d", &w.nt, &w.npt, &w.mb, &w.minb) >= 3) v = w;
     }
   }
   return v;
 }
 
-template <int NT, int NPT, int MB>
+template <int NT, int NPT, int MB, int MINB>
 static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const int64_t* ggrid0,
                            const double* F, const double* gR, const int32_t* gnr, const int32_t* gna,
                            const int64_t* coff, const double* coef, const double* tx, const double* ty,
                            const double* tz, const double* udir, double* u, cudaStream_t s) {
-  auto kern = k_interp<NT, NPT, MB>;
+  auto kern = k_interp<NT, NPT, MB, MINB>;
   if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u);
   return NC_OK;
@@ -626,12 +627,12 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
   const InterpVariant v = interp_variant();
   (void)nrmax;
   (void)namax;
-#define NC_I(NT, NPT, MB)                                                                                  \
-  if (v.nt == NT && v.npt == NPT && v.mb == MB)                                                            \
-    return launch_interp_t<NT, NPT, MB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
-  NC_I(128, 4, 1) NC_I(256, 2, 1) NC_I(512, 1, 1) NC_I(256, 1, 4) NC_I(256, 2, 4)
+#define NC_I(NT, NPT, MB, MINB)                                                                             \
+  if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                           \
+    return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
+  NC_I(128, 4, 1, 1) NC_I(128, 4, 1, 4) NC_I(128, 4, 1, 5) NC_I(256, 2, 1, 1) NC_I(256, 1, 4, 1) NC_I(128, 4, 2, 3)
 #undef NC_I
-  return launch_interp_t<128, 4, 1>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
+  return launch_interp_t<128, 4, 1, 5>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
 }
 
 // ------------------------------------------------------------------------------------------------
