@@ -320,6 +320,36 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   }
   if ((rc = ensure_red(h, 4096))) return bail(rc);
 
+  // fused K1 over the rungs in use (several rungs: one GEMM with a column map instead of one GEMM per rung)
+  {
+    int nused = 0, ncat = 0;
+    for (int k = 0; k < h->nrung; ++k)
+      if (h->rung_used[k]) { ++nused; ncat += h->rung_p[k]; }
+    if (nused > 1) {
+      std::vector<int64_t> cb, cr;
+      std::vector<double> Tc;
+      std::vector<double> Th((size_t)(h->rung_trow[h->nrung - 1] + h->rung_p[h->nrung - 1]) * K);
+      NC_CUDA_TRY(cudaMemcpyAsync(Th.data(), h->d_T, Th.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+      NC_CUDA_TRY(cudaStreamSynchronize(s));
+      for (int k = 0; k < h->nrung; ++k) {
+        if (!h->rung_used[k]) continue;
+        const int pk = h->rung_p[k];
+        for (int m = 0; m < pk; ++m) {
+          cb.push_back(h->rung_soff[k] + 4 * (int64_t)m + 3);
+          cr.push_back(4 * (int64_t)pk);
+        }
+        Tc.insert(Tc.end(), Th.begin() + (size_t)h->rung_trow[k] * K, Th.begin() + (size_t)(h->rung_trow[k] + pk) * K);
+      }
+      if ((rc = dalloc(h, &h->d_Tcat, Tc.size())) || (rc = dalloc(h, &h->d_colbase, cb.size())) ||
+          (rc = dalloc(h, &h->d_colrstride, cr.size())))
+        return bail(rc);
+      UP(h->d_Tcat, Tc.data(), Tc.size());
+      NC_CUDA_TRY(cudaMemcpyAsync(h->d_colbase, cb.data(), cb.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      NC_CUDA_TRY(cudaMemcpyAsync(h->d_colrstride, cr.data(), cr.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      h->ncat = ncat;
+    }
+  }
+
   h->emulated = h->world > 1 && !opt->nccl_id;   // rank emulation: no communicator, nc_matvec_emulated only
 #if NC_WITH_NCCL
   if (h->world > 1 && !h->emulated) {
@@ -362,6 +392,11 @@ static inline void mark(nc_handle* h, int i, cudaStream_t s) {
 // written into the records' 4th slot
 static void outgoing(nc_handle* h, const double* x, int64_t r0, int64_t nr, cudaStream_t s) {
   const int K = h->K;
+  if (h->ncat > 0) {   // all rungs in use in one GEMM (scattered epilogue)
+    launch_gemm_dmma_colmap(x, K, h->d_Tcat, nr, h->ncat, K, h->d_src4, h->d_colbase, h->d_colrstride, r0, s);
+    h->launches_last++;
+    return;
+  }
   for (int k = 0; k < h->nrung; ++k) {
     if (!h->rung_used[k]) continue;
     const int pk = h->rung_p[k];
@@ -696,9 +731,11 @@ void nc_destroy(nc_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   hier_destroy(h);
   double* bufs[] = {h->d_T, h->d_P, h->d_I, h->d_zhat, h->d_shat, h->d_centers, h->d_frames, h->d_tx, h->d_ty,
-                    h->d_tz, h->d_src4, h->d_upart, h->d_V, h->d_red, h->d_b, h->d_hx, h->d_hy};
+                    h->d_tz, h->d_src4, h->d_upart, h->d_V, h->d_red, h->d_b, h->d_hx, h->d_hy, h->d_Tcat};
   for (double* b : bufs)
     if (b) cudaFree(b);
+  if (h->d_colbase) cudaFree(h->d_colbase);
+  if (h->d_colrstride) cudaFree(h->d_colrstride);
   if (h->h_red) cudaFreeHost(h->h_red);
   for (auto& ev : h->ev)
     if (ev) cudaEventDestroy(ev);

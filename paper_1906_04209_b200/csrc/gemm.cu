@@ -8,7 +8,9 @@
 // (profiles/r01_fp64_peak.txt).  CTA tile 64 x 64 x 16, 8 warps (4 x 2), each warp 16 x 32 = 2 x 4 DMMA tiles;
 // operands staged in padded shared memory (row stride BK+4 doubles: conflict-free fragment loads).
 // For step 5 the A operand is the sum of the direct kernel's per-segment partial fields (fused
-// deterministic reduction), and the epilogue adds the identity term.
+// deterministic reduction), and the epilogue adds the identity term.  For step 1 with several outgoing-operator rungs
+// one GEMM applies the concatenated T_k of all rungs in use, its epilogue scattering column (k, m) into rung k's
+// source records through a per-column (base, row stride) map.
 #include "nc_common.cuh"
 
 namespace nc {
@@ -26,7 +28,9 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A, int64_t lda, int nparts,
                                                    int64_t part_stride, const double* __restrict__ Bt, int64_t rows,
                                                    int ncols, int kd, double* __restrict__ C, int64_t ldc,
-                                                   int cstride, const double* __restrict__ X, int64_t ldx) {
+                                                   int cstride, const double* __restrict__ X, int64_t ldx,
+                                                   const int64_t* __restrict__ colbase,
+                                                   const int64_t* __restrict__ colrstride, int64_t crow0) {
   __shared__ double As[BM][LDS];
   __shared__ double Bs[BN][LDS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -85,7 +89,10 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
         if (n >= ncols) continue;
         double v = acc[mi][ni][e];
         if (X) v += X[gr * ldx + n];
-        C[gr * ldc + (int64_t)n * cstride] = v;
+        if (colbase)   // column map: element (i, n) -> C[colbase[n] + (crow0 + i) colrstride[n]]
+          C[colbase[n] + (crow0 + gr) * colrstride[n]] = v;
+        else
+          C[gr * ldc + (int64_t)n * cstride] = v;
       }
     }
   }
@@ -96,7 +103,15 @@ void launch_gemm_dmma(const double* A, int64_t lda, int nparts, int64_t part_str
                       cudaStream_t s) {
   if (rows <= 0) return;
   dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((ncols + BN - 1) / BN));
-  k_gemm_dmma<<<grid, 256, 0, s>>>(A, lda, nparts, part_stride, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx);
+  k_gemm_dmma<<<grid, 256, 0, s>>>(A, lda, nparts, part_stride, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx, nullptr,
+                                   nullptr, 0);
+}
+
+void launch_gemm_dmma_colmap(const double* A, int64_t lda, const double* Bt, int64_t rows, int ncols, int kd, double* C,
+                             const int64_t* colbase, const int64_t* colrstride, int64_t row0, cudaStream_t s) {
+  if (rows <= 0 || ncols <= 0) return;
+  dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((ncols + BN - 1) / BN));
+  k_gemm_dmma<<<grid, 256, 0, s>>>(A, lda, 1, 0, Bt, rows, ncols, kd, C, 0, 0, nullptr, 0, colbase, colrstride, row0);
 }
 
 }  // namespace nc

@@ -104,6 +104,10 @@ struct nc_handle {
   std::vector<int64_t> rung_soff; // offset (doubles) of the rung's records in d_src4
   std::vector<char> rung_used;    // rungs whose rho K1 must produce
   double* d_shat_all = nullptr;   // sum p_k x 3
+  double* d_Tcat = nullptr;       // concatenated T_k of the rungs in use (ncat x K), fused K1
+  int64_t* d_colbase = nullptr;   // per concatenated column: record offset of (rung, m) and row stride 4 p_k
+  int64_t* d_colrstride = nullptr;
+  int ncat = 0;
   double* d_upart = nullptr;      // nseg x (row_count*Kstar) partial fields
   int nseg = 1;
   int pair_tpt = 1;               // targets per thread in the direct kernel (1 or 2)
@@ -158,6 +162,9 @@ void launch_sources(const double* frames, int64_t N, const double* shat, int p, 
 void launch_gemm_dmma(const double* A, int64_t lda, int nparts, int64_t part_stride, const double* Bt, int64_t rows,
                       int ncols, int kd, double* C, int64_t ldc, int cstride, const double* X, int64_t ldx,
                       cudaStream_t s);
+// C[colbase[n] + (row0 + i) colrstride[n]] = sum_k A[i, k] Bt[n, k]   (scattered epilogue, one launch)
+void launch_gemm_dmma_colmap(const double* A, int64_t lda, const double* Bt, int64_t rows, int ncols, int kd, double* C,
+                             const int64_t* colbase, const int64_t* colrstride, int64_t row0, cudaStream_t s);
 
 // direct pair sums: upart[seg][t] = sum over source patches j in segment seg, j != patch(t), of
 // sum_m G(target t, s_jm) rho_jm
