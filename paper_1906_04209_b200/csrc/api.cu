@@ -351,6 +351,7 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   }
 
   h->emulated = h->world > 1 && !opt->nccl_id;   // rank emulation: no communicator, nc_matvec_emulated only
+  if (h->world > 1 && !h->emulated && (rc = dalloc(h, &h->d_xall, (size_t)N * K))) return bail(rc);
 #if NC_WITH_NCCL
   if (h->world > 1 && !h->emulated) {
     ncclUniqueId id;
@@ -437,27 +438,34 @@ int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   h->launches_last = 0;
   mark(h, 0, s);
-  outgoing(h, x, h->row_begin, h->row_count, s);
-  mark(h, 1, s);
-  if (h->world > 1) {
+  if (h->world == 1) {
+    outgoing(h, x, h->row_begin, h->row_count, s);
+    mark(h, 1, s);
+    return matvec_tail(h, x, y, s);
+  }
 #if NC_WITH_NCCL
-    // all-gather-v of the source records: one in-place broadcast per (rung, rank row range)
+  // world > 1: all-gather the coefficient vectors (N K doubles: 109 MB at N = 1e5, a quarter of the rho values of
+  // all rungs and an eighth of their records), one broadcast per rank row range inside a group, then every rank
+  // forms the outgoing records of ALL patches itself (K1 over N rows, ~2 ms): the exchange does not grow with the
+  // number of outgoing-operator rungs.  Everything after is exactly nc_matvec_emulated's path.
+  {
     ncclResult_t r = ncclGroupStart();
-    for (int k = 0; k < h->nrung; ++k) {
-      if (!h->rung_used[k]) continue;
-      const int pk = h->rung_p[k];
-      for (int q = 0; q < h->world && r == ncclSuccess; ++q) {
-        if (h->rank_count[q] == 0) continue;
-        double* seg = h->d_src4 + h->rung_soff[k] + (size_t)h->rank_begin[q] * pk * 4;
-        r = ncclBroadcast(seg, seg, (size_t)h->rank_count[q] * pk * 4, ncclDouble, q, h->comm, s);
-      }
+    for (int q = 0; q < h->world && r == ncclSuccess; ++q) {
+      if (h->rank_count[q] == 0) continue;
+      r = ncclBroadcast(q == h->rank ? (const void*)x : nullptr, h->d_xall + (size_t)h->rank_begin[q] * h->K,
+                        (size_t)h->rank_count[q] * h->K, ncclDouble, q, h->comm, s);
     }
     ncclResult_t r2 = ncclGroupEnd();
     if (r != ncclSuccess || r2 != ncclSuccess)
-      return fail(NC_ENCCL, std::string("all-gather (broadcasts): ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
-#endif
+      return fail(NC_ENCCL, std::string("all-gather of x (broadcasts): ") +
+                                ncclGetErrorString(r != ncclSuccess ? r : r2));
   }
+  mark(h, 1, s);
+  outgoing(h, h->d_xall, 0, h->N, s);
   return matvec_tail(h, x, y, s);
+#else
+  return fail(NC_EUNSUP, "nc_matvec: world > 1 needs a build with NCCL");
+#endif
 }
 
 int nc_matvec_emulated(nc_handle* h, const double* x_all, double* y, void* stream) {
@@ -731,7 +739,7 @@ void nc_destroy(nc_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   hier_destroy(h);
   double* bufs[] = {h->d_T, h->d_P, h->d_I, h->d_zhat, h->d_shat, h->d_centers, h->d_frames, h->d_tx, h->d_ty,
-                    h->d_tz, h->d_src4, h->d_upart, h->d_V, h->d_red, h->d_b, h->d_hx, h->d_hy, h->d_Tcat};
+                    h->d_tz, h->d_src4, h->d_upart, h->d_V, h->d_red, h->d_b, h->d_hx, h->d_hy, h->d_Tcat, h->d_xall};
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (h->d_colbase) cudaFree(h->d_colbase);

@@ -107,11 +107,16 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
   init_table(logtab, logsrc);
   const GridUnit U = units[blockIdx.x];
   double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
-  // adjacent points per thread (l = TPT t + u): a partial chunk leaves at most one partially idle warp
-  const bool any = (int)(TPT * threadIdx.x) < U.npt;
+  // adjacent points per thread (l = TPT t + u): a partial chunk leaves at most one partially idle warp.  A warp whose
+  // share of the chunk is <= 32 points (the chunk's tail) takes one point per lane instead (`single`), halving the
+  // idle lanes it carries.
+  const int wbase = TPT * 32 * (threadIdx.x >> 5);                  // first point of this warp
+  const bool single = TPT > 1 && U.npt - wbase > 0 && U.npt - wbase <= 32;
+  const int lane = threadIdx.x & 31;
+  const bool any = single ? (wbase + lane < U.npt) : ((int)(TPT * threadIdx.x) < U.npt);
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
-    const int l = TPT * threadIdx.x + u;
+    const int l = single ? wbase + lane : TPT * threadIdx.x + u;
     const int64_t g = U.pt0 + min(l, U.npt - 1);
     x[u] = gx[g]; y[u] = gy[g]; z[u] = gz[g];
     cq[u] = 0.5 * fma(x[u], x[u], fma(y[u], y[u], fma(z[u], z[u], 0.25)));
@@ -124,8 +129,12 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
   chp = chp < 1 ? 1 : (chp > kStagePatchesMax ? kStagePatchesMax : chp);
   accumulate_grid<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc,
                                                    [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p, sm,
-                                                   pid, chp, logtab, any);
+                                                   pid, chp, logtab, any, single);
   const int upts = NT * TPT;
+  if (single) {
+    if (wbase + lane < U.npt) part[(int64_t)blockIdx.x * upts + wbase + lane] = acc[0];
+    return;
+  }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
     const int l = TPT * threadIdx.x + u;

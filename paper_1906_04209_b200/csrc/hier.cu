@@ -1091,8 +1091,12 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         u.pad_ = 0;
         units.push_back(u);
         H->slot_pairs += (double)H->upts * u.nsrc * u.p;
-        const int wpts = 32 * (H->upts / kGridThreadsForFill);   // points per warp
-        H->warp_slot_pairs += (double)((u.npt + wpts - 1) / wpts) * wpts * u.nsrc * u.p;
+        {   // active-warp lane slots; a tail warp with <= 32 points runs one point per lane (direct.cu)
+          const int tpt = H->upts / kGridThreadsForFill, wpts = 32 * tpt;
+          const int full = u.npt / wpts, rem = u.npt - full * wpts;
+          const int tail = rem == 0 ? 0 : (tpt > 1 && rem <= 32 ? 32 : wpts);
+          H->warp_slot_pairs += (double)(full * wpts + tail) * u.nsrc * u.p;
+        }
       }
     }
   }

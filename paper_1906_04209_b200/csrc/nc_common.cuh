@@ -108,6 +108,7 @@ struct nc_handle {
   int64_t* d_colbase = nullptr;   // per concatenated column: record offset of (rung, m) and row stride 4 p_k
   int64_t* d_colrstride = nullptr;
   int ncat = 0;
+  double* d_xall = nullptr;       // world > 1: all ranks' coefficient rows (N x K), gathered every matvec
   double* d_upart = nullptr;      // nseg x (row_count*Kstar) partial fields
   int nseg = 1;
   int pair_tpt = 1;               // targets per thread in the direct kernel (1 or 2)

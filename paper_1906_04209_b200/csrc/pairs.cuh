@@ -89,7 +89,8 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
                                                 const double (&cq)[TPT], double (&acc)[TPT], int64_t nlist,
                                                 PatchAt patch_at, const double4* __restrict__ s4, int p,
                                                 double4* __restrict__ sm, int64_t* __restrict__ sm_pid, int chp,
-                                                const Tab* __restrict__ logtab, bool active) {
+                                                const Tab* __restrict__ logtab, bool active,
+                                                bool single = false) {
   for (int64_t c0 = 0; c0 < nlist; c0 += chp) {
     const int nch = (int)min((int64_t)chp, nlist - c0);
     __syncthreads();
@@ -102,6 +103,21 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
     __syncthreads();
     if (!active) continue;
     const int nrec = nch * p;
+    if (single) {   // warp-uniform: a tail warp with <= 32 points evaluates one target per lane
+#pragma unroll UNROLL
+      for (int m = 0; m < nrec; ++m) {
+        const double4 s = sm[m];
+        if (FAR) {
+          const double qh = fma(x[0], s.x, fma(y[0], s.y, fma(z[0], s.z, cq[0])));
+          acc[0] = fma(s.w, green_far_h<KIND>(qh, logtab), acc[0]);
+        } else {
+          const double dx = x[0] - s.x, dy = y[0] - s.y, dz = z[0] - s.z;
+          const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
+          acc[0] = fma(s.w, green_q<KIND>(qd, logtab), acc[0]);
+        }
+      }
+      continue;
+    }
 #pragma unroll UNROLL
     for (int m = 0; m < nrec; ++m) {
       const double4 s = sm[m];
