@@ -74,6 +74,8 @@ typedef struct nc_tables {
   const int32_t* ladder_p;    /* n_ladder skeleton sizes, 1..1024                                  */
   const double* ladder_shat;  /* sum(ladder_p) x 3 skeleton nodes, rung-major                      */
   const double* ladder_T;     /* sum(ladder_p) x K outgoing maps, rung-major                       */
+  double ladder_tol;          /* ID tolerance of the rungs (0: unknown); NC_HIER ignores the ladder */
+                              /* when the requested precision is tighter than this                  */
 } nc_tables;
 
 typedef struct nc_opts {

@@ -71,6 +71,13 @@ class PatchTables:
             assert np.all(np.diff(self.ladder_r) > 0) and self.ladder_r[0] > 2 * self.eps
         return self
 
+    @property
+    def ladder_tol(self) -> float:
+        """ID tolerance of the ladder rungs (table meta; 0 when unknown)."""
+        import re
+        m = re.search(r"'ladder_id_tol': ([0-9.eE+-]+)", str(self.meta.get("repr", "")) if self.meta else "")
+        return float(m.group(1)) if m else 0.0
+
     def without_ladder(self):
         return PatchTables(self.kind, self.eps, self.M, self.zhat, self.P, self.shat, self.T, self.I, self.meta)
 

@@ -237,7 +237,11 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
 
   // tables; outgoing-operator rungs (0 = base, 1.. = ladder, NC_HIER only)
   int rc;
-  h->nrung = 1 + ((opt->mode == NC_HIER) ? tab->n_ladder : 0);
+  // the ladder serves NC_HIER only, and only when the requested precision is not tighter than the rungs' ID
+  // tolerance (their compression error would otherwise set the floor)
+  const bool use_ladder = opt->mode == NC_HIER && tab->n_ladder > 0 &&
+                          !(tab->ladder_tol > 0.0 && opt->precision > 0.0 && opt->precision < tab->ladder_tol);
+  h->nrung = 1 + (use_ladder ? tab->n_ladder : 0);
   h->rung_r.assign(1, 2.0 * eps);
   h->rung_p.assign(1, p);
   for (int k = 1; k < h->nrung; ++k) {

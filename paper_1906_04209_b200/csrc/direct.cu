@@ -95,17 +95,12 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
 // One CTA of NT threads per work unit: <= NT * TPT adjacent points of one incoming grid x one slice (<= kSliceMax
 // patches, one outgoing-operator rung) of its source list.  Sources are staged in shared memory `chp` patches at a
 // time (a CTA barrier per stage); FAR selects the far-field arithmetic (pairs.cuh accumulate_grid, R23).
-template <int KIND, int NT, int TPT, int UNROLL, bool FAR, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restrict__ units, const double* __restrict__ gx,
-                                                   const double* __restrict__ gy, const double* __restrict__ gz,
-                                                   const int32_t* __restrict__ srclist,
-                                                   const double* __restrict__ src4, int stage_records,
-                                                   double* __restrict__ part, const double2* __restrict__ logsrc) {
-  extern __shared__ double4 sm[];
-  __shared__ double2 logtab[kLogTableSize];
-  __shared__ int64_t pid[kStagePatchesMax];
-  init_table(logtab, logsrc);
-  const GridUnit U = units[blockIdx.x];
+template <int KIND, int NT, int TPT, int UNROLL, bool FAR>
+__device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const double* __restrict__ gx,
+                                          const double* __restrict__ gy, const double* __restrict__ gz,
+                                          const int32_t* __restrict__ srclist, const double* __restrict__ src4,
+                                          int stage_records, double* __restrict__ part, double4* __restrict__ sm,
+                                          int64_t* __restrict__ pid, const double2* __restrict__ logtab) {
   double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
   // adjacent points per thread (l = TPT t + u): a partial chunk leaves at most one partially idle warp.  A warp whose
   // share of the chunk is <= 32 points (the chunk's tail) takes one point per lane instead (`single`), halving the
@@ -132,19 +127,45 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
                                                    pid, chp, logtab, any, single);
   const int upts = NT * TPT;
   if (single) {
-    if (wbase + lane < U.npt) part[(int64_t)blockIdx.x * upts + wbase + lane] = acc[0];
+    if (wbase + lane < U.npt) part[uid * upts + wbase + lane] = acc[0];
     return;
   }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
     const int l = TPT * threadIdx.x + u;
-    if (l < U.npt) part[(int64_t)blockIdx.x * upts + l] = acc[u];
+    if (l < U.npt) part[uid * upts + l] = acc[u];
   }
 }
 
-// Same unit, sources streamed by cp.async.bulk into a two-buffer mbarrier pipeline (pairs.cuh accumulate_grid_tma):
-// no CTA barrier after the prologue; warps without an active point leave at once.  Measured slower than the staged
-// kernel at C5 (profiles/r01b_grid_variant_sweep*.jsonl): selectable (NC_GRID_VARIANT), not the default.
+// counter == nullptr: one CTA per unit.  Otherwise a persistent grid: each CTA initialises the log table once and
+// takes units from an atomic counter until all `nunits` are done (results do not depend on the assignment).
+template <int KIND, int NT, int TPT, int UNROLL, bool FAR, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restrict__ units, const double* __restrict__ gx,
+                                                   const double* __restrict__ gy, const double* __restrict__ gz,
+                                                   const int32_t* __restrict__ srclist,
+                                                   const double* __restrict__ src4, int stage_records,
+                                                   double* __restrict__ part, const double2* __restrict__ logsrc,
+                                                   int* __restrict__ counter, int64_t nunits) {
+  extern __shared__ double4 sm[];
+  __shared__ double2 logtab[kLogTableSize];
+  __shared__ int64_t pid[kStagePatchesMax];
+  __shared__ int next;
+  init_table(logtab, logsrc);
+  if (!counter) {
+    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[blockIdx.x], blockIdx.x, gx, gy, gz, srclist, src4, stage_records, part,
+                                          sm, pid, logtab);
+    return;
+  }
+  for (;;) {
+    __syncthreads();   // previous unit done with `next` and the stage buffer
+    if (threadIdx.x == 0) next = atomicAdd(counter, 1);
+    __syncthreads();
+    const int u = next;
+    if (u >= nunits) break;
+    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[u], u, gx, gy, gz, srclist, src4, stage_records, part, sm, pid, logtab);
+  }
+}
+
 template <int KIND, int NT, int TPT, int UNROLL, bool FAR, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_pairs_grid_tma(const GridUnit* __restrict__ units,
                                                        const double* __restrict__ gx, const double* __restrict__ gy,
@@ -201,14 +222,16 @@ static bool stage_ldg() {
 // grid-kernel variant: NC_GRID_VARIANT="NT,TPT,UNROLL,STAGE,FAR,TMA,MINB" (default kGridVariantDefault); only the
 // combinations instantiated in launch_pairs_grid launch (others fall back to the default)
 static GridVariant grid_variant() {
-  static GridVariant v = {0, 0, 0, 0, 0, 0, 0};
+  static GridVariant v = {0, 0, 0, 0, 0, 0, 0, 0};
   if (v.nt == 0) {
     v = kGridVariantDefault;
     if (const char* e = getenv("NC_GRID_VARIANT")) {
       GridVariant w = v;
       w.tma = 0;
       w.minb = 8;
-      if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d", &w.nt, &w.tpt, &w.unroll, &w.stage, &w.far, &w.tma, &w.minb) >= 5 &&
+      w.persist = kGridVariantDefault.persist;
+      if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d", &w.nt, &w.tpt, &w.unroll, &w.stage, &w.far, &w.tma, &w.minb,
+                 &w.persist) >= 5 &&
           (w.nt == 128 || w.nt == 256) && (w.tpt == 1 || w.tpt == 2) && (w.unroll == 1 || w.unroll == 2 || w.unroll == 4) &&
           w.stage >= 32 && (w.far == 0 || w.far == 1) && (w.tma == 0 || w.tma == 1))
         v = w;
@@ -224,22 +247,42 @@ int grid_unit_points() { return grid_variant().nt * grid_variant().tpt; }
 template <int KIND, int NT, int TPT, int UNROLL, bool FAR, bool TMA, int MINB>
 static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* gx, const double* gy, const double* gz,
                           const int32_t* srclist, const double* src4, int stage, int pmax, double* part,
-                          cudaStream_t s) {
+                          int persist, int* counter, cudaStream_t s) {
   const int rec = std::max(stage, pmax);   // records per stage buffer: >= one whole patch of any rung
   const size_t smem = (TMA ? 2 : 1) * (size_t)rec * sizeof(double4);
-  auto kern = TMA ? k_pairs_grid_tma<KIND, NT, TPT, UNROLL, FAR, MINB> : k_pairs_grid<KIND, NT, TPT, UNROLL, FAR, MINB>;
+  if (TMA) {
+    auto kern = k_pairs_grid_tma<KIND, NT, TPT, UNROLL, FAR, MINB>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device());
+    return;
+  }
+  auto kern = k_pairs_grid<KIND, NT, TPT, UNROLL, FAR, MINB>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device());
+  if (!persist) {
+    kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device(), nullptr,
+                                            nunits);
+    return;
+  }
+  // persistent: one wave of CTAs (resident blocks per SM x SMs), units from the handle's atomic counter
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, smem);
+  const int ctas = std::max(1, per) * sms;
+  cudaMemsetAsync(counter, 0, sizeof(int), s);
+  kern<<<(unsigned)std::min<int64_t>(ctas, nunits), NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part,
+                                                                   log_table_device(), counter, nunits);
 }
 
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
                        const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
-                       cudaStream_t s) {
+                       int* counter, cudaStream_t s) {
   if (nunits <= 0) return;
   const GridVariant v = grid_variant();
 #define NC_G(KD, NT, TP, UR, FR, TM, MB)                                                                   \
   if (kind == KD && v.nt == NT && v.tpt == TP && v.unroll == UR && v.far == FR && v.tma == TM && v.minb == MB) \
-    return launch_grid_t<KD, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, pmax, part, s);
+    return launch_grid_t<KD, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, pmax, part, \
+                                                     v.persist, counter, s);
 #define NC_GK(KD)                                                                                                 \
   NC_G(KD, 128, 2, 4, 1, 0, 8) NC_G(KD, 128, 2, 4, 0, 0, 8) NC_G(KD, 128, 2, 4, 1, 1, 8) NC_G(KD, 128, 2, 4, 1, 0, 4) \
   NC_G(KD, 128, 2, 4, 1, 0, 6) NC_G(KD, 256, 1, 4, 1, 0, 1) \
@@ -250,8 +293,11 @@ void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const do
 #undef NC_GK
 #undef NC_G
   const GridVariant d = kGridVariantDefault;   // combination not instantiated: the default
-  if (kind == 0) return launch_grid_t<0, 128, 2, 4, true, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part, s);
-  return launch_grid_t<1, 128, 2, 4, true, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part, s);
+  if (kind == 0)
+    return launch_grid_t<0, 128, 2, 4, true, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
+                                                       d.persist, counter, s);
+  return launch_grid_t<1, 128, 2, 4, true, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
+                                                     d.persist, counter, s);
 }
 
 // ------------------------------------------------------------------------------------------------

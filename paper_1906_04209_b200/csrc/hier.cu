@@ -35,7 +35,8 @@ namespace nc {
 
 constexpr int kLmax = 24;
 constexpr int kSliceMax = 32;          // source patches per grid work unit
-constexpr int kMaxGrids = 3;           // incoming grids per group (source bands by distance; R24)
+constexpr int kMaxGrids = 4;           // incoming grids per group (source bands by distance; R24)
+constexpr int kDefaultGrids = 3;       // NC_MAX_GRIDS overrides (1..kMaxGrids)
 constexpr int kGridCutQuantiles = 48;  // candidate cut points of the multi-grid search
 constexpr int kGridThreadsForFill = 128;   // threads per grid-kernel CTA assumed by the warp-fill statistic
 constexpr double kBetaMin = 1.45;      // smallest source distance / circle radius served by a grid
@@ -76,6 +77,7 @@ struct HierState {
   int32_t *d_gnr = nullptr, *d_gna = nullptr;
   int64_t *d_goff = nullptr, *d_coff = nullptr;
   int32_t* d_grid_ids = nullptr;
+  int* d_counter = nullptr;         // work counter of the persistent grid kernel
   int32_t* d_grid_group = nullptr;
   int64_t* d_ggrid0 = nullptr;
   double *d_gx = nullptr, *d_gy = nullptr, *d_gz = nullptr, *d_gval = nullptr, *d_gcoef = nullptr;
@@ -501,34 +503,57 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
 #pragma unroll
         for (int q = 0; q < NPT; ++q) { cm[q] = 1.0; sm[q] = 0.0; cmm[q] = c1[q]; smm[q] = -s1[q]; }
         if (MB == 1) {
-          for (int m = 0; m <= M; ++m) {
-            const double2* __restrict__ cmj = cg + m * nr;
-            double A[NPT], B[NPT], t0[NPT], t1[NPT];
-            const double2 c0 = cmj[0];
+          // orders in pairs (m even, m + 1 odd); cos/sin(m theta) advanced in place two orders at a time and the
+          // Chebyshev pair (T_n, T_{n+2}) advanced in place two degrees at a time: no register rotation moves
+          double ce[NPT], se[NPT], co[NPT], so[NPT];
 #pragma unroll
-            for (int q = 0; q < NPT; ++q) {
-              t0[q] = (m & 1) ? x[q] : 1.0;
-              t1[q] = (m & 1) ? x[q] * (4.0 * x[q] * x[q] - 3.0) : 2.0 * x[q] * x[q] - 1.0;
-              A[q] = c0.x * t0[q];
-              B[q] = c0.y * t0[q];
-            }
-#pragma unroll 2
-            for (int j = 1; j < nr; ++j) {
-              const double2 c = cmj[j];
+          for (int q = 0; q < NPT; ++q) { ce[q] = 1.0; se[q] = 0.0; co[q] = c1[q]; so[q] = s1[q]; }
+          for (int m = 0; m <= M; m += 2) {
+#pragma unroll
+            for (int par = 0; par < 2; ++par) {
+              if (m + par > M) break;
+              const double2* __restrict__ cmj = cg + (m + par) * nr;
+              double A[NPT], B[NPT], ta[NPT], tb[NPT];
+              const double2 c0 = cmj[0];
 #pragma unroll
               for (int q = 0; q < NPT; ++q) {
-                A[q] = fma(c.x, t1[q], A[q]);
-                B[q] = fma(c.y, t1[q], B[q]);
-                const double t2 = fma(w2[q], t1[q], -t0[q]);
-                t0[q] = t1[q];
-                t1[q] = t2;
+                ta[q] = par ? x[q] : 1.0;                                              // T_par
+                tb[q] = par ? x[q] * (4.0 * x[q] * x[q] - 3.0) : 2.0 * x[q] * x[q] - 1.0;   // T_{par + 2}
+                A[q] = c0.x * ta[q];
+                B[q] = c0.y * ta[q];
               }
+              int j = 1;
+              for (; j + 1 < nr; j += 2) {
+                const double2 ca = cmj[j], cb = cmj[j + 1];
+#pragma unroll
+                for (int q = 0; q < NPT; ++q) {
+                  A[q] = fma(ca.x, tb[q], A[q]);
+                  B[q] = fma(ca.y, tb[q], B[q]);
+                  ta[q] = fma(w2[q], tb[q], -ta[q]);   // T_{par + 2 (j + 1)}
+                  A[q] = fma(cb.x, ta[q], A[q]);
+                  B[q] = fma(cb.y, ta[q], B[q]);
+                  tb[q] = fma(w2[q], ta[q], -tb[q]);   // T_{par + 2 (j + 2)}
+                }
+              }
+              if (j < nr) {
+                const double2 ca = cmj[j];
+#pragma unroll
+                for (int q = 0; q < NPT; ++q) {
+                  A[q] = fma(ca.x, tb[q], A[q]);
+                  B[q] = fma(ca.y, tb[q], B[q]);
+                }
+              }
+#pragma unroll
+              for (int q = 0; q < NPT; ++q)
+                acc[q] = par ? fma(A[q], co[q], fma(B[q], so[q], acc[q])) : fma(A[q], ce[q], fma(B[q], se[q], acc[q]));
             }
 #pragma unroll
-            for (int q = 0; q < NPT; ++q) {
-              acc[q] = fma(A[q], cm[q], fma(B[q], sm[q], acc[q]));
-              const double cn = 2.0 * c1[q] * cm[q] - cmm[q], sn = 2.0 * c1[q] * sm[q] - smm[q];
-              cmm[q] = cm[q]; smm[q] = sm[q]; cm[q] = cn; sm[q] = sn;
+            for (int q = 0; q < NPT; ++q) {   // (m, m + 1) -> (m + 2, m + 3)
+              const double t = 2.0 * c1[q];
+              ce[q] = fma(t, co[q], -ce[q]);
+              se[q] = fma(t, so[q], -se[q]);
+              co[q] = fma(t, ce[q], -co[q]);
+              so[q] = fma(t, se[q], -so[q]);
             }
           }
         } else {
@@ -541,12 +566,12 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
               to[q] = x[q]; top[q] = x[q];
             }
 #pragma unroll
-            for (int b = 0; b < MB; ++b) {
+            for (int b = 0; b < MB; ++b) {   // m0 is even (MB even): the parity of m = m0 + b is b's, known here
               const int m = m0 + b;
               const double2 c = (m <= M) ? cg[m * nr] : make_double2(0.0, 0.0);
 #pragma unroll
               for (int q = 0; q < NPT; ++q) {
-                const double tv = (m & 1) ? to[q] : te[q];
+                const double tv = (b & 1) ? to[q] : te[q];
                 A[b][q] = c.x * tv;
                 B[b][q] = c.y * tv;
               }
@@ -565,7 +590,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
                 const double2 c = (m <= M) ? cg[m * nr + j] : make_double2(0.0, 0.0);
 #pragma unroll
                 for (int q = 0; q < NPT; ++q) {
-                  const double tv = (m & 1) ? to[q] : te[q];
+                  const double tv = (b & 1) ? to[q] : te[q];
                   A[b][q] = fma(c.x, tv, A[b][q]);
                   B[b][q] = fma(c.y, tv, B[b][q]);
                 }
@@ -599,7 +624,7 @@ struct InterpVariant {
 static InterpVariant interp_variant() {
   static InterpVariant v = {-1, 0, 0, 0};
   if (v.nt < 0) {
-    v = {128, 4, 1, 5};
+    v = {128, 4, 1, 4};
     if (const char* e = getenv("NC_INTERP_VARIANT")) {
       InterpVariant w = v;
       w.minb = 1;
@@ -630,9 +655,10 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
 #define NC_I(NT, NPT, MB, MINB)                                                                             \
   if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                           \
     return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
-  NC_I(128, 4, 1, 1) NC_I(128, 4, 1, 4) NC_I(128, 4, 1, 5) NC_I(256, 2, 1, 1) NC_I(256, 1, 4, 1) NC_I(128, 4, 2, 3)
+  NC_I(128, 4, 1, 5) NC_I(128, 4, 1, 4) NC_I(128, 4, 1, 3) NC_I(128, 4, 1, 1) NC_I(256, 2, 1, 2) NC_I(128, 4, 2, 4)
+  NC_I(256, 2, 2, 3)
 #undef NC_I
-  return launch_interp_t<128, 4, 1, 5>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
+  return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -847,8 +873,10 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   // sources, sorted by beta = (distance - eps) / R descending, are cut into up to kMaxGrids consecutive bands, each
   // on its own grid sized by the band's nearest source, and a near tail evaluated directly at the members' Zernike
   // nodes (R12, R24).  The cut minimises the cost model (grid-pair units).
-  int max_grids = kMaxGrids;
+  int max_grids = kDefaultGrids;
   if (const char* e = getenv("NC_MAX_GRIDS")) max_grids = std::max(1, std::min(kMaxGrids, atoi(e)));
+  int ncuts = kGridCutQuantiles;
+  if (const char* e = getenv("NC_GRID_CUTS")) ncuts = std::max(4, std::min(512, atoi(e)));
   std::vector<std::vector<int32_t>> nsrc(G);
   struct GridPlan {
     int32_t group, nr, na;
@@ -922,7 +950,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     std::vector<size_t> cuts;   // band boundaries chosen (ascending, last = end of the grid-served prefix)
     if (max_grids >= 2 && n_ok >= 2) {
       std::vector<size_t> qs;
-      for (int k = 1; k <= kGridCutQuantiles; ++k) qs.push_back(std::max<size_t>(1, (n_ok * k) / kGridCutQuantiles));
+      for (int k = 1; k <= ncuts; ++k) qs.push_back(std::max<size_t>(1, (n_ok * k) / ncuts));
       qs.erase(std::unique(qs.begin(), qs.end()), qs.end());
       const int Q = (int)qs.size();
       std::vector<double> qi(Q), ovh(Q);
@@ -1157,6 +1185,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_TRY(upload(h, &H->d_goff, H->goff, s));
   NC_TRY(upload(h, &H->d_coff, H->coff, s));
   NC_TRY(upload(h, &H->d_grid_ids, H->grid_ids, s));
+  NC_TRY(halloc(h, &H->d_counter, 1));
   NC_TRY(upload(h, &H->d_grid_group, H->grid_group, s));
   NC_TRY(upload(h, &H->d_ggrid0, H->ggrid0, s));
   NC_TRY(upload(h, &H->d_units, units, s));
@@ -1196,7 +1225,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   const int Ks = h->Kstar, K = h->K;
   // steps 2-3: interaction-list and leaf-neighbour sources on the incoming grids
   launch_pairs_grid(h->kind, H->d_units, H->nunits, H->d_gx, H->d_gy, H->d_gz, H->d_srclist, h->d_src4, H->pmax,
-                    H->d_part, s);
+                    H->d_part, H->d_counter, s);
   h->launches_last += H->nunits > 0;
   if (h->time_stages) cudaEventRecord(h->ev[3], s);
   if (H->nchunks) {
@@ -1250,7 +1279,7 @@ void hier_destroy(nc_handle* h) {
   HierState* H = h->hier;
   if (!H) return;
   void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_ids,
-                  H->d_grid_group, H->d_ggrid0,
+                  H->d_grid_group, H->d_ggrid0, H->d_counter,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
                   H->d_chunks, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
                   H->d_udir, H->d_u};

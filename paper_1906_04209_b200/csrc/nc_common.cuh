@@ -48,8 +48,9 @@ struct HierState;
 // tma), far-field arithmetic, bulk-copy mbarrier pipeline}; NC_GRID_VARIANT overrides (tools/sweep_grid.py)
 struct GridVariant {
   int nt, tpt, unroll, stage, far, tma, minb;   // minb: __launch_bounds__ min blocks per SM (register cap)
+  int persist;                                  // 1: persistent CTAs taking units from an atomic counter
 };
-#define kGridVariantDefault (GridVariant{128, 2, 4, 256, 1, 0, 8})
+#define kGridVariantDefault (GridVariant{128, 2, 4, 256, 1, 0, 8, 0})
 int grid_far_variant();
 int grid_unit_points();                // grid points per work unit = threads per CTA x targets per thread
 
@@ -177,7 +178,7 @@ int pairs_direct_blocks_per_sm(int p, int tpt);
 void split_rows(const double* w, int64_t N, int world, int64_t* begin, int64_t* count);
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
                        const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
-                       cudaStream_t s);
+                       int* counter /* device int, persistent variant */, cudaStream_t s);
 void launch_pairs_near(int kind, const double* tx, const double* ty, const double* tz, int Kstar, const int32_t* work,
                        int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
                        double* udir, cudaStream_t s);

@@ -32,7 +32,7 @@ class NcTables(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int32), ("K", ctypes.c_int32), ("Kstar", ctypes.c_int32), ("p", ctypes.c_int32),
                 ("zhat", _dp), ("P", _dp), ("shat", _dp), ("T", _dp), ("I", _dp),
                 ("n_ladder", ctypes.c_int32), ("ladder_r", _dp), ("ladder_p", ctypes.POINTER(ctypes.c_int32)),
-                ("ladder_shat", _dp), ("ladder_T", _dp)]
+                ("ladder_shat", _dp), ("ladder_T", _dp), ("ladder_tol", ctypes.c_double)]
 
 
 class NcOpts(ctypes.Structure):
@@ -144,7 +144,7 @@ class Handle:
         zhat, P, shat, T, I = self._keep
         tab = NcTables(int(tables.M), T.shape[1], zhat.shape[0], shat.shape[0],
                        zhat.ctypes.data_as(_dp), P.ctypes.data_as(_dp), shat.ctypes.data_as(_dp),
-                       T.ctypes.data_as(_dp), I.ctypes.data_as(_dp), 0, None, None, None, None)
+                       T.ctypes.data_as(_dp), I.ctypes.data_as(_dp), 0, None, None, None, None, 0.0)
         if use_ladder and getattr(tables, "ladder_r", None) is not None and len(tables.ladder_r) > 0:
             lr = np.ascontiguousarray(tables.ladder_r, dtype=np.float64)
             lp = np.ascontiguousarray(tables.ladder_p, dtype=np.int32)
@@ -156,6 +156,7 @@ class Handle:
             tab.ladder_p = lp.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
             tab.ladder_shat = ls.ctypes.data_as(_dp)
             tab.ladder_T = lt.ctypes.data_as(_dp)
+            tab.ladder_tol = float(getattr(tables, "ladder_tol", 0.0) or 0.0)
         idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         opts = NcOpts(int(mode), float(precision), int(device), int(world), int(rank),
                       ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None, int(bool(check_separation)))

@@ -176,3 +176,32 @@ def test_far_field_pair_variant_error(tmp_path):
         subprocess.run([sys.executable, "-c", _FAR_CHILD], env=env, check=True, timeout=600)
         outs.append(np.load(out))
     assert rel(outs[1], outs[0]) <= 1e-11
+
+
+@pytest.mark.parametrize("precision", [1e-7, 1e-11])
+def test_hier_precision_knob_C2(precision):
+    """The requested precision controls the incoming-grid tolerance (R21): the matvec error tracks it
+    (<= precision, with the calibrated margin), and a tighter request costs more grid pairs."""
+    cfg = CONFIGS["C2"]
+    c = cfg.centers()
+    tab = _phys("C2")
+    x = random_coeffs(cfg.N, tab.K, 2007)
+    hd = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_DIRECT)
+    hh = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_HIER, precision=precision)
+    hr = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_HIER, precision=1e-9)
+    assert rel(gpu_matvec(hh, x), gpu_matvec(hd, x)) <= max(precision, 1e-11)
+    if precision < 1e-9:
+        assert hh.stats()["hier_grid_pairs"] > hr.stats()["hier_grid_pairs"]
+    else:
+        assert hh.stats()["hier_grid_pairs"] < hr.stats()["hier_grid_pairs"]
+
+
+@pytest.mark.parametrize("layout,N,eps,kind", [("uniform", 37, 0.05, 0), ("vmf", 300, 0.01, 1), ("uniform", 2, 0.3, 0)])
+def test_hier_small_layouts_vs_oracle(layout, N, eps, kind):
+    """Small hierarchical cases (shallow trees, near lists, N = 2) against the oracle's full brute-force matvec,
+    synthetic tables with real node geometry (SURVEY.md §7 phase 1)."""
+    c = make_centers(layout, N, eps, seed=11)
+    tab = synthetic_tables(kind, eps, seed=3)
+    x = random_coeffs(N, tab.K, 12)
+    h = _nc().Handle(kind, c, eps, tab, mode=_nc().NC_HIER, precision=1e-9)
+    assert rel(gpu_matvec(h, x), O.matvec(kind, c, tab, x)) <= HIER_TOL
