@@ -50,7 +50,7 @@ struct GridVariant {
   int nt, tpt, unroll, stage, far, tma, minb;   // minb: __launch_bounds__ min blocks per SM (register cap)
   int persist;                                  // 1: persistent CTAs taking units from an atomic counter
 };
-#define kGridVariantDefault (GridVariant{128, 2, 4, 256, 1, 0, 8, 0})
+#define kGridVariantDefault (GridVariant{128, 2, 4, 256, 1, 0, 8, 1})
 int grid_far_variant();
 int grid_unit_points();                // grid points per work unit = threads per CTA x targets per thread
 
