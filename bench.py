@@ -57,7 +57,7 @@ def load_fp64_peak():
 
 
 # ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
-TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01h_ncu_full_pairs_grid.json"}
+TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01k_ncu_full_pairs_grid.json"}
 
 
 def profiled_traffic(kernel, config, mode):
@@ -332,6 +332,28 @@ def main():
             tf = fl / (ms * 1e-3) / 1e12
             gemms[name] = {"bound": "tensor", "kernel": "k_gemm_dmma", "ms": ms, "achieved": tf, "unit": "TFLOP/s",
                            "peak": peaks.get("dmma"), "frac": tf / peaks["dmma"] if peaks.get("dmma") else None}
+    # issue-bound model of the dominant kernel: an FP64 warp instruction holds its SMSP's dispatch
+    # 2 cycles, any other 1; per-pair counts from this build's SASS main loop (tools/sass_loop.py, cuobjdump)
+    if roof is not None and not os.environ.get("NC_GRID_VARIANT"):
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from sass_loop import main_loop
+            import paper_1906_04209_b200 as ncmod
+            pat = (f"k_pairs_gridILi{cfg.kind}ELi128ELi2ELi4ELb1" if args.mode == "hier"
+                   else f"k_pairs_directILi{cfg.kind}ELi2")
+            ml = main_loop(ncmod.nc.LIB_PATH, pat)
+            clk_hz = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+            if ml:
+                fp, oth = ml
+                cyc = 2.0 * fp + oth
+                ideal_ms = pairs / 32.0 * cyc / (148 * 4 * clk_hz) * 1e3
+                roof["issue_model"] = {"fp64_inst_per_pair": fp, "other_inst_per_pair": oth,
+                                       "cycles_per_warp_pair": cyc, "ideal_ms": ideal_ms,
+                                       "frac": ideal_ms / pair_ms,
+                                       "note": "2 dispatch cycles per FP64 warp instruction + 1 per other, SASS "
+                                               "main loop of this build, 592 SMSPs at the sampled SM clock"}
+        except Exception as e:  # pragma: no cover
+            roof["issue_model"] = {"error": str(e)[:200]}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
