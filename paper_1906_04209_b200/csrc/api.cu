@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <string>
 #include <unordered_map>
@@ -23,6 +24,15 @@
 namespace nc {
 
 static thread_local std::string g_err;
+
+void setup_tick(const char* phase) {
+  static const bool on = getenv("NC_SETUP_TIMING") != nullptr;
+  static thread_local std::chrono::steady_clock::time_point last;
+  if (!on) return;
+  const auto now = std::chrono::steady_clock::now();
+  if (phase) fprintf(stderr, "[nc setup] %-28s %9.1f ms\n", phase, std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
 
 void set_error(const std::string& msg) { g_err = msg; }
 int fail(int code, const std::string& msg) {
@@ -194,7 +204,9 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
                     centers[3 * i + 2] * centers[3 * i + 2]);
     if (!(fabs(r - 1.0) < 1e-10)) return fail(NC_EINVAL, "nc_setup: centre " + std::to_string(i) + " is not unit");
   }
+  setup_tick(nullptr);
   if (opt->check_separation) NC_TRY(check_separation(centers, N, eps));
+  setup_tick("separation check");
 #if !NC_WITH_NCCL
   if (opt->world > 1 && opt->nccl_id) return fail(NC_EUNSUP, "nc_setup: world > 1 needs a build with NCCL");
 #endif
@@ -289,8 +301,10 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   for (int64_t i = 0; i < N; ++i) h->perm[i] = i;
   std::vector<double> cs(centers, centers + 3 * N);
   if (h->mode == NC_HIER) {
+    setup_tick("tables, stream");
     rc = hier_order(h, cs);          // Morton order of the cube-face quadtree; fills h->perm, permutes cs
     if (rc) return bail(rc);
+    setup_tick("keys, sort (device)");
   }
 
   if ((rc = dalloc(h, &h->d_centers, (size_t)N * 3)) || (rc = dalloc(h, &h->d_frames, (size_t)N * 9))) return bail(rc);
@@ -321,6 +335,7 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   } else {
     rc = hier_setup(h, cs, s);       // tree, lists, grids, work-weighted partition
     if (rc) return bail(rc);
+    setup_tick("hier setup (rest)");
   }
   if ((rc = ensure_red(h, 4096))) return bail(rc);
 
@@ -353,6 +368,7 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
       h->ncat = ncat;
     }
   }
+  setup_tick("fused K1 tables");
 
   h->emulated = h->world > 1 && !opt->nccl_id;   // rank emulation: no communicator, nc_matvec_emulated only
   if (h->world > 1 && !h->emulated && (rc = dalloc(h, &h->d_xall, (size_t)N * K))) return bail(rc);

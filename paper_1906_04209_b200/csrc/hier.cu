@@ -815,6 +815,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     for (int64_t g = H->lvl_off[lvl]; g < H->lvl_off[lvl + 1]; ++g)
       H->glast[g] = (g + 1 < H->lvl_off[lvl + 1]) ? H->gfirst[g + 1] : (int32_t)N;
 
+  setup_tick("boxes per level");
   // ---- neighbours, interaction lists, circles (device) ----
   int64_t *d_gkey = nullptr, *d_lvl = nullptr, *d_cnt = nullptr, *d_off = nullptr;
   int32_t *d_nbr = nullptr, *d_gfirst = nullptr, *d_glast = nullptr, *d_pg = nullptr, *d_il = nullptr;
@@ -857,6 +858,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     cudaFree(q);
   NC_CUDA_TRY(cudaGetLastError());
 
+  setup_tick("neighbours, lists, caps (dev)");
   // ---- grid vs near routing, grid sizes (host) ----
   // per-grid interpolation tolerance = kGridTolFactor x requested precision (calibrated, R21;
   // NC_GRID_TOL_FACTOR overrides for calibration runs)
@@ -1012,6 +1014,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     fprintf(stderr, "[nc hier diag] cost %.4g, grids %zu, groups with several grids %lld, max grids %d\n", diag_cost,
             plans.size(), (long long)diag_groups2, max_grids);
 
+  setup_tick("routing + grid bands (host)");
   // rungs in use: a global decision (identical on every rank, so the per-rung all-gathers match)
   for (const GridPlan& gp : plans)
     for (int r : gp.rung) h->rung_used[r] = 1;
@@ -1133,6 +1136,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     for (int k = 0; k < h->nrung; ++k) fprintf(stderr, " %.3g:%.3g", h->rung_r[k] / eps, rung_pairs[k]);
     fprintf(stderr, "\n");
   }
+  setup_tick("partition, offsets, units");
   // near lists for local patches (concatenated over levels)
   std::vector<int64_t> near_off(rc + 1, 0);
   std::vector<int32_t> near_all;
@@ -1175,6 +1179,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         }
   }
 
+  setup_tick("near lists, tree audit lists");
   for (int k = 0; k < h->nrung; ++k) H->pmax = std::max(H->pmax, h->rung_p[k]);
   // ---- uploads and device grids ----
   H->nunits = (int64_t)units.size();

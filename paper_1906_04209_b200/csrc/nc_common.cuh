@@ -39,6 +39,9 @@ constexpr int kPairThreads = 256;   // threads per CTA in the direct pair-sum ke
 constexpr int kDefaultPairTpt = 2;  // targets per thread (NC_PAIR_TPT=1|2 overrides)
 constexpr int kDefaultStageLdg = 0; // 1: pair kernels read sources via L1 broadcasts (NC_PAIR_STAGE=ldg|smem)
 
+// setup phase timer (NC_SETUP_TIMING=1 prints wall-clock ms per phase to stderr)
+void setup_tick(const char* phase);
+
 // ------------------------------------------------------------------------------------------------
 // hierarchical-mode state (hier.cu) and its step-2/3 work unit (direct.cu)
 // ------------------------------------------------------------------------------------------------
