@@ -727,9 +727,17 @@ int nc_stats(const nc_handle* h, nc_stats_t* o) {
   const int interior = h->kind == NC_INTERIOR;
   o->pair_fp64_inst_direct = 22;
   o->pair_fp64_flops_direct = 33 + interior;
-  const bool far = grid_far_variant() != 0;
-  o->pair_fp64_inst_grid = 22 - 6 * far;
-  o->pair_fp64_flops_grid = far ? 26 + interior : 33 + interior;
+  // far table (R25, green_far_t) cubic: 10 DFMA + 1 DMUL + 2 DADD exterior (23 flops), 11 + 1 + 1 interior (24);
+  // quartic: one DFMA more
+  const int far = grid_far_variant();
+  if (far >= 2) {
+    const int quartic = far == 3 || far == 6;
+    o->pair_fp64_inst_grid = 13 + quartic;
+    o->pair_fp64_flops_grid = 23 + interior + 2 * quartic;
+  } else {
+    o->pair_fp64_inst_grid = far ? 16 : 22;
+    o->pair_fp64_flops_grid = far ? 26 + interior : 33 + interior;
+  }
   hier_fill_stats(h, o);
   return NC_OK;
 }

@@ -95,12 +95,13 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
 // One CTA of NT threads per work unit: <= NT * TPT adjacent points of one incoming grid x one slice (<= kSliceMax
 // patches, one outgoing-operator rung) of its source list.  Sources are staged in shared memory `chp` patches at a
 // time (a CTA barrier per stage); FAR selects the far-field arithmetic (pairs.cuh accumulate_grid, R23).
-template <int KIND, int NT, int TPT, int UNROLL, bool FAR>
+template <int KIND, int NT, int TPT, int UNROLL, int FAR>
 __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const double* __restrict__ gx,
                                           const double* __restrict__ gy, const double* __restrict__ gz,
                                           const int32_t* __restrict__ srclist, const double* __restrict__ src4,
                                           int stage_records, double* __restrict__ part, double4* __restrict__ sm,
-                                          int64_t* __restrict__ pid, const double2* __restrict__ logtab) {
+                                          int64_t* __restrict__ pid, const double2* __restrict__ logtab,
+                                          unsigned ftb, int flim, double fa2, double fa3) {
   double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
   // adjacent points per thread (l = TPT t + u): a partial chunk leaves at most one partially idle warp.  A warp whose
   // share of the chunk is <= 32 points (the chunk's tail) takes one point per lane instead (`single`), halving the
@@ -124,7 +125,7 @@ __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const 
   chp = chp < 1 ? 1 : (chp > kStagePatchesMax ? kStagePatchesMax : chp);
   accumulate_grid<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc,
                                                    [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p, sm,
-                                                   pid, chp, logtab, any, single);
+                                                   pid, chp, logtab, any, single, ftb, flim, fa2, fa3);
   const int upts = NT * TPT;
   if (single) {
     if (wbase + lane < U.npt) part[uid * upts + wbase + lane] = acc[0];
@@ -139,21 +140,39 @@ __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const 
 
 // counter == nullptr: one CTA per unit.  Otherwise a persistent grid: each CTA initialises the log table once and
 // takes units from an atomic counter until all `nunits` are done (results do not depend on the assignment).
-template <int KIND, int NT, int TPT, int UNROLL, bool FAR, int MINB>
+template <int KIND, int NT, int TPT, int UNROLL, int FAR, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restrict__ units, const double* __restrict__ gx,
                                                    const double* __restrict__ gy, const double* __restrict__ gz,
                                                    const int32_t* __restrict__ srclist,
                                                    const double* __restrict__ src4, int stage_records,
                                                    double* __restrict__ part, const double2* __restrict__ logsrc,
-                                                   int* __restrict__ counter, int64_t nunits) {
+                                                   int* __restrict__ counter, int64_t nunits,
+                                                   const double2* __restrict__ fsrc, int fn, int fbase) {
   extern __shared__ double4 sm[];
-  __shared__ double2 logtab[kLogTableSize];
+  __shared__ double2 logtab[FAR >= 2 ? 1 : kLogTableSize];
   __shared__ int64_t pid[kStagePatchesMax];
   __shared__ int next;
-  init_table(logtab, logsrc);
+  // FAR >= 2: the far table follows the stage buffer in dynamic shared memory; tb is indexed by hi(x) >> (20 - bits)
+  // entries: (c, L) double2 (green_far_t) or L alone, packed two per double2 (green_far_r)
+  double2* ftab = reinterpret_cast<double2*>(sm + stage_records);
+  constexpr unsigned kEsz = far_table_rcp(FAR) ? 8u : 16u;
+  const int nvec = far_table_rcp(FAR) ? fn / 2 : fn;
+  const unsigned tb = smem_u32(ftab) - kEsz * (unsigned)fbase;
+  const int flim = KIND == 1 ? fbase + fn - 1 : fbase;
+  // the polynomial constants ride after the table (a load: ptxas cannot rematerialise them as immediates in the loop)
+  double fa2 = 0.0, fa3 = 0.0;
+  if (FAR >= 2) {
+    const double2 cst = __ldg(fsrc + nvec);
+    fa2 = cst.x;
+    fa3 = cst.y;
+    for (int j = threadIdx.x; j < nvec; j += NT) ftab[j] = fsrc[j];
+  } else {
+    init_table(logtab, logsrc);
+  }
   if (!counter) {
+    __syncthreads();
     grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[blockIdx.x], blockIdx.x, gx, gy, gz, srclist, src4, stage_records, part,
-                                          sm, pid, logtab);
+                                          sm, pid, logtab, tb, flim, fa2, fa3);
     return;
   }
   for (;;) {
@@ -162,11 +181,12 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
     __syncthreads();
     const int u = next;
     if (u >= nunits) break;
-    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[u], u, gx, gy, gz, srclist, src4, stage_records, part, sm, pid, logtab);
+    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[u], u, gx, gy, gz, srclist, src4, stage_records, part, sm, pid, logtab,
+                                          tb, flim, fa2, fa3);
   }
 }
 
-template <int KIND, int NT, int TPT, int UNROLL, bool FAR, int MINB>
+template <int KIND, int NT, int TPT, int UNROLL, int FAR, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_pairs_grid_tma(const GridUnit* __restrict__ units,
                                                        const double* __restrict__ gx, const double* __restrict__ gy,
                                                        const double* __restrict__ gz,
@@ -233,7 +253,7 @@ static GridVariant grid_variant() {
       if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d", &w.nt, &w.tpt, &w.unroll, &w.stage, &w.far, &w.tma, &w.minb,
                  &w.persist) >= 5 &&
           (w.nt == 128 || w.nt == 256) && (w.tpt == 1 || w.tpt == 2) && (w.unroll == 1 || w.unroll == 2 || w.unroll == 4) &&
-          w.stage >= 32 && (w.far == 0 || w.far == 1) && (w.tma == 0 || w.tma == 1))
+          w.stage >= 32 && (w.far >= 0 && w.far <= 6) && (w.tma == 0 || w.tma == 1))
         v = w;
     }
   }
@@ -241,15 +261,18 @@ static GridVariant grid_variant() {
 }
 
 int grid_far_variant() { return grid_variant().far; }
+int grid_far_table_bits() { return grid_variant().far >= 2 ? far_table_bits(grid_variant().far) : 0; }
+int grid_far_table_rcp() { return far_table_rcp(grid_variant().far); }
+void grid_far_poly(double* a2, double* a3) { far_poly(grid_variant().far, a2, a3); }
 
 int grid_unit_points() { return grid_variant().nt * grid_variant().tpt; }
 
-template <int KIND, int NT, int TPT, int UNROLL, bool FAR, bool TMA, int MINB>
+template <int KIND, int NT, int TPT, int UNROLL, int FAR, bool TMA, int MINB>
 static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* gx, const double* gy, const double* gz,
                           const int32_t* srclist, const double* src4, int stage, int pmax, double* part,
-                          int persist, int* counter, cudaStream_t s) {
+                          int persist, int* counter, const FarTable& ft, cudaStream_t s) {
   const int rec = std::max(stage, pmax);   // records per stage buffer: >= one whole patch of any rung
-  const size_t smem = (TMA ? 2 : 1) * (size_t)rec * sizeof(double4);
+  const size_t smem = (TMA ? 2 : 1) * (size_t)rec * sizeof(double4) + (FAR >= 2 ? (size_t)ft.n * (far_table_rcp(FAR) ? 8 : 16) : 0);
   if (TMA) {
     auto kern = k_pairs_grid_tma<KIND, NT, TPT, UNROLL, FAR, MINB>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -260,7 +283,7 @@ static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* g
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (!persist) {
     kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device(), nullptr,
-                                            nunits);
+                                            nunits, ft.d, ft.n, ft.base);
     return;
   }
   // persistent: one wave of CTAs (resident blocks per SM x SMs), units from the handle's atomic counter
@@ -271,19 +294,23 @@ static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* g
   const int ctas = std::max(1, per) * sms;
   cudaMemsetAsync(counter, 0, sizeof(int), s);
   kern<<<(unsigned)std::min<int64_t>(ctas, nunits), NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part,
-                                                                   log_table_device(), counter, nunits);
+                                                                   log_table_device(), counter, nunits, ft.d, ft.n,
+                                                                   ft.base);
 }
 
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
                        const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
-                       int* counter, cudaStream_t s) {
+                       int* counter, const FarTable& ft, cudaStream_t s) {
   if (nunits <= 0) return;
   const GridVariant v = grid_variant();
 #define NC_G(KD, NT, TP, UR, FR, TM, MB)                                                                   \
   if (kind == KD && v.nt == NT && v.tpt == TP && v.unroll == UR && v.far == FR && v.tma == TM && v.minb == MB) \
     return launch_grid_t<KD, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, pmax, part, \
-                                                     v.persist, counter, s);
+                                                     v.persist, counter, ft, s);
 #define NC_GK(KD)                                                                                                 \
+  NC_G(KD, 128, 2, 4, 2, 0, 8) NC_G(KD, 128, 2, 4, 3, 0, 8) NC_G(KD, 128, 2, 4, 4, 0, 8) NC_G(KD, 128, 2, 4, 2, 0, 6) \
+  NC_G(KD, 128, 2, 4, 5, 0, 8) NC_G(KD, 128, 2, 4, 6, 0, 8) NC_G(KD, 128, 2, 4, 5, 0, 6) NC_G(KD, 128, 2, 4, 6, 0, 6) \
+  NC_G(KD, 128, 2, 2, 5, 0, 8) NC_G(KD, 256, 1, 4, 5, 0, 4) \
   NC_G(KD, 128, 2, 4, 1, 0, 8) NC_G(KD, 128, 2, 4, 0, 0, 8) NC_G(KD, 128, 2, 4, 1, 1, 8) NC_G(KD, 128, 2, 4, 1, 0, 4) \
   NC_G(KD, 128, 2, 4, 1, 0, 6) NC_G(KD, 256, 1, 4, 1, 0, 1) \
   NC_G(KD, 256, 1, 4, 1, 0, 5) NC_G(KD, 256, 1, 4, 1, 0, 6) NC_G(KD, 256, 1, 2, 1, 0, 6) NC_G(KD, 256, 2, 2, 1, 0, 5) \
@@ -294,10 +321,10 @@ void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const do
 #undef NC_G
   const GridVariant d = kGridVariantDefault;   // combination not instantiated: the default
   if (kind == 0)
-    return launch_grid_t<0, 128, 2, 4, true, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
-                                                       d.persist, counter, s);
-  return launch_grid_t<1, 128, 2, 4, true, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
-                                                     d.persist, counter, s);
+    return launch_grid_t<0, 128, 2, 4, 1, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
+                                                    d.persist, counter, ft, s);
+  return launch_grid_t<1, 128, 2, 4, 1, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
+                                                  d.persist, counter, ft, s);
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -115,6 +115,101 @@ __device__ __forceinline__ double green_far_h(double qh, const double2* __restri
   return w - (h + l1);
 }
 
+// Far-field G with an exponent-indexed log table (k_pairs_grid FAR >= 2, hierarchical mode only; R25).
+// The table is indexed by the top 11 + FB bits of x (biased exponent and FB mantissa bits: one shift), and its
+// entry (c, L) already carries the exponent: c = 1 / (2^e (1 + (j + 1/2) / 2^FB)), L = -log c (+ ln 2 interior, so
+// that L + log1p(r) = log(2 x) = log(q (1 + w))).  Then log x = L + log1p(r) with r = x c - 1, |r| <= 2^-(FB+1),
+// and log1p(r) = r (1 + r (a2 + r a3 [+ r^2 a4])) with minimax coefficients for |r| <= 1 / (2^(FB+1) + 1)
+// (absolute error 9.9e-12 for FB = 7 cubic, 6.3e-14 FB = 7 quartic, 6.2e-13 FB = 8 cubic; fitted by
+// tools/fit_log1p.py).  G = (w - L) - r p(r): no exponent extraction, no k ln 2 term.
+// 13 FP64 instructions per pair with the caller's dot product and accumulate (cubic), 14 quartic.
+// The table covers the x range of grid pairs (d >= eps / 4, far_table_build); the index is clamped on the open side.
+template <int FB, int DEG>
+struct FarPoly;
+template <>
+struct FarPoly<7, 3> {
+  static constexpr double a2 = -0.50000313945533437, a3 = 0.33333636142100315, a4 = 0.0;
+};
+template <>
+struct FarPoly<7, 4> {
+  static constexpr double a2 = -0.49999999200264428, a3 = 0.33333636142100315, a4 = -0.25053074075115417;
+};
+template <>
+struct FarPoly<6, 4> {
+  static constexpr double a2 = -0.49999999926820904, a3 = 0.33334535235773449, a4 = -0.25002219360866496;
+};
+template <>
+struct FarPoly<8, 3> {
+  static constexpr double a2 = -0.50000078809143556, a3 = 0.33333409330333852, a4 = 0.0;
+};
+
+// tbase: shared-memory byte address of the table minus base * 16 (so that tbase + (hi(x) >> (20 - FB)) * 16 is the
+// entry; one IMAD); lim: the index clamp (largest valid index exterior, smallest interior).  a2r (and a3r, quartic)
+// are the polynomial constants held in registers by the caller (an FP64 FMA takes at most one immediate / uniform
+// operand, and the compiler would otherwise rematerialise the second constant in the loop with two moves per pair).
+template <int KIND, int FB, int DEG>
+__device__ __forceinline__ double green_far_t(double qh, unsigned tbase, int lim, double a2r, double a3r) {
+  const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
+  const double t = qh * y;
+  const double e = fma(-t, y, 0.5);
+  const double w = fma(y, e, y);
+  const double x = (KIND == 1) ? 1.0 + w : fma(qh, w, qh);   // 1 + w  |  qh (1 + w) = q (1 + w) / 2
+  int ix = __double2hiint(x) >> (20 - FB);
+  ix = (KIND == 1) ? min(ix, lim) : max(ix, lim);
+  double cj, lj;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(cj), "=d"(lj) : "r"(tbase + ((unsigned)ix << 4)));
+  const double r = fma(x, cj, -1.0);
+  double p;
+  if (DEG == 4) {
+    p = fma(r, FarPoly<FB, DEG>::a4, a3r);
+    p = fma(r, p, a2r);
+  } else {
+    p = fma(r, FarPoly<FB, DEG>::a3, a2r);
+  }
+  p = fma(r, p, 1.0);
+  return fma(-r, p, w - lj);
+}
+
+// Far-field G, reciprocal-seeded variant (k_pairs_grid FAR 5, 6; R25).  Same reduction as green_far_t,
+// but c = rcp.approx(x_mid) comes from the SFU (x_mid: x's high word with the mantissa below the top FB bits set to
+// the bin midpoint) and only L = -log c (+ ln 2 interior) is read from shared memory: an 8-byte load instead of a
+// 16-byte one.  The pair kernels are bound by shared-memory wavefronts (a warp's 32 random table reads conflict in
+// the banks), so halving the entry halves the dominant traffic.  c is a deterministic function of x_mid's high word:
+// far_table_build_rcp evaluates the same instruction on the device for every bin and tabulates L = -log c exactly.
+__device__ __forceinline__ double rcp_approx(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+template <int FB>
+__device__ __forceinline__ double far_mid(int hx) {   // the bin midpoint of x (high word only; low word 0)
+  return __hiloint2double((hx & ~((1 << (20 - FB)) - 1)) | (1 << (19 - FB)), 0);
+}
+template <int KIND, int FB, int DEG>
+__device__ __forceinline__ double green_far_r(double qh, unsigned tbase, int lim, double a2r, double a3r) {
+  const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
+  const double t = qh * y;
+  const double e = fma(-t, y, 0.5);
+  const double w = fma(y, e, y);
+  const double x = (KIND == 1) ? 1.0 + w : fma(qh, w, qh);
+  const int hx = __double2hiint(x);
+  const double c = rcp_approx(far_mid<FB>(hx));
+  int ix = hx >> (20 - FB);
+  ix = (KIND == 1) ? min(ix, lim) : max(ix, lim);
+  double lj;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(lj) : "r"(tbase + ((unsigned)ix << 3)));
+  const double r = fma(x, c, -1.0);
+  double p;
+  if (DEG == 4) {
+    p = fma(r, FarPoly<FB, DEG>::a4, a3r);
+    p = fma(r, p, a2r);
+  } else {
+    p = fma(r, FarPoly<FB, DEG>::a3, a2r);
+  }
+  p = fma(r, p, 1.0);
+  return fma(-r, p, w - lj);
+}
+
 // reference-accuracy variant (libdevice), used by the self-check path
 template <int KIND>
 __device__ __forceinline__ double green_q_libdevice(double q) {

@@ -4,6 +4,7 @@
 
 #include <map>
 #include <mutex>
+#include <vector>
 
 #include "green.cuh"
 #include "nc_common.cuh"
@@ -28,6 +29,63 @@ const double2* log_table_device() {
   if (cudaMemcpy(d, host, sizeof(host), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
   tabs[dev] = d;
   return d;
+}
+
+// c of the reciprocal-seeded far form (green.cuh green_far_r), evaluated by the same instruction the pair kernel uses
+__global__ void k_far_rcp(int Elo, int bits, int cnt, double* c) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int per = 1 << bits;
+  const int hx = ((Elo + t / per) << 20) | ((t % per) << (20 - bits));
+  c[t] = rcp_approx(__hiloint2double((hx & ~((1 << (20 - bits)) - 1)) | (1 << (19 - bits)), 0));
+}
+
+// far table (green.cuh green_far_t / green_far_r): entries for every biased exponent E that x takes on grid pairs
+// with d in [eps / 4, 2] (exterior x = 1 + 2/d in [2, 1 + 8/eps]; interior x = d^2/8 + d/4 in
+// [eps^2/128 + eps/16, 1]), one exponent of margin on each side; j = the top `bits` mantissa bits.
+int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a3, double2** d, int* n, int* base) {
+  const double dlo = 0.25 * eps;
+  const double xlo = kind == 1 ? 2.0 : dlo * dlo / 8.0 + dlo / 4.0;
+  const double xhi = kind == 1 ? 1.0 + 2.0 / dlo : 1.0;
+  int elo = 0, ehi = 0;
+  frexp(xlo, &elo);   // x = f 2^e, f in [0.5, 1): biased exponent of x is e - 1 + 1023
+  frexp(xhi, &ehi);
+  const int Elo = elo - 1 + 1023 - 1, Ehi = ehi - 1 + 1023 + 1;
+  const int per = 1 << bits;
+  const int cnt = (Ehi - Elo + 1) * per;
+  std::vector<double> c((size_t)cnt);
+  if (rcp) {   // c = rcp.approx(midpoint) as the device computes it
+    double* dc = nullptr;
+    if (cudaMalloc(&dc, c.size() * sizeof(double)) != cudaSuccess) return 1;
+    k_far_rcp<<<(cnt + 255) / 256, 256>>>(Elo, bits, cnt, dc);
+    const bool ok = cudaMemcpy(c.data(), dc, c.size() * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(dc);
+    if (!ok) return 1;
+  } else {
+    for (int t = 0; t < cnt; ++t)
+      c[t] = (double)(1.0L / ldexpl(1.0L + ((t % per) + 0.5L) / per, Elo + t / per - 1023));
+  }
+  const int nvec = rcp ? cnt / 2 : cnt;
+  std::vector<double2> host((size_t)nvec + 1);
+  for (int t = 0; t < cnt; ++t) {
+    long double L = -logl((long double)c[t]);
+    if (kind == 0) L += logl(2.0L);
+    if (rcp)
+      reinterpret_cast<double*>(host.data())[t] = (double)L;
+    else
+      host[t] = make_double2(c[t], (double)L);
+  }
+  host[(size_t)nvec] = make_double2(a2, a3);
+  double2* p = nullptr;
+  if (cudaMalloc(&p, host.size() * sizeof(double2)) != cudaSuccess) return 1;
+  if (cudaMemcpy(p, host.data(), host.size() * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(p);
+    return 1;
+  }
+  *d = p;
+  *n = cnt;
+  *base = Elo * per;
+  return 0;
 }
 
 }  // namespace nc

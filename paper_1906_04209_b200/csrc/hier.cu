@@ -78,6 +78,8 @@ struct HierState {
   int64_t *d_goff = nullptr, *d_coff = nullptr;
   int32_t* d_grid_ids = nullptr;
   int* d_counter = nullptr;         // work counter of the persistent grid kernel
+  double2* d_ftab = nullptr;        // far log table of the grid kernel (FAR >= 2)
+  FarTable ftab;
   int32_t* d_grid_group = nullptr;
   int64_t* d_ggrid0 = nullptr;
   double *d_gx = nullptr, *d_gy = nullptr, *d_gz = nullptr, *d_gval = nullptr, *d_gcoef = nullptr;
@@ -1191,6 +1193,14 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_TRY(upload(h, &H->d_coff, H->coff, s));
   NC_TRY(upload(h, &H->d_grid_ids, H->grid_ids, s));
   NC_TRY(halloc(h, &H->d_counter, 1));
+  if (const int fb = grid_far_table_bits()) {   // far log table of the grid kernel (green.cuh green_far_t)
+    double a2 = 0.0, a3 = 0.0;
+    grid_far_poly(&a2, &a3);
+    if (far_table_build(h->kind, h->eps, fb, grid_far_table_rcp(), a2, a3, &H->d_ftab, &H->ftab.n, &H->ftab.base))
+      return fail(NC_ECUDA, "nc_setup: far log table upload failed");
+    H->ftab.d = H->d_ftab;
+    h->device_bytes += (double)H->ftab.n * sizeof(double2);
+  }
   NC_TRY(upload(h, &H->d_grid_group, H->grid_group, s));
   NC_TRY(upload(h, &H->d_ggrid0, H->ggrid0, s));
   NC_TRY(upload(h, &H->d_units, units, s));
@@ -1230,7 +1240,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   const int Ks = h->Kstar, K = h->K;
   // steps 2-3: interaction-list and leaf-neighbour sources on the incoming grids
   launch_pairs_grid(h->kind, H->d_units, H->nunits, H->d_gx, H->d_gy, H->d_gz, H->d_srclist, h->d_src4, H->pmax,
-                    H->d_part, H->d_counter, s);
+                    H->d_part, H->d_counter, H->ftab, s);
   h->launches_last += H->nunits > 0;
   if (h->time_stages) cudaEventRecord(h->ev[3], s);
   if (H->nchunks) {
@@ -1284,7 +1294,7 @@ void hier_destroy(nc_handle* h) {
   HierState* H = h->hier;
   if (!H) return;
   void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_ids,
-                  H->d_grid_group, H->d_ggrid0, H->d_counter,
+                  H->d_grid_group, H->d_ggrid0, H->d_counter, H->d_ftab,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
                   H->d_chunks, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
                   H->d_udir, H->d_u};

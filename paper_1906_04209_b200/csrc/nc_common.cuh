@@ -53,8 +53,19 @@ struct GridVariant {
   int nt, tpt, unroll, stage, far, tma, minb;   // minb: __launch_bounds__ min blocks per SM (register cap)
   int persist;                                  // 1: persistent CTAs taking units from an atomic counter
 };
-#define kGridVariantDefault (GridVariant{128, 2, 4, 256, 1, 0, 8, 1})
+#define kGridVariantDefault (GridVariant{128, 2, 4, 256, 5, 0, 8, 1})
 int grid_far_variant();
+int grid_far_table_bits();             // bits of the far table the grid-kernel variant in use needs (0: none)
+void grid_far_poly(double* a2, double* a3);   // its log1p polynomial constants (carried after the table)
+int grid_far_table_rcp();              // 1: the variant takes c from rcp.approx and reads L alone (8-byte entries)
+struct FarTable {                      // exponent-indexed far log table (green.cuh green_far_t) on device
+  const double2* d = nullptr;
+  int n = 0, base = 0;
+};
+// host: build and upload the far table for (kind, eps, bits) (green_table.cu); *base = first index (biased
+// exponent << bits), *n entries, followed by one extra entry (a2, a3); the caller owns *d (cudaFree).  0 on success.
+// rcp != 0: the entries are L alone (8 bytes, two per double2; n even) for c = rcp.approx(bin midpoint).
+int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a3, double2** d, int* n, int* base);
 int grid_unit_points();                // grid points per work unit = threads per CTA x targets per thread
 
 struct GridUnit {      // <= grid_unit_points() points of one incoming grid x one slice of its source-patch list
@@ -181,7 +192,7 @@ int pairs_direct_blocks_per_sm(int p, int tpt);
 void split_rows(const double* w, int64_t N, int world, int64_t* begin, int64_t* count);
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
                        const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
-                       int* counter /* device int, persistent variant */, cudaStream_t s);
+                       int* counter /* device int, persistent variant */, const FarTable& ft, cudaStream_t s);
 void launch_pairs_near(int kind, const double* tx, const double* ty, const double* tz, int Kstar, const int32_t* work,
                        int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
                        double* udir, cudaStream_t s);

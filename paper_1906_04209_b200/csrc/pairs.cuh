@@ -84,13 +84,33 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
 // distance from the dot product, qh = (|X|^2 + 1/4)/2 - X.S with the target pre-negated (3 DFMA instead of 6 FP64
 // ops; absolute error ~2e-16, i.e. relative ~1e-10 at the closest grid pairs qh ~ eps^2/8, far below the
 // hierarchical tolerance) and green_far_h.  x/y/z hold -X when FAR, and cq[u] = (|X_u|^2 + 1/4)/2.
-template <int KIND, int TPT, int UNROLL, bool FAR, class Tab, class PatchAt>
+// FAR >= 2: the exponent-indexed far table.  green_far_t (16-byte (c, L) entries): 2 = 7 bits cubic, 3 = 7 bits
+// quartic, 4 = 8 bits cubic; green_far_r (8-byte L entries, c from the SFU): 5 = 7 bits cubic, 6 = 6 bits quartic
+__host__ __device__ constexpr int far_table_bits(int far) { return far == 4 ? 8 : far == 6 ? 6 : 7; }
+__host__ __device__ constexpr bool far_table_rcp(int far) { return far >= 5; }
+inline void far_poly(int far, double* a2, double* a3) {   // the polynomial constants the table carries (host)
+  *a2 = far == 3 ? FarPoly<7, 4>::a2 : far == 4 ? FarPoly<8, 3>::a2 : far == 6 ? FarPoly<6, 4>::a2 : FarPoly<7, 3>::a2;
+  *a3 = far == 3 ? FarPoly<7, 4>::a3 : far == 6 ? FarPoly<6, 4>::a3 : 0.0;
+}
+template <int KIND, int FAR>
+__device__ __forceinline__ double green_far_any(double qh, const double2* __restrict__ logtab, unsigned tbase,
+                                                int lim, double a2, double a3) {
+  if (FAR == 1) return green_far_h<KIND>(qh, logtab);
+  if (FAR == 2) return green_far_t<KIND, 7, 3>(qh, tbase, lim, a2, a3);
+  if (FAR == 3) return green_far_t<KIND, 7, 4>(qh, tbase, lim, a2, a3);
+  if (FAR == 4) return green_far_t<KIND, 8, 3>(qh, tbase, lim, a2, a3);
+  if (FAR == 5) return green_far_r<KIND, 7, 3>(qh, tbase, lim, a2, a3);
+  return green_far_r<KIND, 6, 4>(qh, tbase, lim, a2, a3);
+}
+
+template <int KIND, int TPT, int UNROLL, int FAR, class Tab, class PatchAt>
 __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
                                                 const double (&cq)[TPT], double (&acc)[TPT], int64_t nlist,
                                                 PatchAt patch_at, const double4* __restrict__ s4, int p,
                                                 double4* __restrict__ sm, int64_t* __restrict__ sm_pid, int chp,
                                                 const Tab* __restrict__ logtab, bool active,
-                                                bool single = false) {
+                                                bool single = false, unsigned ftb = 0, int flim = 0,
+                                                double fa2 = 0.0, double fa3 = 0.0) {
   for (int64_t c0 = 0; c0 < nlist; c0 += chp) {
     const int nch = (int)min((int64_t)chp, nlist - c0);
     __syncthreads();
@@ -109,7 +129,7 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
         const double4 s = sm[m];
         if (FAR) {
           const double qh = fma(x[0], s.x, fma(y[0], s.y, fma(z[0], s.z, cq[0])));
-          acc[0] = fma(s.w, green_far_h<KIND>(qh, logtab), acc[0]);
+          acc[0] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3), acc[0]);
         } else {
           const double dx = x[0] - s.x, dy = y[0] - s.y, dz = z[0] - s.z;
           const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
@@ -125,7 +145,7 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
       for (int u = 0; u < TPT; ++u) {
         if (FAR) {
           const double qh = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
-          acc[u] = fma(s.w, green_far_h<KIND>(qh, logtab), acc[u]);
+          acc[u] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3), acc[u]);
         } else {
           const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
           const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
@@ -170,7 +190,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // bufs: 2 x brec records; bars: full[2], empty[2] (initialised here; the caller __syncthreads() before the first
 // wait is done inside).  Threads of warps with no active target must not call (they return before).  nwarps_act:
 // warps that call.  lst: the unit's source-patch list (nsrc entries), s4: the rung's records.
-template <int KIND, int TPT, int UNROLL, bool FAR, class Tab>
+template <int KIND, int TPT, int UNROLL, int FAR, class Tab>
 __device__ __forceinline__ void accumulate_grid_tma(const double (&x)[TPT], const double (&y)[TPT],
                                                     const double (&z)[TPT], const double (&cq)[TPT],
                                                     double (&acc)[TPT], int nsrc, const int32_t* __restrict__ lst,

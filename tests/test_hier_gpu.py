@@ -164,13 +164,15 @@ np.save(os.environ["OUT"], h.matvec(x).cpu().numpy())
 """
 
 
-def test_far_field_pair_variant_error(tmp_path):
-    """k_pairs_grid's far-field evaluation (dot-product distance + one-Newton rsqrt, R23) against the
-    exact pair kernel on the same grids (C3): the difference must stay far below the hierarchical precision."""
+@pytest.mark.parametrize("far", [1, 2, 5, 6])
+def test_far_field_pair_variant_error(tmp_path, far):
+    """k_pairs_grid's far-field evaluations (R23: dot-product distance + one-Newton rsqrt; R25: the
+    exponent-indexed log table, 16-byte (c, L) entries or c from rcp.approx and 8-byte L entries) against the exact
+    pair kernel on the same grids (C3): the difference must stay far below the hierarchical precision."""
     import subprocess
     import sys
     outs = []
-    for v in ("2,4,0,256,0", "2,4,0,256,1"):
+    for v in ("128,2,4,256,0", f"128,2,4,256,{far}"):
         out = str(tmp_path / f"y{v[-1]}.npy")
         env = dict(os.environ, NC_GRID_VARIANT=v, ROOT=ROOT, OUT=out)
         subprocess.run([sys.executable, "-c", _FAR_CHILD], env=env, check=True, timeout=600)
