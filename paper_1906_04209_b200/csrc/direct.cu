@@ -95,7 +95,7 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
 // One CTA of NT threads per work unit: <= NT * TPT adjacent points of one incoming grid x one slice (<= kSliceMax
 // patches, one outgoing-operator rung) of its source list.  Sources are staged in shared memory `chp` patches at a
 // time (a CTA barrier per stage); FAR selects the far-field arithmetic (pairs.cuh accumulate_grid, R23).
-template <int KIND, int NT, int TPT, int UNROLL, int FAR>
+template <int KIND, int NT, int TPT, int UNROLL, int FAR, bool ASYNC>
 __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const double* __restrict__ gx,
                                           const double* __restrict__ gy, const double* __restrict__ gz,
                                           const int32_t* __restrict__ srclist, const double* __restrict__ src4,
@@ -121,11 +121,17 @@ __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const 
   }
   const int32_t* __restrict__ lst = srclist + U.src0;
   const double4* __restrict__ s4 = reinterpret_cast<const double4*>(src4 + U.soff);   // the unit's rung
-  int chp = stage_records / U.p;
-  chp = chp < 1 ? 1 : (chp > kStagePatchesMax ? kStagePatchesMax : chp);
-  accumulate_grid<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc,
-                                                   [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p, sm,
-                                                   pid, chp, logtab, any, single, ftb, flim, fa2, fa3);
+  if (ASYNC) {
+    accumulate_grid_async<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc, lst, s4, U.p, sm, stage_records,
+                                                           reinterpret_cast<int32_t*>(pid), logtab, any, single, ftb,
+                                                           flim, fa2, fa3);
+  } else {
+    int chp = stage_records / U.p;
+    chp = chp < 1 ? 1 : (chp > kStagePatchesMax ? kStagePatchesMax : chp);
+    accumulate_grid<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc,
+                                                     [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p,
+                                                     sm, pid, chp, logtab, any, single, ftb, flim, fa2, fa3);
+  }
   const int upts = NT * TPT;
   if (single) {
     if (wbase + lane < U.npt) part[uid * upts + wbase + lane] = acc[0];
@@ -140,7 +146,7 @@ __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const 
 
 // counter == nullptr: one CTA per unit.  Otherwise a persistent grid: each CTA initialises the log table once and
 // takes units from an atomic counter until all `nunits` are done (results do not depend on the assignment).
-template <int KIND, int NT, int TPT, int UNROLL, int FAR, int MINB>
+template <int KIND, int NT, int TPT, int UNROLL, int FAR, int MINB, bool ASYNC>
 __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restrict__ units, const double* __restrict__ gx,
                                                    const double* __restrict__ gy, const double* __restrict__ gz,
                                                    const int32_t* __restrict__ srclist,
@@ -150,11 +156,11 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
                                                    const double2* __restrict__ fsrc, int fn, int fbase) {
   extern __shared__ double4 sm[];
   __shared__ double2 logtab[FAR >= 2 ? 1 : kLogTableSize];
-  __shared__ int64_t pid[kStagePatchesMax];
+  __shared__ int64_t pid[ASYNC ? 16 : kStagePatchesMax];   // async: the unit's <= 32 source patches (int32)
   __shared__ int next;
   // FAR >= 2: the far table follows the stage buffer in dynamic shared memory; tb is indexed by hi(x) >> (20 - bits)
   // entries: (c, L) double2 (green_far_t) or L alone, packed two per double2 (green_far_r)
-  double2* ftab = reinterpret_cast<double2*>(sm + stage_records);
+  double2* ftab = reinterpret_cast<double2*>(sm + (ASYNC ? 2 : 1) * stage_records);
   constexpr unsigned kEsz = far_table_rcp(FAR) ? 8u : 16u;
   const int nvec = far_table_rcp(FAR) ? fn / 2 : fn;
   const unsigned tb = smem_u32(ftab) - kEsz * (unsigned)fbase;
@@ -171,7 +177,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
   }
   if (!counter) {
     __syncthreads();
-    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[blockIdx.x], blockIdx.x, gx, gy, gz, srclist, src4, stage_records, part,
+    grid_unit<KIND, NT, TPT, UNROLL, FAR, ASYNC>(units[blockIdx.x], blockIdx.x, gx, gy, gz, srclist, src4, stage_records, part,
                                           sm, pid, logtab, tb, flim, fa2, fa3);
     return;
   }
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
     __syncthreads();
     const int u = next;
     if (u >= nunits) break;
-    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[u], u, gx, gy, gz, srclist, src4, stage_records, part, sm, pid, logtab,
+    grid_unit<KIND, NT, TPT, UNROLL, FAR, ASYNC>(units[u], u, gx, gy, gz, srclist, src4, stage_records, part, sm, pid, logtab,
                                           tb, flim, fa2, fa3);
   }
 }
@@ -253,7 +259,7 @@ static GridVariant grid_variant() {
       if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d", &w.nt, &w.tpt, &w.unroll, &w.stage, &w.far, &w.tma, &w.minb,
                  &w.persist) >= 5 &&
           (w.nt == 128 || w.nt == 256) && (w.tpt == 1 || w.tpt == 2) && (w.unroll == 1 || w.unroll == 2 || w.unroll == 4) &&
-          w.stage >= 32 && (w.far >= 0 && w.far <= 6) && (w.tma == 0 || w.tma == 1))
+          w.stage >= 32 && (w.far >= 0 && w.far <= 6) && (w.tma >= 0 && w.tma <= 2))
         v = w;
     }
   }
@@ -267,19 +273,19 @@ void grid_far_poly(double* a2, double* a3) { far_poly(grid_variant().far, a2, a3
 
 int grid_unit_points() { return grid_variant().nt * grid_variant().tpt; }
 
-template <int KIND, int NT, int TPT, int UNROLL, int FAR, bool TMA, int MINB>
+template <int KIND, int NT, int TPT, int UNROLL, int FAR, int TMA, int MINB>
 static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* gx, const double* gy, const double* gz,
                           const int32_t* srclist, const double* src4, int stage, int pmax, double* part,
                           int persist, int* counter, const FarTable& ft, cudaStream_t s) {
   const int rec = std::max(stage, pmax);   // records per stage buffer: >= one whole patch of any rung
   const size_t smem = (TMA ? 2 : 1) * (size_t)rec * sizeof(double4) + (FAR >= 2 ? (size_t)ft.n * (far_table_rcp(FAR) ? 8 : 16) : 0);
-  if (TMA) {
+  if (TMA == 1) {
     auto kern = k_pairs_grid_tma<KIND, NT, TPT, UNROLL, FAR, MINB>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device());
     return;
   }
-  auto kern = k_pairs_grid<KIND, NT, TPT, UNROLL, FAR, MINB>;
+  auto kern = k_pairs_grid<KIND, NT, TPT, UNROLL, FAR, MINB, TMA == 2>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (!persist) {
     kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device(), nullptr,
@@ -309,6 +315,7 @@ void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const do
                                                      v.persist, counter, ft, s);
 #define NC_GK(KD)                                                                                                 \
   NC_G(KD, 128, 2, 4, 2, 0, 8) NC_G(KD, 128, 2, 4, 3, 0, 8) NC_G(KD, 128, 2, 4, 4, 0, 8) NC_G(KD, 128, 2, 4, 2, 0, 6) \
+  NC_G(KD, 128, 2, 4, 5, 2, 8) NC_G(KD, 128, 2, 4, 5, 2, 7) NC_G(KD, 128, 2, 4, 5, 2, 6) NC_G(KD, 128, 2, 2, 5, 2, 8) \
   NC_G(KD, 128, 2, 4, 5, 0, 8) NC_G(KD, 128, 2, 4, 6, 0, 8) NC_G(KD, 128, 2, 4, 5, 0, 6) NC_G(KD, 128, 2, 4, 6, 0, 6) \
   NC_G(KD, 128, 2, 2, 5, 0, 8) NC_G(KD, 256, 1, 4, 5, 0, 4) \
   NC_G(KD, 128, 2, 4, 1, 0, 8) NC_G(KD, 128, 2, 4, 0, 0, 8) NC_G(KD, 128, 2, 4, 1, 1, 8) NC_G(KD, 128, 2, 4, 1, 0, 4) \
@@ -321,9 +328,9 @@ void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const do
 #undef NC_G
   const GridVariant d = kGridVariantDefault;   // combination not instantiated: the default
   if (kind == 0)
-    return launch_grid_t<0, 128, 2, 4, 1, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
+    return launch_grid_t<0, 128, 2, 4, 1, 0, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
                                                     d.persist, counter, ft, s);
-  return launch_grid_t<1, 128, 2, 4, 1, false, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
+  return launch_grid_t<1, 128, 2, 4, 1, 0, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
                                                   d.persist, counter, ft, s);
 }
 

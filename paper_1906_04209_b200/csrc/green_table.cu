@@ -40,17 +40,19 @@ __global__ void k_far_rcp(int Elo, int bits, int cnt, double* c) {
   c[t] = rcp_approx(__hiloint2double((hx & ~((1 << (20 - bits)) - 1)) | (1 << (19 - bits)), 0));
 }
 
-// far table (green.cuh green_far_t / green_far_r): entries for every biased exponent E that x takes on grid pairs
-// with d in [eps / 4, 2] (exterior x = 1 + 2/d in [2, 1 + 8/eps]; interior x = d^2/8 + d/4 in
-// [eps^2/128 + eps/16, 1]), one exponent of margin on each side; j = the top `bits` mantissa bits.
+// far table (green.cuh green_far_t / green_far_r): entries for every biased exponent E that x takes on grid pairs.
+// A grid pair is at chord distance d >= eps (the source's rung is valid from 2 eps of its centre, its skeleton lies
+// within eps of it: DESIGN.md R22); the table covers d in [eps / 2, 2]: exterior x = 1 + 2/d in [2, 1 + 4/eps]
+// (plus the exponent below 2, reachable by rounding of w ~ 1), interior x = d^2/8 + d/4 in [eps^2/32 + eps/8, 1];
+// j = the top `bits` mantissa bits.  The kernel clamps the index on the open side (exterior above, interior below).
 int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a3, double2** d, int* n, int* base) {
-  const double dlo = 0.25 * eps;
+  const double dlo = 0.5 * eps;
   const double xlo = kind == 1 ? 2.0 : dlo * dlo / 8.0 + dlo / 4.0;
   const double xhi = kind == 1 ? 1.0 + 2.0 / dlo : 1.0;
   int elo = 0, ehi = 0;
   frexp(xlo, &elo);   // x = f 2^e, f in [0.5, 1): biased exponent of x is e - 1 + 1023
   frexp(xhi, &ehi);
-  const int Elo = elo - 1 + 1023 - 1, Ehi = ehi - 1 + 1023 + 1;
+  const int Elo = elo - 1 + 1023 - (kind == 1 ? 1 : 0), Ehi = ehi - 1 + 1023;
   const int per = 1 << bits;
   const int cnt = (Ehi - Elo + 1) * per;
   std::vector<double> c((size_t)cnt);

@@ -79,6 +79,19 @@ struct HierState {
   int32_t* d_grid_ids = nullptr;
   int* d_counter = nullptr;         // work counter of the persistent grid kernel
   double2* d_ftab = nullptr;        // far log table of the grid kernel (FAR >= 2)
+  // separable step 4 for single-member groups (k_interp_sep): node rings of the canonical Zernike nodes
+  bool sep_nodes = false;           // the nodes lie on rings (detected from the tables; NC_INTERP_SEP=0 disables)
+  int nring = 0;
+  std::vector<double> ring_t;       // geodesic radius of each ring
+  std::vector<int32_t> node_ring;   // ring of each node
+  std::vector<double> node_cs;      // (cos, sin) of each node's angle in the canonical frame
+  uint8_t* d_gsep = nullptr;        // group evaluated by k_interp_sep
+  int32_t* d_work_sep = nullptr;    // local patches with at least one such level
+  int64_t nwork_sep = 0;
+  double* d_ring_t = nullptr;
+  int32_t* d_node_ring = nullptr;
+  double* d_node_cs = nullptr;
+  double sep_terms = 0.0;           // node x coefficient terms those groups represent (part of interp_terms)
   FarTable ftab;
   int32_t* d_grid_group = nullptr;
   int64_t* d_ggrid0 = nullptr;
@@ -348,6 +361,18 @@ __global__ void k_group_frames(const double* __restrict__ gc, int64_t ngroups, d
   r[0] = ex; r[1] = ey; r[2] = ez; r[3] = fx; r[4] = fy; r[5] = fz; r[6] = cx; r[7] = cy; r[8] = cz;
 }
 
+// A group with one member takes that patch's own centre and frame (the ABI frame rule gives the same frame up to
+// rounding): the member's Zernike nodes then sit exactly on their canonical rings in the group frame, which the
+// separable step-4 evaluation (k_interp_sep) relies on.
+__global__ void k_single_frames(const int32_t* __restrict__ gfirst, const int32_t* __restrict__ glast, int64_t ngroups,
+                                const double* __restrict__ frames, double* __restrict__ gc, double* __restrict__ F) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ngroups || glast[g] - gfirst[g] != 1) return;
+  const double* R = frames + 9 * (int64_t)gfirst[g];   // [e1 | e2 | c], the same order as the group rows
+  for (int t = 0; t < 9; ++t) F[9 * g + t] = R[t];
+  for (int t = 0; t < 3; ++t) gc[3 * g + t] = R[6 + t];
+}
+
 // incoming-grid points: r_k = R cos(pi (k + 1/2) / (2 n_r)) (positive half of a 2 n_r Chebyshev grid),
 // theta_l = 2 pi l / n_a;  x = cos(r) c + sin(r) (cos(theta) e1 + sin(theta) e2), stored x 1/2
 __global__ void k_grid_points(const int32_t* __restrict__ grids, int64_t ngr, const int32_t* __restrict__ grid_group,
@@ -438,6 +463,72 @@ __global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, cons
   }
 }
 
+// One grid's expansion at NPT nodes, angular sums first (MB = 0 variant of k_interp): per parity of m,
+//   E_j = sum_{m of that parity} c[m][j] . (cos m theta, sin m theta)        (2 FMA per (m, j, node))
+//   u  += sum_j E_j T_{par + 2 j}(x)                                          (once per grid and parity)
+// The n_r accumulators per node live in registers (NR = n_r exactly, one instantiation per n_r: no idle FMAs).
+template <int NR, int NPT>
+__device__ __forceinline__ void grid_eval_ang(const double2* __restrict__ cg, int M, const double (&x)[NPT],
+                                              const double (&w2)[NPT], const double (&c1)[NPT],
+                                              const double (&s1)[NPT], double (&acc)[NPT]) {
+#pragma unroll
+  for (int par = 0; par < 2; ++par) {
+    if (par > M) break;
+    double E[NPT][NR];
+    double cm[NPT], sm[NPT], cp[NPT], sp[NPT], t2[NPT];   // cos/sin(m theta), ((m - 2) theta); 2 cos 2 theta
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+#pragma unroll
+      for (int j = 0; j < NR; ++j) E[q][j] = 0.0;
+      const double c2 = fma(2.0 * c1[q], c1[q], -1.0), s2 = 2.0 * s1[q] * c1[q];
+      t2[q] = 2.0 * c2;
+      if (par == 0) { cm[q] = 1.0; sm[q] = 0.0; cp[q] = c2; sp[q] = -s2; }
+      else { cm[q] = c1[q]; sm[q] = s1[q]; cp[q] = c1[q]; sp[q] = -s1[q]; }
+    }
+    for (int m = par; m <= M; m += 2) {
+      const double2* __restrict__ cmj = cg + m * NR;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const double2 c = cmj[j];
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) E[q][j] = fma(c.x, cm[q], fma(c.y, sm[q], E[q][j]));
+      }
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) {   // (m, m - 2) -> (m + 2, m)
+        const double cn = fma(t2[q], cm[q], -cp[q]), sn = fma(t2[q], sm[q], -sp[q]);
+        cp[q] = cm[q]; sp[q] = sm[q]; cm[q] = cn; sm[q] = sn;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {   // sum_j E_j T_{par + 2 j}(x), T_{n+2} = w2 T_n - T_{n-2}
+      double ta = par ? x[q] : 1.0;                                               // T_par
+      double tb = par ? x[q] * fma(4.0 * x[q], x[q], -3.0) : fma(2.0 * x[q], x[q], -1.0);   // T_{par+2}
+      double v = E[q][0] * ta;
+#pragma unroll
+      for (int j = 1; j < NR; ++j) {
+        v = fma(E[q][j], tb, v);
+        const double tn = fma(w2[q], tb, -ta);
+        ta = tb;
+        tb = tn;
+      }
+      acc[q] += v;
+    }
+  }
+}
+
+template <int NPT>
+__device__ __forceinline__ bool grid_eval_ang_any(int nr, const double2* __restrict__ cg, int M, const double (&x)[NPT],
+                                                  const double (&w2)[NPT], const double (&c1)[NPT],
+                                                  const double (&s1)[NPT], double (&acc)[NPT]) {
+  switch (nr) {
+#define NC_GE(R) \
+  case R: grid_eval_ang<R, NPT>(cg, M, x, w2, c1, s1, acc); return true;
+    NC_GE(1) NC_GE(2) NC_GE(3) NC_GE(4) NC_GE(5) NC_GE(6) NC_GE(7) NC_GE(8) NC_GE(9) NC_GE(10) NC_GE(11) NC_GE(12)
+#undef NC_GE
+    default: return false;
+  }
+}
+
 // step 4b: u_i(node) = udir + sum over levels of the level's group expansions at the node,
 //   u(x, theta) = sum_m sum_j c[m][j] . (cos m theta, sin m theta) T_{(m & 1) + 2 j}(rho / R)
 // (rho = geodesic distance from the cap centre).  One CTA of NT threads per target patch, NPT nodes per thread.
@@ -454,7 +545,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
                                                const int64_t* __restrict__ coff, const double* __restrict__ coef,
                                                const double* __restrict__ tx, const double* __restrict__ ty,
                                                const double* __restrict__ tz, const double* __restrict__ udir,
-                                               double* __restrict__ u) {
+                                               double* __restrict__ u, const uint8_t* __restrict__ gsep) {
   extern __shared__ double2 c2[];
   const int64_t i = blockIdx.x;
   for (int kb = 0; kb < Kstar; kb += NPT * NT) {
@@ -470,6 +561,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
       const int g = pgl[(int64_t)lvl * rc + i];
       const int64_t kg0 = ggrid0[g], kg1 = ggrid0[g + 1];
       if (kg0 == kg1 || gnr[kg0] == 0) continue;   // block-uniform (a group's grids are all local or none)
+      if (gsep && gsep[g]) continue;                // evaluated by k_interp_sep
       __syncthreads();                              // previous level's readers of c2 are done
       {
         int base = 0;
@@ -501,10 +593,11 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
         const int nr = gnr[kg], M = gna[kg] / 2;
         const double2* __restrict__ cg = c2 + base;
         base += (M + 1) * nr;
+        if (MB == 0 && grid_eval_ang_any<NPT>(nr, cg, M, x, w2, c1, s1, acc)) continue;   // n_r <= 12
         double cm[NPT], sm[NPT], cmm[NPT], smm[NPT];   // cos/sin(m theta), ((m - 1) theta)
 #pragma unroll
         for (int q = 0; q < NPT; ++q) { cm[q] = 1.0; sm[q] = 0.0; cmm[q] = c1[q]; smm[q] = -s1[q]; }
-        if (MB == 1) {
+        if (MB <= 1) {
           // orders in pairs (m even, m + 1 odd); cos/sin(m theta) advanced in place two orders at a time and the
           // Chebyshev pair (T_n, T_{n+2}) advanced in place two degrees at a time: no register rotation moves
           double ce[NPT], se[NPT], co[NPT], so[NPT];
@@ -560,7 +653,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
           }
         } else {
           for (int m0 = 0; m0 <= M; m0 += MB) {
-            double A[MB][NPT], B[MB][NPT], te[NPT], tep[NPT], to[NPT], top[NPT];
+            double A[MB > 1 ? MB : 1][NPT], B[MB > 1 ? MB : 1][NPT], te[NPT], tep[NPT], to[NPT], top[NPT];
             // T_0 = 1, T_1 = x; the step-2 recurrence starts from T_{-2} = T_2 and T_{-1} = T_1 (T_{-n} = T_n)
 #pragma unroll
             for (int q = 0; q < NPT; ++q) {
@@ -619,14 +712,108 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
   }
 }
 
-// interpolation variant: NC_INTERP_VARIANT="NT,NPT,MB" (k_interp<NT,NPT,MB>; default 128,4,1)
+// step 4b for single-member groups (evaluated separably): the group frame is the member's own
+// (k_single_frames), so node k lies at geodesic radius t_a (its ring a) and angle theta_k, and
+//   u_k += sum_m A_a[m] . (cos m theta_k, sin m theta_k),   A_a[m] = sum_j c[m][j] T_{(m & 1) + 2 j}(t_a / R)
+// costs nA (M+1) n_r + K* (M+1) terms per grid instead of K* (M+1) n_r.  One CTA per patch of `work`, all its
+// single-member levels; runs after k_interp (which skipped those levels) and adds to u.
+template <int NT, int NPT>
+__global__ void __launch_bounds__(NT) k_interp_sep(int L, int64_t rc, int Ks, const int32_t* __restrict__ work,
+                                                   const int32_t* __restrict__ pgl, const uint8_t* __restrict__ gsep,
+                                                   const int64_t* __restrict__ ggrid0, const double* __restrict__ gR,
+                                                   const int32_t* __restrict__ gnr, const int32_t* __restrict__ gna,
+                                                   const int64_t* __restrict__ coff, const double* __restrict__ coef,
+                                                   int nA, const double* __restrict__ ring_t,
+                                                   const int32_t* __restrict__ node_ring,
+                                                   const double* __restrict__ node_cs, int cpairs, int Mmax,
+                                                   int nrmax, double* __restrict__ u) {
+  extern __shared__ double2 sx2[];
+  double2* cb = sx2;                                  // the grid's coefficient pairs c[m][j]
+  double2* A = sx2 + cpairs;                          // nA x (Mmax + 1)
+  double* T = reinterpret_cast<double*>(A + (size_t)nA * (Mmax + 1));   // nA x (2 nrmax + 1)
+  const int TS = 2 * nrmax + 1;
+  const int64_t i = work[blockIdx.x];
+  double acc[NPT], c1[NPT], s1[NPT];
+  int ring[NPT];
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    const int k = min((int)threadIdx.x + q * NT, Ks - 1);
+    acc[q] = 0.0;
+    ring[q] = node_ring[k];
+    c1[q] = node_cs[2 * k];
+    s1[q] = node_cs[2 * k + 1];
+  }
+  for (int lvl = 0; lvl <= L; ++lvl) {
+    const int g = pgl[(int64_t)lvl * rc + i];
+    if (!gsep[g]) continue;                                     // block-uniform
+    const double invR = 1.0 / gR[g];
+    for (int64_t kg = ggrid0[g]; kg < ggrid0[g + 1]; ++kg) {
+      const int nr = gnr[kg], M = gna[kg] / 2;
+      __syncthreads();                                          // previous grid's readers are done
+      {
+        const int ncp = (M + 1) * nr;
+        const double2* __restrict__ src = reinterpret_cast<const double2*>(coef + coff[kg]);
+        for (int t = threadIdx.x; t < ncp; t += NT) cb[t] = src[t];
+      }
+      for (int a = threadIdx.x; a < nA; a += NT) {              // T_n(t_a / R), n <= 2 nr - 1
+        const double x = ring_t[a] * invR;
+        double* Ta = T + a * TS;
+        double tm = 1.0, tn = x;
+        Ta[0] = 1.0;
+        Ta[1] = x;
+        for (int n = 2; n < 2 * nr; ++n) {
+          const double t2 = fma(2.0 * x, tn, -tm);
+          Ta[n] = t2;
+          tm = tn;
+          tn = t2;
+        }
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < nA * (M + 1); t += NT) {   // A_a[m]
+        const int a = t / (M + 1), m = t - a * (M + 1);
+        const double2* __restrict__ cm = cb + m * nr;
+        const double* __restrict__ Ta = T + a * TS + (m & 1);
+        double ax = 0.0, ay = 0.0;
+        for (int j = 0; j < nr; ++j) {
+          const double tv = Ta[2 * j];
+          ax = fma(cm[j].x, tv, ax);
+          ay = fma(cm[j].y, tv, ay);
+        }
+        A[a * (Mmax + 1) + m] = make_double2(ax, ay);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) {
+        const double2* __restrict__ Aa = A + ring[q] * (Mmax + 1);
+        double cm = 1.0, sm = 0.0, cp = c1[q], sp = -s1[q];   // cos/sin(m theta), ((m - 1) theta)
+        const double tc = 2.0 * c1[q];
+        double v = 0.0;
+        for (int m = 0; m <= M; ++m) {
+          const double2 am = Aa[m];
+          v = fma(am.x, cm, fma(am.y, sm, v));
+          const double cn = fma(tc, cm, -cp), sn = fma(tc, sm, -sp);
+          cp = cm; sp = sm; cm = cn; sm = sn;
+        }
+        acc[q] += v;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    const int k = (int)threadIdx.x + q * NT;
+    if (k < Ks) u[i * Ks + k] += acc[q];
+  }
+}
+
+// interpolation variant: NC_INTERP_VARIANT="NT,NPT,MB,MINB" (k_interp<NT,NPT,MB,MINB>; default 256,2,0,2;
+// MB = 0: grid_eval_ang for n_r <= 12, MB = 1: Chebyshev sums first, MB > 1: MB orders per radial loop)
 struct InterpVariant {
   int nt, npt, mb, minb;
 };
 static InterpVariant interp_variant() {
   static InterpVariant v = {-1, 0, 0, 0};
   if (v.nt < 0) {
-    v = {128, 4, 1, 4};
+    v = {256, 2, 0, 2};   // angular sums first (grid_eval_ang), measured fastest at C5 (profiles/r01l_interp_*)
     if (const char* e = getenv("NC_INTERP_VARIANT")) {
       InterpVariant w = v;
       w.minb = 1;
@@ -640,27 +827,29 @@ template <int NT, int NPT, int MB, int MINB>
 static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const int64_t* ggrid0,
                            const double* F, const double* gR, const int32_t* gnr, const int32_t* gna,
                            const int64_t* coff, const double* coef, const double* tx, const double* ty,
-                           const double* tz, const double* udir, double* u, cudaStream_t s) {
+                           const double* tz, const double* udir, double* u, const uint8_t* gsep, cudaStream_t s) {
   auto kern = k_interp<NT, NPT, MB, MINB>;
   if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u);
+  kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep);
   return NC_OK;
 }
 
 static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int namax, const int32_t* pgl,
                          const int64_t* ggrid0, const double* F, const double* gR, const int32_t* gnr,
                          const int32_t* gna, const int64_t* coff, const double* coef, const double* tx,
-                         const double* ty, const double* tz, const double* udir, double* u, cudaStream_t s) {
+                         const double* ty, const double* tz, const double* udir, double* u, const uint8_t* gsep,
+                         cudaStream_t s) {
   const InterpVariant v = interp_variant();
   (void)nrmax;
   (void)namax;
 #define NC_I(NT, NPT, MB, MINB)                                                                             \
   if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                           \
-    return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
+    return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep, s);
   NC_I(128, 4, 1, 5) NC_I(128, 4, 1, 4) NC_I(128, 4, 1, 3) NC_I(128, 4, 1, 1) NC_I(256, 2, 1, 2) NC_I(128, 4, 2, 4)
-  NC_I(256, 2, 2, 3)
+  NC_I(256, 2, 2, 3) NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6)
 #undef NC_I
-  return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, s);
+  return launch_interp_t<256, 2, 0, 2>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
+                                       s);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -779,6 +968,31 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   const int L = H->L;
   const double eps = h->eps;
   const int Ks = h->Kstar, p = h->p;
+  // ---- node rings of the canonical Zernike nodes (separable step 4 for single-member groups) ----
+  {
+    const char* e = getenv("NC_INTERP_SEP");
+    std::vector<double> z;
+    NC_TRY(download(z, h->d_zhat, (size_t)3 * Ks, s));
+    H->node_ring.assign(Ks, -1);
+    H->node_cs.assign(2 * (size_t)Ks, 0.0);
+    H->ring_t.clear();
+    bool ok = !(e && e[0] == '0');
+    for (int k = 0; k < Ks && ok; ++k) {
+      const double rho = std::hypot(z[3 * k], z[3 * k + 1]);
+      const double t = std::atan2(rho, z[3 * k + 2]);   // geodesic radius (unit sphere)
+      if (!(rho > 0.0)) { ok = false; break; }         // a node at the centre has no angle
+      H->node_cs[2 * k] = z[3 * k] / rho;
+      H->node_cs[2 * k + 1] = z[3 * k + 1] / rho;
+      int a = 0;
+      for (; a < (int)H->ring_t.size(); ++a)
+        if (std::fabs(H->ring_t[a] - t) <= 1e-13 * std::max(1.0, t)) break;
+      if (a == (int)H->ring_t.size()) H->ring_t.push_back(t);
+      H->node_ring[k] = a;
+    }
+    // worth it only when the rings are few (a tensor-product node set: nA rings x angles)
+    H->nring = (int)H->ring_t.size();
+    H->sep_nodes = ok && H->nring > 0 && 4 * H->nring <= Ks;
+  }
   // ---- boxes per level (device flags + scan) ----
   int *d_flag = nullptr, *d_scan = nullptr;
   NC_TRY(halloc(h, &d_flag, N));
@@ -850,6 +1064,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   k_ilist<<<gb, 128, 0, s>>>(d_gkey, d_lvl, L, G, d_nbr, d_gfirst, d_pg, N, d_off, d_cnt, d_il);
   k_circles<<<(unsigned)((32 * G + 127) / 128), 128, 0, s>>>(d_cen, d_gfirst, d_glast, G, eps, d_gc, H->d_gR);
   k_group_frames<<<gb, 128, 0, s>>>(d_gc, G, H->d_gframe);
+  if (H->sep_nodes) k_single_frames<<<gb, 128, 0, s>>>(d_gfirst, d_glast, G, h->d_frames, d_gc, H->d_gframe);
   NC_TRY(download(H->nbr, d_nbr, 8 * G, s));
   NC_TRY(download(H->il, d_il, nil, s));
   NC_TRY(download(H->gc, d_gc, 3 * G, s));
@@ -1158,11 +1373,22 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       H->pairs_near += (double)nl[i].size() * Ks * p;
     }
   }
+  std::vector<double> lvl_terms(L + 1, 0.0), lvl_single(L + 1, 0.0);
   for (int64_t i = rb; i < re; ++i)
     for (int lvl = 0; lvl <= L; ++lvl) {
       const int32_t g = H->pgroup[(size_t)lvl * N + i];
-      for (int64_t kg = H->ggrid0[g]; kg < H->ggrid0[g + 1]; ++kg) H->interp_terms += (double)Ks * H->gnr[kg] * H->gna[kg];
+      for (int64_t kg = H->ggrid0[g]; kg < H->ggrid0[g + 1]; ++kg) {
+        const double t = (double)Ks * H->gnr[kg] * H->gna[kg];
+        H->interp_terms += t;
+        lvl_terms[lvl] += t;
+        if (H->glast[g] - H->gfirst[g] == 1) lvl_single[lvl] += t;
+      }
     }
+  if (diag) {
+    fprintf(stderr, "[nc hier diag] interpolation terms by level (all / single-member groups):");
+    for (int lvl = 0; lvl <= L; ++lvl) fprintf(stderr, " %d:%.3g/%.3g", lvl, lvl_terms[lvl], lvl_single[lvl]);
+    fprintf(stderr, "\n");
+  }
   // tree lists for introspection (audit): (level, target group, source group)
   H->ilist_entries.clear();
   H->nbr_entries.clear();
@@ -1213,6 +1439,31 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   for (int lvl = 0; lvl <= L; ++lvl)
     for (int64_t i = 0; i < rc; ++i) pgl[(size_t)lvl * rc + i] = H->pgroup[(size_t)lvl * N + rb + i];
   NC_TRY(upload(h, &H->d_pgl, pgl, s));
+  if (H->sep_nodes) {   // single-member groups with local grids go to k_interp_sep
+    std::vector<uint8_t> gsep(G, 0);
+    for (int64_t g = 0; g < G; ++g)
+      gsep[g] = H->glast[g] - H->gfirst[g] == 1 && H->ggrid0[g] < H->ggrid0[g + 1] && H->gnr[H->ggrid0[g]] > 0;
+    std::vector<int32_t> work_sep;
+    for (int64_t i = 0; i < rc; ++i) {
+      bool any = false;
+      for (int lvl = 0; lvl <= L; ++lvl) {
+        const int32_t g = pgl[(size_t)lvl * rc + i];
+        if (gsep[g]) {
+          any = true;
+          for (int64_t kg = H->ggrid0[g]; kg < H->ggrid0[g + 1]; ++kg) H->sep_terms += (double)Ks * H->gnr[kg] * H->gna[kg];
+        }
+      }
+      if (any) work_sep.push_back((int32_t)i);
+    }
+    H->nwork_sep = (int64_t)work_sep.size();
+    NC_TRY(upload(h, &H->d_gsep, gsep, s));
+    NC_TRY(upload(h, &H->d_work_sep, work_sep, s));
+    NC_TRY(upload(h, &H->d_ring_t, H->ring_t, s));
+    NC_TRY(upload(h, &H->d_node_ring, H->node_ring, s));
+    NC_TRY(upload(h, &H->d_node_cs, H->node_cs, s));
+    if (diag) fprintf(stderr, "[nc hier diag] separable step 4: %lld patches, %.3g of %.3g interpolation terms\n",
+                      (long long)H->nwork_sep, H->sep_terms, H->interp_terms);
+  }
   NC_TRY(halloc(h, &H->d_gx, H->Q));
   NC_TRY(halloc(h, &H->d_gy, H->Q));
   NC_TRY(halloc(h, &H->d_gz, H->Q));
@@ -1265,7 +1516,20 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   if (rc > 0) {
     const size_t shm = (size_t)std::max(H->cgroupmax, 1) * sizeof(double);   // all grids of one group
     NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gR,
-                         H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u, s));
+                         H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u,
+                         H->d_gsep, s));
+    h->launches_last++;
+  }
+  if (H->nwork_sep) {   // single-member groups, separably (adds to u)
+    const int Mmax = H->namax / 2, cpairs = std::max(H->cmax / 2, 1);
+    const size_t shm = (size_t)cpairs * sizeof(double2) + (size_t)H->nring * (Mmax + 1) * sizeof(double2) +
+                       (size_t)H->nring * (2 * H->nrmax + 1) * sizeof(double);
+    auto kern = k_interp_sep<128, 4>;
+    if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    kern<<<(unsigned)H->nwork_sep, 128, shm, s>>>(H->L, rc, Ks, H->d_work_sep, H->d_pgl, H->d_gsep, H->d_ggrid0,
+                                                   H->d_gR, H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->nring,
+                                                   H->d_ring_t, H->d_node_ring, H->d_node_cs, cpairs, Mmax, H->nrmax,
+                                                   H->d_u);
     h->launches_last++;
   }
   // step 5: y = x + U P^T
@@ -1294,7 +1558,8 @@ void hier_destroy(nc_handle* h) {
   HierState* H = h->hier;
   if (!H) return;
   void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_ids,
-                  H->d_grid_group, H->d_ggrid0, H->d_counter, H->d_ftab,
+                  H->d_grid_group, H->d_ggrid0, H->d_counter, H->d_ftab, H->d_gsep, H->d_work_sep, H->d_ring_t,
+                  H->d_node_ring, H->d_node_cs,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
                   H->d_chunks, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
                   H->d_udir, H->d_u};

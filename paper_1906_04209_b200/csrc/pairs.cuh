@@ -103,6 +103,45 @@ __device__ __forceinline__ double green_far_any(double qh, const double2* __rest
   return green_far_r<KIND, 6, 4>(qh, tbase, lim, a2, a3);
 }
 
+// the records [0, nrec) of a staged chunk against the thread's targets (incoming-grid sums, no self exclusion)
+template <int KIND, int TPT, int UNROLL, int FAR, class Tab>
+__device__ __forceinline__ void accumulate_span(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
+                                                const double (&cq)[TPT], double (&acc)[TPT],
+                                                const double4* __restrict__ sm, int nrec, bool single,
+                                                const Tab* __restrict__ logtab, unsigned ftb, int flim, double fa2,
+                                                double fa3) {
+  if (single) {   // warp-uniform: a tail warp with <= 32 points evaluates one target per lane
+#pragma unroll UNROLL
+    for (int m = 0; m < nrec; ++m) {
+      const double4 s = sm[m];
+      if (FAR) {
+        const double qh = fma(x[0], s.x, fma(y[0], s.y, fma(z[0], s.z, cq[0])));
+        acc[0] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3), acc[0]);
+      } else {
+        const double dx = x[0] - s.x, dy = y[0] - s.y, dz = z[0] - s.z;
+        const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
+        acc[0] = fma(s.w, green_q<KIND>(qd, logtab), acc[0]);
+      }
+    }
+    return;
+  }
+#pragma unroll UNROLL
+  for (int m = 0; m < nrec; ++m) {
+    const double4 s = sm[m];
+#pragma unroll
+    for (int u = 0; u < TPT; ++u) {
+      if (FAR) {
+        const double qh = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
+        acc[u] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3), acc[u]);
+      } else {
+        const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
+        const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
+        acc[u] = fma(s.w, green_q<KIND>(qd, logtab), acc[u]);
+      }
+    }
+  }
+}
+
 template <int KIND, int TPT, int UNROLL, int FAR, class Tab, class PatchAt>
 __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
                                                 const double (&cq)[TPT], double (&acc)[TPT], int64_t nlist,
@@ -122,37 +161,58 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
     }
     __syncthreads();
     if (!active) continue;
-    const int nrec = nch * p;
-    if (single) {   // warp-uniform: a tail warp with <= 32 points evaluates one target per lane
-#pragma unroll UNROLL
-      for (int m = 0; m < nrec; ++m) {
-        const double4 s = sm[m];
-        if (FAR) {
-          const double qh = fma(x[0], s.x, fma(y[0], s.y, fma(z[0], s.z, cq[0])));
-          acc[0] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3), acc[0]);
-        } else {
-          const double dx = x[0] - s.x, dy = y[0] - s.y, dz = z[0] - s.z;
-          const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
-          acc[0] = fma(s.w, green_q<KIND>(qd, logtab), acc[0]);
-        }
-      }
-      continue;
+    accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, sm, nch * p, single, logtab, ftb, flim, fa2, fa3);
+  }
+}
+
+// Asynchronous double-buffered variant: the unit's source list (<= 32 patches) is staged once; chunk c + 1 is copied
+// global -> shared with cp.async (16-byte pieces, no registers in flight) while chunk c is evaluated, so the warps
+// wait at the chunk barrier only for the slowest warp, not for the copy.  bufs: 2 x brec records.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int KIND, int TPT, int UNROLL, int FAR, class Tab>
+__device__ __forceinline__ void accumulate_grid_async(const double (&x)[TPT], const double (&y)[TPT],
+                                                      const double (&z)[TPT], const double (&cq)[TPT],
+                                                      double (&acc)[TPT], int nsrc, const int32_t* __restrict__ lst,
+                                                      const double4* __restrict__ s4, int p,
+                                                      double4* __restrict__ bufs, int brec, int32_t* __restrict__ slst,
+                                                      const Tab* __restrict__ logtab, bool active, bool single,
+                                                      unsigned ftb, int flim, double fa2, double fa3) {
+  __syncthreads();   // the previous unit is done with slst and the buffers
+  if ((int)threadIdx.x < nsrc) slst[threadIdx.x] = lst[threadIdx.x];
+  __syncthreads();
+  const int chp = max(1, brec / p);
+  const int nch = (nsrc + chp - 1) / chp;
+  auto issue = [&](int c) {
+    const int k0 = c * chp, k1 = min(nsrc, k0 + chp);
+    double2* dst = reinterpret_cast<double2*>(bufs + (size_t)(c & 1) * brec);
+    const int n16 = (k1 - k0) * p * 2;
+    for (int t = threadIdx.x; t < n16; t += blockDim.x) {
+      const int rr = t >> 1, q = rr / p, m = rr - q * p;
+      cp_async16(dst + t, reinterpret_cast<const double2*>(s4 + (size_t)slst[k0 + q] * p + m) + (t & 1));
     }
-#pragma unroll UNROLL
-    for (int m = 0; m < nrec; ++m) {
-      const double4 s = sm[m];
-#pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        if (FAR) {
-          const double qh = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
-          acc[u] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3), acc[u]);
-        } else {
-          const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
-          const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
-          acc[u] = fma(s.w, green_q<KIND>(qd, logtab), acc[u]);
-        }
-      }
+    cp_async_commit();
+  };
+  issue(0);
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) {
+      issue(c + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
+    __syncthreads();   // chunk c is in shared memory for every thread
+    if (active)
+      accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, bufs + (size_t)(c & 1) * brec,
+                                              (min(nsrc, (c + 1) * chp) - c * chp) * p, single, logtab, ftb, flim,
+                                              fa2, fa3);
+    __syncthreads();   // every thread is done with buffer c & 1 before chunk c + 2 overwrites it
   }
 }
 

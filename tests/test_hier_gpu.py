@@ -180,6 +180,23 @@ def test_far_field_pair_variant_error(tmp_path, far):
     assert rel(outs[1], outs[0]) <= 1e-11
 
 
+@pytest.mark.parametrize("env", [{"NC_INTERP_SEP": "0"}, {"NC_INTERP_VARIANT": "128,4,1,4"},
+                                 {"NC_INTERP_VARIANT": "128,4,2,4"}])
+def test_step4_evaluation_variants_agree(tmp_path, env):
+    """Step 4 evaluated three ways: angular sums first with register accumulators (default),
+    Chebyshev sums first (MB = 1) or blocked orders (MB = 2), and single-member groups separably on the Zernike node
+    rings (k_interp_sep) or directly (NC_INTERP_SEP=0).  The same expansion at the same nodes: rounding-level agreement."""
+    import subprocess
+    import sys
+    outs = []
+    for e in ({}, env):
+        out = str(tmp_path / f"y{len(outs)}.npy")
+        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(os.environ, ROOT=ROOT, OUT=out, **e), check=True,
+                       timeout=600)
+        outs.append(np.load(out))
+    assert rel(outs[1], outs[0]) <= 1e-13
+
+
 @pytest.mark.parametrize("precision", [1e-7, 1e-11])
 def test_hier_precision_knob_C2(precision):
     """The requested precision controls the incoming-grid tolerance (R21): the matvec error tracks it
