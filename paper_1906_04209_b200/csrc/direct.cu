@@ -245,6 +245,28 @@ static bool stage_ldg() {
   return v == 1;
 }
 
+// instantiated grid-kernel variants: warp-level units (tpt, unroll, far, warps per CTA, minb) and CTA units
+// (nt, tpt, unroll, far, tma, minb); NC_GRID_VARIANT must name one of them (else the default is kept)
+#define NC_GRID_W_LIST(X) X(2, 4, 5, 8, 3) X(2, 4, 5, 8, 4) X(2, 4, 5, 4, 8) X(2, 2, 5, 8, 4) X(2, 4, 6, 8, 4)
+#define NC_GRID_C_LIST(X)                                                                                        \
+  X(128, 2, 4, 2, 0, 8) X(128, 2, 4, 3, 0, 8) X(128, 2, 4, 4, 0, 8) X(128, 2, 4, 2, 0, 6) X(128, 2, 4, 5, 2, 8)   \
+  X(128, 2, 4, 5, 2, 7) X(128, 2, 4, 5, 2, 6) X(128, 2, 2, 5, 2, 8) X(128, 2, 4, 5, 0, 8) X(128, 2, 4, 6, 0, 8)   \
+  X(128, 2, 4, 5, 0, 6) X(128, 2, 4, 6, 0, 6) X(128, 2, 2, 5, 0, 8) X(256, 1, 4, 5, 0, 4) X(128, 2, 4, 1, 0, 8)   \
+  X(128, 2, 4, 0, 0, 8) X(128, 2, 4, 1, 1, 8) X(128, 2, 4, 1, 0, 4) X(128, 2, 4, 1, 0, 6) X(256, 1, 4, 1, 0, 1)   \
+  X(256, 1, 4, 1, 0, 5) X(256, 1, 4, 1, 0, 6) X(256, 1, 2, 1, 0, 6) X(256, 2, 2, 1, 0, 5) X(256, 1, 4, 1, 1, 6)
+
+static bool grid_variant_instantiated(const GridVariant& v) {
+#define NC_GW(TP, UR, FR, WP, MB) \
+  if (v.tma == 3 && v.tpt == TP && v.unroll == UR && v.far == FR && v.nt == WP && v.minb == MB) return true;
+#define NC_G(NT, TP, UR, FR, TM, MB) \
+  if (v.tma == TM && v.nt == NT && v.tpt == TP && v.unroll == UR && v.far == FR && v.minb == MB) return true;
+  NC_GRID_W_LIST(NC_GW)
+  NC_GRID_C_LIST(NC_G)
+#undef NC_G
+#undef NC_GW
+  return false;
+}
+
 // grid-kernel variant: NC_GRID_VARIANT="NT,TPT,UNROLL,STAGE,FAR,TMA,MINB" (default kGridVariantDefault); only the
 // combinations instantiated in launch_pairs_grid launch (others fall back to the default)
 static GridVariant grid_variant() {
@@ -257,9 +279,10 @@ static GridVariant grid_variant() {
       w.minb = 8;
       w.persist = kGridVariantDefault.persist;
       if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d", &w.nt, &w.tpt, &w.unroll, &w.stage, &w.far, &w.tma, &w.minb,
-                 &w.persist) >= 5 &&
-          (w.nt == 128 || w.nt == 256) && (w.tpt == 1 || w.tpt == 2) && (w.unroll == 1 || w.unroll == 2 || w.unroll == 4) &&
-          w.stage >= 32 && (w.far >= 0 && w.far <= 6) && (w.tma >= 0 && w.tma <= 2))
+                 &w.persist) >= 5 && grid_variant_instantiated(w) &&
+          ((w.tma == 3 && (w.nt == 4 || w.nt == 8)) || w.nt == 128 || w.nt == 256) && (w.tpt == 1 || w.tpt == 2) &&
+          (w.unroll == 1 || w.unroll == 2 || w.unroll == 4) && w.stage >= 32 && (w.far >= 0 && w.far <= 6) &&
+          (w.tma >= 0 && w.tma <= 3))
         v = w;
     }
   }
@@ -271,7 +294,113 @@ int grid_far_table_bits() { return grid_variant().far >= 2 ? far_table_bits(grid
 int grid_far_table_rcp() { return far_table_rcp(grid_variant().far); }
 void grid_far_poly(double* a2, double* a3) { far_poly(grid_variant().far, a2, a3); }
 
-int grid_unit_points() { return grid_variant().nt * grid_variant().tpt; }
+// points per work unit: a CTA's (NT x TPT), or a warp's (32 x TPT) for the warp-level kernel (tma = 3)
+int grid_unit_points() { return (grid_variant().tma == 3 ? 32 : grid_variant().nt) * grid_variant().tpt; }
+int grid_unit_tpt() { return grid_variant().tpt; }
+
+// ------------------------------------------------------------------------------------------------
+// Warp-level work units (variant tma = 3): every warp takes (<= 32 TPT points of one incoming grid) x (one slice of
+// its source list) units from the atomic counter on its own.  The unit's sources are copied global -> shared into
+// the warp's two chunk buffers with cp.async (chunks of `wrec` records, which may split a patch) while the previous
+// chunk is evaluated; after the CTA's one-time table load no CTA barrier is taken, so a CTA never holds idle warps
+// (a CTA-sized unit leaves the warps beyond the grid's last point waiting at every stage barrier).
+// ------------------------------------------------------------------------------------------------
+template <int KIND, int TPT, int UNROLL, int FAR, int WPC, int MINB>
+__global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit* __restrict__ units,
+                                                          const double* __restrict__ gx, const double* __restrict__ gy,
+                                                          const double* __restrict__ gz,
+                                                          const int32_t* __restrict__ srclist,
+                                                          const double* __restrict__ src4, int wrec,
+                                                          double* __restrict__ part, const double2* __restrict__ fsrc,
+                                                          int fn, int fbase, int* __restrict__ counter,
+                                                          int64_t nunits) {
+  static_assert(FAR >= 2 && far_table_rcp(FAR), "warp-level grid kernel: reciprocal-seeded far table only");
+  extern __shared__ double4 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double4* buf = sm + (size_t)warp * 2 * wrec;   // this warp's two chunk buffers
+  int32_t* slst = reinterpret_cast<int32_t*>(sm + (size_t)WPC * 2 * wrec) + warp * 32;
+  double2* ftab = reinterpret_cast<double2*>(reinterpret_cast<int32_t*>(sm + (size_t)WPC * 2 * wrec) + WPC * 32);
+  const int nvec = fn / 2;
+  const unsigned tb = smem_u32(ftab) - 8u * (unsigned)fbase;
+  const int flim = KIND == 1 ? fbase + fn - 1 : fbase;
+  const double2 cst = __ldg(fsrc + nvec);
+  const double fa2 = cst.x, fa3 = cst.y;
+  for (int j = threadIdx.x; j < nvec; j += 32 * WPC) ftab[j] = fsrc[j];
+  __syncthreads();
+  constexpr int upts = 32 * TPT;
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(counter, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= nunits) break;
+    const GridUnit U = units[u];
+    const bool single = TPT > 1 && U.npt <= 32;   // one point per lane
+    double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
+#pragma unroll
+    for (int t = 0; t < TPT; ++t) {
+      const int l = single ? lane : TPT * lane + t;
+      const int64_t g = U.pt0 + min(l, U.npt - 1);
+      x[t] = gx[g]; y[t] = gy[g]; z[t] = gz[g];
+      cq[t] = 0.5 * fma(x[t], x[t], fma(y[t], y[t], fma(z[t], z[t], 0.25)));
+      x[t] = -x[t]; y[t] = -y[t]; z[t] = -z[t];
+      acc[t] = 0.0;
+    }
+    if (lane < U.nsrc) slst[lane] = srclist[U.src0 + lane];
+    __syncwarp();
+    const double4* __restrict__ s4 = reinterpret_cast<const double4*>(src4 + U.soff);
+    const int p = U.p, ntot = U.nsrc * p, nch = (ntot + wrec - 1) / wrec;
+    auto issue = [&](int c) {
+      const int r0 = c * wrec, n = min(wrec, ntot - r0);
+      double2* dst = reinterpret_cast<double2*>(buf + (size_t)(c & 1) * wrec);
+      for (int t = lane; t < 2 * n; t += 32) {
+        const int rr = r0 + (t >> 1), q = rr / p, m = rr - q * p;
+        cp_async16(dst + t, reinterpret_cast<const double2*>(s4 + (size_t)slst[q] * p + m) + (t & 1));
+      }
+      cp_async_commit();
+    };
+    issue(0);
+    for (int c = 0; c < nch; ++c) {
+      if (c + 1 < nch) {
+        issue(c + 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, buf + (size_t)(c & 1) * wrec,
+                                              min(wrec, ntot - c * wrec), single, (const double2*)nullptr, tb, flim,
+                                              fa2, fa3);
+      __syncwarp();
+    }
+    if (single) {
+      if (lane < U.npt) part[(int64_t)u * upts + lane] = acc[0];
+    } else {
+#pragma unroll
+      for (int t = 0; t < TPT; ++t) {
+        const int l = TPT * lane + t;
+        if (l < U.npt) part[(int64_t)u * upts + l] = acc[t];
+      }
+    }
+  }
+}
+
+template <int KIND, int TPT, int UNROLL, int FAR, int WPC, int MINB>
+static void launch_grid_w(const GridUnit* units, int64_t nunits, const double* gx, const double* gy, const double* gz,
+                          const int32_t* srclist, const double* src4, int wrec, double* part, int* counter,
+                          const FarTable& ft, cudaStream_t s) {
+  const size_t smem = (size_t)WPC * 2 * wrec * sizeof(double4) + (size_t)WPC * 32 * sizeof(int32_t) +
+                      (size_t)(ft.n / 2) * sizeof(double2);
+  auto kern = k_pairs_grid_w<KIND, TPT, UNROLL, FAR, WPC, MINB>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * WPC, smem);
+  const int64_t ctas = std::min<int64_t>((int64_t)std::max(1, per) * sms, (nunits + WPC - 1) / WPC);
+  cudaMemsetAsync(counter, 0, sizeof(int), s);
+  kern<<<(unsigned)ctas, 32 * WPC, smem, s>>>(units, gx, gy, gz, srclist, src4, wrec, part, ft.d, ft.n, ft.base,
+                                              counter, nunits);
+}
 
 template <int KIND, int NT, int TPT, int UNROLL, int FAR, int TMA, int MINB>
 static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* gx, const double* gy, const double* gz,
@@ -308,30 +437,27 @@ void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const do
                        const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
                        int* counter, const FarTable& ft, cudaStream_t s) {
   if (nunits <= 0) return;
-  const GridVariant v = grid_variant();
-#define NC_G(KD, NT, TP, UR, FR, TM, MB)                                                                   \
-  if (kind == KD && v.nt == NT && v.tpt == TP && v.unroll == UR && v.far == FR && v.tma == TM && v.minb == MB) \
-    return launch_grid_t<KD, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, pmax, part, \
-                                                     v.persist, counter, ft, s);
-#define NC_GK(KD)                                                                                                 \
-  NC_G(KD, 128, 2, 4, 2, 0, 8) NC_G(KD, 128, 2, 4, 3, 0, 8) NC_G(KD, 128, 2, 4, 4, 0, 8) NC_G(KD, 128, 2, 4, 2, 0, 6) \
-  NC_G(KD, 128, 2, 4, 5, 2, 8) NC_G(KD, 128, 2, 4, 5, 2, 7) NC_G(KD, 128, 2, 4, 5, 2, 6) NC_G(KD, 128, 2, 2, 5, 2, 8) \
-  NC_G(KD, 128, 2, 4, 5, 0, 8) NC_G(KD, 128, 2, 4, 6, 0, 8) NC_G(KD, 128, 2, 4, 5, 0, 6) NC_G(KD, 128, 2, 4, 6, 0, 6) \
-  NC_G(KD, 128, 2, 2, 5, 0, 8) NC_G(KD, 256, 1, 4, 5, 0, 4) \
-  NC_G(KD, 128, 2, 4, 1, 0, 8) NC_G(KD, 128, 2, 4, 0, 0, 8) NC_G(KD, 128, 2, 4, 1, 1, 8) NC_G(KD, 128, 2, 4, 1, 0, 4) \
-  NC_G(KD, 128, 2, 4, 1, 0, 6) NC_G(KD, 256, 1, 4, 1, 0, 1) \
-  NC_G(KD, 256, 1, 4, 1, 0, 5) NC_G(KD, 256, 1, 4, 1, 0, 6) NC_G(KD, 256, 1, 2, 1, 0, 6) NC_G(KD, 256, 2, 2, 1, 0, 5) \
-  NC_G(KD, 256, 1, 4, 1, 1, 6)
-  NC_GK(0)
-  NC_GK(1)
-#undef NC_GK
+  const GridVariant v = grid_variant();   // always an instantiated combination (grid_variant checks)
+#define NC_GW(TP, UR, FR, WP, MB)                                                                                  \
+  if (v.tma == 3 && v.tpt == TP && v.unroll == UR && v.far == FR && v.nt == WP && v.minb == MB) {                 \
+    if (kind == 0)                                                                                                 \
+      return launch_grid_w<0, TP, UR, FR, WP, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, part, counter, \
+                                                  ft, s);                                                          \
+    return launch_grid_w<1, TP, UR, FR, WP, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, part, counter,   \
+                                                ft, s);                                                            \
+  }
+  NC_GRID_W_LIST(NC_GW)
+#undef NC_GW
+#define NC_G(NT, TP, UR, FR, TM, MB)                                                                              \
+  if (v.tma == TM && v.nt == NT && v.tpt == TP && v.unroll == UR && v.far == FR && v.minb == MB) {                \
+    if (kind == 0)                                                                                                 \
+      return launch_grid_t<0, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, pmax, part, \
+                                                      v.persist, counter, ft, s);                                  \
+    return launch_grid_t<1, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, pmax, part,   \
+                                                    v.persist, counter, ft, s);                                    \
+  }
+  NC_GRID_C_LIST(NC_G)
 #undef NC_G
-  const GridVariant d = kGridVariantDefault;   // combination not instantiated: the default
-  if (kind == 0)
-    return launch_grid_t<0, 128, 2, 4, 1, 0, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
-                                                    d.persist, counter, ft, s);
-  return launch_grid_t<1, 128, 2, 4, 1, 0, 8>(units, nunits, gx, gy, gz, srclist, src4, d.stage, pmax, part,
-                                                  d.persist, counter, ft, s);
 }
 
 // ------------------------------------------------------------------------------------------------

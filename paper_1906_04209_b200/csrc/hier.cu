@@ -38,7 +38,6 @@ constexpr int kSliceMax = 32;          // source patches per grid work unit
 constexpr int kMaxGrids = 4;           // incoming grids per group (source bands by distance; R24)
 constexpr int kDefaultGrids = 3;       // NC_MAX_GRIDS overrides (1..kMaxGrids)
 constexpr int kGridCutQuantiles = 48;  // candidate cut points of the multi-grid search
-constexpr int kGridThreadsForFill = 128;   // threads per grid-kernel CTA assumed by the warp-fill statistic
 constexpr double kBetaMin = 1.45;      // smallest source distance / circle radius served by a grid
 constexpr double kCostNear = 1.0, kCostInterp = 0.15, kCostTransform = 0.1;   // grid-vs-near cost model (grid-pair units)
 constexpr double kGridTolFactor = 1000.0;  // per-grid tolerance / requested precision (calibrated: DESIGN.md R21)
@@ -1340,7 +1339,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         units.push_back(u);
         H->slot_pairs += (double)H->upts * u.nsrc * u.p;
         {   // active-warp lane slots; a tail warp with <= 32 points runs one point per lane (direct.cu)
-          const int tpt = H->upts / kGridThreadsForFill, wpts = 32 * tpt;
+          const int tpt = grid_unit_tpt(), wpts = 32 * tpt;
           const int full = u.npt / wpts, rem = u.npt - full * wpts;
           const int tail = rem == 0 ? 0 : (tpt > 1 && rem <= 32 ? 32 : wpts);
           H->warp_slot_pairs += (double)(full * wpts + tail) * u.nsrc * u.p;

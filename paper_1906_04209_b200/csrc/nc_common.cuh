@@ -53,7 +53,7 @@ struct GridVariant {
   int nt, tpt, unroll, stage, far, tma, minb;   // minb: __launch_bounds__ min blocks per SM (register cap)
   int persist;                                  // 1: persistent CTAs taking units from an atomic counter
 };
-#define kGridVariantDefault (GridVariant{128, 2, 4, 256, 5, 0, 8, 1})
+#define kGridVariantDefault (GridVariant{8, 2, 4, 64, 5, 3, 3, 1})   // warp-level units (tma = 3)
 int grid_far_variant();
 int grid_far_table_bits();             // bits of the far table the grid-kernel variant in use needs (0: none)
 void grid_far_poly(double* a2, double* a3);   // its log1p polynomial constants (carried after the table)
@@ -66,7 +66,8 @@ struct FarTable {                      // exponent-indexed far log table (green.
 // exponent << bits), *n entries, followed by one extra entry (a2, a3); the caller owns *d (cudaFree).  0 on success.
 // rcp != 0: the entries are L alone (8 bytes, two per double2; n even) for c = rcp.approx(bin midpoint).
 int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a3, double2** d, int* n, int* base);
-int grid_unit_points();                // grid points per work unit = threads per CTA x targets per thread
+int grid_unit_points();                // grid points per work unit = (threads per CTA or warp) x targets per thread
+int grid_unit_tpt();                   // targets (grid points) per thread of the grid-kernel variant in use
 
 struct GridUnit {      // <= grid_unit_points() points of one incoming grid x one slice of its source-patch list
   int64_t pt0;         // first grid point (global grid-point index)
