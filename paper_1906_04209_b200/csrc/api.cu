@@ -125,7 +125,7 @@ static void compute_nseg(nc_handle* h) {
   if (tiles < 1) tiles = 1;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-  const int64_t W = (int64_t)sms * pairs_direct_blocks_per_sm(h->p, h->pair_tpt);
+  const int64_t W = (int64_t)sms * pairs_direct_blocks_per_sm(h->p, h->pair_tpt, h->xtab);
   const int64_t cap = std::min<int64_t>(h->N, 64);
   int best = 1;
   double best_cost = 1e30;
@@ -246,6 +246,15 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   cudaStream_t s = h->stream;
   const int K = h->K, Ks = h->Kstar, p = h->p;
   if (!log_table_device()) return bail(fail(NC_ECUDA, "nc_setup: log table upload failed"));
+  {   // exact-form log table of the direct / near-list pair kernels (green_exact_r; NC_EXACT_TABLE=0: mantissa table)
+    const char* e = getenv("NC_EXACT_TABLE");
+    if (!(e && e[0] == '0')) {
+      if (far_table_build(h->kind, h->eps, 7, 1, FarPoly<7, 4>::a2, FarPoly<7, 4>::a3, &h->d_xtab, &h->xtab.n,
+                          &h->xtab.base, 1))
+        return bail(fail(NC_ECUDA, "nc_setup: exact-form log table upload failed"));
+      h->xtab.d = h->d_xtab;
+    }
+  }
 
   // tables; outgoing-operator rungs (0 = base, 1.. = ladder, NC_HIER only)
   int rc;
@@ -433,7 +442,7 @@ static int matvec_tail(nc_handle* h, const double* x, double* y, cudaStream_t s)
   mark(h, 2, s);
   if (h->mode == NC_DIRECT) {
     launch_pairs_direct(h->kind, h->pair_tpt, h->d_tx, h->d_ty, h->d_tz, h->row_count * Ks, Ks, h->row_begin, h->d_src4, p, h->N,
-                        h->nseg, h->d_upart, s);
+                        h->nseg, h->d_upart, h->xtab, s);
     mark(h, 3, s);
     // K3: Y = X + (sum_seg U_seg) P^T
     launch_gemm_dmma(h->d_upart, Ks, h->nseg, h->row_count * Ks, h->d_P, h->row_count, K, Ks, y, K, 1, x, K, s);
@@ -725,8 +734,10 @@ int nc_stats(const nc_handle* h, nc_stats_t* o) {
   // 6 DADD interior;
   // far-field form (R23, green_far_h) 10 DFMA + 2 DMUL + 4 DADD exterior, 11 DFMA + 2 DMUL + 3 DADD interior
   const int interior = h->kind == NC_INTERIOR;
-  o->pair_fp64_inst_direct = 22;
-  o->pair_fp64_flops_direct = 33 + interior;
+  // exact form with the exact-form table (green_exact_r, default): 11 DFMA + 3 DMUL + 5 DADD exterior (30 flops),
+  // 12 + 3 + 4 interior (31)
+  o->pair_fp64_inst_direct = h->xtab.d ? 19 : 22;
+  o->pair_fp64_flops_direct = h->xtab.d ? 30 + interior : 33 + interior;
   // far table (R25, green_far_t) cubic: 10 DFMA + 1 DMUL + 2 DADD exterior (23 flops), 11 + 1 + 1 interior (24);
   // quartic: one DFMA more
   const int far = grid_far_variant();
@@ -768,6 +779,7 @@ void nc_destroy(nc_handle* h) {
   hier_destroy(h);
   double* bufs[] = {h->d_T, h->d_P, h->d_I, h->d_zhat, h->d_shat, h->d_centers, h->d_frames, h->d_tx, h->d_ty,
                     h->d_tz, h->d_src4, h->d_upart, h->d_V, h->d_red, h->d_b, h->d_hx, h->d_hy, h->d_Tcat, h->d_xall};
+  if (h->d_xtab) cudaFree(h->d_xtab);
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (h->d_colbase) cudaFree(h->d_colbase);

@@ -19,18 +19,26 @@
 
 namespace nc {
 
-template <int KIND, int TPT>
+// EX: the exact-form table (green_exact_r, 8-byte L entries after the stage buffer) instead of the 16-byte
+// (c_j, -log c_j) mantissa table
+template <int KIND, int TPT, bool EX>
 __global__ void __launch_bounds__(kPairThreads, 2) k_pairs_direct(const double* __restrict__ tx,
                                                                 const double* __restrict__ ty,
                                                                 const double* __restrict__ tz, int64_t n_tgt,
                                                                 int Kstar, int64_t tgt_patch0,
                                                                 const double* __restrict__ src4, int p, int64_t N,
                                                                 int nseg, int chp, double* __restrict__ upart,
-                                                                const double2* __restrict__ logsrc) {
+                                                                const double2* __restrict__ logsrc,
+                                                                const double2* __restrict__ xsrc, int xn, int xbase) {
   extern __shared__ double4 sm[];
-  __shared__ double2 logtab[kLogTableSize];
+  __shared__ double2 logtab[EX ? 1 : kLogTableSize];
   __shared__ int64_t pid[kStagePatchesMax];
-  init_log_table(logtab, logsrc);
+  ExactTab xt{};
+  if (EX)
+    xt = init_exact_table(KIND, reinterpret_cast<double2*>(sm + (size_t)chp * p), xsrc, xn, xbase);
+  else
+    init_log_table(logtab, logsrc);
+  auto green = [&](double q) { return EX ? green_exact_r<KIND>(q, xt.tb, xt.lim, xt.a2, xt.a3) : green_q<KIND>(q, logtab); };
   double x[TPT], y[TPT], z[TPT], acc[TPT];
   int64_t excl[TPT];
   const int64_t t0 = (int64_t)blockIdx.x * kPairThreads * TPT + threadIdx.x;
@@ -49,7 +57,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_pairs_direct(const double* 
                                    reinterpret_cast<const double4*>(src4), p, logtab);
   } else {
     accumulate_list<KIND, TPT>(x, y, z, excl, acc, j1 - j0, [=] __device__(int64_t k) { return j0 + k; },
-                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, true);
+                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, green, true);
   }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
@@ -60,31 +68,44 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_pairs_direct(const double* 
 
 static bool stage_ldg();
 
-int pairs_direct_blocks_per_sm(int p, int tpt) {
+static bool exact_table_on(const FarTable& xt) { return xt.d != nullptr && !stage_ldg(); }
+
+int pairs_direct_blocks_per_sm(int p, int tpt, const FarTable& xt) {
   int nb = 0;
+  const bool ex = exact_table_on(xt);
   size_t smem = stage_ldg() ? 0 : (size_t)stage_patches(p) * p * sizeof(double4);
-  if (tpt == 2)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pairs_direct<1, 2>, kPairThreads, smem);
+  if (ex) smem += (size_t)xt.n * sizeof(double);
+  if (ex)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tpt == 2 ? k_pairs_direct<1, 2, true> : k_pairs_direct<1, 1, true>,
+                                                  kPairThreads, smem);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_pairs_direct<1, 1>, kPairThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tpt == 2 ? k_pairs_direct<1, 2, false> : k_pairs_direct<1, 1, false>,
+                                                  kPairThreads, smem);
   return max(nb, 1);
 }
 
 void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, const double* tz, int64_t n_tgt,
                          int Kstar, int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
-                         cudaStream_t s) {
+                         const FarTable& xt, cudaStream_t s) {
   if (n_tgt <= 0) return;
   const int chp = stage_ldg() ? 0 : stage_patches(p);
-  const size_t smem = (size_t)chp * p * sizeof(double4);
+  const bool ex = exact_table_on(xt);
+  const size_t smem = (size_t)chp * p * sizeof(double4) + (ex ? (size_t)xt.n * sizeof(double) : 0);
   const int64_t per_block = (int64_t)kPairThreads * tpt;
   dim3 grid((unsigned)((n_tgt + per_block - 1) / per_block), (unsigned)nseg);
-#define NC_LAUNCH(KD, TP) \
-  k_pairs_direct<KD, TP><<<grid, kPairThreads, smem, s>>>(tx, ty, tz, n_tgt, Kstar, tgt_patch0, src4, p, N, nseg, chp, upart, \
-                                                          log_table_device())
+#define NC_LAUNCH(KD, TP, EX)                                                                                       \
+  {                                                                                                                \
+    auto kern = k_pairs_direct<KD, TP, EX>;                                                                        \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+    kern<<<grid, kPairThreads, smem, s>>>(tx, ty, tz, n_tgt, Kstar, tgt_patch0, src4, p, N, nseg, chp, upart,       \
+                                          log_table_device(), xt.d, xt.n, xt.base);                                \
+  }
   if (kind == NC_EXTERIOR) {
-    if (tpt == 2) NC_LAUNCH(1, 2); else NC_LAUNCH(1, 1);
+    if (ex) { if (tpt == 2) NC_LAUNCH(1, 2, true) else NC_LAUNCH(1, 1, true) }
+    else { if (tpt == 2) NC_LAUNCH(1, 2, false) else NC_LAUNCH(1, 1, false) }
   } else {
-    if (tpt == 2) NC_LAUNCH(0, 2); else NC_LAUNCH(0, 1);
+    if (ex) { if (tpt == 2) NC_LAUNCH(0, 2, true) else NC_LAUNCH(0, 1, true) }
+    else { if (tpt == 2) NC_LAUNCH(0, 2, false) else NC_LAUNCH(0, 1, false) }
   }
 #undef NC_LAUNCH
 }
@@ -463,7 +484,7 @@ void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const do
 // ------------------------------------------------------------------------------------------------
 // hierarchical mode: near-list sources evaluated directly at the target patch's Zernike nodes
 // ------------------------------------------------------------------------------------------------
-template <int KIND, int TPT>
+template <int KIND, int TPT, bool EX>
 __global__ void __launch_bounds__(kPairThreads) k_pairs_near(const double* __restrict__ tx,
                                                               const double* __restrict__ ty,
                                                               const double* __restrict__ tz, int Kstar,
@@ -472,11 +493,17 @@ __global__ void __launch_bounds__(kPairThreads) k_pairs_near(const double* __res
                                                               const int32_t* __restrict__ near,
                                                               const double* __restrict__ src4, int p, int chp,
                                                               double* __restrict__ udir,
-                                                              const double2* __restrict__ logsrc) {
+                                                              const double2* __restrict__ logsrc,
+                                                              const double2* __restrict__ xsrc, int xn, int xbase) {
   extern __shared__ double4 sm[];
-  __shared__ double2 logtab[kLogTableSize];
+  __shared__ double2 logtab[EX ? 1 : kLogTableSize];
   __shared__ int64_t pid[kStagePatchesMax];
-  init_log_table(logtab, logsrc);
+  ExactTab xt{};
+  if (EX)
+    xt = init_exact_table(KIND, reinterpret_cast<double2*>(sm + (size_t)chp * p), xsrc, xn, xbase);
+  else
+    init_log_table(logtab, logsrc);
+  auto green = [&](double q) { return EX ? green_exact_r<KIND>(q, xt.tb, xt.lim, xt.a2, xt.a3) : green_q<KIND>(q, logtab); };
   const int tiles = (Kstar + kPairThreads * TPT - 1) / (kPairThreads * TPT);
   const int64_t i = work[blockIdx.x / tiles];           // local target patch
   const int tile = blockIdx.x % tiles;
@@ -498,7 +525,7 @@ __global__ void __launch_bounds__(kPairThreads) k_pairs_near(const double* __res
                                    reinterpret_cast<const double4*>(src4), p, logtab);
   } else {
     accumulate_list<KIND, TPT>(x, y, z, excl, acc, o1 - o0, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
-                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, logtab, true);
+                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, green, true);
   }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
@@ -509,18 +536,26 @@ __global__ void __launch_bounds__(kPairThreads) k_pairs_near(const double* __res
 
 void launch_pairs_near(int kind, const double* tx, const double* ty, const double* tz, int Kstar, const int32_t* work,
                        int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
-                       double* udir, cudaStream_t s) {
+                       double* udir, const FarTable& xt, cudaStream_t s) {
   if (nwork <= 0) return;
   const int chp = stage_ldg() ? 0 : stage_patches(p);
-  const size_t smem = (size_t)chp * p * sizeof(double4);
+  const bool ex = exact_table_on(xt);
+  const size_t smem = (size_t)chp * p * sizeof(double4) + (ex ? (size_t)xt.n * sizeof(double) : 0);
   const int tiles = (Kstar + kPairThreads * 2 - 1) / (kPairThreads * 2);
   const unsigned nb = (unsigned)(nwork * tiles);
-  if (kind == NC_EXTERIOR)
-    k_pairs_near<1, 2><<<nb, kPairThreads, smem, s>>>(tx, ty, tz, Kstar, work, near_off, near, src4, p, chp, udir,
-                                                      log_table_device());
-  else
-    k_pairs_near<0, 2><<<nb, kPairThreads, smem, s>>>(tx, ty, tz, Kstar, work, near_off, near, src4, p, chp, udir,
-                                                      log_table_device());
+#define NC_LAUNCH(KD, EX)                                                                                           \
+  {                                                                                                                \
+    auto kern = k_pairs_near<KD, 2, EX>;                                                                           \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+    kern<<<nb, kPairThreads, smem, s>>>(tx, ty, tz, Kstar, work, near_off, near, src4, p, chp, udir,                \
+                                        log_table_device(), xt.d, xt.n, xt.base);                                  \
+  }
+  if (kind == NC_EXTERIOR) {
+    if (ex) NC_LAUNCH(1, true) else NC_LAUNCH(1, false)
+  } else {
+    if (ex) NC_LAUNCH(0, true) else NC_LAUNCH(0, false)
+  }
+#undef NC_LAUNCH
 }
 
 }  // namespace nc

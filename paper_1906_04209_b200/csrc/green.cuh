@@ -210,6 +210,48 @@ __device__ __forceinline__ double green_far_r(double qh, unsigned tbase, int lim
   return fma(-r, p, w - lj);
 }
 
+// Exact-form G with the reciprocal-seeded table (direct sums, near lists; R25): q = |z - s|^2 / 4 from
+// coordinate differences (caller), w = 2/d by fast_rsqrt (third-order Newton), x = 1 + w (exterior) or q (1 + w)
+// (interior, no ln 2: the table's L = -log c for this form), log x = L + log1p(r) with c = rcp.approx(bin midpoint),
+// r = x c - 1 and the quartic minimax log1p of FB = 7 (absolute error 6.3e-14): 20 FP64 instructions per pair with
+// the caller's distance and accumulate, and an 8-byte table read instead of the 16-byte (c_j, -log c_j) one.
+template <int KIND>
+__device__ __forceinline__ double green_exact_r(double q, unsigned tbase, int lim, double a2r, double a3r) {
+  const double w = fast_rsqrt(q);
+  const double x = (KIND == 1) ? 1.0 + w : fma(q, w, q);
+  const int hx = __double2hiint(x);
+  const double c = rcp_approx(far_mid<7>(hx));
+  int ix = hx >> 13;
+  ix = (KIND == 1) ? min(ix, lim) : max(ix, lim);
+  double lj;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(lj) : "r"(tbase + ((unsigned)ix << 3)));
+  const double r = fma(x, c, -1.0);
+  double p = fma(r, FarPoly<7, 4>::a4, a3r);
+  p = fma(r, p, a2r);
+  p = fma(r, p, 1.0);
+  return fma(-r, p, w - lj);
+}
+
+// the exact-form table as the kernels hold it: shared-memory base address (minus base * 8), clamp, constants
+struct ExactTab {
+  unsigned tb;
+  int lim;
+  double a2, a3;
+};
+// Call with all threads of the CTA (then __syncthreads()): copies the n L entries (n / 2 double2) into smem and
+// returns the kernel-side handle.  src[n / 2] holds (a2, a3).
+__device__ __forceinline__ ExactTab init_exact_table(int kind, double2* smem, const double2* __restrict__ src, int n,
+                                                     int base) {
+  for (int j = threadIdx.x; j < n / 2; j += blockDim.x) smem[j] = src[j];
+  const double2 cst = __ldg(src + n / 2);
+  ExactTab t;
+  t.tb = (unsigned)__cvta_generic_to_shared(smem) - 8u * (unsigned)base;
+  t.lim = kind == 1 ? base + n - 1 : base;
+  t.a2 = cst.x;
+  t.a3 = cst.y;
+  return t;
+}
+
 // reference-accuracy variant (libdevice), used by the self-check path
 template <int KIND>
 __device__ __forceinline__ double green_q_libdevice(double q) {

@@ -45,10 +45,12 @@ __global__ void k_far_rcp(int Elo, int bits, int cnt, double* c) {
 // within eps of it: DESIGN.md R22); the table covers d in [eps / 2, 2]: exterior x = 1 + 2/d in [2, 1 + 4/eps]
 // (plus the exponent below 2, reachable by rounding of w ~ 1), interior x = d^2/8 + d/4 in [eps^2/32 + eps/8, 1];
 // j = the top `bits` mantissa bits.  The kernel clamps the index on the open side (exterior above, interior below).
-int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a3, double2** d, int* n, int* base) {
-  const double dlo = 0.5 * eps;
-  const double xlo = kind == 1 ? 2.0 : dlo * dlo / 8.0 + dlo / 4.0;
-  const double xhi = kind == 1 ? 1.0 + 2.0 / dlo : 1.0;
+int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a3, double2** d, int* n, int* base,
+                    int exact) {
+  // exact form (green_exact_r): interior x = q (1 + w) = d^2/4 + d/2 in [eps^2/16 + eps/4, 2], L without ln 2
+  const double dlo = 0.5 * eps, sc = exact ? 2.0 : 1.0;
+  const double xlo = kind == 1 ? 2.0 : sc * (dlo * dlo / 8.0 + dlo / 4.0);
+  const double xhi = kind == 1 ? 1.0 + 2.0 / dlo : sc;
   int elo = 0, ehi = 0;
   frexp(xlo, &elo);   // x = f 2^e, f in [0.5, 1): biased exponent of x is e - 1 + 1023
   frexp(xhi, &ehi);
@@ -71,7 +73,7 @@ int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a
   std::vector<double2> host((size_t)nvec + 1);
   for (int t = 0; t < cnt; ++t) {
     long double L = -logl((long double)c[t]);
-    if (kind == 0) L += logl(2.0L);
+    if (kind == 0 && !exact) L += logl(2.0L);
     if (rcp)
       reinterpret_cast<double*>(host.data())[t] = (double)L;
     else

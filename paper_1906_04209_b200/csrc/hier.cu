@@ -1509,7 +1509,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   // near lists at the Zernike nodes
   NC_CUDA_TRY(cudaMemsetAsync(H->d_udir, 0, (size_t)rc * Ks * sizeof(double), s));
   launch_pairs_near(h->kind, H->d_tx, H->d_ty, H->d_tz, Ks, H->d_work_near, H->nwork_near, H->d_near_off, H->d_near,
-                    h->d_src4, h->p, H->d_udir, s);
+                    h->d_src4, h->p, H->d_udir, h->xtab, s);
   h->launches_last += H->nwork_near > 0;
   // step 4b: interpolation to the Zernike nodes, summed over levels
   if (rc > 0) {

@@ -65,7 +65,9 @@ struct FarTable {                      // exponent-indexed far log table (green.
 // host: build and upload the far table for (kind, eps, bits) (green_table.cu); *base = first index (biased
 // exponent << bits), *n entries, followed by one extra entry (a2, a3); the caller owns *d (cudaFree).  0 on success.
 // rcp != 0: the entries are L alone (8 bytes, two per double2; n even) for c = rcp.approx(bin midpoint).
-int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a3, double2** d, int* n, int* base);
+// exact != 0: the table of the exact form (green_exact_r: interior x = q (1 + w), L without ln 2).
+int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a3, double2** d, int* n, int* base,
+                    int exact = 0);
 int grid_unit_points();                // grid points per work unit = (threads per CTA or warp) x targets per thread
 int grid_unit_tpt();                   // targets (grid points) per thread of the grid-kernel variant in use
 
@@ -112,6 +114,8 @@ struct nc_handle {
   double* d_ty = nullptr;
   double* d_tz = nullptr;
   double* d_src4 = nullptr;       // per rung k: N * p_k records (x, y, z, rho), coordinates scaled by 1/2
+  nc::FarTable xtab;              // exact-form log table of the direct / near-list kernels (green_exact_r)
+  double2* d_xtab = nullptr;
   // outgoing-operator rungs: 0 = base (T, shat, p); 1.. = per-level ladder
   int nrung = 1;
   std::vector<double> rung_r;     // inner radius (arc length) of validity
@@ -187,16 +191,16 @@ void launch_gemm_dmma_colmap(const double* A, int64_t lda, const double* Bt, int
 // sum_m G(target t, s_jm) rho_jm
 void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, const double* tz, int64_t n_tgt,
                          int Kstar, int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
-                         cudaStream_t s);
+                         const FarTable& xt, cudaStream_t s);
 
-int pairs_direct_blocks_per_sm(int p, int tpt);
+int pairs_direct_blocks_per_sm(int p, int tpt, const FarTable& xt);
 void split_rows(const double* w, int64_t N, int world, int64_t* begin, int64_t* count);
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
                        const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
                        int* counter /* device int, persistent variant */, const FarTable& ft, cudaStream_t s);
 void launch_pairs_near(int kind, const double* tx, const double* ty, const double* tz, int Kstar, const int32_t* work,
                        int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
-                       double* udir, cudaStream_t s);
+                       double* udir, const FarTable& xt, cudaStream_t s);
 
 // BLAS-1 style helpers for GMRES (deterministic two-stage reductions)
 int64_t multidot_partials(int64_t n);

@@ -25,12 +25,13 @@ __host__ __device__ inline int stage_patches(int p) {
 // patch_at(k) -> patch index of the k-th list entry.  All threads of the CTA must call (barriers inside).
 // UNROLL: source records in flight per target (independent FP64 chains = TPT x UNROLL); Tab: double2 (c_j, -log c_j)
 // (c_j, -log c_j).
-template <int KIND, int TPT, int UNROLL = 2, class Tab = double2, class PatchAt>
+// green(q) evaluates G from q = |z - s|^2 / 4 (green_q with the mantissa table, or green_exact_r)
+template <int KIND, int TPT, int UNROLL = 2, class GreenQ, class PatchAt>
 __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
                                                 const int64_t (&excl)[TPT], double (&acc)[TPT], int64_t nlist,
                                                 PatchAt patch_at, const double4* __restrict__ s4, int p,
                                                 double4* __restrict__ sm, int64_t* __restrict__ sm_pid, int chp,
-                                                const Tab* __restrict__ logtab, bool active) {
+                                                GreenQ green, bool active) {
   for (int64_t c0 = 0; c0 < nlist; c0 += chp) {
     const int nch = (int)min((int64_t)chp, nlist - c0);
     __syncthreads();
@@ -60,7 +61,7 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
           for (int u = 0; u < TPT; ++u) {
             const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
             const double qd = fma(dz, dz, fma(dy, dy, dx * dx));   // |z - s|^2 / 4 (scaled coordinates)
-            acc[u] = fma(s.w, green_q<KIND>(qd, logtab), acc[u]);
+            acc[u] = fma(s.w, green(qd), acc[u]);
           }
         }
       } else {
@@ -71,7 +72,7 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
             const double4 s = sp[m];
             const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
             const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
-            acc[u] = fma(s.w, green_q<KIND>(qd, logtab), acc[u]);
+            acc[u] = fma(s.w, green(qd), acc[u]);
           }
         }
       }
