@@ -339,8 +339,8 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "tools"))
             from sass_loop import main_loop
             import paper_1906_04209_b200 as ncmod
-            pat = (f"k_pairs_gridILi{cfg.kind}ELi128ELi2ELi4ELb1" if args.mode == "hier"
-                   else f"k_pairs_directILi{cfg.kind}ELi2")
+            pat = (f"k_pairs_grid_wILi{cfg.kind}ELi2ELi4ELi5ELi8ELi3E" if args.mode == "hier"   # the default variant
+                   else f"k_pairs_directILi{cfg.kind}ELi2ELb1E")
             ml = main_loop(ncmod.nc.LIB_PATH, pat)
             clk_hz = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
             if ml:
@@ -354,6 +354,30 @@ def main():
                                                "main loop of this build, 592 SMSPs at the sampled SM clock"}
         except Exception as e:  # pragma: no cover
             roof["issue_model"] = {"error": str(e)[:200]}
+    # NEXT-3: the off-surface field of the solution (nc_field, host points in / values out, synchronous) at 4096
+    # points on a sphere inside (interior: radius 0.5) or outside (exterior: radius 2) the unit sphere
+    field = None
+    if world == 1:
+        n_f = 4096
+        k = np.arange(n_f) + 0.5
+        zf = 1.0 - 2.0 * k / n_f
+        phi = np.pi * (1.0 + 5.0 ** 0.5) * k
+        rf = 0.5 if cfg.kind == 0 else 2.0
+        pts = rf * np.stack([np.sqrt(1 - zf * zf) * np.cos(phi), np.sqrt(1 - zf * zf) * np.sin(phi), zf], 1)
+        xf = xs if solve is not None else x
+        h.field(xf, pts[:8])   # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        vf, _ = h.field(xf, pts)
+        tf = time.perf_counter() - t0
+        fpairs = float(n_f) * cfg.N * tab.p
+        field = {"points": n_f, "radius": rf, "pairs": fpairs, "ms": tf * 1e3, "pairs_per_s": fpairs / tf,
+                 "mean_value": float(np.mean(vf)),
+                 "note": "nc_field end to end (H2D points, base-rung rho, k_field, D2H values); pairs = points x N x p"}
+        if solve is not None and cfg.kind == 0 and args.tables == "physical":
+            v0, _ = h.field(xf, np.zeros((1, 3)))
+            field["v_origin"] = float(v0[0])
+            field["mfpt_origin"] = float((1.0 - v0[0]) / (3.0 * solve["I_sigma"]) + 1.0 / 6.0)   # eq:vtilde, D = -I_sigma
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -379,7 +403,7 @@ def main():
                                          "hier_interp_terms", "hier_grid_points", "hier_grid_units", "hier_grid_fill",
                                          "hier_grid_warp_fill")}
                      if args.mode == "hier" else None),
-            "solve": solve}
+            "solve": solve, "field": field}
     print(json.dumps(line), flush=True)
     h.close()
     if world > 1:

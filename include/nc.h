@@ -172,6 +172,22 @@ int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x
  * Errors: NC_ESTATE when the interior I_sigma <= 0 (the Lemma of PAPER.md:579-590 needs I_sigma != 0). */
 int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* value);
 
+/* Off-surface field of the solution (NEXT-3): the single-layer potential
+ *   interior  v(p) = int G_I(p, x') sigma dS   (eq:intBVPansatz; the MFPT is
+ *             vbar = (v - 1) / (3 D) + (1 - |p|^2) / 6 with D = -I_sigma, eq:vtilde PAPER.md:533-536)
+ *   exterior  u(p) = int G_E(p, x') sigma dS   (eq:urep)
+ * with the off-surface Green's functions eq:Gintoffsurface / eq:Gextoffsurface and each
+ * patch's density in its compressed outgoing representation (skeleton nodes, rho_j = T fhat_j, eq:outgoingcompressed).
+ *   x_all  device, N x K: the coefficients of ALL patches, internal order (world 1: the nc_gmres solution)
+ *   pts    host, n_pts x 3 (row-major); interior: every |p| < 1, exterior: every |p| > 1
+ *   out    host, n_pts: the potential at each point
+ *   dmin   host, n_pts or NULL: the distance from each point to the nearest skeleton node
+ * The compressed representation is valid only away from the patches: every point must be at least 3 eps from every
+ * skeleton node (the skeleton is certified >= 2 eps from a patch centre; R27).  Uses the handle's stream
+ * and synchronizes.  Errors: NC_EINVAL (null argument, a point on the wrong side of the sphere or closer than
+ * 3 eps to a skeleton node: out and dmin are still written), NC_ENOMEM, NC_ECUDA. */
+int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts, double* out, double* dmin);
+
 /* Counters and the last matvec's per-stage device times.  nc_time_stages(h, 1) makes the next
  * matvecs record per-stage CUDA events on the matvec's stream (no host synchronisation inside nc_matvec);
  * nc_stats waits for the last recorded matvec's events and converts them to ms_last. */

@@ -60,6 +60,10 @@ def lib():
         L.oracle_green_batch.argtypes = [ctypes.c_int, ctypes.c_int64, dp, dp, dp]
         L.oracle_green_batch.restype = None
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_offsurface.argtypes = [ctypes.c_int, ctypes.c_int64, dp, ctypes.c_int64, dp, dp, dp, dp, dp]
+        L.oracle_offsurface.restype = None
+        L.oracle_green_off_batch.argtypes = [ctypes.c_int, ctypes.c_int64, dp, dp, dp]
+        L.oracle_green_off_batch.restype = None
         _lib = L
     return _lib
 
@@ -84,6 +88,15 @@ def green(kind: int, x: np.ndarray, y: np.ndarray) -> np.ndarray:
     y = np.ascontiguousarray(np.broadcast_to(y, np.broadcast(x, y).shape), dtype=np.float64).reshape(-1, 3)
     g = np.empty(len(x))
     lib().oracle_green_batch(int(kind), len(x), _dp(x), _dp(y), _dp(g))
+    return g
+
+
+def green_off(kind: int, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Off-surface G(x, x') for |x'| = 1 (eq:Gintoffsurface / eq:Gextoffsurface)."""
+    x = np.ascontiguousarray(np.broadcast_to(x, np.broadcast(x, y).shape), dtype=np.float64).reshape(-1, 3)
+    y = np.ascontiguousarray(np.broadcast_to(y, np.broadcast(x, y).shape), dtype=np.float64).reshape(-1, 3)
+    g = np.empty(len(x))
+    lib().oracle_green_off_batch(int(kind), len(x), _dp(x), _dp(y), _dp(g))
     return g
 
 
@@ -127,6 +140,30 @@ def field(kind, tgt, tpatch, src, spatch, rho):
     lib().oracle_field(int(kind), len(tgt), _dp(tgt), _ip(tpatch), len(src), _dp(src), _ip(spatch), _dp(rho),
                        _dp(u))
     return u
+
+
+def offsurface(kind, centers, tab, x, pts, with_absum=False):
+    """NEXT-3: the single-layer potential of the solution at off-surface points,
+    v(p) = int G_I(p, x') sigma dS (interior, eq:intBVPansatz) or u(p) = int G_E(p, x') sigma dS (exterior,
+    eq:urep), each patch's density in its compressed outgoing representation (eq:outgoingcompressed:
+    skeleton nodes s_jm = R_j shat_m, charges rho_j = T fhat_j).  Returns (values, min distance to a skeleton node)
+    per point.  ``with_absum``: also return sum |G rho| per point (the conditioning scale of the sum)."""
+    N = len(centers)
+    x = np.asarray(x, dtype=np.float64).reshape(N, -1)
+    s = global_nodes(frames(centers), tab.shat).reshape(-1, 3)
+    rho = outgoing(tab.T, x).reshape(-1)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    out, dmin, absum = np.empty(len(pts)), np.empty(len(pts)), np.empty(len(pts))
+    lib().oracle_offsurface(int(kind), len(pts), _dp(pts), len(s), _dp(np.ascontiguousarray(s)),
+                            _dp(np.ascontiguousarray(rho)), _dp(out), _dp(dmin), _dp(absum))
+    return (out, dmin, absum) if with_absum else (out, dmin)
+
+
+def mfpt_field(v, pts, I_sigma):
+    """Interior MFPT at a point from the potential v (eq:vtilde, with D = -I_sigma from the lemma
+    at PAPER.md:556-566): vbar = (v - 1) / (3 D) + (1 - |x|^2) / 6."""
+    r2 = np.sum(np.asarray(pts, dtype=np.float64).reshape(-1, 3) ** 2, axis=1)
+    return (np.asarray(v) - 1.0) / (3.0 * (-I_sigma)) + (1.0 - r2) / 6.0
 
 
 def matvec(kind, centers, tab, x, rows=None, R=None):

@@ -62,6 +62,58 @@ void oracle_field(int kind, int64_t nt, const double* tx, const int64_t* tpatch,
   }
 }
 
+/*
+ * Off-surface Neumann Green's functions (x anywhere, x' on the unit sphere), the paper's literal forms:
+ *   interior, eq:Gintoffsurface:  G_I = 2/|x-x'| + log( 2 / (1 - x.x' + |x-x'|) )
+ *   exterior, eq:Gextoffsurface:  G_E = 2/|x-x'| + log( (|x| - x.x') / (1 - x.x' + |x-x'|) )
+ */
+/* Evaluated literally, in long double (x87 80-bit): for an exterior point nearly on the ray through x', both
+ * |x| - x.x' and 1 - x.x' + |x-x'| cancel catastrophically (each ~ |x| theta^2 / 2 for the angle theta between x
+ * and x'); the 11 extra mantissa bits keep the literal form accurate to ~1e-15 relative at the angles a test
+ * layout produces (theta >~ 1e-3), so the oracle needs no algebraic rewriting. */
+double oracle_green_off(int kind, const double* x, const double* yin) {
+  /* the formulas hold for x' on the sphere: the node (a unit vector only to ~4e-16 in fp64) is projected onto it
+   * in long double first; without that, |x'| - 1 = delta enters the literal ratio as ~delta / theta^2 */
+  long double yn = sqrtl((long double)yin[0] * yin[0] + (long double)yin[1] * yin[1] + (long double)yin[2] * yin[2]);
+  long double y[3] = {yin[0] / yn, yin[1] / yn, yin[2] / yn};
+  long double dx = (long double)x[0] - y[0], dy = (long double)x[1] - y[1], dz = (long double)x[2] - y[2];
+  long double d = sqrtl(dx * dx + dy * dy + dz * dz);
+  long double xy = (long double)x[0] * y[0] + (long double)x[1] * y[1] + (long double)x[2] * y[2];
+  if (kind == 0) return (double)(2.0L / d + logl(2.0L / (1.0L - xy + d)));
+  long double nx = sqrtl((long double)x[0] * x[0] + (long double)x[1] * x[1] + (long double)x[2] * x[2]);
+  return (double)(2.0L / d + logl((nx - xy) / (1.0L - xy + d)));
+}
+
+/*
+ * The single-layer potential of the compressed densities at off-surface points (NEXT-3, SURVEY.md §8(f);
+ * eq:intBVPansatz PAPER.md:556-558 for the interior v, eq:urep PAPER.md:466-468 for the exterior u):
+ *     out_t = sum_s G_off(p_t, y_s) rho_s ,      dmin_t = min_s |p_t - y_s|
+ * over ALL sources (a target belongs to no patch).  Neumaier-compensated.
+ */
+void oracle_offsurface(int kind, int64_t nt, const double* px, int64_t ns, const double* sx, const double* rho,
+                       double* out, double* dmin, double* absum) {
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t t = 0; t < nt; ++t) {
+    double sum = 0.0, comp = 0.0, dm = INFINITY, as = 0.0;
+    for (int64_t s = 0; s < ns; ++s) {
+      const double* y = sx + 3 * s;
+      double dx = px[3 * t] - y[0], dy = px[3 * t + 1] - y[1], dz = px[3 * t + 2] - y[2];
+      double d = sqrt(dx * dx + dy * dy + dz * dz);
+      if (d < dm) dm = d;
+      double term = oracle_green_off(kind, px + 3 * t, y) * rho[s];
+      neumaier_add(&sum, &comp, term);
+      as += fabs(term);
+    }
+    out[t] = sum + comp;
+    dmin[t] = dm;
+    absum[t] = as; /* sum of |terms|: the scale of the sum's conditioning (parity bound for mixed-sign charges) */
+  }
+}
+
+void oracle_green_off_batch(int kind, int64_t n, const double* x, const double* y, double* g) {
+  for (int64_t i = 0; i < n; ++i) g[i] = oracle_green_off(kind, x + 3 * i, y + 3 * i);
+}
+
 /* Batched Green's function values (for the kernel pins in tests/test_oracle.py). */
 void oracle_green_batch(int kind, int64_t n, const double* x, const double* y, double* g) {
   for (int64_t i = 0; i < n; ++i) g[i] = oracle_green(kind, x + 3 * i, y + 3 * i);

@@ -704,6 +704,58 @@ int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* valu
   return NC_OK;
 }
 
+int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts, double* out, double* dmin) {
+  if (!h || !x_all || n_pts < 0 || (n_pts > 0 && (!pts || !out))) return fail(NC_EINVAL, "nc_field: bad argument");
+  if (n_pts == 0) return NC_OK;
+  for (int64_t t = 0; t < n_pts; ++t) {   // the problem's side of the sphere (interior: inside, exterior: outside)
+    const double r = std::sqrt(pts[3 * t] * pts[3 * t] + pts[3 * t + 1] * pts[3 * t + 1] + pts[3 * t + 2] * pts[3 * t + 2]);
+    if (!(h->kind == NC_EXTERIOR ? r > 1.0 : r < 1.0))
+      return fail(NC_EINVAL, "nc_field: point " + std::to_string(t) + " is not on the " +
+                                 (h->kind == NC_EXTERIOR ? "exterior" : "interior") + " side of the unit sphere");
+  }
+  NC_CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t s = h->stream;
+  const int K = h->K, p0 = h->rung_p[0];
+  // rho of the base rung for all N patches (K1 restricted to rung 0)
+  launch_gemm_dmma(x_all, K, 1, 0, h->d_T + (size_t)h->rung_trow[0] * K, h->N, p0, K,
+                   h->d_src4 + h->rung_soff[0] + 3, (int64_t)p0 * 4, 4, nullptr, 0, s);
+  const int64_t nrec = h->N * p0;
+  const int nseg = field_segments(n_pts, nrec);
+  double *d_pts = nullptr, *d_part = nullptr, *d_out = nullptr;
+  cudaError_t e = cudaMalloc(&d_pts, (size_t)n_pts * 3 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_part, (size_t)2 * nseg * n_pts * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, (size_t)2 * n_pts * sizeof(double));
+  int rc = NC_OK;
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    rc = fail(NC_ENOMEM, "nc_field: device allocation failed");
+  } else {
+    e = cudaMemcpyAsync(d_pts, pts, (size_t)n_pts * 3 * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+      launch_field(h->kind, d_pts, n_pts, h->d_src4 + h->rung_soff[0], nrec, nseg, d_part, d_part + (size_t)nseg * n_pts,
+                   d_out, d_out + n_pts, s);
+      e = cudaGetLastError();
+    }
+    std::vector<double> dm(n_pts);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_out, (size_t)n_pts * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dm.data(), d_out + n_pts, (size_t)n_pts * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "nc_field");
+    } else {
+      if (dmin) std::copy(dm.begin(), dm.end(), dmin);
+      for (int64_t t = 0; t < n_pts && rc == NC_OK; ++t)
+        if (!(dm[t] >= 3.0 * h->eps))
+          rc = fail(NC_EINVAL, "nc_field: point " + std::to_string(t) + " is " + std::to_string(dm[t] / h->eps) +
+                                   " eps from a skeleton node (< 3 eps: the compressed representation is not valid)");
+    }
+  }
+  cudaFree(d_pts);
+  cudaFree(d_part);
+  cudaFree(d_out);
+  return rc;
+}
+
 int nc_stats(const nc_handle* h, nc_stats_t* o) {
   if (!h || !o) return fail(NC_EINVAL, "nc_stats: null argument");
   NC_TRY(read_stages(const_cast<nc_handle*>(h)));

@@ -202,6 +202,12 @@ void launch_pairs_near(int kind, const double* tx, const double* ty, const doubl
                        int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
                        double* udir, const FarTable& xt, cudaStream_t s);
 
+// off-surface field (field.cu, NEXT-3): out[t] = sum over all source records of G_off(pts_t, s) rho_s, dmin[t] =
+// min |pts_t - s|; part / dpart: nseg x n scratch
+int field_segments(int64_t n, int64_t nrec);
+void launch_field(int kind, const double* pts, int64_t n, const double* src4, int64_t nrec, int nseg, double* part,
+                  double* dpart, double* out, double* dmin, cudaStream_t s);
+
 // BLAS-1 style helpers for GMRES (deterministic two-stage reductions)
 int64_t multidot_partials(int64_t n);
 void launch_multidot(const double* V, int64_t ldv, int nv, const double* w, int64_t n, double* part, double* out,

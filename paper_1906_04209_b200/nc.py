@@ -57,7 +57,8 @@ class NcStats(ctypes.Structure):
                 ("hier_grid_fill", ctypes.c_double), ("hier_grid_warp_fill", ctypes.c_double)]
 
 
-EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt", "nc_stats",
+EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt",
+           "nc_field", "nc_stats",
            "nc_time_stages", "nc_tree_lists", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
 
 _lib = None
@@ -80,6 +81,7 @@ def load_library(path: str = LIB_PATH):
     L.nc_matvec_host.argtypes = [vp, _dp, _dp]
     L.nc_gmres.argtypes = [vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int), _dp, vp]
     L.nc_flux_or_mfpt.argtypes = [vp, vp, _dp, _dp]
+    L.nc_field.argtypes = [vp, vp, ctypes.c_int64, _dp, _dp, _dp]
     L.nc_stats.argtypes = [vp, ctypes.POINTER(NcStats)]
     L.nc_time_stages.argtypes = [vp, ctypes.c_int]
     L.nc_tree_lists.argtypes = [vp, _i64p, _i64p, _i64p, _i64p, _i64p]
@@ -220,6 +222,16 @@ class Handle:
         Is, v = ctypes.c_double(), ctypes.c_double()
         _check(self._L.nc_flux_or_mfpt(self._h, _ptr(x), ctypes.byref(Is), ctypes.byref(v)))
         return Is.value, v.value
+
+    def field(self, x_all, pts):
+        """Off-surface potential of the solution at host points ``pts`` (n x 3): v (interior) or u (exterior), and
+        each point's distance to the nearest skeleton node (nc_field; ``x_all`` = all patches' coefficients on
+        the device, internal order)."""
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        out, dmin = np.empty(len(pts)), np.empty(len(pts))
+        _check(self._L.nc_field(self._h, _ptr(x_all), len(pts), pts.ctypes.data_as(_dp), out.ctypes.data_as(_dp),
+                                dmin.ctypes.data_as(_dp)))
+        return out, dmin
 
     def time_stages(self, enable=True):
         _check(self._L.nc_time_stages(self._h, int(enable)))
