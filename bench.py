@@ -378,6 +378,18 @@ def main():
             v0, _ = h.field(xf, np.zeros((1, 3)))
             field["v_origin"] = float(v0[0])
             field["mfpt_origin"] = float((1.0 - v0[0]) / (3.0 * solve["I_sigma"]) + 1.0 / 6.0)   # eq:vtilde, D = -I_sigma
+    # NEXT-4: the paper's accuracy metric eq:l2res (relative L2 residual of the multiple-scattering system on a
+    # patch, on the tables' independent residual grid) for 16 seeded random patches of the solved system
+    residual = None
+    if world == 1 and solve is not None and getattr(tab, "res_S", None) is not None:
+        pats = np.random.default_rng(77).choice(cfg.N, min(16, cfg.N), replace=False)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rv, _ = h.residual(xs, pats, tab)
+        residual = {"patches": int(len(pats)), "max": float(np.max(rv)), "median": float(np.median(rv)),
+                    "ms": (time.perf_counter() - t0) * 1e3, "grid_points": int(tab.res_w.size),
+                    "note": "eq:l2res on 16 seeded random patches (nc_residual); the one-patch tables' own residual "
+                            "(eq:patcherrl2) at this eps bounds it from below"}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -403,7 +415,7 @@ def main():
                                          "hier_interp_terms", "hier_grid_points", "hier_grid_units", "hier_grid_fill",
                                          "hier_grid_warp_fill")}
                      if args.mode == "hier" else None),
-            "solve": solve, "field": field}
+            "solve": solve, "field": field, "residual": residual}
     print(json.dumps(line), flush=True)
     h.close()
     if world > 1:

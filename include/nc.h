@@ -188,6 +188,21 @@ int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* valu
  * 3 eps to a skeleton node: out and dmin are still written), NC_ENOMEM, NC_ECUDA. */
 int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts, double* out, double* dmin);
 
+/* L2 residual diagnostic (NEXT-4): the paper's accuracy metric eq:l2res,
+ *   res_i = || S sigma_i + sum_{j != i} S_ij sigma_j - 1 ||_{L2(Gamma_i)} / |Gamma_i|
+ * for n_sel listed patches, by quadrature on a residual grid that is independent of the solve's grids
+ * (PAPER.md:1720-1724): S sigma_i = res_S fhat_i (the self-patch potential of the basis solutions, a per-eps table
+ * built by nc_tables/residual.py), the other patches through their compressed outgoing representation.
+ *   x_all     device, N x K: the coefficients of ALL patches, internal order (world 1: the nc_gmres solution)
+ *   patches   host, n_sel caller patch indices (0 <= index < N)
+ *   res_rhat  host, n_res x 3: the residual grid in the canonical frame (patch centre +z, theta = 0 along +x)
+ *   res_w     host, n_res: quadrature weights of int_Gamma f dS (their sum is |Gamma|)
+ *   res_S     host, n_res x K row-major
+ *   res       host, n_sel (output);  pointwise  host, n_sel x n_res or NULL (output: the residual at each point)
+ * Uses the handle's stream and synchronizes.  Errors: NC_EINVAL (bad argument or index), NC_ENOMEM, NC_ECUDA. */
+int nc_residual(nc_handle* h, const double* x_all, int n_sel, const int64_t* patches, int n_res,
+                const double* res_rhat, const double* res_w, const double* res_S, double* res, double* pointwise);
+
 /* Counters and the last matvec's per-stage device times.  nc_time_stages(h, 1) makes the next
  * matvecs record per-stage CUDA events on the matvec's stream (no host synchronisation inside nc_matvec);
  * nc_stats waits for the last recorded matvec's events and converts them to ms_last. */

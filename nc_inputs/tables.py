@@ -44,6 +44,12 @@ class PatchTables:
     ladder_p: np.ndarray | None = None
     ladder_shat: np.ndarray | None = None
     ladder_T: np.ndarray | None = None
+    # optional residual-grid table for the L2 residual diagnostic (NEXT-4; nc_tables/residual.py):
+    #   res_rhat (n_res, 3) residual grid (canonical frame), res_w (n_res,) weights of int_Gamma f dS,
+    #   res_S (n_res, K) self-patch potential of each basis solution at the grid
+    res_rhat: np.ndarray | None = None
+    res_w: np.ndarray | None = None
+    res_S: np.ndarray | None = None
 
     @property
     def K(self) -> int:
@@ -65,6 +71,9 @@ class PatchTables:
         assert self.zhat.shape == (self.Kstar, 3) and self.shat.shape == (self.p, 3)
         for a in (self.zhat, self.shat):
             assert np.allclose(np.linalg.norm(a, axis=1), 1.0, atol=1e-13)
+        if self.res_S is not None:
+            assert self.res_rhat.shape == (self.res_S.shape[0], 3) and self.res_w.shape == (self.res_S.shape[0],)
+            assert self.res_S.shape[1] == K
         if self.ladder_r is not None:
             n = int(np.sum(self.ladder_p))
             assert self.ladder_shat.shape == (n, 3) and self.ladder_T.shape == (n, K)
@@ -79,11 +88,15 @@ class PatchTables:
         return float(m.group(1)) if m else 0.0
 
     def without_ladder(self):
-        return PatchTables(self.kind, self.eps, self.M, self.zhat, self.P, self.shat, self.T, self.I, self.meta)
+        return PatchTables(self.kind, self.eps, self.M, self.zhat, self.P, self.shat, self.T, self.I, self.meta,
+                           res_rhat=self.res_rhat, res_w=self.res_w, res_S=self.res_S)
+
+
+_OPTIONAL = ("ladder_r", "ladder_p", "ladder_shat", "ladder_T", "res_rhat", "res_w", "res_S")
 
 
 def save_tables(path, t: PatchTables):
-    extra = {k: getattr(t, k) for k in ("ladder_r", "ladder_p", "ladder_shat", "ladder_T") if getattr(t, k) is not None}
+    extra = {k: getattr(t, k) for k in _OPTIONAL if getattr(t, k) is not None}
     np.savez(path, version=TABLE_VERSION, kind=t.kind, eps=t.eps, M=t.M, zhat=t.zhat, P=t.P,
              shat=t.shat, T=t.T, I=t.I, meta=np.array(repr(t.meta)), **extra)
 
@@ -91,7 +104,7 @@ def save_tables(path, t: PatchTables):
 def load_tables(path) -> PatchTables:
     z = np.load(path, allow_pickle=False)
     assert int(z["version"]) == TABLE_VERSION, "table file version mismatch"
-    lad = {k: np.ascontiguousarray(z[k]) for k in ("ladder_r", "ladder_p", "ladder_shat", "ladder_T") if k in z.files}
+    lad = {k: np.ascontiguousarray(z[k]) for k in _OPTIONAL if k in z.files}
     return PatchTables(kind=int(z["kind"]), eps=float(z["eps"]), M=int(z["M"]),
                        zhat=np.ascontiguousarray(z["zhat"]), P=np.ascontiguousarray(z["P"]),
                        shat=np.ascontiguousarray(z["shat"]), T=np.ascontiguousarray(z["T"]),
@@ -134,3 +147,17 @@ def synthetic_tables(kind: int, eps: float, seed: int, M: int = 15, p: int = 120
     I = rng.standard_normal(K) * eps
     return PatchTables(kind=kind, eps=eps, M=M, zhat=zhat, P=P, shat=shat, T=T, I=I,
                        meta={"synthetic": True, "seed": seed, "coupling": coupling}).validate()
+
+
+def synthetic_residual(tab: PatchTables, seed: int, n_r: int = 24, n_theta: int = 33) -> PatchTables:
+    """Attach a parity-only residual table to ``tab``: the residual grid geometry (Gauss-Legendre radii x offset
+    equispaced angles), its quadrature weights, and a random self-potential matrix."""
+    rng = np.random.default_rng(seed)
+    x, w = np.polynomial.legendre.leggauss(n_r)
+    t = 0.5 * tab.eps * (x + 1.0)
+    th = 2.0 * np.pi * (np.arange(n_theta) + 0.5) / n_theta
+    T, TH = np.meshgrid(t, th, indexing="ij")
+    tab.res_rhat = patch_point(T.ravel(), TH.ravel())
+    tab.res_w = ((0.5 * tab.eps * w * np.sin(t))[:, None] * np.full(n_theta, 2.0 * np.pi / n_theta)[None, :]).ravel()
+    tab.res_S = rng.standard_normal((n_r * n_theta, tab.K)) / np.sqrt(tab.K)
+    return tab.validate()

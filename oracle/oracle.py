@@ -159,6 +159,30 @@ def offsurface(kind, centers, tab, x, pts, with_absum=False):
     return (out, dmin, absum) if with_absum else (out, dmin)
 
 
+def residual(kind, centers, tab, x, patches):
+    """NEXT-4: the relative L2 residual of the multiple-scattering system on patch i,
+    eq:l2res:  (1/|Gamma_i|) || S sigma_i + sum_{j != i} S_ij sigma_j - 1 ||_{L2(Gamma_i)},
+    on the residual grid of the tables (independent of the solve's grids):
+      S sigma_i at the grid = res_S fhat_i  (the self-patch potential of the basis solutions, nc_tables/residual.py)
+      sum_{j != i} S_ij sigma_j = the compressed field of every other patch (steps 2-4 of ``matvec``)
+      the norm and |Gamma_i| by the grid's quadrature weights.
+    Returns (res per listed patch, pointwise residual (n, n_res))."""
+    N = len(centers)
+    x = np.asarray(x, dtype=np.float64).reshape(N, -1)
+    R = frames(centers)
+    s = global_nodes(R, tab.shat).reshape(-1, 3)
+    spatch = np.repeat(np.arange(N, dtype=np.int64), tab.shat.shape[0])
+    rho = outgoing(tab.T, x).reshape(-1)
+    res, pw = [], []
+    for i in np.asarray(patches, dtype=np.int64):
+        xr = global_nodes(R[[i]], tab.res_rhat)[0]
+        u = field(kind, xr, np.full(len(xr), i, dtype=np.int64), s, spatch, rho)
+        r = tab.res_S @ x[i] + u - 1.0
+        pw.append(r)
+        res.append(np.sqrt(np.sum(tab.res_w * r * r)) / np.sum(tab.res_w))
+    return np.array(res), np.array(pw)
+
+
 def mfpt_field(v, pts, I_sigma):
     """Interior MFPT at a point from the potential v (eq:vtilde, with D = -I_sigma from the lemma
     at PAPER.md:556-566): vbar = (v - 1) / (3 D) + (1 - |x|^2) / 6."""

@@ -756,6 +756,66 @@ int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts
   return rc;
 }
 
+int nc_residual(nc_handle* h, const double* x_all, int n_sel, const int64_t* patches, int n_res,
+                const double* res_rhat, const double* res_w, const double* res_S, double* res, double* pointwise) {
+  if (!h || !x_all || n_sel < 0 || n_res < 1 || (n_sel > 0 && (!patches || !res_rhat || !res_w || !res_S || !res)))
+    return fail(NC_EINVAL, "nc_residual: bad argument");
+  if (n_sel == 0) return NC_OK;
+  std::vector<int64_t> inv(h->N);
+  for (int64_t r = 0; r < h->N; ++r) inv[h->perm[r]] = r;
+  std::vector<int64_t> rows(n_sel);
+  for (int q = 0; q < n_sel; ++q) {
+    if (patches[q] < 0 || patches[q] >= h->N)
+      return fail(NC_EINVAL, "nc_residual: patch index " + std::to_string(patches[q]) + " out of range");
+    rows[q] = inv[patches[q]];
+  }
+  NC_CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t s = h->stream;
+  const int K = h->K, p0 = h->rung_p[0];
+  const double* src0 = h->d_src4 + h->rung_soff[0];
+  // rho of the base rung for all N patches (K1 restricted to rung 0)
+  launch_gemm_dmma(x_all, K, 1, 0, h->d_T + (size_t)h->rung_trow[0] * K, h->N, p0, K, h->d_src4 + h->rung_soff[0] + 3,
+                   (int64_t)p0 * 4, 4, nullptr, 0, s);
+  const int nseg = (int)std::min<int64_t>(h->N, 128);
+  const size_t nr = (size_t)n_res;
+  double *d_rhat = nullptr, *d_w = nullptr, *d_S = nullptr, *d_t = nullptr, *d_up = nullptr, *d_out = nullptr;
+  int64_t* d_rows = nullptr;
+  cudaError_t e = cudaMalloc(&d_rhat, nr * 3 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_w, nr * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_S, nr * K * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_t, (size_t)n_sel * nr * 3 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_up, (size_t)n_sel * nseg * nr * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, ((size_t)n_sel * nr + n_sel) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_rows, (size_t)n_sel * sizeof(int64_t));
+  int rc = NC_OK;
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    rc = fail(NC_ENOMEM, "nc_residual: device allocation failed");
+  } else {
+    e = cudaMemcpyAsync(d_rhat, res_rhat, nr * 3 * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_w, res_w, nr * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_S, res_S, nr * K * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_rows, rows.data(), (size_t)n_sel * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+      for (int q = 0; q < n_sel; ++q) {   // the residual grid on patch rows[q] (scaled by 1/2), then the other patches' field
+        double* tx = d_t + (size_t)q * nr * 3;
+        launch_targets(h->d_frames, rows[q], 1, d_rhat, n_res, 0.5, tx, tx + nr, tx + 2 * nr, s);
+        launch_pairs_direct(h->kind, h->pair_tpt, tx, tx + nr, tx + 2 * nr, n_res, n_res, rows[q], src0, p0, h->N, nseg,
+                            d_up + (size_t)q * nseg * nr, h->xtab, s);
+      }
+      launch_residual(n_sel, n_res, K, nseg, d_rows, x_all, d_S, d_w, d_up, d_out, d_out + (size_t)n_sel * nr, s);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(res, d_out + (size_t)n_sel * nr, (size_t)n_sel * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && pointwise)
+      e = cudaMemcpyAsync(pointwise, d_out, (size_t)n_sel * nr * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "nc_residual");
+  }
+  for (void* b : {(void*)d_rhat, (void*)d_w, (void*)d_S, (void*)d_t, (void*)d_up, (void*)d_out, (void*)d_rows}) cudaFree(b);
+  return rc;
+}
+
 int nc_stats(const nc_handle* h, nc_stats_t* o) {
   if (!h || !o) return fail(NC_EINVAL, "nc_stats: null argument");
   NC_TRY(read_stages(const_cast<nc_handle*>(h)));

@@ -1,4 +1,6 @@
-// field.cu -- NEXT-3: the single-layer potential of the solved densities at off-surface points,
+// field.cu -- NEXT-3 and NEXT-4.
+//
+// NEXT-3: the single-layer potential of the solved densities at off-surface points,
 //
 //   interior (narrow escape):   v(p) = sum_j sum_m G_I(p, s_jm) rho_jm      eq:intBVPansatz
 //   exterior (narrow capture):  u(p) = sum_j sum_m G_E(p, s_jm) rho_jm      eq:urep
@@ -102,6 +104,53 @@ void launch_field(int kind, const double* pts, int64_t n, const double* src4, in
   else
     k_field<0><<<grid, kFieldThreads, 0, s>>>(pts, n, s4, nrec, nseg, part, dpart);
   k_field_reduce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, dpart, n, nseg, out, dmin);
+}
+
+// NEXT-4: the relative L2 residual of the multiple-scattering system on patch i (eq:l2res),
+//   res_i = || S sigma_i + sum_{j != i} S_ij sigma_j - 1 ||_{L2(Gamma_i)} / |Gamma_i|
+// on the tables' residual grid.  The field of the other patches comes from the direct pair kernel (api.cu launches
+// k_pairs_direct per listed patch with the grid as its targets); this kernel adds the self term res_S fhat_i,
+// subtracts the data 1, and forms the weighted norm.  One CTA per listed patch; fixed-order reductions.
+__global__ void k_residual(int n_sel, int n_res, int K, int nseg, const int64_t* __restrict__ rows,
+                           const double* __restrict__ x_all, const double* __restrict__ S,
+                           const double* __restrict__ w, const double* __restrict__ upart,
+                           double* __restrict__ pointwise, double* __restrict__ res) {
+  __shared__ double red[256];
+  const int q = blockIdx.x;
+  const double* xi = x_all + rows[q] * K;
+  const double* up = upart + (size_t)q * nseg * n_res;
+  double acc = 0.0, area = 0.0;
+  for (int k = threadIdx.x; k < n_res; k += blockDim.x) {
+    double u = 0.0;
+    for (int sg = 0; sg < nseg; ++sg) u += up[(size_t)sg * n_res + k];
+    double self = 0.0;
+    for (int a = 0; a < K; ++a) self = fma(S[(size_t)k * K + a], xi[a], self);
+    const double r = (self + u) - 1.0;
+    pointwise[(size_t)q * n_res + k] = r;
+    acc = fma(w[k] * r, r, acc);
+    area += w[k];
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  const double tot = red[0];
+  __syncthreads();
+  red[threadIdx.x] = area;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) res[q] = sqrt(tot) / red[0];
+}
+
+void launch_residual(int n_sel, int n_res, int K, int nseg, const int64_t* rows, const double* x_all, const double* S,
+                     const double* w, const double* upart, double* pointwise, double* res, cudaStream_t s) {
+  if (n_sel <= 0) return;
+  k_residual<<<(unsigned)n_sel, 256, 0, s>>>(n_sel, n_res, K, nseg, rows, x_all, S, w, upart, pointwise, res);
 }
 
 }  // namespace nc

@@ -208,6 +208,11 @@ int field_segments(int64_t n, int64_t nrec);
 void launch_field(int kind, const double* pts, int64_t n, const double* src4, int64_t nrec, int nseg, double* part,
                   double* dpart, double* out, double* dmin, cudaStream_t s);
 
+// L2 residual diagnostic (field.cu, NEXT-4): per listed patch q (internal row rows[q]), pointwise[q][k] =
+// (S x_q)_k + sum_seg upart[q][seg][k] - 1 and res[q] = sqrt(sum_k w_k pointwise^2) / sum_k w_k
+void launch_residual(int n_sel, int n_res, int K, int nseg, const int64_t* rows, const double* x_all, const double* S,
+                     const double* w, const double* upart, double* pointwise, double* res, cudaStream_t s);
+
 // BLAS-1 style helpers for GMRES (deterministic two-stage reductions)
 int64_t multidot_partials(int64_t n);
 void launch_multidot(const double* V, int64_t ldv, int nv, const double* w, int64_t n, double* part, double* out,

@@ -58,7 +58,7 @@ class NcStats(ctypes.Structure):
 
 
 EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt",
-           "nc_field", "nc_stats",
+           "nc_field", "nc_residual", "nc_stats",
            "nc_time_stages", "nc_tree_lists", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
 
 _lib = None
@@ -82,6 +82,7 @@ def load_library(path: str = LIB_PATH):
     L.nc_gmres.argtypes = [vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int), _dp, vp]
     L.nc_flux_or_mfpt.argtypes = [vp, vp, _dp, _dp]
     L.nc_field.argtypes = [vp, vp, ctypes.c_int64, _dp, _dp, _dp]
+    L.nc_residual.argtypes = [vp, vp, ctypes.c_int, _i64p, ctypes.c_int, _dp, _dp, _dp, _dp, _dp]
     L.nc_stats.argtypes = [vp, ctypes.POINTER(NcStats)]
     L.nc_time_stages.argtypes = [vp, ctypes.c_int]
     L.nc_tree_lists.argtypes = [vp, _i64p, _i64p, _i64p, _i64p, _i64p]
@@ -232,6 +233,21 @@ class Handle:
         _check(self._L.nc_field(self._h, _ptr(x_all), len(pts), pts.ctypes.data_as(_dp), out.ctypes.data_as(_dp),
                                 dmin.ctypes.data_as(_dp)))
         return out, dmin
+
+    def residual(self, x_all, patches, tables):
+        """L2 residual (eq:l2res) on the listed caller patches with the tables' residual grid (nc_residual);
+        returns (res per patch, pointwise residual (n, n_res))."""
+        if tables.res_S is None:
+            raise ValueError("the tables carry no residual grid (nc_tables/residual.py)")
+        pat = np.ascontiguousarray(patches, dtype=np.int64).reshape(-1)
+        rh = np.ascontiguousarray(tables.res_rhat, dtype=np.float64)
+        rw = np.ascontiguousarray(tables.res_w, dtype=np.float64)
+        rs = np.ascontiguousarray(tables.res_S, dtype=np.float64)
+        res, pw = np.empty(len(pat)), np.empty((len(pat), len(rw)))
+        _check(self._L.nc_residual(self._h, _ptr(x_all), len(pat), pat.ctypes.data_as(_i64p), len(rw),
+                                   rh.ctypes.data_as(_dp), rw.ctypes.data_as(_dp), rs.ctypes.data_as(_dp),
+                                   res.ctypes.data_as(_dp), pw.ctypes.data_as(_dp)))
+        return res, pw
 
     def time_stages(self, enable=True):
         _check(self._L.nc_time_stages(self._h, int(enable)))
