@@ -268,7 +268,8 @@ static bool stage_ldg() {
 
 // instantiated grid-kernel variants: warp-level units (tpt, unroll, far, warps per CTA, minb) and CTA units
 // (nt, tpt, unroll, far, tma, minb); NC_GRID_VARIANT must name one of them (else the default is kept)
-#define NC_GRID_W_LIST(X) X(2, 4, 5, 8, 3) X(2, 4, 5, 8, 4) X(2, 4, 5, 4, 8) X(2, 2, 5, 8, 4) X(2, 4, 6, 8, 4)
+#define NC_GRID_W_LIST(X) X(2, 4, 5, 8, 3) X(2, 4, 5, 8, 4) X(2, 4, 5, 4, 8) X(2, 2, 5, 8, 4) X(2, 4, 6, 8, 4) \
+  X(2, 4, 2, 8, 3) X(2, 4, 3, 8, 3)
 #define NC_GRID_C_LIST(X)                                                                                        \
   X(128, 2, 4, 2, 0, 8) X(128, 2, 4, 3, 0, 8) X(128, 2, 4, 4, 0, 8) X(128, 2, 4, 2, 0, 6) X(128, 2, 4, 5, 2, 8)   \
   X(128, 2, 4, 5, 2, 7) X(128, 2, 4, 5, 2, 6) X(128, 2, 2, 5, 2, 8) X(128, 2, 4, 5, 0, 8) X(128, 2, 4, 6, 0, 8)   \
@@ -335,14 +336,14 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
                                                           double* __restrict__ part, const double2* __restrict__ fsrc,
                                                           int fn, int fbase, int* __restrict__ counter,
                                                           int64_t nunits) {
-  static_assert(FAR >= 2 && far_table_rcp(FAR), "warp-level grid kernel: reciprocal-seeded far table only");
+  static_assert(FAR >= 2, "warp-level grid kernel: exponent-indexed far table only");
   extern __shared__ double4 sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double4* buf = sm + (size_t)warp * 2 * wrec;   // this warp's two chunk buffers
   int32_t* slst = reinterpret_cast<int32_t*>(sm + (size_t)WPC * 2 * wrec) + warp * 32;
   double2* ftab = reinterpret_cast<double2*>(reinterpret_cast<int32_t*>(sm + (size_t)WPC * 2 * wrec) + WPC * 32);
-  const int nvec = fn / 2;
-  const unsigned tb = smem_u32(ftab) - 8u * (unsigned)fbase;
+  const int nvec = far_table_rcp(FAR) ? fn / 2 : fn;   // 8-byte L entries (rcp forms) or 16-byte (c, L)
+  const unsigned tb = smem_u32(ftab) - (far_table_rcp(FAR) ? 8u : 16u) * (unsigned)fbase;
   const int flim = KIND == 1 ? fbase + fn - 1 : fbase;
   const double2 cst = __ldg(fsrc + nvec);
   const double fa2 = cst.x, fa3 = cst.y;
@@ -410,7 +411,7 @@ static void launch_grid_w(const GridUnit* units, int64_t nunits, const double* g
                           const int32_t* srclist, const double* src4, int wrec, double* part, int* counter,
                           const FarTable& ft, cudaStream_t s) {
   const size_t smem = (size_t)WPC * 2 * wrec * sizeof(double4) + (size_t)WPC * 32 * sizeof(int32_t) +
-                      (size_t)(ft.n / 2) * sizeof(double2);
+                      (size_t)ft.n * (far_table_rcp(FAR) ? 8 : 16) + sizeof(double2);
   auto kern = k_pairs_grid_w<KIND, TPT, UNROLL, FAR, WPC, MINB>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 148, per = 1;

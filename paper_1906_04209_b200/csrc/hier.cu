@@ -515,6 +515,8 @@ __device__ __forceinline__ void grid_eval_ang(const double2* __restrict__ cg, in
   }
 }
 
+constexpr int kAngNrMax = 12;   // grid_eval_ang instantiations (n_r = 1..12)
+
 template <int NPT>
 __device__ __forceinline__ bool grid_eval_ang_any(int nr, const double2* __restrict__ cg, int M, const double (&x)[NPT],
                                                   const double (&w2)[NPT], const double (&c1)[NPT],
@@ -544,7 +546,11 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
                                                const int64_t* __restrict__ coff, const double* __restrict__ coef,
                                                const double* __restrict__ tx, const double* __restrict__ ty,
                                                const double* __restrict__ tz, const double* __restrict__ udir,
-                                               double* __restrict__ u, const uint8_t* __restrict__ gsep) {
+                                               double* __restrict__ u, const uint8_t* __restrict__ gsep,
+                                               int nr_big) {
+  // MB = 0 evaluates the grids with n_r <= kAngNrMax only (grid_eval_ang); a second pass (MB = 1, nr_big = 1) adds
+  // the rest to u when any exists (tight precisions): the register-held accumulators of the first pass then need
+  // no fallback code in the same kernel
   extern __shared__ double2 c2[];
   const int64_t i = blockIdx.x;
   for (int kb = 0; kb < Kstar; kb += NPT * NT) {
@@ -554,7 +560,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
       const int k = min(kb + (int)threadIdx.x + q * NT, Kstar - 1);
       const int64_t t = i * Kstar + k;
       px[q] = 2.0 * tx[t]; py[q] = 2.0 * ty[t]; pz[q] = 2.0 * tz[t];
-      acc[q] = udir ? udir[t] : 0.0;
+      acc[q] = nr_big ? u[t] : (udir ? udir[t] : 0.0);   // second pass: add to the first's result
     }
     for (int lvl = 0; lvl <= L; ++lvl) {
       const int g = pgl[(int64_t)lvl * rc + i];
@@ -592,7 +598,11 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
         const int nr = gnr[kg], M = gna[kg] / 2;
         const double2* __restrict__ cg = c2 + base;
         base += (M + 1) * nr;
-        if (MB == 0 && grid_eval_ang_any<NPT>(nr, cg, M, x, w2, c1, s1, acc)) continue;   // n_r <= 12
+        if (MB == 0) {
+          grid_eval_ang_any<NPT>(nr, cg, M, x, w2, c1, s1, acc);   // n_r <= kAngNrMax (larger: the second pass)
+          continue;
+        }
+        if (nr_big && nr <= kAngNrMax) continue;                    // second pass: done by the first
         double cm[NPT], sm[NPT], cmm[NPT], smm[NPT];   // cos/sin(m theta), ((m - 1) theta)
 #pragma unroll
         for (int q = 0; q < NPT; ++q) { cm[q] = 1.0; sm[q] = 0.0; cmm[q] = c1[q]; smm[q] = -s1[q]; }
@@ -826,10 +836,12 @@ template <int NT, int NPT, int MB, int MINB>
 static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const int64_t* ggrid0,
                            const double* F, const double* gR, const int32_t* gnr, const int32_t* gna,
                            const int64_t* coff, const double* coef, const double* tx, const double* ty,
-                           const double* tz, const double* udir, double* u, const uint8_t* gsep, cudaStream_t s) {
+                           const double* tz, const double* udir, double* u, const uint8_t* gsep, cudaStream_t s,
+                           int nr_big = 0) {
   auto kern = k_interp<NT, NPT, MB, MINB>;
   if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep);
+  kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
+                                     nr_big);
   return NC_OK;
 }
 
@@ -839,8 +851,19 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
                          const double* ty, const double* tz, const double* udir, double* u, const uint8_t* gsep,
                          cudaStream_t s) {
   const InterpVariant v = interp_variant();
-  (void)nrmax;
   (void)namax;
+  if (v.mb == 0 && nrmax > kAngNrMax) {   // the first pass leaves the grids with n_r > kAngNrMax to a second one
+    int rc1 = NC_OK;
+#define NC_I(NT, NPT, MB, MINB)                                                                                  \
+  if (rc1 == NC_OK && v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                \
+    rc1 = launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, \
+                                             udir, u, gsep, s);
+    NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6)
+#undef NC_I
+    if (rc1 != NC_OK) return rc1;
+    return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir,
+                                         u, gsep, s, 1);
+  }
 #define NC_I(NT, NPT, MB, MINB)                                                                             \
   if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                           \
     return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep, s);
