@@ -203,6 +203,16 @@ int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts
 int nc_residual(nc_handle* h, const double* x_all, int n_sel, const int64_t* patches, int n_res,
                 const double* res_rhat, const double* res_w, const double* res_S, double* res, double* pointwise);
 
+/* Step-1 table build, GPU part (NEXT-1): the Gaussian sketch of the interpolative decomposition
+ * that compresses a patch's outgoing field (Step 1(b) PAPER.md:1295-1299; nc_tables/skeleton.py)
+ *   Y = Omega A,   A_{tf} = G(x^t_t, x^f_f)   (on-surface G of `kind`, eq:Gintonsurface / eq:Gextonsurface)
+ *   train  host, n_train x 3 training points (far-field region);  fine  host, n_fine x 3 fine-grid points
+ *   omega  host, l x n_train (row-major) Gaussian test matrix;    Y     host, l x n_fine (output)
+ * Needs no handle: allocates on `device`, generates A in HBM (n_fine x n_train doubles), one fp64 tensor-core GEMM,
+ * synchronous.  Errors: NC_EINVAL, NC_ENOMEM, NC_ECUDA. */
+int nc_id_sketch(int kind, int device, int64_t n_train, const double* train, int64_t n_fine, const double* fine,
+                 int l, const double* omega, double* Y);
+
 /* Counters and the last matvec's per-stage device times.  nc_time_stages(h, 1) makes the next
  * matvecs record per-stage CUDA events on the matvec's stream (no host synchronisation inside nc_matvec);
  * nc_stats waits for the last recorded matvec's events and converts them to ms_last. */

@@ -25,13 +25,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20, n_theta: int = 64,
                  id_tol: float = 1e-11, zn_r: int | None = None, zn_theta: int | None = None, verbose=False,
                  ladder: bool = True, ladder_max: float = 1.2, ladder_ratio: float = 2.0 ** (1.0 / 3.0),
-                 ladder_id_tol: float | None = 1e-10):
+                 ladder_id_tol: float | None = 1e-10, gpu_sketch: bool = False):
+    """gpu_sketch: form the ID sketches on the GPU (nc_id_sketch, NEXT-1) instead of numpy."""
+    sk = None
+    if gpu_sketch:
+        import paper_1906_04209_b200 as ncgpu
+        sk = ncgpu.id_sketch
     t0 = time.time()
     op = solve_onepatch(kind, eps, M, npan, k, n_theta)
     t1 = time.time()
     fine, wf, B = fine_grid(op)
     train = training_grid(eps)
-    J, Pi = interp_decomp(kind, train, fine, id_tol)
+    J, Pi = interp_decomp(kind, train, fine, id_tol, sketch=sk)
     T = Pi @ (wf[:, None] * B)
     shat = fine[J]
     t2 = time.time()
@@ -47,7 +52,7 @@ def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20
         rung = 1
         while 2.0 * eps * ladder_ratio ** rung < ladder_max:
             inner = 2.0 * ladder_ratio ** rung
-            Jk, Pik = interp_decomp(kind, training_grid(eps, inner=inner), fine, ladder_id_tol or id_tol)
+            Jk, Pik = interp_decomp(kind, training_grid(eps, inner=inner), fine, ladder_id_tol or id_tol, sketch=sk)
             Tk = Pik @ (wf[:, None] * B)
             lad_r.append(inner * eps)
             lad_p.append(len(Jk))

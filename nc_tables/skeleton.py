@@ -30,16 +30,29 @@ def training_grid(eps: float, n_per_shell: int = 10, n_az: int = 96, inner: floa
     return np.stack([np.sin(R) * np.cos(AZ), np.sin(R) * np.sin(AZ), np.cos(R)], axis=-1).reshape(-1, 3)
 
 
-def interp_decomp(kind: int, train: np.ndarray, fine: np.ndarray, tol: float, oversample: int = 400, seed: int = 0,
-                  chunk: int = 512):
-    """Column ID of A = G(train, fine) from a Gaussian sketch.  Returns (J, Pi) with A ~= A[:, J] Pi."""
+def test_matrix(n_train: int, oversample: int = 400, seed: int = 0, chunk: int = 512) -> np.ndarray:
+    """The Gaussian test matrix Omega (l x n_train), drawn in the column chunks interp_decomp consumes."""
     rng = np.random.default_rng(seed)
+    l = min(oversample, n_train)
+    return np.concatenate([rng.standard_normal((l, min(n_train, a + chunk) - a)) for a in range(0, n_train, chunk)],
+                          axis=1)
+
+
+def interp_decomp(kind: int, train: np.ndarray, fine: np.ndarray, tol: float, oversample: int = 400, seed: int = 0,
+                  chunk: int = 512, sketch=None):
+    """Column ID of A = G(train, fine) from a Gaussian sketch.  Returns (J, Pi) with A ~= A[:, J] Pi.
+    ``sketch(kind, train, fine, omega)``: optional Y = omega A evaluator (the GPU one: paper_1906_04209_b200.id_sketch,
+    NEXT-1); default the numpy chunk loop below."""
     l = min(oversample, train.shape[0])
-    Y = np.zeros((l, fine.shape[0]))
-    for a in range(0, train.shape[0], chunk):
-        b = min(train.shape[0], a + chunk)
-        A = green_xyz(kind, train[a:b, None, :], fine[None, :, :])
-        Y += rng.standard_normal((l, b - a)) @ A
+    if sketch is not None:
+        Y = sketch(kind, train, fine, test_matrix(train.shape[0], oversample, seed, chunk))
+    else:
+        rng = np.random.default_rng(seed)
+        Y = np.zeros((l, fine.shape[0]))
+        for a in range(0, train.shape[0], chunk):
+            b = min(train.shape[0], a + chunk)
+            A = green_xyz(kind, train[a:b, None, :], fine[None, :, :])
+            Y += rng.standard_normal((l, b - a)) @ A
     Q, R, piv = sla.qr(Y, mode="economic", pivoting=True)
     d = np.abs(np.diag(R))
     p = int(np.sum(d > tol * d[0]))

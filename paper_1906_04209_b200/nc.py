@@ -58,7 +58,7 @@ class NcStats(ctypes.Structure):
 
 
 EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt",
-           "nc_field", "nc_residual", "nc_stats",
+           "nc_field", "nc_residual", "nc_id_sketch", "nc_stats",
            "nc_time_stages", "nc_tree_lists", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
 
 _lib = None
@@ -83,6 +83,8 @@ def load_library(path: str = LIB_PATH):
     L.nc_flux_or_mfpt.argtypes = [vp, vp, _dp, _dp]
     L.nc_field.argtypes = [vp, vp, ctypes.c_int64, _dp, _dp, _dp]
     L.nc_residual.argtypes = [vp, vp, ctypes.c_int, _i64p, ctypes.c_int, _dp, _dp, _dp, _dp, _dp]
+    L.nc_id_sketch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, _dp, ctypes.c_int64, _dp, ctypes.c_int, _dp,
+                               _dp]
     L.nc_stats.argtypes = [vp, ctypes.POINTER(NcStats)]
     L.nc_time_stages.argtypes = [vp, ctypes.c_int]
     L.nc_tree_lists.argtypes = [vp, _i64p, _i64p, _i64p, _i64p, _i64p]
@@ -119,6 +121,18 @@ def split_rows(N: int, world: int, weights=None):
     _check(L.nc_split_rows(w.ctypes.data_as(_dp) if w is not None else None, int(N), int(world),
                            b.ctypes.data_as(_i64p), c.ctypes.data_as(_i64p)))
     return b, c
+
+
+def id_sketch(kind: int, train, fine, omega, device: int = 0) -> np.ndarray:
+    """Y = omega @ G(train, fine) on the GPU (nc_id_sketch): the sketch of the Step-1 interpolative decomposition."""
+    L = load_library()
+    tr = np.ascontiguousarray(train, dtype=np.float64).reshape(-1, 3)
+    fi = np.ascontiguousarray(fine, dtype=np.float64).reshape(-1, 3)
+    om = np.ascontiguousarray(omega, dtype=np.float64)
+    Y = np.empty((om.shape[0], len(fi)))
+    _check(L.nc_id_sketch(int(kind), int(device), len(tr), tr.ctypes.data_as(_dp), len(fi), fi.ctypes.data_as(_dp),
+                          om.shape[0], om.ctypes.data_as(_dp), Y.ctypes.data_as(_dp)))
+    return Y
 
 
 def _ptr(t):
