@@ -269,7 +269,7 @@ static bool stage_ldg() {
 // instantiated grid-kernel variants: warp-level units (tpt, unroll, far, warps per CTA, minb) and CTA units
 // (nt, tpt, unroll, far, tma, minb); NC_GRID_VARIANT must name one of them (else the default is kept)
 #define NC_GRID_W_LIST(X) X(2, 4, 5, 8, 3) X(2, 4, 5, 8, 4) X(2, 4, 5, 4, 8) X(2, 2, 5, 8, 4) X(2, 4, 6, 8, 4) \
-  X(2, 4, 2, 8, 3) X(2, 4, 3, 8, 3)
+  X(2, 4, 2, 8, 3) X(2, 4, 3, 8, 3) X(1, 4, 5, 8, 4) X(1, 4, 5, 8, 6) X(2, 4, 5, 8, 2)
 #define NC_GRID_C_LIST(X)                                                                                        \
   X(128, 2, 4, 2, 0, 8) X(128, 2, 4, 3, 0, 8) X(128, 2, 4, 4, 0, 8) X(128, 2, 4, 2, 0, 6) X(128, 2, 4, 5, 2, 8)   \
   X(128, 2, 4, 5, 2, 7) X(128, 2, 4, 5, 2, 6) X(128, 2, 2, 5, 2, 8) X(128, 2, 4, 5, 0, 8) X(128, 2, 4, 6, 0, 8)   \
