@@ -357,14 +357,14 @@ def main():
     # NEXT-3: the off-surface field of the solution (nc_field, host points in / values out, synchronous) at 4096
     # points on a sphere inside (interior: radius 0.5) or outside (exterior: radius 2) the unit sphere
     field = None
-    if world == 1:
+    if world == 1 and solve is not None:   # (skipped with --no-solve: the ncu launch list covers the matvec step only)
         n_f = 4096
         k = np.arange(n_f) + 0.5
         zf = 1.0 - 2.0 * k / n_f
         phi = np.pi * (1.0 + 5.0 ** 0.5) * k
         rf = 0.5 if cfg.kind == 0 else 2.0
         pts = rf * np.stack([np.sqrt(1 - zf * zf) * np.cos(phi), np.sqrt(1 - zf * zf) * np.sin(phi), zf], 1)
-        xf = xs if solve is not None else x
+        xf = xs
         h.field(xf, pts[:8])   # warm-up
         torch.cuda.synchronize()
         t0 = time.perf_counter()

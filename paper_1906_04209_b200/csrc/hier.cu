@@ -1517,7 +1517,8 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   h->launches_last += H->nunits > 0;
   if (h->time_stages) cudaEventRecord(h->ev[3], s);
   if (H->nchunks) {
-    k_reduce_chunks<<<(unsigned)H->nchunks, 256, 0, s>>>(H->d_chunks, H->nchunks, H->d_part, H->upts, H->d_gval);
+    k_reduce_chunks<<<(unsigned)H->nchunks, std::min(256, std::max(32, H->upts)), 0, s>>>(H->d_chunks, H->nchunks,
+                                                                                   H->d_part, H->upts, H->d_gval);
     h->launches_last++;
   }
   // step 4a: grid samples -> coefficients
