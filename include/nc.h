@@ -203,6 +203,15 @@ int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts
 int nc_residual(nc_handle* h, const double* x_all, int n_sel, const int64_t* patches, int n_res,
                 const double* res_rhat, const double* res_w, const double* res_S, double* res, double* pointwise);
 
+/* Density recovery (NEXT-3; eq:recoversig PAPER.md:797-807): sigma_i = B fhat_i, the density of
+ * each listed patch at the one-patch solver's fine grid (B: n_f x K, the per-eps basis solutions sampled there,
+ * nc_tables onepatch.fine_grid; with the fine weights w, w . sigma_i = I . fhat_i = int sigma_i dS).
+ *   x_all   device, N x K (all patches, internal order);  patches  host, n_sel caller indices
+ *   B       host, n_f x K row-major;  sigma  host, n_sel x n_f (output)
+ * One fp64 tensor-core GEMM.  Synchronizes.  Errors: NC_EINVAL, NC_ENOMEM, NC_ECUDA. */
+int nc_density(nc_handle* h, const double* x_all, int n_sel, const int64_t* patches, int n_f, const double* B,
+               double* sigma);
+
 /* Step-1 table build, GPU part (NEXT-1): the Gaussian sketch of the interpolative decomposition
  * that compresses a patch's outgoing field (Step 1(b) PAPER.md:1295-1299; nc_tables/skeleton.py)
  *   Y = Omega A,   A_{tf} = G(x^t_t, x^f_f)   (on-surface G of `kind`, eq:Gintonsurface / eq:Gextonsurface)

@@ -183,6 +183,11 @@ def residual(kind, centers, tab, x, patches):
     return np.array(res), np.array(pw)
 
 
+def density(x, patches, B):
+    """sigma_i = B fhat_i (eq:recoversig) for the listed patches: the definition, a matmul."""
+    return np.asarray(x, dtype=np.float64)[np.asarray(patches, dtype=np.int64)] @ np.asarray(B, dtype=np.float64).T
+
+
 def mfpt_field(v, pts, I_sigma):
     """Interior MFPT at a point from the potential v (eq:vtilde, with D = -I_sigma from the lemma
     at PAPER.md:556-566): vbar = (v - 1) / (3 D) + (1 - |x|^2) / 6."""

@@ -816,6 +816,48 @@ int nc_residual(nc_handle* h, const double* x_all, int n_sel, const int64_t* pat
   return rc;
 }
 
+int nc_density(nc_handle* h, const double* x_all, int n_sel, const int64_t* patches, int n_f, const double* B,
+               double* sigma) {
+  if (!h || !x_all || n_sel < 0 || n_f < 1 || (n_sel > 0 && (!patches || !B || !sigma)))
+    return fail(NC_EINVAL, "nc_density: bad argument");
+  if (n_sel == 0) return NC_OK;
+  std::vector<int64_t> inv(h->N), rows(n_sel);
+  for (int64_t r = 0; r < h->N; ++r) inv[h->perm[r]] = r;
+  for (int q = 0; q < n_sel; ++q) {
+    if (patches[q] < 0 || patches[q] >= h->N)
+      return fail(NC_EINVAL, "nc_density: patch index " + std::to_string(patches[q]) + " out of range");
+    rows[q] = inv[patches[q]];
+  }
+  NC_CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t s = h->stream;
+  const int K = h->K;
+  double *d_B = nullptr, *d_x = nullptr, *d_s = nullptr;
+  int64_t* d_rows = nullptr;
+  cudaError_t e = cudaMalloc(&d_B, (size_t)n_f * K * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_x, (size_t)n_sel * K * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_s, (size_t)n_sel * n_f * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_rows, (size_t)n_sel * sizeof(int64_t));
+  int rc = NC_OK;
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    rc = fail(NC_ENOMEM, "nc_density: device allocation failed");
+  } else {
+    e = cudaMemcpyAsync(d_B, B, (size_t)n_f * K * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_rows, rows.data(), (size_t)n_sel * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+      launch_gather_rows(x_all, d_rows, n_sel, K, d_x, s);
+      // sigma (n_sel x n_f) = X_sel (n_sel x K) . B^T
+      launch_gemm_dmma(d_x, K, 1, 0, d_B, n_sel, n_f, K, d_s, n_f, 1, nullptr, 0, s);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sigma, d_s, (size_t)n_sel * n_f * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "nc_density");
+  }
+  for (void* b : {(void*)d_B, (void*)d_x, (void*)d_s, (void*)d_rows}) cudaFree(b);
+  return rc;
+}
+
 int nc_stats(const nc_handle* h, nc_stats_t* o) {
   if (!h || !o) return fail(NC_EINVAL, "nc_stats: null argument");
   NC_TRY(read_stages(const_cast<nc_handle*>(h)));

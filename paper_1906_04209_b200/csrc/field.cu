@@ -147,6 +147,19 @@ __global__ void k_residual(int n_sel, int n_res, int K, int nseg, const int64_t*
   if (threadIdx.x == 0) res[q] = sqrt(tot) / red[0];
 }
 
+// density recovery (NEXT-3, eq:recoversig PAPER.md:797-807): gather the listed patches' coefficient rows
+__global__ void k_gather_rows(const double* __restrict__ x_all, const int64_t* __restrict__ rows, int n_sel, int K,
+                              double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n_sel * K) return;
+  out[t] = x_all[rows[t / K] * K + t % K];
+}
+
+void launch_gather_rows(const double* x_all, const int64_t* rows, int n_sel, int K, double* out, cudaStream_t s) {
+  if (n_sel <= 0) return;
+  k_gather_rows<<<(unsigned)(((int64_t)n_sel * K + 255) / 256), 256, 0, s>>>(x_all, rows, n_sel, K, out);
+}
+
 void launch_residual(int n_sel, int n_res, int K, int nseg, const int64_t* rows, const double* x_all, const double* S,
                      const double* w, const double* upart, double* pointwise, double* res, cudaStream_t s) {
   if (n_sel <= 0) return;

@@ -213,6 +213,8 @@ void launch_field(int kind, const double* pts, int64_t n, const double* src4, in
 void launch_residual(int n_sel, int n_res, int K, int nseg, const int64_t* rows, const double* x_all, const double* S,
                      const double* w, const double* upart, double* pointwise, double* res, cudaStream_t s);
 
+void launch_gather_rows(const double* x_all, const int64_t* rows, int n_sel, int K, double* out, cudaStream_t s);
+
 // BLAS-1 style helpers for GMRES (deterministic two-stage reductions)
 int64_t multidot_partials(int64_t n);
 void launch_multidot(const double* V, int64_t ldv, int nv, const double* w, int64_t n, double* part, double* out,

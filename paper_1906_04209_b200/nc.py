@@ -58,7 +58,7 @@ class NcStats(ctypes.Structure):
 
 
 EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt",
-           "nc_field", "nc_residual", "nc_id_sketch", "nc_stats",
+           "nc_field", "nc_residual", "nc_density", "nc_id_sketch", "nc_stats",
            "nc_time_stages", "nc_tree_lists", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
 
 _lib = None
@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH):
     L.nc_flux_or_mfpt.argtypes = [vp, vp, _dp, _dp]
     L.nc_field.argtypes = [vp, vp, ctypes.c_int64, _dp, _dp, _dp]
     L.nc_residual.argtypes = [vp, vp, ctypes.c_int, _i64p, ctypes.c_int, _dp, _dp, _dp, _dp, _dp]
+    L.nc_density.argtypes = [vp, vp, ctypes.c_int, _i64p, ctypes.c_int, _dp, _dp]
     L.nc_id_sketch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, _dp, ctypes.c_int64, _dp, ctypes.c_int, _dp,
                                _dp]
     L.nc_stats.argtypes = [vp, ctypes.POINTER(NcStats)]
@@ -262,6 +263,15 @@ class Handle:
                                    rh.ctypes.data_as(_dp), rw.ctypes.data_as(_dp), rs.ctypes.data_as(_dp),
                                    res.ctypes.data_as(_dp), pw.ctypes.data_as(_dp)))
         return res, pw
+
+    def density(self, x_all, patches, B):
+        """sigma_i = B fhat_i at the fine grid for the listed caller patches (nc_density, eq:recoversig)."""
+        pat = np.ascontiguousarray(patches, dtype=np.int64).reshape(-1)
+        Bc = np.ascontiguousarray(B, dtype=np.float64)
+        sig = np.empty((len(pat), Bc.shape[0]))
+        _check(self._L.nc_density(self._h, _ptr(x_all), len(pat), pat.ctypes.data_as(_i64p), Bc.shape[0],
+                                  Bc.ctypes.data_as(_dp), sig.ctypes.data_as(_dp)))
+        return sig
 
     def time_stages(self, enable=True):
         _check(self._L.nc_time_stages(self._h, int(enable)))
