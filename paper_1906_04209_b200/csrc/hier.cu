@@ -1123,6 +1123,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     int32_t group, nr, na;
     std::vector<int32_t> src;
     std::vector<int> rung;
+    std::vector<double> dist;   // arc distance from the group's cap centre to each source centre
   };
   std::vector<std::vector<GridPlan>> gplans(G);
   std::vector<double> gwork(G, 0.0);
@@ -1228,6 +1229,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       for (size_t n = a; n < b; ++n) {
         gp.src.push_back(cand[n].second);
         gp.rung.push_back(rung_of[n]);
+        gp.dist.push_back(R * cand[n].first + eps);   // beta = (d - eps) / R
       }
       gplans[g].push_back(std::move(gp));
     };
@@ -1317,57 +1319,153 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   std::vector<GridUnit> units;
   std::vector<ChunkRec> chunks;
   std::vector<int32_t> srclist;
-  for (int32_t k : H->grid_ids) {
-    const GridPlan& gp = plans[k];
-    const int64_t q = H->goff[k + 1] - H->goff[k];
-    // grid sources bucketed by rung (sorted by patch within a bucket); slices never mix rungs
-    std::vector<std::pair<int, int32_t>> rs;
-    for (size_t n = 0; n < gp.src.size(); ++n) rs.push_back({gp.rung[n], gp.src[n]});
-    std::sort(rs.begin(), rs.end());
-    struct Slice { int64_t src0; int32_t nsrc; int rung; };
-    std::vector<Slice> slices;
-    size_t a = 0;
-    while (a < rs.size()) {
-      size_t b = a;
-      while (b < rs.size() && rs[b].first == rs[a].first) ++b;
-      const int rung = rs[a].first;
-      const int64_t s0 = (int64_t)srclist.size();
-      for (size_t k2 = a; k2 < b; ++k2) srclist.push_back(rs[k2].second);
-      const int64_t ns = (int64_t)(b - a);
-      const int64_t nsl = (ns + kSliceMax - 1) / kSliceMax;
-      for (int64_t sl = 0; sl < nsl; ++sl) {
-        const int64_t x0 = s0 + (ns * sl) / nsl, x1 = s0 + (ns * (sl + 1)) / nsl;
-        slices.push_back({x0, (int32_t)(x1 - x0), rung});
+  // per-chunk rungs (default; NC_CHUNK_RUNGS=0: one rung per (grid, source)): a work unit's points lie on the rings
+  // r_kr = R cos((kr + 1/2) pi / (2 n_r)) from its first ring kr0 inward, so the gap from a source to the unit's
+  // points is >= d - r_kr0 >= d - R, and the unit may use the smallest skeleton valid at that gap (PAPER.md:1436-1457:
+  // the per-level recompression, here keyed by the distance to the unit's points instead of the whole grid's)
+  const char* ecr = getenv("NC_CHUNK_RUNGS");
+  const bool chunk_rungs = !(ecr && ecr[0] == '0');
+  bool ladder_monotone = true;   // r_k ascending and p_k non-increasing over k >= 1: binary search
+  for (int kk = 2; kk < h->nrung; ++kk)
+    ladder_monotone = ladder_monotone && h->rung_r[kk] > h->rung_r[kk - 1] && h->rung_p[kk] <= h->rung_p[kk - 1];
+  ladder_monotone = ladder_monotone && (h->nrung < 2 || h->rung_p[1] <= h->rung_p[0]);
+  auto best_rung = [&](double gap) {
+    const double g = gap * (1.0 - 1e-12);
+    if (ladder_monotone) {   // the largest k >= 1 with r_k <= g (0 if none)
+      int lo = 1, hi = h->nrung - 1, best = 0;
+      while (lo <= hi) {
+        const int mid = (lo + hi) / 2;
+        if (h->rung_r[mid] <= g) { best = mid; lo = mid + 1; } else hi = mid - 1;
       }
-      H->pairs_grid += (double)q * ns * h->rung_p[rung];
-      rung_pairs[rung] += (double)q * ns * h->rung_p[rung];
-      a = b;
+      return best;
     }
-    for (int64_t c0 = 0; c0 < q; c0 += H->upts) {
-      ChunkRec cr;
-      cr.pt0 = H->goff[k] + c0;
-      cr.npt = (int32_t)std::min<int64_t>(H->upts, q - c0);
-      cr.u0 = (int64_t)units.size();
-      cr.nu = (int32_t)slices.size();
-      chunks.push_back(cr);
-      for (const Slice& sl : slices) {
-        GridUnit u;
-        u.pt0 = cr.pt0;
-        u.npt = cr.npt;
-        u.src0 = sl.src0;
-        u.nsrc = sl.nsrc;
-        u.soff = h->rung_soff[sl.rung];
-        u.p = h->rung_p[sl.rung];
-        u.pad_ = 0;
-        units.push_back(u);
-        H->slot_pairs += (double)H->upts * u.nsrc * u.p;
-        {   // active-warp lane slots; a tail warp with <= 32 points runs one point per lane (direct.cu)
-          const int tpt = grid_unit_tpt(), wpts = 32 * tpt;
-          const int full = u.npt / wpts, rem = u.npt - full * wpts;
-          const int tail = rem == 0 ? 0 : (tpt > 1 && rem <= 32 ? 32 : wpts);
-          H->warp_slot_pairs += (double)(full * wpts + tail) * u.nsrc * u.p;
+    int rung = 0;
+    for (int kk = 1; kk < h->nrung; ++kk)
+      if (h->rung_r[kk] <= g && h->rung_p[kk] <= h->rung_p[rung]) rung = kk;
+    return rung;
+  };
+  struct Slice { int64_t src0; int32_t nsrc; int rung; };
+  struct GridOut {   // one grid's units / chunks / source lists with grid-local offsets
+    std::vector<GridUnit> units;
+    std::vector<ChunkRec> chunks;
+    std::vector<int32_t> src;
+    double pairs = 0, slot = 0, wslot = 0;
+    std::vector<double> rung_pairs;
+  };
+  const int64_t NGL = (int64_t)H->grid_ids.size();
+  std::vector<GridOut> gout(NGL);
+  const int tpt_fill = grid_unit_tpt(), wpts_fill = 32 * tpt_fill;
+  // grids are independent: host threads build them, then the pieces are concatenated in grid order
+#pragma omp parallel
+  {
+    std::vector<std::pair<int, int32_t>> rs;
+    std::vector<Slice> slices;
+    std::vector<int> ring_rung;   // per (source, ring)
+#pragma omp for schedule(dynamic, 256)
+    for (int64_t gi = 0; gi < NGL; ++gi) {
+      const int32_t k = H->grid_ids[gi];
+      const GridPlan& gp = plans[k];
+      GridOut& o = gout[gi];
+      o.rung_pairs.assign(h->nrung, 0.0);
+      const int64_t q = H->goff[k + 1] - H->goff[k];
+      const double Rg = H->gR[gp.group];
+      const size_t ns_all = gp.src.size();
+      if (chunk_rungs) {
+        ring_rung.assign(ns_all * gp.nr, 0);
+        for (int kr = 0; kr < gp.nr; ++kr) {
+          const double rr = Rg * std::cos((kr + 0.5) * M_PI / (2.0 * gp.nr));
+          for (size_t n = 0; n < ns_all; ++n) ring_rung[n * gp.nr + kr] = best_rung(gp.dist[n] - rr);   // >= d - R
         }
       }
+      // the unit's sources bucketed by rung (sorted by patch within a bucket); slices never mix rungs
+      auto make_slices = [&](int kr0) {
+        rs.clear();
+        slices.clear();
+        for (size_t n = 0; n < ns_all; ++n)
+          rs.push_back({chunk_rungs ? ring_rung[n * gp.nr + kr0] : gp.rung[n], gp.src[n]});
+        std::sort(rs.begin(), rs.end());
+        size_t a = 0;
+        while (a < rs.size()) {
+          size_t b = a;
+          while (b < rs.size() && rs[b].first == rs[a].first) ++b;
+          const int64_t s0 = (int64_t)o.src.size();
+          for (size_t k2 = a; k2 < b; ++k2) o.src.push_back(rs[k2].second);
+          const int64_t ns = (int64_t)(b - a);
+          const int64_t nsl = (ns + kSliceMax - 1) / kSliceMax;
+          for (int64_t sl = 0; sl < nsl; ++sl) {
+            const int64_t x0 = s0 + (ns * sl) / nsl, x1 = s0 + (ns * (sl + 1)) / nsl;
+            slices.push_back({x0, (int32_t)(x1 - x0), rs[a].first});
+          }
+          a = b;
+        }
+      };
+      if (!chunk_rungs) make_slices(0);   // one list per grid, shared by its units
+      int kr_cached = -1;                 // chunks with the same first ring share their lists
+      for (int64_t c0 = 0; c0 < q; c0 += H->upts) {
+        ChunkRec cr;
+        cr.pt0 = H->goff[k] + c0;
+        cr.npt = (int32_t)std::min<int64_t>(H->upts, q - c0);
+        if (chunk_rungs) {
+          const int kr0 = (int)(c0 / gp.na);
+          if (kr0 != kr_cached) {
+            make_slices(kr0);
+            kr_cached = kr0;
+          }
+        }
+        cr.u0 = (int64_t)o.units.size();
+        cr.nu = (int32_t)slices.size();
+        o.chunks.push_back(cr);
+        for (const Slice& sl : slices) {
+          GridUnit u;
+          u.pt0 = cr.pt0;
+          u.npt = cr.npt;
+          u.src0 = sl.src0;
+          u.nsrc = sl.nsrc;
+          u.soff = h->rung_soff[sl.rung];
+          u.p = h->rung_p[sl.rung];
+          u.pad_ = 0;
+          o.units.push_back(u);
+          const double pr = (double)cr.npt * sl.nsrc * h->rung_p[sl.rung];
+          o.pairs += pr;
+          o.rung_pairs[sl.rung] += pr;
+          o.slot += (double)H->upts * u.nsrc * u.p;
+          // active-warp lane slots; a tail warp with <= 32 points runs one point per lane (direct.cu)
+          const int full = u.npt / wpts_fill, rem = u.npt - full * wpts_fill;
+          const int tail = rem == 0 ? 0 : (tpt_fill > 1 && rem <= 32 ? 32 : wpts_fill);
+          o.wslot += (double)(full * wpts_fill + tail) * u.nsrc * u.p;
+        }
+      }
+    }
+  }
+  {   // concatenate in grid order (offsets shifted), fixed-order statistics
+    int64_t nu = 0, nch = 0, nsr = 0;
+    for (const GridOut& o : gout) {
+      nu += (int64_t)o.units.size();
+      nch += (int64_t)o.chunks.size();
+      nsr += (int64_t)o.src.size();
+    }
+    units.reserve(nu);
+    chunks.reserve(nch);
+    srclist.reserve(nsr);
+    for (GridOut& o : gout) {
+      const int64_t u_off = (int64_t)units.size(), s_off = (int64_t)srclist.size();
+      for (GridUnit u : o.units) {
+        u.src0 += s_off;
+        units.push_back(u);
+        for (int kk = 0; kk < h->nrung; ++kk)
+          if (u.soff == h->rung_soff[kk]) h->rung_used[kk] = 1;
+      }
+      for (ChunkRec c : o.chunks) {
+        c.u0 += u_off;
+        chunks.push_back(c);
+      }
+      srclist.insert(srclist.end(), o.src.begin(), o.src.end());
+      H->pairs_grid += o.pairs;
+      H->slot_pairs += o.slot;
+      H->warp_slot_pairs += o.wslot;
+      for (int kk = 0; kk < h->nrung; ++kk) rung_pairs[kk] += o.rung_pairs[kk];
+      GridOut().units.swap(o.units);
+      GridOut().src.swap(o.src);
     }
   }
   if (diag) {

@@ -8,7 +8,7 @@ from nc_inputs.tables import load_tables
 name = sys.argv[1]
 precs = [float(v) for v in sys.argv[2:]] or [1e-9]
 cfg = CONFIGS[name]
-tab = load_tables(f"tables/data/{name}.npz")
+tab = load_tables(os.environ.get("NC_TABLES_FILE") or f"tables/data/{name}.npz")
 c = cfg.centers()
 xr = random_coeffs(cfg.N, tab.K, 7)
 xb = np.tile(tab.P @ np.ones(tab.Kstar), (cfg.N, 1))        # the physical right-hand side P.1 (coherent charges)
