@@ -1,7 +1,7 @@
 """Step-1 precomputation: build the patch-operator tables for one (kind, eps).
 
     python -m nc_tables.build --kind 0 --eps 0.003 --out tables/data/C5.npz
-    python -m nc_tables.build --configs          # the five BASELINE.json configs
+    python -m nc_tables.build --configs [--gpu-sketch]   # the five BASELINE.json configs (K* = 248, residual grids)
 
 CPU, untimed, N-independent; its output file is the `nc_tables` input of nc_setup (include/nc.h) and of the
 oracle.  Neither the oracle nor the CUDA path imports this package.
@@ -25,8 +25,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20, n_theta: int = 64,
                  id_tol: float = 1e-11, zn_r: int | None = None, zn_theta: int | None = None, verbose=False,
                  ladder: bool = True, ladder_max: float = 1.2, ladder_ratio: float = 2.0 ** (1.0 / 3.0),
-                 ladder_id_tol: float | None = 1e-10, gpu_sketch: bool = False):
-    """gpu_sketch: form the ID sketches on the GPU (nc_id_sketch, NEXT-1) instead of numpy."""
+                 ladder_id_tol: float | None = 1e-10, gpu_sketch: bool = False, zn_radial: str = "r2"):
+    """gpu_sketch: form the ID sketches on the GPU (nc_id_sketch, NEXT-1) instead of numpy.  zn_radial: the Zernike
+    sampling rule, "r2" (default: 8 Gauss nodes in r^2 x 31 angles, K* = 248, R7) or "r" (16 x 32 = 512)."""
     sk = None
     if gpu_sketch:
         import paper_1906_04209_b200 as ncgpu
@@ -40,7 +41,7 @@ def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20
     T = Pi @ (wf[:, None] * B)
     shat = fine[J]
     t2 = time.time()
-    r, th, P = zernike.transform(M, zn_r, zn_theta)
+    r, th, P = zernike.transform(M, zn_r, zn_theta, zn_radial)
     zhat = zernike.patch_xyz(eps, r, th)
     I = wf @ B
     err = outgoing_error(kind, fine, wf, B, shat, T, eps)
@@ -62,6 +63,7 @@ def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20
             rung += 1
     t3 = time.time()
     meta = dict(kind=kind, eps=eps, M=M, npan=npan, k=k, n_theta=n_theta, id_tol=id_tol, p=len(J), n_f=len(wf),
+                zn_radial=zn_radial, Kstar=len(r),
                 ladder_ratio=ladder_ratio, ladder_id_tol=ladder_id_tol or id_tol,
                 n_train=len(train), outgoing_rel_err=err, t_onepatch_s=t1 - t0, t_id_s=t2 - t1,
                 ladder_r=lad_r, ladder_p=lad_p, ladder_err=lad_err, t_ladder_s=t3 - t2)
@@ -89,7 +91,10 @@ def main():
     ap.add_argument("--id-tol", type=float, default=1e-11)
     ap.add_argument("--ladder-ratio", type=float, default=2.0 ** (1.0 / 3.0))
     ap.add_argument("--ladder-id-tol", type=float, default=1e-10)
+    ap.add_argument("--radial", default="r2", choices=["r2", "r"])
+    ap.add_argument("--gpu-sketch", action="store_true")
     a = ap.parse_args()
+    from .residual import add_to_tables
     outdir = os.path.join(ROOT, "tables", "data")
     os.makedirs(outdir, exist_ok=True)
     if a.configs:
@@ -97,12 +102,15 @@ def main():
         from nc_inputs import CONFIGS
         for name, cfg in CONFIGS.items():
             d = build_tables(cfg.kind, cfg.eps, id_tol=a.id_tol, verbose=True, ladder_ratio=a.ladder_ratio,
-                             ladder_id_tol=a.ladder_id_tol)
+                             ladder_id_tol=a.ladder_id_tol, gpu_sketch=a.gpu_sketch, zn_radial=a.radial)
             save(d, os.path.join(outdir, f"{name}.npz"))
+            add_to_tables(os.path.join(outdir, f"{name}.npz"))
         return
     d = build_tables(a.kind, a.eps, id_tol=a.id_tol, verbose=True, ladder_ratio=a.ladder_ratio,
-                     ladder_id_tol=a.ladder_id_tol)
-    save(d, a.out or os.path.join(outdir, f"k{a.kind}_eps{a.eps:g}.npz"))
+                     ladder_id_tol=a.ladder_id_tol, gpu_sketch=a.gpu_sketch, zn_radial=a.radial)
+    path = a.out or os.path.join(outdir, f"k{a.kind}_eps{a.eps:g}.npz")
+    save(d, path)
+    add_to_tables(path)
 
 
 if __name__ == "__main__":

@@ -52,7 +52,22 @@ def q_eval(M: int, r, theta):
     return Q
 
 
-def sampling_grid(M: int, n_r: int | None = None, n_theta: int | None = None):
+def sampling_grid(M: int, n_r: int | None = None, n_theta: int | None = None, radial: str = "r"):
+    """radial = "r": n_r (default M+1) Gauss-Legendre radii in r with weight r (2M+2 angles by default: K* = 512 at
+    M = 15); radial = "r2": n_r (default (M+1)/2 rounded up) Gauss-Legendre nodes in s = r^2 (r dr = ds/2) with
+    2M+1 angles (K* = 8 x 31 = 248 at M = 15).  Both integrate every product of two basis functions
+    exactly (radial: R R' r is a polynomial of degree <= 2M+1 in r, or R R' of degree <= M in r^2; angular:
+    frequencies <= 2M), so P Q = I_K either way."""
+    if radial == "r2":
+        n_r = n_r or (M + 2) // 2
+        n_theta = n_theta or (2 * M + 1)
+        x, w = np.polynomial.legendre.leggauss(n_r)
+        r = np.sqrt(0.5 * (x + 1.0))
+        wr = 0.25 * w                     # int_0^1 f r dr = int_0^1 f ds / 2, ds = dx / 2
+        th = 2.0 * np.pi * np.arange(n_theta) / n_theta
+        R, TH = np.meshgrid(r, th, indexing="ij")
+        WR = np.broadcast_to(wr[:, None], R.shape)
+        return R.ravel(), TH.ravel(), WR.ravel() * (2.0 * np.pi / n_theta)
     n_r = n_r or (M + 1)
     n_theta = n_theta or (2 * M + 2)
     x, w = np.polynomial.legendre.leggauss(n_r)
@@ -64,9 +79,9 @@ def sampling_grid(M: int, n_r: int | None = None, n_theta: int | None = None):
     return R.ravel(), TH.ravel(), (WR * R).ravel() * (2.0 * np.pi / n_theta)
 
 
-def transform(M: int, n_r: int | None = None, n_theta: int | None = None):
+def transform(M: int, n_r: int | None = None, n_theta: int | None = None, radial: str = "r"):
     """Returns (r, theta, P) with P (K x Kstar): coefficients = P @ samples (the discrete Zernike transform)."""
-    r, th, w = sampling_grid(M, n_r, n_theta)
+    r, th, w = sampling_grid(M, n_r, n_theta, radial)
     Q = q_eval(M, r, th)
     P = (Q * w[:, None]).T
     return r, th, P

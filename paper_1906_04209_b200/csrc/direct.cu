@@ -485,8 +485,8 @@ void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const do
 // ------------------------------------------------------------------------------------------------
 // hierarchical mode: near-list sources evaluated directly at the target patch's Zernike nodes
 // ------------------------------------------------------------------------------------------------
-template <int KIND, int TPT, bool EX>
-__global__ void __launch_bounds__(kPairThreads) k_pairs_near(const double* __restrict__ tx,
+template <int KIND, int TPT, bool EX, int NT>
+__global__ void __launch_bounds__(NT) k_pairs_near(const double* __restrict__ tx,
                                                               const double* __restrict__ ty,
                                                               const double* __restrict__ tz, int Kstar,
                                                               const int32_t* __restrict__ work,  // local patch ids
@@ -505,14 +505,14 @@ __global__ void __launch_bounds__(kPairThreads) k_pairs_near(const double* __res
   else
     init_log_table(logtab, logsrc);
   auto green = [&](double q) { return EX ? green_exact_r<KIND>(q, xt.tb, xt.lim, xt.a2, xt.a3) : green_q<KIND>(q, logtab); };
-  const int tiles = (Kstar + kPairThreads * TPT - 1) / (kPairThreads * TPT);
+  const int tiles = (Kstar + NT * TPT - 1) / (NT * TPT);
   const int64_t i = work[blockIdx.x / tiles];           // local target patch
   const int tile = blockIdx.x % tiles;
   double x[TPT], y[TPT], z[TPT], acc[TPT];
   int64_t excl[TPT];
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
-    const int k = min(tile * kPairThreads * TPT + (int)threadIdx.x + u * kPairThreads, Kstar - 1);
+    const int k = min(tile * NT * TPT + (int)threadIdx.x + u * NT, Kstar - 1);
     const int64_t t = i * Kstar + k;
     x[u] = tx[t]; y[u] = ty[t]; z[u] = tz[t];
     excl[u] = -1;
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kPairThreads) k_pairs_near(const double* __res
   }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
-    const int k = tile * kPairThreads * TPT + (int)threadIdx.x + u * kPairThreads;
+    const int k = tile * NT * TPT + (int)threadIdx.x + u * NT;
     if (k < Kstar) udir[i * Kstar + k] = acc[u];
   }
 }
@@ -542,20 +542,25 @@ void launch_pairs_near(int kind, const double* tx, const double* ty, const doubl
   const int chp = stage_ldg() ? 0 : stage_patches(p);
   const bool ex = exact_table_on(xt);
   const size_t smem = (size_t)chp * p * sizeof(double4) + (ex ? (size_t)xt.n * sizeof(double) : 0);
-  const int tiles = (Kstar + kPairThreads * 2 - 1) / (kPairThreads * 2);
+  // one tile of NT x 2 nodes per target patch when K* <= 256 (the 248-node rule), else 256-thread tiles
+  const int nt = Kstar <= 256 ? 128 : kPairThreads;
+  const int tiles = (Kstar + nt * 2 - 1) / (nt * 2);
   const unsigned nb = (unsigned)(nwork * tiles);
-#define NC_LAUNCH(KD, EX)                                                                                           \
+#define NC_LAUNCH(KD, EX, NTT)                                                                                      \
   {                                                                                                                \
-    auto kern = k_pairs_near<KD, 2, EX>;                                                                           \
+    auto kern = k_pairs_near<KD, 2, EX, NTT>;                                                                      \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
-    kern<<<nb, kPairThreads, smem, s>>>(tx, ty, tz, Kstar, work, near_off, near, src4, p, chp, udir,                \
-                                        log_table_device(), xt.d, xt.n, xt.base);                                  \
+    kern<<<nb, NTT, smem, s>>>(tx, ty, tz, Kstar, work, near_off, near, src4, p, chp, udir, log_table_device(),     \
+                               xt.d, xt.n, xt.base);                                                               \
   }
+#define NC_LAUNCH_NT(KD, EX) \
+  if (nt == 128) NC_LAUNCH(KD, EX, 128) else NC_LAUNCH(KD, EX, kPairThreads)
   if (kind == NC_EXTERIOR) {
-    if (ex) NC_LAUNCH(1, true) else NC_LAUNCH(1, false)
+    if (ex) { NC_LAUNCH_NT(1, true) } else { NC_LAUNCH_NT(1, false) }
   } else {
-    if (ex) NC_LAUNCH(0, true) else NC_LAUNCH(0, false)
+    if (ex) { NC_LAUNCH_NT(0, true) } else { NC_LAUNCH_NT(0, false) }
   }
+#undef NC_LAUNCH_NT
 #undef NC_LAUNCH
 }
 

@@ -850,15 +850,16 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
                          const int32_t* gna, const int64_t* coff, const double* coef, const double* tx,
                          const double* ty, const double* tz, const double* udir, double* u, const uint8_t* gsep,
                          cudaStream_t s) {
-  const InterpVariant v = interp_variant();
+  InterpVariant v = interp_variant();
   (void)namax;
+  if (!getenv("NC_INTERP_VARIANT") && Ks <= 256) v = {128, 2, 0, 4};   // the 248-node rule: one 256-slot CTA per patch
   if (v.mb == 0 && nrmax > kAngNrMax) {   // the first pass leaves the grids with n_r > kAngNrMax to a second one
     int rc1 = NC_OK;
 #define NC_I(NT, NPT, MB, MINB)                                                                                  \
   if (rc1 == NC_OK && v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                \
     rc1 = launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, \
                                              udir, u, gsep, s);
-    NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6)
+    NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6) NC_I(128, 2, 0, 4)
 #undef NC_I
     if (rc1 != NC_OK) return rc1;
     return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir,
@@ -869,6 +870,7 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
     return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep, s);
   NC_I(128, 4, 1, 5) NC_I(128, 4, 1, 4) NC_I(128, 4, 1, 3) NC_I(128, 4, 1, 1) NC_I(256, 2, 1, 2) NC_I(128, 4, 2, 4)
   NC_I(256, 2, 2, 3) NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6)
+  NC_I(128, 2, 0, 4)
 #undef NC_I
   return launch_interp_t<256, 2, 0, 2>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
                                        s);
@@ -1645,7 +1647,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
     const int Mmax = H->namax / 2, cpairs = std::max(H->cmax / 2, 1);
     const size_t shm = (size_t)cpairs * sizeof(double2) + (size_t)H->nring * (Mmax + 1) * sizeof(double2) +
                        (size_t)H->nring * (2 * H->nrmax + 1) * sizeof(double);
-    auto kern = k_interp_sep<128, 4>;
+    auto kern = Ks <= 256 ? k_interp_sep<128, 2> : k_interp_sep<128, 4>;   // node slots >= K*
     if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     kern<<<(unsigned)H->nwork_sep, 128, shm, s>>>(H->L, rc, Ks, H->d_work_sep, H->d_pgl, H->d_gsep, H->d_ggrid0,
                                                    H->d_gR, H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->nring,

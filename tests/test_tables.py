@@ -96,7 +96,7 @@ def test_config_tables(name):
     from nc_inputs import CONFIGS
     tab = _load(name)
     cfg = CONFIGS[name]
-    assert tab.kind == cfg.kind and tab.eps == cfg.eps and tab.K == 136 and tab.Kstar == 512
+    assert tab.kind == cfg.kind and tab.eps == cfg.eps and tab.K == 136 and tab.Kstar == 248
     meta = eval(tab.meta["repr"], {"__builtins__": {}}) if tab.meta.get("repr", "").startswith("{") else {}
     if meta:
         assert meta["outgoing_rel_err"] < 1e-9        # eq:outgoingcompressed at ID tol 1e-11
