@@ -56,6 +56,9 @@ def load_fp64_peak():
     return best
 
 
+# SMSP-cycles per warp-pair of green_far_r's loop body in isolation (tools/pair_mix_bench.cu, profiles/r01o_pair_mix.txt)
+PAIR_MIX_CYCLES = 47.22
+
 # ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
 TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01o_ncu_full_pairs_grid.json"}
 
@@ -354,6 +357,14 @@ def main():
                                                "main loop of this build, 592 SMSPs at the sampled SM clock"}
         except Exception as e:  # pragma: no cover
             roof["issue_model"] = {"error": str(e)[:200]}
+    # the same instruction mix in isolation (sources in registers, no staging / barriers / partial warps), measured
+    # by tools/pair_mix_bench.cu on a B200: SMSP-cycles per warp-pair the hardware sustains for this loop body
+    if roof is not None and args.mode == "hier" and not os.environ.get("NC_GRID_VARIANT"):
+        clk_hz = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+        kc = pair_ms * 1e-3 * clk_hz * 148 * 4 / (pairs / 32.0)
+        roof["instruction_mix_bound"] = {"cycles_per_warp_pair_isolated": PAIR_MIX_CYCLES, "kernel_cycles_per_warp_pair": kc,
+                                         "frac": PAIR_MIX_CYCLES / kc, "source": "tools/pair_mix_bench.cu, "
+                                         "profiles/r01o_pair_mix.txt (best of 2-4 CTAs/SM)"}
     # NEXT-3: the off-surface field of the solution (nc_field, host points in / values out, synchronous) at 4096
     # points on a sphere inside (interior: radius 0.5) or outside (exterior: radius 2) the unit sphere
     field = None
