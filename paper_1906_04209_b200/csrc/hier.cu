@@ -860,6 +860,7 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
     rc1 = launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, \
                                              udir, u, gsep, s);
     NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6) NC_I(128, 2, 0, 4)
+    NC_I(128, 2, 0, 3) NC_I(256, 1, 0, 2) NC_I(256, 1, 0, 3)
 #undef NC_I
     if (rc1 != NC_OK) return rc1;
     return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir,
@@ -870,7 +871,7 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
     return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep, s);
   NC_I(128, 4, 1, 5) NC_I(128, 4, 1, 4) NC_I(128, 4, 1, 3) NC_I(128, 4, 1, 1) NC_I(256, 2, 1, 2) NC_I(128, 4, 2, 4)
   NC_I(256, 2, 2, 3) NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6)
-  NC_I(128, 2, 0, 4)
+  NC_I(128, 2, 0, 4) NC_I(128, 2, 0, 3) NC_I(256, 1, 0, 2) NC_I(256, 1, 0, 3)
 #undef NC_I
   return launch_interp_t<256, 2, 0, 2>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
                                        s);
