@@ -401,6 +401,31 @@ def main():
                     "ms": (time.perf_counter() - t0) * 1e3, "grid_points": int(tab.res_w.size),
                     "note": "eq:l2res on 16 seeded random patches (nc_residual); the one-patch tables' own residual "
                             "(eq:patcherrl2) at this eps bounds it from below"}
+    # the other BASELINE config with a direct mode, measured in the same run (secondary; not the headline metric):
+    # C2 (exterior, N = 1000) direct, physical tables, 3 warm-up + 5 timed matvecs with CUDA events
+    secondary = None
+    if world == 1 and solve is not None and args.config == "C5":
+        cfg2 = CONFIGS["C2"]
+        tab2 = make_tables(cfg2, args.tables)
+        h2 = nc.Handle(cfg2.kind, cfg2.centers(), cfg2.eps, tab2, mode=nc.NC_DIRECT)
+        x2 = torch.from_numpy(h2.to_internal(random_coeffs(cfg2.N, tab2.K, 2002))).cuda()
+        y2 = torch.empty_like(x2)
+        for _ in range(3):
+            h2.matvec(x2, y2)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            h2.matvec(x2, y2)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms2 = e0.elapsed_time(e1) / 5
+        st2 = h2.stats()
+        tf2 = st2["pairs_per_matvec"] * st2["pair_fp64_flops_direct"] / (ms2 * 1e-3) / 1e12
+        secondary = {"workload": "C2 direct", "value": 1e3 / ms2, "unit": "matvec/s", "ms_per_matvec": ms2,
+                     "pairs_per_matvec": st2["pairs_per_matvec"], "fp64_tflops_whole_matvec": tf2,
+                     "frac_of_dfma_peak": tf2 / peaks["dfma"] if peaks.get("dfma") else None}
+        h2.close()
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -426,7 +451,7 @@ def main():
                                          "hier_interp_terms", "hier_grid_points", "hier_grid_units", "hier_grid_fill",
                                          "hier_grid_warp_fill")}
                      if args.mode == "hier" else None),
-            "solve": solve, "field": field, "residual": residual}
+            "solve": solve, "field": field, "residual": residual, "secondary": secondary}
     print(json.dumps(line), flush=True)
     h.close()
     if world > 1:
