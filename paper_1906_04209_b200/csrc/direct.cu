@@ -29,16 +29,17 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_pairs_direct(const double* 
                                                                 const double* __restrict__ src4, int p, int64_t N,
                                                                 int nseg, int chp, double* __restrict__ upart,
                                                                 const double2* __restrict__ logsrc,
-                                                                const double2* __restrict__ xsrc, int xn, int xbase) {
+                                                                const double2* __restrict__ xsrc, int xn, int xbase,
+                                                                int xmid) {
   extern __shared__ double4 sm[];
   __shared__ double2 logtab[EX ? 1 : kLogTableSize];
   __shared__ int64_t pid[kStagePatchesMax];
   ExactTab xt{};
   if (EX)
-    xt = init_exact_table(KIND, reinterpret_cast<double2*>(sm + (size_t)chp * p), xsrc, xn, xbase);
+    xt = init_exact_table(KIND, reinterpret_cast<double2*>(sm + (size_t)chp * p), xsrc, xn, xbase, xmid);
   else
     init_log_table(logtab, logsrc);
-  auto green = [&](double q) { return EX ? green_exact_r<KIND>(q, xt.tb, xt.lim, xt.a2, xt.a3) : green_q<KIND>(q, logtab); };
+  auto green = [&](double q) { return EX ? green_exact_r<KIND>(q, xt.tb, xt.lim, xt.a2, xt.a3, xt.kmid) : green_q<KIND>(q, logtab); };
   double x[TPT], y[TPT], z[TPT], acc[TPT];
   int64_t excl[TPT];
   const int64_t t0 = (int64_t)blockIdx.x * kPairThreads * TPT + threadIdx.x;
@@ -98,7 +99,7 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
     auto kern = k_pairs_direct<KD, TP, EX>;                                                                        \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
     kern<<<grid, kPairThreads, smem, s>>>(tx, ty, tz, n_tgt, Kstar, tgt_patch0, src4, p, N, nseg, chp, upart,       \
-                                          log_table_device(), xt.d, xt.n, xt.base);                                \
+                                          log_table_device(), xt.d, xt.n, xt.base, 1 << 12);                       \
   }
   if (kind == NC_EXTERIOR) {
     if (ex) { if (tpt == 2) NC_LAUNCH(1, 2, true) else NC_LAUNCH(1, 1, true) }
@@ -122,7 +123,7 @@ __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const 
                                           const int32_t* __restrict__ srclist, const double* __restrict__ src4,
                                           int stage_records, double* __restrict__ part, double4* __restrict__ sm,
                                           int64_t* __restrict__ pid, const double2* __restrict__ logtab,
-                                          unsigned ftb, int flim, double fa2, double fa3) {
+                                          unsigned ftb, int flim, double fa2, double fa3, int fmid) {
   double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
   // adjacent points per thread (l = TPT t + u): a partial chunk leaves at most one partially idle warp.  A warp whose
   // share of the chunk is <= 32 points (the chunk's tail) takes one point per lane instead (`single`), halving the
@@ -145,13 +146,13 @@ __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const 
   if (ASYNC) {
     accumulate_grid_async<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc, lst, s4, U.p, sm, stage_records,
                                                            reinterpret_cast<int32_t*>(pid), logtab, any, single, ftb,
-                                                           flim, fa2, fa3);
+                                                           flim, fa2, fa3, fmid);
   } else {
     int chp = stage_records / U.p;
     chp = chp < 1 ? 1 : (chp > kStagePatchesMax ? kStagePatchesMax : chp);
     accumulate_grid<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc,
                                                      [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p,
-                                                     sm, pid, chp, logtab, any, single, ftb, flim, fa2, fa3);
+                                                     sm, pid, chp, logtab, any, single, ftb, flim, fa2, fa3, fmid);
   }
   const int upts = NT * TPT;
   if (single) {
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
                                                    const double* __restrict__ src4, int stage_records,
                                                    double* __restrict__ part, const double2* __restrict__ logsrc,
                                                    int* __restrict__ counter, int64_t nunits,
-                                                   const double2* __restrict__ fsrc, int fn, int fbase) {
+                                                   const double2* __restrict__ fsrc, int fn, int fbase, int fmid) {
   extern __shared__ double4 sm[];
   __shared__ double2 logtab[FAR >= 2 ? 1 : kLogTableSize];
   __shared__ int64_t pid[ASYNC ? 16 : kStagePatchesMax];   // async: the unit's <= 32 source patches (int32)
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
   if (!counter) {
     __syncthreads();
     grid_unit<KIND, NT, TPT, UNROLL, FAR, ASYNC>(units[blockIdx.x], blockIdx.x, gx, gy, gz, srclist, src4, stage_records, part,
-                                          sm, pid, logtab, tb, flim, fa2, fa3);
+                                          sm, pid, logtab, tb, flim, fa2, fa3, fmid);
     return;
   }
   for (;;) {
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
     const int u = next;
     if (u >= nunits) break;
     grid_unit<KIND, NT, TPT, UNROLL, FAR, ASYNC>(units[u], u, gx, gy, gz, srclist, src4, stage_records, part, sm, pid, logtab,
-                                          tb, flim, fa2, fa3);
+                                          tb, flim, fa2, fa3, fmid);
   }
 }
 
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
                                                           const double* __restrict__ src4, int wrec,
                                                           double* __restrict__ part, const double2* __restrict__ fsrc,
                                                           int fn, int fbase, int* __restrict__ counter,
-                                                          int64_t nunits) {
+                                                          int64_t nunits, int fmid) {
   static_assert(FAR >= 2, "warp-level grid kernel: exponent-indexed far table only");
   extern __shared__ double4 sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
       __syncwarp();
       accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, buf + (size_t)(c & 1) * wrec,
                                               min(wrec, ntot - c * wrec), single, (const double2*)nullptr, tb, flim,
-                                              fa2, fa3);
+                                              fa2, fa3, fmid);
       __syncwarp();
     }
     if (single) {
@@ -421,7 +422,7 @@ static void launch_grid_w(const GridUnit* units, int64_t nunits, const double* g
   const int64_t ctas = std::min<int64_t>((int64_t)std::max(1, per) * sms, (nunits + WPC - 1) / WPC);
   cudaMemsetAsync(counter, 0, sizeof(int), s);
   kern<<<(unsigned)ctas, 32 * WPC, smem, s>>>(units, gx, gy, gz, srclist, src4, wrec, part, ft.d, ft.n, ft.base,
-                                              counter, nunits);
+                                              counter, nunits, 1 << (19 - far_table_bits(FAR)));
 }
 
 template <int KIND, int NT, int TPT, int UNROLL, int FAR, int TMA, int MINB>
@@ -440,7 +441,7 @@ static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* g
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (!persist) {
     kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device(), nullptr,
-                                            nunits, ft.d, ft.n, ft.base);
+                                            nunits, ft.d, ft.n, ft.base, 1 << (19 - far_table_bits(FAR)));
     return;
   }
   // persistent: one wave of CTAs (resident blocks per SM x SMs), units from the handle's atomic counter
@@ -452,7 +453,7 @@ static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* g
   cudaMemsetAsync(counter, 0, sizeof(int), s);
   kern<<<(unsigned)std::min<int64_t>(ctas, nunits), NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part,
                                                                    log_table_device(), counter, nunits, ft.d, ft.n,
-                                                                   ft.base);
+                                                                   ft.base, 1 << (19 - far_table_bits(FAR)));
 }
 
 void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
@@ -495,16 +496,17 @@ __global__ void __launch_bounds__(NT) k_pairs_near(const double* __restrict__ tx
                                                               const double* __restrict__ src4, int p, int chp,
                                                               double* __restrict__ udir,
                                                               const double2* __restrict__ logsrc,
-                                                              const double2* __restrict__ xsrc, int xn, int xbase) {
+                                                              const double2* __restrict__ xsrc, int xn, int xbase,
+                                                              int xmid) {
   extern __shared__ double4 sm[];
   __shared__ double2 logtab[EX ? 1 : kLogTableSize];
   __shared__ int64_t pid[kStagePatchesMax];
   ExactTab xt{};
   if (EX)
-    xt = init_exact_table(KIND, reinterpret_cast<double2*>(sm + (size_t)chp * p), xsrc, xn, xbase);
+    xt = init_exact_table(KIND, reinterpret_cast<double2*>(sm + (size_t)chp * p), xsrc, xn, xbase, xmid);
   else
     init_log_table(logtab, logsrc);
-  auto green = [&](double q) { return EX ? green_exact_r<KIND>(q, xt.tb, xt.lim, xt.a2, xt.a3) : green_q<KIND>(q, logtab); };
+  auto green = [&](double q) { return EX ? green_exact_r<KIND>(q, xt.tb, xt.lim, xt.a2, xt.a3, xt.kmid) : green_q<KIND>(q, logtab); };
   const int tiles = (Kstar + NT * TPT - 1) / (NT * TPT);
   const int64_t i = work[blockIdx.x / tiles];           // local target patch
   const int tile = blockIdx.x % tiles;
@@ -551,7 +553,7 @@ void launch_pairs_near(int kind, const double* tx, const double* ty, const doubl
     auto kern = k_pairs_near<KD, 2, EX, NTT>;                                                                      \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
     kern<<<nb, NTT, smem, s>>>(tx, ty, tz, Kstar, work, near_off, near, src4, p, chp, udir, log_table_device(),     \
-                               xt.d, xt.n, xt.base);                                                               \
+                               xt.d, xt.n, xt.base, 1 << 12);                                                      \
   }
 #define NC_LAUNCH_NT(KD, EX) \
   if (nt == 128) NC_LAUNCH(KD, EX, 128) else NC_LAUNCH(KD, EX, kPairThreads)

@@ -185,15 +185,17 @@ template <int FB>
 __device__ __forceinline__ double far_mid(int hx) {   // the bin midpoint of x (high word only; low word 0)
   return __hiloint2double((hx & ~((1 << (20 - FB)) - 1)) | (1 << (19 - FB)), 0);
 }
+// kmid = 1 << (19 - FB), passed in at run time: the midpoint is then one LOP3 (x & ~mask) | kmid with kmid in a
+// register, not two with two immediates
 template <int KIND, int FB, int DEG>
-__device__ __forceinline__ double green_far_r(double qh, unsigned tbase, int lim, double a2r, double a3r) {
+__device__ __forceinline__ double green_far_r(double qh, unsigned tbase, int lim, double a2r, double a3r, int kmid) {
   const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
   const double t = qh * y;
   const double e = fma(-t, y, 0.5);
   const double w = fma(y, e, y);
   const double x = (KIND == 1) ? 1.0 + w : fma(qh, w, qh);
   const int hx = __double2hiint(x);
-  const double c = rcp_approx(far_mid<FB>(hx));
+  const double c = rcp_approx(__hiloint2double((hx & ~((1 << (20 - FB)) - 1)) | kmid, 0));
   int ix = hx >> (20 - FB);
   ix = (KIND == 1) ? min(ix, lim) : max(ix, lim);
   double lj;
@@ -216,11 +218,11 @@ __device__ __forceinline__ double green_far_r(double qh, unsigned tbase, int lim
 // r = x c - 1 and the quartic minimax log1p of FB = 7 (absolute error 6.3e-14): 20 FP64 instructions per pair with
 // the caller's distance and accumulate, and an 8-byte table read instead of the 16-byte (c_j, -log c_j) one.
 template <int KIND>
-__device__ __forceinline__ double green_exact_r(double q, unsigned tbase, int lim, double a2r, double a3r) {
+__device__ __forceinline__ double green_exact_r(double q, unsigned tbase, int lim, double a2r, double a3r, int kmid) {
   const double w = fast_rsqrt(q);
   const double x = (KIND == 1) ? 1.0 + w : fma(q, w, q);
   const int hx = __double2hiint(x);
-  const double c = rcp_approx(far_mid<7>(hx));
+  const double c = rcp_approx(__hiloint2double((hx & ~((1 << 13) - 1)) | kmid, 0));   // kmid = 1 << 12 (run time)
   int ix = hx >> 13;
   ix = (KIND == 1) ? min(ix, lim) : max(ix, lim);
   double lj;
@@ -237,11 +239,12 @@ struct ExactTab {
   unsigned tb;
   int lim;
   double a2, a3;
+  int kmid;   // the bin-midpoint bit 1 << 12, a run-time value (one LOP3 per pair, see green_far_r)
 };
 // Call with all threads of the CTA (then __syncthreads()): copies the n L entries (n / 2 double2) into smem and
 // returns the kernel-side handle.  src[n / 2] holds (a2, a3).
 __device__ __forceinline__ ExactTab init_exact_table(int kind, double2* smem, const double2* __restrict__ src, int n,
-                                                     int base) {
+                                                     int base, int kmid) {
   for (int j = threadIdx.x; j < n / 2; j += blockDim.x) smem[j] = src[j];
   const double2 cst = __ldg(src + n / 2);
   ExactTab t;
@@ -249,6 +252,7 @@ __device__ __forceinline__ ExactTab init_exact_table(int kind, double2* smem, co
   t.lim = kind == 1 ? base + n - 1 : base;
   t.a2 = cst.x;
   t.a3 = cst.y;
+  t.kmid = kmid;
   return t;
 }
 

@@ -95,13 +95,13 @@ inline void far_poly(int far, double* a2, double* a3) {   // the polynomial cons
 }
 template <int KIND, int FAR>
 __device__ __forceinline__ double green_far_any(double qh, const double2* __restrict__ logtab, unsigned tbase,
-                                                int lim, double a2, double a3) {
+                                                int lim, double a2, double a3, int kmid) {
   if (FAR == 1) return green_far_h<KIND>(qh, logtab);
   if (FAR == 2) return green_far_t<KIND, 7, 3>(qh, tbase, lim, a2, a3);
   if (FAR == 3) return green_far_t<KIND, 7, 4>(qh, tbase, lim, a2, a3);
   if (FAR == 4) return green_far_t<KIND, 8, 3>(qh, tbase, lim, a2, a3);
-  if (FAR == 5) return green_far_r<KIND, 7, 3>(qh, tbase, lim, a2, a3);
-  return green_far_r<KIND, 6, 4>(qh, tbase, lim, a2, a3);
+  if (FAR == 5) return green_far_r<KIND, 7, 3>(qh, tbase, lim, a2, a3, kmid);
+  return green_far_r<KIND, 6, 4>(qh, tbase, lim, a2, a3, kmid);
 }
 
 // the records [0, nrec) of a staged chunk against the thread's targets (incoming-grid sums, no self exclusion)
@@ -110,14 +110,14 @@ __device__ __forceinline__ void accumulate_span(const double (&x)[TPT], const do
                                                 const double (&cq)[TPT], double (&acc)[TPT],
                                                 const double4* __restrict__ sm, int nrec, bool single,
                                                 const Tab* __restrict__ logtab, unsigned ftb, int flim, double fa2,
-                                                double fa3) {
+                                                double fa3, int fmid = 0) {
   if (single) {   // warp-uniform: a tail warp with <= 32 points evaluates one target per lane
 #pragma unroll UNROLL
     for (int m = 0; m < nrec; ++m) {
       const double4 s = sm[m];
       if (FAR) {
         const double qh = fma(x[0], s.x, fma(y[0], s.y, fma(z[0], s.z, cq[0])));
-        acc[0] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3), acc[0]);
+        acc[0] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3, fmid), acc[0]);
       } else {
         const double dx = x[0] - s.x, dy = y[0] - s.y, dz = z[0] - s.z;
         const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
@@ -133,7 +133,7 @@ __device__ __forceinline__ void accumulate_span(const double (&x)[TPT], const do
     for (int u = 0; u < TPT; ++u) {
       if (FAR) {
         const double qh = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
-        acc[u] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3), acc[u]);
+        acc[u] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3, fmid), acc[u]);
       } else {
         const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
         const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
@@ -150,7 +150,7 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
                                                 double4* __restrict__ sm, int64_t* __restrict__ sm_pid, int chp,
                                                 const Tab* __restrict__ logtab, bool active,
                                                 bool single = false, unsigned ftb = 0, int flim = 0,
-                                                double fa2 = 0.0, double fa3 = 0.0) {
+                                                double fa2 = 0.0, double fa3 = 0.0, int fmid = 0) {
   for (int64_t c0 = 0; c0 < nlist; c0 += chp) {
     const int nch = (int)min((int64_t)chp, nlist - c0);
     __syncthreads();
@@ -162,7 +162,7 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
     }
     __syncthreads();
     if (!active) continue;
-    accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, sm, nch * p, single, logtab, ftb, flim, fa2, fa3);
+    accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, sm, nch * p, single, logtab, ftb, flim, fa2, fa3, fmid);
   }
 }
 
@@ -184,7 +184,7 @@ __device__ __forceinline__ void accumulate_grid_async(const double (&x)[TPT], co
                                                       const double4* __restrict__ s4, int p,
                                                       double4* __restrict__ bufs, int brec, int32_t* __restrict__ slst,
                                                       const Tab* __restrict__ logtab, bool active, bool single,
-                                                      unsigned ftb, int flim, double fa2, double fa3) {
+                                                      unsigned ftb, int flim, double fa2, double fa3, int fmid) {
   __syncthreads();   // the previous unit is done with slst and the buffers
   if ((int)threadIdx.x < nsrc) slst[threadIdx.x] = lst[threadIdx.x];
   __syncthreads();
@@ -212,7 +212,7 @@ __device__ __forceinline__ void accumulate_grid_async(const double (&x)[TPT], co
     if (active)
       accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, bufs + (size_t)(c & 1) * brec,
                                               (min(nsrc, (c + 1) * chp) - c * chp) * p, single, logtab, ftb, flim,
-                                              fa2, fa3);
+                                              fa2, fa3, fmid);
     __syncthreads();   // every thread is done with buffer c & 1 before chunk c + 2 overwrites it
   }
 }
