@@ -222,6 +222,16 @@ int nc_density(nc_handle* h, const double* x_all, int n_sel, const int64_t* patc
 int nc_id_sketch(int kind, int device, int64_t n_train, const double* train, int64_t n_fine, const double* fine,
                  int l, const double* omega, double* Y);
 
+/* Step-1 table build, GPU part (NEXT-1): the modal kernels of the one-patch solver (§8.2;
+ * nc_tables/kernel.py modal), G_m(t, t') = (1/pi) int_0^pi G(d) cos(m phi) dphi for m = 0..M at npairs (t, t')
+ * pairs, d^2 = 4 sin^2((t - t')/2) + 4 sin t sin t' sin^2(phi/2), by the caller's phi rule:
+ *   t, tp  host, npairs radii (geodesic, in [0, pi]);  phi, wphi  host, nphi nodes and weights on [0, pi]
+ *   out    host, npairs x (M+1) row-major (output)
+ * The integrand matrix is generated in HBM (npairs x nphi) and contracted with the cosine weights by one fp64
+ * tensor-core GEMM.  Synchronous.  Errors: NC_EINVAL, NC_ENOMEM, NC_ECUDA. */
+int nc_modal_kernels(int kind, int device, int64_t npairs, const double* t, const double* tp, int M, int nphi,
+                     const double* phi, const double* wphi, double* out);
+
 /* Counters and the last matvec's per-stage device times.  nc_time_stages(h, 1) makes the next
  * matvecs record per-stage CUDA events on the matvec's stream (no host synchronisation inside nc_matvec);
  * nc_stats waits for the last recorded matvec's events and converts them to ms_last. */

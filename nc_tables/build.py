@@ -28,12 +28,13 @@ def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20
                  ladder_id_tol: float | None = 1e-10, gpu_sketch: bool = False, zn_radial: str = "r2"):
     """gpu_sketch: form the ID sketches on the GPU (nc_id_sketch, NEXT-1) instead of numpy.  zn_radial: the Zernike
     sampling rule, "r2" (default: 8 Gauss nodes in r^2 x 31 angles, K* = 248, R7) or "r" (16 x 32 = 512)."""
-    sk = None
-    if gpu_sketch:
+    sk, mf = None, None
+    if gpu_sketch:   # the GPU parts of Step 1 (NEXT-1): ID sketches and the one-patch solver's modal kernels
         import paper_1906_04209_b200 as ncgpu
-        sk = ncgpu.id_sketch
+        from .kernel import modal_gpu
+        sk, mf = ncgpu.id_sketch, modal_gpu
     t0 = time.time()
-    op = solve_onepatch(kind, eps, M, npan, k, n_theta)
+    op = solve_onepatch(kind, eps, M, npan, k, n_theta, modal_fn=mf)
     t1 = time.time()
     fine, wf, B = fine_grid(op)
     train = training_grid(eps)
@@ -51,16 +52,28 @@ def build_tables(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20
     lad_r, lad_p, lad_s, lad_T, lad_err = [], [], [], [], []
     if ladder:
         rung = 1
+        inners = []
         while 2.0 * eps * ladder_ratio ** rung < ladder_max:
-            inner = 2.0 * ladder_ratio ** rung
+            inners.append(2.0 * ladder_ratio ** rung)
+            rung += 1
+
+        def one_rung(inner):
             Jk, Pik = interp_decomp(kind, training_grid(eps, inner=inner), fine, ladder_id_tol or id_tol, sketch=sk)
             Tk = Pik @ (wf[:, None] * B)
+            return Jk, Tk, outgoing_error(kind, fine, wf, B, fine[Jk], Tk, eps, inner=inner)
+
+        if sk is not None:   # GPU sketches: the host QRs of the rungs run concurrently (LAPACK releases the GIL)
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+                results = list(ex.map(one_rung, inners))
+        else:
+            results = [one_rung(inner) for inner in inners]
+        for inner, (Jk, Tk, ek) in zip(inners, results):
             lad_r.append(inner * eps)
             lad_p.append(len(Jk))
             lad_s.append(fine[Jk])
             lad_T.append(Tk)
-            lad_err.append(outgoing_error(kind, fine, wf, B, fine[Jk], Tk, eps, inner=inner))
-            rung += 1
+            lad_err.append(ek)
     t3 = time.time()
     meta = dict(kind=kind, eps=eps, M=M, npan=npan, k=k, n_theta=n_theta, id_tol=id_tol, p=len(J), n_f=len(wf),
                 zn_radial=zn_radial, Kstar=len(r),

@@ -55,3 +55,10 @@ def modal(kind: int, t, tp, M: int, chunk: int = 4096):
         d = np.sqrt(A[:, None] + B[:, None] * s2[None, :])
         out[a:b] = green_d(kind, d) @ C
     return out
+
+
+def modal_gpu(kind: int, t, tp, M: int):
+    """kernel.modal on the GPU (nc_modal_kernels, NEXT-1) with the same phi rule."""
+    import paper_1906_04209_b200 as nc
+    phi, wphi = phi_rule()
+    return nc.modal_kernels(kind, t, tp, M, phi, wphi)

@@ -79,14 +79,21 @@ def _row_rules(g: RadialGrid, ti: float):
     return out
 
 
-def modal_matrices(kind: int, g: RadialGrid, M: int):
-    """A_m (n x n) for m = 0..M: rows = collocation radii, columns = nodal unknowns (sigma or g values)."""
+def modal_matrices(kind: int, g: RadialGrid, M: int, modal_fn=None):
+    """A_m (n x n) for m = 0..M: rows = collocation radii, columns = nodal unknowns (sigma or g values).
+    ``modal_fn(kind, t, tp, M)``: the modal-kernel evaluator for all rows' quadrature pairs at once (default the
+    numpy kernel.modal; the GPU one is paper_1906_04209_b200.modal_kernels with the same phi rule, NEXT-1)."""
     n = g.t.size
     A = np.zeros((M + 1, n, n))
+    rules_all = [_row_rules(g, ti) for ti in g.t]
+    tq_all = [np.concatenate([r[0] for r in rules]) for rules in rules_all]
+    T = np.concatenate([np.full(tq.size, ti) for ti, tq in zip(g.t, tq_all)])
+    TQ = np.concatenate(tq_all)
+    G_all = (modal_fn or modal)(kind, T, TQ, M)                # (sum nq, M+1)
+    row0 = np.concatenate([[0], np.cumsum([tq.size for tq in tq_all])])
     for i, ti in enumerate(g.t):
-        rules = _row_rules(g, ti)
-        tq = np.concatenate([r[0] for r in rules])
-        Gm = modal(kind, np.full(tq.size, ti), tq, M)          # (nq, M+1)
+        rules = rules_all[i]
+        Gm = G_all[row0[i]:row0[i + 1]]                         # (nq, M+1)
         off = 0
         for pi, (tqp, wt, L) in enumerate(rules):
             sl = slice(off, off + tqp.size)
@@ -109,10 +116,10 @@ class OnePatch:
 
 
 def solve_onepatch(kind: int, eps: float, M: int = 15, npan: int = 13, k: int = 20, n_theta: int | None = None,
-                   A=None) -> OnePatch:
+                   A=None, modal_fn=None) -> OnePatch:
     g = radial_grid(eps, npan, k)
     if A is None:
-        A = modal_matrices(kind, g, M)
+        A = modal_matrices(kind, g, M, modal_fn)
     idx = zernike.basis_indices(M)
     sig = np.zeros((len(idx), g.t.size))
     last = g.panel == g.npan - 1

@@ -58,7 +58,7 @@ class NcStats(ctypes.Structure):
 
 
 EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt",
-           "nc_field", "nc_residual", "nc_density", "nc_id_sketch", "nc_stats",
+           "nc_field", "nc_residual", "nc_density", "nc_id_sketch", "nc_modal_kernels", "nc_stats",
            "nc_time_stages", "nc_tree_lists", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
 
 _lib = None
@@ -84,6 +84,8 @@ def load_library(path: str = LIB_PATH):
     L.nc_field.argtypes = [vp, vp, ctypes.c_int64, _dp, _dp, _dp]
     L.nc_residual.argtypes = [vp, vp, ctypes.c_int, _i64p, ctypes.c_int, _dp, _dp, _dp, _dp, _dp]
     L.nc_density.argtypes = [vp, vp, ctypes.c_int, _i64p, ctypes.c_int, _dp, _dp]
+    L.nc_modal_kernels.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, _dp, _dp, ctypes.c_int, ctypes.c_int,
+                                   _dp, _dp, _dp]
     L.nc_id_sketch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, _dp, ctypes.c_int64, _dp, ctypes.c_int, _dp,
                                _dp]
     L.nc_stats.argtypes = [vp, ctypes.POINTER(NcStats)]
@@ -134,6 +136,19 @@ def id_sketch(kind: int, train, fine, omega, device: int = 0) -> np.ndarray:
     _check(L.nc_id_sketch(int(kind), int(device), len(tr), tr.ctypes.data_as(_dp), len(fi), fi.ctypes.data_as(_dp),
                           om.shape[0], om.ctypes.data_as(_dp), Y.ctypes.data_as(_dp)))
     return Y
+
+
+def modal_kernels(kind: int, t, tp, M: int, phi, wphi, device: int = 0) -> np.ndarray:
+    """G_m(t, t') for m = 0..M at paired radii on the GPU (nc_modal_kernels): the one-patch solver's modal kernels."""
+    L = load_library()
+    t = np.ascontiguousarray(t, dtype=np.float64).ravel()
+    tp = np.ascontiguousarray(tp, dtype=np.float64).ravel()
+    ph = np.ascontiguousarray(phi, dtype=np.float64)
+    wp = np.ascontiguousarray(wphi, dtype=np.float64)
+    out = np.empty((t.size, M + 1))
+    _check(L.nc_modal_kernels(int(kind), int(device), t.size, t.ctypes.data_as(_dp), tp.ctypes.data_as(_dp), int(M),
+                              ph.size, ph.ctypes.data_as(_dp), wp.ctypes.data_as(_dp), out.ctypes.data_as(_dp)))
+    return out
 
 
 def _ptr(t):

@@ -34,3 +34,29 @@ def test_id_sketch_argument_checks():
     import paper_1906_04209_b200 as nc
     with pytest.raises(nc.NcError, match="NC_EINVAL"):
         nc.id_sketch(2, np.zeros((3, 3)), np.ones((2, 3)), np.ones((1, 3)))
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_modal_kernels_match_cpu(kind):
+    """The one-patch solver's modal kernels G_m(t, t') on the GPU against kernel.modal (numpy),
+    including the nearly singular t ~ t' pairs the solver's graded rules produce."""
+    import paper_1906_04209_b200 as nc
+    from nc_tables.kernel import modal, phi_rule
+    from nc_tables.onepatch import _row_rules, radial_grid
+    g = radial_grid(0.02, 8, 10)
+    ti = g.t[[0, 20, 55, 79]]
+    tq = [np.concatenate([r[0] for r in _row_rules(g, t)]) for t in ti]
+    T = np.concatenate([np.full(q.size, t) for t, q in zip(ti, tq)])
+    TQ = np.concatenate(tq)
+    phi, wphi = phi_rule()
+    Gg = nc.modal_kernels(kind, T, TQ, 15, phi, wphi)
+    Gc = modal(kind, T, TQ, 15)
+    assert np.max(np.abs(Gg - Gc) / (np.abs(Gc) + np.max(np.abs(Gc), axis=1, keepdims=True))) <= 1e-13
+
+
+def test_onepatch_gpu_modal_same_solution():
+    from nc_tables import onepatch
+    from nc_tables.kernel import modal_gpu
+    a = onepatch.solve_onepatch(0, 0.05, M=8, npan=8, k=10)
+    b = onepatch.solve_onepatch(0, 0.05, M=8, npan=8, k=10, modal_fn=modal_gpu)
+    assert np.max(np.abs(a.sigma_radial - b.sigma_radial)) <= 1e-11 * np.max(np.abs(a.sigma_radial))
