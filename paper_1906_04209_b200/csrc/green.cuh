@@ -181,10 +181,6 @@ __device__ __forceinline__ double rcp_approx(double x) {
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   return y;
 }
-template <int FB>
-__device__ __forceinline__ double far_mid(int hx) {   // the bin midpoint of x (high word only; low word 0)
-  return __hiloint2double((hx & ~((1 << (20 - FB)) - 1)) | (1 << (19 - FB)), 0);
-}
 // kmid = 1 << (19 - FB), passed in at run time: the midpoint is then one LOP3 (x & ~mask) | kmid with kmid in a
 // register, not two with two immediates
 template <int KIND, int FB, int DEG>
