@@ -66,6 +66,10 @@ struct HierState {
   std::vector<int64_t> ggrid0;      // G+1: grids of group g are [ggrid0[g], ggrid0[g+1])
   std::vector<int32_t> gnr, gna, grid_group;
   std::vector<int64_t> goff, coff;  // ngrids+1 point / coefficient offsets (0-sized for other ranks' groups)
+  std::vector<int64_t> rbase;       // ngrids+1: grid k's ring offsets are roff[rbase[k] .. rbase[k] + n_r]
+  std::vector<int32_t> roff;        // per local grid: n_r + 1 point offsets of its rings (ring-adaptive, R26b)
+  int64_t* d_rbase = nullptr;
+  int32_t* d_roff = nullptr;
   int64_t Q = 0, C = 0;
   int qmax = 0, cmax = 0, pmax = 0, namax = 0, nrmax = 0, cgroupmax = 0;
   std::vector<int32_t> grid_ids;    // grids with points on this rank
@@ -377,15 +381,19 @@ __global__ void k_single_frames(const int32_t* __restrict__ gfirst, const int32_
 __global__ void k_grid_points(const int32_t* __restrict__ grids, int64_t ngr, const int32_t* __restrict__ grid_group,
                               const double* __restrict__ F, const double* __restrict__ gR,
                               const int32_t* __restrict__ gnr, const int32_t* __restrict__ gna,
-                              const int64_t* __restrict__ goff, double* gx, double* gy, double* gz) {
+                              const int64_t* __restrict__ goff, const int64_t* __restrict__ rbase,
+                              const int32_t* __restrict__ roff, double* gx, double* gy, double* gz) {
   const int64_t gi = blockIdx.x;
   if (gi >= ngr) return;
   const int k = grids[gi];
   const int g = grid_group[k];
-  const int nr = gnr[k], na = gna[k];
+  const int nr = gnr[k];
+  const int32_t* ro = roff + rbase[k];   // ring kr holds points [ro[kr], ro[kr + 1]) (R26b: ring-adaptive)
   const double* r9 = F + 9 * (int64_t)g;
-  for (int t = threadIdx.x; t < nr * na; t += blockDim.x) {
-    const int kr = t / na, l = t % na;
+  for (int t = threadIdx.x; t < ro[nr]; t += blockDim.x) {
+    int kr = 0;
+    while (t >= ro[kr + 1]) ++kr;
+    const int na = ro[kr + 1] - ro[kr], l = t - ro[kr];
     const double r = gR[g] * cospi((kr + 0.5) / (2.0 * nr));
     double st, ct, sr, cr;
     sincospi(2.0 * l / na, &st, &ct);
@@ -410,39 +418,52 @@ __global__ void k_reduce_chunks(const ChunkRec* __restrict__ ch, int64_t nch, co
   }
 }
 
-// step 4a: samples f(r_k, theta_l) (n_r x n_a, radius-major) -> parity-restricted
-// Chebyshev-Fourier coefficients c[m][j][cs], layout ((m * n_r + j) * 2 + cs), n = (m & 1) + 2 j:
-//   Fourier:   AB[k][m][cs] = (2 - delta) / n_a  sum_l f(r_k, theta_l) {cos, sin}(2 pi m l / n_a)
+// step 4a: samples f(r_k, theta_l) (ring k: n_a(k) equispaced angles, radius-major) ->
+// parity-restricted Chebyshev-Fourier coefficients c[m][j][cs], layout ((m * n_r + j) * 2 + cs), n = (m & 1) + 2 j:
+//   Fourier:   AB[k][m][cs] = (2 - delta) / n_a(k) sum_l f(r_k, theta_l) {cos, sin}(2 pi m l / n_a(k)),  2m <= n_a(k);
+//              0 for the orders ring k does not resolve (their amplitude there is below the grid tolerance, R26b)
 //   Chebyshev: c[m][j][cs]  = (2 - delta_n0) / n_r sum_k AB[k][m][cs] cos(n pi (2k + 1) / (4 n_r))
-// Twiddles are tabulated once per group in shared memory (exact index reduction, no per-term sincos).
+// Twiddles are tabulated per ring in shared memory (exact index reduction, no per-term sincos).
 __global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, const int32_t* __restrict__ gnr,
                             const int32_t* __restrict__ gna, const int64_t* __restrict__ goff,
-                            const int64_t* __restrict__ coff, const double* __restrict__ gval,
+                            const int64_t* __restrict__ coff, const int64_t* __restrict__ rbase,
+                            const int32_t* __restrict__ roff, const double* __restrict__ gval,
                             double* __restrict__ coef) {
   extern __shared__ double sh[];
   const int g = grids[blockIdx.x];   // grid id
-  const int nr = gnr[g], na = gna[g], M = na / 2;
-  double* f = sh;                      // nr * na
-  double* AB = f + nr * na;            // nr * (M+1) * 2
-  double* tw = AB + nr * (M + 1) * 2;  // 2 * na: (cos, sin)(2 pi r / na)
-  double* ch = tw + 2 * na;            // 8 * nr: cos(pi r / (4 nr))
-  for (int t = threadIdx.x; t < nr * na; t += blockDim.x) f[t] = gval[goff[g] + t];
-  for (int t = threadIdx.x; t < na; t += blockDim.x) sincospi(2.0 * t / na, &tw[2 * t + 1], &tw[2 * t]);
+  const int nr = gnr[g], M = gna[g] / 2;
+  const int32_t* ro = roff + rbase[g];
+  const int q = ro[nr];
+  double* f = sh;                      // q samples
+  double* AB = f + q;                  // nr * (M+1) * 2
+  double* tw = AB + nr * (M + 1) * 2;  // 2 q: ring k's (cos, sin)(2 pi r / n_a(k)) at 2 (ro[k] + r)
+  double* ch = tw + 2 * q;             // 8 * nr: cos(pi r / (4 nr))
+  for (int t = threadIdx.x; t < q; t += blockDim.x) {
+    f[t] = gval[goff[g] + t];
+    int kr = 0;
+    while (t >= ro[kr + 1]) ++kr;
+    sincospi(2.0 * (t - ro[kr]) / (ro[kr + 1] - ro[kr]), &tw[2 * t + 1], &tw[2 * t]);
+  }
   for (int t = threadIdx.x; t < 8 * nr; t += blockDim.x) ch[t] = cospi((double)t / (4.0 * nr));
   __syncthreads();
   for (int t = threadIdx.x; t < nr * (M + 1) * 2; t += blockDim.x) {
     const int k = t / ((M + 1) * 2), rem = t % ((M + 1) * 2), m = rem >> 1, cs = rem & 1;
-    const double* fk = f + k * na;
+    const int na = ro[k + 1] - ro[k];
     double s = 0.0;
-    int r = 0;
-    for (int l = 0; l < na; ++l) {
-      s = fma(fk[l], tw[2 * r + cs], s);
-      r += m;
-      if (r >= na) r -= na;
+    if (2 * m <= na) {
+      const double* fk = f + ro[k];
+      const double* twk = tw + 2 * ro[k];
+      int r = 0;
+      for (int l = 0; l < na; ++l) {
+        s = fma(fk[l], twk[2 * r + cs], s);
+        r += m;
+        if (r >= na) r -= na;
+      }
+      double scale = (m == 0 || 2 * m == na) ? 1.0 / na : 2.0 / na;
+      if (cs && (m == 0 || 2 * m == na)) scale = 0.0;
+      s *= scale;
     }
-    double scale = (m == 0 || 2 * m == na) ? 1.0 / na : 2.0 / na;
-    if (cs && (m == 0 || 2 * m == na)) scale = 0.0;
-    AB[t] = s * scale;
+    AB[t] = s;
   }
   __syncthreads();
   for (int t = threadIdx.x; t < (M + 1) * 2 * nr; t += blockDim.x) {
@@ -919,6 +940,43 @@ static void grid_size(double beta, double tol, int& nr, int& na) {
   na = std::max(na, 8);
 }
 
+// Ring-adaptive angular resolution (R26b): the field of a source at beta R has azimuthal orders of
+// amplitude ~(rho / beta)^m on the ring at radius rho R, so ring k (rho_k = cos((k + 1/2) pi / (2 n_r))) needs the
+// outer ring's count with beta replaced by beta / rho_k: n_a(k) = min(n_a, 1.95 ln(1/tol) / ln(beta / rho_k) + 6).
+// NC_RING_ADAPT=0 keeps n_a on every ring (the tensor grid).
+static bool ring_adapt() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NC_RING_ADAPT");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+static int ring_margin() {   // points added to every adapted ring beyond the fit (NC_RING_MARGIN, default 6)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NC_RING_MARGIN");
+    v = e ? std::max(0, atoi(e)) : 6;
+  }
+  return v;
+}
+static int ring_points(double beta, double tol, int nr, int na, int* out /* nr, or nullptr */) {
+  const double lt = log(1.0 / tol);
+  int q = 0;
+  for (int k = 0; k < nr; ++k) {
+    int nk = na;
+    if (ring_adapt()) {
+      const double rho = cos((k + 0.5) * M_PI / (2.0 * nr));
+      nk = (int)ceil(1.95 * lt / log(std::max(beta, 1.0 + 1e-9) / rho)) + ring_margin();
+      nk += nk & 1;
+      nk = std::min(na, std::max(nk, 8));
+    }
+    if (out) out[k] = nk;
+    q += nk;
+  }
+  return q;
+}
+
 static inline double harc(const double* a, const double* b) {
   double cx = a[1] * b[2] - a[2] * b[1], cy = a[2] * b[0] - a[0] * b[2], cz = a[0] * b[1] - a[1] * b[0];
   return atan2(sqrt(cx * cx + cy * cy + cz * cz), a[0] * b[0] + a[1] * b[1] + a[2] * b[2]);
@@ -1127,6 +1185,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     std::vector<int32_t> src;
     std::vector<int> rung;
     std::vector<double> dist;   // arc distance from the group's cap centre to each source centre
+    double beta = 0.0;          // the grid's nearest source (its size)
   };
   std::vector<std::vector<GridPlan>> gplans(G);
   std::vector<double> gwork(G, 0.0);
@@ -1176,7 +1235,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     // (each source with its own rung) + interpolation to the members' nodes + transform
     auto band = [&](size_t a, size_t b, int& nr, int& na) {
       grid_size(cand[b - 1].first, tol, nr, na);
-      const double q = (double)nr * na;
+      const double q = (double)ring_points(cand[b - 1].first, tol, nr, na, nullptr);
       return q * (psum[b] - psum[a]) + c_interp * (double)mem * Ks * q + c_trans * q * (nr + na);
     };
     auto near_cost = [&](size_t b) { return c_near * (double)mem * Ks * (double)(nc - b) * p0; };
@@ -1202,7 +1261,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       for (int i = 0; i < Q; ++i) {
         int nr, na;
         grid_size(cand[qs[i] - 1].first, tol, nr, na);
-        qi[i] = (double)nr * na;
+        qi[i] = (double)ring_points(cand[qs[i] - 1].first, tol, nr, na, nullptr);
         ovh[i] = c_interp * (double)mem * Ks * qi[i] + c_trans * qi[i] * (nr + na);
       }
       // dp[k][i]: cheapest cover of [0, qs[i]) by k bands; from[k][i]: previous cut index (-1: band starts at 0)
@@ -1229,6 +1288,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       GridPlan gp;
       gp.group = (int32_t)g;
       grid_size(cand[b - 1].first, tol, gp.nr, gp.na);
+      gp.beta = cand[b - 1].first;
       for (size_t n = a; n < b; ++n) {
         gp.src.push_back(cand[n].second);
         gp.rung.push_back(rung_of[n]);
@@ -1292,15 +1352,21 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   H->grid_group.assign(NG, 0);
   H->goff.assign(NG + 1, 0);
   H->coff.assign(NG + 1, 0);
+  H->rbase.assign(NG + 1, 0);
+  H->roff.clear();
   H->grid_ids.clear();
   for (int64_t k = 0; k < NG; ++k) {
     const GridPlan& gp = plans[k];
     H->grid_group[k] = gp.group;
     int64_t q = 0, c = 0;
+    H->rbase[k] = (int64_t)H->roff.size();
     if (rel[gp.group]) {
       H->gnr[k] = gp.nr;
       H->gna[k] = gp.na;
-      q = (int64_t)gp.nr * gp.na;
+      std::vector<int> rs(gp.nr);
+      q = ring_points(gp.beta, tol, gp.nr, gp.na, rs.data());
+      H->roff.push_back(0);
+      for (int kr = 0; kr < gp.nr; ++kr) H->roff.push_back(H->roff.back() + rs[kr]);
       c = (int64_t)(gp.na / 2 + 1) * 2 * gp.nr;
       H->grid_ids.push_back((int32_t)k);
       H->qmax = std::max<int>(H->qmax, (int)q);
@@ -1311,6 +1377,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     H->goff[k + 1] = H->goff[k] + q;
     H->coff[k + 1] = H->coff[k] + c;
   }
+  H->rbase[NG] = (int64_t)H->roff.size();
   H->Q = H->goff[NG];
   H->C = H->coff[NG];
   for (int64_t g = 0; g < G; ++g)
@@ -1409,7 +1476,9 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         cr.pt0 = H->goff[k] + c0;
         cr.npt = (int32_t)std::min<int64_t>(H->upts, q - c0);
         if (chunk_rungs) {
-          const int kr0 = (int)(c0 / gp.na);
+          const int32_t* ro = H->roff.data() + H->rbase[k];
+          int kr0 = 0;
+          while (c0 >= ro[kr0 + 1]) ++kr0;
           if (kr0 != kr_cached) {
             make_slices(kr0);
             kr_cached = kr0;
@@ -1540,6 +1609,8 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_TRY(upload(h, &H->d_gna, H->gna, s));
   NC_TRY(upload(h, &H->d_goff, H->goff, s));
   NC_TRY(upload(h, &H->d_coff, H->coff, s));
+  NC_TRY(upload(h, &H->d_rbase, H->rbase, s));
+  NC_TRY(upload(h, &H->d_roff, H->roff, s));
   NC_TRY(upload(h, &H->d_grid_ids, H->grid_ids, s));
   NC_TRY(halloc(h, &H->d_counter, 1));
   if (const int fb = grid_far_table_bits()) {   // far log table of the grid kernel (green.cuh green_far_t)
@@ -1601,7 +1672,8 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   if (!H->grid_ids.empty())
     k_grid_points<<<(unsigned)H->grid_ids.size(), 128, 0, s>>>(H->d_grid_ids, (int64_t)H->grid_ids.size(),
                                                                H->d_grid_group, H->d_gframe, H->d_gR, H->d_gnr,
-                                                               H->d_gna, H->d_goff, H->d_gx, H->d_gy, H->d_gz);
+                                                               H->d_gna, H->d_goff, H->d_rbase, H->d_roff, H->d_gx,
+                                                               H->d_gy, H->d_gz);
   launch_targets(h->d_frames, rb, rc, h->d_zhat, Ks, 0.5, H->d_tx, H->d_ty, H->d_tz, s);
   NC_CUDA_TRY(cudaGetLastError());
   h->pairs_per_matvec = H->pairs_grid + H->pairs_near;
@@ -1624,11 +1696,11 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   }
   // step 4a: grid samples -> coefficients
   if (!H->grid_ids.empty()) {
-    const size_t shm = (size_t)(H->qmax + H->cmax + 2 * H->namax + 8 * H->nrmax) * sizeof(double);
+    const size_t shm = (size_t)(3 * H->qmax + H->cmax + 8 * H->nrmax) * sizeof(double);
     if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(k_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     k_transform<<<(unsigned)H->grid_ids.size(), 128, shm, s>>>(H->d_grid_ids, (int64_t)H->grid_ids.size(),
                                                                    H->d_gnr, H->d_gna, H->d_goff, H->d_coff,
-                                                                   H->d_gval, H->d_gcoef);
+                                                                   H->d_rbase, H->d_roff, H->d_gval, H->d_gcoef);
     h->launches_last++;
   }
   // near lists at the Zernike nodes
@@ -1682,7 +1754,7 @@ void hier_destroy(nc_handle* h) {
   HierState* H = h->hier;
   if (!H) return;
   void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_ids,
-                  H->d_grid_group, H->d_ggrid0, H->d_counter, H->d_ftab, H->d_gsep, H->d_work_sep, H->d_ring_t,
+                  H->d_grid_group, H->d_ggrid0, H->d_counter, H->d_ftab, H->d_rbase, H->d_roff, H->d_gsep, H->d_work_sep, H->d_ring_t,
                   H->d_node_ring, H->d_node_cs,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
                   H->d_chunks, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
