@@ -118,3 +118,22 @@ def test_residual_gpu_after_solve_C1():
     assert np.all(np.abs(res - ref) <= 1.01 * bound + 1e-30)
     assert np.max(res) <= 1e-6
     h.close()
+
+
+@pytest.mark.gpu
+def test_residual_gpu_hier_handle_matches_direct_handle():
+    """nc_residual needs only the base-rung records, which both modes keep: a hierarchical handle gives the same
+    residuals as a direct one on the same solution (C3-sized layout, physical tables)."""
+    torch = pytest.importorskip("torch")
+    cfg = CONFIGS["C2"]
+    tab = _phys("C2")
+    c = cfg.centers()
+    hd = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_DIRECT)
+    hh = _nc().Handle(cfg.kind, c, cfg.eps, tab, mode=_nc().NC_HIER, precision=cfg.precision)
+    x = random_coeffs(cfg.N, tab.K, 71)
+    pats = np.arange(0, cfg.N, 97)
+    rd, pd = hd.residual(torch.from_numpy(hd.to_internal(x)).cuda(), pats, tab)
+    rh, ph = hh.residual(torch.from_numpy(hh.to_internal(x)).cuda(), pats, tab)
+    assert np.max(np.abs(pd - ph)) <= 1e-12 * max(1.0, np.max(np.abs(pd)))
+    hd.close()
+    hh.close()
