@@ -103,3 +103,20 @@ def test_field_physical_origin_identity_C1():
     vbar0 = O.mfpt_field(v, np.zeros((1, 3)), Is)[0]
     assert 0.0 < vbar0 and np.isfinite(vbar0)
     h.close()
+
+
+def test_field_exterior_far_field_C2():
+    """Exterior problem (physical C2 tables, GPU solve): |x| u(x) -> I_sigma as |x| -> infinity (|x| G_E -> 1,
+    DESIGN.md R3; the capacitance-like identity behind J = -4 pi I_sigma, R2)."""
+    from nc_inputs.tables import load_tables
+    cfg = CONFIGS["C2"]
+    tab = load_tables(os.path.join(ROOT, "tables", "data", "C2.npz"))
+    h = _nc().Handle(cfg.kind, cfg.centers(), cfg.eps, tab, mode=_nc().NC_HIER, precision=cfg.precision)
+    xs, _, _ = h.gmres(rtol=1e-10, max_iter=200)
+    Is, J = h.flux_or_mfpt(xs)
+    d = np.array([[0.3, -0.5, 0.81]])
+    d /= np.linalg.norm(d)
+    for R, tol in ((1e3, 2e-3), (1e5, 2e-5)):
+        u, _ = h.field(xs, R * d)
+        assert abs(R * u[0] - Is) <= tol * abs(Is)
+    h.close()
