@@ -95,6 +95,7 @@ struct HierState {
   int32_t* d_node_ring = nullptr;
   double* d_node_cs = nullptr;
   double sep_terms = 0.0;           // node x coefficient terms those groups represent (part of interp_terms)
+  double interp_lt = 0.0;           // ln(1 / grid tol) for the per-node order truncation of step 4 (R26c; 0: off)
   FarTable ftab;
   int32_t* d_grid_group = nullptr;
   int64_t* d_ggrid0 = nullptr;
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
                                                const double* __restrict__ tx, const double* __restrict__ ty,
                                                const double* __restrict__ tz, const double* __restrict__ udir,
                                                double* __restrict__ u, const uint8_t* __restrict__ gsep,
-                                               int nr_big) {
+                                               int nr_big, double lt) {
   // MB = 0 evaluates the grids with n_r <= kAngNrMax only (grid_eval_ang); a second pass (MB = 1, nr_big = 1) adds
   // the rest to u when any exists (tight precisions): the register-held accumulators of the first pass then need
   // no fallback code in the same kernel
@@ -620,7 +621,19 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
         const double2* __restrict__ cg = c2 + base;
         base += (M + 1) * nr;
         if (MB == 0) {
-          grid_eval_ang_any<NPT>(nr, cg, M, x, w2, c1, s1, acc);   // n_r <= kAngNrMax (larger: the second pass)
+          // orders this thread's nodes need (R26c): order m has amplitude ~(rho / beta)^m at radius rho R, and the
+          // grid's M = n_a / 2 fixes ln beta >= 0.975 ln(1/tol) / (M - 2) (grid_size), so nodes at rho need
+          // m <= 0.975 ln(1/tol) / (ln beta - ln rho) + 3; lt = 0 disables the truncation
+          int Mq = M;
+          if (lt > 0.0 && M > 4) {
+            double xm = x[0];
+#pragma unroll
+            for (int q = 1; q < NPT; ++q) xm = fmax(xm, x[q]);
+            const float lnb = (float)(0.975 * lt) / (float)(M - 2);
+            const float den = lnb - __logf(fmaxf((float)xm, 1e-30f));
+            if (den > 0.0f) Mq = min(M, (int)ceilf((float)(0.975 * lt) / den) + 3);
+          }
+          grid_eval_ang_any<NPT>(nr, cg, Mq, x, w2, c1, s1, acc);   // n_r <= kAngNrMax (larger: the second pass)
           continue;
         }
         if (nr_big && nr <= kAngNrMax) continue;                    // second pass: done by the first
@@ -858,11 +871,11 @@ static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t*
                            const double* F, const double* gR, const int32_t* gnr, const int32_t* gna,
                            const int64_t* coff, const double* coef, const double* tx, const double* ty,
                            const double* tz, const double* udir, double* u, const uint8_t* gsep, cudaStream_t s,
-                           int nr_big = 0) {
+                           int nr_big = 0, double lt = 0.0) {
   auto kern = k_interp<NT, NPT, MB, MINB>;
   if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
-                                     nr_big);
+                                     nr_big, lt);
   return NC_OK;
 }
 
@@ -870,7 +883,7 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
                          const int64_t* ggrid0, const double* F, const double* gR, const int32_t* gnr,
                          const int32_t* gna, const int64_t* coff, const double* coef, const double* tx,
                          const double* ty, const double* tz, const double* udir, double* u, const uint8_t* gsep,
-                         cudaStream_t s) {
+                         double lt, cudaStream_t s) {
   InterpVariant v = interp_variant();
   (void)namax;
   if (!getenv("NC_INTERP_VARIANT") && Ks <= 256) v = {128, 2, 0, 4};   // the 248-node rule: one 256-slot CTA per patch
@@ -879,7 +892,7 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
 #define NC_I(NT, NPT, MB, MINB)                                                                                  \
   if (rc1 == NC_OK && v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                \
     rc1 = launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, \
-                                             udir, u, gsep, s);
+                                             udir, u, gsep, s, 0, lt);
     NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6) NC_I(128, 2, 0, 4)
     NC_I(128, 2, 0, 3) NC_I(256, 1, 0, 2) NC_I(256, 1, 0, 3)
 #undef NC_I
@@ -889,13 +902,13 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
   }
 #define NC_I(NT, NPT, MB, MINB)                                                                             \
   if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                           \
-    return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep, s);
+    return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep, s, 0, lt);
   NC_I(128, 4, 1, 5) NC_I(128, 4, 1, 4) NC_I(128, 4, 1, 3) NC_I(128, 4, 1, 1) NC_I(256, 2, 1, 2) NC_I(128, 4, 2, 4)
   NC_I(256, 2, 2, 3) NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6)
   NC_I(128, 2, 0, 4) NC_I(128, 2, 0, 3) NC_I(256, 1, 0, 2) NC_I(256, 1, 0, 3)
 #undef NC_I
   return launch_interp_t<256, 2, 0, 2>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
-                                       s);
+                                       s, 0, lt);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1165,6 +1178,10 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   double tol_factor = kGridTolFactor;
   if (const char* e = getenv("NC_GRID_TOL_FACTOR")) tol_factor = atof(e);
   const double tol = tol_factor * h->precision;
+  {
+    const char* et = getenv("NC_INTERP_TRUNC");
+    H->interp_lt = (et && et[0] == '0') ? 0.0 : log(1.0 / tol);
+  }
   // relative costs in grid-pair units (measured at C5): a near-list pair (exact form), one
   // interpolation term (node x coefficient), one transform term; NC_COST_NEAR / _INTERP / _TRANSFORM override
   double c_near = kCostNear, c_interp = kCostInterp, c_trans = kCostTransform;
@@ -1713,7 +1730,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
     const size_t shm = (size_t)std::max(H->cgroupmax, 1) * sizeof(double);   // all grids of one group
     NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gR,
                          H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u,
-                         H->d_gsep, s));
+                         H->d_gsep, H->interp_lt, s));
     h->launches_last++;
   }
   if (H->nwork_sep) {   // single-member groups, separably (adds to u)

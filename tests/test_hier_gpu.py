@@ -189,12 +189,26 @@ def test_step4_evaluation_variants_agree(tmp_path, env):
     import subprocess
     import sys
     outs = []
-    for e in ({}, env):
+    for e in ({}, env):   # the per-node order truncation (R26c) off in both: the same expansion, evaluated two ways
         out = str(tmp_path / f"y{len(outs)}.npy")
-        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(os.environ, ROOT=ROOT, OUT=out, **e), check=True,
-                       timeout=600)
+        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(os.environ, ROOT=ROOT, OUT=out, NC_INTERP_TRUNC="0",
+                                                                    **e), check=True, timeout=600)
         outs.append(np.load(out))
     assert rel(outs[1], outs[0]) <= 1e-13
+
+
+def test_step4_order_truncation_below_tolerance(tmp_path):
+    """The per-node order truncation of step 4 (R26c) drops only orders below the grid tolerance: the
+    matvec moves by far less than the requested precision (C3)."""
+    import subprocess
+    import sys
+    outs = []
+    for v in ("0", "1"):
+        out = str(tmp_path / f"y{v}.npy")
+        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(os.environ, ROOT=ROOT, OUT=out, NC_INTERP_TRUNC=v),
+                       check=True, timeout=600)
+        outs.append(np.load(out))
+    assert rel(outs[1], outs[0]) <= 1e-10
 
 
 @pytest.mark.parametrize("precision", [1e-7, 1e-11])
