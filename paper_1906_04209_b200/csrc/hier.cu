@@ -955,7 +955,8 @@ static void grid_size(double beta, double tol, int& nr, int& na) {
 
 // Ring-adaptive angular resolution (R26b): the field of a source at beta R has azimuthal orders of
 // amplitude ~(rho / beta)^m on the ring at radius rho R, so ring k (rho_k = cos((k + 1/2) pi / (2 n_r))) needs the
-// outer ring's count with beta replaced by beta / rho_k: n_a(k) = min(n_a, 1.95 ln(1/tol) / ln(beta / rho_k) + 6).
+// outer ring's count with beta replaced by beta / rho_k: n_a(k) = min(n_a, 1.95 ln(1/tol) / ln(beta / rho_k) + 8),
+// then trimmed towards a whole number of 32-point warps (ring_fill) but never below the margin-6 sizes.
 // NC_RING_ADAPT=0 keeps n_a on every ring (the tensor grid).
 static bool ring_adapt() {
   static int v = -1;
@@ -965,22 +966,22 @@ static bool ring_adapt() {
   }
   return v == 1;
 }
-static int ring_margin() {   // points added to every adapted ring beyond the fit (NC_RING_MARGIN, default 6)
+static int ring_margin() {   // points added to every adapted ring beyond the fit (NC_RING_MARGIN, default 8)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("NC_RING_MARGIN");
-    v = e ? std::max(0, atoi(e)) : 6;
+    v = e ? std::max(0, atoi(e)) : 8;
   }
   return v;
 }
-static int ring_points(double beta, double tol, int nr, int na, int* out /* nr, or nullptr */) {
+static int ring_points_margin(double beta, double tol, int nr, int na, int margin, int* out) {
   const double lt = log(1.0 / tol);
   int q = 0;
   for (int k = 0; k < nr; ++k) {
     int nk = na;
     if (ring_adapt()) {
       const double rho = cos((k + 0.5) * M_PI / (2.0 * nr));
-      nk = (int)ceil(1.95 * lt / log(std::max(beta, 1.0 + 1e-9) / rho)) + ring_margin();
+      nk = (int)ceil(1.95 * lt / log(std::max(beta, 1.0 + 1e-9) / rho)) + margin;
       nk += nk & 1;
       nk = std::min(na, std::max(nk, 8));
     }
@@ -990,6 +991,57 @@ static int ring_points(double beta, double tol, int nr, int na, int* out /* nr, 
   return q;
 }
 
+// Warp-slot cost of a grid of q points in 64-point work units whose last unit runs one point per lane when it has
+// <= 32 points (k_pairs_grid_w): full units x 64 + (0 | 32 | 64)
+static int warp_slots(int q) {
+  const int rem = q % 64;
+  return q - rem + (rem == 0 ? 0 : rem <= 32 ? 32 : 64);
+}
+
+// NC_RING_FILL (default on): when a multiple of 32 points lies between the grid at the floor margin (6) and at the
+// default margin (8), trim the default grid down to it (two points at a time, outermost adapted rings first, never
+// below the floor's ring sizes): the last work unit then has no idle lanes.
+static bool ring_fill() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NC_RING_FILL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static int ring_floor() {   // the smallest margin ring filling may trim to (NC_RING_FLOOR, default 6)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NC_RING_FLOOR");
+    v = e ? std::max(0, atoi(e)) : 6;
+  }
+  return v;
+}
+
+static int ring_points(double beta, double tol, int nr, int na, int* out /* nr, or nullptr */) {
+  std::vector<int> hi(nr), lo(nr);
+  const int qh = ring_points_margin(beta, tol, nr, na, ring_margin(), hi.data());
+  if (!ring_adapt() || !ring_fill() || ring_margin() <= ring_floor()) {
+    if (out) std::copy(hi.begin(), hi.end(), out);
+    return qh;
+  }
+  const int ql = ring_points_margin(beta, tol, nr, na, ring_floor(), lo.data());
+  int target = qh - (qh % 32);   // the largest multiple of 32 <= qh
+  if (target < ql || warp_slots(target) >= warp_slots(qh)) target = qh;
+  int q = qh;
+  for (bool progress = true; q > target && progress;) {
+    progress = false;
+    for (int k = 0; k < nr && q > target; ++k)
+      if (hi[k] - 2 >= lo[k]) {
+        hi[k] -= 2;
+        q -= 2;
+        progress = true;
+      }
+  }
+  if (out) std::copy(hi.begin(), hi.end(), out);
+  return q;
+}
 static inline double harc(const double* a, const double* b) {
   double cx = a[1] * b[2] - a[2] * b[1], cy = a[2] * b[0] - a[0] * b[2], cz = a[0] * b[1] - a[1] * b[0];
   return atan2(sqrt(cx * cx + cy * cy + cz * cz), a[0] * b[0] + a[1] * b[1] + a[2] * b[2]);
