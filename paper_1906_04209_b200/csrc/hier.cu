@@ -13,12 +13,14 @@
 //     radius padded by eps (reading R14).
 // Host bookkeeping: for every (group, source patch) pair of the interaction list (and leaf neighbours, step 3,
 // PAPER.md:1364-1375) decide incoming grid vs direct near-list evaluation (skeleton validity > 2 eps, PAPER.md:1057;
-// DESIGN.md reading R12, with a cost model), size each grid from its nearest grid source, and
-// build the work units.
+// DESIGN.md reading R12, with a cost model; up to three grids per group, R24), size each grid from its nearest grid
+// source with ring-adaptive angular counts filled to whole warps (R26b), and build the warp-level
+// work units (64 grid points x a slice of sources, each with the outgoing rung valid at its own gap, R22).
 //
-// Matvec (Step 3): K1 (api.cu) -> k_pairs_grid (steps 2-3) -> k_reduce_chunks -> k_transform
-// (samples -> parity-restricted Chebyshev-Fourier coefficients) -> k_pairs_near -> k_interp
-// (step 4: evaluate every group's expansion at its members' Zernike nodes, summed over levels) -> K3 (api.cu).
+// Matvec (Step 3): K1 (api.cu) -> k_pairs_grid_w (steps 2-3, direct.cu) -> k_reduce_chunks ->
+// k_transform (samples -> parity-restricted Chebyshev-Fourier coefficients) -> k_pairs_near ->
+// k_interp + k_interp_sep (step 4: every group's expansion at its members' Zernike nodes, summed over levels; R26,
+// R26c) -> K3 (api.cu).
 #include <cub/cub.cuh>
 #include <stdio.h>
 #include <stdlib.h>
