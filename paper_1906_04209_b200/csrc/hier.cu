@@ -946,9 +946,18 @@ static int download(std::vector<T>& dst, const T* src, size_t n, cudaStream_t s)
 // incoming-grid size for a nearest grid source at beta = (distance - eps) / R and tolerance tol
 // (parity-restricted Chebyshev-Fourier; fitted to point-source interpolation tests, DESIGN.md "Incoming grids";
 // verified by tests/test_hier_gpu.py against the direct sum)
+static int nr_margin() {   // rings added beyond the radial fit (NC_NR_MARGIN, default 1; R21)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NC_NR_MARGIN");
+    v = e ? std::max(0, atoi(e)) : 1;
+  }
+  return v;
+}
+
 static void grid_size(double beta, double tol, int& nr, int& na) {
   const double lt = log(1.0 / tol);
-  nr = (int)ceil(0.56 * lt / acosh(std::max(beta, 1.0 + 1e-9))) + 2;
+  nr = (int)ceil(0.56 * lt / acosh(std::max(beta, 1.0 + 1e-9))) + nr_margin();
   na = (int)ceil(1.95 * lt / log(std::max(beta, 1.0 + 1e-9))) + 4;
   na += na & 1;
   nr = std::max(nr, 3);
