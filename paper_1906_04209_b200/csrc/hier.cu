@@ -955,10 +955,19 @@ static int nr_margin() {   // rings added beyond the radial fit (NC_NR_MARGIN, d
   return v;
 }
 
+static int na_margin() {   // angles added beyond the azimuthal fit on the outer ring (NC_NA_MARGIN, default 4)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NC_NA_MARGIN");
+    v = e ? std::max(0, atoi(e)) : 4;
+  }
+  return v;
+}
+
 static void grid_size(double beta, double tol, int& nr, int& na) {
   const double lt = log(1.0 / tol);
   nr = (int)ceil(0.56 * lt / acosh(std::max(beta, 1.0 + 1e-9))) + nr_margin();
-  na = (int)ceil(1.95 * lt / log(std::max(beta, 1.0 + 1e-9))) + 4;
+  na = (int)ceil(1.95 * lt / log(std::max(beta, 1.0 + 1e-9))) + na_margin();
   na += na & 1;
   nr = std::max(nr, 3);
   na = std::max(na, 8);
