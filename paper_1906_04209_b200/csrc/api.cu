@@ -563,18 +563,28 @@ int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = h->row_count * h->K;
   const int64_t ldv = std::max<int64_t>(n, 1);
-  if (h->V_cap < max_iter + 1) {
+  // Krylov basis: allocated for min(max_iter + 1, 64) vectors and doubled on demand inside the iteration (a C5
+  // vector is 109 MB: allocating max_iter + 1 = 301 of them up front would put a 33 GB cudaMalloc in every solve)
+  auto grow_V = [&](int need, int nkeep) -> int {
+    if (h->V_cap >= need) return NC_OK;
+    const int cap = std::min(max_iter + 1, std::max(need, std::max(64, 2 * h->V_cap)));
+    double* nv = nullptr;
+    NC_TRY(dalloc(h, &nv, (size_t)cap * ldv));
+    if (h->d_V && nkeep > 0)
+      NC_CUDA_TRY(cudaMemcpyAsync(nv, h->d_V, (size_t)nkeep * ldv * sizeof(double), cudaMemcpyDeviceToDevice, s));
     if (h->d_V) {
+      NC_CUDA_TRY(cudaStreamSynchronize(s));
       cudaFree(h->d_V);
       h->device_bytes -= (double)h->V_cap * ldv * sizeof(double);
-      h->d_V = nullptr;
     }
-    NC_TRY(dalloc(h, &h->d_V, (size_t)(max_iter + 1) * ldv));
-    h->V_cap = max_iter + 1;
-  }
+    h->d_V = nv;
+    h->V_cap = cap;
+    return NC_OK;
+  };
+  NC_TRY(grow_V(std::min(max_iter + 1, 64), 0));
   // reduction scratch: [0, 2048) small vectors, [2048, ...) multidot partials
   NC_TRY(ensure_red(h, 2048 + (int64_t)(max_iter + 2) * multidot_partials(n) + 16));
-  double* V = h->d_V;
+  double* V = h->d_V;                 // (re-read after every growth of the basis)
   double* d_h1 = h->d_red;            // first-pass projections  (<= max_iter+1)
   double* d_h2 = h->d_red + 640;      // second-pass projections
   double* d_nrm = h->d_red + 1280;    // ||w||^2
@@ -611,6 +621,10 @@ int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x
   int k = 0;
   bool converged = false;
   for (int j = 0; j < m; ++j) {
+    if (j + 2 > h->V_cap) {   // room for v_{j+1}
+      NC_TRY(grow_V(j + 2, j + 1));
+      V = h->d_V;
+    }
     double* w = V + (size_t)(j + 1) * ldv;
     NC_TRY(nc_matvec(h, V + (size_t)j * ldv, w, s));
     // CGS2: two classical Gram-Schmidt passes
