@@ -442,7 +442,7 @@ static int matvec_tail(nc_handle* h, const double* x, double* y, cudaStream_t s)
   mark(h, 2, s);
   if (h->mode == NC_DIRECT) {
     launch_pairs_direct(h->kind, h->pair_tpt, h->d_tx, h->d_ty, h->d_tz, h->row_count * Ks, Ks, h->row_begin, h->d_src4, p, h->N,
-                        h->nseg, h->d_upart, h->xtab, s);
+                        h->nseg, h->d_upart, h->xtab, h->eps, s);
     mark(h, 3, s);
     // K3: Y = X + (sum_seg U_seg) P^T
     launch_gemm_dmma(h->d_upart, Ks, h->nseg, h->row_count * Ks, h->d_P, h->row_count, K, Ks, y, K, 1, x, K, s);
@@ -815,7 +815,7 @@ int nc_residual(nc_handle* h, const double* x_all, int n_sel, const int64_t* pat
         double* tx = d_t + (size_t)q * nr * 3;
         launch_targets(h->d_frames, rows[q], 1, d_rhat, n_res, 0.5, tx, tx + nr, tx + 2 * nr, s);
         launch_pairs_direct(h->kind, h->pair_tpt, tx, tx + nr, tx + 2 * nr, n_res, n_res, rows[q], src0, p0, h->N, nseg,
-                            d_up + (size_t)q * nseg * nr, h->xtab, s);
+                            d_up + (size_t)q * nseg * nr, h->xtab, h->eps, s);
       }
       launch_residual(n_sel, n_res, K, nseg, d_rows, x_all, d_S, d_w, d_up, d_out, d_out + (size_t)n_sel * nr, s);
       e = cudaGetLastError();

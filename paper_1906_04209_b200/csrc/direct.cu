@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_pairs_direct(const double* 
                                                                 int nseg, int chp, double* __restrict__ upart,
                                                                 const double2* __restrict__ logsrc,
                                                                 const double2* __restrict__ xsrc, int xn, int xbase,
-                                                                int xmid) {
+                                                                int xmid, double far_q) {
   extern __shared__ double4 sm[];
   __shared__ double2 logtab[EX ? 1 : kLogTableSize];
   __shared__ int64_t pid[kStagePatchesMax];
@@ -57,8 +57,10 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_pairs_direct(const double* 
     accumulate_list_ldg<KIND, TPT>(x, y, z, excl, acc, j1 - j0, [=] __device__(int64_t k) { return j0 + k; },
                                    reinterpret_cast<const double4*>(src4), p, logtab);
   } else {
+    auto greenfar = [&](double qh) { return green_exact_far<KIND>(qh, xt.tb, xt.lim, xt.a2, xt.a3, xt.kmid); };
     accumulate_list<KIND, TPT>(x, y, z, excl, acc, j1 - j0, [=] __device__(int64_t k) { return j0 + k; },
-                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, green, true);
+                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, green, true, greenfar,
+                               EX ? far_q : 0.0);
   }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
@@ -87,19 +89,28 @@ int pairs_direct_blocks_per_sm(int p, int tpt, const FarTable& xt) {
 
 void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, const double* tz, int64_t n_tgt,
                          int Kstar, int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
-                         const FarTable& xt, cudaStream_t s) {
+                         const FarTable& xt, double eps, cudaStream_t s) {
   if (n_tgt <= 0) return;
   const int chp = stage_ldg() ? 0 : stage_patches(p);
   const bool ex = exact_table_on(xt);
   const size_t smem = (size_t)chp * p * sizeof(double4) + (ex ? (size_t)xt.n * sizeof(double) : 0);
   const int64_t per_block = (int64_t)kPairThreads * tpt;
   dim3 grid((unsigned)((n_tgt + per_block - 1) / per_block), (unsigned)nseg);
+  // far path (R30): source patches whose first node is >= 0.12 + 2 eps from every target of a warp (scaled q units);
+  // NC_DIRECT_FAR=0 disables it
+  static int far_on = -1;
+  if (far_on < 0) {
+    const char* e = getenv("NC_DIRECT_FAR");
+    far_on = (e && e[0] == '0') ? 0 : 1;
+  }
+  const double dfar = 0.12 + 2.0 * eps;
+  const double far_q = far_on ? 0.25 * dfar * dfar : 0.0;
 #define NC_LAUNCH(KD, TP, EX)                                                                                       \
   {                                                                                                                \
     auto kern = k_pairs_direct<KD, TP, EX>;                                                                        \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
     kern<<<grid, kPairThreads, smem, s>>>(tx, ty, tz, n_tgt, Kstar, tgt_patch0, src4, p, N, nseg, chp, upart,       \
-                                          log_table_device(), xt.d, xt.n, xt.base, 1 << 12);                       \
+                                          log_table_device(), xt.d, xt.n, xt.base, 1 << 12, far_q);                \
   }
   if (kind == NC_EXTERIOR) {
     if (ex) { if (tpt == 2) NC_LAUNCH(1, 2, true) else NC_LAUNCH(1, 1, true) }
@@ -528,7 +539,7 @@ __global__ void __launch_bounds__(NT) k_pairs_near(const double* __restrict__ tx
                                    reinterpret_cast<const double4*>(src4), p, logtab);
   } else {
     accumulate_list<KIND, TPT>(x, y, z, excl, acc, o1 - o0, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
-                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, green, true);
+                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, green, true, green, 0.0);
   }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {

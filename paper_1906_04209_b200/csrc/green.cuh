@@ -230,6 +230,37 @@ __device__ __forceinline__ double green_exact_r(double q, unsigned tbase, int li
   return fma(-r, p, w - lj);
 }
 
+// Direct-sum pairs between well-separated patches (k_pairs_direct with FARD, R30): q from the dot product
+// (qh = q/2 = (|X|^2 + 1/4)/2 - X.S for scaled coordinates, 3 DFMA) and w = 2/d by one Newton step from the SFU seed,
+// then the exact-form table log (quartic).  Used only when the source patch is >= 0.12 + 2 eps away from every
+// target of the warp, where the dot product's absolute rounding (~3e-16) is <= 2e-13 relative to q: 15 FP64
+// instructions (interior; 14 exterior) instead of 19.
+template <int KIND>
+__device__ __forceinline__ double green_exact_far(double qh, unsigned tbase, int lim, double a2r, double a3r, int kmid) {
+  const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
+  const double t = qh * y;
+  const double e = fma(-t, y, 0.5);
+  const double w = fma(y, e, y);
+  double x;
+  if (KIND == 1) {
+    x = 1.0 + w;
+  } else {
+    const double xh = fma(qh, w, qh);   // q (1 + w) / 2
+    x = xh + xh;                        // exact doubling
+  }
+  const int hx = __double2hiint(x);
+  const double c = rcp_approx(__hiloint2double((hx & ~((1 << 13) - 1)) | kmid, 0));
+  int ix = hx >> 13;
+  ix = (KIND == 1) ? min(ix, lim) : max(ix, lim);
+  double lj;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(lj) : "r"(tbase + ((unsigned)ix << 3)));
+  const double r = fma(x, c, -1.0);
+  double p = fma(r, FarPoly<7, 4>::a4, a3r);
+  p = fma(r, p, a2r);
+  p = fma(r, p, 1.0);
+  return fma(-r, p, w - lj);
+}
+
 // the exact-form table as the kernels hold it: shared-memory base address (minus base * 8), clamp, constants
 struct ExactTab {
   unsigned tb;

@@ -191,7 +191,7 @@ void launch_gemm_dmma_colmap(const double* A, int64_t lda, const double* Bt, int
 // sum_m G(target t, s_jm) rho_jm
 void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, const double* tz, int64_t n_tgt,
                          int Kstar, int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
-                         const FarTable& xt, cudaStream_t s);
+                         const FarTable& xt, double eps, cudaStream_t s);
 
 int pairs_direct_blocks_per_sm(int p, int tpt, const FarTable& xt);
 void split_rows(const double* w, int64_t N, int world, int64_t* begin, int64_t* count);

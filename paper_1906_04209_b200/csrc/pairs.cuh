@@ -26,12 +26,17 @@ __host__ __device__ inline int stage_patches(int p) {
 // UNROLL: source records in flight per target (independent FP64 chains = TPT x UNROLL); Tab: double2 (c_j, -log c_j)
 // (c_j, -log c_j).
 // green(q) evaluates G from q = |z - s|^2 / 4 (green_q with the mantissa table, or green_exact_r)
-template <int KIND, int TPT, int UNROLL = 2, class GreenQ, class PatchAt>
+// GreenFar: a functor (qh) -> G for well-separated pairs (green_exact_far), used for a whole staged patch when every
+// target of the warp is at least sqrt(4 far_q) (unscaled) from its first record; far_q <= 0 disables it
+template <int KIND, int TPT, int UNROLL = 2, class GreenQ, class PatchAt, class GreenFar = GreenQ>
 __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
                                                 const int64_t (&excl)[TPT], double (&acc)[TPT], int64_t nlist,
                                                 PatchAt patch_at, const double4* __restrict__ s4, int p,
                                                 double4* __restrict__ sm, int64_t* __restrict__ sm_pid, int chp,
-                                                GreenQ green, bool active) {
+                                                GreenQ green, bool active, GreenFar greenfar, double far_q) {
+  double cq[TPT];   // (|X|^2 + 1/4) / 2: qh = cq - X.S for the far path
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) cq[u] = 0.5 * fma(x[u], x[u], fma(y[u], y[u], fma(z[u], z[u], 0.25)));
   for (int64_t c0 = 0; c0 < nlist; c0 += chp) {
     const int nch = (int)min((int64_t)chp, nlist - c0);
     __syncthreads();
@@ -54,6 +59,29 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
       }
       if (none) continue;
       if (all) {
+        bool far = false;
+        if (far_q > 0.0) {   // warp-uniform among the lanes here: every target far from the patch's first node
+          const double4 s0 = sp[0];
+          double mq = 1e300;
+#pragma unroll
+          for (int u = 0; u < TPT; ++u) {
+            const double dx = x[u] - s0.x, dy = y[u] - s0.y, dz = z[u] - s0.z;
+            mq = fmin(mq, fma(dz, dz, fma(dy, dy, dx * dx)));
+          }
+          far = __all_sync(__activemask(), mq >= far_q);
+        }
+        if (far) {
+#pragma unroll UNROLL
+          for (int m = 0; m < p; ++m) {
+            const double4 s = sp[m];
+#pragma unroll
+            for (int u = 0; u < TPT; ++u) {
+              const double qh = fma(-x[u], s.x, fma(-y[u], s.y, fma(-z[u], s.z, cq[u])));
+              acc[u] = fma(s.w, greenfar(qh), acc[u]);
+            }
+          }
+          continue;
+        }
 #pragma unroll UNROLL
         for (int m = 0; m < p; ++m) {
           const double4 s = sp[m];
