@@ -60,7 +60,7 @@ def load_fp64_peak():
 PAIR_MIX_CYCLES = 47.22
 
 # ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
-TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01u_ncu_full_pairs_grid.json"}
+TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01v_ncu_full_pairs_grid.json"}
 
 
 def profiled_traffic(kernel, config, mode):
@@ -421,10 +421,11 @@ def main():
         torch.cuda.synchronize()
         ms2 = e0.elapsed_time(e1) / 5
         st2 = h2.stats()
-        tf2 = st2["pairs_per_matvec"] * st2["pair_fp64_flops_direct"] / (ms2 * 1e-3) / 1e12
         secondary = {"workload": "C2 direct", "value": 1e3 / ms2, "unit": "matvec/s", "ms_per_matvec": ms2,
-                     "pairs_per_matvec": st2["pairs_per_matvec"], "fp64_tflops_whole_matvec": tf2,
-                     "frac_of_dfma_peak": tf2 / peaks["dfma"] if peaks.get("dfma") else None}
+                     "pairs_per_matvec": st2["pairs_per_matvec"],
+                     "pairs_per_s": st2["pairs_per_matvec"] / (ms2 * 1e-3),
+                     "note": "whole matvec (K1 + pair sums + K3); most pairs take the far form (DESIGN.md R30: "
+                             "15 FP64 instructions, exact form 19)"}
         h2.close()
     cpu = None
     if not args.no_cpu_baseline and world == 1:
