@@ -181,17 +181,42 @@ __device__ __forceinline__ double rcp_approx(double x) {
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   return y;
 }
+// fp32 SFU seeds (R31, measured and NOT used by the kernels: tools/pair_mix_bench.cu only).  The idea: an
+// fp64 MUFU (RSQ64H, RCP64H) costs ~2.3 cycles of a saturated FP64 pipe (profiles/r01m_sfu_fp64_overlap.txt) while
+// the fp32 MUFU overlaps the DFMA stream, so take the seeds from the fp32 unit with the format conversions on the
+// integer pipe (a double in the fp32 normal range -> the fp32 of its top 23 mantissa bits: one funnel shift and one
+// add, exponent rebias 1023 -> 127 modulo 2^9; fp32 -> the equal double: a shift-add and a shift).  Accurate
+// (C3/C4 hierarchical error unchanged to 1e-16, profiles/r01w_s32.txt) but slower: the grid kernel is issue-bound
+// and the ~3 extra integer instructions per pair cost more than the fp64 MUFU contention saved (66.3 -> 72.7 ms).
+__device__ __forceinline__ double f32bits_to_double(unsigned u) {
+  return __hiloint2double((int)((u >> 3) + 0x38000000u), (int)(u << 29));
+}
+__device__ __forceinline__ double rsqrt_seed32(double qh) {   // ~ rsqrt(2 qh), relative error < 2^-22
+  const unsigned f = __funnelshift_l((unsigned)__double2loint(qh), (unsigned)__double2hiint(qh), 3) + 0x40800000u;
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__uint_as_float(f)));
+  return f32bits_to_double(__float_as_uint(y));
+}
+__device__ __forceinline__ double rcp_mid32(int h) {   // rcp.approx.f32 of the double (h, 0) (a bin midpoint)
+  float c;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(__uint_as_float(((unsigned)h << 3) + 0x40000000u)));
+  return f32bits_to_double(__float_as_uint(c));
+}
+
 // kmid = 1 << (19 - FB), passed in at run time: the midpoint is then one LOP3 (x & ~mask) | kmid with kmid in a
-// register, not two with two immediates
-template <int KIND, int FB, int DEG>
+// register, not two with two immediates.  S32 (R31, microbenchmark only): bit 0 the fp32 rsqrt seed, bit 1 the fp32
+// midpoint reciprocal.
+template <int KIND, int FB, int DEG, int S32 = 0>
 __device__ __forceinline__ double green_far_r(double qh, unsigned tbase, int lim, double a2r, double a3r, int kmid) {
-  const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
+  const double y = (S32 & 1) ? rsqrt_seed32(qh)
+                             : rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
   const double t = qh * y;
   const double e = fma(-t, y, 0.5);
   const double w = fma(y, e, y);
   const double x = (KIND == 1) ? 1.0 + w : fma(qh, w, qh);
   const int hx = __double2hiint(x);
-  const double c = rcp_approx(__hiloint2double((hx & ~((1 << (20 - FB)) - 1)) | kmid, 0));
+  const int hmid = (hx & ~((1 << (20 - FB)) - 1)) | kmid;
+  const double c = (S32 & 2) ? rcp_mid32(hmid) : rcp_approx(__hiloint2double(hmid, 0));
   int ix = hx >> (20 - FB);
   ix = (KIND == 1) ? min(ix, lim) : max(ix, lim);
   double lj;

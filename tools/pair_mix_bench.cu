@@ -11,7 +11,7 @@
 
 using namespace nc;
 
-template <int KIND, int TPT, int NS>
+template <int KIND, int TPT, int NS, int S32>
 __global__ void __launch_bounds__(256) k_mix(const double2* __restrict__ tsrc, int fn, int fbase, int iters,
                                              double* out) {
   extern __shared__ double2 ft[];
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) k_mix(const double2* __restrict__ tsrc, i
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
         const double qh = fma(x[u], s[k].x, fma(y[u], s[k].y, fma(z[u], s[k].z, cq[u])));
-        acc[u] = fma(s[k].w, green_far_r<KIND, 7, 3>(qh, tb, lim, a2, a3), acc[u]);
+        acc[u] = fma(s[k].w, green_far_r<KIND, 7, 3, S32>(qh, tb, lim, a2, a3, 1 << 12), acc[u]);
       }
     }
   }
@@ -61,22 +61,26 @@ int main() {
   double* out;
   cudaMalloc(&out, sizeof(double) * sms * 8 * 256);
   const int iters = 200, NS = 8;
-  for (int blocksPerSm : {2, 3, 4}) {
+  for (int s32 = 0; s32 < 4; ++s32)
+  for (int blocksPerSm : {3, 4}) {
     const int blocks = sms * blocksPerSm;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     float ms = 0;
-    for (int rep = 0; rep < 2; ++rep) {
+    for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(a);
-      k_mix<0, 2, NS><<<blocks, 256, fn * 8>>>(tab, fn, fbase, iters, out);
+      if (s32 == 0) k_mix<0, 2, NS, 0><<<blocks, 256, fn * 8>>>(tab, fn, fbase, iters, out);
+      if (s32 == 1) k_mix<0, 2, NS, 1><<<blocks, 256, fn * 8>>>(tab, fn, fbase, iters, out);
+      if (s32 == 2) k_mix<0, 2, NS, 2><<<blocks, 256, fn * 8>>>(tab, fn, fbase, iters, out);
+      if (s32 == 3) k_mix<0, 2, NS, 3><<<blocks, 256, fn * 8>>>(tab, fn, fbase, iters, out);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       cudaEventElapsedTime(&ms, a, b);
     }
     const double warp_pairs = (double)blocks * 256 / 32 * iters * NS * 2;
-    printf("TPT 2, %d CTAs of 256 per SM: %.3f ms, %.2f SMSP-cycles per warp-pair (at 1.965 GHz)\n", blocksPerSm, ms,
-           ms * 1e-3 * 1.965e9 * sms * 4 / warp_pairs);
+    printf("S32 %d (bit0 fp32 rsqrt seed, bit1 fp32 rcp), TPT 2, %d CTAs of 256 per SM: %.3f ms, %.2f SMSP-cycles per "
+           "warp-pair (at 1.965 GHz)\n", s32, blocksPerSm, ms, ms * 1e-3 * 1.965e9 * sms * 4 / warp_pairs);
   }
   return 0;
 }

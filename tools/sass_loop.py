@@ -1,7 +1,7 @@
-"""Per-pair instruction counts of a pair kernel's innermost loop(s) containing MUFU.RSQ64H (one per pair).
+"""Per-pair instruction counts of a pair kernel's innermost loop(s) containing MUFU.RSQ64H or MUFU.RSQ (one per pair).
 
     python tools/sass_loop.py <lib.so> <function-substring>
-Prints, for each innermost loop with MUFU.RSQ64H: pairs per iteration, FP64 (DFMA/DMUL/DADD) and other instructions
+Prints, for each innermost loop with MUFU.RSQ(64H): pairs per iteration, FP64 (DFMA/DMUL/DADD) and other instructions
 per pair, and the issue-model cycles per warp-pair 2*FP64 + other.
 """
 import re
@@ -33,13 +33,13 @@ def _inner_loops(f):
             if t and int(t.group(1), 16) < addr:
                 lo = int(t.group(1), 16)
                 body = [o for o in ops if lo <= o[0] <= addr]
-                if any(o[1].startswith("MUFU.RSQ64H") for o in body):
+                if any(o[1].startswith("MUFU.RSQ") for o in body):
                     found.append((lo, addr, body))
     # innermost: no other MUFU-loop strictly inside
     inner = [L for L in found if not any(M is not L and L[0] <= M[0] and M[1] <= L[1] for M in found)]
     res = []
     for lo, hi, body in inner:
-        npair = sum(1 for o in body if o[1].startswith("MUFU.RSQ64H"))
+        npair = sum(1 for o in body if o[1].startswith("MUFU.RSQ"))
         fp = sum(1 for o in body if o[1] in ("DFMA", "DMUL", "DADD"))
         res.append((npair, fp / npair, (len(body) - fp) / npair))
     return res
