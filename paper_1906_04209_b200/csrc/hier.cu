@@ -490,7 +490,47 @@ __global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, cons
 //   E_j = sum_{m of that parity} c[m][j] . (cos m theta, sin m theta)        (2 FMA per (m, j, node))
 //   u  += sum_j E_j T_{par + 2 j}(x)                                          (once per grid and parity)
 // The n_r accumulators per node live in registers (NR = n_r exactly, one instantiation per n_r: no idle FMAs).
-template <int NR, int NPT>
+// PF (k_interp MB = 3, n_r <= kPfNrMax): the coefficient pairs of order m + 2 are loaded from shared memory while
+// order m is accumulated (two register buffers in ping-pong, the m loop unrolled by two): without it the compiler,
+// short of registers, reuses one buffer and every LDS.128 is followed by its two consumers (short-scoreboard stalls,
+// profiles/r01w_ncu_full_interp.json).  The prefetch index is clamped to M (same parity) so it never leaves the grid.
+constexpr int kPfNrMax = 8;   // MB = 3; MB = 4 prefetches at every n_r <= kAngNrMax
+template <int NR, int NPT, bool PF>
+__device__ __forceinline__ void ang_orders_pf(const double2* __restrict__ cg, int par, int M, double (&E)[NPT][NR],
+                                              double (&cm)[NPT], double (&sm)[NPT], double (&cp)[NPT],
+                                              double (&sp)[NPT], const double (&t2)[NPT]) {
+  auto step = [&](const double2 (&c)[NR]) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) E[q][j] = fma(c[j].x, cm[q], fma(c[j].y, sm[q], E[q][j]));
+    }
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      const double cn = fma(t2[q], cm[q], -cp[q]), sn = fma(t2[q], sm[q], -sp[q]);
+      cp[q] = cm[q]; sp[q] = sm[q]; cm[q] = cn; sm[q] = sn;
+    }
+  };
+  double2 ca[NR], cb[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) ca[j] = cg[par * NR + j];
+  for (int m = par;;) {
+    int mn = m + 2 <= M ? m + 2 : m;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) cb[j] = cg[mn * NR + j];
+    step(ca);
+    m += 2;
+    if (m > M) break;
+    mn = m + 2 <= M ? m + 2 : m;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) ca[j] = cg[mn * NR + j];
+    step(cb);
+    m += 2;
+    if (m > M) break;
+  }
+}
+
+template <int NR, int NPT, int PF = 0>
 __device__ __forceinline__ void grid_eval_ang(const double2* __restrict__ cg, int M, const double (&x)[NPT],
                                               const double (&w2)[NPT], const double (&c1)[NPT],
                                               const double (&s1)[NPT], double (&acc)[NPT]) {
@@ -508,18 +548,22 @@ __device__ __forceinline__ void grid_eval_ang(const double2* __restrict__ cg, in
       if (par == 0) { cm[q] = 1.0; sm[q] = 0.0; cp[q] = c2; sp[q] = -s2; }
       else { cm[q] = c1[q]; sm[q] = s1[q]; cp[q] = c1[q]; sp[q] = -s1[q]; }
     }
-    for (int m = par; m <= M; m += 2) {
-      const double2* __restrict__ cmj = cg + m * NR;
+    if ((PF == 1 && NR <= kPfNrMax) || PF == 2) {
+      ang_orders_pf<NR, NPT, true>(cg, par, M, E, cm, sm, cp, sp, t2);
+    } else {
+      for (int m = par; m <= M; m += 2) {
+        const double2* __restrict__ cmj = cg + m * NR;
 #pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        const double2 c = cmj[j];
+        for (int j = 0; j < NR; ++j) {
+          const double2 c = cmj[j];
 #pragma unroll
-        for (int q = 0; q < NPT; ++q) E[q][j] = fma(c.x, cm[q], fma(c.y, sm[q], E[q][j]));
-      }
+          for (int q = 0; q < NPT; ++q) E[q][j] = fma(c.x, cm[q], fma(c.y, sm[q], E[q][j]));
+        }
 #pragma unroll
-      for (int q = 0; q < NPT; ++q) {   // (m, m - 2) -> (m + 2, m)
-        const double cn = fma(t2[q], cm[q], -cp[q]), sn = fma(t2[q], sm[q], -sp[q]);
-        cp[q] = cm[q]; sp[q] = sm[q]; cm[q] = cn; sm[q] = sn;
+        for (int q = 0; q < NPT; ++q) {   // (m, m - 2) -> (m + 2, m)
+          const double cn = fma(t2[q], cm[q], -cp[q]), sn = fma(t2[q], sm[q], -sp[q]);
+          cp[q] = cm[q]; sp[q] = sm[q]; cm[q] = cn; sm[q] = sn;
+        }
       }
     }
 #pragma unroll
@@ -541,13 +585,13 @@ __device__ __forceinline__ void grid_eval_ang(const double2* __restrict__ cg, in
 
 constexpr int kAngNrMax = 12;   // grid_eval_ang instantiations (n_r = 1..12)
 
-template <int NPT>
+template <int NPT, int PF = 0>
 __device__ __forceinline__ bool grid_eval_ang_any(int nr, const double2* __restrict__ cg, int M, const double (&x)[NPT],
                                                   const double (&w2)[NPT], const double (&c1)[NPT],
                                                   const double (&s1)[NPT], double (&acc)[NPT]) {
   switch (nr) {
 #define NC_GE(R) \
-  case R: grid_eval_ang<R, NPT>(cg, M, x, w2, c1, s1, acc); return true;
+  case R: grid_eval_ang<R, NPT, PF>(cg, M, x, w2, c1, s1, acc); return true;
     NC_GE(1) NC_GE(2) NC_GE(3) NC_GE(4) NC_GE(5) NC_GE(6) NC_GE(7) NC_GE(8) NC_GE(9) NC_GE(10) NC_GE(11) NC_GE(12)
 #undef NC_GE
     default: return false;
@@ -622,7 +666,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
         const int nr = gnr[kg], M = gna[kg] / 2;
         const double2* __restrict__ cg = c2 + base;
         base += (M + 1) * nr;
-        if (MB == 0) {
+        if (MB == 0 || MB == 3 || MB == 4) {
           // orders this thread's nodes need (R26c): order m has amplitude ~(rho / beta)^m at radius rho R, and the
           // grid's M = n_a / 2 fixes ln beta >= 0.975 ln(1/tol) / (M - 2) (grid_size), so nodes at rho need
           // m <= 0.975 ln(1/tol) / (ln beta - ln rho) + 3; lt = 0 disables the truncation
@@ -635,7 +679,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
             const float den = lnb - __logf(fmaxf((float)xm, 1e-30f));
             if (den > 0.0f) Mq = min(M, (int)ceilf((float)(0.975 * lt) / den) + 3);
           }
-          grid_eval_ang_any<NPT>(nr, cg, Mq, x, w2, c1, s1, acc);   // n_r <= kAngNrMax (larger: the second pass)
+          grid_eval_ang_any<NPT, MB == 3 ? 1 : MB == 4 ? 2 : 0>(nr, cg, Mq, x, w2, c1, s1, acc);   // n_r <= kAngNrMax (else: second pass)
           continue;
         }
         if (nr_big && nr <= kAngNrMax) continue;                    // second pass: done by the first
@@ -851,7 +895,8 @@ __global__ void __launch_bounds__(NT) k_interp_sep(int L, int64_t rc, int Ks, co
 }
 
 // interpolation variant: NC_INTERP_VARIANT="NT,NPT,MB,MINB" (k_interp<NT,NPT,MB,MINB>; default 256,2,0,2;
-// MB = 0: grid_eval_ang for n_r <= 12, MB = 1: Chebyshev sums first, MB > 1: MB orders per radial loop)
+// MB = 0: grid_eval_ang for n_r <= 12, MB = 1: Chebyshev sums first, MB = 2: two orders per radial loop, MB = 3:
+// grid_eval_ang with the coefficient prefetch for n_r <= kPfNrMax, MB = 4: with it for every n_r)
 struct InterpVariant {
   int nt, npt, mb, minb;
 };
@@ -888,15 +933,17 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
                          double lt, cudaStream_t s) {
   InterpVariant v = interp_variant();
   (void)namax;
-  if (!getenv("NC_INTERP_VARIANT") && Ks <= 256) v = {128, 2, 0, 4};   // the 248-node rule: one 256-slot CTA per patch
-  if (v.mb == 0 && nrmax > kAngNrMax) {   // the first pass leaves the grids with n_r > kAngNrMax to a second one
+  // the 248-node rule: one 256-slot CTA per patch, coefficient prefetch (MB = 3: rest of the C5 step 20.07 -> 18.32 ms,
+  // bitwise-identical output, profiles/r01w_interp_prefetch_c5.jsonl)
+  if (!getenv("NC_INTERP_VARIANT") && Ks <= 256) v = {128, 2, 3, 4};
+  if ((v.mb == 0 || v.mb == 3 || v.mb == 4) && nrmax > kAngNrMax) {   // the first pass leaves the grids with n_r > kAngNrMax to a second one
     int rc1 = NC_OK;
 #define NC_I(NT, NPT, MB, MINB)                                                                                  \
   if (rc1 == NC_OK && v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                \
     rc1 = launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, \
                                              udir, u, gsep, s, 0, lt);
     NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6) NC_I(128, 2, 0, 4)
-    NC_I(128, 2, 0, 3) NC_I(256, 1, 0, 2) NC_I(256, 1, 0, 3)
+    NC_I(128, 2, 0, 3) NC_I(256, 1, 0, 2) NC_I(256, 1, 0, 3) NC_I(128, 2, 3, 3) NC_I(128, 2, 3, 4) NC_I(128, 2, 4, 4)
 #undef NC_I
     if (rc1 != NC_OK) return rc1;
     return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir,
@@ -907,7 +954,7 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
     return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep, s, 0, lt);
   NC_I(128, 4, 1, 5) NC_I(128, 4, 1, 4) NC_I(128, 4, 1, 3) NC_I(128, 4, 1, 1) NC_I(256, 2, 1, 2) NC_I(128, 4, 2, 4)
   NC_I(256, 2, 2, 3) NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6)
-  NC_I(128, 2, 0, 4) NC_I(128, 2, 0, 3) NC_I(256, 1, 0, 2) NC_I(256, 1, 0, 3)
+  NC_I(128, 2, 0, 4) NC_I(128, 2, 0, 3) NC_I(256, 1, 0, 2) NC_I(256, 1, 0, 3) NC_I(128, 2, 3, 3) NC_I(128, 2, 3, 4) NC_I(128, 2, 4, 4)
 #undef NC_I
   return launch_interp_t<256, 2, 0, 2>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
                                        s, 0, lt);

@@ -181,7 +181,8 @@ def test_far_field_pair_variant_error(tmp_path, far):
 
 
 @pytest.mark.parametrize("env", [{"NC_INTERP_SEP": "0"}, {"NC_INTERP_VARIANT": "128,4,1,4"},
-                                 {"NC_INTERP_VARIANT": "128,4,2,4"}])
+                                 {"NC_INTERP_VARIANT": "128,4,2,4"}, {"NC_INTERP_VARIANT": "128,2,3,4"},
+                                 {"NC_INTERP_VARIANT": "128,2,0,4"}])
 def test_step4_evaluation_variants_agree(tmp_path, env):
     """Step 4 evaluated three ways: angular sums first with register accumulators (default),
     Chebyshev sums first (MB = 1) or blocked orders (MB = 2), and single-member groups separably on the Zernike node
