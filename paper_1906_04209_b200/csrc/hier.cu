@@ -438,7 +438,7 @@ __global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, cons
   const int32_t* ro = roff + rbase[g];
   const int q = ro[nr];
   double* f = sh;                      // q samples
-  double* AB = f + q;                  // nr * (M+1) * 2
+  double* AB = f + ((q + 1) & ~1);     // nr * (M+1) * 2 (16-byte aligned: tw is read as double2)
   double* tw = AB + nr * (M + 1) * 2;  // 2 q: ring k's (cos, sin)(2 pi r / n_a(k)) at 2 (ro[k] + r)
   double* ch = tw + 2 * q;             // 8 * nr: cos(pi r / (4 nr))
   for (int t = threadIdx.x; t < q; t += blockDim.x) {
@@ -449,24 +449,31 @@ __global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, cons
   }
   for (int t = threadIdx.x; t < 8 * nr; t += blockDim.x) ch[t] = cospi((double)t / (4.0 * nr));
   __syncthreads();
-  for (int t = threadIdx.x; t < nr * (M + 1) * 2; t += blockDim.x) {
-    const int k = t / ((M + 1) * 2), rem = t % ((M + 1) * 2), m = rem >> 1, cs = rem & 1;
+  // one thread per (ring k, order m): both components from one 16-byte (cos, sin) twiddle read per sample (the
+  // twiddle gathers at l m mod n_a are the kernel's shared-memory wavefront cost), same summation order as one
+  // component per thread
+  const double2* __restrict__ tw2 = reinterpret_cast<const double2*>(tw);
+  for (int t = threadIdx.x; t < nr * (M + 1); t += blockDim.x) {
+    const int k = t / (M + 1), m = t % (M + 1);
     const int na = ro[k + 1] - ro[k];
-    double s = 0.0;
+    double sc = 0.0, ss = 0.0;
     if (2 * m <= na) {
       const double* fk = f + ro[k];
-      const double* twk = tw + 2 * ro[k];
+      const double2* twk = tw2 + ro[k];
       int r = 0;
       for (int l = 0; l < na; ++l) {
-        s = fma(fk[l], twk[2 * r + cs], s);
+        const double2 w = twk[r];
+        sc = fma(fk[l], w.x, sc);
+        ss = fma(fk[l], w.y, ss);
         r += m;
         if (r >= na) r -= na;
       }
-      double scale = (m == 0 || 2 * m == na) ? 1.0 / na : 2.0 / na;
-      if (cs && (m == 0 || 2 * m == na)) scale = 0.0;
-      s *= scale;
+      const bool edge = m == 0 || 2 * m == na;
+      sc *= edge ? 1.0 / na : 2.0 / na;
+      ss = edge ? 0.0 : ss * (2.0 / na);
     }
-    AB[t] = s;
+    AB[2 * t] = sc;
+    AB[2 * t + 1] = ss;
   }
   __syncthreads();
   for (int t = threadIdx.x; t < (M + 1) * 2 * nr; t += blockDim.x) {
@@ -1832,7 +1839,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   }
   // step 4a: grid samples -> coefficients
   if (!H->grid_ids.empty()) {
-    const size_t shm = (size_t)(3 * H->qmax + H->cmax + 8 * H->nrmax) * sizeof(double);
+    const size_t shm = (size_t)(3 * H->qmax + 1 + H->cmax + 8 * H->nrmax) * sizeof(double);
     if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(k_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     k_transform<<<(unsigned)H->grid_ids.size(), 128, shm, s>>>(H->d_grid_ids, (int64_t)H->grid_ids.size(),
                                                                    H->d_gnr, H->d_gna, H->d_goff, H->d_coff,
