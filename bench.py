@@ -60,7 +60,7 @@ def load_fp64_peak():
 PAIR_MIX_CYCLES = 47.22
 
 # ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
-TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01w_ncu_full_pairs_grid.json"}
+TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01x_ncu_full_pairs_grid.json"}
 
 
 def profiled_traffic(kernel, config, mode):
