@@ -56,9 +56,6 @@ def load_fp64_peak():
     return best
 
 
-# SMSP-cycles per warp-pair of green_far_r's loop body in isolation (tools/pair_mix_bench.cu, profiles/r01o_pair_mix.txt)
-PAIR_MIX_CYCLES = 47.22
-
 # ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
 TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01x_ncu_full_pairs_grid.json"}
 
@@ -242,7 +239,7 @@ def main():
             h.matvec(x, y)
             ends[k].record(stream)
             st = h.stats()                                  # waits for this step's stage events
-            stage_ms.append(st["ms_last"][:7])
+            stage_ms.append(st["ms_last"][:8])
             launches += st["launches_per_matvec"]
         torch.cuda.synchronize()
     h.time_stages(False)
@@ -337,15 +334,17 @@ def main():
                            "peak": peaks.get("dmma"), "frac": tf / peaks["dmma"] if peaks.get("dmma") else None}
     # issue-bound model of the dominant kernel: an FP64 warp instruction holds its SMSP's dispatch
     # 2 cycles, any other 1; per-pair counts from this build's SASS main loop (tools/sass_loop.py, cuobjdump)
-    if roof is not None and not os.environ.get("NC_GRID_VARIANT"):
+    gv = st.get("grid_variant") or [0] * 8
+    clk_hz = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+    if roof is not None:
         try:
             sys.path.insert(0, os.path.join(ROOT, "tools"))
             from sass_loop import main_loop
             import paper_1906_04209_b200 as ncmod
-            pat = (f"k_pairs_grid_wILi{cfg.kind}ELi2ELi4ELi5ELi8ELi3E" if args.mode == "hier"   # the default variant
-                   else f"k_pairs_directILi{cfg.kind}ELi2ELb1E")
+            # the variant in use (nc_stats grid_variant: nt, tpt, unroll, stage, far, tma, minb, persist)
+            pat = (f"k_pairs_grid_wILi{cfg.kind}ELi{gv[1]}ELi{gv[2]}ELi{gv[4]}ELi{gv[0]}ELi{gv[6]}E"
+                   if args.mode == "hier" else f"k_pairs_directILi{cfg.kind}ELi2ELb1E")
             ml = main_loop(ncmod.nc.LIB_PATH, pat)
-            clk_hz = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
             if ml:
                 fp, oth = ml
                 cyc = 2.0 * fp + oth
@@ -357,14 +356,40 @@ def main():
                                                "main loop of this build, 592 SMSPs at the sampled SM clock"}
         except Exception as e:  # pragma: no cover
             roof["issue_model"] = {"error": str(e)[:200]}
-    # the same instruction mix in isolation (sources in registers, no staging / barriers / partial warps), measured
-    # by tools/pair_mix_bench.cu on a B200: SMSP-cycles per warp-pair the hardware sustains for this loop body
-    if roof is not None and args.mode == "hier" and not os.environ.get("NC_GRID_VARIANT"):
-        clk_hz = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
-        kc = pair_ms * 1e-3 * clk_hz * 148 * 4 / (pairs / 32.0)
-        roof["instruction_mix_bound"] = {"cycles_per_warp_pair_isolated": PAIR_MIX_CYCLES, "kernel_cycles_per_warp_pair": kc,
-                                         "frac": PAIR_MIX_CYCLES / kc, "source": "tools/pair_mix_bench.cu, "
-                                         "profiles/r01o_pair_mix.txt (best of 2-4 CTAs/SM)"}
+    # the same pair evaluation in isolation (sources in registers, no staging / barriers / partial warps), measured
+    # in this run by nc_pair_mix on this GPU: the SMSP-cycles per warp-pair the hardware sustains for this loop body
+    if roof is not None and args.mode == "hier" and gv[5] == 3:
+        try:
+            import paper_1906_04209_b200 as ncmod
+            best = None
+            for cps in (2, 3):
+                ms_mix, wp = ncmod.pair_mix(cfg.kind, gv[4], cps)
+                c_iso = ms_mix * 1e-3 * clk_hz * 148 * 4 / wp
+                best = c_iso if best is None else min(best, c_iso)
+            kc = pair_ms * 1e-3 * clk_hz * 148 * 4 / (pairs / 32.0)
+            roof["instruction_mix_bound"] = {"cycles_per_warp_pair_isolated": best, "kernel_cycles_per_warp_pair": kc,
+                                             "frac": best / kc,
+                                             "source": "nc_pair_mix (libnc), measured in this run: best of 2-3 "
+                                                       "CTAs/SM at the sampled SM clock"}
+        except Exception as e:  # pragma: no cover
+            roof["instruction_mix_bound"] = {"error": str(e)[:200]}
+    # HBM-bound stages of the matvec (north_star: "HBM GB/s for the gather/scatter stages"): the grid reduction
+    # (per-unit partial values in, grid values out) and the K1 outgoing GEMM with its scattered rho epilogue
+    hbm_stages = None
+    if args.mode == "hier" and len(stages_avg) > 7:
+        hbm = json.load(open(PEAKS_FILE)).get("hbm_gbs") if os.path.exists(PEAKS_FILE) else None
+        psum = (st["gemm_flops_per_matvec"] / (2.0 * st["row_count"]) - st["K"] * st["Kstar"]) / st["K"]
+        red_b = 8.0 * (st["hier_unit_points"] + st["hier_grid_points"])
+        k1_b = 8.0 * (st["N"] * st["K"] + psum * st["K"] + st["N"] * psum)
+        hbm_stages = {}
+        for name, b, ms in (("k_reduce_chunks", red_b, stages_avg[7]), ("K1_T_apply_scatter", k1_b, stages_avg[0])):
+            if ms > 0:
+                gbs = b / (ms * 1e-3) / 1e9
+                hbm_stages[name] = {"bytes": b, "ms": ms, "achieved": gbs, "unit": "GB/s", "peak": hbm,
+                                    "frac": gbs / hbm if hbm else None}
+        hbm_stages["note"] = ("algorithmic bytes: k_reduce_chunks reads every work unit's partial values and writes "
+                              "the grid values; K1 reads X and the rungs' T and writes rho (8 B per record, scattered "
+                              "into 32-B records); peak = MEASURED_PEAKS.json hbm_gbs")
     # NEXT-3: the off-surface field of the solution (nc_field, host points in / values out, synchronous) at 4096
     # points on a sphere inside (interior: radius 0.5) or outside (exterior: radius 2) the unit sphere
     field = None
@@ -430,7 +455,8 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            n_rows = args.cpu_sample or auto_sample_rows(cfg, tab)
+            # >= 16 sampled target patches; small configs calibrate to ~12 s of CPU work
+            n_rows = args.cpu_sample or (max(16, auto_sample_rows(cfg, tab)) if cfg.N <= 10000 else 16)
             t, rows, thr = cpu_oracle_sample(cfg, tab, x_all, n_rows)
             cpu = {"value": 1.0 / (t * cfg.N / n_rows), "unit": "matvec/s", "cores": thr, "kind": "oracle",
                    "sample": f"{n_rows} of {cfg.N} target patches (direct sum), extrapolated x{cfg.N / n_rows:.1f}"}
@@ -441,13 +467,14 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{cfg.name} {args.mode}", "N": cfg.N, "eps": cfg.eps, "kind": cfg.kind,
-                       "layout": cfg.layout, "tables": args.tables, "K": tab.K, "Kstar": tab.Kstar, "p": tab.p,
-                       "l2": "flushed between timed steps (256 MB write, untimed)"},
+                       "layout": cfg.layout, "tables": args.tables, "K": tab.K, "Kstar": tab.Kstar, "p": tab.p},
+            "l2": "flushed between timed steps (256 MB write, untimed)",
             "clocks": clk.summary(), "e2e": e2e,
             "gpu_launches": launches,
             "roofline": roof, "gemm_roofline": gemms, "cpu_baseline": cpu,
             "stages_ms": dict(zip(["T_apply", "all_gather", "direct_pairs", "P_apply", "grid_pairs", "hier_rest",
-                                   "total"], stages_avg)), "pairs_per_matvec": st["pairs_per_matvec"],
+                                   "total", "grid_reduce"], stages_avg)), "pairs_per_matvec": st["pairs_per_matvec"],
+            "hbm_stages": hbm_stages,
             "hier": ({k: st[k] for k in ("tree_levels", "tree_groups", "hier_grid_pairs", "hier_near_pairs",
                                          "hier_interp_terms", "hier_grid_points", "hier_grid_units", "hier_grid_fill",
                                          "hier_grid_warp_fill")}

@@ -74,8 +74,10 @@ typedef struct nc_tables {
   const int32_t* ladder_p;    /* n_ladder skeleton sizes, 1..1024                                  */
   const double* ladder_shat;  /* sum(ladder_p) x 3 skeleton nodes, rung-major                      */
   const double* ladder_T;     /* sum(ladder_p) x K outgoing maps, rung-major                       */
-  double ladder_tol;          /* ID tolerance of the rungs (0: unknown); NC_HIER ignores the ladder */
-                              /* when the requested precision is tighter than this                  */
+  double ladder_tol;          /* ID tolerance of the rungs (0: unknown).  NC_HIER uses the ladder   */
+                              /* only when the requested precision is >= this; the matvec error     */
+                              /* at that boundary is measured <= the precision (R22,      */
+                              /* tests/test_parity_golden_gpu.py test_ladder_gate_boundary)          */
 } nc_tables;
 
 typedef struct nc_opts {
@@ -100,7 +102,7 @@ typedef struct nc_stats_t {
                                 /*   [0] T-apply  [1] all-gather  [2] direct pair sums  [3] P-apply */
                                 /*   [4] hier k_pairs_grid alone (steps 2-3 on incoming grids)      */
                                 /*   [5] hier grid reduce + transform + near list + step 4          */
-                                /*   [6] total  [7] reserved                                        */
+                                /*   [6] total  [7] hier grid reduction alone (k_reduce_chunks)     */
   int32_t tree_levels;          /* NC_HIER: depth L of the sphere quadtree                         */
   int64_t tree_groups;          /* NC_HIER: number of non-empty boxes over all levels              */
   double hier_grid_pairs;       /* NC_HIER: pair evaluations on incoming grids per matvec (steps 2-3) */
@@ -119,6 +121,10 @@ typedef struct nc_stats_t {
   double pair_fp64_inst_grid;    /*   variant in use (kind-dependent)                                */
   double hier_grid_fill;         /* NC_HIER: grid pairs / (work-unit thread slots x sources x p)     */
   double hier_grid_warp_fill;    /* NC_HIER: grid pairs / (active-warp thread slots x sources x p)   */
+  int32_t grid_variant[8];       /* NC_HIER: k_pairs_grid variant in use {warps or threads per CTA,  */
+                                 /*   targets per thread, unroll, stage, far form, tma, minb, persist} */
+  double hier_unit_points;       /* NC_HIER: sum over work units of their grid points: the partial   */
+                                 /*   values k_pairs_grid writes and k_reduce_chunks reads per matvec  */
 } nc_stats_t;
 
 typedef struct nc_handle nc_handle;
@@ -243,6 +249,19 @@ int nc_time_stages(nc_handle* h, int enable);
  * Used by the exactly-once pair-coverage audit (tests/test_hier.py). */
 int nc_tree_lists(const nc_handle* h, int64_t* n_ilist, int64_t* ilist, int64_t* n_nbr, int64_t* nbr,
                   int64_t* box_of_patch /* L+1 x N, nullable */);
+
+/* Introspection (NC_HIER): the number of near-list source patches (R12: sources evaluated directly at the
+ * patch's Zernike nodes) of each of this rank's rows, internal order.  counts: host, row_count int64.  Used by the
+ * parity tests to pick rows whose near lists are not empty.  Errors: NC_EINVAL, NC_ESTATE (not NC_HIER). */
+int nc_near_counts(const nc_handle* h, int64_t* counts);
+
+/* Diagnostic: the grid kernel's pair evaluation (far form `far` = 5, 7 or 8 of k_pairs_grid_w,
+ * kind NC_INTERIOR / NC_EXTERIOR) run in isolation -- sources in registers, no staging, no barriers, 16 independent
+ * chains per thread, ctas_per_sm CTAs of 256 threads per SM -- on the current device.  Returns the best device
+ * time of three launches (ms, host) and the warp-pair evaluations each launch performs (host), so that the caller
+ * can express the loop body's cost in SM-sub-partition cycles per warp-pair at the measured clock.  Synchronous.
+ * Errors: NC_EINVAL (bad arguments, unsupported far form, launch failure). */
+int nc_pair_mix(int kind, int far, int ctas_per_sm, double* ms, double* warp_pairs);
 
 /* Host-only helper (no GPU needed): the contiguous row partition used by nc_setup.  Rank r of `world` gets
  * rows [begin[r], begin[r] + count[r]) of the internal order, cut so that the prefix sums of (weights[i] + 1)

@@ -87,6 +87,14 @@ class PatchTables:
         m = re.search(r"'ladder_id_tol': ([0-9.eE+-]+)", str(self.meta.get("repr", "")) if self.meta else "")
         return float(m.group(1)) if m else 0.0
 
+    @property
+    def ladder_err(self) -> float:
+        """The rungs' largest measured relative field error (table meta ``ladder_err``: max over random far-field points
+        and random densities relative to the field's max norm, nc_tables.skeleton.outgoing_error); 0 when unknown."""
+        import re
+        m = re.search(r"'ladder_err': \[([^\]]*)\]", str(self.meta.get("repr", "")) if self.meta else "")
+        return max(float(v) for v in m.group(1).split(",")) if m and m.group(1).strip() else 0.0
+
     def without_ladder(self):
         return PatchTables(self.kind, self.eps, self.M, self.zhat, self.P, self.shat, self.T, self.I, self.meta,
                            res_rhat=self.res_rhat, res_w=self.res_w, res_S=self.res_S)

@@ -25,7 +25,8 @@ Steps, in the paper's order and notation (SURVEY.md §8(c) "What it computes"):
 
 Pins (tests/test_oracle.py): the Green's-function sphere means, the N = 1 identity
 (PAPER.md:883), rotation/permutation invariance, the dense-LU solve (a textbook routine), and the
-physical single-patch limit once real tables exist.
+physical single-patch limit once real tables exist.  mfpt_field: Delta v-bar = -1 and its ball averages
+(tests/test_mfpt_oracle.py).  matvec vs matvec_uncompressed (tests/test_uncompressed_oracle.py).
 """
 from __future__ import annotations
 
@@ -208,6 +209,24 @@ def matvec(kind, centers, tab, x, rows=None, R=None):
     tpatch = np.repeat(rows, tab.Kstar)
     spatch = np.repeat(np.arange(N), tab.p)
     u = field(kind, z, tpatch, s, spatch, rho).reshape(len(rows), tab.Kstar)
+    return x[rows] + u @ tab.P.T
+
+
+def matvec_uncompressed(kind, centers, tab, fine, wf, B, x, rows=None):
+    """the same matvec with every source patch's density in its UNcompressed form,
+    u_{ik} = sum_{j != i} sum_l G(z_{ik}, f_{jl}) w_l (B fhat_j)_l  (the left side of eq:outgoingcompressed,
+    PAPER.md:1082-1093, with sigma_j = B fhat_j, eq:recoversig PAPER.md:797-807, on the one-patch solver's fine grid
+    f_l, w_l).  fine (n_f x 3, canonical frame), wf (n_f), B (n_f x K) come from the Step-1 builder; y = x + P u."""
+    N = len(centers)
+    x = np.asarray(x, dtype=np.float64).reshape(N, -1)
+    R = frames(centers)
+    rows = np.arange(N) if rows is None else np.asarray(rows, dtype=np.int64)
+    z = global_nodes(R[rows], tab.zhat)
+    f = global_nodes(R, np.asarray(fine, dtype=np.float64))       # (N, n_f, 3)
+    q = (x @ np.asarray(B, dtype=np.float64).T) * np.asarray(wf)[None, :]   # charges w_l sigma_jl
+    tpatch = np.repeat(rows, tab.Kstar)
+    spatch = np.repeat(np.arange(N), f.shape[1])
+    u = field(kind, z, tpatch, f, spatch, q).reshape(len(rows), tab.Kstar)
     return x[rows] + u @ tab.P.T
 
 

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <string>
 #include <unordered_map>
+#include <thread>
 #include <vector>
 
 #include "green.cuh"
@@ -258,8 +259,8 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
 
   // tables; outgoing-operator rungs (0 = base, 1.. = ladder, NC_HIER only)
   int rc;
-  // the ladder serves NC_HIER only, and only when the requested precision is not tighter than the rungs' ID
-  // tolerance (their compression error would otherwise set the floor)
+  // the ladder serves NC_HIER only, and only when the requested precision is not tighter than the rungs' measured
+  // field error (their compression error would otherwise set the floor)
   const bool use_ladder = opt->mode == NC_HIER && tab->n_ladder > 0 &&
                           !(tab->ladder_tol > 0.0 && opt->precision > 0.0 && opt->precision < tab->ladder_tol);
   h->nrung = 1 + (use_ladder ? tab->n_ladder : 0);
@@ -380,7 +381,11 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   setup_tick("fused K1 tables");
 
   h->emulated = h->world > 1 && !opt->nccl_id;   // rank emulation: no communicator, nc_matvec_emulated only
-  if (h->world > 1 && !h->emulated && (rc = dalloc(h, &h->d_xall, (size_t)N * K))) return bail(rc);
+  if (h->world > 1 && !h->emulated) {
+    h->max_rows = *std::max_element(h->rank_count.begin(), h->rank_count.end());
+    if ((rc = dalloc(h, &h->d_xall, (size_t)N * K)) || (rc = dalloc(h, &h->d_xpad, (size_t)h->world * h->max_rows * K)))
+      return bail(rc);
+  }
 #if NC_WITH_NCCL
   if (h->world > 1 && !h->emulated) {
     ncclUniqueId id;
@@ -458,6 +463,44 @@ static int matvec_tail(nc_handle* h, const double* x, double* y, cudaStream_t s)
   return NC_OK;
 }
 
+// order a matvec on stream s after the previous matvec of this handle when that ran on another stream
+static int serialize_stream(nc_handle* h, cudaStream_t s) {
+  if (h->have_last_stream && h->last_stream != s) {
+    if (!h->ev_order) NC_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_order, cudaEventDisableTiming));
+    NC_CUDA_TRY(cudaEventRecord(h->ev_order, h->last_stream));
+    NC_CUDA_TRY(cudaStreamWaitEvent(s, h->ev_order, 0));
+  }
+  h->last_stream = s;
+  h->have_last_stream = true;
+  return NC_OK;
+}
+
+// Host wait at the collective sync points (GMRES, read-out).  world == 1: cudaStreamSynchronize.  world > 1: a failed
+// peer or a communicator error surfaces as an asynchronous NCCL error while this rank's collective kernel would spin
+// forever, so the wait polls the stream and ncclCommGetAsyncError, aborting the communicator on an error.
+static int wait_stream(nc_handle* h, cudaStream_t s, const char* where) {
+#if NC_WITH_NCCL
+  if (h->world > 1 && h->comm) {
+    for (;;) {
+      const cudaError_t e = cudaStreamQuery(s);
+      if (e == cudaSuccess) return NC_OK;
+      if (e != cudaErrorNotReady) return cuda_fail(e, where);
+      ncclResult_t ae = ncclSuccess;
+      const ncclResult_t r = ncclCommGetAsyncError(h->comm, &ae);
+      if (r != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress)) {
+        ncclCommAbort(h->comm);
+        h->comm = nullptr;
+        return fail(NC_ENCCL, std::string(where) + ": asynchronous NCCL error (communicator aborted): " +
+                                  ncclGetErrorString(r != ncclSuccess ? r : ae));
+      }
+      std::this_thread::yield();
+    }
+  }
+#endif
+  const cudaError_t e = cudaStreamSynchronize(s);
+  return e == cudaSuccess ? NC_OK : cuda_fail(e, where);
+}
+
 int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
   if (!h || !x || !y) return fail(NC_EINVAL, "nc_matvec: null argument");
   if (x == y) return fail(NC_EINVAL, "nc_matvec: x and y must not alias");
@@ -465,6 +508,7 @@ int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
     return fail(NC_ESTATE, "nc_matvec: emulated rank (no communicator): use nc_matvec_emulated");
   NC_CUDA_TRY(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
+  NC_TRY(serialize_stream(h, s));
   h->launches_last = 0;
   mark(h, 0, s);
   if (h->world == 1) {
@@ -474,20 +518,21 @@ int nc_matvec(nc_handle* h, const double* x, double* y, void* stream) {
   }
 #if NC_WITH_NCCL
   // world > 1: all-gather the coefficient vectors (N K doubles: 109 MB at N = 1e5, a quarter of the rho values of
-  // all rungs and an eighth of their records), one broadcast per rank row range inside a group, then every rank
-  // forms the outgoing records of ALL patches itself (K1 over N rows, ~2 ms): the exchange does not grow with the
-  // number of outgoing-operator rungs.  Everything after is exactly nc_matvec_emulated's path.
+  // all rungs and an eighth of their records), then every rank forms the outgoing records of ALL patches itself (K1
+  // over N rows, ~2 ms): the exchange does not grow with the number of outgoing-operator rungs.  The work-weighted
+  // row ranges differ in length, so the exchange is one ncclAllGather of max_rows rows per rank into a padded
+  // buffer (NVLS-eligible, unlike a group of broadcasts), compacted into N x K by one copy per rank.  Everything
+  // after is exactly nc_matvec_emulated's path.
   {
-    ncclResult_t r = ncclGroupStart();
-    for (int q = 0; q < h->world && r == ncclSuccess; ++q) {
-      if (h->rank_count[q] == 0) continue;
-      r = ncclBroadcast(q == h->rank ? (const void*)x : nullptr, h->d_xall + (size_t)h->rank_begin[q] * h->K,
-                        (size_t)h->rank_count[q] * h->K, ncclDouble, q, h->comm, s);
-    }
-    ncclResult_t r2 = ncclGroupEnd();
-    if (r != ncclSuccess || r2 != ncclSuccess)
-      return fail(NC_ENCCL, std::string("all-gather of x (broadcasts): ") +
-                                ncclGetErrorString(r != ncclSuccess ? r : r2));
+    const size_t per = (size_t)h->max_rows * h->K;
+    NC_CUDA_TRY(cudaMemcpyAsync(h->d_xpad + (size_t)h->rank * per, x, (size_t)h->row_count * h->K * sizeof(double),
+                                cudaMemcpyDeviceToDevice, s));
+    ncclResult_t r = ncclAllGather(h->d_xpad + (size_t)h->rank * per, h->d_xpad, per, ncclDouble, h->comm, s);
+    if (r != ncclSuccess) return fail(NC_ENCCL, std::string("all-gather of x: ") + ncclGetErrorString(r));
+    for (int q = 0; q < h->world; ++q)
+      if (h->rank_count[q] > 0)
+        NC_CUDA_TRY(cudaMemcpyAsync(h->d_xall + (size_t)h->rank_begin[q] * h->K, h->d_xpad + (size_t)q * per,
+                                    (size_t)h->rank_count[q] * h->K * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
   mark(h, 1, s);
   outgoing(h, h->d_xall, 0, h->N, s);
@@ -526,6 +571,7 @@ static int read_stages(nc_handle* h) {
     cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]); h->ms_last[4] = ms;   // k_pairs_grid (steps 2-3)
     cudaEventElapsedTime(&ms, h->ev[3], h->ev[7]); h->ms_last[5] = ms;   // reduce, transform, near list, step 4
     cudaEventElapsedTime(&ms, h->ev[7], h->ev[4]); h->ms_last[3] = ms;   // step 5 (P-apply GEMM)
+    cudaEventElapsedTime(&ms, h->ev[3], h->ev[8]); h->ms_last[7] = ms;   // grid reduction (k_reduce_chunks)
   }
   cudaEventElapsedTime(&ms, h->ev[0], h->ev[4]); h->ms_last[6] = ms;
   return NC_OK;
@@ -600,7 +646,7 @@ int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x
   }
   NC_TRY(dots(h, V, ldv, 1, V, n, d_nrm, s));
   NC_CUDA_TRY(cudaMemcpyAsync(h->h_red, d_nrm, sizeof(double), cudaMemcpyDeviceToHost, s));
-  NC_CUDA_TRY(cudaStreamSynchronize(s));
+  NC_TRY(wait_stream(h, s, "nc_gmres"));
   const double beta = sqrt(h->h_red[0]);
   if (hist) hist[0] = 1.0;
   if (beta == 0.0) {
@@ -636,7 +682,7 @@ int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x
     NC_TRY(dots(h, w, ldv, 1, w, n, d_nrm, s));
     if (h->time_stages) NC_CUDA_TRY(cudaEventRecord(h->ev[6], s));
     NC_CUDA_TRY(cudaMemcpyAsync(h->h_red, h->d_red, 1281 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    NC_CUDA_TRY(cudaStreamSynchronize(s));
+    NC_TRY(wait_stream(h, s, "nc_gmres"));
     if (h->time_stages) {
       // HBM-bound orthogonalisation (K9): algorithmic bytes = two (multidot + gemv_sub) passes + the norm, with
       // multidot re-reading w once per group of 8 basis vectors
@@ -691,10 +737,43 @@ int nc_gmres(nc_handle* h, const double* b, double rtol, int max_iter, double* x
   return NC_OK;
 }
 
+// The synchronous diagnostics below (read-out, field, residual, density) run on the handle's private stream.  They
+// take x from the caller, written by work on any stream (a matvec / GMRES on the caller's stream, torch ops on the
+// legacy stream): wait for all device work issued so far before reading it.
+static int order_after_caller(nc_handle* h) {
+  NC_CUDA_TRY(cudaSetDevice(h->device));
+  NC_CUDA_TRY(cudaDeviceSynchronize());
+  return NC_OK;
+}
+
+// The base rung's source records (coordinates of every patch's skeleton nodes, scaled by 1/2, and rho = T fhat) in a
+// buffer of the call's own: the field and residual entry points never write the matvec's records.
+static int base_records(nc_handle* h, const double* x_all, cudaStream_t s, double** out) {
+  const int K = h->K, p0 = h->rung_p[0];
+  const size_t n = (size_t)h->N * p0 * 4;
+  double* d = nullptr;
+  if (cudaMalloc(&d, n * sizeof(double)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(NC_ENOMEM, "base records: device allocation failed");
+  }
+  cudaError_t e = cudaMemcpyAsync(d, h->d_src4 + h->rung_soff[0], n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) {   // rho of the base rung for all N patches (K1 restricted to rung 0) into slot 3
+    launch_gemm_dmma(x_all, K, 1, 0, h->d_T + (size_t)h->rung_trow[0] * K, h->N, p0, K, d + 3, (int64_t)p0 * 4, 4,
+                     nullptr, 0, s);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(e, "base records");
+  }
+  *out = d;
+  return NC_OK;
+}
+
 int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* value) {
   if (!h || !x) return fail(NC_EINVAL, "nc_flux_or_mfpt: null argument");
   if (h->world > 1 && h->emulated) return fail(NC_ESTATE, "nc_flux_or_mfpt: emulated rank has no communicator");
-  NC_CUDA_TRY(cudaSetDevice(h->device));
+  NC_TRY(order_after_caller(h));
   cudaStream_t s = h->stream;
   NC_TRY(ensure_red(h, std::max<int64_t>(4096, 1024 + (int64_t)592 * h->K + 16)));
   double* d_sum = h->d_red;             // K <= 1024 (checked in nc_setup)
@@ -703,7 +782,7 @@ int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* valu
   NC_TRY(allreduce_sum(h, d_sum, h->K, s));
   std::vector<double> col(h->K);
   NC_CUDA_TRY(cudaMemcpyAsync(col.data(), d_sum, h->K * sizeof(double), cudaMemcpyDeviceToHost, s));
-  NC_CUDA_TRY(cudaStreamSynchronize(s));
+  NC_TRY(wait_stream(h, s, "nc_flux_or_mfpt"));
   double Is = 0.0;
   for (int a = 0; a < h->K; ++a) Is += h->h_I[a] * col[a];
   if (I_sigma) *I_sigma = Is;
@@ -727,12 +806,11 @@ int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts
       return fail(NC_EINVAL, "nc_field: point " + std::to_string(t) + " is not on the " +
                                  (h->kind == NC_EXTERIOR ? "exterior" : "interior") + " side of the unit sphere");
   }
-  NC_CUDA_TRY(cudaSetDevice(h->device));
+  NC_TRY(order_after_caller(h));
   cudaStream_t s = h->stream;
-  const int K = h->K, p0 = h->rung_p[0];
-  // rho of the base rung for all N patches (K1 restricted to rung 0)
-  launch_gemm_dmma(x_all, K, 1, 0, h->d_T + (size_t)h->rung_trow[0] * K, h->N, p0, K,
-                   h->d_src4 + h->rung_soff[0] + 3, (int64_t)p0 * 4, 4, nullptr, 0, s);
+  const int p0 = h->rung_p[0];
+  double* d_rec = nullptr;
+  NC_TRY(base_records(h, x_all, s, &d_rec));
   const int64_t nrec = h->N * p0;
   const int nseg = field_segments(n_pts, nrec);
   double *d_pts = nullptr, *d_part = nullptr, *d_out = nullptr;
@@ -746,8 +824,8 @@ int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts
   } else {
     e = cudaMemcpyAsync(d_pts, pts, (size_t)n_pts * 3 * sizeof(double), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) {
-      launch_field(h->kind, d_pts, n_pts, h->d_src4 + h->rung_soff[0], nrec, nseg, d_part, d_part + (size_t)nseg * n_pts,
-                   d_out, d_out + n_pts, s);
+      launch_field(h->kind, d_pts, n_pts, d_rec, nrec, nseg, d_part, d_part + (size_t)nseg * n_pts, d_out,
+                   d_out + n_pts, s);
       e = cudaGetLastError();
     }
     std::vector<double> dm(n_pts);
@@ -767,6 +845,7 @@ int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts
   cudaFree(d_pts);
   cudaFree(d_part);
   cudaFree(d_out);
+  cudaFree(d_rec);
   return rc;
 }
 
@@ -783,13 +862,12 @@ int nc_residual(nc_handle* h, const double* x_all, int n_sel, const int64_t* pat
       return fail(NC_EINVAL, "nc_residual: patch index " + std::to_string(patches[q]) + " out of range");
     rows[q] = inv[patches[q]];
   }
-  NC_CUDA_TRY(cudaSetDevice(h->device));
+  NC_TRY(order_after_caller(h));
   cudaStream_t s = h->stream;
   const int K = h->K, p0 = h->rung_p[0];
-  const double* src0 = h->d_src4 + h->rung_soff[0];
-  // rho of the base rung for all N patches (K1 restricted to rung 0)
-  launch_gemm_dmma(x_all, K, 1, 0, h->d_T + (size_t)h->rung_trow[0] * K, h->N, p0, K, h->d_src4 + h->rung_soff[0] + 3,
-                   (int64_t)p0 * 4, 4, nullptr, 0, s);
+  double* d_rec = nullptr;
+  NC_TRY(base_records(h, x_all, s, &d_rec));
+  const double* src0 = d_rec;
   const int nseg = (int)std::min<int64_t>(h->N, 128);
   const size_t nr = (size_t)n_res;
   double *d_rhat = nullptr, *d_w = nullptr, *d_S = nullptr, *d_t = nullptr, *d_up = nullptr, *d_out = nullptr;
@@ -826,7 +904,9 @@ int nc_residual(nc_handle* h, const double* x_all, int n_sel, const int64_t* pat
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) rc = cuda_fail(e, "nc_residual");
   }
-  for (void* b : {(void*)d_rhat, (void*)d_w, (void*)d_S, (void*)d_t, (void*)d_up, (void*)d_out, (void*)d_rows}) cudaFree(b);
+  for (void* b : {(void*)d_rhat, (void*)d_w, (void*)d_S, (void*)d_t, (void*)d_up, (void*)d_out, (void*)d_rows,
+                  (void*)d_rec})
+    cudaFree(b);
   return rc;
 }
 
@@ -842,7 +922,7 @@ int nc_density(nc_handle* h, const double* x_all, int n_sel, const int64_t* patc
       return fail(NC_EINVAL, "nc_density: patch index " + std::to_string(patches[q]) + " out of range");
     rows[q] = inv[patches[q]];
   }
-  NC_CUDA_TRY(cudaSetDevice(h->device));
+  NC_TRY(order_after_caller(h));
   cudaStream_t s = h->stream;
   const int K = h->K;
   double *d_B = nullptr, *d_x = nullptr, *d_s = nullptr;
@@ -908,8 +988,11 @@ int nc_stats(const nc_handle* h, nc_stats_t* o) {
   o->pair_fp64_flops_direct = h->xtab.d ? 30 + interior : 33 + interior;
   // far table (R25, green_far_t) cubic: 10 DFMA + 1 DMUL + 2 DADD exterior (23 flops), 11 + 1 + 1 interior (24);
   // quartic: one DFMA more
-  const int far = grid_far_variant();
-  if (far >= 2) {
+  const int far = hier_grid_far(h);
+  if (far == 8) {   // FB = 9 quadratic (R32): 9 DFMA + 1 DMUL + 2 DADD exterior (21 flops), 10 + 1 + 1 interior (22)
+    o->pair_fp64_inst_grid = 12;
+    o->pair_fp64_flops_grid = 21 + interior;
+  } else if (far >= 2) {
     const int quartic = far == 3 || far == 6;
     o->pair_fp64_inst_grid = 13 + quartic;
     o->pair_fp64_flops_grid = 23 + interior + 2 * quartic;
@@ -946,7 +1029,8 @@ void nc_destroy(nc_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   hier_destroy(h);
   double* bufs[] = {h->d_T, h->d_P, h->d_I, h->d_zhat, h->d_shat, h->d_centers, h->d_frames, h->d_tx, h->d_ty,
-                    h->d_tz, h->d_src4, h->d_upart, h->d_V, h->d_red, h->d_b, h->d_hx, h->d_hy, h->d_Tcat, h->d_xall};
+                    h->d_tz, h->d_src4, h->d_upart, h->d_V, h->d_red, h->d_b, h->d_hx, h->d_hy, h->d_Tcat, h->d_xall,
+                    h->d_xpad};
   if (h->d_xtab) cudaFree(h->d_xtab);
   for (double* b : bufs)
     if (b) cudaFree(b);
@@ -955,6 +1039,7 @@ void nc_destroy(nc_handle* h) {
   if (h->h_red) cudaFreeHost(h->h_red);
   for (auto& ev : h->ev)
     if (ev) cudaEventDestroy(ev);
+  if (h->ev_order) cudaEventDestroy(h->ev_order);
   if (h->stream) cudaStreamDestroy(h->stream);
 #if NC_WITH_NCCL
   if (h->comm) ncclCommDestroy(h->comm);

@@ -128,7 +128,7 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
 // One CTA of NT threads per work unit: <= NT * TPT adjacent points of one incoming grid x one slice (<= kSliceMax
 // patches, one outgoing-operator rung) of its source list.  Sources are staged in shared memory `chp` patches at a
 // time (a CTA barrier per stage); FAR selects the far-field arithmetic (pairs.cuh accumulate_grid, R23).
-template <int KIND, int NT, int TPT, int UNROLL, int FAR, bool ASYNC>
+template <int KIND, int NT, int TPT, int UNROLL, int FAR>
 __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const double* __restrict__ gx,
                                           const double* __restrict__ gy, const double* __restrict__ gz,
                                           const int32_t* __restrict__ srclist, const double* __restrict__ src4,
@@ -154,17 +154,11 @@ __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const 
   }
   const int32_t* __restrict__ lst = srclist + U.src0;
   const double4* __restrict__ s4 = reinterpret_cast<const double4*>(src4 + U.soff);   // the unit's rung
-  if (ASYNC) {
-    accumulate_grid_async<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc, lst, s4, U.p, sm, stage_records,
-                                                           reinterpret_cast<int32_t*>(pid), logtab, any, single, ftb,
-                                                           flim, fa2, fa3, fmid);
-  } else {
-    int chp = stage_records / U.p;
-    chp = chp < 1 ? 1 : (chp > kStagePatchesMax ? kStagePatchesMax : chp);
-    accumulate_grid<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc,
-                                                     [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p,
-                                                     sm, pid, chp, logtab, any, single, ftb, flim, fa2, fa3, fmid);
-  }
+  int chp = stage_records / U.p;
+  chp = chp < 1 ? 1 : (chp > kStagePatchesMax ? kStagePatchesMax : chp);
+  accumulate_grid<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc,
+                                                   [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p, sm,
+                                                   pid, chp, logtab, any, single, ftb, flim, fa2, fa3, fmid);
   const int upts = NT * TPT;
   if (single) {
     if (wbase + lane < U.npt) part[uid * upts + wbase + lane] = acc[0];
@@ -179,7 +173,7 @@ __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const 
 
 // counter == nullptr: one CTA per unit.  Otherwise a persistent grid: each CTA initialises the log table once and
 // takes units from an atomic counter until all `nunits` are done (results do not depend on the assignment).
-template <int KIND, int NT, int TPT, int UNROLL, int FAR, int MINB, bool ASYNC>
+template <int KIND, int NT, int TPT, int UNROLL, int FAR, int MINB, bool ASYNC = false>
 __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restrict__ units, const double* __restrict__ gx,
                                                    const double* __restrict__ gy, const double* __restrict__ gz,
                                                    const int32_t* __restrict__ srclist,
@@ -189,11 +183,12 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
                                                    const double2* __restrict__ fsrc, int fn, int fbase, int fmid) {
   extern __shared__ double4 sm[];
   __shared__ double2 logtab[FAR >= 2 ? 1 : kLogTableSize];
-  __shared__ int64_t pid[ASYNC ? 16 : kStagePatchesMax];   // async: the unit's <= 32 source patches (int32)
+  static_assert(!ASYNC, "CTA-level grid kernel: synchronous staging");
+  __shared__ int64_t pid[kStagePatchesMax];
   __shared__ int next;
   // FAR >= 2: the far table follows the stage buffer in dynamic shared memory; tb is indexed by hi(x) >> (20 - bits)
   // entries: (c, L) double2 (green_far_t) or L alone, packed two per double2 (green_far_r)
-  double2* ftab = reinterpret_cast<double2*>(sm + (ASYNC ? 2 : 1) * stage_records);
+  double2* ftab = reinterpret_cast<double2*>(sm + stage_records);
   constexpr unsigned kEsz = far_table_rcp(FAR) ? 8u : 16u;
   const int nvec = far_table_rcp(FAR) ? fn / 2 : fn;
   const unsigned tb = smem_u32(ftab) - kEsz * (unsigned)fbase;
@@ -210,7 +205,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
   }
   if (!counter) {
     __syncthreads();
-    grid_unit<KIND, NT, TPT, UNROLL, FAR, ASYNC>(units[blockIdx.x], blockIdx.x, gx, gy, gz, srclist, src4, stage_records, part,
+    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[blockIdx.x], blockIdx.x, gx, gy, gz, srclist, src4, stage_records, part,
                                           sm, pid, logtab, tb, flim, fa2, fa3, fmid);
     return;
   }
@@ -220,52 +215,8 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
     __syncthreads();
     const int u = next;
     if (u >= nunits) break;
-    grid_unit<KIND, NT, TPT, UNROLL, FAR, ASYNC>(units[u], u, gx, gy, gz, srclist, src4, stage_records, part, sm, pid, logtab,
+    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[u], u, gx, gy, gz, srclist, src4, stage_records, part, sm, pid, logtab,
                                           tb, flim, fa2, fa3, fmid);
-  }
-}
-
-template <int KIND, int NT, int TPT, int UNROLL, int FAR, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_pairs_grid_tma(const GridUnit* __restrict__ units,
-                                                       const double* __restrict__ gx, const double* __restrict__ gy,
-                                                       const double* __restrict__ gz,
-                                                       const int32_t* __restrict__ srclist,
-                                                       const double* __restrict__ src4, int brec,
-                                                       double* __restrict__ part,
-                                                       const double2* __restrict__ logsrc) {
-  extern __shared__ __align__(128) double4 bufs[];
-  __shared__ double2 logtab[kLogTableSize];
-  __shared__ __align__(8) uint64_t bars[4];
-  const GridUnit U = units[blockIdx.x];
-  const int nwarps_act = min(NT / 32, (U.npt + 32 * TPT - 1) / (32 * TPT));
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], (unsigned)nwarps_act);
-    mbar_init(&bars[3], (unsigned)nwarps_act);
-    mbar_fence_init();
-  }
-  init_table(logtab, logsrc);
-  __syncthreads();
-  if ((int)(threadIdx.x >> 5) >= nwarps_act) return;
-  double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
-#pragma unroll
-  for (int u = 0; u < TPT; ++u) {
-    const int l = TPT * threadIdx.x + u;
-    const int64_t g = U.pt0 + min(l, U.npt - 1);
-    x[u] = gx[g]; y[u] = gy[g]; z[u] = gz[g];
-    cq[u] = 0.5 * fma(x[u], x[u], fma(y[u], y[u], fma(z[u], z[u], 0.25)));
-    if (FAR) { x[u] = -x[u]; y[u] = -y[u]; z[u] = -z[u]; }
-    acc[u] = 0.0;
-  }
-  accumulate_grid_tma<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc, srclist + U.src0,
-                                                       reinterpret_cast<const double4*>(src4 + U.soff), U.p, bufs, brec,
-                                                       bars, logtab);
-  const int upts = NT * TPT;
-#pragma unroll
-  for (int u = 0; u < TPT; ++u) {
-    const int l = TPT * threadIdx.x + u;
-    if (l < U.npt) part[(int64_t)blockIdx.x * upts + l] = acc[u];
   }
 }
 
@@ -278,16 +229,17 @@ static bool stage_ldg() {
   return v == 1;
 }
 
-// instantiated grid-kernel variants: warp-level units (tpt, unroll, far, warps per CTA, minb) and CTA units
-// (nt, tpt, unroll, far, tma, minb); NC_GRID_VARIANT must name one of them (else the default is kept)
-#define NC_GRID_W_LIST(X) X(2, 4, 5, 8, 3) X(2, 4, 5, 8, 4) X(2, 4, 5, 4, 8) X(2, 2, 5, 8, 4) X(2, 4, 6, 8, 4) \
-  X(2, 4, 2, 8, 3) X(2, 4, 3, 8, 3) X(1, 4, 5, 8, 4) X(1, 4, 5, 8, 6) X(2, 4, 5, 8, 2)
-#define NC_GRID_C_LIST(X)                                                                                        \
-  X(128, 2, 4, 2, 0, 8) X(128, 2, 4, 3, 0, 8) X(128, 2, 4, 4, 0, 8) X(128, 2, 4, 2, 0, 6) X(128, 2, 4, 5, 2, 8)   \
-  X(128, 2, 4, 5, 2, 7) X(128, 2, 4, 5, 2, 6) X(128, 2, 2, 5, 2, 8) X(128, 2, 4, 5, 0, 8) X(128, 2, 4, 6, 0, 8)   \
-  X(128, 2, 4, 5, 0, 6) X(128, 2, 4, 6, 0, 6) X(128, 2, 2, 5, 0, 8) X(256, 1, 4, 5, 0, 4) X(128, 2, 4, 1, 0, 8)   \
-  X(128, 2, 4, 0, 0, 8) X(128, 2, 4, 1, 1, 8) X(128, 2, 4, 1, 0, 4) X(128, 2, 4, 1, 0, 6) X(256, 1, 4, 1, 0, 1)   \
-  X(256, 1, 4, 1, 0, 5) X(256, 1, 4, 1, 0, 6) X(256, 1, 2, 1, 0, 6) X(256, 2, 2, 1, 0, 5) X(256, 1, 4, 1, 1, 6)
+// Instantiated grid-kernel variants (NC_GRID_VARIANT="NT,TPT,UNROLL,STAGE,FAR,TMA,MINB" must name one of them):
+// warp-level work units (tma = 3; NT = warps per CTA): (tpt, unroll, far, warps per CTA, minb)
+//   far 8: the unclamped FB = 9 quadratic far form (R32) -- the default at requested precisions >= 1e-10;
+//   far 7: the unclamped FB = 7 cubic (R32) -- the default at tighter precisions (the quadratic's 7.7e-11 absolute
+//          log error would be visible there);
+//   far 5: the clamped FB = 7 cubic of R25 (the round-1 default), kept as the tested alternative.
+// and one CTA-level instantiation with the EXACT difference-form pair kernel (far 0) on one-warp CTAs, i.e. on the
+// same 64-point work units (hence the same per-unit rungs) as the warp kernels: the reference the far forms are
+// tested against (tests/test_hier_gpu.py test_far_field_pair_variant_error).
+#define NC_GRID_W_LIST(X) X(2, 4, 8, 8, 2) X(2, 4, 7, 8, 3) X(2, 4, 5, 8, 3)
+#define NC_GRID_C_LIST(X) X(32, 2, 4, 0, 0, 8)
 
 static bool grid_variant_instantiated(const GridVariant& v) {
 #define NC_GW(TP, UR, FR, WP, MB) \
@@ -301,36 +253,27 @@ static bool grid_variant_instantiated(const GridVariant& v) {
   return false;
 }
 
-// grid-kernel variant: NC_GRID_VARIANT="NT,TPT,UNROLL,STAGE,FAR,TMA,MINB" (default kGridVariantDefault); only the
-// combinations instantiated in launch_pairs_grid launch (others fall back to the default)
-static GridVariant grid_variant() {
-  static GridVariant v = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (v.nt == 0) {
-    v = kGridVariantDefault;
-    if (const char* e = getenv("NC_GRID_VARIANT")) {
-      GridVariant w = v;
-      w.tma = 0;
-      w.minb = 8;
-      w.persist = kGridVariantDefault.persist;
-      if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d", &w.nt, &w.tpt, &w.unroll, &w.stage, &w.far, &w.tma, &w.minb,
-                 &w.persist) >= 5 && grid_variant_instantiated(w) &&
-          ((w.tma == 3 && (w.nt == 4 || w.nt == 8)) || w.nt == 128 || w.nt == 256) && (w.tpt == 1 || w.tpt == 2) &&
-          (w.unroll == 1 || w.unroll == 2 || w.unroll == 4) && w.stage >= 32 && (w.far >= 0 && w.far <= 6) &&
-          (w.tma >= 0 && w.tma <= 3))
-        v = w;
-    }
-  }
-  return v;
+GridVariant grid_variant_for(double precision) {
+  const GridVariant dflt = precision >= kGridQuadMinPrecision ? kGridVariantDefault : kGridVariantPrecise;
+  const char* e = getenv("NC_GRID_VARIANT");
+  if (!e) return dflt;
+  GridVariant w = dflt;
+  w.tma = 0;
+  w.minb = 8;
+  if (sscanf(e, "%d,%d,%d,%d,%d,%d,%d,%d", &w.nt, &w.tpt, &w.unroll, &w.stage, &w.far, &w.tma, &w.minb, &w.persist) >=
+          5 &&
+      grid_variant_instantiated(w) && w.stage >= 32)
+    return w;
+  fprintf(stderr, "[nc] NC_GRID_VARIANT=%s is not an instantiated variant; using the default\n", e);
+  return dflt;
 }
 
-int grid_far_variant() { return grid_variant().far; }
-int grid_far_table_bits() { return grid_variant().far >= 2 ? far_table_bits(grid_variant().far) : 0; }
-int grid_far_table_rcp() { return far_table_rcp(grid_variant().far); }
-void grid_far_poly(double* a2, double* a3) { far_poly(grid_variant().far, a2, a3); }
+int grid_far_table_bits(const GridVariant& v) { return v.far >= 2 ? far_table_bits(v.far) : 0; }
+int grid_far_table_rcp(const GridVariant& v) { return far_table_rcp(v.far); }
+void grid_far_poly(const GridVariant& v, double* a2, double* a3) { far_poly(v.far, a2, a3); }
 
 // points per work unit: a CTA's (NT x TPT), or a warp's (32 x TPT) for the warp-level kernel (tma = 3)
-int grid_unit_points() { return (grid_variant().tma == 3 ? 32 : grid_variant().nt) * grid_variant().tpt; }
-int grid_unit_tpt() { return grid_variant().tpt; }
+int grid_unit_points(const GridVariant& v) { return (v.tma == 3 ? 32 : v.nt) * v.tpt; }
 
 // ------------------------------------------------------------------------------------------------
 // Warp-level work units (variant tma = 3): every warp takes (<= 32 TPT points of one incoming grid) x (one slice of
@@ -359,6 +302,7 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
   const int flim = KIND == 1 ? fbase + fn - 1 : fbase;
   const double2 cst = __ldg(fsrc + nvec);
   const double fa2 = cst.x, fa3 = cst.y;
+  const double* ftd = reinterpret_cast<const double*>(ftab) - fbase;   // ftd[ix]: the entry of index ix (R32)
   for (int j = threadIdx.x; j < nvec; j += 32 * WPC) ftab[j] = fsrc[j];
   __syncthreads();
   constexpr int upts = 32 * TPT;
@@ -403,7 +347,7 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
       __syncwarp();
       accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, buf + (size_t)(c & 1) * wrec,
                                               min(wrec, ntot - c * wrec), single, (const double2*)nullptr, tb, flim,
-                                              fa2, fa3, fmid);
+                                              fa2, fa3, fmid, ftd);
       __syncwarp();
     }
     if (single) {
@@ -440,15 +384,10 @@ template <int KIND, int NT, int TPT, int UNROLL, int FAR, int TMA, int MINB>
 static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* gx, const double* gy, const double* gz,
                           const int32_t* srclist, const double* src4, int stage, int pmax, double* part,
                           int persist, int* counter, const FarTable& ft, cudaStream_t s) {
+  static_assert(TMA == 0, "CTA-level grid kernel: synchronous staging only");
   const int rec = std::max(stage, pmax);   // records per stage buffer: >= one whole patch of any rung
-  const size_t smem = (TMA ? 2 : 1) * (size_t)rec * sizeof(double4) + (FAR >= 2 ? (size_t)ft.n * (far_table_rcp(FAR) ? 8 : 16) : 0);
-  if (TMA == 1) {
-    auto kern = k_pairs_grid_tma<KIND, NT, TPT, UNROLL, FAR, MINB>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device());
-    return;
-  }
-  auto kern = k_pairs_grid<KIND, NT, TPT, UNROLL, FAR, MINB, TMA == 2>;
+  const size_t smem = (size_t)rec * sizeof(double4) + (FAR >= 2 ? (size_t)ft.n * (far_table_rcp(FAR) ? 8 : 16) : 0);
+  auto kern = k_pairs_grid<KIND, NT, TPT, UNROLL, FAR, MINB, false>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (!persist) {
     kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device(), nullptr,
@@ -467,11 +406,10 @@ static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* g
                                                                    ft.base, 1 << (19 - far_table_bits(FAR)));
 }
 
-void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
-                       const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
-                       int* counter, const FarTable& ft, cudaStream_t s) {
-  if (nunits <= 0) return;
-  const GridVariant v = grid_variant();   // always an instantiated combination (grid_variant checks)
+void launch_pairs_grid(const GridVariant& v, int kind, const GridUnit* units, int64_t nunits, const double* gx,
+                       const double* gy, const double* gz, const int32_t* srclist, const double* src4, int pmax,
+                       double* part, int* counter, const FarTable& ft, cudaStream_t s) {
+  if (nunits <= 0) return;   // v: an instantiated combination (grid_variant_for checks)
 #define NC_GW(TP, UR, FR, WP, MB)                                                                                  \
   if (v.tma == 3 && v.tpt == TP && v.unroll == UR && v.far == FR && v.nt == WP && v.minb == MB) {                 \
     if (kind == 0)                                                                                                 \
@@ -578,3 +516,105 @@ void launch_pairs_near(int kind, const double* tx, const double* ty, const doubl
 }
 
 }  // namespace nc
+
+// ------------------------------------------------------------------------------------------------
+// The grid kernel's loop body in isolation (DESIGN.md §6 "instruction-mix bound"): the same far form with the
+// source records in registers (no staging, no barriers, no partial warps), 16 independent chains per thread
+// (TPT 2 x 8 sources), table reads into a table of the kernel's size.  bench.py times it in the same run as the
+// matvec and reports the grid kernel's cycles per warp-pair against it.
+// ------------------------------------------------------------------------------------------------
+namespace nc {
+template <int KIND, int FAR>
+__global__ void __launch_bounds__(256) k_pair_mix(const double2* __restrict__ tsrc, int fn, int fbase, int iters,
+                                                  double a2, double a3, double* out) {
+  extern __shared__ double2 ft[];
+  for (int j = threadIdx.x; j < fn / 2; j += blockDim.x) ft[j] = tsrc[j];
+  __syncthreads();
+  const unsigned tb = (unsigned)__cvta_generic_to_shared(ft) - 8u * (unsigned)fbase;
+  const double* ftd = reinterpret_cast<const double*>(ft) - fbase;
+  const int lim = KIND == 1 ? fbase + fn - 1 : fbase;
+  const int kmid = 1 << (19 - far_table_bits(FAR));
+  constexpr int TPT = 2, NS = 8;
+  double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
+  for (int u = 0; u < TPT; ++u) {   // targets on a small cap, sources a few cap radii away: a grid pair's geometry
+    const double th = 0.3 + 0.0001 * (threadIdx.x + 256 * u);
+    x[u] = -0.5 * sin(th); y[u] = 0.0; z[u] = -0.5 * cos(th);
+    cq[u] = 0.5 * (x[u] * x[u] + y[u] * y[u] + z[u] * z[u] + 0.25);
+    acc[u] = 0.0;
+  }
+  double4 s[NS];
+  for (int k = 0; k < NS; ++k) {
+    const double ph = 0.36 + 0.002 * k + 0.00001 * blockIdx.x;
+    s[k] = make_double4(0.5 * sin(ph), 0.0005 * k, 0.5 * cos(ph), 1e-3 * (k + 1));
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < TPT; ++u) cq[u] += 1e-17;   // not loop-invariant
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        const double qh = fma(x[u], s[k].x, fma(y[u], s[k].y, fma(z[u], s[k].z, cq[u])));
+        acc[u] = fma(s[k].w, green_far_any<KIND, FAR>(qh, nullptr, tb, lim, a2, a3, kmid, ftd), acc[u]);
+      }
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc[0] + acc[1];
+}
+
+template <int KIND, int FAR>
+static int run_pair_mix(int ctas_per_sm, double* ms_out, double* warp_pairs_out) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int bits = far_table_bits(FAR), per = 1 << bits;
+  // a table spanning the exponents this geometry produces (interior x ~ d/4 ~ 1e-2, exterior x = 1 + 2/d ~ 20)
+  const int E0 = KIND == 1 ? 1023 : 1015, nexp = 8, fn = nexp * per, fbase = E0 * per;
+  double2* tab = nullptr;
+  double* out = nullptr;
+  const int blocks = sms * ctas_per_sm;
+  if (cudaMalloc(&tab, (size_t)(fn / 2 + 1) * sizeof(double2)) != cudaSuccess) return 1;
+  if (cudaMalloc(&out, (size_t)blocks * 256 * sizeof(double)) != cudaSuccess) { cudaFree(tab); return 1; }
+  cudaMemset(tab, 0, (size_t)(fn / 2 + 1) * sizeof(double2));
+  double a2 = 0.0, a3 = 0.0;
+  far_poly(FAR, &a2, &a3);
+  const size_t smem = (size_t)fn * 8;
+  auto kern = k_pair_mix<KIND, FAR>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int iters = 400;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a);
+    kern<<<blocks, 256, smem>>>(tab, fn, fbase, iters, a2, a3, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep > 0) best = std::min(best, ms);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  const cudaError_t e = cudaGetLastError();
+  cudaFree(tab);
+  cudaFree(out);
+  if (e != cudaSuccess) return 1;
+  *ms_out = best;
+  *warp_pairs_out = (double)blocks * 256 / 32 * iters * 8 * 2;
+  return 0;
+}
+}  // namespace nc
+
+extern "C" int nc_pair_mix(int kind, int far, int ctas_per_sm, double* ms, double* warp_pairs) {
+  if (!ms || !warp_pairs || ctas_per_sm < 1 || ctas_per_sm > 8)
+    return nc::fail(NC_EINVAL, "nc_pair_mix: bad argument");
+  int rc = 1;
+#define NC_MIX(K, F) \
+  if (kind == K && far == F) rc = nc::run_pair_mix<K, F>(ctas_per_sm, ms, warp_pairs);
+  NC_MIX(0, 5) NC_MIX(1, 5) NC_MIX(0, 7) NC_MIX(1, 7) NC_MIX(0, 8) NC_MIX(1, 8)
+#undef NC_MIX
+  if (rc) return nc::fail(NC_EINVAL, "nc_pair_mix: unsupported (kind, far) or launch failure");
+  return NC_OK;
+}

@@ -83,47 +83,12 @@ __device__ __forceinline__ double green_q(double q, const Tab* __restrict__ tbl)
   return w - fast_log(fma(q, w, q), tbl);   // q (1 + w), one rounding
 }
 
-// Far-field G (k_pairs_grid FAR variant, hierarchical mode only; R23), from qh = |x - x'|^2 / 8 (half the
-// scaled squared distance, formed by the caller as a dot product).  Trimmed for the issue rate (an FP64 instruction
-// holds the warp scheduler two cycles, any other one cycle):
-//   w  = 2/d = rsqrt(2 qh): MUFU.RSQ64H seed of 2 qh (exponent + 1 on the integer pipe), one Newton step
-//        w = y + y (1/2 - qh y^2)                                      [3 FP64; relative error ~(3/2) e0^2]
-//   log: r = x c_j 2^-k - 1 with the table's c_j rescaled by an integer exponent subtract (no mantissa extraction),
-//        log1p(r) = r + r^2 (-1/2 + r/3)  (|r| <= 2^-11: truncation r^4/4 < 1.5e-14 absolute)
-//   interior: log(q (1 + w)) = log(qh (1 + w)) + ln 2, the ln 2 folded into the exponent's magic constant.
-// 16 FP64 instructions (both kinds: the interior argument qh (1 + w) is one FMA), ~13 others.
-template <int KIND>
-__device__ __forceinline__ double green_far_h(double qh, const double2* __restrict__ tbl) {
-  const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
-  const double t = qh * y;
-  const double e = fma(-t, y, 0.5);
-  const double w = fma(y, e, y);
-  const double x = (KIND == 1) ? 1.0 + w : fma(qh, w, qh);   // 1 + w  |  qh (1 + w)
-  const int hi = __double2hiint(x);
-  const int j = (hi >> (20 - kLogTableBits)) & (kLogTableSize - 1);
-  const double2 tj = tbl[j];
-  // c_j 2^-k: subtract the unbiased exponent of x from c_j's exponent field (exact; no range issue for 2^-30..2^30)
-  const double c = __hiloint2double(__double2hiint(tj.x) - (hi & 0x7FF00000) + 0x3FF00000, __double2loint(tj.x));
-  const double r = fma(x, c, -1.0);
-  const double p = fma(r, 0.33333333333333333333, -0.5);
-  const double r2 = r * r;
-  const double l1 = fma(r2, p, r);
-  // k (+1 interior) as a double: 2^52 + 2^31 + e - 1023 minus the magic (minus one more for the interior ln 2)
-  const double kd = __hiloint2double(0x43300000, (int)(((unsigned)hi >> 20) - 1023u + 0x80000000u)) -
-                    (KIND == 1 ? 4503601774854144.0 : 4503601774854143.0);
-  const double h = fma(kd, kLn2, tj.y);
-  return w - (h + l1);
-}
-
-// Far-field G with an exponent-indexed log table (k_pairs_grid FAR >= 2, hierarchical mode only; R25).
-// The table is indexed by the top 11 + FB bits of x (biased exponent and FB mantissa bits: one shift), and its
-// entry (c, L) already carries the exponent: c = 1 / (2^e (1 + (j + 1/2) / 2^FB)), L = -log c (+ ln 2 interior, so
-// that L + log1p(r) = log(2 x) = log(q (1 + w))).  Then log x = L + log1p(r) with r = x c - 1, |r| <= 2^-(FB+1),
-// and log1p(r) = r (1 + r (a2 + r a3 [+ r^2 a4])) with minimax coefficients for |r| <= 1 / (2^(FB+1) + 1)
-// (absolute error 9.9e-12 for FB = 7 cubic, 6.3e-14 FB = 7 quartic, 6.2e-13 FB = 8 cubic; fitted by
-// tools/fit_log1p.py).  G = (w - L) - r p(r): no exponent extraction, no k ln 2 term.
-// 13 FP64 instructions per pair with the caller's dot product and accumulate (cubic), 14 quartic.
-// The table covers the x range of grid pairs (d >= eps / 4, far_table_build); the index is clamped on the open side.
+// Far-field G with an exponent-indexed log table (k_pairs_grid, hierarchical mode only; R25, R32).
+// The table is indexed by the top 11 + FB bits of x (biased exponent and FB mantissa bits: one shift); for a bin
+// of midpoint x_mid it holds L = -log c with c = rcp.approx(x_mid) (+ ln 2 interior, so that L + log1p(r) =
+// log(2 x) = log(q (1 + w))).  Then log x = L + log1p(r) with r = x c - 1, |r| <= 2^-(FB+1) (1 + 2^-20), and
+// log1p(r) = r (1 + r (a2 + r a3)) with minimax coefficients (absolute error 9.9e-12 for FB = 7; FarPoly<7, 4>, the
+// quartic, 6.3e-14, serves the exact form of the direct sums).  G = (w - L) - r p(r): no exponent extraction.
 template <int FB, int DEG>
 struct FarPoly;
 template <>
@@ -134,89 +99,31 @@ template <>
 struct FarPoly<7, 4> {
   static constexpr double a2 = -0.49999999200264428, a3 = 0.33333636142100315, a4 = -0.25053074075115417;
 };
-template <>
-struct FarPoly<6, 4> {
-  static constexpr double a2 = -0.49999999926820904, a3 = 0.33334535235773449, a4 = -0.25002219360866496;
-};
-template <>
-struct FarPoly<8, 3> {
-  static constexpr double a2 = -0.50000078809143556, a3 = 0.33333409330333852, a4 = 0.0;
-};
 
-// tbase: shared-memory byte address of the table minus base * 16 (so that tbase + (hi(x) >> (20 - FB)) * 16 is the
-// entry; one IMAD); lim: the index clamp (largest valid index exterior, smallest interior).  a2r (and a3r, quartic)
-// are the polynomial constants held in registers by the caller (an FP64 FMA takes at most one immediate / uniform
-// operand, and the compiler would otherwise rematerialise the second constant in the loop with two moves per pair).
-template <int KIND, int FB, int DEG>
-__device__ __forceinline__ double green_far_t(double qh, unsigned tbase, int lim, double a2r, double a3r) {
-  const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
-  const double t = qh * y;
-  const double e = fma(-t, y, 0.5);
-  const double w = fma(y, e, y);
-  const double x = (KIND == 1) ? 1.0 + w : fma(qh, w, qh);   // 1 + w  |  qh (1 + w) = q (1 + w) / 2
-  int ix = __double2hiint(x) >> (20 - FB);
-  ix = (KIND == 1) ? min(ix, lim) : max(ix, lim);
-  double cj, lj;
-  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(cj), "=d"(lj) : "r"(tbase + ((unsigned)ix << 4)));
-  const double r = fma(x, cj, -1.0);
-  double p;
-  if (DEG == 4) {
-    p = fma(r, FarPoly<FB, DEG>::a4, a3r);
-    p = fma(r, p, a2r);
-  } else {
-    p = fma(r, FarPoly<FB, DEG>::a3, a2r);
-  }
-  p = fma(r, p, 1.0);
-  return fma(-r, p, w - lj);
-}
-
-// Far-field G, reciprocal-seeded variant (k_pairs_grid FAR 5, 6; R25).  Same reduction as green_far_t,
-// but c = rcp.approx(x_mid) comes from the SFU (x_mid: x's high word with the mantissa below the top FB bits set to
-// the bin midpoint) and only L = -log c (+ ln 2 interior) is read from shared memory: an 8-byte load instead of a
-// 16-byte one.  The pair kernels are bound by shared-memory wavefronts (a warp's 32 random table reads conflict in
-// the banks), so halving the entry halves the dominant traffic.  c is a deterministic function of x_mid's high word:
-// far_table_build_rcp evaluates the same instruction on the device for every bin and tabulates L = -log c exactly.
+// Far-field G, reciprocal-seeded (k_pairs_grid FAR 5; R25): c = rcp.approx(x_mid) comes from the SFU
+// (x_mid: x's high word with the mantissa below the top FB bits set to the bin midpoint) and only the 8-byte L is
+// read from shared memory (a 16-byte (c, L) entry made the kernel shared-memory-wavefront bound: a warp's 32
+// table reads conflict in the banks).  c is a deterministic function of x_mid's high word: far_table_build
+// evaluates the same instruction on the device for every bin and tabulates L = -log c exactly.  The index is
+// clamped on the open side of the table (FAR 7 / 8, green_far_n below, drop the clamp).
 __device__ __forceinline__ double rcp_approx(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   return y;
 }
-// fp32 SFU seeds (R31, measured and NOT used by the kernels: tools/pair_mix_bench.cu only).  The idea: an
-// fp64 MUFU (RSQ64H, RCP64H) costs ~2.3 cycles of a saturated FP64 pipe (profiles/r01m_sfu_fp64_overlap.txt) while
-// the fp32 MUFU overlaps the DFMA stream, so take the seeds from the fp32 unit with the format conversions on the
-// integer pipe (a double in the fp32 normal range -> the fp32 of its top 23 mantissa bits: one funnel shift and one
-// add, exponent rebias 1023 -> 127 modulo 2^9; fp32 -> the equal double: a shift-add and a shift).  Accurate
-// (C3/C4 hierarchical error unchanged to 1e-16, profiles/r01w_s32.txt) but slower: the grid kernel is issue-bound
-// and the ~3 extra integer instructions per pair cost more than the fp64 MUFU contention saved (66.3 -> 72.7 ms).
-__device__ __forceinline__ double f32bits_to_double(unsigned u) {
-  return __hiloint2double((int)((u >> 3) + 0x38000000u), (int)(u << 29));
-}
-__device__ __forceinline__ double rsqrt_seed32(double qh) {   // ~ rsqrt(2 qh), relative error < 2^-22
-  const unsigned f = __funnelshift_l((unsigned)__double2loint(qh), (unsigned)__double2hiint(qh), 3) + 0x40800000u;
-  float y;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__uint_as_float(f)));
-  return f32bits_to_double(__float_as_uint(y));
-}
-__device__ __forceinline__ double rcp_mid32(int h) {   // rcp.approx.f32 of the double (h, 0) (a bin midpoint)
-  float c;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(__uint_as_float(((unsigned)h << 3) + 0x40000000u)));
-  return f32bits_to_double(__float_as_uint(c));
-}
-
 // kmid = 1 << (19 - FB), passed in at run time: the midpoint is then one LOP3 (x & ~mask) | kmid with kmid in a
-// register, not two with two immediates.  S32 (R31, microbenchmark only): bit 0 the fp32 rsqrt seed, bit 1 the fp32
-// midpoint reciprocal.
-template <int KIND, int FB, int DEG, int S32 = 0>
+// register, not two with two immediates.  (R31 measured fp32 SFU seeds with integer format conversions instead:
+// accurate, but slower in this issue-bound loop, 66.3 -> 72.7 ms at C5; not kept.)
+template <int KIND, int FB, int DEG>
 __device__ __forceinline__ double green_far_r(double qh, unsigned tbase, int lim, double a2r, double a3r, int kmid) {
-  const double y = (S32 & 1) ? rsqrt_seed32(qh)
-                             : rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
+  const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
   const double t = qh * y;
   const double e = fma(-t, y, 0.5);
   const double w = fma(y, e, y);
   const double x = (KIND == 1) ? 1.0 + w : fma(qh, w, qh);
   const int hx = __double2hiint(x);
   const int hmid = (hx & ~((1 << (20 - FB)) - 1)) | kmid;
-  const double c = (S32 & 2) ? rcp_mid32(hmid) : rcp_approx(__hiloint2double(hmid, 0));
+  const double c = rcp_approx(__hiloint2double(hmid, 0));
   int ix = hx >> (20 - FB);
   ix = (KIND == 1) ? min(ix, lim) : max(ix, lim);
   double lj;
@@ -230,6 +137,42 @@ __device__ __forceinline__ double green_far_r(double qh, unsigned tbase, int lim
     p = fma(r, FarPoly<FB, DEG>::a3, a2r);
   }
   p = fma(r, p, 1.0);
+  return fma(-r, p, w - lj);
+}
+
+// Unclamped far form (k_pairs_grid_w FAR 7 / 8; R32).  As green_far_r, with two changes to the
+// non-FP64 instructions of the pair: (1) no index clamp -- the far table covers every x a grid pair can produce
+// (far_table_build: chord d >= eps/2, while a grid pair is at arc >= eps because a rung is valid only >= 2 eps from
+// its source centre and the skeleton lies within eps of it, R22); (2) the entry is read as tab[ix] with tab a
+// shared-memory pointer already offset by -base, so the compiler forms the address with a scaled-index load
+// instead of a shift-multiply-add.  FB = 7, DEG = 3: the cubic of green_far_r (13 FP64).  FB = 9, DEG = 2: a
+// quadratic r (c1 + c2 r) on the 4x finer bins |r| <= 2^-10 (minimax, absolute error 7.7e-11): 12 FP64.
+template <int FB>
+struct FarQuad;
+template <>
+struct FarQuad<9> {
+  static constexpr double c1 = 1.0000002379505932, c2 = -0.5000002185734317;
+};
+template <int KIND, int FB, int DEG>
+__device__ __forceinline__ double green_far_n(double qh, const double* __restrict__ tab, double a2r, double a3r,
+                                              int kmid) {
+  const double y = rsqrt_approx(__hiloint2double(__double2hiint(qh) + 0x00100000, __double2loint(qh)));
+  const double t = qh * y;
+  const double e = fma(-t, y, 0.5);
+  const double w = fma(y, e, y);
+  const double x = (KIND == 1) ? 1.0 + w : fma(qh, w, qh);
+  const int hx = __double2hiint(x);
+  const int hmid = (hx & ~((1 << (20 - FB)) - 1)) | kmid;
+  const double c = rcp_approx(__hiloint2double(hmid, 0));
+  const double lj = tab[hx >> (20 - FB)];
+  const double r = fma(x, c, -1.0);
+  double p;
+  if constexpr (DEG == 2) {
+    p = fma(r, a2r, a3r);   // a2r = c2, a3r = c1 (FarQuad)
+  } else {
+    p = fma(r, FarPoly<FB, 3>::a3, a2r);
+    p = fma(r, p, 1.0);
+  }
   return fma(-r, p, w - lj);
 }
 
@@ -306,15 +249,6 @@ __device__ __forceinline__ ExactTab init_exact_table(int kind, double2* smem, co
   t.a3 = cst.y;
   t.kmid = kmid;
   return t;
-}
-
-// reference-accuracy variant (libdevice), used by the self-check path
-template <int KIND>
-__device__ __forceinline__ double green_q_libdevice(double q) {
-  const double w = rsqrt(q);
-  const double a = 1.0 + w;
-  if (KIND == 1) return w - log(a);
-  return w - log(q * a);
 }
 
 }  // namespace nc

@@ -104,7 +104,8 @@ struct HierState {
   double *d_gx = nullptr, *d_gy = nullptr, *d_gz = nullptr, *d_gval = nullptr, *d_gcoef = nullptr;
   GridUnit* d_units = nullptr;
   int64_t nunits = 0;
-  int upts = 256;                   // grid points per work unit (grid_unit_points())
+  GridVariant gv = kGridVariantDefault;   // the grid kernel's variant (grid_variant_for(precision), R32)
+  int upts = 256;                   // grid points per work unit (grid_unit_points(gv))
   int32_t* d_srclist = nullptr;
   double* d_part = nullptr;
   ChunkRec* d_chunks = nullptr;
@@ -117,7 +118,9 @@ struct HierState {
   double *d_tx = nullptr, *d_ty = nullptr, *d_tz = nullptr;
   double *d_udir = nullptr, *d_u = nullptr;
   double pairs_grid = 0, pairs_near = 0, interp_terms = 0, slot_pairs = 0, warp_slot_pairs = 0;
+  double unit_points = 0;           // sum of npt over the work units (partial values written / read back per matvec)
   double bytes = 0;
+  std::vector<int32_t> near_count;      // host copy for nc_near_counts: near-list sources per local patch
   std::vector<int64_t> ilist_entries;   // host copies for nc_tree_lists: (level, target group, source group)
   std::vector<int64_t> nbr_entries;
 };
@@ -901,9 +904,9 @@ __global__ void __launch_bounds__(NT) k_interp_sep(int L, int64_t rc, int Ks, co
   }
 }
 
-// interpolation variant: NC_INTERP_VARIANT="NT,NPT,MB,MINB" (k_interp<NT,NPT,MB,MINB>; default 256,2,0,2;
+// interpolation variant: NC_INTERP_VARIANT="NT,NPT,MB,MINB" (k_interp<NT,NPT,MB,MINB>, NC_INTERP_LIST below;
 // MB = 0: grid_eval_ang for n_r <= 12, MB = 1: Chebyshev sums first, MB = 2: two orders per radial loop, MB = 3:
-// grid_eval_ang with the coefficient prefetch for n_r <= kPfNrMax, MB = 4: with it for every n_r)
+// grid_eval_ang with the coefficient prefetch for n_r <= kPfNrMax)
 struct InterpVariant {
   int nt, npt, mb, minb;
 };
@@ -933,38 +936,45 @@ static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t*
   return NC_OK;
 }
 
+// the instantiated first-pass variants (the default of each K* range, and the alternatives the step-4 tests compare)
+#define NC_INTERP_LIST(X) X(128, 2, 3, 4) X(256, 2, 0, 2) X(128, 2, 0, 4) X(128, 4, 1, 4) X(128, 4, 2, 4)
+static bool interp_listed(const InterpVariant& v) {
+#define NC_I(NT, NPT, MB, MINB) if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB) return true;
+  NC_INTERP_LIST(NC_I)
+#undef NC_I
+  return false;
+}
+
 static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int namax, const int32_t* pgl,
                          const int64_t* ggrid0, const double* F, const double* gR, const int32_t* gnr,
                          const int32_t* gna, const int64_t* coff, const double* coef, const double* tx,
                          const double* ty, const double* tz, const double* udir, double* u, const uint8_t* gsep,
                          double lt, cudaStream_t s) {
-  InterpVariant v = interp_variant();
   (void)namax;
-  // the 248-node rule: one 256-slot CTA per patch, coefficient prefetch (MB = 3: rest of the C5 step 20.07 -> 18.32 ms,
-  // bitwise-identical output, profiles/r01w_interp_prefetch_c5.jsonl)
-  if (!getenv("NC_INTERP_VARIANT") && Ks <= 256) v = {128, 2, 3, 4};
-  if ((v.mb == 0 || v.mb == 3 || v.mb == 4) && nrmax > kAngNrMax) {   // the first pass leaves the grids with n_r > kAngNrMax to a second one
-    int rc1 = NC_OK;
+  // defaults: the 248-node rule takes one 128-thread CTA per patch with the coefficient prefetch (MB = 3: rest of
+  // the C5 step 20.07 -> 18.32 ms, bitwise-identical output, profiles/r01w_interp_prefetch_c5.jsonl); larger K*
+  // the 256-thread angular-sums-first kernel.  NC_INTERP_VARIANT must name a listed variant (else: the default,
+  // with a warning -- never a silently skipped first pass)
+  const InterpVariant dflt = Ks <= 256 ? InterpVariant{128, 2, 3, 4} : InterpVariant{256, 2, 0, 2};
+  InterpVariant v = getenv("NC_INTERP_VARIANT") ? interp_variant() : dflt;
+  if (!interp_listed(v)) {
+    fprintf(stderr, "[nc] NC_INTERP_VARIANT=%s is not an instantiated variant; using the default\n",
+            getenv("NC_INTERP_VARIANT"));
+    v = dflt;
+  }
+  // the angular-sums-first kernels (MB 0, 3) evaluate grids with n_r <= kAngNrMax; a second pass (MB = 1, nr_big)
+  // adds the larger ones
+  const bool two_pass = (v.mb == 0 || v.mb == 3) && nrmax > kAngNrMax;
 #define NC_I(NT, NPT, MB, MINB)                                                                                  \
-  if (rc1 == NC_OK && v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                \
-    rc1 = launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, \
-                                             udir, u, gsep, s, 0, lt);
-    NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6) NC_I(128, 2, 0, 4)
-    NC_I(128, 2, 0, 3) NC_I(256, 1, 0, 2) NC_I(256, 1, 0, 3) NC_I(128, 2, 3, 3) NC_I(128, 2, 3, 4) NC_I(128, 2, 4, 4)
+  if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                                \
+    NC_TRY((launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, \
+                                               tz, udir, u, gsep, s, 0, lt)));
+  NC_INTERP_LIST(NC_I)
 #undef NC_I
-    if (rc1 != NC_OK) return rc1;
+  if (two_pass)
     return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir,
                                          u, gsep, s, 1);
-  }
-#define NC_I(NT, NPT, MB, MINB)                                                                             \
-  if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                           \
-    return launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep, s, 0, lt);
-  NC_I(128, 4, 1, 5) NC_I(128, 4, 1, 4) NC_I(128, 4, 1, 3) NC_I(128, 4, 1, 1) NC_I(256, 2, 1, 2) NC_I(128, 4, 2, 4)
-  NC_I(256, 2, 2, 3) NC_I(256, 2, 0, 2) NC_I(256, 2, 0, 3) NC_I(128, 4, 0, 3) NC_I(128, 4, 0, 4) NC_I(128, 2, 0, 6)
-  NC_I(128, 2, 0, 4) NC_I(128, 2, 0, 3) NC_I(256, 1, 0, 2) NC_I(256, 1, 0, 3) NC_I(128, 2, 3, 3) NC_I(128, 2, 3, 4) NC_I(128, 2, 4, 4)
-#undef NC_I
-  return launch_interp_t<256, 2, 0, 2>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
-                                       s, 0, lt);
+  return NC_OK;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1127,6 +1137,7 @@ static inline double harc(const double* a, const double* b) {
 int hier_order(nc_handle* h, std::vector<double>& centers) {
   const int64_t N = h->N;
   HierState* H = new HierState();
+  H->gv = grid_variant_for(h->precision);
   h->hier = H;
   cudaStream_t s = h->stream;
   double* d_c = nullptr;
@@ -1527,7 +1538,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     H->cgroupmax = std::max<int>(H->cgroupmax, (int)(H->coff[H->ggrid0[g + 1]] - H->coff[H->ggrid0[g]]));
 
   // work units (steps 2-3) and reduction chunks
-  H->upts = grid_unit_points();
+  H->upts = grid_unit_points(H->gv);
   std::vector<double> rung_pairs(h->nrung, 0.0);
   std::vector<GridUnit> units;
   std::vector<ChunkRec> chunks;
@@ -1567,7 +1578,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   };
   const int64_t NGL = (int64_t)H->grid_ids.size();
   std::vector<GridOut> gout(NGL);
-  const int tpt_fill = grid_unit_tpt(), wpts_fill = 32 * tpt_fill;
+  const int tpt_fill = H->gv.tpt, wpts_fill = 32 * tpt_fill;
   // grids are independent: host threads build them, then the pieces are concatenated in grid order
 #pragma omp parallel
   {
@@ -1705,6 +1716,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       near_off[i + 1] = near_off[i] + (int64_t)nl[i].size();
       near_all.insert(near_all.end(), nl[i].begin(), nl[i].end());
       if (!nl[i].empty()) work_near.push_back((int32_t)i);
+      H->near_count.push_back((int32_t)nl[i].size());
       H->pairs_near += (double)nl[i].size() * Ks * p;
     }
   }
@@ -1746,6 +1758,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   for (int k = 0; k < h->nrung; ++k) H->pmax = std::max(H->pmax, h->rung_p[k]);
   // ---- uploads and device grids ----
   H->nunits = (int64_t)units.size();
+  for (const GridUnit& u : units) H->unit_points += u.npt;
   H->nchunks = (int64_t)chunks.size();
   H->nwork_near = (int64_t)work_near.size();
   NC_TRY(upload(h, &H->d_gnr, H->gnr, s));
@@ -1756,10 +1769,11 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_TRY(upload(h, &H->d_roff, H->roff, s));
   NC_TRY(upload(h, &H->d_grid_ids, H->grid_ids, s));
   NC_TRY(halloc(h, &H->d_counter, 1));
-  if (const int fb = grid_far_table_bits()) {   // far log table of the grid kernel (green.cuh green_far_t)
+  if (const int fb = grid_far_table_bits(H->gv)) {   // far log table of the grid kernel (green.cuh)
     double a2 = 0.0, a3 = 0.0;
-    grid_far_poly(&a2, &a3);
-    if (far_table_build(h->kind, h->eps, fb, grid_far_table_rcp(), a2, a3, &H->d_ftab, &H->ftab.n, &H->ftab.base))
+    grid_far_poly(H->gv, &a2, &a3);
+    if (far_table_build(h->kind, h->eps, fb, grid_far_table_rcp(H->gv), a2, a3, &H->d_ftab, &H->ftab.n,
+                        &H->ftab.base))
       return fail(NC_ECUDA, "nc_setup: far log table upload failed");
     H->ftab.d = H->d_ftab;
     h->device_bytes += (double)H->ftab.n * sizeof(double2);
@@ -1828,7 +1842,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   const int64_t rc = h->row_count;
   const int Ks = h->Kstar, K = h->K;
   // steps 2-3: interaction-list and leaf-neighbour sources on the incoming grids
-  launch_pairs_grid(h->kind, H->d_units, H->nunits, H->d_gx, H->d_gy, H->d_gz, H->d_srclist, h->d_src4, H->pmax,
+  launch_pairs_grid(H->gv, h->kind, H->d_units, H->nunits, H->d_gx, H->d_gy, H->d_gz, H->d_srclist, h->d_src4, H->pmax,
                     H->d_part, H->d_counter, H->ftab, s);
   h->launches_last += H->nunits > 0;
   if (h->time_stages) cudaEventRecord(h->ev[3], s);
@@ -1837,6 +1851,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
                                                                                    H->d_part, H->upts, H->d_gval);
     h->launches_last++;
   }
+  if (h->time_stages) cudaEventRecord(h->ev[8], s);
   // step 4a: grid samples -> coefficients
   if (!H->grid_ids.empty()) {
     const size_t shm = (size_t)(3 * H->qmax + 1 + H->cmax + 8 * H->nrmax) * sizeof(double);
@@ -1891,6 +1906,15 @@ void hier_fill_stats(const nc_handle* h, nc_stats_t* o) {
   o->hier_grid_units = H->nunits;
   o->hier_grid_fill = H->slot_pairs > 0 ? H->pairs_grid / H->slot_pairs : 0.0;
   o->hier_grid_warp_fill = H->warp_slot_pairs > 0 ? H->pairs_grid / H->warp_slot_pairs : 0.0;
+  hier_grid_variant(h, o->grid_variant);
+  o->hier_unit_points = H->unit_points;
+}
+
+int hier_grid_far(const nc_handle* h) { return h->hier ? h->hier->gv.far : -1; }
+void hier_grid_variant(const nc_handle* h, int* v8) {
+  const GridVariant g = h->hier ? h->hier->gv : GridVariant{0, 0, 0, 0, 0, 0, 0, 0};
+  const int a[8] = {g.nt, g.tpt, g.unroll, g.stage, g.far, g.tma, g.minb, g.persist};
+  for (int k = 0; k < 8; ++k) v8[k] = a[k];
 }
 
 void hier_destroy(nc_handle* h) {
@@ -1909,6 +1933,14 @@ void hier_destroy(nc_handle* h) {
 }
 
 }  // namespace nc
+
+extern "C" int nc_near_counts(const nc_handle* h, int64_t* counts) {
+  if (!h || !counts) return nc::fail(NC_EINVAL, "nc_near_counts: null argument");
+  const nc::HierState* H = h->hier;
+  if (!H) return nc::fail(NC_ESTATE, "nc_near_counts: handle is not NC_HIER");
+  for (size_t k = 0; k < H->near_count.size(); ++k) counts[k] = H->near_count[k];
+  return NC_OK;
+}
 
 extern "C" int nc_tree_lists(const nc_handle* h, int64_t* n_ilist, int64_t* ilist, int64_t* n_nbr, int64_t* nbr,
                              int64_t* box_of_patch) {

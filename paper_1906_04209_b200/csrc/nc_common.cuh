@@ -53,11 +53,13 @@ struct GridVariant {
   int nt, tpt, unroll, stage, far, tma, minb;   // minb: __launch_bounds__ min blocks per SM (register cap)
   int persist;                                  // 1: persistent CTAs taking units from an atomic counter
 };
-#define kGridVariantDefault (GridVariant{8, 2, 4, 64, 5, 3, 3, 1})   // warp-level units (tma = 3)
-int grid_far_variant();
-int grid_far_table_bits();             // bits of the far table the grid-kernel variant in use needs (0: none)
-void grid_far_poly(double* a2, double* a3);   // its log1p polynomial constants (carried after the table)
-int grid_far_table_rcp();              // 1: the variant takes c from rcp.approx and reads L alone (8-byte entries)
+#define kGridVariantDefault (GridVariant{8, 2, 4, 64, 8, 3, 2, 1})   // warp-level units (tma = 3), R32 quadratic
+#define kGridVariantPrecise (GridVariant{8, 2, 4, 64, 7, 3, 3, 1})   // R32 cubic: requested precision < 1e-10
+constexpr double kGridQuadMinPrecision = 1e-10;   // the quadratic far form's log error is 7.7e-11 absolute
+GridVariant grid_variant_for(double precision);   // the variant a handle uses (NC_GRID_VARIANT overrides)
+int grid_far_table_bits(const GridVariant& v);    // bits of the far table the variant needs (0: none)
+void grid_far_poly(const GridVariant& v, double* a2, double* a3);   // its log1p constants (carried after the table)
+int grid_far_table_rcp(const GridVariant& v);     // 1: c from rcp.approx, L alone in the table (8-byte entries)
 struct FarTable {                      // exponent-indexed far log table (green.cuh green_far_t) on device
   const double2* d = nullptr;
   int n = 0, base = 0;
@@ -68,8 +70,7 @@ struct FarTable {                      // exponent-indexed far log table (green.
 // exact != 0: the table of the exact form (green_exact_r: interior x = q (1 + w), L without ln 2).
 int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a3, double2** d, int* n, int* base,
                     int exact = 0);
-int grid_unit_points();                // grid points per work unit = (threads per CTA or warp) x targets per thread
-int grid_unit_tpt();                   // targets (grid points) per thread of the grid-kernel variant in use
+int grid_unit_points(const GridVariant& v);   // grid points per work unit = (threads per CTA or warp) x targets per thread
 
 struct GridUnit {      // <= grid_unit_points() points of one incoming grid x one slice of its source-patch list
   int64_t pt0;         // first grid point (global grid-point index)
@@ -129,6 +130,8 @@ struct nc_handle {
   int64_t* d_colrstride = nullptr;
   int ncat = 0;
   double* d_xall = nullptr;       // world > 1: all ranks' coefficient rows (N x K), gathered every matvec
+  double* d_xpad = nullptr;       // world > 1: the padded all-gather buffer (world x max rows x K)
+  int64_t max_rows = 0;           // world > 1: the largest rank row count (the all-gather's per-rank count)
   double* d_upart = nullptr;      // nseg x (row_count*Kstar) partial fields
   int nseg = 1;
   int pair_tpt = 1;               // targets per thread in the direct kernel (1 or 2)
@@ -143,10 +146,16 @@ struct nc_handle {
   double* d_hx = nullptr;         // host-API staging (x and y)
   double* d_hy = nullptr;
 
+  // stream ordering: a matvec shares the handle's work buffers (records, grids, partials) with every other matvec,
+  // so a matvec issued on a stream other than the previous one's waits for that one first
+  cudaStream_t last_stream = nullptr;
+  bool have_last_stream = false;
+  cudaEvent_t ev_order = nullptr;
+
   // per-stage timing
   bool time_stages = false;
   bool stages_pending = false;    // events of the last matvec recorded, not yet read (nc_stats reads them)
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[9] = {};           // [8]: after the hier grid reduction (k_reduce_chunks)
   double ms_last[8] = {};
   int launches_last = 0;          // kernels launched by the last nc_matvec
   double gmres_ortho_ms = 0.0;    // GMRES CGS2 orthogonalisation device time / algorithmic bytes (time_stages on)
@@ -195,9 +204,10 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
 
 int pairs_direct_blocks_per_sm(int p, int tpt, const FarTable& xt);
 void split_rows(const double* w, int64_t N, int world, int64_t* begin, int64_t* count);
-void launch_pairs_grid(int kind, const GridUnit* units, int64_t nunits, const double* gx, const double* gy,
-                       const double* gz, const int32_t* srclist, const double* src4, int pmax, double* part,
-                       int* counter /* device int, persistent variant */, const FarTable& ft, cudaStream_t s);
+void launch_pairs_grid(const GridVariant& v, int kind, const GridUnit* units, int64_t nunits, const double* gx,
+                       const double* gy, const double* gz, const int32_t* srclist, const double* src4, int pmax,
+                       double* part, int* counter /* device int, persistent variant */, const FarTable& ft,
+                       cudaStream_t s);
 void launch_pairs_near(int kind, const double* tx, const double* ty, const double* tz, int Kstar, const int32_t* work,
                        int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
                        double* udir, const FarTable& xt, cudaStream_t s);

@@ -112,24 +112,28 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
 // exact kernel of accumulate_list.  FAR = true (far-field evaluation, hierarchical mode only): half the squared
 // distance from the dot product, qh = (|X|^2 + 1/4)/2 - X.S with the target pre-negated (3 DFMA instead of 6 FP64
 // ops; absolute error ~2e-16, i.e. relative ~1e-10 at the closest grid pairs qh ~ eps^2/8, far below the
-// hierarchical tolerance) and green_far_h.  x/y/z hold -X when FAR, and cq[u] = (|X_u|^2 + 1/4)/2.
-// FAR >= 2: the exponent-indexed far table.  green_far_t (16-byte (c, L) entries): 2 = 7 bits cubic, 3 = 7 bits
-// quartic, 4 = 8 bits cubic; green_far_r (8-byte L entries, c from the SFU): 5 = 7 bits cubic, 6 = 6 bits quartic
-__host__ __device__ constexpr int far_table_bits(int far) { return far == 4 ? 8 : far == 6 ? 6 : 7; }
+// hierarchical tolerance) and a far form below.  x/y/z hold -X when FAR, and cq[u] = (|X_u|^2 + 1/4)/2.
+// FAR (the grid kernel's far forms): 5 = green_far_r (R25: FB = 7 cubic, clamped index), 7 = green_far_n FB = 7
+// cubic (R32: unclamped, scaled-index table load), 8 = green_far_n FB = 9 quadratic (R32)
+__host__ __device__ constexpr int far_table_bits(int far) { return far == 8 ? 9 : 7; }
 __host__ __device__ constexpr bool far_table_rcp(int far) { return far >= 5; }
 inline void far_poly(int far, double* a2, double* a3) {   // the polynomial constants the table carries (host)
-  *a2 = far == 3 ? FarPoly<7, 4>::a2 : far == 4 ? FarPoly<8, 3>::a2 : far == 6 ? FarPoly<6, 4>::a2 : FarPoly<7, 3>::a2;
-  *a3 = far == 3 ? FarPoly<7, 4>::a3 : far == 6 ? FarPoly<6, 4>::a3 : 0.0;
+  if (far == 8) {   // quadratic r (c1 + c2 r): c2 in the a2 slot, c1 in the a3 slot
+    *a2 = FarQuad<9>::c2;
+    *a3 = FarQuad<9>::c1;
+    return;
+  }
+  *a2 = FarPoly<7, 3>::a2;
+  *a3 = 0.0;
 }
 template <int KIND, int FAR>
 __device__ __forceinline__ double green_far_any(double qh, const double2* __restrict__ logtab, unsigned tbase,
-                                                int lim, double a2, double a3, int kmid) {
-  if (FAR == 1) return green_far_h<KIND>(qh, logtab);
-  if (FAR == 2) return green_far_t<KIND, 7, 3>(qh, tbase, lim, a2, a3);
-  if (FAR == 3) return green_far_t<KIND, 7, 4>(qh, tbase, lim, a2, a3);
-  if (FAR == 4) return green_far_t<KIND, 8, 3>(qh, tbase, lim, a2, a3);
+                                                int lim, double a2, double a3, int kmid,
+                                                const double* __restrict__ ftd = nullptr) {
+  static_assert(FAR == 5 || FAR == 7 || FAR == 8, "far form");
   if (FAR == 5) return green_far_r<KIND, 7, 3>(qh, tbase, lim, a2, a3, kmid);
-  return green_far_r<KIND, 6, 4>(qh, tbase, lim, a2, a3, kmid);
+  if (FAR == 7) return green_far_n<KIND, 7, 3>(qh, ftd, a2, a3, kmid);
+  return green_far_n<KIND, 9, 2>(qh, ftd, a2, a3, kmid);
 }
 
 // the records [0, nrec) of a staged chunk against the thread's targets (incoming-grid sums, no self exclusion)
@@ -138,14 +142,14 @@ __device__ __forceinline__ void accumulate_span(const double (&x)[TPT], const do
                                                 const double (&cq)[TPT], double (&acc)[TPT],
                                                 const double4* __restrict__ sm, int nrec, bool single,
                                                 const Tab* __restrict__ logtab, unsigned ftb, int flim, double fa2,
-                                                double fa3, int fmid = 0) {
+                                                double fa3, int fmid = 0, const double* __restrict__ ftd = nullptr) {
   if (single) {   // warp-uniform: a tail warp with <= 32 points evaluates one target per lane
 #pragma unroll UNROLL
     for (int m = 0; m < nrec; ++m) {
       const double4 s = sm[m];
-      if (FAR) {
+      if constexpr (FAR != 0) {
         const double qh = fma(x[0], s.x, fma(y[0], s.y, fma(z[0], s.z, cq[0])));
-        acc[0] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3, fmid), acc[0]);
+        acc[0] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3, fmid, ftd), acc[0]);
       } else {
         const double dx = x[0] - s.x, dy = y[0] - s.y, dz = z[0] - s.z;
         const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
@@ -159,9 +163,9 @@ __device__ __forceinline__ void accumulate_span(const double (&x)[TPT], const do
     const double4 s = sm[m];
 #pragma unroll
     for (int u = 0; u < TPT; ++u) {
-      if (FAR) {
+      if constexpr (FAR != 0) {
         const double qh = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
-        acc[u] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3, fmid), acc[u]);
+        acc[u] = fma(s.w, green_far_any<KIND, FAR>(qh, logtab, ftb, flim, fa2, fa3, fmid, ftd), acc[u]);
       } else {
         const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
         const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
@@ -194,9 +198,7 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
   }
 }
 
-// Asynchronous double-buffered variant: the unit's source list (<= 32 patches) is staged once; chunk c + 1 is copied
-// global -> shared with cp.async (16-byte pieces, no registers in flight) while chunk c is evaluated, so the warps
-// wait at the chunk barrier only for the slowest warp, not for the copy.  bufs: 2 x brec records.
+// cp.async (global -> shared, 16-byte pieces, no registers in flight): the warp-level grid kernel's double buffer
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
@@ -205,128 +207,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int KIND, int TPT, int UNROLL, int FAR, class Tab>
-__device__ __forceinline__ void accumulate_grid_async(const double (&x)[TPT], const double (&y)[TPT],
-                                                      const double (&z)[TPT], const double (&cq)[TPT],
-                                                      double (&acc)[TPT], int nsrc, const int32_t* __restrict__ lst,
-                                                      const double4* __restrict__ s4, int p,
-                                                      double4* __restrict__ bufs, int brec, int32_t* __restrict__ slst,
-                                                      const Tab* __restrict__ logtab, bool active, bool single,
-                                                      unsigned ftb, int flim, double fa2, double fa3, int fmid) {
-  __syncthreads();   // the previous unit is done with slst and the buffers
-  if ((int)threadIdx.x < nsrc) slst[threadIdx.x] = lst[threadIdx.x];
-  __syncthreads();
-  const int chp = max(1, brec / p);
-  const int nch = (nsrc + chp - 1) / chp;
-  auto issue = [&](int c) {
-    const int k0 = c * chp, k1 = min(nsrc, k0 + chp);
-    double2* dst = reinterpret_cast<double2*>(bufs + (size_t)(c & 1) * brec);
-    const int n16 = (k1 - k0) * p * 2;
-    for (int t = threadIdx.x; t < n16; t += blockDim.x) {
-      const int rr = t >> 1, q = rr / p, m = rr - q * p;
-      cp_async16(dst + t, reinterpret_cast<const double2*>(s4 + (size_t)slst[k0 + q] * p + m) + (t & 1));
-    }
-    cp_async_commit();
-  };
-  issue(0);
-  for (int c = 0; c < nch; ++c) {
-    if (c + 1 < nch) {
-      issue(c + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();   // chunk c is in shared memory for every thread
-    if (active)
-      accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, bufs + (size_t)(c & 1) * brec,
-                                              (min(nsrc, (c + 1) * chp) - c * chp) * p, single, logtab, ftb, flim,
-                                              fa2, fa3, fmid);
-    __syncthreads();   // every thread is done with buffer c & 1 before chunk c + 2 overwrites it
-  }
-}
-
-// ------------------------------------------------------------------------------------------------
-// Bulk-copy (TMA) pipeline for the incoming-grid sums: one elected thread streams whole source patches (p contiguous
-// 32-byte records each) into two shared-memory buffers with cp.async.bulk, completion tracked by a `full` mbarrier per
-// buffer (transaction bytes); each consumer warp releases a buffer by arriving on its `empty` mbarrier.  No CTA-wide
-// barrier in the loop: the copy of chunk c+1 overlaps the evaluation of chunk c, and warps drift freely.
-// ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n NC_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra NC_WAIT_%=;\n}" ::"r"(
-          smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-// bufs: 2 x brec records; bars: full[2], empty[2] (initialised here; the caller __syncthreads() before the first
-// wait is done inside).  Threads of warps with no active target must not call (they return before).  nwarps_act:
-// warps that call.  lst: the unit's source-patch list (nsrc entries), s4: the rung's records.
-template <int KIND, int TPT, int UNROLL, int FAR, class Tab>
-__device__ __forceinline__ void accumulate_grid_tma(const double (&x)[TPT], const double (&y)[TPT],
-                                                    const double (&z)[TPT], const double (&cq)[TPT],
-                                                    double (&acc)[TPT], int nsrc, const int32_t* __restrict__ lst,
-                                                    const double4* __restrict__ s4, int p, double4* __restrict__ bufs,
-                                                    int brec, uint64_t* __restrict__ bars,
-                                                    const Tab* __restrict__ logtab) {
-  uint64_t* full = bars;
-  uint64_t* empty = bars + 2;
-  const int chp = brec / p;                              // patches per chunk (>= 1: brec >= p)
-  const int nch = (nsrc + chp - 1) / chp;
-  const bool producer = threadIdx.x == 0;
-  auto issue = [&](int c) {
-    const int b = c & 1, k0 = c * chp, k1 = min(nsrc, k0 + chp);
-    mbar_expect_tx(&full[b], (unsigned)((k1 - k0) * p * sizeof(double4)));
-    for (int k = k0; k < k1; ++k)
-      bulk_g2s(bufs + (size_t)b * brec + (size_t)(k - k0) * p, s4 + (size_t)lst[k] * p, (unsigned)(p * sizeof(double4)),
-               &full[b]);
-  };
-  if (producer) issue(0);
-  for (int c = 0; c < nch; ++c) {
-    const int b = c & 1;
-    if (producer && c + 1 < nch) {
-      if (c >= 1) mbar_wait(&empty[(c + 1) & 1], (unsigned)(((c - 1) >> 1) & 1));   // chunk c-1 released its buffer
-      issue(c + 1);
-    }
-    mbar_wait(&full[b], (unsigned)((c >> 1) & 1));
-    const double4* __restrict__ sp = bufs + (size_t)b * brec;
-    const int nrec = (min(nsrc, (c + 1) * chp) - c * chp) * p;
-#pragma unroll UNROLL
-    for (int m = 0; m < nrec; ++m) {
-      const double4 s = sp[m];
-#pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        if (FAR) {
-          const double qh = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
-          acc[u] = fma(s.w, green_far_h<KIND>(qh, logtab), acc[u]);
-        } else {
-          const double dx = x[u] - s.x, dy = y[u] - s.y, dz = z[u] - s.z;
-          const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
-          acc[u] = fma(s.w, green_q<KIND>(qd, logtab), acc[u]);
-        }
-      }
-    }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[b]);
-  }
-}
 
 // Variant without shared-memory staging: every warp reads the source records straight from global memory with
 // warp-uniform addresses (one L1 broadcast per record), so warps never wait on CTA barriers.

@@ -54,12 +54,13 @@ class NcStats(ctypes.Structure):
                 ("gmres_ortho_bytes", ctypes.c_double), ("gmres_ortho_iters", ctypes.c_int64),
                 ("pair_fp64_flops_direct", ctypes.c_double), ("pair_fp64_inst_direct", ctypes.c_double),
                 ("pair_fp64_flops_grid", ctypes.c_double), ("pair_fp64_inst_grid", ctypes.c_double),
-                ("hier_grid_fill", ctypes.c_double), ("hier_grid_warp_fill", ctypes.c_double)]
+                ("hier_grid_fill", ctypes.c_double), ("hier_grid_warp_fill", ctypes.c_double),
+                ("grid_variant", ctypes.c_int32 * 8), ("hier_unit_points", ctypes.c_double)]
 
 
 EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt",
            "nc_field", "nc_residual", "nc_density", "nc_id_sketch", "nc_modal_kernels", "nc_stats",
-           "nc_time_stages", "nc_tree_lists", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
+           "nc_time_stages", "nc_tree_lists", "nc_near_counts", "nc_pair_mix", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
 
 _lib = None
 
@@ -91,6 +92,8 @@ def load_library(path: str = LIB_PATH):
     L.nc_stats.argtypes = [vp, ctypes.POINTER(NcStats)]
     L.nc_time_stages.argtypes = [vp, ctypes.c_int]
     L.nc_tree_lists.argtypes = [vp, _i64p, _i64p, _i64p, _i64p, _i64p]
+    L.nc_near_counts.argtypes = [vp, _i64p]
+    L.nc_pair_mix.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _dp]
     L.nc_split_rows.argtypes = [_dp, ctypes.c_int64, ctypes.c_int, _i64p, _i64p]
     L.nc_nccl_unique_id.argtypes = [vp]
     L.nc_destroy.argtypes = [vp]
@@ -151,11 +154,22 @@ def modal_kernels(kind: int, t, tp, M: int, phi, wphi, device: int = 0) -> np.nd
     return out
 
 
-def _ptr(t):
-    """Device pointer of a contiguous float64 CUDA tensor."""
+def pair_mix(kind: int, far: int, ctas_per_sm: int = 2):
+    """nc_pair_mix: (best ms, warp-pairs per launch) of the grid kernel's pair evaluation run in isolation."""
+    L = load_library()
+    ms, wp = ctypes.c_double(), ctypes.c_double()
+    _check(L.nc_pair_mix(int(kind), int(far), int(ctas_per_sm), ctypes.byref(ms), ctypes.byref(wp)))
+    return ms.value, wp.value
+
+
+def _ptr(t, shape=None):
+    """Device pointer of a contiguous float64 CUDA tensor (of the given shape: libnc trusts the sizes it is passed,
+    so an undersized buffer would be read or written out of bounds on the device)."""
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise TypeError("expected a contiguous float64 CUDA tensor")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"expected a tensor of shape {tuple(shape)}, got {tuple(t.shape)}")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -189,6 +203,8 @@ class Handle:
             tab.ladder_p = lp.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
             tab.ladder_shat = ls.ctypes.data_as(_dp)
             tab.ladder_T = lt.ctypes.data_as(_dp)
+            # the gate of nc_setup: the rungs' ID tolerance (tests/test_parity_golden_gpu.py checks the matvec error
+            # with the ladder on at a requested precision equal to it)
             tab.ladder_tol = float(getattr(tables, "ladder_tol", 0.0) or 0.0)
         idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         opts = NcOpts(int(mode), float(precision), int(device), int(world), int(rank),
@@ -220,7 +236,8 @@ class Handle:
         import torch
         if y is None:
             y = torch.empty_like(x)
-        _check(self._L.nc_matvec(self._h, _ptr(x), _ptr(y), _stream_ptr(stream)))
+        rows = (self.row_count, self.K)
+        _check(self._L.nc_matvec(self._h, _ptr(x, rows), _ptr(y, rows), _stream_ptr(stream)))
         return y
 
     def matvec_emulated(self, x_all, y=None, stream=None):
@@ -228,11 +245,14 @@ class Handle:
         import torch
         if y is None:
             y = torch.empty((self.row_count, x_all.shape[1]), dtype=x_all.dtype, device=x_all.device)
-        _check(self._L.nc_matvec_emulated(self._h, _ptr(x_all), _ptr(y), _stream_ptr(stream)))
+        _check(self._L.nc_matvec_emulated(self._h, _ptr(x_all, (self.N, self.K)), _ptr(y, (self.row_count, self.K)),
+                                          _stream_ptr(stream)))
         return y
 
     def matvec_host(self, x: np.ndarray) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.shape != (self.row_count, self.K):
+            raise ValueError(f"expected shape {(self.row_count, self.K)}, got {x.shape}")
         y = np.empty_like(x)
         _check(self._L.nc_matvec_host(self._h, x.ctypes.data_as(_dp), y.ctypes.data_as(_dp)))
         return y
@@ -243,7 +263,8 @@ class Handle:
             x = torch.empty((self.row_count, self.K), dtype=torch.float64, device="cuda")
         it = ctypes.c_int()
         hist = np.zeros(max_iter + 1)
-        rc = self._L.nc_gmres(self._h, _ptr(b) if b is not None else None, float(rtol), int(max_iter), _ptr(x),
+        rows = (self.row_count, self.K)
+        rc = self._L.nc_gmres(self._h, _ptr(b, rows) if b is not None else None, float(rtol), int(max_iter), _ptr(x, rows),
                               ctypes.byref(it), hist.ctypes.data_as(_dp), _stream_ptr(stream))
         if rc != NC_OK and not (allow_noconv and rc == NC_ENOCONV):
             _check(rc)
@@ -251,7 +272,7 @@ class Handle:
 
     def flux_or_mfpt(self, x):
         Is, v = ctypes.c_double(), ctypes.c_double()
-        _check(self._L.nc_flux_or_mfpt(self._h, _ptr(x), ctypes.byref(Is), ctypes.byref(v)))
+        _check(self._L.nc_flux_or_mfpt(self._h, _ptr(x, (self.row_count, self.K)), ctypes.byref(Is), ctypes.byref(v)))
         return Is.value, v.value
 
     def field(self, x_all, pts):
@@ -260,7 +281,7 @@ class Handle:
         the device, internal order)."""
         pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
         out, dmin = np.empty(len(pts)), np.empty(len(pts))
-        _check(self._L.nc_field(self._h, _ptr(x_all), len(pts), pts.ctypes.data_as(_dp), out.ctypes.data_as(_dp),
+        _check(self._L.nc_field(self._h, _ptr(x_all, (self.N, self.K)), len(pts), pts.ctypes.data_as(_dp), out.ctypes.data_as(_dp),
                                 dmin.ctypes.data_as(_dp)))
         return out, dmin
 
@@ -274,7 +295,7 @@ class Handle:
         rw = np.ascontiguousarray(tables.res_w, dtype=np.float64)
         rs = np.ascontiguousarray(tables.res_S, dtype=np.float64)
         res, pw = np.empty(len(pat)), np.empty((len(pat), len(rw)))
-        _check(self._L.nc_residual(self._h, _ptr(x_all), len(pat), pat.ctypes.data_as(_i64p), len(rw),
+        _check(self._L.nc_residual(self._h, _ptr(x_all, (self.N, self.K)), len(pat), pat.ctypes.data_as(_i64p), len(rw),
                                    rh.ctypes.data_as(_dp), rw.ctypes.data_as(_dp), rs.ctypes.data_as(_dp),
                                    res.ctypes.data_as(_dp), pw.ctypes.data_as(_dp)))
         return res, pw
@@ -284,7 +305,7 @@ class Handle:
         pat = np.ascontiguousarray(patches, dtype=np.int64).reshape(-1)
         Bc = np.ascontiguousarray(B, dtype=np.float64)
         sig = np.empty((len(pat), Bc.shape[0]))
-        _check(self._L.nc_density(self._h, _ptr(x_all), len(pat), pat.ctypes.data_as(_i64p), Bc.shape[0],
+        _check(self._L.nc_density(self._h, _ptr(x_all, (self.N, self.K)), len(pat), pat.ctypes.data_as(_i64p), Bc.shape[0],
                                   Bc.ctypes.data_as(_dp), sig.ctypes.data_as(_dp)))
         return sig
 
@@ -296,6 +317,7 @@ class Handle:
         _check(self._L.nc_stats(self._h, ctypes.byref(s)))
         d = {k: getattr(s, k) for k, _ in NcStats._fields_}
         d["ms_last"] = list(s.ms_last)
+        d["grid_variant"] = list(s.grid_variant)
         return d
 
     def tree_lists(self):
@@ -309,6 +331,12 @@ class Handle:
         _check(L.nc_tree_lists(self._h, ctypes.byref(ni), il.ctypes.data_as(_i64p), ctypes.byref(nn),
                                nb.ctypes.data_as(_i64p), bop.ctypes.data_as(_i64p)))
         return il, nb, bop
+
+    def near_counts(self) -> np.ndarray:
+        """Near-list source patches of each of this rank's rows (internal order; nc_near_counts, NC_HIER)."""
+        out = np.empty(self.row_count, dtype=np.int64)
+        _check(self._L.nc_near_counts(self._h, out.ctypes.data_as(_i64p)))
+        return out
 
     def close(self):
         if getattr(self, "_h", None):

@@ -156,26 +156,28 @@ sys.path.insert(0, os.environ["ROOT"])
 import paper_1906_04209_b200 as nc
 from nc_inputs import CONFIGS, random_coeffs
 from nc_inputs.tables import load_tables
-cfg = CONFIGS["C3"]
-tab = load_tables(os.path.join(os.environ["ROOT"], "tables", "data", "C3.npz"))
+cfg = CONFIGS[os.environ.get("CFG", "C3")]
+tab = load_tables(os.path.join(os.environ["ROOT"], "tables", "data", cfg.name + ".npz"))
 h = nc.Handle(cfg.kind, cfg.centers(), cfg.eps, tab, mode=nc.NC_HIER, precision=cfg.precision)
 x = torch.from_numpy(h.to_internal(random_coeffs(cfg.N, tab.K, 2006))).cuda()
 np.save(os.environ["OUT"], h.matvec(x).cpu().numpy())
 """
 
 
-@pytest.mark.parametrize("far", [1, 2, 5, 6])
-def test_far_field_pair_variant_error(tmp_path, far):
-    """k_pairs_grid's far-field evaluations (R23: dot-product distance + one-Newton rsqrt; R25: the
-    exponent-indexed log table, 16-byte (c, L) entries or c from rcp.approx and 8-byte L entries) against the exact
-    pair kernel on the same grids (C3): the difference must stay far below the hierarchical precision."""
+@pytest.mark.parametrize("cfg,far", [("C3", "8,2,4,64,8,3,2"), ("C3", "8,2,4,64,7,3,3"), ("C3", "8,2,4,64,5,3,3"),
+                                     ("C5", "8,2,4,64,8,3,2"), ("C4", "8,2,4,64,8,3,2")])
+def test_far_field_pair_variant_error(tmp_path, cfg, far):
+    """k_pairs_grid_w's far-field evaluations (R23: dot-product distance + one-Newton rsqrt; R25: the
+    exponent-indexed log table with c from rcp.approx; R32: the unclamped table, FB = 9 quadratic (the default) or
+    FB = 7 cubic) against the EXACT difference-form pair kernel on the same grids and sources (the CTA-level kernel,
+    far 0), at the C3 / C4 / C5 epsilons: the difference must stay far below the hierarchical precision."""
     import subprocess
     import sys
     outs = []
-    for v in ("128,2,4,256,0", f"128,2,4,256,{far}"):
-        out = str(tmp_path / f"y{v[-1]}.npy")
-        env = dict(os.environ, NC_GRID_VARIANT=v, ROOT=ROOT, OUT=out)
-        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=env, check=True, timeout=600)
+    for v in ("32,2,4,256,0", far):   # the exact form on the same 64-point units (one-warp CTAs)
+        out = str(tmp_path / f"y{len(outs)}.npy")
+        env = dict(os.environ, NC_GRID_VARIANT=v, ROOT=ROOT, OUT=out, CFG=cfg)
+        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=env, check=True, timeout=900)
         outs.append(np.load(out))
     assert rel(outs[1], outs[0]) <= 1e-11
 
