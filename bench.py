@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="target patches in the oracle sample (0 = auto)")
+    ap.add_argument("--field-points", type=int, default=16384,
+                    help="NEXT-3 sweep: points on the sphere of radius 1 -+ eps/5 (nc_field_near)")
     return ap.parse_args()
 
 
@@ -390,30 +392,32 @@ def main():
         hbm_stages["note"] = ("algorithmic bytes: k_reduce_chunks reads every work unit's partial values and writes "
                               "the grid values; K1 reads X and the rungs' T and writes rho (8 B per record, scattered "
                               "into 32-B records); peak = MEASURED_PEAKS.json hbm_gbs")
-    # NEXT-3: the off-surface field of the solution (nc_field, host points in / values out, synchronous) at 4096
-    # points on a sphere inside (interior: radius 0.5) or outside (exterior: radius 2) the unit sphere
+    # NEXT-3: the field of the solution on the sphere of radius 1 -+ eps/5, where the paper plots the MFPT (PAPER.md:2069-2097,
+    # Fig. sphereplots): nc_field_near (host points in, values and v-bar out, synchronous; the patches within 4 eps of a
+    # point from their density, the others from their compressed skeleton), Fibonacci points
     field = None
-    if world == 1 and solve is not None:   # (skipped with --no-solve: the ncu launch list covers the matvec step only)
-        n_f = 4096
+    if world == 1 and solve is not None and getattr(tab, "near_sigma", None) is not None and args.field_points > 0:
+        n_f = args.field_points
         k = np.arange(n_f) + 0.5
         zf = 1.0 - 2.0 * k / n_f
         phi = np.pi * (1.0 + 5.0 ** 0.5) * k
-        rf = 0.5 if cfg.kind == 0 else 2.0
+        rf = 1.0 - cfg.eps / 5 if cfg.kind == 0 else 1.0 + cfg.eps / 5
         pts = rf * np.stack([np.sqrt(1 - zf * zf) * np.cos(phi), np.sqrt(1 - zf * zf) * np.sin(phi), zf], 1)
-        xf = xs
-        h.field(xf, pts[:8])   # warm-up
+        want_mfpt = cfg.kind == 0 and args.tables == "physical"
+        h.field_near(xs, pts[:8], tab, mfpt=want_mfpt)   # warm-up
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        vf, _ = h.field(xf, pts)
+        vf, mf, nnear = h.field_near(xs, pts, tab, mfpt=want_mfpt)
         tf = time.perf_counter() - t0
         fpairs = float(n_f) * cfg.N * tab.p
-        field = {"points": n_f, "radius": rf, "pairs": fpairs, "ms": tf * 1e3, "pairs_per_s": fpairs / tf,
-                 "mean_value": float(np.mean(vf)),
-                 "note": "nc_field end to end (H2D points, base-rung rho, k_field, D2H values); pairs = points x N x p"}
-        if solve is not None and cfg.kind == 0 and args.tables == "physical":
-            v0, _ = h.field(xf, np.zeros((1, 3)))
-            field["v_origin"] = float(v0[0])
-            field["mfpt_origin"] = float((1.0 - v0[0]) / (3.0 * solve["I_sigma"]) + 1.0 / 6.0)   # eq:vtilde, D = -I_sigma
+        field = {"points": n_f, "radius": rf, "near_pairs": nnear, "far_pairs": fpairs, "ms": tf * 1e3,
+                 "points_per_s": n_f / tf, "mean_value": float(np.mean(vf)),
+                 "note": "nc_field_near end to end (H2D points, compressed field of every patch, near pairs, density "
+                         "quadrature of the near patches, D2H values)"}
+        if want_mfpt:
+            field.update({"mfpt_mean": float(np.mean(mf)), "mfpt_min": float(np.min(mf)), "mfpt_max": float(np.max(mf))})
+            v0, m0, _ = h.field_near(xs, np.zeros((1, 3)), tab, mfpt=True)
+            field["v_origin"], field["mfpt_origin"] = float(v0[0]), float(m0[0])
     # NEXT-4: the paper's accuracy metric eq:l2res (relative L2 residual of the multiple-scattering system on a
     # patch, on the tables' independent residual grid) for 16 seeded random patches of the solved system
     residual = None

@@ -194,6 +194,37 @@ int nc_flux_or_mfpt(nc_handle* h, const double* x, double* I_sigma, double* valu
  * 3 eps to a skeleton node: out and dmin are still written), NC_ENOMEM, NC_ECUDA. */
 int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts, double* out, double* dmin);
 
+/* Near-field table of a patch radius (NEXT-3; nc_tables/nearfield.py): the one-patch solver's radial panels and
+ * basis densities sigma_a(t), canonical frame.  n_r = npan k. */
+typedef struct nc_near_tables {
+  int32_t npan, k;           /* panels; Gauss nodes per panel (k <= 32)                                   */
+  const double* edges;       /* npan + 1 panel breakpoints in t (arc length from the centre), 0 .. eps     */
+  const double* t;           /* n_r radial nodes, panel-major (Gauss-Legendre; Gauss-Jacobi on the last)    */
+  const double* w;           /* n_r weights: int_0^eps F(t) sigma(t) sin t dt = sum_j w_j F(t_j) sigma(t_j) */
+  const double* sigma;       /* K x n_r: sigma_a(t_j) of basis column a (row-major)                       */
+  const int32_t* m;          /* K: angular order of column a (0 .. 15)                                     */
+  const int32_t* c;          /* K: +1 cos(m theta), -1 sin(m theta)                                        */
+} nc_near_tables;
+
+/* NEXT-3 at any off-surface point, including the layer near the patches where the compressed skeleton is not valid
+ * (PAPER.md:2069-2097 plot the MFPT on the sphere of radius 1 - eps/5): v (interior) or u (exterior) as in nc_field,
+ * with the patches whose centre is closer than 4 eps to a point evaluated from their density sigma = B fhat
+ * (eq:recoversig) by panel-refined radial x converged trapezoid angular quadrature
+ * (csrc/nearfield.cu), the others from their compressed skeleton.
+ *   x_all  device, N x K (all patches, internal order; world 1: the nc_gmres solution)
+ *   pts    host, n_pts x 3: interior |p| < 1, exterior |p| > 1; a point within 4 eps of a patch centre must be at
+ *          least eps / 100 off the sphere (the angular rule's resolution limit)
+ *   nt     the near-field table of this eps (nc_tables/nearfield.py)
+ *   out    host, n_pts (output): the potential
+ *   mfpt   host, n_pts or NULL (output, interior only): the mean first passage time
+ *          vbar = (v - 1) / (3 D) + (1 - |p|^2) / 6, D = -I_sigma (eq:vtilde PAPER.md:533-536, Lemma PAPER.md:556-566),
+ *          I_sigma = I . sum_i fhat_i from x_all (eq:getI)
+ *   n_near host or NULL (output): the number of (point, near patch) pairs evaluated by quadrature
+ * Synchronous.  Errors: NC_EINVAL (bad argument, a point on the wrong side or too close to the sphere near a patch,
+ * or mfpt requested for the exterior problem), NC_ENOMEM, NC_ECUDA. */
+int nc_field_near(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts, const nc_near_tables* nt,
+                  double* out, double* mfpt, int64_t* n_near);
+
 /* L2 residual diagnostic (NEXT-4): the paper's accuracy metric eq:l2res,
  *   res_i = || S sigma_i + sum_{j != i} S_ij sigma_j - 1 ||_{L2(Gamma_i)} / |Gamma_i|
  * for n_sel listed patches, by quadrature on a residual grid that is independent of the solve's grids

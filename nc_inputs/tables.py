@@ -50,6 +50,16 @@ class PatchTables:
     res_rhat: np.ndarray | None = None
     res_w: np.ndarray | None = None
     res_S: np.ndarray | None = None
+    # optional near-field table for the near-surface potential (NEXT-3; nc_tables/nearfield.py): the one-patch
+    # solver's radial panels and basis densities sigma_a(t) (canonical frame):
+    #   near_edges (npan+1), near_t (n_r), near_w (n_r), near_sigma (K, n_r), near_m (K,), near_c (K,), near_k ()
+    near_edges: np.ndarray | None = None
+    near_t: np.ndarray | None = None
+    near_w: np.ndarray | None = None
+    near_sigma: np.ndarray | None = None
+    near_m: np.ndarray | None = None
+    near_c: np.ndarray | None = None
+    near_k: int | None = None
 
     @property
     def K(self) -> int:
@@ -74,6 +84,10 @@ class PatchTables:
         if self.res_S is not None:
             assert self.res_rhat.shape == (self.res_S.shape[0], 3) and self.res_w.shape == (self.res_S.shape[0],)
             assert self.res_S.shape[1] == K
+        if self.near_sigma is not None:
+            assert self.near_sigma.shape == (K, self.near_t.size) and self.near_w.shape == self.near_t.shape
+            assert self.near_m.shape == (K,) and self.near_c.shape == (K,)
+            assert self.near_edges.size * self.near_k == self.near_t.size + self.near_k
         if self.ladder_r is not None:
             n = int(np.sum(self.ladder_p))
             assert self.ladder_shat.shape == (n, 3) and self.ladder_T.shape == (n, K)
@@ -97,10 +111,13 @@ class PatchTables:
 
     def without_ladder(self):
         return PatchTables(self.kind, self.eps, self.M, self.zhat, self.P, self.shat, self.T, self.I, self.meta,
-                           res_rhat=self.res_rhat, res_w=self.res_w, res_S=self.res_S)
+                           res_rhat=self.res_rhat, res_w=self.res_w, res_S=self.res_S, near_edges=self.near_edges,
+                           near_t=self.near_t, near_w=self.near_w, near_sigma=self.near_sigma, near_m=self.near_m,
+                           near_c=self.near_c, near_k=self.near_k)
 
 
-_OPTIONAL = ("ladder_r", "ladder_p", "ladder_shat", "ladder_T", "res_rhat", "res_w", "res_S")
+_OPTIONAL = ("ladder_r", "ladder_p", "ladder_shat", "ladder_T", "res_rhat", "res_w", "res_S", "near_edges", "near_t",
+             "near_w", "near_sigma", "near_m", "near_c", "near_k")
 
 
 def save_tables(path, t: PatchTables):
@@ -113,6 +130,8 @@ def load_tables(path) -> PatchTables:
     z = np.load(path, allow_pickle=False)
     assert int(z["version"]) == TABLE_VERSION, "table file version mismatch"
     lad = {k: np.ascontiguousarray(z[k]) for k in _OPTIONAL if k in z.files}
+    if "near_k" in lad:
+        lad["near_k"] = int(np.asarray(lad["near_k"]).reshape(-1)[0])
     return PatchTables(kind=int(z["kind"]), eps=float(z["eps"]), M=int(z["M"]),
                        zhat=np.ascontiguousarray(z["zhat"]), P=np.ascontiguousarray(z["P"]),
                        shat=np.ascontiguousarray(z["shat"]), T=np.ascontiguousarray(z["T"]),

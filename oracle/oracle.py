@@ -65,6 +65,8 @@ def lib():
         L.oracle_offsurface.restype = None
         L.oracle_green_off_batch.argtypes = [ctypes.c_int, ctypes.c_int64, dp, dp, dp]
         L.oracle_green_off_batch.restype = None
+        L.oracle_rings.argtypes = [ctypes.c_int, dp, ctypes.c_int64, dp, ctypes.c_int, ctypes.c_int, dp, dp, dp]
+        L.oracle_rings.restype = None
         _lib = L
     return _lib
 
@@ -187,6 +189,128 @@ def residual(kind, centers, tab, x, patches):
 def density(x, patches, B):
     """sigma_i = B fhat_i (eq:recoversig) for the listed patches: the definition, a matmul."""
     return np.asarray(x, dtype=np.float64)[np.asarray(patches, dtype=np.int64)] @ np.asarray(B, dtype=np.float64).T
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-3 near the surface: the density itself, by adaptive quadrature
+# ---------------------------------------------------------------------------------------------
+def _panel_profiles(tab, xj):
+    """Per angular order m: the radial profiles A_m(t), B_m(t) at the table's radial nodes, sigma(t, theta) =
+    sum_m A_m(t) cos(m theta) + B_m(t) sin(m theta) = sum_a fhat_a sigma_a(t) ang_a(theta) (eq:recoversig)."""
+    M1 = int(np.max(tab.near_m)) + 1
+    AB = np.zeros((tab.near_t.size, 2 * M1))
+    for a, (m, c) in enumerate(zip(tab.near_m, tab.near_c)):
+        AB[:, 2 * m + (0 if c > 0 else 1)] += xj[a] * tab.near_sigma[a]
+    return AB, M1
+
+
+def _interp_profiles(tab, AB, panel, tq, g_only=False):
+    """The profiles at radii tq inside one panel: degree-(k-1) polynomial interpolation of the panel's k nodal
+    values (numpy Legendre fit through k points = the interpolant); on the last panel the polynomial is
+    g = sigma sqrt(eps - t) (sigma has the 1/sqrt(eps - t) edge singularity there), returned as
+    g itself when g_only."""
+    k, eps = tab.near_k, tab.eps
+    sl = slice(panel * k, (panel + 1) * k)
+    tn, vals = tab.near_t[sl], AB[sl]
+    a, b = tab.near_edges[panel], tab.near_edges[panel + 1]
+    last = panel == len(tab.near_edges) - 2
+    if last:
+        vals = vals * np.sqrt(eps - tn)[:, None]
+    out = np.empty((len(tq), AB.shape[1]))
+    for c in range(AB.shape[1]):
+        out[:, c] = np.polynomial.Legendre.fit(tn, vals[:, c], k - 1, domain=[a, b])(tq)
+    if last and not g_only:
+        out /= np.sqrt(eps - tq)[:, None]
+    return out
+
+
+def _rings(kind, p, t, AB, M1):
+    """int_0^2pi G_off(p, x'(t, theta)) sigma(t, theta) dtheta for each t: trapezoid rule, doubled until converged."""
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    AB = np.ascontiguousarray(AB, dtype=np.float64)
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    prev = None
+    n = 64
+    while True:
+        out, ab = np.empty(len(t)), np.empty(len(t))
+        lib().oracle_rings(int(kind), _dp(p), len(t), _dp(t), n, M1, _dp(AB), _dp(out), _dp(ab))
+        # converged: the doubled rule changes each ring integral by less than rounding of its terms' sum
+        if prev is not None and np.all(np.abs(out - prev) <= 1e-15 * np.maximum(np.abs(out), 1e-300) + 1e-15 * ab):
+            return out
+        if n >= 524288:
+            raise RuntimeError("oracle ring integral did not converge")
+        prev, n = out, 2 * n
+
+
+def near_patch(kind, tab, xj, p_local, rtol=1e-14):
+    """The potential of ONE patch's density at p_local (the patch's canonical frame), by adaptive quadrature of
+    int_Gamma G_off(p, x') sigma(x') dS = int_0^eps sin t int_0^2pi G_off sigma dtheta dt (eq:intBVPansatz /
+    eq:urep restricted to one patch, sigma = B fhat by eq:recoversig).  Radial: on every panel of the one-patch
+    grid, 20-point Gauss-Legendre on the panel compared with the sum over its halves, bisected until they agree
+    (the last panel in s = sqrt(eps - t), where sigma ds is smooth); angular: the converged trapezoid rule."""
+    AB, M1 = _panel_profiles(tab, np.asarray(xj, dtype=np.float64))
+    eps = tab.eps
+    xg, wg = np.polynomial.legendre.leggauss(20)
+    npan = len(tab.near_edges) - 1
+
+    def F(panel, tq, g_only=False):                    # sin t x ring integral at radii tq of a panel
+        return np.sin(tq) * _rings(kind, p_local, tq, _interp_profiles(tab, AB, panel, tq, g_only), M1)
+
+    def gl(panel, a, b, last):
+        if last:   # t = eps - s^2, dt = 2 s ds, sigma = g / s: the integrand in s is 2 sin t ring(g), smooth
+            s = 0.5 * (a + b) + 0.5 * (b - a) * xg
+            return 0.5 * (b - a) * np.sum(wg * 2.0 * F(panel, eps - s * s, g_only=True))
+        tq = 0.5 * (a + b) + 0.5 * (b - a) * xg
+        return 0.5 * (b - a) * np.sum(wg * F(panel, tq))
+
+    # scale of the patch's potential (native nodes): the adaptive criterion is absolute relative to it
+    scale = np.sum(np.abs(tab.near_w * _rings(kind, p_local, tab.near_t, AB, M1)))
+    total = 0.0
+    for panel in range(npan):
+        a, b = tab.near_edges[panel], tab.near_edges[panel + 1]
+        last = panel == npan - 1
+        if last:
+            a, b = 0.0, np.sqrt(eps - a)
+        stack = [(a, b, gl(panel, a, b, last), 0)]
+        while stack:
+            lo, hi, whole, depth = stack.pop()
+            mid = 0.5 * (lo + hi)
+            left, right = gl(panel, lo, mid, last), gl(panel, mid, hi, last)
+            if abs(left + right - whole) <= rtol * scale or depth >= 40:
+                total += left + right
+            else:
+                stack += [(lo, mid, left, depth + 1), (mid, hi, right, depth + 1)]
+    return total
+
+
+def nearfield(kind, centers, tab, x, pts, near_r=4.0):
+    """NEXT-3 at any off-surface point (PAPER.md:2069-2097 plot the MFPT at radius 1 - eps/5): v(p) (interior) or
+    u(p) (exterior) = sum over patches j of the patch's single-layer potential, by near_patch (the density itself,
+    eq:recoversig) for patches whose centre is closer than near_r eps to p, and by the compressed skeleton
+    (eq:outgoingcompressed, valid >= 3 eps from every skeleton node, R27) for the others."""
+    N = len(centers)
+    x = np.asarray(x, dtype=np.float64).reshape(N, -1)
+    c = np.asarray(centers, dtype=np.float64)
+    R = frames(c)
+    s = global_nodes(R, tab.shat)                                     # (N, p, 3)
+    rho = outgoing(tab.T, x)                                          # (N, p)
+    pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+    out = np.empty(len(pts))
+    for i, p in enumerate(pts):
+        near = np.where(np.linalg.norm(c - p, axis=1) < near_r * tab.eps)[0]
+        far = np.setdiff1d(np.arange(N), near)
+        v = 0.0
+        if len(far):
+            sf = np.ascontiguousarray(s[far].reshape(-1, 3))
+            rf = np.ascontiguousarray(rho[far].reshape(-1))
+            o, dm, ab = np.empty(1), np.empty(1), np.empty(1)
+            lib().oracle_offsurface(int(kind), 1, _dp(np.ascontiguousarray(p[None])), len(sf), _dp(sf), _dp(rf),
+                                    _dp(o), _dp(dm), _dp(ab))
+            v += o[0]
+        for j in near:
+            v += near_patch(kind, tab, x[j], R[j].T @ p)
+        out[i] = v
+    return out
 
 
 def mfpt_field(v, pts, I_sigma):

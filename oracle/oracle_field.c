@@ -25,6 +25,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 double oracle_green(int kind, const double* x, const double* y) {
   double dx = x[0] - y[0], dy = x[1] - y[1], dz = x[2] - y[2];
@@ -126,4 +127,43 @@ int oracle_num_threads(void) {
 #else
   return 1;
 #endif
+}
+
+/*
+ * Ring integrals of the near-surface potential (NEXT-3; eq:recoversig PAPER.md:797-807 for the
+ * density, eq:Gintoffsurface / eq:Gextoffsurface for G): for each radius t[i] of a patch in its canonical frame
+ * (centre +z, theta from +x),
+ *     out[i] = (2 pi / ntheta) sum_k G_off(p, x'(t_i, theta_k)) sigma(t_i, theta_k),   theta_k = 2 pi k / ntheta,
+ *     x'(t, theta) = (sin t cos theta, sin t sin theta, cos t),
+ *     sigma(t_i, theta) = sum_{m < M1} AB[i][2m] cos(m theta) + AB[i][2m + 1] sin(m theta)
+ * (the trapezoid rule: exact for the trigonometric polynomial sigma times the analytic periodic G up to the
+ * aliasing error, which the caller drives down by doubling ntheta).  Neumaier-compensated.
+ */
+void oracle_rings(int kind, const double* p, int64_t nt, const double* t, int ntheta, int M1, const double* AB,
+                  double* out, double* absum) {
+  const double twopi = 6.283185307179586476925286766559;
+  double* cs = (double*)malloc(sizeof(double) * 2 * (size_t)M1 * ntheta);
+  for (int k = 0; k < ntheta; ++k)
+    for (int m = 0; m < M1; ++m) {
+      const double a = twopi * (double)(((int64_t)m * k) % ntheta) / ntheta;
+      cs[(size_t)k * 2 * M1 + 2 * m] = cos(a);
+      cs[(size_t)k * 2 * M1 + 2 * m + 1] = sin(a);
+    }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t i = 0; i < nt; ++i) {
+    const double st = sin(t[i]), ct = cos(t[i]);
+    double sum = 0.0, comp = 0.0, as = 0.0;
+    for (int k = 0; k < ntheta; ++k) {
+      const double* c = cs + (size_t)k * 2 * M1;
+      double sig = 0.0;
+      for (int m = 0; m < M1; ++m) sig += AB[i * 2 * M1 + 2 * m] * c[2 * m] + AB[i * 2 * M1 + 2 * m + 1] * c[2 * m + 1];
+      const double y[3] = {st * c[2], st * c[3], ct};   /* c[2], c[3] = cos theta, sin theta (m = 1) */
+      const double term = oracle_green_off(kind, p, y) * sig;
+      neumaier_add(&sum, &comp, term);
+      as += fabs(term);
+    }
+    out[i] = (sum + comp) * (twopi / ntheta);
+    absum[i] = as * (twopi / ntheta);   /* the conditioning scale of the ring sum */
+  }
+  free(cs);
 }

@@ -849,6 +849,168 @@ int nc_field(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts
   return rc;
 }
 
+int nc_field_near(nc_handle* h, const double* x_all, int64_t n_pts, const double* pts, const nc_near_tables* nt,
+                  double* out, double* mfpt, int64_t* n_near) {
+  if (!h || !x_all || n_pts < 0 || (n_pts > 0 && (!pts || !out)) || !nt || !nt->edges || !nt->t || !nt->w ||
+      !nt->sigma || !nt->m || !nt->c || nt->npan < 1 || nt->k < 2 || nt->k > 32)
+    return fail(NC_EINVAL, "nc_field_near: bad argument");
+  if (mfpt && h->kind != NC_INTERIOR) return fail(NC_EINVAL, "nc_field_near: the MFPT is an interior quantity");
+  const int K = h->K, n_r = nt->npan * nt->k;
+  int M1 = 0;
+  for (int a = 0; a < K; ++a) {
+    if (nt->m[a] < 0 || nt->m[a] > 15 || (nt->c[a] != 1 && nt->c[a] != -1))
+      return fail(NC_EINVAL, "nc_field_near: basis orders must be 0..15 with c = +-1");
+    M1 = std::max(M1, nt->m[a] + 1);
+  }
+  if (n_near) *n_near = 0;
+  if (n_pts == 0) return NC_OK;
+  for (int64_t t = 0; t < n_pts; ++t) {
+    const double r = std::sqrt(pts[3 * t] * pts[3 * t] + pts[3 * t + 1] * pts[3 * t + 1] + pts[3 * t + 2] * pts[3 * t + 2]);
+    if (!(h->kind == NC_EXTERIOR ? r > 1.0 : r < 1.0))
+      return fail(NC_EINVAL, "nc_field_near: point " + std::to_string(t) + " is not on the " +
+                                 (h->kind == NC_EXTERIOR ? "exterior" : "interior") + " side of the unit sphere");
+  }
+  NC_TRY(order_after_caller(h));
+  cudaStream_t s = h->stream;
+  const int p0 = h->rung_p[0];
+  double* d_rec = nullptr;
+  NC_TRY(base_records(h, x_all, s, &d_rec));
+  const int64_t nrec = h->N * p0;
+  const int nseg = field_segments(n_pts, nrec);
+  // host-built near table: reference Gauss nodes / weights of the regular panels (from the first panel), their
+  // barycentric weights, the (m, cos | sin) CSR of the basis columns, the angle table
+  std::vector<double> glx(nt->k), glw(nt->k), bary(nt->k), trig(2 * kNearTrigN);
+  {
+    const double a = nt->edges[0], b = nt->edges[1], hh = 0.5 * (b - a);
+    for (int e = 0; e < nt->k; ++e) {
+      glx[e] = (nt->t[e] - a) / hh - 1.0;
+      glw[e] = nt->w[e] / (hh * std::sin(nt->t[e]));
+    }
+    for (int e = 0; e < nt->k; ++e) {
+      long double pr = 1.0L;
+      for (int f = 0; f < nt->k; ++f)
+        if (f != e) pr *= (long double)(glx[e] - glx[f]);
+      bary[e] = (double)(1.0L / pr);
+    }
+    for (int k = 0; k < kNearTrigN; ++k) {
+      const long double th = 2.0L * 3.14159265358979323846264338327950288L * k / kNearTrigN;
+      trig[2 * k] = (double)cosl(th);
+      trig[2 * k + 1] = (double)sinl(th);
+    }
+  }
+  std::vector<int> mc_off(2 * M1 + 1, 0), mc_col;
+  for (int comp = 0; comp < 2 * M1; ++comp) {
+    for (int a = 0; a < K; ++a)
+      if (2 * nt->m[a] + (nt->c[a] > 0 ? 0 : 1) == comp) mc_col.push_back(a);
+    mc_off[comp + 1] = (int)mc_col.size();
+  }
+  std::vector<void*> bufs;
+  auto dup = [&](const void* src, size_t bytes, void** dst) -> cudaError_t {
+    cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) return e;
+    bufs.push_back(*dst);
+    return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, s);
+  };
+  NearDev nd{};
+  nd.npan = nt->npan; nd.k = nt->k; nd.n_r = n_r; nd.M1 = M1; nd.K = K;
+  double *d_pts = nullptr, *d_part = nullptr, *d_out = nullptr, *d_corr = nullptr;
+  int64_t *d_cnt = nullptr, *d_off = nullptr, *d_list = nullptr, *d_ppt = nullptr;
+  int* d_status = nullptr;
+  int rc = NC_OK;
+  cudaError_t e = cudaSuccess;
+  void* v = nullptr;
+#define NC_DUP(ptr, bytes, field) \
+  if (e == cudaSuccess) { e = dup(ptr, bytes, &v); field = (decltype(field))v; }
+  NC_DUP(nt->edges, (size_t)(nt->npan + 1) * 8, nd.edges)
+  NC_DUP(nt->t, (size_t)n_r * 8, nd.t)
+  NC_DUP(nt->w, (size_t)n_r * 8, nd.w)
+  NC_DUP(nt->sigma, (size_t)K * n_r * 8, nd.sigma)
+  NC_DUP(mc_off.data(), mc_off.size() * sizeof(int), nd.mc_off)
+  NC_DUP(mc_col.data(), mc_col.size() * sizeof(int), nd.mc_col)
+  NC_DUP(glx.data(), glx.size() * 8, nd.gl_x)
+  NC_DUP(glw.data(), glw.size() * 8, nd.gl_w)
+  NC_DUP(bary.data(), bary.size() * 8, nd.bary)
+  NC_DUP(trig.data(), trig.size() * 8, nd.trig)
+  NC_DUP(pts, (size_t)n_pts * 3 * 8, d_pts)
+#undef NC_DUP
+  auto dal = [&](size_t bytes, void** dst) -> cudaError_t {
+    cudaError_t e2 = cudaMalloc(dst, std::max<size_t>(bytes, 16));
+    if (e2 == cudaSuccess) bufs.push_back(*dst);
+    return e2;
+  };
+  if (e == cudaSuccess) e = dal((size_t)2 * nseg * n_pts * 8, &v), d_part = (double*)v;
+  if (e == cudaSuccess) e = dal((size_t)2 * n_pts * 8, &v), d_out = (double*)v;
+  if (e == cudaSuccess) e = dal((size_t)(n_pts + 1) * 8, &v), d_cnt = (int64_t*)v;
+  if (e == cudaSuccess) e = dal((size_t)(n_pts + 1) * 8, &v), d_off = (int64_t*)v;
+  if (e == cudaSuccess) e = dal(sizeof(int), &v), d_status = (int*)v;
+  int64_t npairs = 0;
+  std::vector<int64_t> off(n_pts + 1, 0);
+  if (e == cudaSuccess) {
+    // the compressed field of every patch, then the near pairs
+    launch_field(h->kind, d_pts, n_pts, d_rec, nrec, nseg, d_part, d_part + (size_t)nseg * n_pts, d_out,
+                 d_out + n_pts, s);
+    launch_near_count(d_pts, n_pts, h->d_centers, h->N, kNearRadius * h->eps, d_cnt, nullptr, nullptr, s);
+    std::vector<int64_t> cnt(n_pts);
+    e = cudaMemcpyAsync(cnt.data(), d_cnt, (size_t)n_pts * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    for (int64_t t = 0; t < n_pts && e == cudaSuccess; ++t) {
+      off[t + 1] = off[t] + cnt[t];
+      const double r = std::sqrt(pts[3 * t] * pts[3 * t] + pts[3 * t + 1] * pts[3 * t + 1] + pts[3 * t + 2] * pts[3 * t + 2]);
+      if (cnt[t] > 0 && std::fabs(1.0 - r) < kNearMinHeight * h->eps && rc == NC_OK)
+        rc = fail(NC_EINVAL, "nc_field_near: point " + std::to_string(t) + " is closer than eps/100 to the sphere "
+                             "near a patch");
+    }
+    npairs = off[n_pts];
+  }
+  if (e == cudaSuccess && rc == NC_OK && npairs > 0) {
+    std::vector<int64_t> ppt(npairs);
+    for (int64_t t = 0; t < n_pts; ++t)
+      for (int64_t q = off[t]; q < off[t + 1]; ++q) ppt[q] = t;
+    e = cudaMemcpyAsync(d_off, off.data(), (size_t)(n_pts + 1) * 8, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = dal((size_t)npairs * 8, &v), d_list = (int64_t*)v;
+    if (e == cudaSuccess) e = dal((size_t)npairs * 8, &v), d_corr = (double*)v;
+    if (e == cudaSuccess) e = dup(ppt.data(), (size_t)npairs * 8, &v), d_ppt = (int64_t*)v;
+    if (e == cudaSuccess) e = cudaMemsetAsync(d_status, 0, sizeof(int), s);
+    if (e == cudaSuccess) {
+      launch_near_count(d_pts, n_pts, h->d_centers, h->N, kNearRadius * h->eps, nullptr, d_list, d_off, s);
+      launch_near_quad(h->kind, d_ppt, d_list, npairs, d_pts, h->d_frames, x_all, nd, d_rec, p0, d_corr, d_status, s);
+      launch_near_apply(d_off, d_corr, n_pts, d_out, s);
+      e = cudaGetLastError();
+    }
+    int status = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && status)
+      rc = fail(NC_EINVAL, status == 1 ? "nc_field_near: a point needs more than the radial node budget"
+                                       : "nc_field_near: a point is too close to a patch for the angular rule");
+  }
+  if (e == cudaSuccess && rc == NC_OK) e = cudaMemcpyAsync(out, d_out, (size_t)n_pts * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess && rc == NC_OK) rc = cuda_fail(e, "nc_field_near");
+  if (rc == NC_OK && mfpt) {   // vbar (eq:vtilde) with D = -I_sigma; I_sigma = I . sum_i fhat_i (eq:getI)
+    rc = ensure_red(h, std::max<int64_t>(4096, 1024 + (int64_t)592 * h->K + 16));
+    if (rc == NC_OK) {
+      double* d_sum = h->d_red;
+      launch_colsum(x_all, h->N, h->K, h->d_red + 1024, d_sum, s);
+      std::vector<double> col(h->K);
+      e = cudaMemcpyAsync(col.data(), d_sum, h->K * sizeof(double), cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "nc_field_near (I_sigma)");
+      double Is = 0.0;
+      for (int a = 0; a < h->K; ++a) Is += h->h_I[a] * col[a];
+      const double D = -Is;
+      for (int64_t t = 0; t < n_pts && rc == NC_OK; ++t) {
+        const double r2 = pts[3 * t] * pts[3 * t] + pts[3 * t + 1] * pts[3 * t + 1] + pts[3 * t + 2] * pts[3 * t + 2];
+        mfpt[t] = (out[t] - 1.0) / (3.0 * D) + (1.0 - r2) / 6.0;
+      }
+    }
+  }
+  if (n_near) *n_near = npairs;
+  for (void* b : bufs) cudaFree(b);
+  cudaFree(d_rec);
+  return rc;
+}
+
 int nc_residual(nc_handle* h, const double* x_all, int n_sel, const int64_t* patches, int n_res,
                 const double* res_rhat, const double* res_w, const double* res_S, double* res, double* pointwise) {
   if (!h || !x_all || n_sel < 0 || n_res < 1 || (n_sel > 0 && (!patches || !res_rhat || !res_w || !res_S || !res)))

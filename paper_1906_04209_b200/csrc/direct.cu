@@ -536,15 +536,17 @@ __global__ void __launch_bounds__(256) k_pair_mix(const double2* __restrict__ ts
   const int kmid = 1 << (19 - far_table_bits(FAR));
   constexpr int TPT = 2, NS = 8;
   double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
-  for (int u = 0; u < TPT; ++u) {   // targets on a small cap, sources a few cap radii away: a grid pair's geometry
-    const double th = 0.3 + 0.0001 * (threadIdx.x + 256 * u);
+  // targets on a small cap (arc 0.300 .. 0.305), sources 0.055 .. 0.075 away: x = qh (1 + w) in [2^-8, 2^-5)
+  // interior, 1 + w in [2^4, 2^6) exterior -- inside the table run_pair_mix builds (the loop reads it unclamped)
+  for (int u = 0; u < TPT; ++u) {
+    const double th = 0.3 + 1e-5 * (threadIdx.x + 256 * u);
     x[u] = -0.5 * sin(th); y[u] = 0.0; z[u] = -0.5 * cos(th);
     cq[u] = 0.5 * (x[u] * x[u] + y[u] * y[u] + z[u] * z[u] + 0.25);
     acc[u] = 0.0;
   }
   double4 s[NS];
   for (int k = 0; k < NS; ++k) {
-    const double ph = 0.36 + 0.002 * k + 0.00001 * blockIdx.x;
+    const double ph = 0.36 + 0.002 * k + 1e-7 * blockIdx.x;
     s[k] = make_double4(0.5 * sin(ph), 0.0005 * k, 0.5 * cos(ph), 1e-3 * (k + 1));
   }
   for (int it = 0; it < iters; ++it) {
@@ -568,8 +570,9 @@ static int run_pair_mix(int ctas_per_sm, double* ms_out, double* warp_pairs_out)
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int bits = far_table_bits(FAR), per = 1 << bits;
-  // a table spanning the exponents this geometry produces (interior x ~ d/4 ~ 1e-2, exterior x = 1 + 2/d ~ 20)
-  const int E0 = KIND == 1 ? 1023 : 1015, nexp = 8, fn = nexp * per, fbase = E0 * per;
+  // a table spanning the exponents this geometry produces with margin (k_pair_mix: interior [2^-8, 2^-5), exterior
+  // [2^4, 2^6)): biased exponents 1012..1022 interior, 1023..1033 exterior
+  const int E0 = KIND == 1 ? 1023 : 1012, nexp = 11, fn = nexp * per, fbase = E0 * per;
   double2* tab = nullptr;
   double* out = nullptr;
   const int blocks = sms * ctas_per_sm;

@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "hier.cuh"
+#include "pairs.cuh"
 
 namespace nc {
 
@@ -79,6 +80,8 @@ struct HierState {
   int64_t* d_keys = nullptr;
   double* d_gframe = nullptr;
   double* d_gR = nullptr;
+  double* d_gRinv = nullptr;        // 1 / R per group (step 4: x = arc / R)
+  int asin_terms = 0;               // step 4 node geometry: terms of the asin series (0: atan2 per node)
   int32_t *d_gnr = nullptr, *d_gna = nullptr;
   int64_t *d_goff = nullptr, *d_coff = nullptr;
   int32_t* d_grid_ids = nullptr;
@@ -595,6 +598,10 @@ __device__ __forceinline__ void grid_eval_ang(const double2* __restrict__ cg, in
 
 constexpr int kAngNrMax = 12;   // grid_eval_ang instantiations (n_r = 1..12)
 
+// asin(s) = s sum_k c_k s^(2k), c_k = (2k)! / (4^k (k!)^2 (2k + 1))  (k_interp node geometry)
+__constant__ double kAsinC[10] = {1.0, 1.0 / 6.0, 3.0 / 40.0, 5.0 / 112.0, 35.0 / 1152.0, 63.0 / 2816.0,
+                                  231.0 / 13312.0, 143.0 / 10240.0, 6435.0 / 557056.0, 12155.0 / 1245184.0};
+
 template <int NPT, int PF = 0>
 __device__ __forceinline__ bool grid_eval_ang_any(int nr, const double2* __restrict__ cg, int M, const double (&x)[NPT],
                                                   const double (&w2)[NPT], const double (&c1)[NPT],
@@ -619,18 +626,53 @@ __device__ __forceinline__ bool grid_eval_ang_any(int nr, const double2* __restr
 template <int NT, int NPT, int MB, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Kstar, const int32_t* __restrict__ pgl,
                                                const int64_t* __restrict__ ggrid0,
-                                               const double* __restrict__ F, const double* __restrict__ gR,
+                                               const double* __restrict__ F, const double* __restrict__ gRinv,
                                                const int32_t* __restrict__ gnr, const int32_t* __restrict__ gna,
                                                const int64_t* __restrict__ coff, const double* __restrict__ coef,
                                                const double* __restrict__ tx, const double* __restrict__ ty,
                                                const double* __restrict__ tz, const double* __restrict__ udir,
                                                double* __restrict__ u, const uint8_t* __restrict__ gsep,
-                                               int nr_big, double lt) {
+                                               int nr_big, double lt, const double* __restrict__ cen,
+                                               int asin_terms, int cap) {
   // MB = 0 evaluates the grids with n_r <= kAngNrMax only (grid_eval_ang); a second pass (MB = 1, nr_big = 1) adds
   // the rest to u when any exists (tight precisions): the register-held accumulators of the first pass then need
   // no fallback code in the same kernel
   extern __shared__ double2 c2[];
+  // per level (one thread each, once per CTA): the group's grids (count, n_r, M, coefficient offset), frame, 1 / R,
+  // and the patch centre's (arc, sin arc, cos arc) about the group centre -- the level loop then reads no global
+  // metadata (its dependent load chains were the kernel's long-scoreboard stalls, profiles/r02d_ncu_full_interp)
+  __shared__ double lv_a0[kLmax + 1], lv_r0[kLmax + 1], lv_c0[kLmax + 1], lv_invR[kLmax + 1], lv_r9[kLmax + 1][9];
+  __shared__ int64_t lv_coff[kLmax + 1][kMaxGrids];
+  __shared__ int lv_ng[kLmax + 1], lv_nr[kLmax + 1][kMaxGrids], lv_M[kLmax + 1][kMaxGrids];
   const int64_t i = blockIdx.x;
+  if ((int)threadIdx.x <= L) {
+    const int lvl = threadIdx.x;
+    const int g = pgl[(int64_t)lvl * rc + i];
+    const int64_t kg0 = ggrid0[g], kg1 = ggrid0[g + 1];
+    const bool ok = kg0 != kg1 && gnr[kg0] != 0 && !(gsep && gsep[g]);
+    lv_ng[lvl] = ok ? (int)(kg1 - kg0) : 0;
+    if (ok) {
+      for (int64_t kg = kg0; kg < kg1; ++kg) {
+        lv_nr[lvl][kg - kg0] = gnr[kg];
+        lv_M[lvl][kg - kg0] = gna[kg] / 2;
+        lv_coff[lvl][kg - kg0] = coff[kg];
+      }
+      const double* r9 = F + 9 * (int64_t)g;
+      for (int e = 0; e < 9; ++e) lv_r9[lvl][e] = r9[e];
+      lv_invR[lvl] = gRinv[g];
+      if (asin_terms > 0) {
+        const double cx = cen[3 * i], cy = cen[3 * i + 1], czc = cen[3 * i + 2];
+        const double sx = r9[0] * cx + r9[1] * cy + r9[2] * czc;
+        const double sy = r9[3] * cx + r9[4] * cy + r9[5] * czc;
+        const double cz = r9[6] * cx + r9[7] * cy + r9[8] * czc;
+        const double r0 = sqrt(sx * sx + sy * sy);
+        lv_a0[lvl] = atan2(r0, cz);
+        lv_r0[lvl] = r0;
+        lv_c0[lvl] = cz;
+      }
+    }
+  }
+  __syncthreads();
   for (int kb = 0; kb < Kstar; kb += NPT * NT) {
     double acc[NPT], px[NPT], py[NPT], pz[NPT];
 #pragma unroll
@@ -640,41 +682,74 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
       px[q] = 2.0 * tx[t]; py[q] = 2.0 * ty[t]; pz[q] = 2.0 * tz[t];
       acc[q] = nr_big ? u[t] : (udir ? udir[t] : 0.0);   // second pass: add to the first's result
     }
-    for (int lvl = 0; lvl <= L; ++lvl) {
-      const int g = pgl[(int64_t)lvl * rc + i];
-      const int64_t kg0 = ggrid0[g], kg1 = ggrid0[g + 1];
-      if (kg0 == kg1 || gnr[kg0] == 0) continue;   // block-uniform (a group's grids are all local or none)
-      if (gsep && gsep[g]) continue;                // evaluated by k_interp_sep
-      __syncthreads();                              // previous level's readers of c2 are done
-      {
-        int base = 0;
-        for (int64_t kg = kg0; kg < kg1; ++kg) {
-          const int ncp = (gna[kg] / 2 + 1) * gnr[kg];
-          const double2* __restrict__ src = reinterpret_cast<const double2*>(coef + coff[kg]);
-          for (int t = threadIdx.x; t < ncp; t += NT) c2[base + t] = src[t];
-          base += ncp;
-        }
+    // the levels whose group has grids here (block-uniform: a group's grids are all local or none; single-member
+    // groups are k_interp_sep's); the coefficients of every grid of the next such level are copied global ->
+    // shared with cp.async into the other half of c2 while this level is evaluated (double buffer, cap pairs each)
+    auto next_level = [&](int lv) {
+      while (lv <= L && lv_ng[lv] == 0) ++lv;
+      return lv;
+    };
+    auto stage = [&](int lv, double2* dst) {
+      int base = 0;
+      for (int q = 0; q < lv_ng[lv]; ++q) {
+        const int ncp = (lv_M[lv][q] + 1) * lv_nr[lv][q];
+        const double2* __restrict__ src = reinterpret_cast<const double2*>(coef + lv_coff[lv][q]);
+        for (int t = threadIdx.x; t < ncp; t += NT) cp_async16(dst + base + t, src + t);
+        base += ncp;
       }
-      __syncthreads();
-      const double* r9 = F + 9 * (int64_t)g;
-      const double invR = 1.0 / gR[g];
+      cp_async_commit();
+    };
+    int buf = 0;
+    int lvl = next_level(0);
+    if (lvl <= L) stage(lvl, c2);
+    while (lvl <= L) {
+      const int nxt = next_level(lvl + 1);
+      if (nxt <= L) {
+        stage(nxt, c2 + (size_t)(buf ^ 1) * cap);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();                              // this level's coefficients are in shared memory
+      const double2* __restrict__ cl = c2 + (size_t)buf * cap;
+      const double* r9 = lv_r9[lvl];
+      const double invR = lv_invR[lvl];
       double x[NPT], w2[NPT], c1[NPT], s1[NPT];
 #pragma unroll
       for (int q = 0; q < NPT; ++q) {
         const double sx = r9[0] * px[q] + r9[1] * py[q] + r9[2] * pz[q];
         const double sy = r9[3] * px[q] + r9[4] * py[q] + r9[5] * pz[q];
         const double cz = r9[6] * px[q] + r9[7] * py[q] + r9[8] * pz[q];
-        const double rho = sqrt(sx * sx + sy * sy);
-        x[q] = atan2(rho, cz) * invR;
-        const double irho = rho > 0 ? 1.0 / rho : 0.0;
-        c1[q] = rho > 0 ? sx * irho : 1.0;
-        s1[q] = rho > 0 ? sy * irho : 0.0;
+        const double rho2 = fma(sx, sx, sy * sy);
+        double rho = 0.0;
+        if (rho2 > 0.0) {
+          const double irho = fast_rsqrt(rho2);
+          rho = rho2 * irho;
+          c1[q] = sx * irho;
+          s1[q] = sy * irho;
+        } else {
+          c1[q] = 1.0;
+          s1[q] = 0.0;
+        }
+        double arc;
+        if (asin_terms > 0) {
+          // arc = arc(centre) + asin(sin(arc - arc(centre))), |arc - arc(centre)| <= eps: the series in s^2 (Horner,
+          // asin_terms terms, block-uniform) instead of an fp64 atan2 per node and level
+          const double sd = fma(rho, lv_c0[lvl], -cz * lv_r0[lvl]);
+          const double z = sd * sd;
+          double pa = kAsinC[asin_terms - 1];
+          for (int k = asin_terms - 2; k >= 0; --k) pa = fma(pa, z, kAsinC[k]);
+          arc = fma(sd, pa, lv_a0[lvl]);
+        } else {
+          arc = atan2(rho, cz);
+        }
+        x[q] = arc * invR;
         w2[q] = 4.0 * x[q] * x[q] - 2.0;
       }
       int base = 0;
-      for (int64_t kg = kg0; kg < kg1; ++kg) {
-        const int nr = gnr[kg], M = gna[kg] / 2;
-        const double2* __restrict__ cg = c2 + base;
+      for (int qg = 0; qg < lv_ng[lvl]; ++qg) {
+        const int nr = lv_nr[lvl][qg], M = lv_M[lvl][qg];
+        const double2* __restrict__ cg = cl + base;
         base += (M + 1) * nr;
         if (MB == 0 || MB == 3 || MB == 4) {
           // orders this thread's nodes need (R26c): order m has amplitude ~(rho / beta)^m at radius rho R, and the
@@ -802,6 +877,9 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
           }
         }
       }
+      __syncthreads();                              // every reader of buffer `buf` is done before it is refilled
+      lvl = nxt;
+      buf ^= 1;
     }
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
@@ -925,14 +1003,15 @@ static InterpVariant interp_variant() {
 
 template <int NT, int NPT, int MB, int MINB>
 static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t* pgl, const int64_t* ggrid0,
-                           const double* F, const double* gR, const int32_t* gnr, const int32_t* gna,
+                           const double* F, const double* gRinv, const int32_t* gnr, const int32_t* gna,
                            const int64_t* coff, const double* coef, const double* tx, const double* ty,
                            const double* tz, const double* udir, double* u, const uint8_t* gsep, cudaStream_t s,
-                           int nr_big = 0, double lt = 0.0) {
+                           int nr_big, double lt, const double* cen, int asin_terms) {
   auto kern = k_interp<NT, NPT, MB, MINB>;
   if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
-                                     nr_big, lt);
+  // shm: the two coefficient buffers (cap = shm / 32 pairs each, 16-byte aligned halves)
+  kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
+                                     nr_big, lt, cen, asin_terms, (int)(shm / (2 * sizeof(double2))));
   return NC_OK;
 }
 
@@ -946,10 +1025,10 @@ static bool interp_listed(const InterpVariant& v) {
 }
 
 static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int namax, const int32_t* pgl,
-                         const int64_t* ggrid0, const double* F, const double* gR, const int32_t* gnr,
+                         const int64_t* ggrid0, const double* F, const double* gRinv, const int32_t* gnr,
                          const int32_t* gna, const int64_t* coff, const double* coef, const double* tx,
                          const double* ty, const double* tz, const double* udir, double* u, const uint8_t* gsep,
-                         double lt, cudaStream_t s) {
+                         double lt, const double* cen, int asin_terms, cudaStream_t s) {
   (void)namax;
   // defaults: the 248-node rule takes one 128-thread CTA per patch with the coefficient prefetch (MB = 3: rest of
   // the C5 step 20.07 -> 18.32 ms, bitwise-identical output, profiles/r01w_interp_prefetch_c5.jsonl); larger K*
@@ -967,13 +1046,13 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
   const bool two_pass = (v.mb == 0 || v.mb == 3) && nrmax > kAngNrMax;
 #define NC_I(NT, NPT, MB, MINB)                                                                                  \
   if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                                \
-    NC_TRY((launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, \
-                                               tz, udir, u, gsep, s, 0, lt)));
+    NC_TRY((launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx,   \
+                                               ty, tz, udir, u, gsep, s, 0, lt, cen, asin_terms)));
   NC_INTERP_LIST(NC_I)
 #undef NC_I
   if (two_pass)
-    return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gR, gnr, gna, coff, coef, tx, ty, tz, udir,
-                                         u, gsep, s, 1);
+    return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx, ty, tz, udir,
+                                         u, gsep, s, 1, 0.0, cen, asin_terms);
   return NC_OK;
 }
 
@@ -1302,6 +1381,23 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_TRY(download(H->il, d_il, nil, s));
   NC_TRY(download(H->gc, d_gc, 3 * G, s));
   NC_TRY(download(H->gR, H->d_gR, G, s));
+  {
+    std::vector<double> rinv(G);
+    for (int64_t g = 0; g < G; ++g) rinv[g] = 1.0 / H->gR[g];
+    NC_TRY(upload(h, &H->d_gRinv, rinv, s));
+  }
+  // step-4 node geometry (k_interp): a node's arc from the group centre is arc(patch centre) + asin(sin(difference));
+  // |difference| <= eps, and the series s (1 + s^2/6 + 3 s^4/40 + ...) needs n terms for |s|^(2n+1)/(2n+1) < 1e-17
+  {
+    const double smax = std::sin(1.02 * eps);
+    H->asin_terms = 0;
+    if (smax < 0.2)
+      for (int n = 1; n <= 10; ++n)
+        if (std::pow(smax, 2 * n + 1) / (2 * n + 1) < 1e-17) {
+          H->asin_terms = n;
+          break;
+        }
+  }
   cudaFree(d_tmp);
   for (void* q : {(void*)d_gkey, (void*)d_lvl, (void*)d_cnt, (void*)d_off, (void*)d_nbr, (void*)d_gfirst,
                   (void*)d_glast, (void*)d_pg, (void*)d_il, (void*)d_cen, (void*)d_gc})
@@ -1868,10 +1964,11 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   h->launches_last += H->nwork_near > 0;
   // step 4b: interpolation to the Zernike nodes, summed over levels
   if (rc > 0) {
-    const size_t shm = (size_t)std::max(H->cgroupmax, 1) * sizeof(double);   // all grids of one group
-    NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gR,
+    // two buffers for all grids of one group (cgroupmax doubles, even: pairs)
+    const size_t shm = 2 * (size_t)std::max(H->cgroupmax, 2) * sizeof(double);
+    NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
                          H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u,
-                         H->d_gsep, H->interp_lt, s));
+                         H->d_gsep, H->interp_lt, h->d_centers + 3 * h->row_begin, H->asin_terms, s));
     h->launches_last++;
   }
   if (H->nwork_sep) {   // single-member groups, separably (adds to u)
@@ -1920,7 +2017,7 @@ void hier_grid_variant(const nc_handle* h, int* v8) {
 void hier_destroy(nc_handle* h) {
   HierState* H = h->hier;
   if (!H) return;
-  void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_ids,
+  void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gRinv, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_ids,
                   H->d_grid_group, H->d_ggrid0, H->d_counter, H->d_ftab, H->d_rbase, H->d_roff, H->d_gsep, H->d_work_sep, H->d_ring_t,
                   H->d_node_ring, H->d_node_cs,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,

@@ -225,6 +225,32 @@ void launch_residual(int n_sel, int n_res, int K, int nseg, const int64_t* rows,
 
 void launch_gather_rows(const double* x_all, const int64_t* rows, int n_sel, int K, double* out, cudaStream_t s);
 
+// NEXT-3 near the surface (nearfield.cu): the density quadrature of the patches near each point
+struct NearDev {
+  int npan, k, n_r, M1, K;
+  const double* edges;   // npan + 1
+  const double* t;       // n_r
+  const double* w;       // n_r
+  const double* sigma;   // K x n_r
+  const int* mc_off;     // 2 M1 + 1: CSR over (m, cos|sin) of the basis columns
+  const int* mc_col;     // K
+  const double* gl_x;    // k reference Gauss-Legendre nodes on [-1, 1] (of the regular panels)
+  const double* gl_w;    // k weights
+  const double* bary;    // k barycentric weights of those nodes
+  const double* trig;    // 4096 x (cos, sin) of 2 pi k / 4096
+};
+constexpr double kNearRadius = 4.0;          // a patch is near a point closer than this x eps to its centre
+constexpr double kNearMinHeight = 0.01;      // points near a patch must be >= this x eps off the sphere
+constexpr int kNearTrigN = 4096;
+// list == nullptr: cnt[t] = the number of centres within r of point t; else list[off[t] ..] = their indices
+void launch_near_count(const double* pts, int64_t n, const double* cen, int64_t N, double r, int64_t* cnt,
+                       int64_t* list, const int64_t* off, cudaStream_t s);
+size_t near_quad_smem(int n_r, int M1);
+int launch_near_quad(int kind, const int64_t* pair_pt, const int64_t* pair_patch, int64_t npairs, const double* pts,
+                     const double* frames, const double* x_all, const NearDev& nd, const double* rec, int p0,
+                     double* corr, int* status, cudaStream_t s);
+void launch_near_apply(const int64_t* off, const double* corr, int64_t n, double* out, cudaStream_t s);
+
 // BLAS-1 style helpers for GMRES (deterministic two-stage reductions)
 int64_t multidot_partials(int64_t n);
 void launch_multidot(const double* V, int64_t ldv, int nv, const double* w, int64_t n, double* part, double* out,

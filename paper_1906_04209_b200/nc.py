@@ -41,6 +41,11 @@ class NcOpts(ctypes.Structure):
                 ("check_separation", ctypes.c_int32)]
 
 
+class NcNearTables(ctypes.Structure):
+    _fields_ = [("npan", ctypes.c_int32), ("k", ctypes.c_int32), ("edges", _dp), ("t", _dp), ("w", _dp),
+                ("sigma", _dp), ("m", ctypes.POINTER(ctypes.c_int32)), ("c", ctypes.POINTER(ctypes.c_int32))]
+
+
 class NcStats(ctypes.Structure):
     _fields_ = [("N", ctypes.c_int64), ("row_begin", ctypes.c_int64), ("row_count", ctypes.c_int64),
                 ("K", ctypes.c_int32), ("Kstar", ctypes.c_int32), ("p", ctypes.c_int32), ("mode", ctypes.c_int32),
@@ -59,7 +64,7 @@ class NcStats(ctypes.Structure):
 
 
 EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt",
-           "nc_field", "nc_residual", "nc_density", "nc_id_sketch", "nc_modal_kernels", "nc_stats",
+           "nc_field", "nc_field_near", "nc_residual", "nc_density", "nc_id_sketch", "nc_modal_kernels", "nc_stats",
            "nc_time_stages", "nc_tree_lists", "nc_near_counts", "nc_pair_mix", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
 
 _lib = None
@@ -83,6 +88,7 @@ def load_library(path: str = LIB_PATH):
     L.nc_gmres.argtypes = [vp, vp, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int), _dp, vp]
     L.nc_flux_or_mfpt.argtypes = [vp, vp, _dp, _dp]
     L.nc_field.argtypes = [vp, vp, ctypes.c_int64, _dp, _dp, _dp]
+    L.nc_field_near.argtypes = [vp, vp, ctypes.c_int64, _dp, vp, _dp, _dp, _i64p]
     L.nc_residual.argtypes = [vp, vp, ctypes.c_int, _i64p, ctypes.c_int, _dp, _dp, _dp, _dp, _dp]
     L.nc_density.argtypes = [vp, vp, ctypes.c_int, _i64p, ctypes.c_int, _dp, _dp]
     L.nc_modal_kernels.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, _dp, _dp, ctypes.c_int, ctypes.c_int,
@@ -284,6 +290,30 @@ class Handle:
         _check(self._L.nc_field(self._h, _ptr(x_all, (self.N, self.K)), len(pts), pts.ctypes.data_as(_dp), out.ctypes.data_as(_dp),
                                 dmin.ctypes.data_as(_dp)))
         return out, dmin
+
+    def field_near(self, x_all, pts, tables, mfpt=False):
+        """NEXT-3 at any off-surface point, near the patches included (nc_field_near): the potential v (interior)
+        or u (exterior) at host points ``pts`` (n x 3), the patches within 4 eps of a point from their density
+        (the tables' near-field arrays, nc_tables/nearfield.py).  Returns (values, mfpt or None, near pairs)."""
+        if getattr(tables, "near_sigma", None) is None:
+            raise ValueError("the tables carry no near-field table (nc_tables/nearfield.py)")
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        keep = [np.ascontiguousarray(tables.near_edges, dtype=np.float64),
+                np.ascontiguousarray(tables.near_t, dtype=np.float64),
+                np.ascontiguousarray(tables.near_w, dtype=np.float64),
+                np.ascontiguousarray(tables.near_sigma, dtype=np.float64),
+                np.ascontiguousarray(tables.near_m, dtype=np.int32), np.ascontiguousarray(tables.near_c, dtype=np.int32)]
+        i32 = ctypes.POINTER(ctypes.c_int32)
+        nt = NcNearTables(len(keep[0]) - 1, int(tables.near_k), keep[0].ctypes.data_as(_dp), keep[1].ctypes.data_as(_dp),
+                          keep[2].ctypes.data_as(_dp), keep[3].ctypes.data_as(_dp), keep[4].ctypes.data_as(i32),
+                          keep[5].ctypes.data_as(i32))
+        out = np.empty(len(pts))
+        mf = np.empty(len(pts)) if mfpt else None
+        nn = ctypes.c_int64()
+        _check(self._L.nc_field_near(self._h, _ptr(x_all, (self.N, self.K)), len(pts), pts.ctypes.data_as(_dp),
+                                     ctypes.byref(nt), out.ctypes.data_as(_dp),
+                                     mf.ctypes.data_as(_dp) if mf is not None else None, ctypes.byref(nn)))
+        return out, mf, nn.value
 
     def residual(self, x_all, patches, tables):
         """L2 residual (eq:l2res) on the listed caller patches with the tables' residual grid (nc_residual);
