@@ -1137,14 +1137,30 @@ static int ring_margin() {   // points added to every adapted ring beyond the fi
   }
   return v;
 }
-static int ring_points_margin(double beta, double tol, int nr, int na, int margin, int* out) {
+// ring radii rho_k = cos((k + 1/2) pi / (2 n_r)) per n_r, computed once (the same expression as inline)
+constexpr int kRingMax = 64;
+static const double* ring_rho(int nr) {
+  static const std::vector<double> tab = [] {
+    std::vector<double> t((size_t)(kRingMax + 1) * kRingMax, 0.0);
+    for (int n = 1; n <= kRingMax; ++n)
+      for (int k = 0; k < n; ++k) t[(size_t)n * kRingMax + k] = cos((k + 0.5) * M_PI / (2.0 * n));
+    return t;
+  }();
+  return tab.data() + (size_t)nr * kRingMax;
+}
+// per ring k: 1.95 ln(1/tol) / ln(beta / rho_k), the ring-adaptive count before the margin (allocation-free: the
+// routing calls this for every candidate band of every group)
+static void ring_fit(double beta, double tol, int nr, double* fit) {
   const double lt = log(1.0 / tol);
+  const double* rho = ring_rho(nr);
+  for (int k = 0; k < nr; ++k) fit[k] = 1.95 * lt / log(std::max(beta, 1.0 + 1e-9) / rho[k]);
+}
+static int ring_points_margin_fit(const double* fit, int nr, int na, int margin, int* out) {
   int q = 0;
   for (int k = 0; k < nr; ++k) {
     int nk = na;
     if (ring_adapt()) {
-      const double rho = cos((k + 0.5) * M_PI / (2.0 * nr));
-      nk = (int)ceil(1.95 * lt / log(std::max(beta, 1.0 + 1e-9) / rho)) + margin;
+      nk = (int)ceil(fit[k]) + margin;
       nk += nk & 1;
       nk = std::min(na, std::max(nk, 8));
     }
@@ -1183,13 +1199,16 @@ static int ring_floor() {   // the smallest margin ring filling may trim to (NC_
 }
 
 static int ring_points(double beta, double tol, int nr, int na, int* out /* nr, or nullptr */) {
-  std::vector<int> hi(nr), lo(nr);
-  const int qh = ring_points_margin(beta, tol, nr, na, ring_margin(), hi.data());
+  if (nr > kRingMax) nr = kRingMax;   // (grid_size gives n_r ~ 10 at the tightest precisions)
+  double fit[kRingMax];
+  int hi[kRingMax], lo[kRingMax];
+  ring_fit(beta, tol, nr, fit);
+  const int qh = ring_points_margin_fit(fit, nr, na, ring_margin(), hi);
   if (!ring_adapt() || !ring_fill() || ring_margin() <= ring_floor()) {
-    if (out) std::copy(hi.begin(), hi.end(), out);
+    if (out) std::copy(hi, hi + nr, out);
     return qh;
   }
-  const int ql = ring_points_margin(beta, tol, nr, na, ring_floor(), lo.data());
+  const int ql = ring_points_margin_fit(fit, nr, na, ring_floor(), lo);
   int target = qh - (qh % 32);   // the largest multiple of 32 <= qh
   if (target < ql || warp_slots(target) >= warp_slots(qh)) target = qh;
   int q = qh;
@@ -1202,7 +1221,7 @@ static int ring_points(double beta, double tol, int nr, int na, int* out /* nr, 
         progress = true;
       }
   }
-  if (out) std::copy(hi.begin(), hi.end(), out);
+  if (out) std::copy(hi, hi + nr, out);
   return q;
 }
 static inline double harc(const double* a, const double* b) {
@@ -1557,6 +1576,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     diag_cost += best_cost;
     diag_groups2 += cuts.size() > 1;
   }
+  setup_tick("routing: per-group plans (host, parallel)");
   std::vector<GridPlan> plans;
   H->ggrid0.assign(G + 1, 0);
   for (int64_t g = 0; g < G; ++g) {
@@ -1759,6 +1779,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       }
     }
   }
+  setup_tick("units: per-grid (host, parallel)");
   {   // concatenate in grid order (offsets shifted), fixed-order statistics
     int64_t nu = 0, nch = 0, nsr = 0;
     for (const GridOut& o : gout) {
