@@ -24,7 +24,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peak.txt")
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "r02h_fp64_peak.txt")   # clocks during it: r02h_fp64_peak_clocks.csv
 
 
 def parse():

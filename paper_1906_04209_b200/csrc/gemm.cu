@@ -11,6 +11,9 @@
 // deterministic reduction), and the epilogue adds the identity term.  For step 1 with several outgoing-operator rungs
 // one GEMM applies the concatenated T_k of all rungs in use, its epilogue scattering column (k, m) into rung k's
 // source records through a per-column (base, row stride) map.
+#include <stdint.h>
+#include <stdlib.h>
+
 #include "nc_common.cuh"
 
 namespace nc {
@@ -98,10 +101,130 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Pipelined variant (single A operand): CTA tile 128 x 64 x 16, 8 warps (4 x 2) of 32 x 32 = 4 x 4 DMMA tiles (8
+// fragment loads per 16 DMMA), both operands copied global -> shared by cp.async into a double buffer (zero-filled
+// beyond the matrix edges), so the next k-slab streams in while the current one is multiplied (the
+// single-buffered kernel above reached 0.38 / 0.46 of the DMMA peak on K1 / P-apply).
+// ------------------------------------------------------------------------------------------------
+namespace {
+constexpr int PM = 128, PN = 64, PK = 16, PLD = PK + 4;
+
+__device__ __forceinline__ void cp16_zfill(void* dst, const void* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_gemm_dmma_pipe(const double* __restrict__ A, int64_t lda,
+                                                        const double* __restrict__ Bt, int64_t rows, int ncols, int kd,
+                                                        double* __restrict__ C, int64_t ldc, int cstride,
+                                                        const double* __restrict__ X, int64_t ldx,
+                                                        const int64_t* __restrict__ colbase,
+                                                        const int64_t* __restrict__ colrstride, int64_t crow0) {
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;                              // [2][PM][PLD]
+  double* Bs = gsm + 2 * PM * PLD;               // [2][PN][PLD]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;       // warp tile rows wm*32.., cols wn*32..
+  const int64_t row0 = (int64_t)blockIdx.x * PM;
+  const int col0 = blockIdx.y * PN;
+  auto issue = [&](int k0, int b) {
+    // A: 128 rows x 16 k = 1024 16-byte pieces (2 doubles), 4 per thread; B: 64 x 16 = 512, 2 per thread
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q, r = e >> 3, c = (e & 7) * 2;
+      const int64_t gr = row0 + r;
+      const int gk = k0 + c;
+      const bool ok = gr < rows && gk < kd;   // kd even: a piece is all in or all out
+      cp16_zfill(As + ((size_t)b * PM + r) * PLD + c, ok ? (const void*)(A + gr * lda + gk) : (const void*)A, ok);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int e = tid + 256 * q, r = e >> 3, c = (e & 7) * 2;
+      const int n = col0 + r;
+      const int gk = k0 + c;
+      const bool ok = n < ncols && gk < kd;
+      cp16_zfill(Bs + ((size_t)b * PN + r) * PLD + c, ok ? (const void*)(Bt + (int64_t)n * kd + gk) : (const void*)Bt,
+                 ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int nk = (kd + PK - 1) / PK;
+  issue(0, 0);
+  for (int s = 0; s < nk; ++s) {
+    if (s + 1 < nk) {
+      issue((s + 1) * PK, (s + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* as = As + (size_t)(s & 1) * PM * PLD;
+    const double* bs = Bs + (size_t)(s & 1) * PN * PLD;
+#pragma unroll
+    for (int kk = 0; kk < PK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) af[mi] = as[(wm * 32 + mi * 8 + (lane >> 2)) * PLD + kk + (lane & 3)];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[(wn * 32 + ni * 8 + (lane >> 2)) * PLD + kk + (lane & 3)];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
+    }
+    __syncthreads();   // every warp is done with buffer s & 1 before slab s + 2 is copied into it
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int64_t gr = row0 + wm * 32 + mi * 8 + (lane >> 2);
+    if (gr >= rows) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = col0 + wn * 32 + ni * 8 + (lane & 3) * 2 + e;
+        if (n >= ncols) continue;
+        double v = acc[mi][ni][e];
+        if (X) v += X[gr * ldx + n];
+        if (colbase)
+          C[colbase[n] + (crow0 + gr) * colrstride[n]] = v;
+        else
+          C[gr * ldc + (int64_t)n * cstride] = v;
+      }
+    }
+  }
+}
+
+static bool gemm_pipe_ok(const double* A, int64_t lda, const double* Bt, int kd) {
+  // cp.async needs 16-byte aligned rows: even leading dimensions and 16-byte aligned bases
+  return (lda % 2 == 0) && (kd % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)Bt % 16 == 0) &&
+         !getenv("NC_GEMM_SIMPLE");
+}
+
+static void launch_pipe(const double* A, int64_t lda, const double* Bt, int64_t rows, int ncols, int kd, double* C,
+                        int64_t ldc, int cstride, const double* X, int64_t ldx, const int64_t* colbase,
+                        const int64_t* colrstride, int64_t crow0, cudaStream_t s) {
+  const size_t smem = (size_t)2 * (PM + PN) * PLD * sizeof(double);
+  cudaFuncSetAttribute(k_gemm_dmma_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((unsigned)((rows + PM - 1) / PM), (unsigned)((ncols + PN - 1) / PN));
+  k_gemm_dmma_pipe<<<grid, 256, smem, s>>>(A, lda, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx, colbase, colrstride,
+                                           crow0);
+}
+
 void launch_gemm_dmma(const double* A, int64_t lda, int nparts, int64_t part_stride, const double* Bt, int64_t rows,
                       int ncols, int kd, double* C, int64_t ldc, int cstride, const double* X, int64_t ldx,
                       cudaStream_t s) {
   if (rows <= 0) return;
+  if (nparts == 1 && gemm_pipe_ok(A, lda, Bt, kd))
+    return launch_pipe(A, lda, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx, nullptr, nullptr, 0, s);
   dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((ncols + BN - 1) / BN));
   k_gemm_dmma<<<grid, 256, 0, s>>>(A, lda, nparts, part_stride, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx, nullptr,
                                    nullptr, 0);
@@ -110,6 +233,8 @@ void launch_gemm_dmma(const double* A, int64_t lda, int nparts, int64_t part_str
 void launch_gemm_dmma_colmap(const double* A, int64_t lda, const double* Bt, int64_t rows, int ncols, int kd, double* C,
                              const int64_t* colbase, const int64_t* colrstride, int64_t row0, cudaStream_t s) {
   if (rows <= 0 || ncols <= 0) return;
+  if (gemm_pipe_ok(A, lda, Bt, kd))
+    return launch_pipe(A, lda, Bt, rows, ncols, kd, C, 0, 0, nullptr, 0, colbase, colrstride, row0, s);
   dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((ncols + BN - 1) / BN));
   k_gemm_dmma<<<grid, 256, 0, s>>>(A, lda, 1, 0, Bt, rows, ncols, kd, C, 0, 0, nullptr, 0, colbase, colrstride, row0);
 }

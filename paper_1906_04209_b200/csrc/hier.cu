@@ -22,6 +22,7 @@
 // k_interp + k_interp_sep (step 4: every group's expansion at its members' Zernike nodes, summed over levels; R26,
 // R26c) -> K3 (api.cu).
 #include <cub/cub.cuh>
+#include <omp.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -1296,6 +1297,13 @@ int hier_order(nc_handle* h, std::vector<double>& centers) {
 int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   HierState* H = h->hier;
   const int64_t N = h->N;
+  // the host parts of the setup run on OpenMP threads; the ranks of one node share its cores (one process per GPU),
+  // so each takes its share (NC_SETUP_THREADS overrides)
+  if (const char* e = getenv("NC_SETUP_THREADS")) {
+    omp_set_num_threads(std::max(1, atoi(e)));
+  } else if (h->world > 1) {
+    omp_set_num_threads(std::max(1, omp_get_num_procs() / h->world));
+  }
   const int L = H->L;
   const double eps = h->eps;
   const int Ks = h->Kstar, p = h->p;
@@ -1448,23 +1456,46 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   if (const char* e = getenv("NC_MAX_GRIDS")) max_grids = std::max(1, std::min(kMaxGrids, atoi(e)));
   int ncuts = kGridCutQuantiles;
   if (const char* e = getenv("NC_GRID_CUTS")) ncuts = std::max(4, std::min(512, atoi(e)));
-  std::vector<std::vector<int32_t>> nsrc(G);
+  // every group's candidate sources, sorted, in flat arrays: group g's live at [cand_off[g], cand_off[g + 1]); its
+  // grids take consecutive bands of them, its near tail the rest (sorted by patch).  No per-group heap objects: the
+  // routing runs over ~2e5 groups at C5 and per-group vectors made it allocator-bound.
+  std::vector<int64_t> cand_off(G + 1, 0);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t g = 0; g < G; ++g) {
+    int64_t c = 0;
+    for (int64_t k = H->il_off[g]; k < H->il_off[g + 1]; ++k) c += H->glast[H->il[k]] - H->gfirst[H->il[k]];
+    if (H->glevel[g] == L)
+      for (int k = 0; k < 8; ++k)
+        if (H->nbr[8 * g + k] >= 0) c += H->glast[H->nbr[8 * g + k]] - H->gfirst[H->nbr[8 * g + k]];
+    cand_off[g + 1] = c;
+  }
+  for (int64_t g = 0; g < G; ++g) cand_off[g + 1] += cand_off[g];
+  std::vector<int32_t> F_src((size_t)cand_off[G]);
+  std::vector<int32_t> F_rung((size_t)cand_off[G]);
+  std::vector<double> F_dist((size_t)cand_off[G]);   // arc distance from the group's cap centre to each source centre
   struct GridPlan {
-    int32_t group, nr, na;
-    std::vector<int32_t> src;
-    std::vector<int> rung;
-    std::vector<double> dist;   // arc distance from the group's cap centre to each source centre
+    int32_t group = 0, nr = 0, na = 0;
+    int32_t cnt = 0;            // its sources: F_src / F_rung / F_dist [off, off + cnt)
+    int64_t off = 0;
     double beta = 0.0;          // the grid's nearest source (its size)
   };
-  std::vector<std::vector<GridPlan>> gplans(G);
+  std::vector<GridPlan> gp_slot((size_t)G * kMaxGrids);
+  std::vector<int8_t> gp_cnt(G, 0);
+  std::vector<int64_t> near_beg(G, 0), near_end(G, 0);   // the near tail of group g: F_src [near_beg, near_end)
   std::vector<double> gwork(G, 0.0);
   const bool diag = getenv("NC_HIER_DIAG") != nullptr;
   double diag_cost = 0.0;
   int64_t diag_groups2 = 0;
-  // groups are independent: host threads (OpenMP), results stored per group and concatenated in group order
-#pragma omp parallel for schedule(dynamic, 64) reduction(+ : diag_cost, diag_groups2)
+  // groups are independent: host threads (OpenMP) with per-thread scratch, results in per-group slots
+#pragma omp parallel reduction(+ : diag_cost, diag_groups2)
+  {
+  std::vector<std::pair<double, int32_t>> cand;
+  std::vector<int> rung_of;
+  std::vector<double> psum, qi, ovh, dp;
+  std::vector<size_t> qs, cuts;
+  std::vector<int> from;
+#pragma omp for schedule(dynamic, 64)
   for (int64_t g = 0; g < G; ++g) {
-    std::vector<std::pair<double, int32_t>> cand;
     const int lvl = H->glevel[g];
     const double* cg = &H->gc[3 * g];
     const double R = H->gR[g];
@@ -1490,8 +1521,8 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     // gap = d - R = R (beta - 1) + eps (per-level recompression)
     const size_t nc = cand.size();
     const int p0 = h->rung_p[0];
-    std::vector<int> rung_of(nc, 0);
-    std::vector<double> psum(nc + 1, 0.0);   // sum of the rung sizes of the n farthest candidates
+    rung_of.assign(nc, 0);
+    psum.assign(nc + 1, 0.0);   // sum of the rung sizes of the n farthest candidates
     for (size_t n = 0; n < nc; ++n) {
       const double gap = R * (cand[n].first - 1.0) + eps;
       int rung = 0;   // the smallest skeleton among the rungs valid on the whole grid (r_k <= gap)
@@ -1520,68 +1551,75 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     }
     // K >= 2 bands: dynamic programme over cut points on kGridCutQuantiles quantiles of the servable candidates;
     // a band ending at cut i lives on a grid sized by cand[cut_i - 1] (its q and overhead precomputed per cut)
-    std::vector<size_t> cuts;   // band boundaries chosen (ascending, last = end of the grid-served prefix)
+    cuts.clear();   // band boundaries chosen (ascending, last = end of the grid-served prefix)
     if (max_grids >= 2 && n_ok >= 2) {
-      std::vector<size_t> qs;
+      qs.clear();
       for (int k = 1; k <= ncuts; ++k) qs.push_back(std::max<size_t>(1, (n_ok * k) / ncuts));
       qs.erase(std::unique(qs.begin(), qs.end()), qs.end());
       const int Q = (int)qs.size();
-      std::vector<double> qi(Q), ovh(Q);
+      qi.assign(Q, 0.0);
+      ovh.assign(Q, 0.0);
       for (int i = 0; i < Q; ++i) {
         int nr, na;
         grid_size(cand[qs[i] - 1].first, tol, nr, na);
         qi[i] = (double)ring_points(cand[qs[i] - 1].first, tol, nr, na, nullptr);
         ovh[i] = c_interp * (double)mem * Ks * qi[i] + c_trans * qi[i] * (nr + na);
       }
-      // dp[k][i]: cheapest cover of [0, qs[i]) by k bands; from[k][i]: previous cut index (-1: band starts at 0)
-      std::vector<std::vector<double>> dp(max_grids + 1, std::vector<double>(Q, 1e300));
-      std::vector<std::vector<int>> from(max_grids + 1, std::vector<int>(Q, -1));
-      for (int i = 0; i < Q; ++i) dp[1][i] = qi[i] * psum[qs[i]] + ovh[i];
+      // dp[k Q + i]: cheapest cover of [0, qs[i]) by k bands; from[k Q + i]: previous cut index (-1: starts at 0)
+      dp.assign((size_t)(max_grids + 1) * Q, 1e300);
+      from.assign((size_t)(max_grids + 1) * Q, -1);
+      for (int i = 0; i < Q; ++i) dp[1 * Q + i] = qi[i] * psum[qs[i]] + ovh[i];
       for (int k = 2; k <= max_grids; ++k)
         for (int i = 1; i < Q; ++i)
           for (int j = 0; j < i; ++j) {
-            const double c = dp[k - 1][j] + qi[i] * (psum[qs[i]] - psum[qs[j]]) + ovh[i];
-            if (c < dp[k][i]) { dp[k][i] = c; from[k][i] = j; }
+            const double c = dp[(k - 1) * Q + j] + qi[i] * (psum[qs[i]] - psum[qs[j]]) + ovh[i];
+            if (c < dp[k * Q + i]) { dp[k * Q + i] = c; from[k * Q + i] = j; }
           }
       int bk = 0, bi = -1;
       for (int k = 2; k <= max_grids; ++k)
         for (int i = 0; i < Q; ++i) {
-          const double c = dp[k][i] + near_cost(qs[i]);
+          const double c = dp[k * Q + i] + near_cost(qs[i]);
           if (c < best_cost) { best_cost = c; bk = k; bi = i; }
         }
-      for (int k = bk, i = bi; k >= 1 && i >= 0; i = from[k][i], --k) cuts.push_back(qs[i]);
+      for (int k = bk, i = bi; k >= 1 && i >= 0; i = from[k * Q + i], --k) cuts.push_back(qs[i]);
       std::reverse(cuts.begin(), cuts.end());
     }
     if (cuts.empty() && cut2 > 0) cuts.push_back(cut2);   // the best single grid
+    const int64_t o0 = cand_off[g];
     auto emit = [&](size_t a, size_t b) {
       GridPlan gp;
       gp.group = (int32_t)g;
       grid_size(cand[b - 1].first, tol, gp.nr, gp.na);
       gp.beta = cand[b - 1].first;
+      gp.off = o0 + (int64_t)a;
+      gp.cnt = (int32_t)(b - a);
       for (size_t n = a; n < b; ++n) {
-        gp.src.push_back(cand[n].second);
-        gp.rung.push_back(rung_of[n]);
-        gp.dist.push_back(R * cand[n].first + eps);   // beta = (d - eps) / R
+        F_src[o0 + n] = cand[n].second;
+        F_rung[o0 + n] = rung_of[n];
+        F_dist[o0 + n] = R * cand[n].first + eps;   // beta = (d - eps) / R
       }
-      gplans[g].push_back(std::move(gp));
+      gp_slot[(size_t)g * kMaxGrids + gp_cnt[g]++] = gp;
     };
     size_t prev = 0;
     for (size_t c : cuts) {
       emit(prev, c);
       prev = c;
     }
-    for (size_t n = prev; n < nc; ++n) nsrc[g].push_back(cand[n].second);
-    std::sort(nsrc[g].begin(), nsrc[g].end());
+    for (size_t n = prev; n < nc; ++n) F_src[o0 + n] = cand[n].second;
+    std::sort(F_src.begin() + o0 + prev, F_src.begin() + o0 + nc);
+    near_beg[g] = o0 + (int64_t)prev;
+    near_end[g] = o0 + (int64_t)nc;
     gwork[g] = best_cost;
     diag_cost += best_cost;
     diag_groups2 += cuts.size() > 1;
+  }
   }
   setup_tick("routing: per-group plans (host, parallel)");
   std::vector<GridPlan> plans;
   H->ggrid0.assign(G + 1, 0);
   for (int64_t g = 0; g < G; ++g) {
     H->ggrid0[g] = (int64_t)plans.size();
-    for (GridPlan& gp : gplans[g]) plans.push_back(std::move(gp));
+    for (int q = 0; q < gp_cnt[g]; ++q) plans.push_back(gp_slot[(size_t)g * kMaxGrids + q]);
   }
   H->ggrid0[G] = (int64_t)plans.size();
   if (diag)
@@ -1591,7 +1629,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   setup_tick("routing + grid bands (host)");
   // rungs in use: a global decision (identical on every rank, so the per-rung all-gathers match)
   for (const GridPlan& gp : plans)
-    for (int r : gp.rung) h->rung_used[r] = 1;
+    for (int32_t n = 0; n < gp.cnt; ++n) h->rung_used[F_rung[gp.off + n]] = 1;
 
   // ---- partition: contiguous internal rows, weighted by work (world > 1) ----
   {
@@ -1685,131 +1723,163 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     return rung;
   };
   struct Slice { int64_t src0; int32_t nsrc; int rung; };
-  struct GridOut {   // one grid's units / chunks / source lists with grid-local offsets
-    std::vector<GridUnit> units;
-    std::vector<ChunkRec> chunks;
-    std::vector<int32_t> src;
-    double pairs = 0, slot = 0, wslot = 0;
-    std::vector<double> rung_pairs;
-  };
+  // grids are independent: blocks of kBlk grids go to host threads, each appending to its own buffers (no per-grid
+  // heap objects); the blocks are then copied into place in grid order with their offsets shifted (in parallel)
+  constexpr int64_t kBlk = 256;
   const int64_t NGL = (int64_t)H->grid_ids.size();
-  std::vector<GridOut> gout(NGL);
+  const int64_t nblk = (NGL + kBlk - 1) / kBlk;
+  struct BlockOut {
+    int thr = 0;
+    int64_t u0 = 0, nu = 0, c0 = 0, nc = 0, s0 = 0, ns = 0;   // ranges in the thread's buffers
+    double pairs = 0, slot = 0, wslot = 0;
+  };
+  std::vector<BlockOut> blk(nblk);
+  const int nthr = std::max(1, omp_get_max_threads());
+  std::vector<std::vector<GridUnit>> T_units(nthr);
+  std::vector<std::vector<ChunkRec>> T_chunks(nthr);
+  std::vector<std::vector<int32_t>> T_src(nthr);
+  std::vector<std::vector<double>> T_rp(nthr, std::vector<double>(h->nrung, 0.0));
   const int tpt_fill = H->gv.tpt, wpts_fill = 32 * tpt_fill;
-  // grids are independent: host threads build them, then the pieces are concatenated in grid order
 #pragma omp parallel
   {
+    const int th = omp_get_thread_num();
+    std::vector<GridUnit>& TU = T_units[th];
+    std::vector<ChunkRec>& TC = T_chunks[th];
+    std::vector<int32_t>& TS = T_src[th];
+    std::vector<double>& TR = T_rp[th];
     std::vector<std::pair<int, int32_t>> rs;
     std::vector<Slice> slices;
     std::vector<int> ring_rung;   // per (source, ring)
-#pragma omp for schedule(dynamic, 256)
-    for (int64_t gi = 0; gi < NGL; ++gi) {
-      const int32_t k = H->grid_ids[gi];
-      const GridPlan& gp = plans[k];
-      GridOut& o = gout[gi];
-      o.rung_pairs.assign(h->nrung, 0.0);
-      const int64_t q = H->goff[k + 1] - H->goff[k];
-      const double Rg = H->gR[gp.group];
-      const size_t ns_all = gp.src.size();
-      if (chunk_rungs) {
-        ring_rung.assign(ns_all * gp.nr, 0);
-        for (int kr = 0; kr < gp.nr; ++kr) {
-          const double rr = Rg * std::cos((kr + 0.5) * M_PI / (2.0 * gp.nr));
-          for (size_t n = 0; n < ns_all; ++n) ring_rung[n * gp.nr + kr] = best_rung(gp.dist[n] - rr);   // >= d - R
-        }
-      }
-      // the unit's sources bucketed by rung (sorted by patch within a bucket); slices never mix rungs
-      auto make_slices = [&](int kr0) {
-        rs.clear();
-        slices.clear();
-        for (size_t n = 0; n < ns_all; ++n)
-          rs.push_back({chunk_rungs ? ring_rung[n * gp.nr + kr0] : gp.rung[n], gp.src[n]});
-        std::sort(rs.begin(), rs.end());
-        size_t a = 0;
-        while (a < rs.size()) {
-          size_t b = a;
-          while (b < rs.size() && rs[b].first == rs[a].first) ++b;
-          const int64_t s0 = (int64_t)o.src.size();
-          for (size_t k2 = a; k2 < b; ++k2) o.src.push_back(rs[k2].second);
-          const int64_t ns = (int64_t)(b - a);
-          const int64_t nsl = (ns + kSliceMax - 1) / kSliceMax;
-          for (int64_t sl = 0; sl < nsl; ++sl) {
-            const int64_t x0 = s0 + (ns * sl) / nsl, x1 = s0 + (ns * (sl + 1)) / nsl;
-            slices.push_back({x0, (int32_t)(x1 - x0), rs[a].first});
-          }
-          a = b;
-        }
-      };
-      if (!chunk_rungs) make_slices(0);   // one list per grid, shared by its units
-      int kr_cached = -1;                 // chunks with the same first ring share their lists
-      for (int64_t c0 = 0; c0 < q; c0 += H->upts) {
-        ChunkRec cr;
-        cr.pt0 = H->goff[k] + c0;
-        cr.npt = (int32_t)std::min<int64_t>(H->upts, q - c0);
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t bi = 0; bi < nblk; ++bi) {
+      BlockOut& bo = blk[bi];
+      bo.thr = th;
+      bo.u0 = (int64_t)TU.size();
+      bo.c0 = (int64_t)TC.size();
+      bo.s0 = (int64_t)TS.size();
+      for (int64_t gi = bi * kBlk; gi < std::min(NGL, (bi + 1) * kBlk); ++gi) {
+        const int32_t k = H->grid_ids[gi];
+        const GridPlan& gp = plans[k];
+        const int64_t q = H->goff[k + 1] - H->goff[k];
+        const double Rg = H->gR[gp.group];
+        const size_t ns_all = (size_t)gp.cnt;
+        const int32_t* g_src = F_src.data() + gp.off;
+        const int32_t* g_rung = F_rung.data() + gp.off;
+        const double* g_dist = F_dist.data() + gp.off;
         if (chunk_rungs) {
-          const int32_t* ro = H->roff.data() + H->rbase[k];
-          int kr0 = 0;
-          while (c0 >= ro[kr0 + 1]) ++kr0;
-          if (kr0 != kr_cached) {
-            make_slices(kr0);
-            kr_cached = kr0;
+          ring_rung.assign(ns_all * gp.nr, 0);
+          for (int kr = 0; kr < gp.nr; ++kr) {
+            const double rr = Rg * std::cos((kr + 0.5) * M_PI / (2.0 * gp.nr));
+            for (size_t n = 0; n < ns_all; ++n) ring_rung[n * gp.nr + kr] = best_rung(g_dist[n] - rr);   // >= d - R
           }
         }
-        cr.u0 = (int64_t)o.units.size();
-        cr.nu = (int32_t)slices.size();
-        o.chunks.push_back(cr);
-        for (const Slice& sl : slices) {
-          GridUnit u;
-          u.pt0 = cr.pt0;
-          u.npt = cr.npt;
-          u.src0 = sl.src0;
-          u.nsrc = sl.nsrc;
-          u.soff = h->rung_soff[sl.rung];
-          u.p = h->rung_p[sl.rung];
-          u.pad_ = 0;
-          o.units.push_back(u);
-          const double pr = (double)cr.npt * sl.nsrc * h->rung_p[sl.rung];
-          o.pairs += pr;
-          o.rung_pairs[sl.rung] += pr;
-          o.slot += (double)H->upts * u.nsrc * u.p;
-          // active-warp lane slots; a tail warp with <= 32 points runs one point per lane (direct.cu)
-          const int full = u.npt / wpts_fill, rem = u.npt - full * wpts_fill;
-          const int tail = rem == 0 ? 0 : (tpt_fill > 1 && rem <= 32 ? 32 : wpts_fill);
-          o.wslot += (double)(full * wpts_fill + tail) * u.nsrc * u.p;
+        // the unit's sources bucketed by rung (sorted by patch within a bucket); slices never mix rungs; slice
+        // offsets are block-relative (shifted when the block is copied into place)
+        auto make_slices = [&](int kr0) {
+          rs.clear();
+          slices.clear();
+          for (size_t n = 0; n < ns_all; ++n)
+            rs.push_back({chunk_rungs ? ring_rung[n * gp.nr + kr0] : g_rung[n], g_src[n]});
+          std::sort(rs.begin(), rs.end());
+          size_t a = 0;
+          while (a < rs.size()) {
+            size_t b = a;
+            while (b < rs.size() && rs[b].first == rs[a].first) ++b;
+            const int64_t s0 = (int64_t)TS.size() - bo.s0;
+            for (size_t k2 = a; k2 < b; ++k2) TS.push_back(rs[k2].second);
+            const int64_t ns = (int64_t)(b - a);
+            const int64_t nsl = (ns + kSliceMax - 1) / kSliceMax;
+            for (int64_t sl = 0; sl < nsl; ++sl) {
+              const int64_t x0 = s0 + (ns * sl) / nsl, x1 = s0 + (ns * (sl + 1)) / nsl;
+              slices.push_back({x0, (int32_t)(x1 - x0), rs[a].first});
+            }
+            a = b;
+          }
+        };
+        if (!chunk_rungs) make_slices(0);   // one list per grid, shared by its units
+        int kr_cached = -1;                 // chunks with the same first ring share their lists
+        for (int64_t c0 = 0; c0 < q; c0 += H->upts) {
+          ChunkRec cr;
+          cr.pt0 = H->goff[k] + c0;
+          cr.npt = (int32_t)std::min<int64_t>(H->upts, q - c0);
+          if (chunk_rungs) {
+            const int32_t* ro = H->roff.data() + H->rbase[k];
+            int kr0 = 0;
+            while (c0 >= ro[kr0 + 1]) ++kr0;
+            if (kr0 != kr_cached) {
+              make_slices(kr0);
+              kr_cached = kr0;
+            }
+          }
+          cr.u0 = (int64_t)TU.size() - bo.u0;
+          cr.nu = (int32_t)slices.size();
+          TC.push_back(cr);
+          for (const Slice& sl : slices) {
+            GridUnit u;
+            u.pt0 = cr.pt0;
+            u.npt = cr.npt;
+            u.src0 = sl.src0;
+            u.nsrc = sl.nsrc;
+            u.soff = h->rung_soff[sl.rung];
+            u.p = h->rung_p[sl.rung];
+            u.pad_ = 0;
+            TU.push_back(u);
+            const double pr = (double)cr.npt * sl.nsrc * h->rung_p[sl.rung];   // integers: sums are exact
+            bo.pairs += pr;
+            TR[sl.rung] += pr;
+            bo.slot += (double)H->upts * u.nsrc * u.p;
+            // active-warp lane slots; a tail warp with <= 32 points runs one point per lane (direct.cu)
+            const int full = u.npt / wpts_fill, rem = u.npt - full * wpts_fill;
+            const int tail = rem == 0 ? 0 : (tpt_fill > 1 && rem <= 32 ? 32 : wpts_fill);
+            bo.wslot += (double)(full * wpts_fill + tail) * u.nsrc * u.p;
+          }
         }
       }
+      bo.nu = (int64_t)TU.size() - bo.u0;
+      bo.nc = (int64_t)TC.size() - bo.c0;
+      bo.ns = (int64_t)TS.size() - bo.s0;
     }
   }
   setup_tick("units: per-grid (host, parallel)");
-  {   // concatenate in grid order (offsets shifted), fixed-order statistics
-    int64_t nu = 0, nch = 0, nsr = 0;
-    for (const GridOut& o : gout) {
-      nu += (int64_t)o.units.size();
-      nch += (int64_t)o.chunks.size();
-      nsr += (int64_t)o.src.size();
+  {   // place the blocks in grid order (offsets shifted), statistics summed in block order (exact: integer-valued)
+    std::vector<int64_t> ub(nblk + 1, 0), cb(nblk + 1, 0), sb(nblk + 1, 0);
+    for (int64_t bi = 0; bi < nblk; ++bi) {
+      ub[bi + 1] = ub[bi] + blk[bi].nu;
+      cb[bi + 1] = cb[bi] + blk[bi].nc;
+      sb[bi + 1] = sb[bi] + blk[bi].ns;
+      H->pairs_grid += blk[bi].pairs;
+      H->slot_pairs += blk[bi].slot;
+      H->warp_slot_pairs += blk[bi].wslot;
     }
-    units.reserve(nu);
-    chunks.reserve(nch);
-    srclist.reserve(nsr);
-    for (GridOut& o : gout) {
-      const int64_t u_off = (int64_t)units.size(), s_off = (int64_t)srclist.size();
-      for (GridUnit u : o.units) {
-        u.src0 += s_off;
-        units.push_back(u);
+    units.resize(ub[nblk]);
+    chunks.resize(cb[nblk]);
+    srclist.resize(sb[nblk]);
+    std::vector<std::vector<char>> used(nthr, std::vector<char>(h->nrung, 0));
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t bi = 0; bi < nblk; ++bi) {
+      const BlockOut& bo = blk[bi];
+      std::vector<char>& us = used[omp_get_thread_num()];
+      const GridUnit* su = T_units[bo.thr].data() + bo.u0;
+      for (int64_t e = 0; e < bo.nu; ++e) {
+        GridUnit u = su[e];
+        u.src0 += sb[bi];
+        units[ub[bi] + e] = u;
         for (int kk = 0; kk < h->nrung; ++kk)
-          if (u.soff == h->rung_soff[kk]) h->rung_used[kk] = 1;
+          if (u.soff == h->rung_soff[kk]) us[kk] = 1;
       }
-      for (ChunkRec c : o.chunks) {
-        c.u0 += u_off;
-        chunks.push_back(c);
+      const ChunkRec* sc = T_chunks[bo.thr].data() + bo.c0;
+      for (int64_t e = 0; e < bo.nc; ++e) {
+        ChunkRec c = sc[e];
+        c.u0 += ub[bi];
+        chunks[cb[bi] + e] = c;
       }
-      srclist.insert(srclist.end(), o.src.begin(), o.src.end());
-      H->pairs_grid += o.pairs;
-      H->slot_pairs += o.slot;
-      H->warp_slot_pairs += o.wslot;
-      for (int kk = 0; kk < h->nrung; ++kk) rung_pairs[kk] += o.rung_pairs[kk];
-      GridOut().units.swap(o.units);
-      GridOut().src.swap(o.src);
+      std::copy(T_src[bo.thr].begin() + bo.s0, T_src[bo.thr].begin() + bo.s0 + bo.ns, srclist.begin() + sb[bi]);
     }
+    for (int t = 0; t < nthr; ++t)
+      for (int kk = 0; kk < h->nrung; ++kk) {
+        if (used[t][kk]) h->rung_used[kk] = 1;
+        rung_pairs[kk] += T_rp[t][kk];
+      }
   }
   if (diag) {
     fprintf(stderr, "[nc hier diag] grid pairs by rung (r/eps: pairs):");
@@ -1824,9 +1894,10 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   {
     std::vector<std::vector<int32_t>> nl(rc);
     for (int64_t g = 0; g < G; ++g) {
-      if (!rel[g] || nsrc[g].empty()) continue;
+      if (!rel[g] || near_beg[g] == near_end[g]) continue;
       const int64_t a = std::max<int64_t>(H->gfirst[g], rb), b = std::min<int64_t>(H->glast[g], re);
-      for (int64_t i = a; i < b; ++i) nl[i - rb].insert(nl[i - rb].end(), nsrc[g].begin(), nsrc[g].end());
+      for (int64_t i = a; i < b; ++i)
+        nl[i - rb].insert(nl[i - rb].end(), F_src.begin() + near_beg[g], F_src.begin() + near_end[g]);
     }
     for (int64_t i = 0; i < rc; ++i) {
       std::sort(nl[i].begin(), nl[i].end());
@@ -1872,6 +1943,22 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   }
 
   setup_tick("near lists, tree audit lists");
+  if (getenv("NC_SETUP_DIGEST")) {   // FNV-1a digests of the host plan (refactors of the setup must reproduce it)
+    auto fnv = [](const void* p, size_t n) {
+      uint64_t hsh = 1469598103934665603ull;
+      const unsigned char* b = (const unsigned char*)p;
+      for (size_t i = 0; i < n; ++i) hsh = (hsh ^ b[i]) * 1099511628211ull;
+      return (unsigned long long)hsh;
+    };
+    fprintf(stderr, "[nc setup digest] units %llx chunks %llx srclist %llx gnr %llx gna %llx goff %llx roff %llx "
+                    "ggrid0 %llx near_off %llx near %llx work_near %llx pairs %.17g\n",
+            fnv(units.data(), units.size() * sizeof(GridUnit)), fnv(chunks.data(), chunks.size() * sizeof(ChunkRec)),
+            fnv(srclist.data(), srclist.size() * 4), fnv(H->gnr.data(), H->gnr.size() * 4),
+            fnv(H->gna.data(), H->gna.size() * 4), fnv(H->goff.data(), H->goff.size() * 8),
+            fnv(H->roff.data(), H->roff.size() * 4), fnv(H->ggrid0.data(), H->ggrid0.size() * 8),
+            fnv(near_off.data(), near_off.size() * 8), fnv(near_all.data(), near_all.size() * 4),
+            fnv(work_near.data(), work_near.size() * 4), H->pairs_grid);
+  }
   for (int k = 0; k < h->nrung; ++k) H->pmax = std::max(H->pmax, h->rung_p[k]);
   // ---- uploads and device grids ----
   H->nunits = (int64_t)units.size();

@@ -241,3 +241,17 @@ def test_hier_small_layouts_vs_oracle(layout, N, eps, kind):
     x = random_coeffs(N, tab.K, 12)
     h = _nc().Handle(kind, c, eps, tab, mode=_nc().NC_HIER, precision=1e-9)
     assert rel(gpu_matvec(h, x), O.matvec(kind, c, tab, x)) <= HIER_TOL
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_matvec_bitwise_reproducible(name):
+    """Two matvecs of the same input are bitwise identical (fixed-order reductions everywhere, R16).  With
+    compute-sanitizer closed on this GPU pool, this is also the run-time evidence against races in the warp-level
+    grid kernel's cp.async double buffer and k_interp's: a race would make the sums order- or timing-dependent."""
+    cfg = CONFIGS[name]
+    tab = _phys(name)
+    h = _nc().Handle(cfg.kind, cfg.centers(), cfg.eps, tab, mode=_nc().NC_HIER, precision=cfg.precision)
+    x = torch.from_numpy(h.to_internal(random_coeffs(cfg.N, tab.K, 31))).cuda()
+    ys = [h.matvec(x).cpu().numpy() for _ in range(3)]
+    assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
+    h.close()
