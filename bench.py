@@ -59,7 +59,7 @@ def load_fp64_peak():
 
 
 # ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
-TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r01x_ncu_full_pairs_grid.json"}
+TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r02f_ncu_full_pairs_grid.json"}
 
 
 def profiled_traffic(kernel, config, mode):
@@ -323,7 +323,7 @@ def main():
                 "kernel": kname, "kernel_ms": pair_ms, "kernel_share_of_step": pair_ms / (ms_total / args.steps),
                 "note": "FP64 flops executed per pair by the running variant (SASS count, 2 per DFMA; nc_stats) x pairs "
                         "/ kernel ms (CUDA events around the kernel in every timed step); peak = measured DFMA "
-                        "throughput (profiles/r01_fp64_peak.txt, of measured); fp64_pipe_util = FP64 instructions / "
+                        "throughput (profiles/r02h_fp64_peak.txt, of measured, SM clock 1965 MHz under load); fp64_pipe_util = FP64 instructions / "
                         "(peak / 2); traffic = DRAM bytes per launch from " + (tsrc or "no capture"),
                 "pairs_per_s": pairs / (pair_ms * 1e-3)}
     # the fp64 tensor-core GEMMs (K1 T-apply over the used rungs, K3 P-apply + identity): DMMA roofline

@@ -61,37 +61,52 @@ static int dalloc(nc_handle* h, T** p, size_t count) {
 // -------------------------------------------------------------------------------------------------
 // host-side validation helpers
 // -------------------------------------------------------------------------------------------------
-// Minimum arc separation >= 3 eps (§3) via a uniform 3-D hash grid on chords.
+// Minimum arc separation >= 3 eps (§3) via a uniform 3-D cell grid on chords: the points sorted by
+// cell key, each point's 27 neighbour cells found by binary search; the check runs on the host threads and reports the
+// first offending pair in index order (deterministic).
 static int check_separation(const double* c, int64_t N, double eps) {
   const double min_arc = 3.0 * eps * (1.0 - 1e-12);
   const double chord = 2.0 * sin(0.5 * std::min(min_arc, M_PI));
   const double cell = std::max(chord, 1e-6);
   const int64_t nc = (int64_t)ceil(2.0 / cell) + 2;
   auto key = [&](int64_t a, int64_t b, int64_t d) { return (a * nc + b) * nc + d; };
-  std::unordered_map<int64_t, std::vector<int64_t>> grid;
-  grid.reserve((size_t)N * 2);
   auto cidx = [&](double v) { return (int64_t)floor((v + 1.0) / cell); };
-  for (int64_t i = 0; i < N; ++i) grid[key(cidx(c[3 * i]), cidx(c[3 * i + 1]), cidx(c[3 * i + 2]))].push_back(i);
+  std::vector<std::pair<int64_t, int64_t>> kc((size_t)N);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < N; ++i) kc[i] = {key(cidx(c[3 * i]), cidx(c[3 * i + 1]), cidx(c[3 * i + 2])), i};
+  std::sort(kc.begin(), kc.end());
+  int64_t bad_i = N, bad_j = N;
+  double bad_arc = 0.0;
+#pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t i = 0; i < N; ++i) {
-    int64_t a = cidx(c[3 * i]), b = cidx(c[3 * i + 1]), d = cidx(c[3 * i + 2]);
+    const int64_t a = cidx(c[3 * i]), b = cidx(c[3 * i + 1]), d = cidx(c[3 * i + 2]);
     for (int da = -1; da <= 1; ++da)
       for (int db = -1; db <= 1; ++db)
         for (int dd = -1; dd <= 1; ++dd) {
-          auto it = grid.find(key(a + da, b + db, d + dd));
-          if (it == grid.end()) continue;
-          for (int64_t j : it->second) {
+          const int64_t kk = key(a + da, b + db, d + dd);
+          auto it = std::lower_bound(kc.begin(), kc.end(), std::make_pair(kk, (int64_t)-1));
+          for (; it != kc.end() && it->first == kk; ++it) {
+            const int64_t j = it->second;
             if (j <= i) continue;
-            double dx = c[3 * i] - c[3 * j], dy = c[3 * i + 1] - c[3 * j + 1], dz = c[3 * i + 2] - c[3 * j + 2];
-            double ch = sqrt(dx * dx + dy * dy + dz * dz);
-            double arc = 2.0 * asin(std::min(1.0, 0.5 * ch));
+            const double dx = c[3 * i] - c[3 * j], dy = c[3 * i + 1] - c[3 * j + 1], dz = c[3 * i + 2] - c[3 * j + 2];
+            const double ch = sqrt(dx * dx + dy * dy + dz * dz);
+            const double arc = 2.0 * asin(std::min(1.0, 0.5 * ch));
             if (arc < min_arc) {
-              char buf[256];
-              snprintf(buf, sizeof buf, "patches %lld and %lld are %.6g apart in arc length (< 3 eps = %.6g)",
-                       (long long)i, (long long)j, arc, 3.0 * eps);
-              return fail(NC_ESEP, buf);
+#pragma omp critical(nc_sep)
+              if (i < bad_i || (i == bad_i && j < bad_j)) {
+                bad_i = i;
+                bad_j = j;
+                bad_arc = arc;
+              }
             }
           }
         }
+  }
+  if (bad_i < N) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "patches %lld and %lld are %.6g apart in arc length (< 3 eps = %.6g)",
+             (long long)bad_i, (long long)bad_j, bad_arc, 3.0 * eps);
+    return fail(NC_ESEP, buf);
   }
   return NC_OK;
 }

@@ -1487,20 +1487,32 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   double diag_cost = 0.0;
   int64_t diag_groups2 = 0;
   // groups are independent: host threads (OpenMP) with per-thread scratch, results in per-group slots
+  const bool sub_timing = getenv("NC_SETUP_TIMING") != nullptr;
+  std::vector<double> rt_acc((size_t)std::max(1, omp_get_max_threads()) * 6, 0.0);   // per-thread sub-phase seconds
 #pragma omp parallel reduction(+ : diag_cost, diag_groups2)
   {
+  double* rt = rt_acc.data() + (size_t)omp_get_thread_num() * 6;
+  double tmark = 0.0;
+  auto lap = [&](int k) {
+    if (!sub_timing) return;
+    const double t = omp_get_wtime();
+    if (k >= 0) rt[k] += t - tmark;
+    tmark = t;
+  };
   std::vector<std::pair<double, int32_t>> cand;
   std::vector<int> rung_of;
   std::vector<double> psum, qi, ovh, dp;
   std::vector<size_t> qs, cuts;
   std::vector<int> from;
-#pragma omp for schedule(dynamic, 64)
+  // dynamic 1: the few coarse-level groups (thousands of candidates each) come first and must spread over threads
+#pragma omp for schedule(dynamic, 1)
   for (int64_t g = 0; g < G; ++g) {
     const int lvl = H->glevel[g];
     const double* cg = &H->gc[3 * g];
     const double R = H->gR[g];
     const int64_t mem = H->glast[g] - H->gfirst[g];
     cand.clear();
+    lap(-1);
     auto add_box = [&](int64_t b) {
       for (int32_t j = H->gfirst[b]; j < H->glast[b]; ++j) {
         const double d = harc(cg, &cen[3 * (int64_t)j]);
@@ -1514,9 +1526,11 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       for (int k = 0; k < 8; ++k)
         if (H->nbr[8 * g + k] >= 0) add_box(H->nbr[8 * g + k]);
     if (cand.empty()) continue;
+    lap(0);
     std::sort(cand.begin(), cand.end(), [](const std::pair<double, int32_t>& a, const std::pair<double, int32_t>& b) {
       return a.first > b.first || (a.first == b.first && a.second < b.second);
     });
+    lap(1);
     // grid sources use the outgoing-operator rung valid at their distance to the nearest grid point,
     // gap = d - R = R (beta - 1) + eps (per-level recompression)
     const size_t nc = cand.size();
@@ -1539,6 +1553,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       return q * (psum[b] - psum[a]) + c_interp * (double)mem * Ks * q + c_trans * q * (nr + na);
     };
     auto near_cost = [&](size_t b) { return c_near * (double)mem * Ks * (double)(nc - b) * p0; };
+    lap(2);
     size_t n_ok = 0;   // candidates a grid may serve (beta >= kBetaMin)
     while (n_ok < nc && cand[n_ok].first >= kBetaMin) ++n_ok;
     double best_cost = near_cost(0);   // all direct
@@ -1551,6 +1566,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     }
     // K >= 2 bands: dynamic programme over cut points on kGridCutQuantiles quantiles of the servable candidates;
     // a band ending at cut i lives on a grid sized by cand[cut_i - 1] (its q and overhead precomputed per cut)
+    lap(3);
     cuts.clear();   // band boundaries chosen (ascending, last = end of the grid-served prefix)
     if (max_grids >= 2 && n_ok >= 2) {
       qs.clear();
@@ -1584,6 +1600,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       for (int k = bk, i = bi; k >= 1 && i >= 0; i = from[k * Q + i], --k) cuts.push_back(qs[i]);
       std::reverse(cuts.begin(), cuts.end());
     }
+    lap(4);
     if (cuts.empty() && cut2 > 0) cuts.push_back(cut2);   // the best single grid
     const int64_t o0 = cand_off[g];
     auto emit = [&](size_t a, size_t b) {
@@ -1612,7 +1629,14 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     gwork[g] = best_cost;
     diag_cost += best_cost;
     diag_groups2 += cuts.size() > 1;
+    lap(5);
   }
+  }
+  if (sub_timing) {
+    double tot[6] = {0, 0, 0, 0, 0, 0};
+    for (size_t t = 0; t < rt_acc.size(); ++t) tot[t % 6] += rt_acc[t];
+    fprintf(stderr, "[nc setup]   routing thread-seconds: gather %.3f sort %.3f rungs %.3f single-grid %.3f dp %.3f "
+                    "emit %.3f\n", tot[0], tot[1], tot[2], tot[3], tot[4], tot[5]);
   }
   setup_tick("routing: per-group plans (host, parallel)");
   std::vector<GridPlan> plans;
@@ -1628,8 +1652,16 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
 
   setup_tick("routing + grid bands (host)");
   // rungs in use: a global decision (identical on every rank, so the per-rung all-gathers match)
-  for (const GridPlan& gp : plans)
-    for (int32_t n = 0; n < gp.cnt; ++n) h->rung_used[F_rung[gp.off + n]] = 1;
+  {
+    std::vector<char> used((size_t)std::max(1, omp_get_max_threads()) * h->nrung, 0);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t k = 0; k < (int64_t)plans.size(); ++k) {
+      char* u = used.data() + (size_t)omp_get_thread_num() * h->nrung;
+      for (int32_t n = 0; n < plans[k].cnt; ++n) u[F_rung[plans[k].off + n]] = 1;
+    }
+    for (size_t e = 0; e < used.size(); ++e)
+      if (used[e]) h->rung_used[e % h->nrung] = 1;
+  }
 
   // ---- partition: contiguous internal rows, weighted by work (world > 1) ----
   {
@@ -1663,18 +1695,29 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   H->rbase.assign(NG + 1, 0);
   H->roff.clear();
   H->grid_ids.clear();
+  // ring sizes of every relevant grid in parallel (ring_points per grid), then the offsets in grid order
+  std::vector<int64_t> qk(NG, 0), rb0(NG + 1, 0);
+  for (int64_t k = 0; k < NG; ++k) rb0[k + 1] = rb0[k] + (rel[plans[k].group] ? plans[k].nr + 1 : 0);
+  H->roff.assign((size_t)rb0[NG], 0);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t k = 0; k < NG; ++k) {
+    const GridPlan& gp = plans[k];
+    if (!rel[gp.group]) continue;
+    int rs[kRingMax];
+    qk[k] = ring_points(gp.beta, tol, gp.nr, gp.na, rs);
+    int32_t* ro = H->roff.data() + rb0[k];
+    ro[0] = 0;
+    for (int kr = 0; kr < gp.nr; ++kr) ro[kr + 1] = ro[kr] + rs[kr];
+  }
   for (int64_t k = 0; k < NG; ++k) {
     const GridPlan& gp = plans[k];
     H->grid_group[k] = gp.group;
     int64_t q = 0, c = 0;
-    H->rbase[k] = (int64_t)H->roff.size();
+    H->rbase[k] = rb0[k];
     if (rel[gp.group]) {
       H->gnr[k] = gp.nr;
       H->gna[k] = gp.na;
-      std::vector<int> rs(gp.nr);
-      q = ring_points(gp.beta, tol, gp.nr, gp.na, rs.data());
-      H->roff.push_back(0);
-      for (int kr = 0; kr < gp.nr; ++kr) H->roff.push_back(H->roff.back() + rs[kr]);
+      q = qk[k];
       c = (int64_t)(gp.na / 2 + 1) * 2 * gp.nr;
       H->grid_ids.push_back((int32_t)k);
       H->qmax = std::max<int>(H->qmax, (int)q);
@@ -1725,7 +1768,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   struct Slice { int64_t src0; int32_t nsrc; int rung; };
   // grids are independent: blocks of kBlk grids go to host threads, each appending to its own buffers (no per-grid
   // heap objects); the blocks are then copied into place in grid order with their offsets shifted (in parallel)
-  constexpr int64_t kBlk = 256;
+  constexpr int64_t kBlk = 8;   // small: the coarse-level grids (thousands of sources each) come first in grid order
   const int64_t NGL = (int64_t)H->grid_ids.size();
   const int64_t nblk = (NGL + kBlk - 1) / kBlk;
   struct BlockOut {
@@ -1740,9 +1783,19 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   std::vector<std::vector<int32_t>> T_src(nthr);
   std::vector<std::vector<double>> T_rp(nthr, std::vector<double>(h->nrung, 0.0));
   const int tpt_fill = H->gv.tpt, wpts_fill = 32 * tpt_fill;
+  std::vector<double> ut_acc((size_t)nthr * 3, 0.0);   // per-thread sub-phase seconds (NC_SETUP_TIMING)
 #pragma omp parallel
   {
     const int th = omp_get_thread_num();
+    double* ut = ut_acc.data() + (size_t)th * 3;
+    double umark = 0.0;
+    auto ulap = [&](int k) {
+      if (!sub_timing) return;
+      const double t = omp_get_wtime();
+      if (k >= 0) ut[k] += t - umark;
+      umark = t;
+    };
+    ulap(-1);
     std::vector<GridUnit>& TU = T_units[th];
     std::vector<ChunkRec>& TC = T_chunks[th];
     std::vector<int32_t>& TS = T_src[th];
@@ -1766,6 +1819,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         const int32_t* g_src = F_src.data() + gp.off;
         const int32_t* g_rung = F_rung.data() + gp.off;
         const double* g_dist = F_dist.data() + gp.off;
+        ulap(2);
         if (chunk_rungs) {
           ring_rung.assign(ns_all * gp.nr, 0);
           for (int kr = 0; kr < gp.nr; ++kr) {
@@ -1775,7 +1829,9 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
         }
         // the unit's sources bucketed by rung (sorted by patch within a bucket); slices never mix rungs; slice
         // offsets are block-relative (shifted when the block is copied into place)
+        ulap(0);
         auto make_slices = [&](int kr0) {
+          ulap(2);
           rs.clear();
           slices.clear();
           for (size_t n = 0; n < ns_all; ++n)
@@ -1795,6 +1851,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
             }
             a = b;
           }
+          ulap(1);
         };
         if (!chunk_rungs) make_slices(0);   // one list per grid, shared by its units
         int kr_cached = -1;                 // chunks with the same first ring share their lists
@@ -1838,7 +1895,14 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
       bo.nu = (int64_t)TU.size() - bo.u0;
       bo.nc = (int64_t)TC.size() - bo.c0;
       bo.ns = (int64_t)TS.size() - bo.s0;
+      ulap(2);
     }
+  }
+  if (sub_timing) {
+    double tot[3] = {0, 0, 0};
+    for (size_t t = 0; t < ut_acc.size(); ++t) tot[t % 3] += ut_acc[t];
+    fprintf(stderr, "[nc setup]   units thread-seconds: ring rungs %.3f slices %.3f units %.3f (threads %d)\n", tot[0],
+            tot[1], tot[2], nthr);
   }
   setup_tick("units: per-grid (host, parallel)");
   {   // place the blocks in grid order (offsets shifted), statistics summed in block order (exact: integer-valued)
@@ -1891,21 +1955,32 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   std::vector<int64_t> near_off(rc + 1, 0);
   std::vector<int32_t> near_all;
   std::vector<int32_t> work_near;
-  {
-    std::vector<std::vector<int32_t>> nl(rc);
-    for (int64_t g = 0; g < G; ++g) {
-      if (!rel[g] || near_beg[g] == near_end[g]) continue;
-      const int64_t a = std::max<int64_t>(H->gfirst[g], rb), b = std::min<int64_t>(H->glast[g], re);
-      for (int64_t i = a; i < b; ++i)
-        nl[i - rb].insert(nl[i - rb].end(), F_src.begin() + near_beg[g], F_src.begin() + near_end[g]);
+  {   // per local row: the near tails of its groups at every level (exactly-once coverage: no duplicates), sorted
+    std::vector<int64_t> cnt(rc, 0);
+#pragma omp parallel for schedule(static, 1024)
+    for (int64_t i = 0; i < rc; ++i) {
+      int64_t c = 0;
+      for (int lvl = 0; lvl <= L; ++lvl) {
+        const int64_t g = H->pgroup[(size_t)lvl * N + rb + i];
+        c += near_end[g] - near_beg[g];
+      }
+      cnt[i] = c;
+    }
+    for (int64_t i = 0; i < rc; ++i) near_off[i + 1] = near_off[i] + cnt[i];
+    near_all.resize((size_t)near_off[rc]);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t i = 0; i < rc; ++i) {
+      int64_t o = near_off[i];
+      for (int lvl = 0; lvl <= L; ++lvl) {
+        const int64_t g = H->pgroup[(size_t)lvl * N + rb + i];
+        for (int64_t e = near_beg[g]; e < near_end[g]; ++e) near_all[o++] = F_src[e];
+      }
+      std::sort(near_all.begin() + near_off[i], near_all.begin() + near_off[i + 1]);
     }
     for (int64_t i = 0; i < rc; ++i) {
-      std::sort(nl[i].begin(), nl[i].end());
-      near_off[i + 1] = near_off[i] + (int64_t)nl[i].size();
-      near_all.insert(near_all.end(), nl[i].begin(), nl[i].end());
-      if (!nl[i].empty()) work_near.push_back((int32_t)i);
-      H->near_count.push_back((int32_t)nl[i].size());
-      H->pairs_near += (double)nl[i].size() * Ks * p;
+      if (cnt[i]) work_near.push_back((int32_t)i);
+      H->near_count.push_back((int32_t)cnt[i]);
+      H->pairs_near += (double)cnt[i] * Ks * p;
     }
   }
   std::vector<double> lvl_terms(L + 1, 0.0), lvl_single(L + 1, 0.0);
@@ -1924,25 +1999,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     for (int lvl = 0; lvl <= L; ++lvl) fprintf(stderr, " %d:%.3g/%.3g", lvl, lvl_terms[lvl], lvl_single[lvl]);
     fprintf(stderr, "\n");
   }
-  // tree lists for introspection (audit): (level, target group, source group)
-  H->ilist_entries.clear();
-  H->nbr_entries.clear();
-  for (int64_t g = 0; g < G; ++g) {
-    for (int64_t k = H->il_off[g]; k < H->il_off[g + 1]; ++k) {
-      H->ilist_entries.push_back(H->glevel[g]);
-      H->ilist_entries.push_back(g);
-      H->ilist_entries.push_back(H->il[k]);
-    }
-    if (H->glevel[g] == L)
-      for (int k = 0; k < 8; ++k)
-        if (H->nbr[8 * g + k] >= 0) {
-          H->nbr_entries.push_back(L);
-          H->nbr_entries.push_back(g);
-          H->nbr_entries.push_back(H->nbr[8 * g + k]);
-        }
-  }
-
-  setup_tick("near lists, tree audit lists");
+  setup_tick("near lists");
   if (getenv("NC_SETUP_DIGEST")) {   // FNV-1a digests of the host plan (refactors of the setup must reproduce it)
     auto fnv = [](const void* p, size_t n) {
       uint64_t hsh = 1469598103934665603ull;
@@ -2152,6 +2209,25 @@ extern "C" int nc_tree_lists(const nc_handle* h, int64_t* n_ilist, int64_t* ilis
   if (!h) return nc::fail(NC_EINVAL, "nc_tree_lists: null handle");
   const nc::HierState* H = h->hier;
   if (!H) return nc::fail(NC_ESTATE, "nc_tree_lists: handle is not NC_HIER");
+  // the audit lists (level, target group, source group), built on first request (the setup does not need them)
+  nc::HierState* Hm = const_cast<nc::HierState*>(H);
+  if (Hm->ilist_entries.empty() && Hm->nbr_entries.empty()) {
+    const int64_t G = (int64_t)H->il_off.size() - 1;
+    for (int64_t g = 0; g < G; ++g) {
+      for (int64_t k = H->il_off[g]; k < H->il_off[g + 1]; ++k) {
+        Hm->ilist_entries.push_back(H->glevel[g]);
+        Hm->ilist_entries.push_back(g);
+        Hm->ilist_entries.push_back(H->il[k]);
+      }
+      if (H->glevel[g] == H->L)
+        for (int k = 0; k < 8; ++k)
+          if (H->nbr[8 * g + k] >= 0) {
+            Hm->nbr_entries.push_back(H->L);
+            Hm->nbr_entries.push_back(g);
+            Hm->nbr_entries.push_back(H->nbr[8 * g + k]);
+          }
+    }
+  }
   if (n_ilist) *n_ilist = (int64_t)H->ilist_entries.size() / 3;
   if (n_nbr) *n_nbr = (int64_t)H->nbr_entries.size() / 3;
   if (ilist) std::copy(H->ilist_entries.begin(), H->ilist_entries.end(), ilist);
