@@ -601,8 +601,37 @@ int nc_matvec_host(nc_handle* h, const double* x_host, double* y_host) {
     NC_TRY(dalloc(h, &h->d_hy, n));
   }
   cudaStream_t s = h->stream;
-  NC_CUDA_TRY(cudaMemcpyAsync(h->d_hx, x_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
-  NC_TRY(nc_matvec(h, h->d_hx, h->d_hy, s));
+  if (h->world > 1) {   // collective: the whole x first (the all-gather needs it)
+    NC_CUDA_TRY(cudaMemcpyAsync(h->d_hx, x_host, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    NC_TRY(nc_matvec(h, h->d_hx, h->d_hy, s));
+  } else {
+    // x in kHostBlocks row blocks on the copy stream; K1 of each block on the compute stream as soon as it has
+    // landed (the host-to-device copy overlaps the outgoing GEMM), then the rest of the matvec
+    constexpr int kHostBlocks = 4;
+    if (!h->copy_stream) {
+      NC_CUDA_TRY(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+      for (auto& ev : h->copy_ev) NC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    NC_TRY(serialize_stream(h, s));
+    NC_CUDA_TRY(cudaEventRecord(h->copy_ev[kHostBlocks], s));   // the previous use of d_hx is done
+    NC_CUDA_TRY(cudaStreamWaitEvent(h->copy_stream, h->copy_ev[kHostBlocks], 0));
+    const int64_t rc = h->row_count, K = h->K;
+    for (int b = 0; b < kHostBlocks; ++b) {
+      const int64_t r0 = rc * b / kHostBlocks, r1 = rc * (b + 1) / kHostBlocks;
+      NC_CUDA_TRY(cudaMemcpyAsync(h->d_hx + r0 * K, x_host + r0 * K, (size_t)(r1 - r0) * K * sizeof(double),
+                                  cudaMemcpyHostToDevice, h->copy_stream));
+      NC_CUDA_TRY(cudaEventRecord(h->copy_ev[b], h->copy_stream));
+    }
+    h->launches_last = 0;
+    mark(h, 0, s);
+    for (int b = 0; b < kHostBlocks; ++b) {
+      const int64_t r0 = rc * b / kHostBlocks, r1 = rc * (b + 1) / kHostBlocks;
+      NC_CUDA_TRY(cudaStreamWaitEvent(s, h->copy_ev[b], 0));
+      if (r1 > r0) outgoing(h, h->d_hx + r0 * K, h->row_begin + r0, r1 - r0, s);
+    }
+    mark(h, 1, s);
+    NC_TRY(matvec_tail(h, h->d_hx, h->d_hy, s));
+  }
   NC_CUDA_TRY(cudaMemcpyAsync(y_host, h->d_hy, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   NC_CUDA_TRY(cudaStreamSynchronize(s));
   return NC_OK;
@@ -1217,6 +1246,9 @@ void nc_destroy(nc_handle* h) {
   for (auto& ev : h->ev)
     if (ev) cudaEventDestroy(ev);
   if (h->ev_order) cudaEventDestroy(h->ev_order);
+  for (auto& ev : h->copy_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->stream) cudaStreamDestroy(h->stream);
 #if NC_WITH_NCCL
   if (h->comm) ncclCommDestroy(h->comm);

@@ -416,28 +416,28 @@ __global__ void k_grid_points(const int32_t* __restrict__ grids, int64_t ngr, co
   }
 }
 
-// One warp per chunk (8 chunks per 256-thread CTA), the lanes over the chunk's points; each lane issues the loads of
-// up to 8 units' partial values before summing them in unit order (the same fixed order as one load at a time, so the
-// result is unchanged bit for bit, with 8x the memory-level parallelism: the partials mostly come from DRAM)
+// One thread per grid point of a chunk (256-thread CTAs over 256 / upts chunks); each thread issues the loads of up
+// to 8 units' partial values before summing them in unit order (the same fixed order as one load at a time, so the
+// result is unchanged bit for bit, with up to 8 loads in flight: the partials mostly come from DRAM)
 __global__ void __launch_bounds__(256) k_reduce_chunks(const ChunkRec* __restrict__ ch, int64_t nch,
                                                        const double* __restrict__ part, int upts,
                                                        double* __restrict__ gval) {
-  const int64_t c = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int per = 256 / upts;                                   // chunks per CTA (upts divides 256)
+  const int64_t c = (int64_t)blockIdx.x * per + threadIdx.x / upts;
+  const int t = threadIdx.x % upts;
   if (c >= nch) return;
-  const int lane = threadIdx.x & 31;
   const ChunkRec R = ch[c];
-  for (int t = lane; t < R.npt; t += 32) {
-    double v = 0.0;
-    for (int s0 = 0; s0 < R.nu; s0 += 8) {
-      double a[8];
+  if (t >= R.npt) return;
+  double v = 0.0;
+  for (int s0 = 0; s0 < R.nu; s0 += 8) {
+    double a[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] = (s0 + e < R.nu) ? part[(R.u0 + s0 + e) * upts + t] : 0.0;
+    for (int e = 0; e < 8; ++e) a[e] = (s0 + e < R.nu) ? part[(R.u0 + s0 + e) * upts + t] : 0.0;
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (s0 + e < R.nu) v += a[e];
-    }
-    gval[R.pt0 + t] = v;
+    for (int e = 0; e < 8; ++e)
+      if (s0 + e < R.nu) v += a[e];
   }
+  gval[R.pt0 + t] = v;
 }
 
 // step 4a: samples f(r_k, theta_l) (ring k: n_a(k) equispaced angles, radius-major) ->
@@ -2120,8 +2120,9 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   h->launches_last += H->nunits > 0;
   if (h->time_stages) cudaEventRecord(h->ev[3], s);
   if (H->nchunks) {
-    k_reduce_chunks<<<(unsigned)((H->nchunks + 7) / 8), 256, 0, s>>>(H->d_chunks, H->nchunks, H->d_part, H->upts,
-                                                                      H->d_gval);
+    const int per = 256 / H->upts;   // upts = 64 (warp-level units) or 256 (CTA units)
+    k_reduce_chunks<<<(unsigned)((H->nchunks + per - 1) / per), 256, 0, s>>>(H->d_chunks, H->nchunks, H->d_part,
+                                                                            H->upts, H->d_gval);
     h->launches_last++;
   }
   if (h->time_stages) cudaEventRecord(h->ev[8], s);

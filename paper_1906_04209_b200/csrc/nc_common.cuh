@@ -151,6 +151,9 @@ struct nc_handle {
   cudaStream_t last_stream = nullptr;
   bool have_last_stream = false;
   cudaEvent_t ev_order = nullptr;
+  // nc_matvec_host (world 1): x copied in row blocks on a second stream, each block's K1 as soon as it has landed
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_ev[5] = {};
 
   // per-stage timing
   bool time_stages = false;

@@ -171,3 +171,16 @@ def test_ladder_gate_boundary(name):
     assert hn.stats()["hier_grid_pairs"] > hb.stats()["hier_grid_pairs"]
     for hh in (hb, hd, hn):
         hh.close()
+
+
+def test_C5_solution_residual_on_oracle_rows():
+    """the oracle's residual of the GPU-hierarchical C5 solution on sampled rows,
+    (I + A_off) x - P 1 by the brute-force direct sum, relative to b: the GMRES tolerance plus the hierarchical
+    matvec error (<= the requested precision 1e-9)."""
+    cfg, tab, c, x, h, y = _hier("C5")
+    xs, it, _ = h.gmres(rtol=cfg.gmres_tol, max_iter=200)
+    xg = h.to_caller(xs.cpu().numpy())
+    rows = np.array([3, 4242, 50505, 99999], dtype=np.int64)
+    b = np.tile(tab.P @ np.ones(tab.Kstar), (len(rows), 1))
+    r = O.matvec(cfg.kind, c, tab, xg, rows=rows) - b
+    assert np.linalg.norm(r) / np.linalg.norm(b) <= 2e-9
