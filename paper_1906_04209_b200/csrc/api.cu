@@ -134,7 +134,7 @@ void split_rows(const double* w, int64_t N, int world, int64_t* begin, int64_t* 
 }
 
 static void compute_nseg(nc_handle* h) {
-  const char* ev = getenv("NC_PAIR_TPT");
+  const char* ev = tuning_env("NC_PAIR_TPT");
   h->pair_tpt = (ev && atoi(ev) == 1) ? 1 : (ev && atoi(ev) == 2) ? 2 : kDefaultPairTpt;
   const int64_t per_block = (int64_t)kPairThreads * h->pair_tpt;
   int64_t tiles = (h->row_count * h->Kstar + per_block - 1) / per_block;
@@ -263,7 +263,7 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   const int K = h->K, Ks = h->Kstar, p = h->p;
   if (!log_table_device()) return bail(fail(NC_ECUDA, "nc_setup: log table upload failed"));
   {   // exact-form log table of the direct / near-list pair kernels (green_exact_r; NC_EXACT_TABLE=0: mantissa table)
-    const char* e = getenv("NC_EXACT_TABLE");
+    const char* e = tuning_env("NC_EXACT_TABLE");
     if (!(e && e[0] == '0')) {
       if (far_table_build(h->kind, h->eps, 7, 1, FarPoly<7, 4>::a2, FarPoly<7, 4>::a3, &h->d_xtab, &h->xtab.n,
                           &h->xtab.base, 1))

@@ -100,7 +100,7 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
   // NC_DIRECT_FAR=0 disables it
   static int far_on = -1;
   if (far_on < 0) {
-    const char* e = getenv("NC_DIRECT_FAR");
+    const char* e = tuning_env("NC_DIRECT_FAR");
     far_on = (e && e[0] == '0') ? 0 : 1;
   }
   const double dfar = 0.12 + 2.0 * eps;
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
 static bool stage_ldg() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("NC_PAIR_STAGE");
+    const char* e = tuning_env("NC_PAIR_STAGE");
     v = (e && e[0] == 's') ? 0 : (e && e[0] == 'l') ? 1 : kDefaultStageLdg;
   }
   return v == 1;
@@ -255,7 +255,7 @@ static bool grid_variant_instantiated(const GridVariant& v) {
 
 GridVariant grid_variant_for(double precision) {
   const GridVariant dflt = precision >= kGridQuadMinPrecision ? kGridVariantDefault : kGridVariantPrecise;
-  const char* e = getenv("NC_GRID_VARIANT");
+  const char* e = tuning_env("NC_GRID_VARIANT");
   if (!e) return dflt;
   GridVariant w = dflt;
   w.tma = 0;

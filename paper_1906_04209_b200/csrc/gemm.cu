@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) k_gemm_dmma_pipe(const double* __restrict
 static bool gemm_pipe_ok(const double* A, int64_t lda, const double* Bt, int kd) {
   // cp.async needs 16-byte aligned rows: even leading dimensions and 16-byte aligned bases
   return (lda % 2 == 0) && (kd % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)Bt % 16 == 0) &&
-         !getenv("NC_GEMM_SIMPLE");
+         !tuning_env("NC_GEMM_SIMPLE");
 }
 
 static void launch_pipe(const double* A, int64_t lda, const double* Bt, int64_t rows, int ncols, int kd, double* C,

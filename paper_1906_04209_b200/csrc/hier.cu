@@ -1005,7 +1005,7 @@ static InterpVariant interp_variant() {
   static InterpVariant v = {-1, 0, 0, 0};
   if (v.nt < 0) {
     v = {256, 2, 0, 2};   // angular sums first (grid_eval_ang), measured fastest at C5 (profiles/r01l_interp_*)
-    if (const char* e = getenv("NC_INTERP_VARIANT")) {
+    if (const char* e = tuning_env("NC_INTERP_VARIANT")) {
       InterpVariant w = v;
       w.minb = 1;
       if (sscanf(e, "%d,%d,%d,%d", &w.nt, &w.npt, &w.mb, &w.minb) >= 3) v = w;
@@ -1048,10 +1048,10 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
   // the 256-thread angular-sums-first kernel.  NC_INTERP_VARIANT must name a listed variant (else: the default,
   // with a warning -- never a silently skipped first pass)
   const InterpVariant dflt = Ks <= 256 ? InterpVariant{128, 2, 3, 4} : InterpVariant{256, 2, 0, 2};
-  InterpVariant v = getenv("NC_INTERP_VARIANT") ? interp_variant() : dflt;
+  InterpVariant v = tuning_env("NC_INTERP_VARIANT") ? interp_variant() : dflt;
   if (!interp_listed(v)) {
     fprintf(stderr, "[nc] NC_INTERP_VARIANT=%s is not an instantiated variant; using the default\n",
-            getenv("NC_INTERP_VARIANT"));
+            tuning_env("NC_INTERP_VARIANT"));
     v = dflt;
   }
   // the angular-sums-first kernels (MB 0, 3) evaluate grids with n_r <= kAngNrMax; a second pass (MB = 1, nr_big)
@@ -1105,7 +1105,7 @@ static int download(std::vector<T>& dst, const T* src, size_t n, cudaStream_t s)
 static int nr_margin() {   // rings added beyond the radial fit (NC_NR_MARGIN, default 1; R21)
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("NC_NR_MARGIN");
+    const char* e = tuning_env("NC_NR_MARGIN");
     v = e ? std::max(0, atoi(e)) : 1;
   }
   return v;
@@ -1114,7 +1114,7 @@ static int nr_margin() {   // rings added beyond the radial fit (NC_NR_MARGIN, d
 static int na_margin() {   // angles added beyond the azimuthal fit on the outer ring (NC_NA_MARGIN, default 4)
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("NC_NA_MARGIN");
+    const char* e = tuning_env("NC_NA_MARGIN");
     v = e ? std::max(0, atoi(e)) : 4;
   }
   return v;
@@ -1137,7 +1137,7 @@ static void grid_size(double beta, double tol, int& nr, int& na) {
 static bool ring_adapt() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("NC_RING_ADAPT");
+    const char* e = tuning_env("NC_RING_ADAPT");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
@@ -1145,7 +1145,7 @@ static bool ring_adapt() {
 static int ring_margin() {   // points added to every adapted ring beyond the fit (NC_RING_MARGIN, default 8)
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("NC_RING_MARGIN");
+    const char* e = tuning_env("NC_RING_MARGIN");
     v = e ? std::max(0, atoi(e)) : 8;
   }
   return v;
@@ -1196,7 +1196,7 @@ static int warp_slots(int q) {
 static bool ring_fill() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("NC_RING_FILL");
+    const char* e = tuning_env("NC_RING_FILL");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
@@ -1205,7 +1205,7 @@ static bool ring_fill() {
 static int ring_floor() {   // the smallest margin ring filling may trim to (NC_RING_FLOOR, default 6)
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("NC_RING_FLOOR");
+    const char* e = tuning_env("NC_RING_FLOOR");
     v = e ? std::max(0, atoi(e)) : 6;
   }
   return v;
@@ -1321,7 +1321,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   const int Ks = h->Kstar, p = h->p;
   // ---- node rings of the canonical Zernike nodes (separable step 4 for single-member groups) ----
   {
-    const char* e = getenv("NC_INTERP_SEP");
+    const char* e = tuning_env("NC_INTERP_SEP");
     std::vector<double> z;
     NC_TRY(download(z, h->d_zhat, (size_t)3 * Ks, s));
     H->node_ring.assign(Ks, -1);
@@ -1448,26 +1448,26 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   // per-grid interpolation tolerance = kGridTolFactor x requested precision (calibrated, R21;
   // NC_GRID_TOL_FACTOR overrides for calibration runs)
   double tol_factor = kGridTolFactor;
-  if (const char* e = getenv("NC_GRID_TOL_FACTOR")) tol_factor = atof(e);
+  if (const char* e = tuning_env("NC_GRID_TOL_FACTOR")) tol_factor = atof(e);
   const double tol = tol_factor * h->precision;
   {
-    const char* et = getenv("NC_INTERP_TRUNC");
+    const char* et = tuning_env("NC_INTERP_TRUNC");
     H->interp_lt = (et && et[0] == '0') ? 0.0 : log(1.0 / tol);
   }
   // relative costs in grid-pair units (measured at C5): a near-list pair (exact form), one
   // interpolation term (node x coefficient), one transform term; NC_COST_NEAR / _INTERP / _TRANSFORM override
   double c_near = kCostNear, c_interp = kCostInterp, c_trans = kCostTransform;
-  if (const char* e = getenv("NC_COST_NEAR")) c_near = atof(e);
-  if (const char* e = getenv("NC_COST_INTERP")) c_interp = atof(e);
-  if (const char* e = getenv("NC_COST_TRANSFORM")) c_trans = atof(e);
+  if (const char* e = tuning_env("NC_COST_NEAR")) c_near = atof(e);
+  if (const char* e = tuning_env("NC_COST_INTERP")) c_interp = atof(e);
+  if (const char* e = tuning_env("NC_COST_TRANSFORM")) c_trans = atof(e);
   // Incoming grids per group (§8.1 :1424-1434): the group's interaction-list / leaf-neighbour
   // sources, sorted by beta = (distance - eps) / R descending, are cut into up to kMaxGrids consecutive bands, each
   // on its own grid sized by the band's nearest source, and a near tail evaluated directly at the members' Zernike
   // nodes (R12, R24).  The cut minimises the cost model (grid-pair units).
   int max_grids = kDefaultGrids;
-  if (const char* e = getenv("NC_MAX_GRIDS")) max_grids = std::max(1, std::min(kMaxGrids, atoi(e)));
+  if (const char* e = tuning_env("NC_MAX_GRIDS")) max_grids = std::max(1, std::min(kMaxGrids, atoi(e)));
   int ncuts = kGridCutQuantiles;
-  if (const char* e = getenv("NC_GRID_CUTS")) ncuts = std::max(4, std::min(512, atoi(e)));
+  if (const char* e = tuning_env("NC_GRID_CUTS")) ncuts = std::max(4, std::min(512, atoi(e)));
   // every group's candidate sources, sorted, in flat arrays: group g's live at [cand_off[g], cand_off[g + 1]); its
   // grids take consecutive bands of them, its near tail the rest (sorted by patch).  No per-group heap objects: the
   // routing runs over ~2e5 groups at C5 and per-group vectors made it allocator-bound.
@@ -1756,7 +1756,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   // r_kr = R cos((kr + 1/2) pi / (2 n_r)) from its first ring kr0 inward, so the gap from a source to the unit's
   // points is >= d - r_kr0 >= d - R, and the unit may use the smallest skeleton valid at that gap (PAPER.md:1436-1457:
   // the per-level recompression, here keyed by the distance to the unit's points instead of the whole grid's)
-  const char* ecr = getenv("NC_CHUNK_RUNGS");
+  const char* ecr = tuning_env("NC_CHUNK_RUNGS");
   const bool chunk_rungs = !(ecr && ecr[0] == '0');
   bool ladder_monotone = true;   // r_k ascending and p_k non-increasing over k >= 1: binary search
   for (int kk = 2; kk < h->nrung; ++kk)

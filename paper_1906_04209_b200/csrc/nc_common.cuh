@@ -39,6 +39,17 @@ constexpr int kPairThreads = 256;   // threads per CTA in the direct pair-sum ke
 constexpr int kDefaultPairTpt = 2;  // targets per thread (NC_PAIR_TPT=1|2 overrides)
 constexpr int kDefaultStageLdg = 0; // 1: pair kernels read sources via L1 broadcasts (NC_PAIR_STAGE=ldg|smem)
 
+// The tuning knobs (NC_GRID_VARIANT, NC_INTERP_*, NC_COST_*, NC_RING_*, NC_*_MARGIN, NC_GRID_TOL_FACTOR, ...) change
+// the kernels or the plan and hence the numerics; they are read only when NC_TUNING=1 is also set (sweeps and the
+// variant tests set it), so a default run cannot be altered by a stray environment variable.
+inline const char* tuning_env(const char* name) {
+  static const bool on = [] {
+    const char* e = getenv("NC_TUNING");
+    return e && e[0] == '1';
+  }();
+  return on ? getenv(name) : nullptr;
+}
+
 // setup phase timer (NC_SETUP_TIMING=1 prints wall-clock ms per phase to stderr)
 void setup_tick(const char* phase);
 

@@ -176,7 +176,7 @@ def test_far_field_pair_variant_error(tmp_path, cfg, far):
     outs = []
     for v in ("32,2,4,256,0", far):   # the exact form on the same 64-point units (one-warp CTAs)
         out = str(tmp_path / f"y{len(outs)}.npy")
-        env = dict(os.environ, NC_GRID_VARIANT=v, ROOT=ROOT, OUT=out, CFG=cfg)
+        env = dict(os.environ, NC_TUNING="1", NC_GRID_VARIANT=v, ROOT=ROOT, OUT=out, CFG=cfg)
         subprocess.run([sys.executable, "-c", _FAR_CHILD], env=env, check=True, timeout=900)
         outs.append(np.load(out))
     assert rel(outs[1], outs[0]) <= 1e-11
@@ -194,7 +194,7 @@ def test_step4_evaluation_variants_agree(tmp_path, env):
     outs = []
     for e in ({}, env):   # the per-node order truncation (R26c) off in both: the same expansion, evaluated two ways
         out = str(tmp_path / f"y{len(outs)}.npy")
-        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(os.environ, ROOT=ROOT, OUT=out, NC_INTERP_TRUNC="0",
+        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(os.environ, NC_TUNING="1", ROOT=ROOT, OUT=out, NC_INTERP_TRUNC="0",
                                                                     **e), check=True, timeout=600)
         outs.append(np.load(out))
     assert rel(outs[1], outs[0]) <= 1e-13
@@ -208,7 +208,7 @@ def test_step4_order_truncation_below_tolerance(tmp_path):
     outs = []
     for v in ("0", "1"):
         out = str(tmp_path / f"y{v}.npy")
-        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(os.environ, ROOT=ROOT, OUT=out, NC_INTERP_TRUNC=v),
+        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(os.environ, NC_TUNING="1", ROOT=ROOT, OUT=out, NC_INTERP_TRUNC=v),
                        check=True, timeout=600)
         outs.append(np.load(out))
     assert rel(outs[1], outs[0]) <= 1e-10
@@ -255,3 +255,18 @@ def test_matvec_bitwise_reproducible(name):
     ys = [h.matvec(x).cpu().numpy() for _ in range(3)]
     assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
     h.close()
+
+
+def test_tuning_knobs_ignored_without_nc_tuning(tmp_path):
+    """The numerics-changing knobs (here the grid kernel variant and the interpolation truncation) are read only with
+    NC_TUNING=1: without it a stray environment variable leaves the default matvec bit for bit."""
+    import subprocess
+    import sys
+    outs = []
+    for extra in ({}, {"NC_GRID_VARIANT": "32,2,4,256,0", "NC_INTERP_TRUNC": "0"}):
+        out = str(tmp_path / f"y{len(outs)}.npy")
+        env = {k: v for k, v in os.environ.items() if k != "NC_TUNING"}
+        subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(env, ROOT=ROOT, OUT=out, **extra), check=True,
+                       timeout=600)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])

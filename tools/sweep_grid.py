@@ -47,7 +47,7 @@ def main():
     ref = None
     for k, v in enumerate(sys.argv[2:]):
         out = f"/tmp/sweep_{k}.npy"
-        env = dict(os.environ, ROOT=ROOT, CFG=cfg, OUT=out, VARIANT=v)
+        env = dict(os.environ, NC_TUNING="1", ROOT=ROOT, CFG=cfg, OUT=out, VARIANT=v)
         for spec in v.split(";"):                 # "NAME=value;..." sets env vars, a bare value NC_GRID_VARIANT
             if "=" in spec:
                 k_, v_ = spec.split("=", 1)

@@ -48,6 +48,7 @@ def main():
         href = nc.Handle(cfg.kind, c, cfg.eps, tab, mode=nc.NC_DIRECT)
         ref_kind = "direct"
     else:
+        os.environ["NC_TUNING"] = "1"
         os.environ["NC_GRID_TOL_FACTOR"] = "0.3"
         href = nc.Handle(cfg.kind, c, cfg.eps, tab, mode=nc.NC_HIER, precision=cfg.precision)
         ref_kind = "hier tol factor 0.3"
