@@ -82,6 +82,7 @@ struct HierState {
   double* d_gframe = nullptr;
   double* d_gR = nullptr;
   double* d_gRinv = nullptr;        // 1 / R per group (step 4: x = arc / R)
+  double2* d_twtab = nullptr;       // step 4a twiddles: (cos, sin)(2 pi l / n) at n (n - 1) / 2 + l, n <= namax
   int asin_terms = 0;               // step 4 node geometry: terms of the asin series (0: atan2 per node)
   int32_t *d_gnr = nullptr, *d_gna = nullptr;
   int64_t *d_goff = nullptr, *d_coff = nullptr;
@@ -450,7 +451,7 @@ __global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, cons
                             const int32_t* __restrict__ gna, const int64_t* __restrict__ goff,
                             const int64_t* __restrict__ coff, const int64_t* __restrict__ rbase,
                             const int32_t* __restrict__ roff, const double* __restrict__ gval,
-                            double* __restrict__ coef) {
+                            double* __restrict__ coef, const double2* __restrict__ twtab) {
   extern __shared__ double sh[];
   const int g = grids[blockIdx.x];   // grid id
   const int nr = gnr[g], M = gna[g] / 2;
@@ -464,7 +465,9 @@ __global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, cons
     f[t] = gval[goff[g] + t];
     int kr = 0;
     while (t >= ro[kr + 1]) ++kr;
-    sincospi(2.0 * (t - ro[kr]) / (ro[kr + 1] - ro[kr]), &tw[2 * t + 1], &tw[2 * t]);
+    // (cos, sin)(2 pi l / n) of ring kr (n = n_a(kr) angles) from the handle's table: entry n (n - 1) / 2 + l
+    const int n = ro[kr + 1] - ro[kr], l = t - ro[kr];
+    reinterpret_cast<double2*>(tw)[t] = twtab[(int64_t)n * (n - 1) / 2 + l];
   }
   for (int t = threadIdx.x; t < 8 * nr; t += blockDim.x) ch[t] = cospi((double)t / (4.0 * nr));
   __syncthreads();
@@ -2041,6 +2044,16 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_TRY(upload(h, &H->d_rbase, H->rbase, s));
   NC_TRY(upload(h, &H->d_roff, H->roff, s));
   NC_TRY(upload(h, &H->d_grid_ids, H->grid_ids, s));
+  {   // the ring twiddles of every angle count up to namax, in long double (k_transform reads them, no sincospi)
+    const int nmax = std::max(H->namax, 1);
+    std::vector<double2> tw((size_t)nmax * (nmax + 1) / 2);
+    for (int n = 1; n <= nmax; ++n)
+      for (int l = 0; l < n; ++l) {
+        const long double a = 2.0L * 3.14159265358979323846264338327950288L * l / n;
+        tw[(size_t)n * (n - 1) / 2 + l] = make_double2((double)cosl(a), (double)sinl(a));
+      }
+    NC_TRY(upload(h, &H->d_twtab, tw, s));
+  }
   NC_TRY(halloc(h, &H->d_counter, 1));
   if (const int fb = grid_far_table_bits(H->gv)) {   // far log table of the grid kernel (green.cuh)
     double a2 = 0.0, a3 = 0.0;
@@ -2132,7 +2145,8 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
     if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(k_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     k_transform<<<(unsigned)H->grid_ids.size(), 128, shm, s>>>(H->d_grid_ids, (int64_t)H->grid_ids.size(),
                                                                    H->d_gnr, H->d_gna, H->d_goff, H->d_coff,
-                                                                   H->d_rbase, H->d_roff, H->d_gval, H->d_gcoef);
+                                                                   H->d_rbase, H->d_roff, H->d_gval, H->d_gcoef,
+                                                                   H->d_twtab);
     h->launches_last++;
   }
   // near lists at the Zernike nodes
@@ -2195,7 +2209,7 @@ void hier_grid_variant(const nc_handle* h, int* v8) {
 void hier_destroy(nc_handle* h) {
   HierState* H = h->hier;
   if (!H) return;
-  void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gRinv, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_ids,
+  void* bufs[] = {H->d_keys, H->d_gframe, H->d_gR, H->d_gRinv, H->d_twtab, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_grid_ids,
                   H->d_grid_group, H->d_ggrid0, H->d_counter, H->d_ftab, H->d_rbase, H->d_roff, H->d_gsep, H->d_work_sep, H->d_ring_t,
                   H->d_node_ring, H->d_node_cs,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
