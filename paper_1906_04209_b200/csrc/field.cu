@@ -18,6 +18,7 @@
 
 #include <algorithm>
 
+#include "green.cuh"
 #include "nc_common.cuh"
 
 namespace nc {
@@ -38,15 +39,39 @@ __device__ __forceinline__ double green_off(double px, double py, double pz, dou
   return 2.0 * rd + log((a - c) / ((1.0 - c) + d));
 }
 
+// The same G from the squared distance alone (the sum kernel's form, round 2): with a = |x|, |x'| = 1 and
+// d^2 = |x - x'|^2 (coordinate differences, no cancellation), 1 - x.x' = (d^2 + 1 - a^2) / 2, so
+//   G_I = 2/d + log 2 - log(d^2 / 2 + d + B),                B = (1 - a^2) / 2 per point
+//   G_E = 2/d + log(d - d^2 / 2 - B) - log(a + (a^2 + 1 - d^2) / 2)      (the c >= 0 rewrite of R27; B = (1 - a^2)/2)
+// with 1/d by the MUFU seed and a third-order Newton step (fast_rsqrt, full precision) and log by the exponent-reduced
+// 1024-entry mantissa table (fast_log, ~1e-16 relative): ~25 FP64 instructions per pair instead of libdevice's ~50.
+// The exterior form is used for c = (a^2 + 1 - d^2) / 2 >= 0, the literal ratio otherwise (as green_off).
+template <int KIND>
+__device__ __forceinline__ double green_off_fast(double px, double py, double pz, double a, double B, double sx,
+                                                 double sy, double sz, const double2* __restrict__ tbl) {
+  const double dx = px - sx, dy = py - sy, dz = pz - sz;
+  const double d2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  const double rd = fast_rsqrt(d2);
+  const double d = d2 * rd;
+  if (KIND == 0) return fma(2.0, rd, 0.69314718055994530942) - fast_log(fma(0.5, d2, B) + d, tbl);
+  const double c = fma(-0.5, d2, 0.5 * (a * a + 1.0));
+  if (c >= 0.0) return 2.0 * rd + (fast_log(d - fma(0.5, d2, B), tbl) - fast_log(a + c, tbl));
+  return 2.0 * rd + (fast_log(a - c, tbl) - fast_log((1.0 - c) + d, tbl));
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kFieldThreads) k_field(const double* __restrict__ pts, int64_t n,
                                                          const double4* __restrict__ s4, int64_t nrec, int nseg,
-                                                         double* __restrict__ part, double* __restrict__ dpart) {
+                                                         double* __restrict__ part, double* __restrict__ dpart,
+                                                         const double2* __restrict__ logsrc) {
   __shared__ double4 sm[kFieldStage];
+  __shared__ double2 logtab[kLogTableSize];
+  init_log_table(logtab, logsrc);
   const int64_t t = (int64_t)blockIdx.x * kFieldThreads + threadIdx.x;
   const int64_t tc = t < n ? t : n - 1;
   const double px = pts[3 * tc], py = pts[3 * tc + 1], pz = pts[3 * tc + 2];
   const double a = sqrt(fma(pz, pz, fma(py, py, px * px)));
+  const double B = 0.5 * (1.0 - a * a);
   const int seg = blockIdx.y;
   const int64_t r0 = nrec * seg / nseg, r1 = nrec * (seg + 1) / nseg;
   double acc = 0.0, dm = INFINITY;
@@ -61,7 +86,7 @@ __global__ void __launch_bounds__(kFieldThreads) k_field(const double* __restric
       const double sx = 2.0 * s.x, sy = 2.0 * s.y, sz = 2.0 * s.z;
       const double dx = px - sx, dy = py - sy, dz = pz - sz;
       dm = fmin(dm, fma(dz, dz, fma(dy, dy, dx * dx)));
-      acc = fma(s.w, green_off<KIND>(px, py, pz, a, sx, sy, sz), acc);
+      acc = fma(s.w, green_off_fast<KIND>(px, py, pz, a, B, sx, sy, sz, logtab), acc);
     }
   }
   if (t < n) {
@@ -100,9 +125,9 @@ void launch_field(int kind, const double* pts, int64_t n, const double* src4, in
   dim3 grid((unsigned)((n + kFieldThreads - 1) / kFieldThreads), (unsigned)nseg);
   const double4* s4 = reinterpret_cast<const double4*>(src4);
   if (kind == NC_EXTERIOR)
-    k_field<1><<<grid, kFieldThreads, 0, s>>>(pts, n, s4, nrec, nseg, part, dpart);
+    k_field<1><<<grid, kFieldThreads, 0, s>>>(pts, n, s4, nrec, nseg, part, dpart, log_table_device());
   else
-    k_field<0><<<grid, kFieldThreads, 0, s>>>(pts, n, s4, nrec, nseg, part, dpart);
+    k_field<0><<<grid, kFieldThreads, 0, s>>>(pts, n, s4, nrec, nseg, part, dpart, log_table_device());
   k_field_reduce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, dpart, n, nseg, out, dmin);
 }
 
