@@ -1195,7 +1195,7 @@ int nc_stats(const nc_handle* h, nc_stats_t* o) {
   // far table (R25, green_far_t) cubic: 10 DFMA + 1 DMUL + 2 DADD exterior (23 flops), 11 + 1 + 1 interior (24);
   // quartic: one DFMA more
   const int far = hier_grid_far(h);
-  if (far == 8) {   // FB = 9 quadratic (R32): 9 DFMA + 1 DMUL + 2 DADD exterior (21 flops), 10 + 1 + 1 interior (22)
+  if (far == 8 || far == 9) {   // FB = 9 quadratic (R32, R35): 9 DFMA + 1 DMUL + 2 DADD exterior (21 flops), 10 + 1 + 1 interior (22)
     o->pair_fp64_inst_grid = 12;
     o->pair_fp64_flops_grid = 21 + interior;
   } else if (far >= 2) {

@@ -238,7 +238,7 @@ static bool stage_ldg() {
 // and one CTA-level instantiation with the EXACT difference-form pair kernel (far 0) on one-warp CTAs, i.e. on the
 // same 64-point work units (hence the same per-unit rungs) as the warp kernels: the reference the far forms are
 // tested against (tests/test_hier_gpu.py test_far_field_pair_variant_error).
-#define NC_GRID_W_LIST(X) X(2, 4, 8, 8, 2) X(2, 4, 7, 8, 3) X(2, 4, 5, 8, 3)
+#define NC_GRID_W_LIST(X) X(2, 4, 9, 8, 2) X(4, 2, 9, 8, 2) X(2, 4, 10, 8, 3) X(2, 4, 8, 8, 2) X(2, 4, 7, 8, 3) X(2, 4, 5, 8, 3)
 #define NC_GRID_C_LIST(X) X(32, 2, 4, 0, 0, 8)
 
 static bool grid_variant_instantiated(const GridVariant& v) {
@@ -272,8 +272,9 @@ int grid_far_table_bits(const GridVariant& v) { return v.far >= 2 ? far_table_bi
 int grid_far_table_rcp(const GridVariant& v) { return far_table_rcp(v.far); }
 void grid_far_poly(const GridVariant& v, double* a2, double* a3) { far_poly(v.far, a2, a3); }
 
-// points per work unit: a CTA's (NT x TPT), or a warp's (32 x TPT) for the warp-level kernel (tma = 3)
-int grid_unit_points(const GridVariant& v) { return (v.tma == 3 ? 32 : v.nt) * v.tpt; }
+// points per work unit: a CTA's (NT x TPT), or a warp's for the warp-level kernel (tma = 3): 32 x TPT, or 16 x 4 for
+// TPT = 4 (two half-warps on alternate records, R35)
+int grid_unit_points(const GridVariant& v) { return v.tma == 3 ? (v.tpt == 4 ? 16 : 32) * v.tpt : v.nt * v.tpt; }
 
 // ------------------------------------------------------------------------------------------------
 // Warp-level work units (variant tma = 3): every warp takes (<= 32 TPT points of one incoming grid) x (one slice of
@@ -305,7 +306,11 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
   const double* ftd = reinterpret_cast<const double*>(ftab) - fbase;   // ftd[ix]: the entry of index ix (R32)
   for (int j = threadIdx.x; j < nvec; j += 32 * WPC) ftab[j] = fsrc[j];
   __syncthreads();
-  constexpr int upts = 32 * TPT;
+  // SPLIT (TPT = 4, R35): the warp's two half-warps hold the same 64 points (4 per lane) and take alternate records
+  // of every chunk; their sums are added at the end (one record load per 4 pairs instead of per 2)
+  constexpr bool SPLIT = TPT == 4;
+  constexpr int upts = (SPLIT ? 16 : 32) * TPT;
+  const int tl = SPLIT ? (lane & 15) : lane;
   for (;;) {
     int u = 0;
     if (lane == 0) u = atomicAdd(counter, 1);
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
     double x[TPT], y[TPT], z[TPT], cq[TPT], acc[TPT];
 #pragma unroll
     for (int t = 0; t < TPT; ++t) {
-      const int l = single ? lane : TPT * lane + t;
+      const int l = single ? lane : TPT * tl + t;
       const int64_t g = U.pt0 + min(l, U.npt - 1);
       x[t] = gx[g]; y[t] = gy[g]; z[t] = gz[g];
       cq[t] = 0.5 * fma(x[t], x[t], fma(y[t], y[t], fma(z[t], z[t], 0.25)));
@@ -334,6 +339,9 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
         const int rr = r0 + (t >> 1), q = rr / p, m = rr - q * p;
         cp_async16(dst + t, reinterpret_cast<const double2*>(s4 + (size_t)slst[q] * p + m) + (t & 1));
       }
+      // SPLIT: an odd chunk gets a zero-weight record at the origin (its G is finite: |z| = 1, inside the table),
+      // so both half-warps run the same trip count; n < wrec here (wrec is even)
+      if (SPLIT && (n & 1) && lane == 0) reinterpret_cast<double4*>(dst)[n] = make_double4(0.0, 0.0, 0.0, 0.0);
       cp_async_commit();
     };
     issue(0);
@@ -345,18 +353,26 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
         cp_async_wait<0>();
       }
       __syncwarp();
-      accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, buf + (size_t)(c & 1) * wrec,
-                                              min(wrec, ntot - c * wrec), single, (const double2*)nullptr, tb, flim,
-                                              fa2, fa3, fmid, ftd);
+      const int n = min(wrec, ntot - c * wrec);
+      if (SPLIT && !single)
+        accumulate_span_split<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, buf + (size_t)(c & 1) * wrec + (lane >> 4),
+                                                      (n + 1) >> 1, tb, fa2, fa3, fmid, ftd);
+      else
+        accumulate_span<KIND, TPT, UNROLL, FAR>(x, y, z, cq, acc, buf + (size_t)(c & 1) * wrec, n, single,
+                                                (const double2*)nullptr, tb, flim, fa2, fa3, fmid, ftd);
       __syncwarp();
+    }
+    if (SPLIT && !single) {
+#pragma unroll
+      for (int t = 0; t < TPT; ++t) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], 16);
     }
     if (single) {
       if (lane < U.npt) part[(int64_t)u * upts + lane] = acc[0];
     } else {
 #pragma unroll
       for (int t = 0; t < TPT; ++t) {
-        const int l = TPT * lane + t;
-        if (l < U.npt) part[(int64_t)u * upts + l] = acc[t];
+        const int l = TPT * tl + t;
+        if (l < U.npt && (!SPLIT || lane < 16)) part[(int64_t)u * upts + l] = acc[t];
       }
     }
   }
@@ -616,7 +632,8 @@ extern "C" int nc_pair_mix(int kind, int far, int ctas_per_sm, double* ms, doubl
   int rc = 1;
 #define NC_MIX(K, F) \
   if (kind == K && far == F) rc = nc::run_pair_mix<K, F>(ctas_per_sm, ms, warp_pairs);
-  NC_MIX(0, 5) NC_MIX(1, 5) NC_MIX(0, 7) NC_MIX(1, 7) NC_MIX(0, 8) NC_MIX(1, 8)
+  NC_MIX(0, 5) NC_MIX(1, 5) NC_MIX(0, 7) NC_MIX(1, 7) NC_MIX(0, 8) NC_MIX(1, 8) NC_MIX(0, 9) NC_MIX(1, 9)
+  NC_MIX(0, 10) NC_MIX(1, 10)
 #undef NC_MIX
   if (rc) return nc::fail(NC_EINVAL, "nc_pair_mix: unsupported (kind, far) or launch failure");
   return NC_OK;

@@ -176,6 +176,58 @@ __device__ __forceinline__ double green_far_n(double qh, const double* __restric
   return fma(-r, p, w - lj);
 }
 
+// SFU seeds whose low word is NOT zeroed (far forms 9 / 10, R35).  MUFU.RSQ64H / MUFU.RCP64H read and
+// write only the high word of a double; rsqrt.approx / rcp.approx then zero the low word, one IMAD.MOV per seed
+// (two of the 22.6 instructions of a grid pair).  Here the seed's low word is the input's high word h itself, which
+// already sits in the even register of the pair: the double is (hi = MUFU(h), lo = h), a relative perturbation of
+// the seed below 2^-20 * h / 2^32 <= 2^-22 (h < 2^30 for any x < 2^1024 with the sign clear, which every x here is).
+// The rsqrt seed goes through one Newton step (error 1.5 delta^2: 2^-22.9 seed error + 2^-22 -> 3e-13 relative);
+// the rcp seed c is tabulated exactly as computed (far_table_build evaluates the same two instructions), so
+// L = -log c stays exact and only |r| grows by <= 2^-22 over the bin half-width.
+__device__ __forceinline__ double rsqrt_seed_hl(int h) {
+  double y;
+  asm("{\n\t.reg .f64 s, t;\n\t.reg .b32 tl, th;\n\tmov.b64 s, {%1, %1};\n\trsqrt.approx.ftz.f64 t, s;\n\t"
+      "mov.b64 {tl, th}, t;\n\tmov.b64 %0, {%1, th};\n\t}"
+      : "=d"(y)
+      : "r"(h));
+  return y;
+}
+__device__ __forceinline__ double rcp_seed_hl(int h) {
+  double y;
+  asm("{\n\t.reg .f64 s, t;\n\t.reg .b32 tl, th;\n\tmov.b64 s, {%1, %1};\n\trcp.approx.ftz.f64 t, s;\n\t"
+      "mov.b64 {tl, th}, t;\n\tmov.b64 %0, {%1, th};\n\t}"
+      : "=d"(y)
+      : "r"(h));
+  return y;
+}
+
+// Far form with high-word seeds (k_pairs_grid_w FAR 9 / 10, R35): green_far_n's arithmetic (FB = 9
+// quadratic or FB = 7 cubic) with (1) the two seeds of rsqrt_seed_hl / rcp_seed_hl and (2) the table entry's address
+// taken from the midpoint word in one shift-add: hmid >> (17 - FB) = (hx >> (20 - FB)) * 8 + 4 (kmid = 1 << (19 - FB)
+// contributes the 4), so tadr = (table byte address of index 0) - 4.  12 (quadratic) / 13 (cubic) FP64, 2 MUFU,
+// 4 integer (exponent bump, midpoint LOP3, address LEA.HI, table LDS) per pair.
+template <int KIND, int FB, int DEG>
+__device__ __forceinline__ double green_far_hl(double qh, unsigned tadr, double a2r, double a3r, int kmid) {
+  const double y = rsqrt_seed_hl(__double2hiint(qh) + 0x00100000);
+  const double t = qh * y;
+  const double e = fma(-t, y, 0.5);
+  const double w = fma(y, e, y);
+  const double x = (KIND == 1) ? 1.0 + w : fma(qh, w, qh);
+  const int hmid = (__double2hiint(x) & ~((1 << (20 - FB)) - 1)) | kmid;
+  const double c = rcp_seed_hl(hmid);
+  double lj;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(lj) : "r"(tadr + ((unsigned)hmid >> (17 - FB))));
+  const double r = fma(x, c, -1.0);
+  double p;
+  if constexpr (DEG == 2) {
+    p = fma(r, a2r, a3r);   // a2r = c2, a3r = c1 (FarQuad)
+  } else {
+    p = fma(r, FarPoly<FB, 3>::a3, a2r);
+    p = fma(r, p, 1.0);
+  }
+  return fma(-r, p, w - lj);
+}
+
 // Exact-form G with the reciprocal-seeded table (direct sums, near lists; R25): q = |z - s|^2 / 4 from
 // coordinate differences (caller), w = 2/d by fast_rsqrt (third-order Newton), x = 1 + w (exterior) or q (1 + w)
 // (interior, no ln 2: the table's L = -log c for this form), log x = L + log1p(r) with c = rcp.approx(bin midpoint),

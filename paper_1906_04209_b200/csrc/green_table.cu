@@ -32,12 +32,14 @@ const double2* log_table_device() {
 }
 
 // c of the reciprocal-seeded far form (green.cuh green_far_r), evaluated by the same instruction the pair kernel uses
-__global__ void k_far_rcp(int Elo, int bits, int cnt, double* c) {
+// (hl = 1: c = rcp_seed_hl of the midpoint word, whose low word is that word -- green_far_hl, R35)
+__global__ void k_far_rcp(int Elo, int bits, int cnt, int hl, double* c) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= cnt) return;
   const int per = 1 << bits;
   const int hx = ((Elo + t / per) << 20) | ((t % per) << (20 - bits));
-  c[t] = rcp_approx(__hiloint2double((hx & ~((1 << (20 - bits)) - 1)) | (1 << (19 - bits)), 0));
+  const int hmid = (hx & ~((1 << (20 - bits)) - 1)) | (1 << (19 - bits));
+  c[t] = hl ? rcp_seed_hl(hmid) : rcp_approx(__hiloint2double(hmid, 0));
 }
 
 // far table (green.cuh green_far_t / green_far_r): entries for every biased exponent E that x takes on grid pairs.
@@ -61,7 +63,7 @@ int far_table_build(int kind, double eps, int bits, int rcp, double a2, double a
   if (rcp) {   // c = rcp.approx(midpoint) as the device computes it
     double* dc = nullptr;
     if (cudaMalloc(&dc, c.size() * sizeof(double)) != cudaSuccess) return 1;
-    k_far_rcp<<<(cnt + 255) / 256, 256>>>(Elo, bits, cnt, dc);
+    k_far_rcp<<<(cnt + 255) / 256, 256>>>(Elo, bits, cnt, rcp == 2, dc);
     const bool ok = cudaMemcpy(c.data(), dc, c.size() * sizeof(double), cudaMemcpyDeviceToHost) == cudaSuccess;
     cudaFree(dc);
     if (!ok) return 1;

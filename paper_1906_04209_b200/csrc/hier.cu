@@ -1797,7 +1797,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   std::vector<std::vector<ChunkRec>> T_chunks(nthr);
   std::vector<std::vector<int32_t>> T_src(nthr);
   std::vector<std::vector<double>> T_rp(nthr, std::vector<double>(h->nrung, 0.0));
-  const int tpt_fill = H->gv.tpt, wpts_fill = 32 * tpt_fill;
+  const int tpt_fill = H->gv.tpt, wpts_fill = H->gv.tma == 3 ? H->upts : 32 * tpt_fill;   // points per warp
   std::vector<double> ut_acc((size_t)nthr * 3, 0.0);   // per-thread sub-phase seconds (NC_SETUP_TIMING)
 #pragma omp parallel
   {

@@ -64,13 +64,14 @@ struct GridVariant {
   int nt, tpt, unroll, stage, far, tma, minb;   // minb: __launch_bounds__ min blocks per SM (register cap)
   int persist;                                  // 1: persistent CTAs taking units from an atomic counter
 };
-#define kGridVariantDefault (GridVariant{8, 2, 4, 64, 8, 3, 2, 1})   // warp-level units (tma = 3), R32 quadratic
-#define kGridVariantPrecise (GridVariant{8, 2, 4, 64, 7, 3, 3, 1})   // R32 cubic: requested precision < 1e-10
+#define kGridVariantDefault (GridVariant{8, 2, 4, 64, 9, 3, 2, 1})   // warp-level units (tma = 3), R35 quadratic
+#define kGridVariantPrecise (GridVariant{8, 2, 4, 64, 10, 3, 3, 1})  // R35 cubic: requested precision < 1e-10
 constexpr double kGridQuadMinPrecision = 1e-10;   // the quadratic far form's log error is 7.7e-11 absolute
 GridVariant grid_variant_for(double precision);   // the variant a handle uses (NC_GRID_VARIANT overrides)
 int grid_far_table_bits(const GridVariant& v);    // bits of the far table the variant needs (0: none)
 void grid_far_poly(const GridVariant& v, double* a2, double* a3);   // its log1p constants (carried after the table)
-int grid_far_table_rcp(const GridVariant& v);     // 1: c from rcp.approx, L alone in the table (8-byte entries)
+int grid_far_table_rcp(const GridVariant& v);     // 1: c from rcp.approx, L alone in the table (8-byte entries);
+                                                  // 2: the same with c = rcp_seed_hl (R35)
 struct FarTable {                      // exponent-indexed far log table (green.cuh green_far_t) on device
   const double2* d = nullptr;
   int n = 0, base = 0;

@@ -114,11 +114,13 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
 // ops; absolute error ~2e-16, i.e. relative ~1e-10 at the closest grid pairs qh ~ eps^2/8, far below the
 // hierarchical tolerance) and a far form below.  x/y/z hold -X when FAR, and cq[u] = (|X_u|^2 + 1/4)/2.
 // FAR (the grid kernel's far forms): 5 = green_far_r (R25: FB = 7 cubic, clamped index), 7 = green_far_n FB = 7
-// cubic (R32: unclamped, scaled-index table load), 8 = green_far_n FB = 9 quadratic (R32)
-__host__ __device__ constexpr int far_table_bits(int far) { return far == 8 ? 9 : 7; }
-__host__ __device__ constexpr bool far_table_rcp(int far) { return far >= 5; }
+// cubic (R32: unclamped, scaled-index table load), 8 = green_far_n FB = 9 quadratic (R32), 9 / 10 = green_far_hl
+// (R35: the forms of 8 / 7 with high-word SFU seeds and a one-instruction table address)
+__host__ __device__ constexpr int far_table_bits(int far) { return far == 8 || far == 9 ? 9 : 7; }
+// 0: 16-byte (c, L) entries; 1: 8-byte L for c = rcp.approx(midpoint); 2: 8-byte L for c = rcp_seed_hl(midpoint word)
+__host__ __device__ constexpr int far_table_rcp(int far) { return far >= 9 ? 2 : far >= 5 ? 1 : 0; }
 inline void far_poly(int far, double* a2, double* a3) {   // the polynomial constants the table carries (host)
-  if (far == 8) {   // quadratic r (c1 + c2 r): c2 in the a2 slot, c1 in the a3 slot
+  if (far == 8 || far == 9) {   // quadratic r (c1 + c2 r): c2 in the a2 slot, c1 in the a3 slot
     *a2 = FarQuad<9>::c2;
     *a3 = FarQuad<9>::c1;
     return;
@@ -130,10 +132,13 @@ template <int KIND, int FAR>
 __device__ __forceinline__ double green_far_any(double qh, const double2* __restrict__ logtab, unsigned tbase,
                                                 int lim, double a2, double a3, int kmid,
                                                 const double* __restrict__ ftd = nullptr) {
-  static_assert(FAR == 5 || FAR == 7 || FAR == 8, "far form");
-  if (FAR == 5) return green_far_r<KIND, 7, 3>(qh, tbase, lim, a2, a3, kmid);
-  if (FAR == 7) return green_far_n<KIND, 7, 3>(qh, ftd, a2, a3, kmid);
-  return green_far_n<KIND, 9, 2>(qh, ftd, a2, a3, kmid);
+  static_assert(FAR == 5 || FAR == 7 || FAR == 8 || FAR == 9 || FAR == 10, "far form");
+  if constexpr (FAR == 5) return green_far_r<KIND, 7, 3>(qh, tbase, lim, a2, a3, kmid);
+  if constexpr (FAR == 7) return green_far_n<KIND, 7, 3>(qh, ftd, a2, a3, kmid);
+  if constexpr (FAR == 8) return green_far_n<KIND, 9, 2>(qh, ftd, a2, a3, kmid);
+  // tbase: byte address of table index 0; the midpoint word carries + 4 (green_far_hl)
+  if constexpr (FAR == 9) return green_far_hl<KIND, 9, 2>(qh, tbase - 4u, a2, a3, kmid);
+  if constexpr (FAR == 10) return green_far_hl<KIND, 7, 3>(qh, tbase - 4u, a2, a3, kmid);
 }
 
 // the records [0, nrec) of a staged chunk against the thread's targets (incoming-grid sums, no self exclusion)
@@ -171,6 +176,25 @@ __device__ __forceinline__ void accumulate_span(const double (&x)[TPT], const do
         const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
         acc[u] = fma(s.w, green_q<KIND>(qd, logtab), acc[u]);
       }
+    }
+  }
+}
+
+// the half-warp split of k_pairs_grid_w (TPT = 4, R35): records sm[0], sm[2], ... (sm already offset by the
+// half-warp's parity), npair of them, against the lane's 4 targets
+template <int KIND, int TPT, int UNROLL, int FAR>
+__device__ __forceinline__ void accumulate_span_split(const double (&x)[TPT], const double (&y)[TPT],
+                                                      const double (&z)[TPT], const double (&cq)[TPT],
+                                                      double (&acc)[TPT], const double4* __restrict__ sm, int npair,
+                                                      unsigned ftb, double fa2, double fa3, int fmid,
+                                                      const double* __restrict__ ftd) {
+#pragma unroll UNROLL
+  for (int m = 0; m < npair; ++m) {
+    const double4 s = sm[2 * m];
+#pragma unroll
+    for (int u = 0; u < TPT; ++u) {
+      const double qh = fma(x[u], s.x, fma(y[u], s.y, fma(z[u], s.z, cq[u])));
+      acc[u] = fma(s.w, green_far_any<KIND, FAR>(qh, nullptr, ftb, 0, fa2, fa3, fmid, ftd), acc[u]);
     }
   }
 }

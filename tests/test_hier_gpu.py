@@ -164,12 +164,12 @@ np.save(os.environ["OUT"], h.matvec(x).cpu().numpy())
 """
 
 
-@pytest.mark.parametrize("cfg,far", [("C3", "8,2,4,64,8,3,2"), ("C3", "8,2,4,64,7,3,3"), ("C3", "8,2,4,64,5,3,3"),
-                                     ("C5", "8,2,4,64,8,3,2"), ("C4", "8,2,4,64,8,3,2")])
+@pytest.mark.parametrize("cfg,far", [("C3", "8,2,4,64,9,3,2"), ("C3", "8,2,4,64,10,3,3"), ("C3", "8,2,4,64,5,3,3"),
+                                     ("C3", "8,2,4,64,8,3,2"), ("C5", "8,2,4,64,9,3,2"), ("C4", "8,2,4,64,9,3,2")])
 def test_far_field_pair_variant_error(tmp_path, cfg, far):
     """k_pairs_grid_w's far-field evaluations (R23: dot-product distance + one-Newton rsqrt; R25: the
-    exponent-indexed log table with c from rcp.approx; R32: the unclamped table, FB = 9 quadratic (the default) or
-    FB = 7 cubic) against the EXACT difference-form pair kernel on the same grids and sources (the CTA-level kernel,
+    exponent-indexed log table with c from rcp.approx; R32: the unclamped table, FB = 9 quadratic or FB = 7 cubic;
+    R35: the same with high-word SFU seeds, the defaults) against the EXACT difference-form pair kernel on the same grids and sources (the CTA-level kernel,
     far 0), at the C3 / C4 / C5 epsilons: the difference must stay far below the hierarchical precision."""
     import subprocess
     import sys
