@@ -337,7 +337,8 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
   launch_frames(h->d_centers, N, h->d_frames, s);
 
   // source records (x, y, z, rho) for all N patches and every rung, coordinates scaled by 1/2 (green.cuh)
-  if ((rc = dalloc(h, &h->d_src4, (size_t)N * ptot * 4))) return bail(rc);
+  if ((rc = dalloc(h, &h->d_src4, (size_t)N * ptot * 4)) || (rc = dalloc(h, &h->d_rho, (size_t)N * ptot)))
+    return bail(rc);
   for (int k = 0; k < h->nrung; ++k)
     launch_sources(h->d_frames, N, h->d_shat + 3 * h->rung_trow[k], h->rung_p[k], 0.5, h->d_src4 + h->rung_soff[k],
                    s);
@@ -379,8 +380,8 @@ int nc_setup(nc_handle** out, int kind, int64_t N, const double* centers, double
         if (!h->rung_used[k]) continue;
         const int pk = h->rung_p[k];
         for (int m = 0; m < pk; ++m) {
-          cb.push_back(h->rung_soff[k] + 4 * (int64_t)m + 3);
-          cr.push_back(4 * (int64_t)pk);
+          cb.push_back(h->rung_soff[k] / 4 + m);   // rung k's compact rho: rho_k[i p_k + m]
+          cr.push_back((int64_t)pk);
         }
         Tc.insert(Tc.end(), Th.begin() + (size_t)h->rung_trow[k] * K, Th.begin() + (size_t)(h->rung_trow[k] + pk) * K);
       }
@@ -439,11 +440,11 @@ static inline void mark(nc_handle* h, int i, cudaStream_t s) {
 }
 
 // K1 for rows [r0, r0 + nr) of the internal order (x points at row r0): rho_i = T_k fhat_i for every rung in use,
-// written into the records' 4th slot
+// written into the rung's compact rho array (contiguous rows of p_k: full-sector writes)
 static void outgoing(nc_handle* h, const double* x, int64_t r0, int64_t nr, cudaStream_t s) {
   const int K = h->K;
   if (h->ncat > 0) {   // all rungs in use in one GEMM (scattered epilogue)
-    launch_gemm_dmma_colmap(x, K, h->d_Tcat, nr, h->ncat, K, h->d_src4, h->d_colbase, h->d_colrstride, r0, s);
+    launch_gemm_dmma_colmap(x, K, h->d_Tcat, nr, h->ncat, K, h->d_rho, h->d_colbase, h->d_colrstride, r0, s);
     h->launches_last++;
     return;
   }
@@ -451,7 +452,7 @@ static void outgoing(nc_handle* h, const double* x, int64_t r0, int64_t nr, cuda
     if (!h->rung_used[k]) continue;
     const int pk = h->rung_p[k];
     launch_gemm_dmma(x, K, 1, 0, h->d_T + (size_t)h->rung_trow[k] * K, nr, pk, K,
-                     h->d_src4 + h->rung_soff[k] + (size_t)r0 * pk * 4 + 3, (int64_t)pk * 4, 4, nullptr, 0, s);
+                     h->d_rho + h->rung_soff[k] / 4 + (size_t)r0 * pk, (int64_t)pk, 1, nullptr, 0, s);
     h->launches_last++;
   }
 }
@@ -461,7 +462,8 @@ static int matvec_tail(nc_handle* h, const double* x, double* y, cudaStream_t s)
   const int K = h->K, p = h->p, Ks = h->Kstar;
   mark(h, 2, s);
   if (h->mode == NC_DIRECT) {
-    launch_pairs_direct(h->kind, h->pair_tpt, h->d_tx, h->d_ty, h->d_tz, h->row_count * Ks, Ks, h->row_begin, h->d_src4, p, h->N,
+    launch_pairs_direct(h->kind, h->pair_tpt, h->d_tx, h->d_ty, h->d_tz, h->row_count * Ks, Ks, h->row_begin, h->d_src4,
+                        h->d_rho, p, h->N,
                         h->nseg, h->d_upart, h->xtab, h->eps, s);
     mark(h, 3, s);
     // K3: Y = X + (sum_seg U_seg) P^T
@@ -791,18 +793,21 @@ static int order_after_caller(nc_handle* h) {
 }
 
 // The base rung's source records (coordinates of every patch's skeleton nodes, scaled by 1/2, and rho = T fhat) in a
-// buffer of the call's own: the field and residual entry points never write the matvec's records.
+// buffer of the call's own: the field and residual entry points never write the matvec's records or rho.
+// Layout: N p0 records (x, y, z, rho) for the field kernels, then the same rho compactly (N p0) for the pair kernels.
 static int base_records(nc_handle* h, const double* x_all, cudaStream_t s, double** out) {
   const int K = h->K, p0 = h->rung_p[0];
   const size_t n = (size_t)h->N * p0 * 4;
   double* d = nullptr;
-  if (cudaMalloc(&d, n * sizeof(double)) != cudaSuccess) {
+  if (cudaMalloc(&d, (n + n / 4) * sizeof(double)) != cudaSuccess) {
     (void)cudaGetLastError();
     return fail(NC_ENOMEM, "base records: device allocation failed");
   }
   cudaError_t e = cudaMemcpyAsync(d, h->d_src4 + h->rung_soff[0], n * sizeof(double), cudaMemcpyDeviceToDevice, s);
   if (e == cudaSuccess) {   // rho of the base rung for all N patches (K1 restricted to rung 0) into slot 3
     launch_gemm_dmma(x_all, K, 1, 0, h->d_T + (size_t)h->rung_trow[0] * K, h->N, p0, K, d + 3, (int64_t)p0 * 4, 4,
+                     nullptr, 0, s);
+    launch_gemm_dmma(x_all, K, 1, 0, h->d_T + (size_t)h->rung_trow[0] * K, h->N, p0, K, d + n, (int64_t)p0, 1,
                      nullptr, 0, s);
     e = cudaGetLastError();
   }
@@ -1098,7 +1103,8 @@ int nc_residual(nc_handle* h, const double* x_all, int n_sel, const int64_t* pat
       for (int q = 0; q < n_sel; ++q) {   // the residual grid on patch rows[q] (scaled by 1/2), then the other patches' field
         double* tx = d_t + (size_t)q * nr * 3;
         launch_targets(h->d_frames, rows[q], 1, d_rhat, n_res, 0.5, tx, tx + nr, tx + 2 * nr, s);
-        launch_pairs_direct(h->kind, h->pair_tpt, tx, tx + nr, tx + 2 * nr, n_res, n_res, rows[q], src0, p0, h->N, nseg,
+        launch_pairs_direct(h->kind, h->pair_tpt, tx, tx + nr, tx + 2 * nr, n_res, n_res, rows[q], src0,
+                            src0 + (size_t)h->N * p0 * 4, p0, h->N, nseg,
                             d_up + (size_t)q * nseg * nr, h->xtab, h->eps, s);
       }
       launch_residual(n_sel, n_res, K, nseg, d_rows, x_all, d_S, d_w, d_up, d_out, d_out + (size_t)n_sel * nr, s);
@@ -1235,7 +1241,7 @@ void nc_destroy(nc_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   hier_destroy(h);
   double* bufs[] = {h->d_T, h->d_P, h->d_I, h->d_zhat, h->d_shat, h->d_centers, h->d_frames, h->d_tx, h->d_ty,
-                    h->d_tz, h->d_src4, h->d_upart, h->d_V, h->d_red, h->d_b, h->d_hx, h->d_hy, h->d_Tcat, h->d_xall,
+                    h->d_tz, h->d_src4, h->d_rho, h->d_upart, h->d_V, h->d_red, h->d_b, h->d_hx, h->d_hy, h->d_Tcat, h->d_xall,
                     h->d_xpad};
   if (h->d_xtab) cudaFree(h->d_xtab);
   for (double* b : bufs)

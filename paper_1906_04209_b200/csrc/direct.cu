@@ -26,7 +26,8 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_pairs_direct(const double* 
                                                                 const double* __restrict__ ty,
                                                                 const double* __restrict__ tz, int64_t n_tgt,
                                                                 int Kstar, int64_t tgt_patch0,
-                                                                const double* __restrict__ src4, int p, int64_t N,
+                                                                const double* __restrict__ src4,
+                                                                const double* __restrict__ rho, int p, int64_t N,
                                                                 int nseg, int chp, double* __restrict__ upart,
                                                                 const double2* __restrict__ logsrc,
                                                                 const double2* __restrict__ xsrc, int xn, int xbase,
@@ -55,11 +56,11 @@ __global__ void __launch_bounds__(kPairThreads, 2) k_pairs_direct(const double* 
   if (chp == 0) {
     __syncthreads();
     accumulate_list_ldg<KIND, TPT>(x, y, z, excl, acc, j1 - j0, [=] __device__(int64_t k) { return j0 + k; },
-                                   reinterpret_cast<const double4*>(src4), p, logtab);
+                                   reinterpret_cast<const double4*>(src4), rho, p, logtab);
   } else {
     auto greenfar = [&](double qh) { return green_exact_far<KIND>(qh, xt.tb, xt.lim, xt.a2, xt.a3, xt.kmid); };
     accumulate_list<KIND, TPT>(x, y, z, excl, acc, j1 - j0, [=] __device__(int64_t k) { return j0 + k; },
-                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, green, true, greenfar,
+                               reinterpret_cast<const double4*>(src4), rho, p, sm, pid, chp, green, true, greenfar,
                                EX ? far_q : 0.0);
   }
 #pragma unroll
@@ -88,7 +89,8 @@ int pairs_direct_blocks_per_sm(int p, int tpt, const FarTable& xt) {
 }
 
 void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, const double* tz, int64_t n_tgt,
-                         int Kstar, int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
+                         int Kstar, int64_t tgt_patch0, const double* src4, const double* rho, int p, int64_t N,
+                         int nseg, double* upart,
                          const FarTable& xt, double eps, cudaStream_t s) {
   if (n_tgt <= 0) return;
   const int chp = stage_ldg() ? 0 : stage_patches(p);
@@ -109,7 +111,7 @@ void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, 
   {                                                                                                                \
     auto kern = k_pairs_direct<KD, TP, EX>;                                                                        \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
-    kern<<<grid, kPairThreads, smem, s>>>(tx, ty, tz, n_tgt, Kstar, tgt_patch0, src4, p, N, nseg, chp, upart,       \
+    kern<<<grid, kPairThreads, smem, s>>>(tx, ty, tz, n_tgt, Kstar, tgt_patch0, src4, rho, p, N, nseg, chp, upart,  \
                                           log_table_device(), xt.d, xt.n, xt.base, 1 << 12, far_q);                \
   }
   if (kind == NC_EXTERIOR) {
@@ -132,6 +134,7 @@ template <int KIND, int NT, int TPT, int UNROLL, int FAR>
 __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const double* __restrict__ gx,
                                           const double* __restrict__ gy, const double* __restrict__ gz,
                                           const int32_t* __restrict__ srclist, const double* __restrict__ src4,
+                                          const double* __restrict__ rho,
                                           int stage_records, double* __restrict__ part, double4* __restrict__ sm,
                                           int64_t* __restrict__ pid, const double2* __restrict__ logtab,
                                           unsigned ftb, int flim, double fa2, double fa3, int fmid) {
@@ -157,7 +160,8 @@ __device__ __forceinline__ void grid_unit(const GridUnit& U, int64_t uid, const 
   int chp = stage_records / U.p;
   chp = chp < 1 ? 1 : (chp > kStagePatchesMax ? kStagePatchesMax : chp);
   accumulate_grid<KIND, TPT, UNROLL, FAR, double2>(x, y, z, cq, acc, U.nsrc,
-                                                   [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4, U.p, sm,
+                                                   [=] __device__(int64_t k) { return (int64_t)lst[k]; }, s4,
+                                                   rho + U.soff / 4, U.p, sm,
                                                    pid, chp, logtab, any, single, ftb, flim, fa2, fa3, fmid);
   const int upts = NT * TPT;
   if (single) {
@@ -177,7 +181,8 @@ template <int KIND, int NT, int TPT, int UNROLL, int FAR, int MINB, bool ASYNC =
 __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restrict__ units, const double* __restrict__ gx,
                                                    const double* __restrict__ gy, const double* __restrict__ gz,
                                                    const int32_t* __restrict__ srclist,
-                                                   const double* __restrict__ src4, int stage_records,
+                                                   const double* __restrict__ src4, const double* __restrict__ rho,
+                                                   int stage_records,
                                                    double* __restrict__ part, const double2* __restrict__ logsrc,
                                                    int* __restrict__ counter, int64_t nunits,
                                                    const double2* __restrict__ fsrc, int fn, int fbase, int fmid) {
@@ -205,8 +210,8 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
   }
   if (!counter) {
     __syncthreads();
-    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[blockIdx.x], blockIdx.x, gx, gy, gz, srclist, src4, stage_records, part,
-                                          sm, pid, logtab, tb, flim, fa2, fa3, fmid);
+    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[blockIdx.x], blockIdx.x, gx, gy, gz, srclist, src4, rho, stage_records,
+                                          part, sm, pid, logtab, tb, flim, fa2, fa3, fmid);
     return;
   }
   for (;;) {
@@ -215,8 +220,8 @@ __global__ void __launch_bounds__(NT, MINB) k_pairs_grid(const GridUnit* __restr
     __syncthreads();
     const int u = next;
     if (u >= nunits) break;
-    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[u], u, gx, gy, gz, srclist, src4, stage_records, part, sm, pid, logtab,
-                                          tb, flim, fa2, fa3, fmid);
+    grid_unit<KIND, NT, TPT, UNROLL, FAR>(units[u], u, gx, gy, gz, srclist, src4, rho, stage_records, part, sm, pid,
+                                          logtab, tb, flim, fa2, fa3, fmid);
   }
 }
 
@@ -288,7 +293,8 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
                                                           const double* __restrict__ gx, const double* __restrict__ gy,
                                                           const double* __restrict__ gz,
                                                           const int32_t* __restrict__ srclist,
-                                                          const double* __restrict__ src4, int wrec,
+                                                          const double* __restrict__ src4,
+                                                          const double* __restrict__ rho, int wrec,
                                                           double* __restrict__ part, const double2* __restrict__ fsrc,
                                                           int fn, int fbase, int* __restrict__ counter,
                                                           int64_t nunits, int fmid) {
@@ -331,17 +337,25 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
     if (lane < U.nsrc) slst[lane] = srclist[U.src0 + lane];
     __syncwarp();
     const double4* __restrict__ s4 = reinterpret_cast<const double4*>(src4 + U.soff);
+    const double* __restrict__ r1 = rho + U.soff / 4;   // the rung's compact rho (K1 output), same record index
     const int p = U.p, ntot = U.nsrc * p, nch = (ntot + wrec - 1) / wrec;
     auto issue = [&](int c) {
       const int r0 = c * wrec, n = min(wrec, ntot - r0);
-      double2* dst = reinterpret_cast<double2*>(buf + (size_t)(c & 1) * wrec);
-      for (int t = lane; t < 2 * n; t += 32) {
-        const int rr = r0 + (t >> 1), q = rr / p, m = rr - q * p;
-        cp_async16(dst + t, reinterpret_cast<const double2*>(s4 + (size_t)slst[q] * p + m) + (t & 1));
+      double4* dst = buf + (size_t)(c & 1) * wrec;
+      // one record per lane and step: (x, y) and z from the static coordinates, rho from the compact array; the
+      // record's (patch, node) is advanced by 32 per step instead of divided out per piece
+      int q = (r0 + lane) / p, m = r0 + lane - q * p;
+      for (int t = lane; t < n; t += 32) {
+        const size_t g = (size_t)slst[q] * p + m;
+        cp_async16(dst + t, s4 + g);
+        cp_async8(reinterpret_cast<double*>(dst + t) + 2, reinterpret_cast<const double*>(s4 + g) + 2);
+        cp_async8(reinterpret_cast<double*>(dst + t) + 3, r1 + g);
+        m += 32;
+        while (m >= p) { m -= p; ++q; }
       }
       // SPLIT: an odd chunk gets a zero-weight record at the origin (its G is finite: |z| = 1, inside the table),
       // so both half-warps run the same trip count; n < wrec here (wrec is even)
-      if (SPLIT && (n & 1) && lane == 0) reinterpret_cast<double4*>(dst)[n] = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (SPLIT && (n & 1) && lane == 0) dst[n] = make_double4(0.0, 0.0, 0.0, 0.0);
       cp_async_commit();
     };
     issue(0);
@@ -380,8 +394,8 @@ __global__ void __launch_bounds__(32 * WPC, MINB) k_pairs_grid_w(const GridUnit*
 
 template <int KIND, int TPT, int UNROLL, int FAR, int WPC, int MINB>
 static void launch_grid_w(const GridUnit* units, int64_t nunits, const double* gx, const double* gy, const double* gz,
-                          const int32_t* srclist, const double* src4, int wrec, double* part, int* counter,
-                          const FarTable& ft, cudaStream_t s) {
+                          const int32_t* srclist, const double* src4, const double* rho, int wrec, double* part,
+                          int* counter, const FarTable& ft, cudaStream_t s) {
   const size_t smem = (size_t)WPC * 2 * wrec * sizeof(double4) + (size_t)WPC * 32 * sizeof(int32_t) +
                       (size_t)ft.n * (far_table_rcp(FAR) ? 8 : 16) + sizeof(double2);
   auto kern = k_pairs_grid_w<KIND, TPT, UNROLL, FAR, WPC, MINB>;
@@ -392,21 +406,22 @@ static void launch_grid_w(const GridUnit* units, int64_t nunits, const double* g
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 32 * WPC, smem);
   const int64_t ctas = std::min<int64_t>((int64_t)std::max(1, per) * sms, (nunits + WPC - 1) / WPC);
   cudaMemsetAsync(counter, 0, sizeof(int), s);
-  kern<<<(unsigned)ctas, 32 * WPC, smem, s>>>(units, gx, gy, gz, srclist, src4, wrec, part, ft.d, ft.n, ft.base,
+  kern<<<(unsigned)ctas, 32 * WPC, smem, s>>>(units, gx, gy, gz, srclist, src4, rho, wrec, part, ft.d, ft.n, ft.base,
                                               counter, nunits, 1 << (19 - far_table_bits(FAR)));
 }
 
 template <int KIND, int NT, int TPT, int UNROLL, int FAR, int TMA, int MINB>
 static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* gx, const double* gy, const double* gz,
-                          const int32_t* srclist, const double* src4, int stage, int pmax, double* part,
-                          int persist, int* counter, const FarTable& ft, cudaStream_t s) {
+                          const int32_t* srclist, const double* src4, const double* rho, int stage, int pmax,
+                          double* part, int persist, int* counter, const FarTable& ft, cudaStream_t s) {
   static_assert(TMA == 0, "CTA-level grid kernel: synchronous staging only");
   const int rec = std::max(stage, pmax);   // records per stage buffer: >= one whole patch of any rung
   const size_t smem = (size_t)rec * sizeof(double4) + (FAR >= 2 ? (size_t)ft.n * (far_table_rcp(FAR) ? 8 : 16) : 0);
   auto kern = k_pairs_grid<KIND, NT, TPT, UNROLL, FAR, MINB, false>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (!persist) {
-    kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part, log_table_device(), nullptr,
+    kern<<<(unsigned)nunits, NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rho, rec, part, log_table_device(),
+                                            nullptr,
                                             nunits, ft.d, ft.n, ft.base, 1 << (19 - far_table_bits(FAR)));
     return;
   }
@@ -417,32 +432,32 @@ static void launch_grid_t(const GridUnit* units, int64_t nunits, const double* g
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, smem);
   const int ctas = std::max(1, per) * sms;
   cudaMemsetAsync(counter, 0, sizeof(int), s);
-  kern<<<(unsigned)std::min<int64_t>(ctas, nunits), NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rec, part,
+  kern<<<(unsigned)std::min<int64_t>(ctas, nunits), NT, smem, s>>>(units, gx, gy, gz, srclist, src4, rho, rec, part,
                                                                    log_table_device(), counter, nunits, ft.d, ft.n,
                                                                    ft.base, 1 << (19 - far_table_bits(FAR)));
 }
 
 void launch_pairs_grid(const GridVariant& v, int kind, const GridUnit* units, int64_t nunits, const double* gx,
-                       const double* gy, const double* gz, const int32_t* srclist, const double* src4, int pmax,
-                       double* part, int* counter, const FarTable& ft, cudaStream_t s) {
+                       const double* gy, const double* gz, const int32_t* srclist, const double* src4,
+                       const double* rho, int pmax, double* part, int* counter, const FarTable& ft, cudaStream_t s) {
   if (nunits <= 0) return;   // v: an instantiated combination (grid_variant_for checks)
 #define NC_GW(TP, UR, FR, WP, MB)                                                                                  \
   if (v.tma == 3 && v.tpt == TP && v.unroll == UR && v.far == FR && v.nt == WP && v.minb == MB) {                 \
     if (kind == 0)                                                                                                 \
-      return launch_grid_w<0, TP, UR, FR, WP, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, part, counter, \
-                                                  ft, s);                                                          \
-    return launch_grid_w<1, TP, UR, FR, WP, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, part, counter,   \
-                                                ft, s);                                                            \
+      return launch_grid_w<0, TP, UR, FR, WP, MB>(units, nunits, gx, gy, gz, srclist, src4, rho, v.stage, part,     \
+                                                  counter, ft, s);                                                 \
+    return launch_grid_w<1, TP, UR, FR, WP, MB>(units, nunits, gx, gy, gz, srclist, src4, rho, v.stage, part,       \
+                                                counter, ft, s);                                                   \
   }
   NC_GRID_W_LIST(NC_GW)
 #undef NC_GW
 #define NC_G(NT, TP, UR, FR, TM, MB)                                                                              \
   if (v.tma == TM && v.nt == NT && v.tpt == TP && v.unroll == UR && v.far == FR && v.minb == MB) {                \
     if (kind == 0)                                                                                                 \
-      return launch_grid_t<0, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, pmax, part, \
-                                                      v.persist, counter, ft, s);                                  \
-    return launch_grid_t<1, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, v.stage, pmax, part,   \
-                                                    v.persist, counter, ft, s);                                    \
+      return launch_grid_t<0, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, rho, v.stage, pmax, \
+                                                      part, v.persist, counter, ft, s);                            \
+    return launch_grid_t<1, NT, TP, UR, FR, TM, MB>(units, nunits, gx, gy, gz, srclist, src4, rho, v.stage, pmax,   \
+                                                    part, v.persist, counter, ft, s);                              \
   }
   NC_GRID_C_LIST(NC_G)
 #undef NC_G
@@ -458,7 +473,8 @@ __global__ void __launch_bounds__(NT) k_pairs_near(const double* __restrict__ tx
                                                               const int32_t* __restrict__ work,  // local patch ids
                                                               const int64_t* __restrict__ near_off,
                                                               const int32_t* __restrict__ near,
-                                                              const double* __restrict__ src4, int p, int chp,
+                                                              const double* __restrict__ src4,
+                                                              const double* __restrict__ rho, int p, int chp,
                                                               double* __restrict__ udir,
                                                               const double2* __restrict__ logsrc,
                                                               const double2* __restrict__ xsrc, int xn, int xbase,
@@ -490,10 +506,10 @@ __global__ void __launch_bounds__(NT) k_pairs_near(const double* __restrict__ tx
   if (chp == 0) {
     __syncthreads();
     accumulate_list_ldg<KIND, TPT>(x, y, z, excl, acc, o1 - o0, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
-                                   reinterpret_cast<const double4*>(src4), p, logtab);
+                                   reinterpret_cast<const double4*>(src4), rho, p, logtab);
   } else {
     accumulate_list<KIND, TPT>(x, y, z, excl, acc, o1 - o0, [=] __device__(int64_t k) { return (int64_t)lst[k]; },
-                               reinterpret_cast<const double4*>(src4), p, sm, pid, chp, green, true, green, 0.0);
+                               reinterpret_cast<const double4*>(src4), rho, p, sm, pid, chp, green, true, green, 0.0);
   }
 #pragma unroll
   for (int u = 0; u < TPT; ++u) {
@@ -503,8 +519,8 @@ __global__ void __launch_bounds__(NT) k_pairs_near(const double* __restrict__ tx
 }
 
 void launch_pairs_near(int kind, const double* tx, const double* ty, const double* tz, int Kstar, const int32_t* work,
-                       int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
-                       double* udir, const FarTable& xt, cudaStream_t s) {
+                       int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4,
+                       const double* rho, int p, double* udir, const FarTable& xt, cudaStream_t s) {
   if (nwork <= 0) return;
   const int chp = stage_ldg() ? 0 : stage_patches(p);
   const bool ex = exact_table_on(xt);
@@ -517,7 +533,7 @@ void launch_pairs_near(int kind, const double* tx, const double* ty, const doubl
   {                                                                                                                \
     auto kern = k_pairs_near<KD, 2, EX, NTT>;                                                                      \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
-    kern<<<nb, NTT, smem, s>>>(tx, ty, tz, Kstar, work, near_off, near, src4, p, chp, udir, log_table_device(),     \
+    kern<<<nb, NTT, smem, s>>>(tx, ty, tz, Kstar, work, near_off, near, src4, rho, p, chp, udir, log_table_device(),\
                                xt.d, xt.n, xt.base, 1 << 12);                                                      \
   }
 #define NC_LAUNCH_NT(KD, EX) \

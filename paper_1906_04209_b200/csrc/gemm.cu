@@ -128,8 +128,10 @@ __global__ void __launch_bounds__(256) k_gemm_dmma_pipe(const double* __restrict
   double* Bs = gsm + 2 * PM * PLD;               // [2][PN][PLD]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;       // warp tile rows wm*32.., cols wn*32..
-  const int64_t row0 = (int64_t)blockIdx.x * PM;
-  const int col0 = blockIdx.y * PN;
+  // column tiles vary fastest (blockIdx.x): the CTAs resident together share their A row tile through L2, so A is read
+  // from DRAM once rather than once per column tile (the K1 epilogue's record writes otherwise evict it)
+  const int64_t row0 = (int64_t)blockIdx.y * PM;
+  const int col0 = blockIdx.x * PN;
   auto issue = [&](int k0, int b) {
     // A: 128 rows x 16 k = 1024 16-byte pieces (2 doubles), 4 per thread; B: 64 x 16 = 512, 2 per thread
 #pragma unroll
@@ -214,7 +216,7 @@ static void launch_pipe(const double* A, int64_t lda, const double* Bt, int64_t 
                         const int64_t* colrstride, int64_t crow0, cudaStream_t s) {
   const size_t smem = (size_t)2 * (PM + PN) * PLD * sizeof(double);
   cudaFuncSetAttribute(k_gemm_dmma_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((unsigned)((rows + PM - 1) / PM), (unsigned)((ncols + PN - 1) / PN));
+  dim3 grid((unsigned)((ncols + PN - 1) / PN), (unsigned)((rows + PM - 1) / PM));
   k_gemm_dmma_pipe<<<grid, 256, smem, s>>>(A, lda, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx, colbase, colrstride,
                                            crow0);
 }

@@ -2128,7 +2128,8 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   const int64_t rc = h->row_count;
   const int Ks = h->Kstar, K = h->K;
   // steps 2-3: interaction-list and leaf-neighbour sources on the incoming grids
-  launch_pairs_grid(H->gv, h->kind, H->d_units, H->nunits, H->d_gx, H->d_gy, H->d_gz, H->d_srclist, h->d_src4, H->pmax,
+  launch_pairs_grid(H->gv, h->kind, H->d_units, H->nunits, H->d_gx, H->d_gy, H->d_gz, H->d_srclist, h->d_src4, h->d_rho,
+                    H->pmax,
                     H->d_part, H->d_counter, H->ftab, s);
   h->launches_last += H->nunits > 0;
   if (h->time_stages) cudaEventRecord(h->ev[3], s);
@@ -2152,7 +2153,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   // near lists at the Zernike nodes
   NC_CUDA_TRY(cudaMemsetAsync(H->d_udir, 0, (size_t)rc * Ks * sizeof(double), s));
   launch_pairs_near(h->kind, H->d_tx, H->d_ty, H->d_tz, Ks, H->d_work_near, H->nwork_near, H->d_near_off, H->d_near,
-                    h->d_src4, h->p, H->d_udir, h->xtab, s);
+                    h->d_src4, h->d_rho, h->p, H->d_udir, h->xtab, s);
   h->launches_last += H->nwork_near > 0;
   // step 4b: interpolation to the Zernike nodes, summed over levels
   if (rc > 0) {

@@ -126,7 +126,8 @@ struct nc_handle {
   double* d_tx = nullptr;         // row_count*Kstar targets (SoA)
   double* d_ty = nullptr;
   double* d_tz = nullptr;
-  double* d_src4 = nullptr;       // per rung k: N * p_k records (x, y, z, rho), coordinates scaled by 1/2
+  double* d_src4 = nullptr;       // per rung k: N * p_k records (x, y, z, -), coordinates scaled by 1/2 (static)
+  double* d_rho = nullptr;        // per rung k: N * p_k values rho = T_k fhat (K1 output), at d_src4's offset / 4
   nc::FarTable xtab;              // exact-form log table of the direct / near-list kernels (green_exact_r)
   double2* d_xtab = nullptr;
   // outgoing-operator rungs: 0 = base (T, shat, p); 1.. = per-level ladder
@@ -214,18 +215,18 @@ void launch_gemm_dmma_colmap(const double* A, int64_t lda, const double* Bt, int
 // direct pair sums: upart[seg][t] = sum over source patches j in segment seg, j != patch(t), of
 // sum_m G(target t, s_jm) rho_jm
 void launch_pairs_direct(int kind, int tpt, const double* tx, const double* ty, const double* tz, int64_t n_tgt,
-                         int Kstar, int64_t tgt_patch0, const double* src4, int p, int64_t N, int nseg, double* upart,
-                         const FarTable& xt, double eps, cudaStream_t s);
+                         int Kstar, int64_t tgt_patch0, const double* src4, const double* rho, int p, int64_t N,
+                         int nseg, double* upart, const FarTable& xt, double eps, cudaStream_t s);
 
 int pairs_direct_blocks_per_sm(int p, int tpt, const FarTable& xt);
 void split_rows(const double* w, int64_t N, int world, int64_t* begin, int64_t* count);
 void launch_pairs_grid(const GridVariant& v, int kind, const GridUnit* units, int64_t nunits, const double* gx,
-                       const double* gy, const double* gz, const int32_t* srclist, const double* src4, int pmax,
-                       double* part, int* counter /* device int, persistent variant */, const FarTable& ft,
-                       cudaStream_t s);
+                       const double* gy, const double* gz, const int32_t* srclist, const double* src4,
+                       const double* rho, int pmax, double* part, int* counter /* device int, persistent variant */,
+                       const FarTable& ft, cudaStream_t s);
 void launch_pairs_near(int kind, const double* tx, const double* ty, const double* tz, int Kstar, const int32_t* work,
-                       int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4, int p,
-                       double* udir, const FarTable& xt, cudaStream_t s);
+                       int64_t nwork, const int64_t* near_off, const int32_t* near, const double* src4,
+                       const double* rho, int p, double* udir, const FarTable& xt, cudaStream_t s);
 
 // off-surface field (field.cu, NEXT-3): out[t] = sum over all source records of G_off(pts_t, s) rho_s, dmin[t] =
 // min |pts_t - s|; part / dpart: nseg x n scratch

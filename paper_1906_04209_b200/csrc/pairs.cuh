@@ -4,8 +4,9 @@
 //
 // used by the direct sum (a2), the hierarchical interaction-list / neighbour evaluations on incoming grids
 // (a3, a4) and the near-list evaluations at Zernike nodes (a4, reading R12).  Whole source patches
-// (p records of (x, y, z, rho), 32 B each, coordinates pre-scaled by 1/2) are staged in shared memory with
-// coalesced 16 B loads; each thread owns TPT targets (independent FP64 chains sharing every broadcast load).
+// (p records: the static coordinates (x, y, z, -) of 32 B, pre-scaled by 1/2, and rho = T fhat from the compact
+// per-rung array K1 writes) are staged in shared memory as (x, y, z, rho); each thread owns TPT targets (independent
+// FP64 chains sharing every broadcast load).
 #pragma once
 
 #include "green.cuh"
@@ -31,7 +32,8 @@ __host__ __device__ inline int stage_patches(int p) {
 template <int KIND, int TPT, int UNROLL = 2, class GreenQ, class PatchAt, class GreenFar = GreenQ>
 __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
                                                 const int64_t (&excl)[TPT], double (&acc)[TPT], int64_t nlist,
-                                                PatchAt patch_at, const double4* __restrict__ s4, int p,
+                                                PatchAt patch_at, const double4* __restrict__ s4,
+                                                const double* __restrict__ rho, int p,
                                                 double4* __restrict__ sm, int64_t* __restrict__ sm_pid, int chp,
                                                 GreenQ green, bool active, GreenFar greenfar, double far_q) {
   double cq[TPT];   // (|X|^2 + 1/4) / 2: qh = cq - X.S for the far path
@@ -44,7 +46,10 @@ __device__ __forceinline__ void accumulate_list(const double (&x)[TPT], const do
     __syncthreads();
     for (int r = threadIdx.x; r < nch * p; r += blockDim.x) {
       const int q = r / p;
-      sm[r] = s4[sm_pid[q] * p + (r - q * p)];
+      const int64_t g = sm_pid[q] * p + (r - q * p);
+      double4 v = s4[g];
+      v.w = rho[g];
+      sm[r] = v;
     }
     __syncthreads();
     if (!active) continue;
@@ -202,7 +207,8 @@ __device__ __forceinline__ void accumulate_span_split(const double (&x)[TPT], co
 template <int KIND, int TPT, int UNROLL, int FAR, class Tab, class PatchAt>
 __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const double (&y)[TPT], const double (&z)[TPT],
                                                 const double (&cq)[TPT], double (&acc)[TPT], int64_t nlist,
-                                                PatchAt patch_at, const double4* __restrict__ s4, int p,
+                                                PatchAt patch_at, const double4* __restrict__ s4,
+                                                const double* __restrict__ rho, int p,
                                                 double4* __restrict__ sm, int64_t* __restrict__ sm_pid, int chp,
                                                 const Tab* __restrict__ logtab, bool active,
                                                 bool single = false, unsigned ftb = 0, int flim = 0,
@@ -214,7 +220,10 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
     __syncthreads();
     for (int r = threadIdx.x; r < nch * p; r += blockDim.x) {
       const int q = r / p;
-      sm[r] = s4[sm_pid[q] * p + (r - q * p)];
+      const int64_t g = sm_pid[q] * p + (r - q * p);
+      double4 v = s4[g];
+      v.w = rho[g];
+      sm[r] = v;
     }
     __syncthreads();
     if (!active) continue;
@@ -225,6 +234,10 @@ __device__ __forceinline__ void accumulate_grid(const double (&x)[TPT], const do
 // cp.async (global -> shared, 16-byte pieces, no registers in flight): the warp-level grid kernel's double buffer
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -239,8 +252,8 @@ template <int KIND, int TPT, class PatchAt>
 __device__ __forceinline__ void accumulate_list_ldg(const double (&x)[TPT], const double (&y)[TPT],
                                                     const double (&z)[TPT], const int64_t (&excl)[TPT],
                                                     double (&acc)[TPT], int64_t nlist, PatchAt patch_at,
-                                                    const double4* __restrict__ s4, int p,
-                                                    const double2* __restrict__ logtab) {
+                                                    const double4* __restrict__ s4, const double* __restrict__ rho,
+                                                    int p, const double2* __restrict__ logtab) {
   const double2* __restrict__ s2 = reinterpret_cast<const double2*>(s4);
   for (int64_t k = 0; k < nlist; ++k) {
     const int64_t j = patch_at(k);
@@ -252,15 +265,17 @@ __device__ __forceinline__ void accumulate_list_ldg(const double (&x)[TPT], cons
     }
     if (none) continue;
     const double2* __restrict__ sp = s2 + 2 * j * p;
+    const double* __restrict__ rp = rho + j * p;
     if (all) {
 #pragma unroll 2
       for (int m = 0; m < p; ++m) {
         const double2 a = __ldg(sp + 2 * m), b = __ldg(sp + 2 * m + 1);
+        const double w = __ldg(rp + m);
 #pragma unroll
         for (int u = 0; u < TPT; ++u) {
           const double dx = x[u] - a.x, dy = y[u] - a.y, dz = z[u] - b.x;
           const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
-          acc[u] = fma(b.y, green_q<KIND>(qd, logtab), acc[u]);
+          acc[u] = fma(w, green_q<KIND>(qd, logtab), acc[u]);
         }
       }
     } else {
@@ -271,7 +286,7 @@ __device__ __forceinline__ void accumulate_list_ldg(const double (&x)[TPT], cons
           const double2 a = __ldg(sp + 2 * m), b = __ldg(sp + 2 * m + 1);
           const double dx = x[u] - a.x, dy = y[u] - a.y, dz = z[u] - b.x;
           const double qd = fma(dz, dz, fma(dy, dy, dx * dx));
-          acc[u] = fma(b.y, green_q<KIND>(qd, logtab), acc[u]);
+          acc[u] = fma(__ldg(rp + m), green_q<KIND>(qd, logtab), acc[u]);
         }
       }
     }
