@@ -125,6 +125,10 @@ typedef struct nc_stats_t {
                                  /*   targets per thread, unroll, stage, far form, tma, minb, persist} */
   double hier_unit_points;       /* NC_HIER: sum over work units of their grid points: the partial   */
                                  /*   values k_pairs_grid writes and k_reduce_chunks reads per matvec  */
+  int32_t proxy_n;               /* NC_HIER: step-4 proxies per patch (0: every level at the nodes; R36) */
+  double proxy_kappa;            /*   far-level threshold D / h of the rule (nc_proxy_rule)           */
+  double proxy_far_frac;         /*   (patch, multi-member level with grids) pairs evaluated at the    */
+                                 /*   proxies / all such pairs                                         */
 } nc_stats_t;
 
 typedef struct nc_handle nc_handle;
@@ -299,6 +303,19 @@ int nc_pair_mix(int kind, int far, int ctas_per_sm, double* ms, double* warp_pai
  * are split evenly (weights NULL = equal split, as in NC_DIRECT; NC_HIER passes its per-patch work).
  * begin, count: host arrays of `world` entries.  Errors: NC_EINVAL. */
 int nc_split_rows(const double* weights, int64_t N, int world, int64_t* begin, int64_t* count);
+
+/* Host-only helper (no GPU needed): the step-4 proxy rule of NC_HIER handles (R36; PAPER.md:1381-1397,
+ * "evaluate the interpolant ... at the Zernike sampling nodes", carried out for far levels through proxy points).
+ * zhat: host, Kstar x 3 canonical node unit vectors (the tables' zhat).  The proxies are a polar point set on the
+ * node disk of radius h = 1.01 max |(zhat_x, zhat_y)|: the centre plus nring rings at r_k = h cos((k + 1/2) pi /
+ * (2 nring)), max(6, round(cphi r_k / h)) angles each (odd rings offset by half a step), lifted to the unit sphere.
+ * Int maps values at the proxies to the nodes by least squares in the Chebyshev-product basis of total degree <= deg
+ * (it reproduces every such polynomial exactly).  kappa: the smallest D / h (multiples of 1/8 in [1.5, 64]) from
+ * which point sources at distance D h give an interpolation error below tol (relative to max 2/d over the nodes);
+ * HUGE_VAL if none.  Outputs (host): pts (n x 3, nullable), Int (Kstar x n row-major, nullable), kappa, h.
+ * Returns n (> 0) or a negative error code: NC_EINVAL (bad arguments, rank-deficient basis, n > nmax). */
+int nc_proxy_rule(const double* zhat, int Kstar, int deg, int nring, double cphi, double tol, int nmax,
+                  double* pts, double* Int, double* kappa, double* h);
 
 /* world > 1 bootstrap: rank 0 creates the 128-byte NCCL unique id (host buffer), the caller broadcasts it
  * (e.g. torch.distributed) and passes it as nc_opts.nccl_id on every rank.  NC_EUNSUP without NCCL. */

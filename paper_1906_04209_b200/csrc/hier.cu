@@ -103,6 +103,15 @@ struct HierState {
   double* d_node_cs = nullptr;
   double sep_terms = 0.0;           // node x coefficient terms those groups represent (part of interp_terms)
   double interp_lt = 0.0;           // ln(1 / grid tol) for the per-node order truncation of step 4 (R26c; 0: off)
+  // step 4 through patch-local proxies for far levels (R36, proxy.cu)
+  int proxy_n = 0;                  // proxy points per patch (0: every level evaluated at the Zernike nodes)
+  double proxy_kh = 0.0;            // a level is far for a patch when its nearest grid source is >= proxy_kh (arc) away
+  double proxy_kappa = 0.0;         // proxy_kh / h (calibrated, proxy_rule_build)
+  double* d_gdsrc = nullptr;        // per grid: arc from its cap centre to the nearest source node (beta R)
+  double *d_ptx = nullptr, *d_pty = nullptr, *d_ptz = nullptr;   // rc x proxy_n proxy points (scaled by 1/2)
+  double* d_pV = nullptr;           // rc x proxy_n: the far levels' expansions summed at the proxies
+  double* d_pInt = nullptr;         // Ks x proxy_n: proxies -> nodes
+  double proxy_pairs = 0.0, proxy_far = 0.0;   // (patch, level) pairs with grids; of which far (host count)
   FarTable ftab;
   int32_t* d_grid_group = nullptr;
   int64_t* d_ggrid0 = nullptr;
@@ -649,7 +658,8 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
                                                const double* __restrict__ tz, const double* __restrict__ udir,
                                                double* __restrict__ u, const uint8_t* __restrict__ gsep,
                                                int nr_big, double lt, const double* __restrict__ cen,
-                                               int asin_terms, int cap) {
+                                               int asin_terms, int cap, int sel, const double* __restrict__ gdsrc,
+                                               double kh) {
   // MB = 0 evaluates the grids with n_r <= kAngNrMax only (grid_eval_ang); a second pass (MB = 1, nr_big = 1) adds
   // the rest to u when any exists (tight precisions): the register-held accumulators of the first pass then need
   // no fallback code in the same kernel
@@ -676,7 +686,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
       const double* r9 = F + 9 * (int64_t)g;
       for (int e = 0; e < 9; ++e) lv_r9[lvl][e] = r9[e];
       lv_invR[lvl] = gRinv[g];
-      if (asin_terms > 0) {
+      if (asin_terms > 0 || sel != 0) {
         const double cx = cen[3 * i], cy = cen[3 * i + 1], czc = cen[3 * i + 2];
         const double sx = r9[0] * cx + r9[1] * cy + r9[2] * czc;
         const double sy = r9[3] * cx + r9[4] * cy + r9[5] * czc;
@@ -685,6 +695,15 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
         lv_a0[lvl] = atan2(r0, cz);
         lv_r0[lvl] = r0;
         lv_c0[lvl] = cz;
+      }
+      if (sel != 0) {
+        // R36: the level is "far" for this patch when every source of its grids is >= kh (arc) from the patch
+        // centre: (arc from the cap centre to the nearest source node, gdsrc) - (arc of the patch centre) >= kh.
+        // sel 1 keeps the near levels (evaluated at the nodes), sel 2 the far ones (evaluated at the proxies).
+        double dmin = gdsrc[kg0];
+        for (int64_t kg = kg0 + 1; kg < kg1; ++kg) dmin = fmin(dmin, gdsrc[kg]);
+        const bool far = dmin - lv_a0[lvl] >= kh;
+        if (far != (sel == 2)) lv_ng[lvl] = 0;
       }
     }
   }
@@ -936,11 +955,23 @@ __global__ void __launch_bounds__(NT) k_interp_sep(int L, int64_t rc, int Ks, co
     c1[q] = node_cs[2 * k];
     s1[q] = node_cs[2 * k + 1];
   }
+  // the patch's separable levels (group, first and last grid), gathered by one thread per level up front: the level
+  // loop then waits on no dependent global loads (pgl -> gsep -> ggrid0 per level was the kernel's long-scoreboard
+  // stall)
+  __shared__ int sl_g[kLmax + 1];
+  __shared__ int64_t sl_k0[kLmax + 1], sl_k1[kLmax + 1];
+  if ((int)threadIdx.x <= L) {
+    const int g = pgl[(int64_t)threadIdx.x * rc + i];
+    sl_g[threadIdx.x] = gsep[g] ? g : -1;
+    sl_k0[threadIdx.x] = ggrid0[g];
+    sl_k1[threadIdx.x] = ggrid0[g + 1];
+  }
+  __syncthreads();
   for (int lvl = 0; lvl <= L; ++lvl) {
-    const int g = pgl[(int64_t)lvl * rc + i];
-    if (!gsep[g]) continue;                                     // block-uniform
+    const int g = sl_g[lvl];
+    if (g < 0) continue;                                        // block-uniform
     const double invR = 1.0 / gR[g];
-    for (int64_t kg = ggrid0[g]; kg < ggrid0[g + 1]; ++kg) {
+    for (int64_t kg = sl_k0[lvl]; kg < sl_k1[lvl]; ++kg) {
       const int nr = gnr[kg], M = gna[kg] / 2;
       __syncthreads();                                          // previous grid's readers are done
       {
@@ -1022,17 +1053,19 @@ static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t*
                            const double* F, const double* gRinv, const int32_t* gnr, const int32_t* gna,
                            const int64_t* coff, const double* coef, const double* tx, const double* ty,
                            const double* tz, const double* udir, double* u, const uint8_t* gsep, cudaStream_t s,
-                           int nr_big, double lt, const double* cen, int asin_terms) {
+                           int nr_big, double lt, const double* cen, int asin_terms, int sel, const double* gdsrc,
+                           double kh) {
   auto kern = k_interp<NT, NPT, MB, MINB>;
   if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   // shm: the two coefficient buffers (cap = shm / 32 pairs each, 16-byte aligned halves)
   kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
-                                     nr_big, lt, cen, asin_terms, (int)(shm / (2 * sizeof(double2))));
+                                     nr_big, lt, cen, asin_terms, (int)(shm / (2 * sizeof(double2))), sel, gdsrc, kh);
   return NC_OK;
 }
 
 // the instantiated first-pass variants (the default of each K* range, and the alternatives the step-4 tests compare)
-#define NC_INTERP_LIST(X) X(128, 2, 3, 4) X(256, 2, 0, 2) X(128, 2, 0, 4) X(128, 4, 1, 4) X(128, 4, 2, 4)
+#define NC_INTERP_LIST(X) X(128, 2, 3, 4) X(256, 2, 0, 2) X(128, 2, 0, 4) X(128, 4, 1, 4) X(128, 4, 2, 4) \
+  X(96, 1, 3, 6) X(128, 1, 3, 5) X(64, 1, 3, 8)
 static bool interp_listed(const InterpVariant& v) {
 #define NC_I(NT, NPT, MB, MINB) if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB) return true;
   NC_INTERP_LIST(NC_I)
@@ -1044,14 +1077,18 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
                          const int64_t* ggrid0, const double* F, const double* gRinv, const int32_t* gnr,
                          const int32_t* gna, const int64_t* coff, const double* coef, const double* tx,
                          const double* ty, const double* tz, const double* udir, double* u, const uint8_t* gsep,
-                         double lt, const double* cen, int asin_terms, cudaStream_t s) {
+                         double lt, const double* cen, int asin_terms, cudaStream_t s, int sel = 0,
+                         const double* gdsrc = nullptr, double kh = 0.0) {
   (void)namax;
   // defaults: the 248-node rule takes one 128-thread CTA per patch with the coefficient prefetch (MB = 3: rest of
   // the C5 step 20.07 -> 18.32 ms, bitwise-identical output, profiles/r01w_interp_prefetch_c5.jsonl); larger K*
   // the 256-thread angular-sums-first kernel.  NC_INTERP_VARIANT must name a listed variant (else: the default,
   // with a warning -- never a silently skipped first pass)
-  const InterpVariant dflt = Ks <= 256 ? InterpVariant{128, 2, 3, 4} : InterpVariant{256, 2, 0, 2};
-  InterpVariant v = tuning_env("NC_INTERP_VARIANT") ? interp_variant() : dflt;
+  InterpVariant dflt = Ks <= 256 ? InterpVariant{128, 2, 3, 4} : InterpVariant{256, 2, 0, 2};
+  // the proxy pass (sel 2, R36): one point per thread, the CTA the size of the proxy set in whole warps
+  if (sel == 2) dflt = Ks <= 64 ? InterpVariant{64, 1, 3, 8} : Ks <= 96 ? InterpVariant{96, 1, 3, 6}
+                                                             : InterpVariant{128, 1, 3, 5};
+  InterpVariant v = (tuning_env("NC_INTERP_VARIANT") && sel != 2) ? interp_variant() : dflt;
   if (!interp_listed(v)) {
     fprintf(stderr, "[nc] NC_INTERP_VARIANT=%s is not an instantiated variant; using the default\n",
             tuning_env("NC_INTERP_VARIANT"));
@@ -1063,12 +1100,12 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
 #define NC_I(NT, NPT, MB, MINB)                                                                                  \
   if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                                \
     NC_TRY((launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx,   \
-                                               ty, tz, udir, u, gsep, s, 0, lt, cen, asin_terms)));
+                                               ty, tz, udir, u, gsep, s, 0, lt, cen, asin_terms, sel, gdsrc, kh)));
   NC_INTERP_LIST(NC_I)
 #undef NC_I
   if (two_pass)
     return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx, ty, tz, udir,
-                                         u, gsep, s, 1, 0.0, cen, asin_terms);
+                                         u, gsep, s, 1, 0.0, cen, asin_terms, sel, gdsrc, kh);
   return NC_OK;
 }
 
@@ -1306,6 +1343,66 @@ int hier_order(nc_handle* h, std::vector<double>& centers) {
   for (int64_t i = 0; i < N; ++i)
     for (int d = 0; d < 3; ++d) sorted[3 * i + d] = centers[3 * perm[i] + d];
   centers.swap(sorted);
+  return NC_OK;
+}
+
+// Step 4 through proxies (R36, proxy.cu): the rule for the tables' nodes, its far-level threshold, the per-grid
+// nearest-source arcs, the proxies of every local patch and the buffers of the proxy pass.  Off (proxy_n = 0) with
+// NC_PROXY=0 (tuning), when the rule cannot be built, when it never meets its tolerance, or when it would not save
+// evaluations (n >= K* / 2).  The rule's tolerance is kProxyTolFactor x the grids' own (NC_PROXY_TOL overrides).
+constexpr double kProxyTolFactor = 0.01;
+template <class Plan>
+static int proxy_setup(nc_handle* h, HierState* H, const std::vector<Plan>& plans, const std::vector<int32_t>& pgl,
+                       const std::vector<double>& cen, double tol, cudaStream_t s) {
+  const int Ks = h->Kstar;
+  const int64_t rc = h->row_count, rb = h->row_begin;
+  H->proxy_n = 0;
+  if (const char* e = tuning_env("NC_PROXY"))
+    if (e[0] == '0') return NC_OK;
+  int deg = 11, nring = 6;
+  double cphi = 24.0, tf = kProxyTolFactor;
+  if (const char* e = tuning_env("NC_PROXY_RULE")) sscanf(e, "%d,%d,%lf", &deg, &nring, &cphi);
+  if (const char* e = tuning_env("NC_PROXY_TOL")) tf = atof(e);
+  std::vector<double> z;
+  NC_TRY(download(z, h->d_zhat, (size_t)3 * Ks, s));
+  std::vector<double> pts, Int;
+  double kappa = HUGE_VAL, hh = 0.0;
+  const int n = proxy_rule_build(z.data(), Ks, deg, nring, cphi, tf * tol, pts, Int, &kappa, &hh);
+  if (n <= 0 || !(kappa < HUGE_VAL) || 2 * n > Ks || (n & 1) || rc <= 0) return NC_OK;
+  H->proxy_n = n;
+  H->proxy_kappa = kappa;
+  H->proxy_kh = kappa * hh;
+  std::vector<double> gd(std::max<size_t>(plans.size(), 1), 0.0);
+  for (size_t k = 0; k < plans.size(); ++k) gd[k] = plans[k].beta * H->gR[plans[k].group];
+  NC_TRY(upload(h, &H->d_gdsrc, gd, s));
+  NC_TRY(upload(h, &H->d_pInt, Int, s));
+  double* d_ph = nullptr;
+  NC_TRY(upload(h, &d_ph, pts, s));
+  NC_TRY(halloc(h, &H->d_ptx, rc * n));
+  NC_TRY(halloc(h, &H->d_pty, rc * n));
+  NC_TRY(halloc(h, &H->d_ptz, rc * n));
+  NC_TRY(halloc(h, &H->d_pV, rc * n));
+  launch_targets(h->d_frames, rb, rc, d_ph, n, 0.5, H->d_ptx, H->d_pty, H->d_ptz, s);
+  NC_CUDA_TRY(cudaStreamSynchronize(s));
+  cudaFree(d_ph);
+  // host count of the far (patch, level) pairs (stats only; the kernels decide on the device by the same rule)
+  const int L = H->L;
+  double npair = 0.0, nfar = 0.0;
+  for (int lvl = 0; lvl <= L; ++lvl)
+    for (int64_t i = 0; i < rc; ++i) {
+      const int32_t g = pgl[(size_t)lvl * rc + i];
+      const int64_t kg0 = H->ggrid0[g], kg1 = H->ggrid0[g + 1];
+      if (kg0 == kg1 || H->gnr[kg0] == 0 || H->glast[g] - H->gfirst[g] == 1) continue;
+      double dmin = HUGE_VAL;
+      for (int64_t kg = kg0; kg < kg1; ++kg) dmin = std::min(dmin, gd[kg]);
+      npair += 1.0;
+      nfar += dmin - harc(&H->gc[3 * (int64_t)g], &cen[3 * (rb + i)]) >= H->proxy_kh;
+    }
+  H->proxy_pairs = npair;
+  H->proxy_far = nfar;
+  if (getenv("NC_HIER_DIAG"))
+    fprintf(stderr, "[nc hier diag] step-4 proxies: n %d (deg %d), kappa %.3f (h %.3g), far levels %.0f of %.0f\n", n,
+            deg, kappa, hh, nfar, npair);
   return NC_OK;
 }
 
@@ -2118,6 +2215,7 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
                                                                H->d_gna, H->d_goff, H->d_rbase, H->d_roff, H->d_gx,
                                                                H->d_gy, H->d_gz);
   launch_targets(h->d_frames, rb, rc, h->d_zhat, Ks, 0.5, H->d_tx, H->d_ty, H->d_tz, s);
+  NC_TRY(proxy_setup(h, H, plans, pgl, cen, tol, s));
   NC_CUDA_TRY(cudaGetLastError());
   h->pairs_per_matvec = H->pairs_grid + H->pairs_near;
   return NC_OK;
@@ -2159,10 +2257,21 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   if (rc > 0) {
     // two buffers for all grids of one group (cgroupmax doubles, even: pairs)
     const size_t shm = 2 * (size_t)std::max(H->cgroupmax, 2) * sizeof(double);
+    const int np = H->proxy_n;
+    // near levels (all levels without proxies) at the Zernike nodes, on top of the near-list sums
     NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
                          H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u,
-                         H->d_gsep, H->interp_lt, h->d_centers + 3 * h->row_begin, H->asin_terms, s));
+                         H->d_gsep, H->interp_lt, h->d_centers + 3 * h->row_begin, H->asin_terms, s, np ? 1 : 0,
+                         H->d_gdsrc, H->proxy_kh));
     h->launches_last++;
+    if (np) {   // far levels at the proxies, then u += V Int^T (R36)
+      NC_TRY(launch_interp(shm, H->L, rc, np, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
+                           H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_ptx, H->d_pty, H->d_ptz, nullptr, H->d_pV,
+                           H->d_gsep, H->interp_lt, h->d_centers + 3 * h->row_begin, H->asin_terms, s, 2,
+                           H->d_gdsrc, H->proxy_kh));
+      launch_gemm_dmma(H->d_pV, np, 1, 0, H->d_pInt, rc, Ks, np, H->d_u, Ks, 1, H->d_u, Ks, s);
+      h->launches_last += 2;
+    }
   }
   if (H->nwork_sep) {   // single-member groups, separably (adds to u)
     const int Mmax = H->namax / 2, cpairs = std::max(H->cmax / 2, 1);
@@ -2198,6 +2307,9 @@ void hier_fill_stats(const nc_handle* h, nc_stats_t* o) {
   o->hier_grid_warp_fill = H->warp_slot_pairs > 0 ? H->pairs_grid / H->warp_slot_pairs : 0.0;
   hier_grid_variant(h, o->grid_variant);
   o->hier_unit_points = H->unit_points;
+  o->proxy_n = H->proxy_n;
+  o->proxy_kappa = H->proxy_kappa;
+  o->proxy_far_frac = H->proxy_pairs > 0 ? H->proxy_far / H->proxy_pairs : 0.0;
 }
 
 int hier_grid_far(const nc_handle* h) { return h->hier ? h->hier->gv.far : -1; }
@@ -2215,7 +2327,7 @@ void hier_destroy(nc_handle* h) {
                   H->d_node_ring, H->d_node_cs,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
                   H->d_chunks, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
-                  H->d_udir, H->d_u};
+                  H->d_udir, H->d_u, H->d_gdsrc, H->d_ptx, H->d_pty, H->d_ptz, H->d_pV, H->d_pInt};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete H;

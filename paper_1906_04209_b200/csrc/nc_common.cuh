@@ -196,6 +196,9 @@ namespace nc {
 // frames R_i (ABI rule) and global node sets
 void launch_frames(const double* centers, int64_t N, double* frames, cudaStream_t s);
 // (coordinates written pre-multiplied by `scale`; the pair kernels use scale = 1/2, see green.cuh)
+// step-4 proxy rule (proxy.cu, R36): returns n (0: none); pts n x 3, Int Ks x n, kappa (min D / h), h
+int proxy_rule_build(const double* zhat, int Ks, int deg, int nring, double cphi, double tol, std::vector<double>& pts,
+                     std::vector<double>& Int, double* kappa, double* h_out);
 void launch_targets(const double* frames, int64_t row_begin, int64_t row_count, const double* zhat, int Kstar,
                     double scale, double* tx, double* ty, double* tz, cudaStream_t s);
 void launch_sources(const double* frames, int64_t N, const double* shat, int p, double scale, double* src4,

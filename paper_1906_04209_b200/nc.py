@@ -60,12 +60,13 @@ class NcStats(ctypes.Structure):
                 ("pair_fp64_flops_direct", ctypes.c_double), ("pair_fp64_inst_direct", ctypes.c_double),
                 ("pair_fp64_flops_grid", ctypes.c_double), ("pair_fp64_inst_grid", ctypes.c_double),
                 ("hier_grid_fill", ctypes.c_double), ("hier_grid_warp_fill", ctypes.c_double),
-                ("grid_variant", ctypes.c_int32 * 8), ("hier_unit_points", ctypes.c_double)]
+                ("grid_variant", ctypes.c_int32 * 8), ("hier_unit_points", ctypes.c_double),
+                ("proxy_n", ctypes.c_int32), ("proxy_kappa", ctypes.c_double), ("proxy_far_frac", ctypes.c_double)]
 
 
 EXPORTS = ["nc_setup", "nc_partition", "nc_matvec", "nc_matvec_emulated", "nc_matvec_host", "nc_gmres", "nc_flux_or_mfpt",
            "nc_field", "nc_field_near", "nc_residual", "nc_density", "nc_id_sketch", "nc_modal_kernels", "nc_stats",
-           "nc_time_stages", "nc_tree_lists", "nc_near_counts", "nc_pair_mix", "nc_split_rows", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
+           "nc_time_stages", "nc_tree_lists", "nc_near_counts", "nc_pair_mix", "nc_split_rows", "nc_proxy_rule", "nc_nccl_unique_id", "nc_destroy", "nc_last_error", "nc_version"]
 
 _lib = None
 
@@ -101,6 +102,8 @@ def load_library(path: str = LIB_PATH):
     L.nc_near_counts.argtypes = [vp, _i64p]
     L.nc_pair_mix.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _dp]
     L.nc_split_rows.argtypes = [_dp, ctypes.c_int64, ctypes.c_int, _i64p, _i64p]
+    L.nc_proxy_rule.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                ctypes.c_int, _dp, _dp, _dp, _dp]
     L.nc_nccl_unique_id.argtypes = [vp]
     L.nc_destroy.argtypes = [vp]
     L.nc_destroy.restype = None
@@ -133,6 +136,24 @@ def split_rows(N: int, world: int, weights=None):
     _check(L.nc_split_rows(w.ctypes.data_as(_dp) if w is not None else None, int(N), int(world),
                            b.ctypes.data_as(_i64p), c.ctypes.data_as(_i64p)))
     return b, c
+
+
+def proxy_rule(zhat, deg: int = 11, nring: int = 6, cphi: float = 24.0, tol: float = 1e-8):
+    """Host-only: the step-4 proxy rule for the nodes zhat (nc_proxy_rule, R36) -> (pts n x 3,
+    Int Kstar x n, kappa, h)."""
+    L = load_library()
+    z = np.ascontiguousarray(zhat, dtype=np.float64)
+    ks = z.shape[0]
+    nmax = 4096
+    pts = np.zeros((nmax, 3))
+    Int = np.zeros(ks * nmax)
+    kap = ctypes.c_double()
+    h = ctypes.c_double()
+    n = L.nc_proxy_rule(z.ctypes.data_as(_dp), ks, int(deg), int(nring), float(cphi), float(tol), nmax,
+                        pts.ctypes.data_as(_dp), Int.ctypes.data_as(_dp), ctypes.byref(kap), ctypes.byref(h))
+    if n < 0:
+        _check(n)
+    return pts[:n].copy(), Int[:ks * n].reshape(ks, n).copy(), kap.value, h.value
 
 
 def id_sketch(kind: int, train, fine, omega, device: int = 0) -> np.ndarray:

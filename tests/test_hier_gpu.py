@@ -192,10 +192,10 @@ def test_step4_evaluation_variants_agree(tmp_path, env):
     import subprocess
     import sys
     outs = []
-    for e in ({}, env):   # the per-node order truncation (R26c) off in both: the same expansion, evaluated two ways
-        out = str(tmp_path / f"y{len(outs)}.npy")
+    for e in ({}, env):   # the per-node order truncation (R26c) and the proxies (R36) off in both: the same
+        out = str(tmp_path / f"y{len(outs)}.npy")   # expansion at the same nodes, evaluated two ways
         subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(os.environ, NC_TUNING="1", ROOT=ROOT, OUT=out, NC_INTERP_TRUNC="0",
-                                                                    **e), check=True, timeout=600)
+                                                                    NC_PROXY="0", **e), check=True, timeout=600)
         outs.append(np.load(out))
     assert rel(outs[1], outs[0]) <= 1e-13
 
@@ -211,6 +211,34 @@ def test_step4_order_truncation_below_tolerance(tmp_path):
         subprocess.run([sys.executable, "-c", _FAR_CHILD], env=dict(os.environ, NC_TUNING="1", ROOT=ROOT, OUT=out, NC_INTERP_TRUNC=v),
                        check=True, timeout=600)
         outs.append(np.load(out))
+    assert rel(outs[1], outs[0]) <= 1e-10
+
+
+_PROXY_CHILD = _FAR_CHILD + r"""
+import json
+st = h.stats()
+json.dump({k: st[k] for k in ("proxy_n", "proxy_kappa", "proxy_far_frac")}, open(os.environ["OUT"] + ".json", "w"))
+"""
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+def test_step4_proxies_agree_with_nodes(tmp_path, cfg):
+    """DESIGN.md R36: the far levels of step 4 evaluated at the patch's proxy points and carried to the Zernike nodes
+    by the proxy rule's matrix, against every level evaluated at the nodes (NC_PROXY=0, the paper's literal step 4,
+    PAPER.md:1381-1397): the two matvecs differ by far less than the requested precision (1e-9), and the proxies are
+    in use on a large share of the (patch, level) pairs."""
+    import json
+    import subprocess
+    import sys
+    outs, stats = [], []
+    for e in ({"NC_PROXY": "0"}, {}):
+        out = str(tmp_path / f"y{len(outs)}.npy")
+        subprocess.run([sys.executable, "-c", _PROXY_CHILD],
+                       env=dict(os.environ, NC_TUNING="1", ROOT=ROOT, OUT=out, CFG=cfg, **e), check=True, timeout=900)
+        outs.append(np.load(out))
+        stats.append(json.load(open(out + ".json")))
+    assert stats[0]["proxy_n"] == 0
+    assert stats[1]["proxy_n"] > 0 and stats[1]["proxy_far_frac"] > 0.3, stats[1]
     assert rel(outs[1], outs[0]) <= 1e-10
 
 

@@ -9,7 +9,7 @@ timeout 900 python bench.py --no-cpu-baseline > gpurun_out/${T}_bench.json 2> gp
 python -c "import json;d=json.loads(open('gpurun_out/${T}_bench.json').read().strip().splitlines()[-1]);print('bench',d['value'],d['e2e']['value'],d['stages_ms'])"
 if [ -n "$KR" ]; then
   CMD="python bench.py --steps 1 --warmup 1 --no-solve --no-cpu-baseline"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$KR -s 1 -c 1 -o gpurun_out/${T}_prof $CMD > gpurun_out/${T}_ncu_full.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$KR -s ${NCU_SKIP:-1} -c 1 -o gpurun_out/${T}_prof $CMD > gpurun_out/${T}_ncu_full.log 2>&1
   echo "ncu rc=$?"
 fi
 echo done
