@@ -107,7 +107,9 @@ struct HierState {
   int proxy_n = 0;                  // proxy points per patch (0: every level evaluated at the Zernike nodes)
   double proxy_kh = 0.0;            // a level is far for a patch when its nearest grid source is >= proxy_kh (arc) away
   double proxy_kappa = 0.0;         // proxy_kh / h (calibrated, proxy_rule_build)
-  double* d_gdsrc = nullptr;        // per grid: arc from its cap centre to the nearest source node (beta R)
+  uint32_t* d_pfar = nullptr;       // per local patch: bit lvl set when level lvl is evaluated at the proxies
+  int32_t* d_pwork1 = nullptr;      // local patches with a level evaluated at the nodes (the first pass's CTAs)
+  int64_t npwork1 = 0;
   double *d_ptx = nullptr, *d_pty = nullptr, *d_ptz = nullptr;   // rc x proxy_n proxy points (scaled by 1/2)
   double* d_pV = nullptr;           // rc x proxy_n: the far levels' expansions summed at the proxies
   double* d_pInt = nullptr;         // Ks x proxy_n: proxies -> nodes
@@ -658,8 +660,8 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
                                                const double* __restrict__ tz, const double* __restrict__ udir,
                                                double* __restrict__ u, const uint8_t* __restrict__ gsep,
                                                int nr_big, double lt, const double* __restrict__ cen,
-                                               int asin_terms, int cap, int sel, const double* __restrict__ gdsrc,
-                                               double kh) {
+                                               int asin_terms, int cap, int sel, const uint32_t* __restrict__ pfar,
+                                               const int32_t* __restrict__ work) {
   // MB = 0 evaluates the grids with n_r <= kAngNrMax only (grid_eval_ang); a second pass (MB = 1, nr_big = 1) adds
   // the rest to u when any exists (tight precisions): the register-held accumulators of the first pass then need
   // no fallback code in the same kernel
@@ -670,12 +672,15 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
   __shared__ double lv_a0[kLmax + 1], lv_r0[kLmax + 1], lv_c0[kLmax + 1], lv_invR[kLmax + 1], lv_r9[kLmax + 1][9];
   __shared__ int64_t lv_coff[kLmax + 1][kMaxGrids];
   __shared__ int lv_ng[kLmax + 1], lv_nr[kLmax + 1][kMaxGrids], lv_M[kLmax + 1][kMaxGrids];
-  const int64_t i = blockIdx.x;
+  const int64_t i = work ? work[blockIdx.x] : blockIdx.x;
   if ((int)threadIdx.x <= L) {
     const int lvl = threadIdx.x;
     const int g = pgl[(int64_t)lvl * rc + i];
     const int64_t kg0 = ggrid0[g], kg1 = ggrid0[g + 1];
-    const bool ok = kg0 != kg1 && gnr[kg0] != 0 && !(gsep && gsep[g]);
+    // R36: sel 1 keeps the levels evaluated at the nodes, sel 2 the far levels evaluated at the proxies (bit lvl of
+    // pfar[i], decided once on the host: both passes see the same split)
+    const bool keep = sel == 0 || (((pfar[i] >> lvl) & 1u) != 0) == (sel == 2);
+    const bool ok = keep && kg0 != kg1 && gnr[kg0] != 0 && !(gsep && gsep[g]);
     lv_ng[lvl] = ok ? (int)(kg1 - kg0) : 0;
     if (ok) {
       for (int64_t kg = kg0; kg < kg1; ++kg) {
@@ -686,7 +691,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
       const double* r9 = F + 9 * (int64_t)g;
       for (int e = 0; e < 9; ++e) lv_r9[lvl][e] = r9[e];
       lv_invR[lvl] = gRinv[g];
-      if (asin_terms > 0 || sel != 0) {
+      if (asin_terms > 0) {
         const double cx = cen[3 * i], cy = cen[3 * i + 1], czc = cen[3 * i + 2];
         const double sx = r9[0] * cx + r9[1] * cy + r9[2] * czc;
         const double sy = r9[3] * cx + r9[4] * cy + r9[5] * czc;
@@ -695,15 +700,6 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
         lv_a0[lvl] = atan2(r0, cz);
         lv_r0[lvl] = r0;
         lv_c0[lvl] = cz;
-      }
-      if (sel != 0) {
-        // R36: the level is "far" for this patch when every source of its grids is >= kh (arc) from the patch
-        // centre: (arc from the cap centre to the nearest source node, gdsrc) - (arc of the patch centre) >= kh.
-        // sel 1 keeps the near levels (evaluated at the nodes), sel 2 the far ones (evaluated at the proxies).
-        double dmin = gdsrc[kg0];
-        for (int64_t kg = kg0 + 1; kg < kg1; ++kg) dmin = fmin(dmin, gdsrc[kg]);
-        const bool far = dmin - lv_a0[lvl] >= kh;
-        if (far != (sel == 2)) lv_ng[lvl] = 0;
       }
     }
   }
@@ -1053,13 +1049,15 @@ static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t*
                            const double* F, const double* gRinv, const int32_t* gnr, const int32_t* gna,
                            const int64_t* coff, const double* coef, const double* tx, const double* ty,
                            const double* tz, const double* udir, double* u, const uint8_t* gsep, cudaStream_t s,
-                           int nr_big, double lt, const double* cen, int asin_terms, int sel, const double* gdsrc,
-                           double kh) {
+                           int nr_big, double lt, const double* cen, int asin_terms, int sel, const uint32_t* pfar,
+                           const int32_t* work, int64_t nblocks) {
   auto kern = k_interp<NT, NPT, MB, MINB>;
   if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   // shm: the two coefficient buffers (cap = shm / 32 pairs each, 16-byte aligned halves)
-  kern<<<(unsigned)rc, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx, ty, tz, udir, u, gsep,
-                                     nr_big, lt, cen, asin_terms, (int)(shm / (2 * sizeof(double2))), sel, gdsrc, kh);
+  if (nblocks <= 0) return NC_OK;
+  kern<<<(unsigned)nblocks, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx, ty, tz, udir, u,
+                                          gsep, nr_big, lt, cen, asin_terms, (int)(shm / (2 * sizeof(double2))), sel,
+                                          pfar, work);
   return NC_OK;
 }
 
@@ -1078,7 +1076,8 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
                          const int32_t* gna, const int64_t* coff, const double* coef, const double* tx,
                          const double* ty, const double* tz, const double* udir, double* u, const uint8_t* gsep,
                          double lt, const double* cen, int asin_terms, cudaStream_t s, int sel = 0,
-                         const double* gdsrc = nullptr, double kh = 0.0) {
+                         const uint32_t* pfar = nullptr, const int32_t* work = nullptr, int64_t nwork = -1) {
+  const int64_t nb = work ? nwork : rc;   // CTAs: one per patch of the work list (all local patches without one)
   (void)namax;
   // defaults: the 248-node rule takes one 128-thread CTA per patch with the coefficient prefetch (MB = 3: rest of
   // the C5 step 20.07 -> 18.32 ms, bitwise-identical output, profiles/r01w_interp_prefetch_c5.jsonl); larger K*
@@ -1100,12 +1099,12 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
 #define NC_I(NT, NPT, MB, MINB)                                                                                  \
   if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB)                                                \
     NC_TRY((launch_interp_t<NT, NPT, MB, MINB>(shm, L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx,   \
-                                               ty, tz, udir, u, gsep, s, 0, lt, cen, asin_terms, sel, gdsrc, kh)));
+                                               ty, tz, udir, u, gsep, s, 0, lt, cen, asin_terms, sel, pfar, work, nb)));
   NC_INTERP_LIST(NC_I)
 #undef NC_I
   if (two_pass)
     return launch_interp_t<128, 4, 1, 4>(shm, L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx, ty, tz, udir,
-                                         u, gsep, s, 1, 0.0, cen, asin_terms, sel, gdsrc, kh);
+                                         u, gsep, s, 1, 0.0, cen, asin_terms, sel, pfar, work, nb);
   return NC_OK;
 }
 
@@ -1350,7 +1349,7 @@ int hier_order(nc_handle* h, std::vector<double>& centers) {
 // nearest-source arcs, the proxies of every local patch and the buffers of the proxy pass.  Off (proxy_n = 0) with
 // NC_PROXY=0 (tuning), when the rule cannot be built, when it never meets its tolerance, or when it would not save
 // evaluations (n >= K* / 2).  The rule's tolerance is kProxyTolFactor x the grids' own (NC_PROXY_TOL overrides).
-constexpr double kProxyTolFactor = 0.01;
+constexpr double kProxyTolFactor = 0.1;
 template <class Plan>
 static int proxy_setup(nc_handle* h, HierState* H, const std::vector<Plan>& plans, const std::vector<int32_t>& pgl,
                        const std::vector<double>& cen, double tol, cudaStream_t s) {
@@ -1359,7 +1358,7 @@ static int proxy_setup(nc_handle* h, HierState* H, const std::vector<Plan>& plan
   H->proxy_n = 0;
   if (const char* e = tuning_env("NC_PROXY"))
     if (e[0] == '0') return NC_OK;
-  int deg = 11, nring = 6;
+  int deg = 8, nring = 4;   // 64 proxies (profiles/r02w_proxy_sweep.jsonl: the fastest of the rules swept, same error)
   double cphi = 24.0, tf = kProxyTolFactor;
   if (const char* e = tuning_env("NC_PROXY_RULE")) sscanf(e, "%d,%d,%lf", &deg, &nring, &cphi);
   if (const char* e = tuning_env("NC_PROXY_TOL")) tf = atof(e);
@@ -1372,9 +1371,10 @@ static int proxy_setup(nc_handle* h, HierState* H, const std::vector<Plan>& plan
   H->proxy_n = n;
   H->proxy_kappa = kappa;
   H->proxy_kh = kappa * hh;
+  // per grid: arc from its cap centre to the nearest source node, beta R = d - eps (R12/R21: the skeleton lies within
+  // eps of its patch centre), so a patch centre at arc a0 from the cap centre is >= beta R - a0 from every source
   std::vector<double> gd(std::max<size_t>(plans.size(), 1), 0.0);
   for (size_t k = 0; k < plans.size(); ++k) gd[k] = plans[k].beta * H->gR[plans[k].group];
-  NC_TRY(upload(h, &H->d_gdsrc, gd, s));
   NC_TRY(upload(h, &H->d_pInt, Int, s));
   double* d_ph = nullptr;
   NC_TRY(upload(h, &d_ph, pts, s));
@@ -1385,21 +1385,37 @@ static int proxy_setup(nc_handle* h, HierState* H, const std::vector<Plan>& plan
   launch_targets(h->d_frames, rb, rc, d_ph, n, 0.5, H->d_ptx, H->d_pty, H->d_ptz, s);
   NC_CUDA_TRY(cudaStreamSynchronize(s));
   cudaFree(d_ph);
-  // host count of the far (patch, level) pairs (stats only; the kernels decide on the device by the same rule)
+  // the split, once, on the host: bit lvl of pfar[i] when patch i's level-lvl group has grids whose every source is
+  // >= kappa h from the patch centre (single-member groups stay with k_interp_sep when that pass is on)
   const int L = H->L;
+  std::vector<uint32_t> pfar(rc, 0u);
+  std::vector<int32_t> work1;
   double npair = 0.0, nfar = 0.0;
-  for (int lvl = 0; lvl <= L; ++lvl)
-    for (int64_t i = 0; i < rc; ++i) {
+  for (int64_t i = 0; i < rc; ++i) {
+    bool near_level = false;
+    for (int lvl = 0; lvl <= L; ++lvl) {
       const int32_t g = pgl[(size_t)lvl * rc + i];
       const int64_t kg0 = H->ggrid0[g], kg1 = H->ggrid0[g + 1];
-      if (kg0 == kg1 || H->gnr[kg0] == 0 || H->glast[g] - H->gfirst[g] == 1) continue;
+      if (kg0 == kg1 || H->gnr[kg0] == 0) continue;
+      if (H->sep_nodes && H->glast[g] - H->gfirst[g] == 1) continue;   // k_interp_sep's
       double dmin = HUGE_VAL;
       for (int64_t kg = kg0; kg < kg1; ++kg) dmin = std::min(dmin, gd[kg]);
       npair += 1.0;
-      nfar += dmin - harc(&H->gc[3 * (int64_t)g], &cen[3 * (rb + i)]) >= H->proxy_kh;
+      if (dmin - harc(&H->gc[3 * (int64_t)g], &cen[3 * (rb + i)]) >= H->proxy_kh) {
+        pfar[i] |= 1u << lvl;
+        nfar += 1.0;
+      } else {
+        near_level = true;
+      }
     }
+    if (near_level) work1.push_back((int32_t)i);
+  }
   H->proxy_pairs = npair;
   H->proxy_far = nfar;
+  H->npwork1 = (int64_t)work1.size();
+  NC_TRY(upload(h, &H->d_pfar, pfar, s));
+  if (work1.empty()) work1.push_back(0);
+  NC_TRY(upload(h, &H->d_pwork1, work1, s));
   if (getenv("NC_HIER_DIAG"))
     fprintf(stderr, "[nc hier diag] step-4 proxies: n %d (deg %d), kappa %.3f (h %.3g), far levels %.0f of %.0f\n", n,
             deg, kappa, hh, nfar, npair);
@@ -2258,19 +2274,21 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
     // two buffers for all grids of one group (cgroupmax doubles, even: pairs)
     const size_t shm = 2 * (size_t)std::max(H->cgroupmax, 2) * sizeof(double);
     const int np = H->proxy_n;
-    // near levels (all levels without proxies) at the Zernike nodes, on top of the near-list sums
-    NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
-                         H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u,
-                         H->d_gsep, H->interp_lt, h->d_centers + 3 * h->row_begin, H->asin_terms, s, np ? 1 : 0,
-                         H->d_gdsrc, H->proxy_kh));
-    h->launches_last++;
-    if (np) {   // far levels at the proxies, then u += V Int^T (R36)
+    const double* cen = h->d_centers + 3 * h->row_begin;
+    if (!np) {   // every level at the Zernike nodes, on top of the near-list sums
+      NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
+                           H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u,
+                           H->d_gsep, H->interp_lt, cen, H->asin_terms, s));
+      h->launches_last++;
+    } else {     // R36: far levels at the proxies; u = udir + V Int^T; then the other levels at the nodes, in place
       NC_TRY(launch_interp(shm, H->L, rc, np, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
                            H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_ptx, H->d_pty, H->d_ptz, nullptr, H->d_pV,
-                           H->d_gsep, H->interp_lt, h->d_centers + 3 * h->row_begin, H->asin_terms, s, 2,
-                           H->d_gdsrc, H->proxy_kh));
-      launch_gemm_dmma(H->d_pV, np, 1, 0, H->d_pInt, rc, Ks, np, H->d_u, Ks, 1, H->d_u, Ks, s);
-      h->launches_last += 2;
+                           H->d_gsep, H->interp_lt, cen, H->asin_terms, s, 2, H->d_pfar));
+      launch_gemm_dmma(H->d_pV, np, 1, 0, H->d_pInt, rc, Ks, np, H->d_u, Ks, 1, H->d_udir, Ks, s);
+      NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
+                           H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_u, H->d_u,
+                           H->d_gsep, H->interp_lt, cen, H->asin_terms, s, 1, H->d_pfar, H->d_pwork1, H->npwork1));
+      h->launches_last += 2 + (H->npwork1 > 0);
     }
   }
   if (H->nwork_sep) {   // single-member groups, separably (adds to u)
@@ -2327,7 +2345,7 @@ void hier_destroy(nc_handle* h) {
                   H->d_node_ring, H->d_node_cs,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
                   H->d_chunks, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
-                  H->d_udir, H->d_u, H->d_gdsrc, H->d_ptx, H->d_pty, H->d_ptz, H->d_pV, H->d_pInt};
+                  H->d_udir, H->d_u, H->d_pfar, H->d_pwork1, H->d_ptx, H->d_pty, H->d_ptz, H->d_pV, H->d_pInt};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete H;

@@ -138,7 +138,7 @@ def split_rows(N: int, world: int, weights=None):
     return b, c
 
 
-def proxy_rule(zhat, deg: int = 11, nring: int = 6, cphi: float = 24.0, tol: float = 1e-8):
+def proxy_rule(zhat, deg: int = 8, nring: int = 4, cphi: float = 24.0, tol: float = 1e-7):
     """Host-only: the step-4 proxy rule for the nodes zhat (nc_proxy_rule, R36) -> (pts n x 3,
     Int Kstar x n, kappa, h)."""
     L = load_library()

@@ -1,6 +1,6 @@
 """Per-region instruction / stall-sample profile of one kernel from an ncu report (SASS source page).
 
-    python tools/ncu_sass_profile.py <prof.ncu-rep> [top]
+    python tools/ncu_sass_profile.py <prof.ncu-rep> [top] [kernel-name-substring]
 Prints the loops (backward branches) with their executed warp instructions and stall samples, and the top
 instructions by samples.
 """
@@ -11,10 +11,16 @@ import subprocess
 import sys
 
 
-def rows(rep):
+def rows(rep, kernel=None):
+    """SASS rows of the first captured kernel whose name contains `kernel` (default: the first kernel)."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                          text=True).stdout
     lines = out.splitlines()
+    starts = [i for i, l in enumerate(lines) if l.startswith('"Kernel Name"')] + [len(lines)]
+    sec = 0
+    if kernel:
+        sec = [k for k in range(len(starts) - 1) if kernel in lines[starts[k]]][0]
+    lines = lines[starts[sec] + 1:starts[sec + 1]]
     hi = [i for i, l in enumerate(lines) if l.startswith('"Address"')][0]
     rd = list(csv.reader(io.StringIO("\n".join(lines[hi:]))))
     h = rd[0]
@@ -34,7 +40,7 @@ def rows(rep):
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-    R = rows(rep)
+    R = rows(rep, sys.argv[3] if len(sys.argv) > 3 else None)
     base = R[0][0]
     tot_s = sum(r[2] for r in R)
     tot_i = sum(r[3] for r in R)
