@@ -389,9 +389,13 @@ def main():
                 gbs = b / (ms * 1e-3) / 1e9
                 hbm_stages[name] = {"bytes": b, "ms": ms, "achieved": gbs, "unit": "GB/s", "peak": hbm,
                                     "frac": gbs / hbm if hbm else None}
-        hbm_stages["note"] = ("algorithmic bytes: k_reduce_chunks reads every work unit's partial values and writes "
-                              "the grid values; K1 reads X and the rungs' T and writes rho (8 B per record, scattered "
-                              "into 32-B records); peak = MEASURED_PEAKS.json hbm_gbs")
+        if stages_avg[7] < 1e-3:
+            hbm_stages["grid_reduce"] = ("fused into k_transform_w (R37): each warp sums its grid's partial values "
+                                         "straight into shared memory; %.3g GB of partials read per matvec, timed "
+                                         "inside hier_rest" % (8.0 * st["hier_unit_points"] / 1e9))
+        hbm_stages["note"] = ("algorithmic bytes: the grid reduction reads every work unit's partial values and writes "
+                              "the grid values; K1 reads X and the rungs' T and writes rho compactly (8 B per value); "
+                              "peak = MEASURED_PEAKS.json hbm_gbs")
     # NEXT-3: the field of the solution on the sphere of radius 1 -+ eps/5, where the paper plots the MFPT (PAPER.md:2069-2097,
     # Fig. sphereplots): nc_field_near (host points in, values and v-bar out, synchronous; the patches within 4 eps of a
     # point from their density, the others from their compressed skeleton), Fibonacci points

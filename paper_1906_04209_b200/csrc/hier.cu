@@ -126,6 +126,8 @@ struct HierState {
   double* d_part = nullptr;
   ChunkRec* d_chunks = nullptr;
   int64_t nchunks = 0;
+  int64_t* d_gch0 = nullptr;        // per grid: first chunk (NG + 1)
+  bool fuse_reduce = false;         // k_transform_w sums the partials itself (no k_reduce_chunks, no grid values)
   int32_t* d_work_near = nullptr;
   int64_t nwork_near = 0;
   int64_t* d_near_off = nullptr;
@@ -523,6 +525,135 @@ __global__ void k_transform(const int32_t* __restrict__ grids, int64_t ngr, cons
     s *= 2.0 / nr;
     if (n == 0) s *= 0.5;
     coef[coff[g] + t] = s;
+  }
+}
+
+// Warp-per-grid variant of step 4a (default, round 2): the same coefficients, with the Fourier sums of each ring by
+// Clenshaw's recurrence instead of tabulated twiddles (R37):
+//   b_l = f_l + 2 cos(w) b_{l+1} - b_{l+2}  (l = n_a - 1 .. 0, b_{n_a} = b_{n_a + 1} = 0),  w = 2 pi m / n_a(k),
+//   sum_l f_l cos(l w) = b_0 - cos(w) b_1,   sum_l f_l sin(l w) = sin(w) b_1,
+// 2 FP64 per (sample, order) and one broadcast shared-memory read, no per-sample index arithmetic; (cos w, sin w) from
+// the long-double twiddle table.  Each warp transforms one grid with no CTA barrier (the CTA-per-grid kernel above
+// spent its time on barriers and per-sample gathers: FP64 pipe 13%, profiles/r02o_ncu_full_transform.json).  Items
+// (ring k, orders m and m + H) are spread over the lanes; the Chebyshev step is the kernel above's, per warp.
+template <int WPC>
+__global__ void __launch_bounds__(32 * WPC) k_transform_w(const int32_t* __restrict__ grids, int64_t ngr,
+                                                          const int32_t* __restrict__ gnr, const int32_t* __restrict__ gna,
+                                                          const int64_t* __restrict__ goff,
+                                                          const int64_t* __restrict__ coff,
+                                                          const int64_t* __restrict__ rbase,
+                                                          const int32_t* __restrict__ roff,
+                                                          const double* __restrict__ gval, double* __restrict__ coef,
+                                                          const double2* __restrict__ twtab, int wsh,
+                                                          const ChunkRec* __restrict__ chunks,
+                                                          const int64_t* __restrict__ gch0,
+                                                          const double* __restrict__ part, int upts) {
+  extern __shared__ double sh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gi = (int64_t)blockIdx.x * WPC + warp;
+  if (gi >= ngr) return;
+  const int g = grids[gi];
+  const int nr = gnr[g], M = gna[g] / 2;
+  const int32_t* ro = roff + rbase[g];
+  const int q = ro[nr];
+  double* f = sh + (size_t)warp * wsh;                   // q samples
+  double2* AB = reinterpret_cast<double2*>(f + ((q + 1) & ~1));   // nr x (M + 1) (cos, sin) sums
+  double* ch = reinterpret_cast<double*>(AB + nr * (M + 1));      // 8 nr: cos(pi r / (4 nr))
+  if (part) {
+    // fused grid reduction (k_reduce_chunks' sum, same unit order): the grid's chunks of upts points, each point the
+    // sum of its units' partial values, straight into shared memory (no grid-value array in HBM)
+    // (a lane owns points t and t + 32 of every chunk: 16 loads in flight per batch of 8 units)
+    const int64_t pbase = goff[g];
+    for (int64_t c = gch0[g]; c < gch0[g + 1]; ++c) {
+      const ChunkRec R = chunks[c];
+      const bool in0 = lane < R.npt, in1 = lane + 32 < R.npt && upts > 32;
+      double v0 = 0.0, v1 = 0.0;
+      for (int s0 = 0; s0 < R.nu; s0 += 8) {
+        double a0[8], a1[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const double* pp = part + (R.u0 + s0 + e) * upts + lane;
+          a0[e] = (in0 && s0 + e < R.nu) ? pp[0] : 0.0;
+          a1[e] = (in1 && s0 + e < R.nu) ? pp[32] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (s0 + e < R.nu) {
+            v0 += a0[e];
+            v1 += a1[e];
+          }
+      }
+      if (in0) f[R.pt0 - pbase + lane] = v0;
+      if (in1) f[R.pt0 - pbase + lane + 32] = v1;
+    }
+  }
+  const double* __restrict__ gv = gval + goff[g];
+  for (int t0 = 0; !part && t0 < q; t0 += 32 * 8) {   // eight loads in flight per lane
+    double v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int t = t0 + lane + 32 * e;
+      v[e] = t < q ? gv[t] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int t = t0 + lane + 32 * e;
+      if (t < q) f[t] = v[e];
+    }
+  }
+  for (int t = lane; t < 8 * nr; t += 32) ch[t] = cospi((double)t / (4.0 * nr));
+  __syncwarp();
+  // a lane takes two orders m and m + H (H = ceil((M + 1) / 2)) of one ring: two independent recurrences sharing
+  // every sample read
+  const int H = (M + 2) / 2, items = nr * H;
+  for (int t = lane; t < items; t += 32) {
+    const int k = t / H, m1 = t - k * H, m2 = m1 + H;
+    const int r0 = ro[k], na = ro[k + 1] - r0;
+    const bool ok1 = 2 * m1 <= na, ok2 = m2 <= M && 2 * m2 <= na;
+    const double2* __restrict__ twn = twtab + (int64_t)na * (na - 1) / 2;
+    const double2 w1 = ok1 ? twn[m1] : make_double2(0.0, 0.0);   // (cos, sin)(2 pi m / na)
+    const double2 w2 = ok2 ? twn[m2] : make_double2(0.0, 0.0);
+    const double c21 = 2.0 * w1.x, c22 = 2.0 * w2.x;
+    const double* __restrict__ fk = f + r0;
+    double b11 = 0.0, b12 = 0.0, b21 = 0.0, b22 = 0.0;
+    if (ok1) {
+#pragma unroll 4
+      for (int l = na - 1; l >= 0; --l) {
+        const double fl = fk[l];
+        const double n1 = fma(c21, b11, fl - b12);
+        const double n2 = fma(c22, b21, fl - b22);
+        b12 = b11;
+        b11 = n1;
+        b22 = b21;
+        b21 = n2;
+      }
+    }
+    double A1 = fma(-w1.x, b12, b11), B1 = w1.y * b12;   // b_0 - cos(w) b_1, sin(w) b_1
+    double A2 = fma(-w2.x, b22, b21), B2 = w2.y * b22;
+    const bool e1 = m1 == 0 || 2 * m1 == na, e2 = 2 * m2 == na;
+    A1 = ok1 ? A1 * (e1 ? 1.0 / na : 2.0 / na) : 0.0;
+    B1 = (ok1 && !e1) ? B1 * (2.0 / na) : 0.0;
+    A2 = ok2 ? A2 * (e2 ? 1.0 / na : 2.0 / na) : 0.0;
+    B2 = (ok2 && !e2) ? B2 * (2.0 / na) : 0.0;
+    AB[k * (M + 1) + m1] = make_double2(A1, B1);
+    if (m2 <= M) AB[k * (M + 1) + m2] = make_double2(A2, B2);
+  }
+  __syncwarp();
+  for (int t = lane; t < (M + 1) * 2 * nr; t += 32) {
+    const int m = t / (2 * nr), rem = t % (2 * nr), j = rem >> 1, cs = rem & 1;
+    const int n = (m & 1) + 2 * j;
+    const int P = 8 * nr, step = (2 * n) % P;
+    int idx = n % P;   // n (2k + 1) mod 8 n_r, exactly reduced
+    double sacc = 0.0;
+    for (int k = 0; k < nr; ++k) {
+      const double2 ab = AB[k * (M + 1) + m];
+      sacc = fma(cs ? ab.y : ab.x, ch[idx], sacc);
+      idx += step;
+      if (idx >= P) idx -= P;
+    }
+    sacc *= 2.0 / nr;
+    if (n == 0) sacc *= 0.5;
+    coef[coff[g] + t] = sacc;
   }
 }
 
@@ -2181,6 +2312,21 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
   NC_TRY(upload(h, &H->d_ggrid0, H->ggrid0, s));
   NC_TRY(upload(h, &H->d_units, units, s));
   NC_TRY(upload(h, &H->d_chunks, chunks, s));
+  {   // per grid: its chunks [gch0[k], gch0[k + 1]) (chunks are in grid order; the fused reduction + transform)
+    std::vector<int64_t> gch0(NG + 1, 0);
+    int64_t c = 0;
+    bool ordered = true;
+    for (int64_t k = 0; k < NG; ++k) {
+      gch0[k] = c;
+      while (c < (int64_t)chunks.size() && chunks[c].pt0 < H->goff[k + 1]) {
+        ordered = ordered && chunks[c].pt0 >= H->goff[k];
+        ++c;
+      }
+    }
+    gch0[NG] = c;
+    H->fuse_reduce = ordered && c == (int64_t)chunks.size() && H->upts <= 64;   // a lane sums <= 2 points per chunk
+    NC_TRY(upload(h, &H->d_gch0, gch0, s));
+  }
   NC_TRY(upload(h, &H->d_srclist, srclist, s));
   NC_TRY(upload(h, &H->d_near_off, near_off, s));
   NC_TRY(upload(h, &H->d_near, near_all, s));
@@ -2247,7 +2393,13 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
                     H->d_part, H->d_counter, H->ftab, s);
   h->launches_last += H->nunits > 0;
   if (h->time_stages) cudaEventRecord(h->ev[3], s);
-  if (H->nchunks) {
+  static int tw = -1;   // NC_TRANSFORM=0: k_reduce_chunks + the CTA-per-grid transform (the tested alternative)
+  if (tw < 0) {
+    const char* e = tuning_env("NC_TRANSFORM");
+    tw = (e && e[0] == '0') ? 0 : 1;
+  }
+  const bool fused = tw && H->fuse_reduce;
+  if (H->nchunks && !fused) {
     const int per = 256 / H->upts;   // upts = 64 (warp-level units) or 256 (CTA units)
     k_reduce_chunks<<<(unsigned)((H->nchunks + per - 1) / per), 256, 0, s>>>(H->d_chunks, H->nchunks, H->d_part,
                                                                             H->upts, H->d_gval);
@@ -2256,12 +2408,22 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   if (h->time_stages) cudaEventRecord(h->ev[8], s);
   // step 4a: grid samples -> coefficients
   if (!H->grid_ids.empty()) {
-    const size_t shm = (size_t)(3 * H->qmax + 1 + H->cmax + 8 * H->nrmax) * sizeof(double);
-    if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(k_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    k_transform<<<(unsigned)H->grid_ids.size(), 128, shm, s>>>(H->d_grid_ids, (int64_t)H->grid_ids.size(),
-                                                                   H->d_gnr, H->d_gna, H->d_goff, H->d_coff,
-                                                                   H->d_rbase, H->d_roff, H->d_gval, H->d_gcoef,
-                                                                   H->d_twtab);
+    const int64_t ng = (int64_t)H->grid_ids.size();
+    if (tw) {
+      constexpr int WPC = 4;
+      const int wsh = ((H->qmax + 1) & ~1) + H->cmax + 8 * H->nrmax;   // doubles per warp
+      const size_t shm = (size_t)WPC * wsh * sizeof(double);
+      if (shm > 48 * 1024)
+        NC_CUDA_TRY(cudaFuncSetAttribute(k_transform_w<WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+      k_transform_w<WPC><<<(unsigned)((ng + WPC - 1) / WPC), 32 * WPC, shm, s>>>(
+          H->d_grid_ids, ng, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_rbase, H->d_roff, H->d_gval, H->d_gcoef,
+          H->d_twtab, wsh, H->d_chunks, H->d_gch0, fused ? H->d_part : nullptr, H->upts);
+    } else {
+      const size_t shm = (size_t)(3 * H->qmax + 1 + H->cmax + 8 * H->nrmax) * sizeof(double);
+      if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(k_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+      k_transform<<<(unsigned)ng, 128, shm, s>>>(H->d_grid_ids, ng, H->d_gnr, H->d_gna, H->d_goff, H->d_coff,
+                                                 H->d_rbase, H->d_roff, H->d_gval, H->d_gcoef, H->d_twtab);
+    }
     h->launches_last++;
   }
   // near lists at the Zernike nodes
@@ -2344,7 +2506,7 @@ void hier_destroy(nc_handle* h) {
                   H->d_grid_group, H->d_ggrid0, H->d_counter, H->d_ftab, H->d_rbase, H->d_roff, H->d_gsep, H->d_work_sep, H->d_ring_t,
                   H->d_node_ring, H->d_node_cs,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
-                  H->d_chunks, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
+                  H->d_chunks, H->d_gch0, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
                   H->d_udir, H->d_u, H->d_pfar, H->d_pwork1, H->d_ptx, H->d_pty, H->d_ptz, H->d_pV, H->d_pInt};
   for (void* b : bufs)
     if (b) cudaFree(b);

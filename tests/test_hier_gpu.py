@@ -182,13 +182,14 @@ def test_far_field_pair_variant_error(tmp_path, cfg, far):
     assert rel(outs[1], outs[0]) <= 1e-11
 
 
-@pytest.mark.parametrize("env", [{"NC_INTERP_SEP": "0"}, {"NC_INTERP_VARIANT": "128,4,1,4"},
+@pytest.mark.parametrize("env", [{"NC_INTERP_SEP": "0"}, {"NC_TRANSFORM": "0"}, {"NC_INTERP_VARIANT": "128,4,1,4"},
                                  {"NC_INTERP_VARIANT": "128,4,2,4"}, {"NC_INTERP_VARIANT": "128,2,3,4"},
                                  {"NC_INTERP_VARIANT": "128,2,0,4"}])
 def test_step4_evaluation_variants_agree(tmp_path, env):
     """Step 4 evaluated three ways: angular sums first with register accumulators (default),
     Chebyshev sums first (MB = 1) or blocked orders (MB = 2), and single-member groups separably on the Zernike node
-    rings (k_interp_sep) or directly (NC_INTERP_SEP=0).  The same expansion at the same nodes: rounding-level agreement."""
+    rings (k_interp_sep) or directly (NC_INTERP_SEP=0); step 4a's ring Fourier sums by Clenshaw's recurrence
+    (default, R37) or by tabulated twiddles (NC_TRANSFORM=0).  The same expansion at the same nodes: rounding-level agreement."""
     import subprocess
     import sys
     outs = []
