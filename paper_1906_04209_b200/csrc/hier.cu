@@ -128,6 +128,7 @@ struct HierState {
   int64_t nchunks = 0;
   int64_t* d_gch0 = nullptr;        // per grid: first chunk (NG + 1)
   bool fuse_reduce = false;         // k_transform_w sums the partials itself (no k_reduce_chunks, no grid values)
+  bool transform_w = true;          // NC_TRANSFORM=0: k_reduce_chunks + the CTA-per-grid transform (read at setup)
   int32_t* d_work_near = nullptr;
   int64_t nwork_near = 0;
   int64_t* d_near_off = nullptr;
@@ -2326,6 +2327,8 @@ int hier_setup(nc_handle* h, const std::vector<double>& cen, cudaStream_t s) {
     gch0[NG] = c;
     H->fuse_reduce = ordered && c == (int64_t)chunks.size() && H->upts <= 64;   // a lane sums <= 2 points per chunk
     NC_TRY(upload(h, &H->d_gch0, gch0, s));
+    const char* etw = tuning_env("NC_TRANSFORM");
+    H->transform_w = !(etw && etw[0] == '0');
   }
   NC_TRY(upload(h, &H->d_srclist, srclist, s));
   NC_TRY(upload(h, &H->d_near_off, near_off, s));
@@ -2393,11 +2396,7 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
                     H->d_part, H->d_counter, H->ftab, s);
   h->launches_last += H->nunits > 0;
   if (h->time_stages) cudaEventRecord(h->ev[3], s);
-  static int tw = -1;   // NC_TRANSFORM=0: k_reduce_chunks + the CTA-per-grid transform (the tested alternative)
-  if (tw < 0) {
-    const char* e = tuning_env("NC_TRANSFORM");
-    tw = (e && e[0] == '0') ? 0 : 1;
-  }
+  const bool tw = H->transform_w;   // NC_TRANSFORM=0: k_reduce_chunks + the CTA-per-grid transform (tested alternative)
   const bool fused = tw && H->fuse_reduce;
   if (H->nchunks && !fused) {
     const int per = 256 / H->upts;   // upts = 64 (warp-level units) or 256 (CTA units)
