@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256) k_gemm_dmma(const double* __restrict__ A,
 // single-buffered kernel above reached 0.38 / 0.46 of the DMMA peak on K1 / P-apply).
 // ------------------------------------------------------------------------------------------------
 namespace {
-constexpr int PM = 128, PN = 64, PK = 16, PLD = PK + 4;
+constexpr int PM = 128, PK = 16, PLD = PK + 4;
 
 __device__ __forceinline__ void cp16_zfill(void* dst, const void* src, bool valid) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -117,21 +117,24 @@ __device__ __forceinline__ void cp16_zfill(void* dst, const void* src, bool vali
 }
 }  // namespace
 
+// NF: n8 fragments per warp (4: 64-column CTA tiles; 3: 48 -- K3's 136 columns then pad to 144 instead of 192)
+template <int NF>
 __global__ void __launch_bounds__(256) k_gemm_dmma_pipe(const double* __restrict__ A, int64_t lda,
                                                         const double* __restrict__ Bt, int64_t rows, int ncols, int kd,
                                                         double* __restrict__ C, int64_t ldc, int cstride,
                                                         const double* __restrict__ X, int64_t ldx,
                                                         const int64_t* __restrict__ colbase,
                                                         const int64_t* __restrict__ colrstride, int64_t crow0) {
+  constexpr int PNt = 16 * NF;                   // CTA tile columns (2 warps x NF x 8)
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                              // [2][PM][PLD]
-  double* Bs = gsm + 2 * PM * PLD;               // [2][PN][PLD]
+  double* Bs = gsm + 2 * PM * PLD;               // [2][PNt][PLD]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;       // warp tile rows wm*32.., cols wn*32..
+  const int wm = warp >> 1, wn = warp & 1;       // warp tile rows wm*32.., cols wn*8NF..
   // column tiles vary fastest (blockIdx.x): the CTAs resident together share their A row tile through L2, so A is read
   // from DRAM once rather than once per column tile (the K1 epilogue's record writes otherwise evict it)
   const int64_t row0 = (int64_t)blockIdx.y * PM;
-  const int col0 = blockIdx.x * PN;
+  const int col0 = blockIdx.x * PNt;
   auto issue = [&](int k0, int b) {
     // A: 128 rows x 16 k = 1024 16-byte pieces (2 doubles), 4 per thread; B: 64 x 16 = 512, 2 per thread
 #pragma unroll
@@ -143,21 +146,22 @@ __global__ void __launch_bounds__(256) k_gemm_dmma_pipe(const double* __restrict
       cp16_zfill(As + ((size_t)b * PM + r) * PLD + c, ok ? (const void*)(A + gr * lda + gk) : (const void*)A, ok);
     }
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < (PNt * 8 + 255) / 256; ++q) {   // B: PNt rows x 16 k = PNt x 8 pieces
       const int e = tid + 256 * q, r = e >> 3, c = (e & 7) * 2;
+      if (r >= PNt) break;
       const int n = col0 + r;
       const int gk = k0 + c;
       const bool ok = n < ncols && gk < kd;
-      cp16_zfill(Bs + ((size_t)b * PN + r) * PLD + c, ok ? (const void*)(Bt + (int64_t)n * kd + gk) : (const void*)Bt,
+      cp16_zfill(Bs + ((size_t)b * PNt + r) * PLD + c, ok ? (const void*)(Bt + (int64_t)n * kd + gk) : (const void*)Bt,
                  ok);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  double acc[4][4][2];
+  double acc[4][NF][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < NF; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int nk = (kd + PK - 1) / PK;
   issue(0, 0);
   for (int s = 0; s < nk; ++s) {
@@ -169,18 +173,18 @@ __global__ void __launch_bounds__(256) k_gemm_dmma_pipe(const double* __restrict
     }
     __syncthreads();
     const double* as = As + (size_t)(s & 1) * PM * PLD;
-    const double* bs = Bs + (size_t)(s & 1) * PN * PLD;
+    const double* bs = Bs + (size_t)(s & 1) * PNt * PLD;
 #pragma unroll
     for (int kk = 0; kk < PK; kk += 4) {
-      double af[4], bf[4];
+      double af[4], bf[NF];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) af[mi] = as[(wm * 32 + mi * 8 + (lane >> 2)) * PLD + kk + (lane & 3)];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[(wn * 32 + ni * 8 + (lane >> 2)) * PLD + kk + (lane & 3)];
+      for (int ni = 0; ni < NF; ++ni) bf[ni] = bs[(wn * 8 * NF + ni * 8 + (lane >> 2)) * PLD + kk + (lane & 3)];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
+        for (int ni = 0; ni < NF; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
     }
     __syncthreads();   // every warp is done with buffer s & 1 before slab s + 2 is copied into it
   }
@@ -189,10 +193,10 @@ __global__ void __launch_bounds__(256) k_gemm_dmma_pipe(const double* __restrict
     const int64_t gr = row0 + wm * 32 + mi * 8 + (lane >> 2);
     if (gr >= rows) continue;
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
+    for (int ni = 0; ni < NF; ++ni) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int n = col0 + wn * 32 + ni * 8 + (lane & 3) * 2 + e;
+        const int n = col0 + wn * 8 * NF + ni * 8 + (lane & 3) * 2 + e;
         if (n >= ncols) continue;
         double v = acc[mi][ni][e];
         if (X) v += X[gr * ldx + n];
@@ -211,14 +215,25 @@ static bool gemm_pipe_ok(const double* A, int64_t lda, const double* Bt, int kd)
          !tuning_env("NC_GEMM_SIMPLE");
 }
 
+template <int NF>
+static void launch_pipe_nf(const double* A, int64_t lda, const double* Bt, int64_t rows, int ncols, int kd, double* C,
+                           int64_t ldc, int cstride, const double* X, int64_t ldx, const int64_t* colbase,
+                           const int64_t* colrstride, int64_t crow0, cudaStream_t s) {
+  constexpr int PNt = 16 * NF;
+  const size_t smem = (size_t)2 * (PM + PNt) * PLD * sizeof(double);
+  cudaFuncSetAttribute(k_gemm_dmma_pipe<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((unsigned)((ncols + PNt - 1) / PNt), (unsigned)((rows + PM - 1) / PM));
+  k_gemm_dmma_pipe<NF><<<grid, 256, smem, s>>>(A, lda, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx, colbase,
+                                               colrstride, crow0);
+}
+// the column tile that pads the output columns least (64 on ties)
 static void launch_pipe(const double* A, int64_t lda, const double* Bt, int64_t rows, int ncols, int kd, double* C,
                         int64_t ldc, int cstride, const double* X, int64_t ldx, const int64_t* colbase,
                         const int64_t* colrstride, int64_t crow0, cudaStream_t s) {
-  const size_t smem = (size_t)2 * (PM + PN) * PLD * sizeof(double);
-  cudaFuncSetAttribute(k_gemm_dmma_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((unsigned)((ncols + PN - 1) / PN), (unsigned)((rows + PM - 1) / PM));
-  k_gemm_dmma_pipe<<<grid, 256, smem, s>>>(A, lda, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx, colbase, colrstride,
-                                           crow0);
+  const int pad64 = (ncols + 63) / 64 * 64, pad48 = (ncols + 47) / 48 * 48;
+  if (pad48 < pad64)
+    return launch_pipe_nf<3>(A, lda, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx, colbase, colrstride, crow0, s);
+  launch_pipe_nf<4>(A, lda, Bt, rows, ncols, kd, C, ldc, cstride, X, ldx, colbase, colrstride, crow0, s);
 }
 
 void launch_gemm_dmma(const double* A, int64_t lda, int nparts, int64_t part_stride, const double* Bt, int64_t rows,
