@@ -104,15 +104,21 @@ struct HierState {
   double sep_terms = 0.0;           // node x coefficient terms those groups represent (part of interp_terms)
   double interp_lt = 0.0;           // ln(1 / grid tol) for the per-node order truncation of step 4 (R26c; 0: off)
   // step 4 through patch-local proxies for far levels (R36, proxy.cu)
-  int proxy_n = 0;                  // proxy points per patch (0: every level evaluated at the Zernike nodes)
-  double proxy_kh = 0.0;            // a level is far for a patch when its nearest grid source is >= proxy_kh (arc) away
-  double proxy_kappa = 0.0;         // proxy_kh / h (calibrated, proxy_rule_build)
-  uint32_t* d_pfar = nullptr;       // per local patch: bit lvl set when level lvl is evaluated at the proxies
+  // up to kMaxProxyRules rules, by point count ascending (threshold descending); rule r serves the (patch, level)
+  // pairs whose nearest grid source is >= kh[r] away and < kh[r - 1]; nearer ones stay at the nodes
+  int nprule = 0;
+  int proxy_n = 0;                  // points of the smallest rule (0: every level evaluated at the Zernike nodes)
+  double proxy_kappa = 0.0;         // the smallest threshold D / h in use (calibrated, proxy_rule_build)
+  struct PRule {
+    int n = 0;
+    double kh = 0.0;                // threshold (arc)
+    double *ptx = nullptr, *pty = nullptr, *ptz = nullptr;   // rc x n proxies (scaled by 1/2)
+    double* V = nullptr;            // rc x n: the rule's levels summed at its proxies
+    double* Int = nullptr;          // Ks x n: proxies -> nodes
+  } prule[3];
+  uint64_t* d_pcode = nullptr;      // per local patch, 2 bits per level: 0 nodes, r + 1 rule r
   int32_t* d_pwork1 = nullptr;      // local patches with a level evaluated at the nodes (the first pass's CTAs)
   int64_t npwork1 = 0;
-  double *d_ptx = nullptr, *d_pty = nullptr, *d_ptz = nullptr;   // rc x proxy_n proxy points (scaled by 1/2)
-  double* d_pV = nullptr;           // rc x proxy_n: the far levels' expansions summed at the proxies
-  double* d_pInt = nullptr;         // Ks x proxy_n: proxies -> nodes
   double proxy_pairs = 0.0, proxy_far = 0.0;   // (patch, level) pairs with grids; of which far (host count)
   FarTable ftab;
   int32_t* d_grid_group = nullptr;
@@ -792,7 +798,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
                                                const double* __restrict__ tz, const double* __restrict__ udir,
                                                double* __restrict__ u, const uint8_t* __restrict__ gsep,
                                                int nr_big, double lt, const double* __restrict__ cen,
-                                               int asin_terms, int cap, int sel, const uint32_t* __restrict__ pfar,
+                                               int asin_terms, int cap, int sel, const uint64_t* __restrict__ pcode,
                                                const int32_t* __restrict__ work) {
   // MB = 0 evaluates the grids with n_r <= kAngNrMax only (grid_eval_ang); a second pass (MB = 1, nr_big = 1) adds
   // the rest to u when any exists (tight precisions): the register-held accumulators of the first pass then need
@@ -809,9 +815,9 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
     const int lvl = threadIdx.x;
     const int g = pgl[(int64_t)lvl * rc + i];
     const int64_t kg0 = ggrid0[g], kg1 = ggrid0[g + 1];
-    // R36: sel 1 keeps the levels evaluated at the nodes, sel 2 the far levels evaluated at the proxies (bit lvl of
-    // pfar[i], decided once on the host: both passes see the same split)
-    const bool keep = sel == 0 || (((pfar[i] >> lvl) & 1u) != 0) == (sel == 2);
+    // R36: sel 1 keeps the levels evaluated at the nodes, sel 2 + r those of proxy rule r (the level's 2-bit code in
+    // pcode[i], decided once on the host: the passes partition the levels)
+    const bool keep = sel == 0 || (int)((pcode[i] >> (2 * lvl)) & 3u) == sel - 1;
     const bool ok = keep && kg0 != kg1 && gnr[kg0] != 0 && !(gsep && gsep[g]);
     lv_ng[lvl] = ok ? (int)(kg1 - kg0) : 0;
     if (ok) {
@@ -1181,7 +1187,7 @@ static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t*
                            const double* F, const double* gRinv, const int32_t* gnr, const int32_t* gna,
                            const int64_t* coff, const double* coef, const double* tx, const double* ty,
                            const double* tz, const double* udir, double* u, const uint8_t* gsep, cudaStream_t s,
-                           int nr_big, double lt, const double* cen, int asin_terms, int sel, const uint32_t* pfar,
+                           int nr_big, double lt, const double* cen, int asin_terms, int sel, const uint64_t* pfar,
                            const int32_t* work, int64_t nblocks) {
   auto kern = k_interp<NT, NPT, MB, MINB>;
   if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
@@ -1195,7 +1201,7 @@ static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t*
 
 // the instantiated first-pass variants (the default of each K* range, and the alternatives the step-4 tests compare)
 #define NC_INTERP_LIST(X) X(128, 2, 3, 4) X(256, 2, 0, 2) X(128, 2, 0, 4) X(128, 4, 1, 4) X(128, 4, 2, 4) \
-  X(96, 1, 3, 6) X(128, 1, 3, 5) X(64, 1, 3, 8)
+  X(96, 1, 3, 6) X(128, 1, 3, 5) X(64, 1, 3, 8) X(32, 1, 3, 16)
 static bool interp_listed(const InterpVariant& v) {
 #define NC_I(NT, NPT, MB, MINB) if (v.nt == NT && v.npt == NPT && v.mb == MB && v.minb == MINB) return true;
   NC_INTERP_LIST(NC_I)
@@ -1208,7 +1214,7 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
                          const int32_t* gna, const int64_t* coff, const double* coef, const double* tx,
                          const double* ty, const double* tz, const double* udir, double* u, const uint8_t* gsep,
                          double lt, const double* cen, int asin_terms, cudaStream_t s, int sel = 0,
-                         const uint32_t* pfar = nullptr, const int32_t* work = nullptr, int64_t nwork = -1) {
+                         const uint64_t* pfar = nullptr, const int32_t* work = nullptr, int64_t nwork = -1) {
   const int64_t nb = work ? nwork : rc;   // CTAs: one per patch of the work list (all local patches without one)
   (void)namax;
   // defaults: the 248-node rule takes one 128-thread CTA per patch with the coefficient prefetch (MB = 3: rest of
@@ -1216,10 +1222,10 @@ static int launch_interp(size_t shm, int L, int64_t rc, int Ks, int nrmax, int n
   // the 256-thread angular-sums-first kernel.  NC_INTERP_VARIANT must name a listed variant (else: the default,
   // with a warning -- never a silently skipped first pass)
   InterpVariant dflt = Ks <= 256 ? InterpVariant{128, 2, 3, 4} : InterpVariant{256, 2, 0, 2};
-  // the proxy pass (sel 2, R36): one point per thread, the CTA the size of the proxy set in whole warps
-  if (sel == 2) dflt = Ks <= 64 ? InterpVariant{64, 1, 3, 8} : Ks <= 96 ? InterpVariant{96, 1, 3, 6}
-                                                             : InterpVariant{128, 1, 3, 5};
-  InterpVariant v = (tuning_env("NC_INTERP_VARIANT") && sel != 2) ? interp_variant() : dflt;
+  // the proxy passes (sel >= 2, R36): one point per thread, the CTA the size of the proxy set in whole warps
+  if (sel >= 2) dflt = Ks <= 32 ? InterpVariant{32, 1, 3, 16} : Ks <= 64 ? InterpVariant{64, 1, 3, 8}
+                     : Ks <= 96 ? InterpVariant{96, 1, 3, 6} : InterpVariant{128, 1, 3, 5};
+  InterpVariant v = (tuning_env("NC_INTERP_VARIANT") && sel < 2) ? interp_variant() : dflt;
   if (!interp_listed(v)) {
     fprintf(stderr, "[nc] NC_INTERP_VARIANT=%s is not an instantiated variant; using the default\n",
             tuning_env("NC_INTERP_VARIANT"));
@@ -1477,52 +1483,96 @@ int hier_order(nc_handle* h, std::vector<double>& centers) {
   return NC_OK;
 }
 
-// Step 4 through proxies (R36, proxy.cu): the rule for the tables' nodes, its far-level threshold, the per-grid
-// nearest-source arcs, the proxies of every local patch and the buffers of the proxy pass.  Off (proxy_n = 0) with
-// NC_PROXY=0 (tuning), when the rule cannot be built, when it never meets its tolerance, or when it would not save
-// evaluations (n >= K* / 2).  The rule's tolerance is kProxyTolFactor x the grids' own (NC_PROXY_TOL overrides).
+// Step 4 through proxies (R36, proxy.cu): the rules for the tables' nodes, their thresholds, the per-grid
+// nearest-source arcs, the proxies of every local patch and the buffers of the proxy passes.  Off (nprule = 0) with
+// NC_PROXY=0 (tuning).  A rule is dropped when it cannot be built, never meets its tolerance, would not save evaluations
+// (n > K* / 2), or does not lower the threshold of the smaller rules.  The rules' tolerance is kProxyTolFactor x the
+// grids' own (NC_PROXY_TOL overrides); NC_PROXY_RULES="deg,nring,cphi;..." overrides the rule list.
 constexpr double kProxyTolFactor = 0.1;
+constexpr int kMaxProxyRules = 3;
 template <class Plan>
 static int proxy_setup(nc_handle* h, HierState* H, const std::vector<Plan>& plans, const std::vector<int32_t>& pgl,
                        const std::vector<double>& cen, double tol, cudaStream_t s) {
   const int Ks = h->Kstar;
   const int64_t rc = h->row_count, rb = h->row_begin;
+  H->nprule = 0;
   H->proxy_n = 0;
   if (const char* e = tuning_env("NC_PROXY"))
     if (e[0] == '0') return NC_OK;
-  int deg = 8, nring = 4;   // 64 proxies (profiles/r02w_proxy_sweep.jsonl: the fastest of the rules swept, same error)
-  double cphi = 24.0, tf = kProxyTolFactor;
-  if (const char* e = tuning_env("NC_PROXY_RULE")) sscanf(e, "%d,%d,%lf", &deg, &nring, &cphi);
+  if (rc <= 0 || H->L > 31) return NC_OK;
+  // default rules: 32 points (degree 6) and 64 (degree 8), thresholds D / h = 9 and 5.4 at the default tolerance
+  // (profiles/r03l_proxy_rules_sweep.jsonl: C5 step 4 + rest 9.20 ms with these two, 9.42 with the 64-point rule
+  // alone, 9.30 / 9.53 with a 124-point degree-13 rule (threshold 3.1) added for the levels now at the nodes)
+  struct Spec {
+    int deg, nring;
+    double cphi;
+  };
+  std::vector<Spec> specs = {{6, 3, 15.0}, {8, 4, 24.0}};
+  if (const char* e = tuning_env("NC_PROXY_RULES")) {
+    specs.clear();
+    const char* p = e;
+    Spec sp;
+    int used = 0;
+    while (sscanf(p, "%d,%d,%lf%n", &sp.deg, &sp.nring, &sp.cphi, &used) == 3) {
+      specs.push_back(sp);
+      p += used;
+      if (*p != ';') break;
+      ++p;
+    }
+  }
+  double tf = kProxyTolFactor;
   if (const char* e = tuning_env("NC_PROXY_TOL")) tf = atof(e);
   std::vector<double> z;
   NC_TRY(download(z, h->d_zhat, (size_t)3 * Ks, s));
-  std::vector<double> pts, Int;
-  double kappa = HUGE_VAL, hh = 0.0;
-  const int n = proxy_rule_build(z.data(), Ks, deg, nring, cphi, tf * tol, pts, Int, &kappa, &hh);
-  if (n <= 0 || !(kappa < HUGE_VAL) || 2 * n > Ks || (n & 1) || rc <= 0) return NC_OK;
-  H->proxy_n = n;
-  H->proxy_kappa = kappa;
-  H->proxy_kh = kappa * hh;
+  struct Built {
+    int n = 0;
+    double kappa = HUGE_VAL, h = 0.0;
+    std::vector<double> pts, Int;
+  };
+  std::vector<Built> built;
+  for (const Spec& sp : specs) {
+    Built b;
+    b.n = proxy_rule_build(z.data(), Ks, sp.deg, sp.nring, sp.cphi, tf * tol, b.pts, b.Int, &b.kappa, &b.h);
+    if (b.n > 0 && b.kappa < HUGE_VAL && 2 * b.n <= Ks && !(b.n & 1)) built.push_back(std::move(b));
+  }
+  std::sort(built.begin(), built.end(), [](const Built& a, const Built& b) { return a.n < b.n; });
+  std::vector<Built> rules;
+  for (Built& b : built)
+    if ((int)rules.size() < kMaxProxyRules && (rules.empty() || b.kappa < rules.back().kappa))
+      rules.push_back(std::move(b));
+  if (rules.empty()) return NC_OK;
+  const double hh = rules[0].h;
+  H->nprule = (int)rules.size();
+  H->proxy_n = rules[0].n;
+  H->proxy_kappa = rules.back().kappa;
+  for (int r = 0; r < H->nprule; ++r) {
+    HierState::PRule& R = H->prule[r];
+    R.n = rules[r].n;
+    R.kh = rules[r].kappa * hh;
+    NC_TRY(upload(h, &R.Int, rules[r].Int, s));
+    double* d_ph = nullptr;
+    NC_TRY(upload(h, &d_ph, rules[r].pts, s));
+    NC_TRY(halloc(h, &R.ptx, rc * R.n));
+    NC_TRY(halloc(h, &R.pty, rc * R.n));
+    NC_TRY(halloc(h, &R.ptz, rc * R.n));
+    NC_TRY(halloc(h, &R.V, rc * R.n));
+    launch_targets(h->d_frames, rb, rc, d_ph, R.n, 0.5, R.ptx, R.pty, R.ptz, s);
+    NC_CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFree(d_ph);
+  }
   // per grid: arc from its cap centre to the nearest source node, beta R = d - eps (R12/R21: the skeleton lies within
   // eps of its patch centre), so a patch centre at arc a0 from the cap centre is >= beta R - a0 from every source
   std::vector<double> gd(std::max<size_t>(plans.size(), 1), 0.0);
   for (size_t k = 0; k < plans.size(); ++k) gd[k] = plans[k].beta * H->gR[plans[k].group];
-  NC_TRY(upload(h, &H->d_pInt, Int, s));
-  double* d_ph = nullptr;
-  NC_TRY(upload(h, &d_ph, pts, s));
-  NC_TRY(halloc(h, &H->d_ptx, rc * n));
-  NC_TRY(halloc(h, &H->d_pty, rc * n));
-  NC_TRY(halloc(h, &H->d_ptz, rc * n));
-  NC_TRY(halloc(h, &H->d_pV, rc * n));
-  launch_targets(h->d_frames, rb, rc, d_ph, n, 0.5, H->d_ptx, H->d_pty, H->d_ptz, s);
-  NC_CUDA_TRY(cudaStreamSynchronize(s));
-  cudaFree(d_ph);
-  // the split, once, on the host: bit lvl of pfar[i] when patch i's level-lvl group has grids whose every source is
-  // >= kappa h from the patch centre (single-member groups stay with k_interp_sep when that pass is on)
+  // the split, once, on the host: the 2-bit code of patch i's level lvl is r + 1 for the smallest rule r whose
+  // threshold its grids' nearest source clears, 0 (nodes) if none (single-member groups stay with k_interp_sep)
   const int L = H->L;
-  std::vector<uint32_t> pfar(rc, 0u);
+  std::vector<uint64_t> pcode(rc, 0ull);
   std::vector<int32_t> work1;
   double npair = 0.0, nfar = 0.0;
+  std::vector<int64_t> per_rule(H->nprule + 1, 0);
+  const double dbin[] = {2.0, 3.0, 3.125, 4.0, 5.375, 7.0, 9.0, 12.0, 20.0, HUGE_VAL};
+  int64_t dhist[10] = {0};   // NC_HIER_DIAG: D / h of the (patch, multi-member level) pairs
   for (int64_t i = 0; i < rc; ++i) {
     bool near_level = false;
     for (int lvl = 0; lvl <= L; ++lvl) {
@@ -1533,8 +1583,18 @@ static int proxy_setup(nc_handle* h, HierState* H, const std::vector<Plan>& plan
       double dmin = HUGE_VAL;
       for (int64_t kg = kg0; kg < kg1; ++kg) dmin = std::min(dmin, gd[kg]);
       npair += 1.0;
-      if (dmin - harc(&H->gc[3 * (int64_t)g], &cen[3 * (rb + i)]) >= H->proxy_kh) {
-        pfar[i] |= 1u << lvl;
+      const double dist = dmin - harc(&H->gc[3 * (int64_t)g], &cen[3 * (rb + i)]);
+      {
+        int b = 0;
+        while (dist / hh >= dbin[b]) ++b;
+        ++dhist[b];
+      }
+      int code = 0;
+      for (int r = 0; r < H->nprule && !code; ++r)
+        if (dist >= H->prule[r].kh) code = r + 1;
+      ++per_rule[code];
+      if (code) {
+        pcode[i] |= (uint64_t)code << (2 * lvl);
         nfar += 1.0;
       } else {
         near_level = true;
@@ -1545,12 +1605,18 @@ static int proxy_setup(nc_handle* h, HierState* H, const std::vector<Plan>& plan
   H->proxy_pairs = npair;
   H->proxy_far = nfar;
   H->npwork1 = (int64_t)work1.size();
-  NC_TRY(upload(h, &H->d_pfar, pfar, s));
+  NC_TRY(upload(h, &H->d_pcode, pcode, s));
   if (work1.empty()) work1.push_back(0);
   NC_TRY(upload(h, &H->d_pwork1, work1, s));
-  if (getenv("NC_HIER_DIAG"))
-    fprintf(stderr, "[nc hier diag] step-4 proxies: n %d (deg %d), kappa %.3f (h %.3g), far levels %.0f of %.0f\n", n,
-            deg, kappa, hh, nfar, npair);
+  if (getenv("NC_HIER_DIAG")) {
+    fprintf(stderr, "[nc hier diag] step-4 proxies (h %.3g): nodes %lld", hh, (long long)per_rule[0]);
+    for (int r = 0; r < H->nprule; ++r)
+      fprintf(stderr, ", rule %d (n %d, kappa %.3f) %lld", r, H->prule[r].n, H->prule[r].kh / hh,
+              (long long)per_rule[r + 1]);
+    fprintf(stderr, " (patch, level) pairs\n[nc hier diag] D/h histogram (upper edges 2 3 3.125 4 5.375 7 9 12 20 inf):");
+    for (int b = 0; b < 10; ++b) fprintf(stderr, " %lld", (long long)dhist[b]);
+    fprintf(stderr, "\n");
+  }
   return NC_OK;
 }
 
@@ -2434,22 +2500,25 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
   if (rc > 0) {
     // two buffers for all grids of one group (cgroupmax doubles, even: pairs)
     const size_t shm = 2 * (size_t)std::max(H->cgroupmax, 2) * sizeof(double);
-    const int np = H->proxy_n;
+    const int np = H->nprule;
     const double* cen = h->d_centers + 3 * h->row_begin;
     if (!np) {   // every level at the Zernike nodes, on top of the near-list sums
       NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
                            H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_udir, H->d_u,
                            H->d_gsep, H->interp_lt, cen, H->asin_terms, s));
       h->launches_last++;
-    } else {     // R36: far levels at the proxies; u = udir + V Int^T; then the other levels at the nodes, in place
-      NC_TRY(launch_interp(shm, H->L, rc, np, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
-                           H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_ptx, H->d_pty, H->d_ptz, nullptr, H->d_pV,
-                           H->d_gsep, H->interp_lt, cen, H->asin_terms, s, 2, H->d_pfar));
-      launch_gemm_dmma(H->d_pV, np, 1, 0, H->d_pInt, rc, Ks, np, H->d_u, Ks, 1, H->d_udir, Ks, s);
+    } else {     // R36: each rule's levels at its proxies, u = udir + sum_r V_r Int_r^T; the rest at the nodes, in place
+      for (int r = 0; r < np; ++r) {
+        const HierState::PRule& R = H->prule[r];
+        NC_TRY(launch_interp(shm, H->L, rc, R.n, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
+                             H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, R.ptx, R.pty, R.ptz, nullptr, R.V, H->d_gsep,
+                             H->interp_lt, cen, H->asin_terms, s, 2 + r, H->d_pcode));
+        launch_gemm_dmma(R.V, R.n, 1, 0, R.Int, rc, Ks, R.n, H->d_u, Ks, 1, r == 0 ? H->d_udir : H->d_u, Ks, s);
+      }
       NC_TRY(launch_interp(shm, H->L, rc, Ks, H->nrmax, H->namax, H->d_pgl, H->d_ggrid0, H->d_gframe, H->d_gRinv,
                            H->d_gnr, H->d_gna, H->d_coff, H->d_gcoef, H->d_tx, H->d_ty, H->d_tz, H->d_u, H->d_u,
-                           H->d_gsep, H->interp_lt, cen, H->asin_terms, s, 1, H->d_pfar, H->d_pwork1, H->npwork1));
-      h->launches_last += 2 + (H->npwork1 > 0);
+                           H->d_gsep, H->interp_lt, cen, H->asin_terms, s, 1, H->d_pcode, H->d_pwork1, H->npwork1));
+      h->launches_last += 2 * np + (H->npwork1 > 0);
     }
   }
   if (H->nwork_sep) {   // single-member groups, separably (adds to u)
@@ -2506,9 +2575,12 @@ void hier_destroy(nc_handle* h) {
                   H->d_node_ring, H->d_node_cs,
                   H->d_gx, H->d_gy, H->d_gz, H->d_gval, H->d_gcoef, H->d_units, H->d_srclist, H->d_part,
                   H->d_chunks, H->d_gch0, H->d_work_near, H->d_near_off, H->d_near, H->d_pgl, H->d_tx, H->d_ty, H->d_tz,
-                  H->d_udir, H->d_u, H->d_pfar, H->d_pwork1, H->d_ptx, H->d_pty, H->d_ptz, H->d_pV, H->d_pInt};
+                  H->d_udir, H->d_u, H->d_pcode, H->d_pwork1};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (HierState::PRule& R : H->prule)
+    for (void* b : {(void*)R.ptx, (void*)R.pty, (void*)R.ptz, (void*)R.V, (void*)R.Int})
+      if (b) cudaFree(b);
   delete H;
   h->hier = nullptr;
 }
