@@ -557,11 +557,38 @@ __global__ void __launch_bounds__(32 * WPC) k_transform_w(const int32_t* __restr
                                                           const double* __restrict__ part, int upts) {
   extern __shared__ double sh[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t gi = (int64_t)blockIdx.x * WPC + warp;
-  if (gi >= ngr) return;
-  const int g = grids[gi];
-  const int nr = gnr[g], M = gna[g] / 2;
-  const int32_t* ro = roff + rbase[g];
+  // persistent warps (grid-stride over the grids) with the next grid's metadata loaded one grid ahead: the dependent
+  // chain grids -> (n_r, M, offsets) no longer stalls every grid
+  struct Meta {
+    int g, nr, na;
+    int64_t rb, go, co, c0, c1;
+  };
+  auto meta = [&](int g) {   // the loads of grid g's metadata (g < 0: none)
+    Meta m{};
+    m.g = g;
+    if (g >= 0) {
+      m.nr = gnr[g];
+      m.na = gna[g];
+      m.rb = rbase[g];
+      m.go = goff[g];
+      m.co = coff[g];
+      if (part) {
+        m.c0 = gch0[g];
+        m.c1 = gch0[g + 1];
+      }
+    }
+    return m;
+  };
+  const int64_t nw = (int64_t)gridDim.x * WPC;
+  int64_t gi = (int64_t)blockIdx.x * WPC + warp;
+  Meta mn = meta(gi < ngr ? grids[gi] : -1);
+  int gn2 = gi + nw < ngr ? grids[gi + nw] : -1;   // two grids ahead: the id; one ahead: the metadata
+  for (; gi < ngr; gi += nw) {
+  const Meta mc = mn;
+  mn = meta(gn2);
+  gn2 = gi + 2 * nw < ngr ? grids[gi + 2 * nw] : -1;
+  const int nr = mc.nr, M = mc.na / 2;
+  const int32_t* ro = roff + mc.rb;
   const int q = ro[nr];
   double* f = sh + (size_t)warp * wsh;                   // q samples
   double2* AB = reinterpret_cast<double2*>(f + ((q + 1) & ~1));   // nr x (M + 1) (cos, sin) sums
@@ -570,8 +597,8 @@ __global__ void __launch_bounds__(32 * WPC) k_transform_w(const int32_t* __restr
     // fused grid reduction (k_reduce_chunks' sum, same unit order): the grid's chunks of upts points, each point the
     // sum of its units' partial values, straight into shared memory (no grid-value array in HBM)
     // (a lane owns points t and t + 32 of every chunk: 16 loads in flight per batch of 8 units)
-    const int64_t pbase = goff[g];
-    for (int64_t c = gch0[g]; c < gch0[g + 1]; ++c) {
+    const int64_t pbase = mc.go;
+    for (int64_t c = mc.c0; c < mc.c1; ++c) {
       const ChunkRec R = chunks[c];
       const bool in0 = lane < R.npt, in1 = lane + 32 < R.npt && upts > 32;
       double v0 = 0.0, v1 = 0.0;
@@ -594,7 +621,7 @@ __global__ void __launch_bounds__(32 * WPC) k_transform_w(const int32_t* __restr
       if (in1) f[R.pt0 - pbase + lane + 32] = v1;
     }
   }
-  const double* __restrict__ gv = gval + goff[g];
+  const double* __restrict__ gv = gval + mc.go;
   for (int t0 = 0; !part && t0 < q; t0 += 32 * 8) {   // eight loads in flight per lane
     double v[8];
 #pragma unroll
@@ -660,7 +687,9 @@ __global__ void __launch_bounds__(32 * WPC) k_transform_w(const int32_t* __restr
     }
     sacc *= 2.0 / nr;
     if (n == 0) sacc *= 0.5;
-    coef[coff[g] + t] = sacc;
+    coef[mc.co + t] = sacc;
+  }
+  __syncwarp();   // every lane is done with this grid's shared memory before the next grid fills it
   }
 }
 
@@ -2480,7 +2509,12 @@ int hier_matvec(nc_handle* h, const double* x, double* y, cudaStream_t s) {
       const size_t shm = (size_t)WPC * wsh * sizeof(double);
       if (shm > 48 * 1024)
         NC_CUDA_TRY(cudaFuncSetAttribute(k_transform_w<WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-      k_transform_w<WPC><<<(unsigned)((ng + WPC - 1) / WPC), 32 * WPC, shm, s>>>(
+      int per = 1, dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_transform_w<WPC>, 32 * WPC, shm);
+      const int64_t nb = std::min<int64_t>((ng + WPC - 1) / WPC, (int64_t)std::max(per, 1) * sms);
+      k_transform_w<WPC><<<(unsigned)nb, 32 * WPC, shm, s>>>(
           H->d_grid_ids, ng, H->d_gnr, H->d_gna, H->d_goff, H->d_coff, H->d_rbase, H->d_roff, H->d_gval, H->d_gcoef,
           H->d_twtab, wsh, H->d_chunks, H->d_gch0, fused ? H->d_part : nullptr, H->upts);
     } else {
