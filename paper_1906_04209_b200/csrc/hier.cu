@@ -897,12 +897,18 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
       }
       cp_async_commit();
     };
+    // cap >= 0: double buffer (the next level's copy overlaps this level); cap < 0: one buffer of -cap pairs, each
+    // level copied and then evaluated (half the shared memory: more resident CTAs for the 32-point proxy pass)
+    const bool db = cap >= 0;
     int buf = 0;
     int lvl = next_level(0);
-    if (lvl <= L) stage(lvl, c2);
+    if (db && lvl <= L) stage(lvl, c2);
     while (lvl <= L) {
       const int nxt = next_level(lvl + 1);
-      if (nxt <= L) {
+      if (!db) {
+        stage(lvl, c2);
+        cp_async_wait<0>();
+      } else if (nxt <= L) {
         stage(nxt, c2 + (size_t)(buf ^ 1) * cap);
         cp_async_wait<1>();
       } else {
@@ -1077,7 +1083,7 @@ __global__ void __launch_bounds__(NT, MINB) k_interp(int L, int64_t rc, int Ksta
       }
       __syncthreads();                              // every reader of buffer `buf` is done before it is refilled
       lvl = nxt;
-      buf ^= 1;
+      if (db) buf ^= 1;
     }
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
@@ -1219,12 +1225,15 @@ static int launch_interp_t(size_t shm, int L, int64_t rc, int Ks, const int32_t*
                            int nr_big, double lt, const double* cen, int asin_terms, int sel, const uint64_t* pfar,
                            const int32_t* work, int64_t nblocks) {
   auto kern = k_interp<NT, NPT, MB, MINB>;
-  if (shm > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  // shm: the two coefficient buffers (cap = shm / 32 pairs each, 16-byte aligned halves)
+  // shm: the two coefficient buffers (cap = shm / 32 pairs each, 16-byte aligned halves); the one-warp CTAs of the
+  // 32-point proxy pass take one buffer of half the size (cap < 0: 20 resident CTAs per SM instead of 10)
+  const bool single = NT <= 32;
+  const size_t sh = single ? shm / 2 : shm;
+  const int cap = single ? -(int)(sh / sizeof(double2)) : (int)(shm / (2 * sizeof(double2)));
+  if (sh > 48 * 1024) NC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
   if (nblocks <= 0) return NC_OK;
-  kern<<<(unsigned)nblocks, NT, shm, s>>>(L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx, ty, tz, udir, u,
-                                          gsep, nr_big, lt, cen, asin_terms, (int)(shm / (2 * sizeof(double2))), sel,
-                                          pfar, work);
+  kern<<<(unsigned)nblocks, NT, sh, s>>>(L, rc, Ks, pgl, ggrid0, F, gRinv, gnr, gna, coff, coef, tx, ty, tz, udir, u,
+                                         gsep, nr_big, lt, cen, asin_terms, cap, sel, pfar, work);
   return NC_OK;
 }
 
