@@ -59,7 +59,7 @@ def load_fp64_peak():
 
 
 # ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
-TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r03m_ncu_full_pairs_grid.json"}
+TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r05a_ncu_full_pairs_grid.json"}
 
 
 def profiled_traffic(kernel, config, mode):
@@ -74,6 +74,27 @@ def profiled_traffic(kernel, config, mode):
     except (OSError, ValueError):
         pass
     return None, None
+
+
+def profiled_shared_wavefronts(kernel, config, mode, sms=148):
+    """The second bound of the grid kernel: shared-memory load wavefronts per SM-cycle (the L1 data
+    pipe retires one per cycle) and the share of them that are bank-conflict replays, from the committed capture."""
+    rel = TRAFFIC_PROFILES.get((kernel, config, mode))
+    if not rel:
+        return None
+    try:
+        for rec in json.load(open(os.path.join(ROOT, rel))):
+            if kernel not in rec.get("kernel", ""):
+                continue
+            num = lambda k: float(str(rec[k]).split()[0])
+            wf = num("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum")
+            cf = num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum")
+            cycles = num("gpu__time_duration.sum") * 1e-3 * num("sm__cycles_elapsed.avg.per_second") * 1e9 * sms
+            return {"shared_ld_wavefronts_per_sm_cycle": wf / cycles, "bank_conflict_share": cf / wf,
+                    "source": rel + " (ncu capture, not this run)"}
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
 
 
 def make_tables(cfg, which):
@@ -325,7 +346,8 @@ def main():
                         "/ kernel ms (CUDA events around the kernel in every timed step); peak = measured DFMA "
                         "throughput (profiles/r02h_fp64_peak.txt, of measured, SM clock 1965 MHz under load); fp64_pipe_util = FP64 instructions / "
                         "(peak / 2); traffic = DRAM bytes per launch from " + (tsrc or "no capture"),
-                "pairs_per_s": pairs / (pair_ms * 1e-3)}
+                "pairs_per_s": pairs / (pair_ms * 1e-3),
+                "l1_shared_wavefront_bound": profiled_shared_wavefronts(kname, cfg.name, args.mode)}
     # the fp64 tensor-core GEMMs (K1 T-apply over the used rungs, K3 P-apply + identity): DMMA roofline
     kd = st["K"] * st["Kstar"] * 2.0 * st["row_count"]
     gemms = {}

@@ -1,6 +1,6 @@
 """One setting of the grid-size knobs per process (the margins are read once per process): hierarchical matvec error
 (C3, C4 against the GPU direct sum; C5 against the hierarchical matvec at tolerance factor 100 with the default
-margins), grid pairs and matvec time.  References are cached under /tmp by the first call of a sweep.
+margins), the per-tag error on the oracle's golden rows (tests/golden/oracle_rows_*.npz), grid pairs and matvec time.  References are cached under /tmp by the first call of a sweep.
 
     NC_TUNING=1 [NC_GRID_TOL_FACTOR=.. NC_NA_MARGIN=.. NC_NR_MARGIN=.. NC_RING_MARGIN=.. NC_RING_FLOOR=..] \
         python tools/margin_sweep.py <label> [configs...]
@@ -19,7 +19,7 @@ from nc_inputs.tables import load_tables  # noqa: E402
 
 assert os.environ.get("NC_TUNING") == "1"
 label = sys.argv[1]
-KNOBS = ["NC_GRID_TOL_FACTOR", "NC_NA_MARGIN", "NC_NR_MARGIN", "NC_RING_MARGIN", "NC_RING_FLOOR"]
+KNOBS = ["NC_GRID_TOL_FACTOR", "NC_NA_MARGIN", "NC_NR_MARGIN", "NC_RING_MARGIN", "NC_RING_FLOOR", "NC_PROXY_TOL"]
 for name in sys.argv[2:] or ["C3", "C4", "C5"]:
     cfg = CONFIGS[name]
     tab = load_tables(f"tables/data/{name}.npz")
@@ -51,7 +51,26 @@ for name in sys.argv[2:] or ["C3", "C4", "C5"]:
         ms = hh.stats()["ms_last"]
         grid.append(ms[4]); rest.append(ms[5]); tot.append(ms[6])
     st = hh.stats()
-    print(json.dumps({"config": name, "setting": label, "knobs": {k: os.environ[k] for k in KNOBS if k in os.environ},
+    # the physical solve (b = P 1) and the paper's accuracy metric eq:l2res on 64 seeded patches (as bench.py, which
+    # takes 16): a smooth, coherent x, on which the grids' truncation error adds up differently from a random x
+    solve = None
+    if getattr(tab, "res_S", None) is not None:
+        xs, its, hist = hh.gmres(rtol=cfg.gmres_tol, max_iter=300, allow_noconv=True)
+        Is, val = hh.flux_or_mfpt(xs)
+        pats = np.random.default_rng(77).choice(cfg.N, min(64, cfg.N), replace=False)
+        rv, _ = hh.residual(xs, pats, tab)
+        solve = {"iters": int(its), "value": float(val), "l2res_max": float(np.max(rv)),
+                 "l2res_median": float(np.median(rv)), "l2res_max16": float(np.max(rv[:16])),
+                 "l2res_median16": float(np.median(rv[:16]))}
+    g = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                             f"oracle_rows_{name}.npz"))
+    xg = random_coeffs(cfg.N, tab.K, int(g["x_seed"]))   # the golden rows' x (tests/test_parity_golden_gpu.py)
+    yg = hh.to_caller(hh.matvec(torch.from_numpy(hh.to_internal(xg)).cuda()).cpu().numpy())
+    rows, tags, ref = g["rows"], g["tags"], g["y"]
+    rl = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    golden = {str(t): rl(yg[rows[tags == t]], ref[tags == t]) for t in np.unique(tags)}
+    golden["all"] = rl(yg[rows], ref)
+    print(json.dumps({"config": name, "setting": label, "golden_rows_rel_err": golden, "solve": solve, "knobs": {k: os.environ[k] for k in KNOBS if k in os.environ},
                       "rel_err": float(np.linalg.norm(y - yr) / np.linalg.norm(yr)),
                       "reference": "GPU direct" if cfg.N <= 20000 else "hier, factor 100, default margins",
                       "grid_pairs": st["hier_grid_pairs"], "total_ms": float(np.median(tot)),
