@@ -59,7 +59,7 @@ def load_fp64_peak():
 
 
 # ncu --set full captures of the dominant kernel (tools/ncu_summary.py full), keyed by (kernel, config, mode)
-TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r05a_ncu_full_pairs_grid.json"}
+TRAFFIC_PROFILES = {("k_pairs_grid", "C5", "hier"): "profiles/r05o_ncu_full_pairs_grid.json"}
 
 
 def profiled_traffic(kernel, config, mode):
